@@ -1,0 +1,288 @@
+/*
+ * kd.h — C ABI of the B200-native kernel-disaggregation hot path
+ * (arXiv 2604.10180, "kernel disaggregation"; P:n = PAPER.md line n,
+ *  S:n = SPEC.md line n, R# = readings in DESIGN.md / SURVEY §8(c)).
+ *
+ * The path: build a kernel DAG from declared per-kernel buffer read/write
+ * sets (P:241-242 library kernels, P:276 DDG) → assign kernels to devices
+ * (E1-E7) → plan a per-device schedule → run a
+ * decode step with N micro-batches on B200s, where cut edges are streamed
+ * into the consumer GPU's HBM by the producer kernel itself (fused peer-store
+ * epilogue + flag release) instead of the paper's NCCL/IBGDA send/recv
+ * kernels.
+ *
+ * Conventions (apply to every call unless stated):
+ *  - No exception crosses the ABI. Every call returns kd_status; on failure a
+ *    thread-local message is available from kd_last_error(). Out-parameters
+ *    are written only when KD_OK is returned.
+ *  - Host pointers are plain C arrays owned by the caller and only read during
+ *    the call. Device pointers ("dev ptr") are owned by the caller (PyTorch
+ *    allocations); the library borrows them for the lifetime of the object it
+ *    was given to and owns no device memory itself.
+ *  - cudaStream_t is passed as void*.
+ *  - Objects are not thread-safe; distinct objects may be used concurrently.
+ *  - Integer time is picoseconds, sizes are bytes (R7).
+ */
+#ifndef KD_H_
+#define KD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+typedef int32_t kd_status;
+enum {
+  KD_OK = 0,
+  KD_ERR_INVALID_ARG = 1,   /* null pointer, zero-length span, bad enum, bad shape */
+  KD_ERR_RANGE = 2,         /* span outside its buffer; output capacity too small */
+  KD_ERR_STATE = 3,         /* wrong call order (e.g. add after finalize) */
+  KD_ERR_PIN_CONFLICT = 4,  /* two pins disagree inside one template class */
+  KD_ERR_INFEASIBLE = 5,    /* no candidate placement / schedule deadlock */
+  KD_ERR_UNSUPPORTED = 6,   /* op, shape or cut pattern the runtime cannot execute */
+  KD_ERR_CUDA = 7,          /* a CUDA runtime/driver call failed (message has the CUDA error) */
+  KD_ERR_NCCL = 8,          /* reserved for the TP all-reduce path */
+  KD_ERR_TIMEOUT = 9,       /* a device-side flag wait exceeded its watchdog */
+  KD_ERR_OOM = 10           /* workspace smaller than kd_plan_workspace_bytes */
+};
+const char* kd_status_str(kd_status s);
+const char* kd_last_error(void);
+/* library version: (major << 16) | minor */
+uint32_t kd_version(void);
+
+/* ------------------------------------------------------------------ graph
+ * Buffers and kernels are declared in PROGRAM ORDER (= execution order,
+ * P:276 "By iterating over kernels in execution order"). A kernel's read and
+ * write sets are declared spans (the paper's library-kernel case, P:241-242:
+ * "cublasSgemm(.,A,B,.,C,.) reads bufferA and bufferB and writes bufferC").
+ * The graph describes ONE micro-batch of the step; kd_plan_create instantiates
+ * it N times (buffers flagged KD_BUF_PER_MICROBATCH get one instance per
+ * micro-batch, others are shared).
+ */
+typedef struct kd_graph kd_graph;
+
+enum {
+  KD_BUF_WEIGHT = 1u << 0,         /* read-only, initialised by the caller: never a DAG source (R5) */
+  KD_BUF_INPUT = 1u << 1,          /* initialised by the caller before each step */
+  KD_BUF_OUTPUT = 1u << 2,         /* read by the caller after the step */
+  KD_BUF_PERSISTENT = 1u << 3,     /* cross-iteration state (KV cache, SSM state); all
+                                      kernels touching it must be co-located (R6) */
+  KD_BUF_PER_MICROBATCH = 1u << 4  /* one instance per micro-batch */
+};
+
+typedef struct {
+  uint32_t buf;     /* buffer id from kd_graph_add_buffer */
+  uint32_t pad_;
+  uint64_t offset;  /* bytes from the buffer start */
+  uint64_t len;     /* bytes, > 0; offset + len <= buffer size */
+} kd_span;
+
+/* op codes: the kernels of the decoder-layer graph */
+enum {
+  KD_OP_NONE = 0,          /* bookkeeping node: costs a launch, executes nothing */
+  KD_OP_ADD_RMSNORM = 1,   /* a3  reads [r, delta?, gamma] writes [h, r]          */
+  KD_OP_GEMM = 2,          /* a4/a7/a9/a10 reads [X, W] writes [Y]: Y = X·Wᵀ       */
+  KD_OP_ROPE_APPEND = 3,   /* a5  reads [qkv, block_table, seq_len] writes [q, Kc, Vc] */
+  KD_OP_ATTENTION = 4,     /* a6  reads [q, Kc, Vc, block_table, seq_len] writes [out] */
+  KD_OP_SILU_MUL = 5,      /* a8  reads [gu] writes [a]                          */
+  KD_OP_RESIDUAL_ADD = 6   /* C1.11 reads [r, delta] writes [r]                  */
+};
+
+/* element types of activations / KV */
+enum { KD_BF16 = 0, KD_F32 = 1 };
+
+/* Op attributes (the op's "API signature"). The FIRST write span of
+ * every op is its primary output: the only output the runtime may stream to
+ * another device (other outputs must stay co-located with their readers). */
+typedef struct { uint32_t rows, hidden, has_delta, dtype; float eps; uint32_t pad_; } kd_attr_add_rmsnorm;
+typedef struct { uint32_t M, N, K, dtype; } kd_attr_gemm;            /* X [M,K], W [N,K] row-major, Y [M,N] */
+typedef struct {
+  uint32_t rows, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype, pad_;
+  double theta;   /* RoPE base (R12) */
+} kd_attr_rope_append;
+typedef struct {
+  uint32_t rows, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype, pad_;
+} kd_attr_attention;
+typedef struct { uint32_t rows, ffn, dtype, pad_; } kd_attr_silu_mul;  /* gu [rows, 2F] 64-col gate/up blocks */
+typedef struct { uint32_t rows, hidden; } kd_attr_residual_add;       /* r fp32 [rows,H] += delta (act dtype) */
+
+typedef struct {
+  uint32_t op;              /* KD_OP_* */
+  uint32_t n_reads, n_writes;
+  int32_t pin_device;       /* -1: free; else the kernel is fixed there (A4 indirect-access fallback) */
+  int32_t template_id;      /* -1: none; kernels with equal ids get one device (A15 repeated layers) */
+  uint32_t pad_;
+  uint64_t flops;           /* declared algorithmic flops (cost model) */
+  const kd_span* reads;
+  const kd_span* writes;
+  const void* attrs;        /* one of kd_attr_*; copied */
+  uint32_t attrs_size;
+  uint32_t pad2_;
+} kd_kernel_desc;
+
+typedef struct {
+  uint32_t src, dst, buf, pad_;
+  uint64_t offset, len;     /* one maximal span whose last writer is src (R1-R3) */
+} kd_edge;
+
+kd_status kd_graph_create(kd_graph** out);
+void kd_graph_destroy(kd_graph* g);
+/* Declares a buffer of `bytes` bytes. ids are dense from 0. */
+kd_status kd_graph_add_buffer(kd_graph* g, uint64_t bytes, uint32_t flags, uint32_t* id);
+/* Declares the next kernel in program order; ids dense from 0. Spans are
+ * validated (KD_ERR_RANGE if outside the buffer, KD_ERR_INVALID_ARG if empty);
+ * reads and writes may overlap (in-place kernels). */
+kd_status kd_graph_add_kernel(kd_graph* g, const kd_kernel_desc* desc, uint32_t* id);
+/* Builds the RAW DDG: a global registry of the last writer of every
+ * byte; for each kernel in order, every read byte whose last writer w is not
+ * the kernel itself yields an edge (w → k); then the kernel's writes update
+ * the registry (R2). No WAR/WAW edges (R4). Weights/inputs never written have
+ * no writer (R5). After finalize, add_* returns KD_ERR_STATE. */
+kd_status kd_graph_finalize(kd_graph* g);
+kd_status kd_graph_num_kernels(const kd_graph* g, uint32_t* n);
+kd_status kd_graph_num_buffers(const kd_graph* g, uint32_t* n);
+/* Edge records sorted by (dst, src, buf, offset). If cap < required, returns
+ * KD_ERR_RANGE and writes the required count to *n. */
+kd_status kd_graph_edges(const kd_graph* g, kd_edge* out, uint32_t cap, uint32_t* n);
+
+/* ------------------------------------------------------------------ cost / placement
+ * Machine description in integers (R7). link matrices are n×n row-major
+ * [u*n + g], diagonal ignored. */
+typedef struct {
+  uint32_t n_dev, pad_;
+  const uint64_t* hbm_Bps;      /* [n] HBM bytes/s */
+  const uint64_t* tc_flops;     /* [n] tensor flop/s */
+  const uint64_t* link_Bps;     /* [n*n] bw_{u,g} (Table 2) */
+  const uint64_t* link_lat_ps;  /* [n*n] ℓ_{u,g} (Table 2) */
+  uint64_t launch_ps;           /* per-kernel launch floor */
+} kd_machine;
+
+/* t_{k,g} (Table 2, replaced by a roofline, A10):
+ * t = max(⌈bytes·10¹²/hbm_g⌉, ⌈flops·10¹²/tc_g⌉) + launch_ps, where bytes =
+ * union-of-read-spans + union-of-write-spans of kernel k. t_ps is K×n_dev. */
+kd_status kd_cost(const kd_graph* g, const kd_machine* m, int64_t* t_ps);
+
+enum { KD_OBJ_AUTO = 0, KD_OBJ_THROUGHPUT = 1, KD_OBJ_LATENCY = 2 };
+typedef struct {
+  uint32_t n_micro;      /* N ≥ 1 */
+  uint32_t objective;    /* AUTO: LATENCY (E7) when N == 1, THROUGHPUT (E6) otherwise (R8) */
+  uint64_t max_nodes;    /* search budget (0 = unlimited); exceeding it → KD_ERR_INFEASIBLE */
+} kd_place_opts;
+
+/* Objective of a given assignment: E2 T_g = N·Σ t, E3/E4 M_g = N·Σ over cut
+ * edges into g of (ℓ + ⌈d_ij·10¹²/bw⌉), E5/E6 max_g max(T_g, M_g) or E7
+ * Σ T + Σ M. T and M (nullable) receive n_dev values each. */
+kd_status kd_objective(const kd_graph* g, const kd_machine* m, const int32_t* assign,
+                       uint32_t n_micro, uint32_t objective, int64_t* obj_ps, int64_t* T_ps, int64_t* M_ps);
+/* Exact search over template classes (A15) with pins (A4): branch and bound
+ * in lexicographic device order; the optimum returned is the
+ * lexicographically smallest assign among optima (R7). */
+kd_status kd_place(const kd_graph* g, const kd_machine* m, const kd_place_opts* opts,
+                   int32_t* assign, int64_t* objective_ps, uint64_t* nodes_visited);
+
+/* Chunk partition (R10): q = ⌈⌈len/unit⌉/n⌉·unit; chunk c = [c·q, min((c+1)·q, len)),
+ * empty chunks dropped. begin_end receives 2·(*n_out) values; cap in chunks. */
+kd_status kd_chunks(uint64_t len, uint64_t unit, uint32_t n, uint64_t* begin_end, uint32_t cap, uint32_t* n_out);
+
+/* ------------------------------------------------------------------ plan
+ * Deterministic list schedule of (micro-batch i, kernel k) under the cost
+ * model (P:380 recv-before/send-after; P:401-402 earlier micro-batch first):
+ * one kernel at a time per device, ready-set priority (i, k), one transfer at
+ * a time per ordered channel. The global order (start, dev, i, k) is
+ * topological; each device executes its subsequence in that order (which
+ * makes the spin-waits deadlock free). */
+typedef struct kd_plan kd_plan;
+typedef struct {
+  uint32_t dev, micro, kernel, pad_;
+  int64_t start_ps, end_ps;
+} kd_sched_entry;
+typedef struct {
+  uint32_t micro, producer, dst_dev, pad_;
+  uint64_t bytes;               /* union of spans the dst device's consumers read */
+  int64_t issue_ps, arrival_ps; /* simulated */
+} kd_transfer;
+
+kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* assign,
+                         uint32_t n_micro, kd_plan** out);
+void kd_plan_destroy(kd_plan* p);
+kd_status kd_plan_schedule(const kd_plan* p, kd_sched_entry* out, uint32_t cap, uint32_t* n);
+kd_status kd_plan_transfers(const kd_plan* p, kd_transfer* out, uint32_t cap, uint32_t* n);
+kd_status kd_plan_makespan(const kd_plan* p, int64_t* ps);
+/* Device workspace the runtime carves into activations, landing slots,
+ * flags and kernel scratch. Must be ZERO-initialised once by the caller. */
+kd_status kd_plan_workspace_bytes(const kd_plan* p, uint32_t dev, uint64_t* bytes);
+/* Whether the caller must bind (buf, dev): 1 for external buffers
+ * (WEIGHT/INPUT/OUTPUT/PERSISTENT) touched by a kernel placed on dev. */
+kd_status kd_plan_needs_binding(const kd_plan* p, uint32_t buf, uint32_t dev, int32_t* needed);
+
+/* ------------------------------------------------------------------ runtime
+ * One runtime drives the logical devices listed at creation. Logical device d
+ * runs on CUDA device cuda_ordinal[d]; several logical devices may share one
+ * physical GPU ("loopback": same flag protocol, landing slots in the same HBM).
+ * Multi-process use: create with n_local = 1 (this rank's logical device) and
+ * give every peer's workspace pointer, as mapped in this process (CUDA IPC),
+ * with kd_runtime_set_peer_workspace. */
+typedef struct kd_runtime kd_runtime;
+enum {
+  KD_MODE_DISAGG = 0,       /* default: execute the plan                                    */
+  KD_MODE_NO_TRANSFER = 1,  /* ablation: peer stores and waits removed (exposed-transfer = DISAGG − this) */
+  KD_MODE_LOG = 2           /* record %globaltimer around every launch (kd_runtime_log)        */
+};
+kd_status kd_runtime_create(const kd_plan* p, const uint32_t* local_devs, const int32_t* cuda_ordinal,
+                            uint32_t n_local, kd_runtime** out);
+void kd_runtime_destroy(kd_runtime* rt);
+/* External buffer instance: micro is ignored (use 0) unless the buffer is
+ * KD_BUF_PER_MICROBATCH. dev_ptr must stay valid for the runtime lifetime. */
+kd_status kd_runtime_bind(kd_runtime* rt, uint32_t buf, uint32_t micro, uint32_t dev, void* dev_ptr);
+kd_status kd_runtime_set_workspace(kd_runtime* rt, uint32_t dev, void* dev_ptr, uint64_t bytes);
+kd_status kd_runtime_set_peer_workspace(kd_runtime* rt, uint32_t dev, void* mapped_ptr);
+kd_status kd_runtime_set_mode(kd_runtime* rt, uint32_t mode);
+/* 1 = capture each device's step into a CUDA graph on first kd_step and
+ * replay it afterwards (default 1). */
+kd_status kd_runtime_set_graph(kd_runtime* rt, int32_t enable);
+/* Resolves every pointer, encodes TMA descriptors, enables peer access. */
+kd_status kd_runtime_prepare(kd_runtime* rt);
+/* Enqueue one decode step on streams[j] for local device j (async). Device
+ * errors (flag watchdog) surface at kd_runtime_check or the next kd_step. */
+kd_status kd_step(kd_runtime* rt, void* const* streams);
+kd_status kd_runtime_check(kd_runtime* rt);
+/* Number of kernel launches one kd_step enqueues on local device j. */
+kd_status kd_runtime_launch_count(const kd_runtime* rt, uint32_t j, uint32_t* n);
+/* Profiling: record CUDA events around every launch of `op` (0 = off) on the
+ * stream it is launched on; kd_runtime_op_time returns the summed event time
+ * (ms) and launch count since the last reset (events are read after a sync). */
+kd_status kd_runtime_profile_op(kd_runtime* rt, uint32_t op);
+kd_status kd_runtime_op_time(kd_runtime* rt, double* ms, uint64_t* launches);
+
+/* ------------------------------------------------------------------ single ops
+ * Direct entry points to the device kernels the runtime launches (for parity
+ * tests and micro-benchmarks). Pointers are device pointers; layouts as in
+ * the kd_attr_* comments. `scratch` is a ZERO-initialised device buffer of at
+ * least kd_op_scratch_bytes(op, attrs) bytes (left zeroed on return). */
+kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes);
+/* a3: r' = r + delta (fp32, in place; delta may be NULL), h = r'/sqrt(mean r'^2 + eps)·gamma */
+kd_status kd_op_add_rmsnorm(const kd_attr_add_rmsnorm* a, float* r, const void* delta,
+                            const void* gamma, void* h, void* stream);
+/* a4/a7/a9/a10: Y[M,N] = X[M,K]·W[N,K]ᵀ, bf16 in, fp32 accumulate (tcgen05, TMEM), bf16 out. */
+kd_status kd_op_gemm(const kd_attr_gemm* a, const void* X, const void* W, void* Y,
+                     void* scratch, void* stream);
+/* a5: NeoX RoPE of q and k at pos = seq_len[b]-1, append (k_rot, v) to the
+ * HND paged cache [pages][Hkv][page][D]; q_out [rows, Hq·D]. */
+kd_status kd_op_rope_append(const kd_attr_rope_append* a, const void* qkv, const int32_t* block_table,
+                            const int32_t* seq_len, void* q_out, void* k_cache, void* v_cache, void* stream);
+/* a6: split-KV paged GQA decode attention, deterministic fixed-order combine. */
+kd_status kd_op_attention(const kd_attr_attention* a, const void* q, const void* k_cache, const void* v_cache,
+                          const int32_t* block_table, const int32_t* seq_len, void* out,
+                          void* scratch, void* stream);
+/* a8: a[:, 64j+i] = silu(gu[:, 128j+i]) · gu[:, 128j+64+i] */
+kd_status kd_op_silu_mul(const kd_attr_silu_mul* a, const void* gu, void* out, void* stream);
+/* C1.11: r += delta */
+kd_status kd_op_residual_add(const kd_attr_residual_add* a, float* r, const void* delta, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KD_H_ */

@@ -1,0 +1,268 @@
+"""Pythonic wrappers over the C ABI (include/kd.h). Argument marshalling only:
+every computation (DAG, cost, placement, schedule, kernels) runs in libkd."""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence, Tuple
+
+from . import _kd as K
+from ._kd import check
+
+Span = Tuple[int, int, int]  # (buf, offset, len)
+
+
+def _spans(spans: Sequence[Span]):
+    arr = (K.kd_span * max(1, len(spans)))()
+    for i, (b, o, n) in enumerate(spans):
+        arr[i].buf, arr[i].offset, arr[i].len = b, o, n
+    return arr
+
+
+class Graph:
+    """kd_graph: buffers and kernels in program order, RAW DDG on finalize."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        check(K.kd_graph_create(C.byref(h)), "kd_graph_create")
+        self.h = h
+        self._keep = []
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            K.kd_graph_destroy(self.h)
+            self.h = None
+
+    def add_buffer(self, nbytes: int, flags: int = 0) -> int:
+        i = C.c_uint32()
+        check(K.kd_graph_add_buffer(self.h, int(nbytes), int(flags), C.byref(i)), "kd_graph_add_buffer")
+        return i.value
+
+    def add_kernel(self, op: int, reads: Sequence[Span], writes: Sequence[Span], attrs=None, flops: int = 0,
+                   pin: int = -1, template: int = -1) -> int:
+        d = K.kd_kernel_desc()
+        d.op, d.n_reads, d.n_writes = op, len(reads), len(writes)
+        d.pin_device, d.template_id, d.flops = pin, template, int(flops)
+        r, w = _spans(reads), _spans(writes)
+        d.reads = C.cast(r, C.POINTER(K.kd_span))
+        d.writes = C.cast(w, C.POINTER(K.kd_span))
+        if attrs is not None:
+            d.attrs = C.cast(C.byref(attrs), C.c_void_p)
+            d.attrs_size = C.sizeof(attrs)
+        i = C.c_uint32()
+        check(K.kd_graph_add_kernel(self.h, C.byref(d), C.byref(i)), "kd_graph_add_kernel")
+        return i.value
+
+    def finalize(self):
+        check(K.kd_graph_finalize(self.h), "kd_graph_finalize")
+
+    @property
+    def num_kernels(self) -> int:
+        n = C.c_uint32()
+        check(K.kd_graph_num_kernels(self.h, C.byref(n)))
+        return n.value
+
+    def edges(self) -> List[Tuple[int, int, int, int, int]]:
+        n = C.c_uint32()
+        st = K.kd_graph_edges(self.h, None, 0, C.byref(n))
+        if st not in (K.KD_OK, K.KD_ERR_RANGE):
+            check(st, "kd_graph_edges")
+        arr = (K.kd_edge * max(1, n.value))()
+        check(K.kd_graph_edges(self.h, arr, n.value, C.byref(n)), "kd_graph_edges")
+        return [(e.src, e.dst, e.buf, e.offset, e.len) for e in arr[:n.value]]
+
+
+class Machine:
+    """kd_machine from integer per-device / per-link parameters (R7)."""
+
+    def __init__(self, hbm_Bps, tc_flops, link_Bps, link_lat_ps, launch_ps: int):
+        n = len(hbm_Bps)
+        self.n_dev = n
+        self._hbm = (C.c_uint64 * n)(*[int(x) for x in hbm_Bps])
+        self._tc = (C.c_uint64 * n)(*[int(x) for x in tc_flops])
+        self._bw = (C.c_uint64 * (n * n))(*[int(link_Bps[u][g]) for u in range(n) for g in range(n)])
+        self._lat = (C.c_uint64 * (n * n))(*[int(link_lat_ps[u][g]) for u in range(n) for g in range(n)])
+        self.m = K.kd_machine(n, 0, self._hbm, self._tc, self._bw, self._lat, int(launch_ps))
+        self.hbm_Bps, self.tc_flops = list(hbm_Bps), list(tc_flops)
+        self.link_Bps, self.link_lat_ps, self.launch_ps = link_Bps, link_lat_ps, launch_ps
+
+    @classmethod
+    def uniform(cls, n, hbm_Bps, tc_flops, link_Bps, link_lat_ps, launch_ps):
+        return cls([hbm_Bps] * n, [tc_flops] * n, [[link_Bps] * n for _ in range(n)],
+                   [[link_lat_ps] * n for _ in range(n)], launch_ps)
+
+
+def cost(g: Graph, m: Machine) -> List[List[int]]:
+    K_ = g.num_kernels
+    arr = (C.c_int64 * (K_ * m.n_dev))()
+    check(K.kd_cost(g.h, C.byref(m.m), arr), "kd_cost")
+    return [[arr[k * m.n_dev + d] for d in range(m.n_dev)] for k in range(K_)]
+
+
+def objective(g: Graph, m: Machine, assign: Sequence[int], n_micro: int, obj: int = K.KD_OBJ_AUTO):
+    a = (C.c_int32 * len(assign))(*assign)
+    o = C.c_int64()
+    T = (C.c_int64 * m.n_dev)()
+    M = (C.c_int64 * m.n_dev)()
+    check(K.kd_objective(g.h, C.byref(m.m), a, n_micro, obj, C.byref(o), T, M), "kd_objective")
+    return o.value, list(T), list(M)
+
+
+def place(g: Graph, m: Machine, n_micro: int, obj: int = K.KD_OBJ_AUTO, max_nodes: int = 0):
+    opts = K.kd_place_opts(n_micro, obj, max_nodes)
+    a = (C.c_int32 * g.num_kernels)()
+    o = C.c_int64()
+    nodes = C.c_uint64()
+    check(K.kd_place(g.h, C.byref(m.m), C.byref(opts), a, C.byref(o), C.byref(nodes)), "kd_place")
+    return list(a), o.value, nodes.value
+
+
+def chunks(length: int, unit: int, n: int):
+    out = (C.c_uint64 * (2 * n))()
+    cnt = C.c_uint32()
+    check(K.kd_chunks(length, unit, n, out, n, C.byref(cnt)), "kd_chunks")
+    return [(out[2 * i], out[2 * i + 1]) for i in range(cnt.value)]
+
+
+class Plan:
+    def __init__(self, g: Graph, m: Machine, assign: Sequence[int], n_micro: int):
+        self.g, self.m = g, m
+        a = (C.c_int32 * len(assign))(*assign)
+        h = C.c_void_p()
+        check(K.kd_plan_create(g.h, C.byref(m.m), a, n_micro, C.byref(h)), "kd_plan_create")
+        self.h = h
+        self.assign = list(assign)
+        self.n_micro = n_micro
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            K.kd_plan_destroy(self.h)
+            self.h = None
+
+    def schedule(self):
+        n = C.c_uint32()
+        K.kd_plan_schedule(self.h, None, 0, C.byref(n))
+        arr = (K.kd_sched_entry * max(1, n.value))()
+        check(K.kd_plan_schedule(self.h, arr, n.value, C.byref(n)), "kd_plan_schedule")
+        return [(e.dev, e.micro, e.kernel, e.start_ps, e.end_ps) for e in arr[:n.value]]
+
+    def transfers(self):
+        n = C.c_uint32()
+        K.kd_plan_transfers(self.h, None, 0, C.byref(n))
+        arr = (K.kd_transfer * max(1, n.value))()
+        check(K.kd_plan_transfers(self.h, arr, n.value, C.byref(n)), "kd_plan_transfers")
+        return [(t.micro, t.producer, t.dst_dev, t.bytes, t.issue_ps, t.arrival_ps) for t in arr[:n.value]]
+
+    @property
+    def makespan(self) -> int:
+        v = C.c_int64()
+        check(K.kd_plan_makespan(self.h, C.byref(v)))
+        return v.value
+
+    def workspace_bytes(self, dev: int) -> int:
+        v = C.c_uint64()
+        check(K.kd_plan_workspace_bytes(self.h, dev, C.byref(v)), "kd_plan_workspace_bytes")
+        return v.value
+
+    def needs_binding(self, buf: int, dev: int) -> bool:
+        v = C.c_int32()
+        check(K.kd_plan_needs_binding(self.h, buf, dev, C.byref(v)), "kd_plan_needs_binding")
+        return bool(v.value)
+
+
+class Runtime:
+    def __init__(self, plan: Plan, local_devs: Sequence[int], cuda_ordinals: Sequence[int]):
+        self.plan = plan
+        n = len(local_devs)
+        h = C.c_void_p()
+        check(K.kd_runtime_create(plan.h, (C.c_uint32 * n)(*local_devs), (C.c_int32 * n)(*cuda_ordinals), n,
+                                  C.byref(h)), "kd_runtime_create")
+        self.h = h
+        self.local_devs = list(local_devs)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            K.kd_runtime_destroy(self.h)
+            self.h = None
+
+    def bind(self, buf: int, micro: int, dev: int, ptr: int):
+        check(K.kd_runtime_bind(self.h, buf, micro, dev, C.c_void_p(int(ptr))), "kd_runtime_bind")
+
+    def set_workspace(self, dev: int, ptr: int, nbytes: int):
+        check(K.kd_runtime_set_workspace(self.h, dev, C.c_void_p(int(ptr)), int(nbytes)), "kd_runtime_set_workspace")
+
+    def set_peer_workspace(self, dev: int, ptr: int):
+        check(K.kd_runtime_set_peer_workspace(self.h, dev, C.c_void_p(int(ptr))), "kd_runtime_set_peer_workspace")
+
+    def set_mode(self, mode: int):
+        check(K.kd_runtime_set_mode(self.h, mode), "kd_runtime_set_mode")
+
+    def set_graph(self, enable: bool):
+        check(K.kd_runtime_set_graph(self.h, 1 if enable else 0), "kd_runtime_set_graph")
+
+    def prepare(self):
+        check(K.kd_runtime_prepare(self.h), "kd_runtime_prepare")
+
+    def step(self, streams: Sequence[int]):
+        arr = (C.c_void_p * len(streams))(*[C.c_void_p(int(s)) for s in streams])
+        check(K.kd_step(self.h, arr), "kd_step")
+
+    def check(self):
+        check(K.kd_runtime_check(self.h), "kd_runtime_check")
+
+    def launch_count(self, j: int = 0) -> int:
+        n = C.c_uint32()
+        check(K.kd_runtime_launch_count(self.h, j, C.byref(n)), "kd_runtime_launch_count")
+        return n.value
+
+    def profile_op(self, op: int):
+        check(K.kd_runtime_profile_op(self.h, op), "kd_runtime_profile_op")
+
+    def op_time(self):
+        ms = C.c_double()
+        n = C.c_uint64()
+        check(K.kd_runtime_op_time(self.h, C.byref(ms), C.byref(n)), "kd_runtime_op_time")
+        return ms.value, n.value
+
+
+# ------------------------------------------------------------------ single ops (torch tensors → pointers)
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream().cuda_stream
+    return C.c_void_p(int(stream))
+
+
+def op_scratch_bytes(op: int, attrs) -> int:
+    v = C.c_uint64()
+    check(K.kd_op_scratch_bytes(op, C.byref(attrs), C.byref(v)), "kd_op_scratch_bytes")
+    return v.value
+
+
+def add_rmsnorm(attrs, r, delta, gamma, h, stream=None):
+    check(K.kd_op_add_rmsnorm(C.byref(attrs), _p(r), _p(delta), _p(gamma), _p(h), _stream(stream)), "kd_op_add_rmsnorm")
+
+
+def gemm(attrs, X, W, Y, scratch, stream=None):
+    check(K.kd_op_gemm(C.byref(attrs), _p(X), _p(W), _p(Y), _p(scratch), _stream(stream)), "kd_op_gemm")
+
+
+def rope_append(attrs, qkv, block_table, seq_len, q_out, k_cache, v_cache, stream=None):
+    check(K.kd_op_rope_append(C.byref(attrs), _p(qkv), _p(block_table), _p(seq_len), _p(q_out), _p(k_cache),
+                              _p(v_cache), _stream(stream)), "kd_op_rope_append")
+
+
+def attention(attrs, q, k_cache, v_cache, block_table, seq_len, out, scratch, stream=None):
+    check(K.kd_op_attention(C.byref(attrs), _p(q), _p(k_cache), _p(v_cache), _p(block_table), _p(seq_len), _p(out),
+                            _p(scratch), _stream(stream)), "kd_op_attention")
+
+
+def silu_mul(attrs, gu, out, stream=None):
+    check(K.kd_op_silu_mul(C.byref(attrs), _p(gu), _p(out), _stream(stream)), "kd_op_silu_mul")
+
+
+def residual_add(attrs, r, delta, stream=None):
+    check(K.kd_op_residual_add(C.byref(attrs), _p(r), _p(delta), _stream(stream)), "kd_op_residual_add")

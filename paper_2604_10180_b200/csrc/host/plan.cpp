@@ -1,0 +1,267 @@
+// plan.cpp — deterministic list schedule of (micro-batch, kernel) entries and
+// the per-device workspace layout (§3.3: recv before k / send after k
+// on communication streams; pipelined requests with earlier-first
+// priority; readings R3, R4, R7, R10, R11 in DESIGN.md).
+#include <algorithm>
+#include <set>
+
+#include "internal.hpp"
+
+using namespace kd;
+
+namespace kd {
+kd_status op_scratch_bytes(uint32_t op, const std::vector<uint8_t>& attrs, u64* bytes);  // ops.cu
+
+static u64 align_up(u64 x, u64 a) { return (x + a - 1) / a * a; }
+}  // namespace kd
+
+extern "C" {
+
+kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* assign, uint32_t n_micro,
+                         kd_plan** out) {
+  if (!g || !assign || !out) return fail(KD_ERR_INVALID_ARG, "kd_plan_create: NULL argument");
+  if (!g->finalized) return fail(KD_ERR_STATE, "kd_plan_create: graph not finalized");
+  if (!machine_valid(m) || n_micro == 0) return fail(KD_ERR_INVALID_ARG, "kd_plan_create: bad machine/n_micro");
+  const uint32_t K = (uint32_t)g->kernels.size(), n = m->n_dev, N = n_micro;
+  for (uint32_t k = 0; k < K; ++k)
+    if (assign[k] < 0 || (uint32_t)assign[k] >= n) return fail(KD_ERR_INVALID_ARG, "kd_plan_create: bad assign");
+  // R6: every kernel touching a PERSISTENT buffer sits on one device
+  {
+    std::map<uint32_t, int32_t> dev_of_buf;
+    for (uint32_t k = 0; k < K; ++k) {
+      const Kernel& Kk = g->kernels[k];
+      for (const auto* v : {&Kk.reads, &Kk.writes})
+        for (const auto& s : *v)
+          if (g->buffers[s.buf].flags & KD_BUF_PERSISTENT) {
+            auto it = dev_of_buf.find(s.buf);
+            if (it == dev_of_buf.end())
+              dev_of_buf[s.buf] = assign[k];
+            else if (it->second != assign[k])
+              return fail(KD_ERR_UNSUPPORTED, "kd_plan_create: PERSISTENT buffer touched from two devices (R6)");
+          }
+    }
+  }
+
+  auto* p = new kd_plan();
+  p->g = g;
+  p->n_dev = n;
+  p->n_micro = N;
+  p->assign.assign(assign, assign + K);
+
+  // predecessors and transfers (producer k, remote device d) = union of spans (R3)
+  std::vector<std::vector<uint32_t>> preds(K);
+  std::map<std::pair<uint32_t, uint32_t>, std::vector<Span>> xspans;
+  for (const auto& e : g->edges) {
+    auto& pv = preds[e.dst];
+    if (std::find(pv.begin(), pv.end(), e.src) == pv.end()) pv.push_back(e.src);
+    uint32_t gd = assign[e.dst];
+    if (gd != (uint32_t)assign[e.src]) xspans[{e.src, gd}].push_back({e.buf, e.offset, e.len});
+  }
+  std::vector<std::vector<std::pair<uint32_t, u64>>> out_x(K);  // k -> [(dev, bytes)] ascending dev
+  for (auto& kv : xspans) out_x[kv.first.first].push_back({kv.first.second, union_bytes(kv.second)});
+
+  std::vector<i64> t(K);
+  for (uint32_t k = 0; k < K; ++k) t[k] = kernel_time(*g, *m, k, assign[k]);
+
+  // ---- discrete-event list schedule (same semantics as oracle/schedule.py)
+  const i64 UNSET = -1;
+  std::vector<i64> end((size_t)N * K, UNSET);
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, i64> arrival;  // (i, producer, dev)
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, i64> issue;
+  std::vector<i64> chan_free((size_t)n * n, 0);
+  struct Run {
+    bool on = false;
+    i64 e = 0;
+    uint32_t i = 0, k = 0;
+  };
+  std::vector<Run> running(n);
+  std::set<std::pair<uint32_t, uint32_t>> todo;
+  for (uint32_t i = 0; i < N; ++i)
+    for (uint32_t k = 0; k < K; ++k) todo.insert({i, k});
+  i64 tau = 0;
+  auto available = [&](uint32_t i, uint32_t k, i64 now) {
+    uint32_t gd = assign[k];
+    for (uint32_t q : preds[k]) {
+      i64 e = end[(size_t)i * K + q];
+      if (e == UNSET || e > now) return false;
+      if ((uint32_t)assign[q] != gd && arrival.at({i, q, gd}) > now) return false;
+    }
+    return true;
+  };
+  size_t n_running = 0;
+  while (!todo.empty() || n_running) {
+    // 1) completions in (end, i, k, dev) order issue their transfers
+    std::vector<std::tuple<i64, uint32_t, uint32_t, uint32_t>> fin;
+    for (uint32_t d = 0; d < n; ++d)
+      if (running[d].on && running[d].e <= tau) fin.emplace_back(running[d].e, running[d].i, running[d].k, d);
+    std::sort(fin.begin(), fin.end());
+    for (const auto& f : fin) {
+      i64 e = std::get<0>(f);
+      uint32_t i = std::get<1>(f), k = std::get<2>(f), d = std::get<3>(f);
+      running[d].on = false;
+      --n_running;
+      for (const auto& x : out_x[k]) {
+        uint32_t u = assign[k], v = x.first;
+        i64 st = std::max(e, chan_free[(size_t)u * n + v]);
+        i64 arr = st + edge_cost(*m, x.second, u, v);
+        chan_free[(size_t)u * n + v] = arr;
+        arrival[{i, k, v}] = arr;
+        issue[{i, k, v}] = e;
+      }
+    }
+    // 2) idle devices start their smallest available (i, k)  (R11)
+    for (uint32_t d = 0; d < n; ++d) {
+      if (running[d].on) continue;
+      for (auto it = todo.begin(); it != todo.end(); ++it) {
+        uint32_t i = it->first, k = it->second;
+        if ((uint32_t)assign[k] != d || !available(i, k, tau)) continue;
+        i64 e = tau + t[k];
+        end[(size_t)i * K + k] = e;
+        running[d] = {true, e, i, k};
+        ++n_running;
+        p->sched.push_back({d, i, k, 0, tau, e});
+        todo.erase(it);
+        break;
+      }
+    }
+    // 3) next event
+    i64 nxt = -1;
+    for (uint32_t d = 0; d < n; ++d)
+      if (running[d].on && running[d].e > tau && (nxt < 0 || running[d].e < nxt)) nxt = running[d].e;
+    for (const auto& a : arrival)
+      if (a.second > tau && (nxt < 0 || a.second < nxt)) nxt = a.second;
+    if (nxt < 0) {
+      if (!todo.empty()) {
+        delete p;
+        return fail(KD_ERR_INFEASIBLE, "kd_plan_create: schedule deadlock");
+      }
+      break;
+    }
+    tau = nxt;
+  }
+  std::sort(p->sched.begin(), p->sched.end(), [](const kd_sched_entry& a, const kd_sched_entry& b) {
+    if (a.start_ps != b.start_ps) return a.start_ps < b.start_ps;
+    if (a.dev != b.dev) return a.dev < b.dev;
+    if (a.micro != b.micro) return a.micro < b.micro;
+    return a.kernel < b.kernel;
+  });
+  for (const auto& s : p->sched) p->makespan = std::max(p->makespan, s.end_ps);
+  for (uint32_t i = 0; i < N; ++i)
+    for (uint32_t k = 0; k < K; ++k)
+      for (const auto& x : out_x[k]) {
+        kd_transfer tr{i, k, x.first, 0, x.second, issue[{i, k, x.first}], arrival[{i, k, x.first}]};
+        p->transfers.push_back(tr);
+      }
+
+  // ---- workspace layout per device
+  const u64 AL = 256;
+  p->layout.resize(n);
+  p->needs_bind.assign(g->buffers.size(), std::vector<uint8_t>(n, 0));
+  const uint32_t EXT = KD_BUF_WEIGHT | KD_BUF_INPUT | KD_BUF_OUTPUT | KD_BUF_PERSISTENT;
+  for (uint32_t d = 0; d < n; ++d) {
+    auto& L = p->layout[d];
+    u64 off = 0;
+    L.ctrl_off = 0;
+    L.ctrl_bytes = align_up(64 + 4ull * n, AL);
+    off = L.ctrl_bytes;
+    // flags: one u32 per incoming transfer
+    L.flags_off = off;
+    u64 nflags = 0;
+    for (uint32_t ti = 0; ti < p->transfers.size(); ++ti)
+      if (p->transfers[ti].dst_dev == d) L.landing[ti] = {0, L.flags_off + 4 * nflags++};
+    L.flags_bytes = align_up(std::max<u64>(4 * nflags, 4), AL);
+    off += L.flags_bytes;
+    // scratch = max over kernels placed here
+    u64 scr = 0;
+    for (uint32_t k = 0; k < K; ++k)
+      if ((uint32_t)assign[k] == d) {
+        u64 b = 0;
+        kd_status s = op_scratch_bytes(g->kernels[k].op, g->kernels[k].attrs, &b);
+        if (s) {
+          delete p;
+          return s;
+        }
+        scr = std::max(scr, b);
+      }
+    L.scratch_off = off;
+    L.scratch_bytes = align_up(std::max<u64>(scr, 4), AL);
+    off += L.scratch_bytes;
+    // local instances of internal buffers touched here; binding needs of external ones
+    std::set<uint32_t> touched;
+    for (uint32_t k = 0; k < K; ++k)
+      if ((uint32_t)assign[k] == d) {
+        for (const auto& s : g->kernels[k].reads) touched.insert(s.buf);
+        for (const auto& s : g->kernels[k].writes) touched.insert(s.buf);
+      }
+    for (uint32_t b : touched) {
+      const auto& B = g->buffers[b];
+      if (B.flags & EXT) {
+        p->needs_bind[b][d] = 1;
+        continue;
+      }
+      uint32_t inst = (B.flags & KD_BUF_PER_MICROBATCH) ? N : 1;
+      for (uint32_t i = 0; i < inst; ++i) {
+        L.act[{b, i}] = off;
+        off = align_up(off + B.bytes, AL);
+      }
+    }
+    // landing slots: the producer's primary output span
+    for (auto& kv : L.landing) {
+      const kd_transfer& tr = p->transfers[kv.first];
+      const Kernel& P = g->kernels[tr.producer];
+      u64 len = P.writes.empty() ? 0 : P.writes[0].len;
+      kv.second.first = off;
+      off = align_up(off + std::max<u64>(len, 1), AL);
+    }
+    L.total = align_up(off, AL);
+  }
+  *out = p;
+  return KD_OK;
+}
+
+void kd_plan_destroy(kd_plan* p) { delete p; }
+
+kd_status kd_plan_schedule(const kd_plan* p, kd_sched_entry* out, uint32_t cap, uint32_t* n) {
+  if (!p || !n) return fail(KD_ERR_INVALID_ARG, "kd_plan_schedule: NULL argument");
+  uint32_t need = (uint32_t)p->sched.size();
+  if (cap < need || (need && !out)) {
+    *n = need;
+    return fail(KD_ERR_RANGE, "kd_plan_schedule: capacity too small");
+  }
+  std::copy(p->sched.begin(), p->sched.end(), out);
+  *n = need;
+  return KD_OK;
+}
+
+kd_status kd_plan_transfers(const kd_plan* p, kd_transfer* out, uint32_t cap, uint32_t* n) {
+  if (!p || !n) return fail(KD_ERR_INVALID_ARG, "kd_plan_transfers: NULL argument");
+  uint32_t need = (uint32_t)p->transfers.size();
+  if (cap < need || (need && !out)) {
+    *n = need;
+    return fail(KD_ERR_RANGE, "kd_plan_transfers: capacity too small");
+  }
+  std::copy(p->transfers.begin(), p->transfers.end(), out);
+  *n = need;
+  return KD_OK;
+}
+
+kd_status kd_plan_makespan(const kd_plan* p, int64_t* ps) {
+  if (!p || !ps) return fail(KD_ERR_INVALID_ARG, "kd_plan_makespan: NULL argument");
+  *ps = p->makespan;
+  return KD_OK;
+}
+
+kd_status kd_plan_workspace_bytes(const kd_plan* p, uint32_t dev, uint64_t* bytes) {
+  if (!p || !bytes || dev >= p->n_dev) return fail(KD_ERR_INVALID_ARG, "kd_plan_workspace_bytes: bad argument");
+  *bytes = p->layout[dev].total;
+  return KD_OK;
+}
+
+kd_status kd_plan_needs_binding(const kd_plan* p, uint32_t buf, uint32_t dev, int32_t* needed) {
+  if (!p || !needed || dev >= p->n_dev || buf >= p->needs_bind.size())
+    return fail(KD_ERR_INVALID_ARG, "kd_plan_needs_binding: bad argument");
+  *needed = p->needs_bind[buf][dev];
+  return KD_OK;
+}
+
+}  // extern "C"

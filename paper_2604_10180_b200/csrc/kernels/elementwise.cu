@@ -1,0 +1,341 @@
+// elementwise.cu — the memory-role kernels other than attention:
+//   a3  fused residual add + RMSNorm
+//   a5  NeoX RoPE + paged KV append      (a5, C1.3-C1.4)
+//   a8  SiLU·mul on 64-col gate/up blocks (a8, C1.9)
+//   C1.11 final residual add
+// plus the runtime's step-begin barrier and flag-wait kernels (a13/a15).
+// All are HBM- or launch-bound: 16-byte vector loads, fp32 math, one pass.
+#include <math.h>
+
+#include "launch.hpp"
+
+namespace kd {
+
+kd_status set_cuda_error(cudaError_t e, const char* where) {
+  return fail(KD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ a3
+// one CTA per row; each thread keeps up to 4 chunks of 8 elements in registers
+constexpr int kNormThreads = 256;
+constexpr int kNormChunks = 4;  // H <= 8 * 256 * 4 = 8192
+
+__global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __restrict__ r,
+                                                                  const __nv_bfloat16* __restrict__ delta,
+                                                                  const __nv_bfloat16* __restrict__ gamma,
+                                                                  __nv_bfloat16* __restrict__ h, int H, float eps,
+                                                                  Epi epi) {
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const int nch = H / 8;
+  float v[kNormChunks][8];
+  float ss = 0.f;
+  float* rr = r + (size_t)row * H;
+#pragma unroll
+  for (int c = 0; c < kNormChunks; ++c) {
+    int ch = tid + c * kNormThreads;
+    if (ch < nch) {
+      float4 a = reinterpret_cast<const float4*>(rr)[2 * ch];
+      float4 b = reinterpret_cast<const float4*>(rr)[2 * ch + 1];
+      v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
+      v[c][4] = b.x; v[c][5] = b.y; v[c][6] = b.z; v[c][7] = b.w;
+      if (delta) {
+        uint4 d = reinterpret_cast<const uint4*>(delta + (size_t)row * H)[ch];
+        v[c][0] += bf16lo(d.x); v[c][1] += bf16hi(d.x);
+        v[c][2] += bf16lo(d.y); v[c][3] += bf16hi(d.y);
+        v[c][4] += bf16lo(d.z); v[c][5] += bf16hi(d.z);
+        v[c][6] += bf16lo(d.w); v[c][7] += bf16hi(d.w);
+        reinterpret_cast<float4*>(rr)[2 * ch] = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
+        reinterpret_cast<float4*>(rr)[2 * ch + 1] = make_float4(v[c][4], v[c][5], v[c][6], v[c][7]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss += v[c][j] * v[c][j];
+    }
+  }
+  __shared__ float red[kNormThreads / 32];
+  ss = warp_sum(ss);
+  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < kNormThreads / 32; ++w) tot += red[w];  // fixed order: deterministic
+  const float inv = rsqrtf(tot / (float)H + eps);
+#pragma unroll
+  for (int c = 0; c < kNormChunks; ++c) {
+    int ch = tid + c * kNormThreads;
+    if (ch < nch) {
+      uint4 gm = reinterpret_cast<const uint4*>(gamma)[ch];
+      uint4 o;
+      o.x = pack_bf16(v[c][0] * inv * bf16lo(gm.x), v[c][1] * inv * bf16hi(gm.x));
+      o.y = pack_bf16(v[c][2] * inv * bf16lo(gm.y), v[c][3] * inv * bf16hi(gm.y));
+      o.z = pack_bf16(v[c][4] * inv * bf16lo(gm.z), v[c][5] * inv * bf16hi(gm.z));
+      o.w = pack_bf16(v[c][6] * inv * bf16lo(gm.w), v[c][7] * inv * bf16hi(gm.w));
+      size_t e = (size_t)row * nch + ch;
+      reinterpret_cast<uint4*>(h)[e] = o;
+      for (int p = 0; p < epi.n; ++p) reinterpret_cast<uint4*>(epi.dst[p])[e] = o;
+    }
+  }
+  epi_signal(epi);
+}
+
+kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const void* delta, const void* gamma, void* h,
+                             const LaunchCtx& c, uint32_t* signals) {
+  if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "add_rmsnorm: only bf16 activations");
+  if (a.rows == 0 || a.hidden == 0 || a.hidden % 8 || a.hidden > 8 * kNormThreads * kNormChunks)
+    return fail(KD_ERR_UNSUPPORTED, "add_rmsnorm: hidden must be a multiple of 8 and <= 8192");
+  if (!r || !gamma || !h || (a.has_delta && !delta)) return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: NULL pointer");
+  add_rmsnorm_kernel<<<a.rows, kNormThreads, 0, c.stream>>>(
+      r, a.has_delta ? (const __nv_bfloat16*)delta : nullptr, (const __nv_bfloat16*)gamma, (__nv_bfloat16*)h,
+      (int)a.hidden, a.eps, c.epi);
+  KD_CUDA_CHECK(cudaGetLastError(), "add_rmsnorm launch");
+  if (signals) *signals = a.rows;
+  return KD_OK;
+}
+
+// ------------------------------------------------------------------ C1.11
+__global__ void residual_add_kernel(float* __restrict__ r, const __nv_bfloat16* __restrict__ d, size_t n8,
+                                    Epi epi) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x) {
+    float4 a = reinterpret_cast<float4*>(r)[2 * i];
+    float4 b = reinterpret_cast<float4*>(r)[2 * i + 1];
+    uint4 x = reinterpret_cast<const uint4*>(d)[i];
+    a.x += bf16lo(x.x); a.y += bf16hi(x.x); a.z += bf16lo(x.y); a.w += bf16hi(x.y);
+    b.x += bf16lo(x.z); b.y += bf16hi(x.z); b.z += bf16lo(x.w); b.w += bf16hi(x.w);
+    reinterpret_cast<float4*>(r)[2 * i] = a;
+    reinterpret_cast<float4*>(r)[2 * i + 1] = b;
+    for (int p = 0; p < epi.n; ++p) {
+      reinterpret_cast<float4*>(epi.dst[p])[2 * i] = a;
+      reinterpret_cast<float4*>(epi.dst[p])[2 * i + 1] = b;
+    }
+  }
+  epi_signal(epi);
+}
+
+static int residual_grid(const kd_attr_residual_add& a) {
+  size_t n8 = (size_t)a.rows * a.hidden / 8;
+  return (int)std::max<size_t>(1, std::min<size_t>((n8 + 255) / 256, 4 * kNumSMs));
+}
+
+kd_status launch_residual_add(const kd_attr_residual_add& a, float* r, const void* delta, const LaunchCtx& c,
+                              uint32_t* signals) {
+  size_t n = (size_t)a.rows * a.hidden;
+  if (n == 0 || a.hidden % 8) return fail(KD_ERR_UNSUPPORTED, "residual_add: hidden must be a multiple of 8");
+  if (!r || !delta) return fail(KD_ERR_INVALID_ARG, "residual_add: NULL pointer");
+  size_t n8 = n / 8;
+  int grid = residual_grid(a);
+  residual_add_kernel<<<grid, 256, 0, c.stream>>>(r, (const __nv_bfloat16*)delta, n8, c.epi);
+  KD_CUDA_CHECK(cudaGetLastError(), "residual_add launch");
+  if (signals) *signals = grid;
+  return KD_OK;
+}
+
+// ------------------------------------------------------------------ a8
+__global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int rows,
+                                int F, Epi epi) {
+  // one thread = 8 consecutive outputs; block j of 64 outputs reads gate
+  // columns [128j, 128j+64) and up columns [128j+64, 128j+128)
+  const int per_row = F / 8;
+  const size_t n = (size_t)rows * per_row;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
+    int row = (int)(t / per_row), c8 = (int)(t % per_row);
+    int col = c8 * 8, j = col / 64, i = col % 64;
+    const __nv_bfloat16* g = gu + (size_t)row * 2 * F + 128 * j + i;
+    uint4 gv = *reinterpret_cast<const uint4*>(g);
+    uint4 uv = *reinterpret_cast<const uint4*>(g + 64);
+    const uint32_t* gp = &gv.x;
+    const uint32_t* up = &uv.x;
+    uint4 o;
+    uint32_t* op = &o.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float g0 = bf16lo(gp[q]), g1 = bf16hi(gp[q]);
+      float s0 = g0 / (1.f + __expf(-g0)), s1 = g1 / (1.f + __expf(-g1));
+      op[q] = pack_bf16(s0 * bf16lo(up[q]), s1 * bf16hi(up[q]));
+    }
+    size_t e = (size_t)row * per_row + c8;
+    reinterpret_cast<uint4*>(out)[e] = o;
+    for (int p = 0; p < epi.n; ++p) reinterpret_cast<uint4*>(epi.dst[p])[e] = o;
+  }
+  epi_signal(epi);
+}
+
+static int silu_grid(const kd_attr_silu_mul& a) {
+  size_t n = (size_t)a.rows * a.ffn / 8;
+  return (int)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 4 * kNumSMs));
+}
+
+kd_status launch_silu_mul(const kd_attr_silu_mul& a, const void* gu, void* out, const LaunchCtx& c,
+                          uint32_t* signals) {
+  if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "silu_mul: only bf16 activations");
+  if (a.rows == 0 || a.ffn == 0 || a.ffn % 64) return fail(KD_ERR_UNSUPPORTED, "silu_mul: ffn must be a multiple of 64");
+  if (!gu || !out) return fail(KD_ERR_INVALID_ARG, "silu_mul: NULL pointer");
+  int grid = silu_grid(a);
+  silu_mul_kernel<<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)gu, (__nv_bfloat16*)out, (int)a.rows,
+                                             (int)a.ffn, c.epi);
+  KD_CUDA_CHECK(cudaGetLastError(), "silu_mul launch");
+  if (signals) *signals = grid;
+  return KD_OK;
+}
+
+// ------------------------------------------------------------------ a5
+// one CTA per token row; cos/sin of pos·θ^(−2i/D) computed once per row in
+// fp64 (R12) into shared memory; threads own (head, pair of dims) work items.
+__global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ bt,
+                                   const int32_t* __restrict__ sl, __nv_bfloat16* __restrict__ q_out,
+                                   __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int Hq, int Hkv,
+                                   int D, int page, int pps, double theta, Epi epi) {
+  extern __shared__ float cs[];  // [D/2] cos, [D/2] sin
+  const int b = blockIdx.x, half = D / 2, G = Hq / Hkv;
+  const int pos = sl[b] - 1;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    double ang = (double)pos * pow(theta, -2.0 * (double)i / (double)D);
+    double s, c;
+    sincos(ang, &s, &c);
+    cs[i] = (float)c;
+    cs[half + i] = (float)s;
+  }
+  __syncthreads();
+  const int32_t pg = bt[(size_t)b * pps + pos / page];
+  const int off = pos % page;
+  const __nv_bfloat16* src = qkv + (size_t)b * (Hq + 2 * Hkv) * D;
+  const int pairs = half / 2;  // bf16x2 items per rotated head
+  // rotated heads: Hq q heads then Hkv k heads
+  const int n_rot = (Hq + Hkv) * pairs;
+  for (int t = threadIdx.x; t < n_rot; t += blockDim.x) {
+    int hh = t / pairs, i = (t % pairs) * 2;
+    const __nv_bfloat16* x;
+    __nv_bfloat16* dst;
+    size_t qoff = 0;
+    bool is_q = hh < Hq;
+    if (is_q) {
+      int g = hh / G, j = hh % G;
+      x = src + (size_t)g * (G + 2) * D + (size_t)j * D;
+      qoff = (size_t)b * Hq * D + (size_t)hh * D;
+      dst = q_out + qoff;
+    } else {
+      int g = hh - Hq;
+      x = src + (size_t)g * (G + 2) * D + (size_t)G * D;
+      dst = kc + (((size_t)pg * Hkv + g) * page + off) * D;
+    }
+    uint32_t a = *reinterpret_cast<const uint32_t*>(x + i);
+    uint32_t bb = *reinterpret_cast<const uint32_t*>(x + half + i);
+    float x0 = bf16lo(a), x1 = bf16hi(a), y0 = bf16lo(bb), y1 = bf16hi(bb);
+    float c0 = cs[i], c1 = cs[i + 1], s0 = cs[half + i], s1 = cs[half + i + 1];
+    uint32_t lo = pack_bf16(x0 * c0 - y0 * s0, x1 * c1 - y1 * s1);
+    uint32_t hi = pack_bf16(y0 * c0 + x0 * s0, y1 * c1 + x1 * s1);
+    *reinterpret_cast<uint32_t*>(dst + i) = lo;
+    *reinterpret_cast<uint32_t*>(dst + half + i) = hi;
+    if (is_q)
+      for (int p = 0; p < epi.n; ++p) {
+        __nv_bfloat16* pd = (__nv_bfloat16*)epi.dst[p] + qoff;
+        *reinterpret_cast<uint32_t*>(pd + i) = lo;
+        *reinterpret_cast<uint32_t*>(pd + half + i) = hi;
+      }
+  }
+  // v: plain copy into the cache slot
+  const int n_v = Hkv * (D / 8);
+  for (int t = threadIdx.x; t < n_v; t += blockDim.x) {
+    int g = t / (D / 8), c8 = (t % (D / 8)) * 8;
+    const __nv_bfloat16* x = src + (size_t)g * (G + 2) * D + (size_t)(G + 1) * D + c8;
+    __nv_bfloat16* dst = vc + (((size_t)pg * Hkv + g) * page + off) * D + c8;
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(x);
+  }
+  epi_signal(epi);
+}
+
+kd_status launch_rope_append(const kd_attr_rope_append& a, const void* qkv, const int32_t* bt, const int32_t* sl,
+                             void* q_out, void* kc, void* vc, const LaunchCtx& c, uint32_t* signals) {
+  if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "rope_append: only bf16 activations");
+  if (a.rows == 0 || a.n_kv_heads == 0 || a.n_heads % a.n_kv_heads || a.head_dim % 8 || a.head_dim < 8 ||
+      a.page == 0 || a.pages_per_seq == 0)
+    return fail(KD_ERR_UNSUPPORTED, "rope_append: unsupported shape");
+  if (!qkv || !bt || !sl || !q_out || !kc || !vc) return fail(KD_ERR_INVALID_ARG, "rope_append: NULL pointer");
+  size_t smem = sizeof(float) * a.head_dim;
+  rope_append_kernel<<<a.rows, 256, smem, c.stream>>>(
+      (const __nv_bfloat16*)qkv, bt, sl, (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc,
+      (int)a.n_heads, (int)a.n_kv_heads, (int)a.head_dim, (int)a.page, (int)a.pages_per_seq, a.theta, c.epi);
+  KD_CUDA_CHECK(cudaGetLastError(), "rope_append launch");
+  if (signals) *signals = a.rows;
+  return KD_OK;
+}
+
+// ------------------------------------------------------------------ runtime support
+struct PeerSlots {
+  unsigned* slot[8];     // &peer.ctrl.barrier[me]
+  unsigned* mine[8];     // &my.ctrl.barrier[peer]
+};
+
+__global__ void step_begin_kernel2(unsigned* epoch, PeerSlots ps, int n_peers) {
+  if (threadIdx.x != 0) return;
+  unsigned e = *epoch + 1;
+  *epoch = e;
+  if (n_peers == 0) return;
+  fence_acq_rel_sys();
+  for (int p = 0; p < n_peers; ++p) red_release_sys_add(ps.slot[p], 1u);
+  for (int p = 0; p < n_peers; ++p) {
+    long long spins = 0;
+    while (ld_acquire_sys(ps.mine[p]) < e) {
+      if (++spins > (1ll << 34)) break;  // watchdog (~tens of seconds); surfaces as a stuck step
+      __nanosleep(64);
+    }
+  }
+}
+
+kd_status launch_step_begin(unsigned* epoch, unsigned* const* mine, unsigned* const* peer_slots, int n_peers,
+                            cudaStream_t s) {
+  // mine[j] = my barrier word counting peer j's arrivals; peer_slots[j] = peer j's word for me
+  if (n_peers > 8) return fail(KD_ERR_UNSUPPORTED, "step_begin: more than 8 peers");
+  PeerSlots ps{};
+  for (int j = 0; j < n_peers; ++j) {
+    ps.slot[j] = peer_slots[j];
+    ps.mine[j] = mine[j];
+  }
+  step_begin_kernel2<<<1, 32, 0, s>>>(epoch, ps, n_peers);
+  KD_CUDA_CHECK(cudaGetLastError(), "step_begin launch");
+  return KD_OK;
+}
+
+__global__ void wait_kernel(WaitList w, const unsigned* epoch, unsigned* err) {
+  if (threadIdx.x >= w.n) return;
+  const unsigned target = (*epoch) * w.mult[threadIdx.x];
+  long long spins = 0;
+  while (ld_acquire_sys(w.flag[threadIdx.x]) < target) {
+    if (++spins > (1ll << 30)) {  // watchdog: record and give up (KD_ERR_TIMEOUT at kd_runtime_check)
+      atomicExch(err, 1u);
+      break;
+    }
+    __nanosleep(32);
+  }
+}
+
+kd_status launch_wait(const WaitList& w, const unsigned* epoch, unsigned* err, cudaStream_t s) {
+  if (w.n <= 0) return KD_OK;
+  wait_kernel<<<1, 32, 0, s>>>(w, epoch, err);
+  KD_CUDA_CHECK(cudaGetLastError(), "wait launch");
+  return KD_OK;
+}
+
+template <typename T>
+static kd_status attrs_of(const std::vector<uint8_t>& v, T* out) {
+  if (v.size() != sizeof(T)) return fail(KD_ERR_INVALID_ARG, "op attrs have the wrong size for the op");
+  std::memcpy(out, v.data(), sizeof(T));
+  return KD_OK;
+}
+
+kd_status attention_signals(const kd_attr_attention& a, uint32_t* s);  // attention.cu
+kd_status gemm_signals(const kd_attr_gemm& a, uint32_t* s);            // gemm.cu
+
+kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* signals) {
+  kd_status st = KD_OK;
+  switch (op) {
+    case KD_OP_ADD_RMSNORM: { kd_attr_add_rmsnorm a; if ((st = attrs_of(attrs, &a))) return st; *signals = a.rows; return KD_OK; }
+    case KD_OP_ROPE_APPEND: { kd_attr_rope_append a; if ((st = attrs_of(attrs, &a))) return st; *signals = a.rows; return KD_OK; }
+    case KD_OP_SILU_MUL: { kd_attr_silu_mul a; if ((st = attrs_of(attrs, &a))) return st; *signals = silu_grid(a); return KD_OK; }
+    case KD_OP_RESIDUAL_ADD: { kd_attr_residual_add a; if ((st = attrs_of(attrs, &a))) return st; *signals = residual_grid(a); return KD_OK; }
+    case KD_OP_ATTENTION: { kd_attr_attention a; if ((st = attrs_of(attrs, &a))) return st; return attention_signals(a, signals); }
+    case KD_OP_GEMM: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(a, signals); }
+  }
+  *signals = 0;
+  return KD_OK;
+}
+
+}  // namespace kd

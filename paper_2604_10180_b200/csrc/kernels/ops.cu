@@ -1,0 +1,104 @@
+// ops.cu — single-op entry points of the C ABI (kd.h "single ops") and the
+// per-op scratch sizing used by the planner's workspace layout.
+#include "launch.hpp"
+
+namespace kd {
+
+template <typename T>
+static kd_status attrs_as(const std::vector<uint8_t>& v, T* out) {
+  if (v.size() != sizeof(T)) return fail(KD_ERR_INVALID_ARG, "op attrs have the wrong size for the op");
+  std::memcpy(out, v.data(), sizeof(T));
+  return KD_OK;
+}
+
+kd_status op_scratch_bytes(uint32_t op, const std::vector<uint8_t>& attrs, u64* bytes) {
+  *bytes = 0;
+  switch (op) {
+    case KD_OP_GEMM: {
+      kd_attr_gemm a;
+      kd_status s = attrs_as(attrs, &a);
+      if (s) return s;
+      return gemm_scratch_bytes(a, bytes);
+    }
+    case KD_OP_ATTENTION: {
+      kd_attr_attention a;
+      kd_status s = attrs_as(attrs, &a);
+      if (s) return s;
+      return attention_scratch_bytes(a, bytes);
+    }
+    default:
+      return KD_OK;
+  }
+}
+
+}  // namespace kd
+
+using namespace kd;
+
+extern "C" {
+
+kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes) {
+  if (!attrs || !bytes) return fail(KD_ERR_INVALID_ARG, "kd_op_scratch_bytes: NULL argument");
+  switch (op) {
+    case KD_OP_GEMM: return gemm_scratch_bytes(*(const kd_attr_gemm*)attrs, bytes);
+    case KD_OP_ATTENTION: return attention_scratch_bytes(*(const kd_attr_attention*)attrs, bytes);
+    case KD_OP_ADD_RMSNORM:
+    case KD_OP_ROPE_APPEND:
+    case KD_OP_SILU_MUL:
+    case KD_OP_RESIDUAL_ADD: *bytes = 0; return KD_OK;
+  }
+  return fail(KD_ERR_INVALID_ARG, "kd_op_scratch_bytes: unknown op");
+}
+
+kd_status kd_op_add_rmsnorm(const kd_attr_add_rmsnorm* a, float* r, const void* delta, const void* gamma, void* h,
+                            void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_add_rmsnorm: NULL attrs");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  return launch_add_rmsnorm(*a, r, delta, gamma, h, c, nullptr);
+}
+
+kd_status kd_op_gemm(const kd_attr_gemm* a, const void* X, const void* W, void* Y, void* scratch, void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_gemm: NULL attrs");
+  GemmPlan gp;
+  kd_status s = gemm_prepare(*a, X, W, &gp);
+  if (s) return s;
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  c.scratch = scratch;
+  return launch_gemm(gp, Y, c, nullptr);
+}
+
+kd_status kd_op_rope_append(const kd_attr_rope_append* a, const void* qkv, const int32_t* block_table,
+                            const int32_t* seq_len, void* q_out, void* k_cache, void* v_cache, void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_rope_append: NULL attrs");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  return launch_rope_append(*a, qkv, block_table, seq_len, q_out, k_cache, v_cache, c, nullptr);
+}
+
+kd_status kd_op_attention(const kd_attr_attention* a, const void* q, const void* k_cache, const void* v_cache,
+                          const int32_t* block_table, const int32_t* seq_len, void* out, void* scratch,
+                          void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_attention: NULL attrs");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  c.scratch = scratch;
+  return launch_attention(*a, q, k_cache, v_cache, block_table, seq_len, out, c, nullptr);
+}
+
+kd_status kd_op_silu_mul(const kd_attr_silu_mul* a, const void* gu, void* out, void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_silu_mul: NULL attrs");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  return launch_silu_mul(*a, gu, out, c, nullptr);
+}
+
+kd_status kd_op_residual_add(const kd_attr_residual_add* a, float* r, const void* delta, void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_residual_add: NULL attrs");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  return launch_residual_add(*a, r, delta, c, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,506 @@
+// runtime.cu — per-device execution of a plan (§3.3 GPU workers:
+// "each GPU worker only executes the kernels assigned to it" P:378; recv
+// before k / send after k P:380; per-GPU CUDA-graph subgraphs P:398, P:456;
+// pipelined requests P:401-402). B200 redesign:
+//  * the send is fused into the producer kernel (peer stores of its primary
+//    output into the consumer GPU's landing slot + a system-scope release of
+//    a per-(micro-batch, producer, device) flag), see common.cuh `Epi`;
+//  * the recv is a 1-warp wait kernel on the consumer's stream that acquires
+//    the flag (target = epoch × signals; epochs advance once per step, so
+//    flags are never reset);
+//  * each device replays its static schedule (a subsequence of one global
+//    topological order → deadlock free) from a CUDA graph;
+//  * a step-begin barrier keeps a device from overwriting landing slots of a
+//    step its peers are still reading (WAR, R4).
+#include <algorithm>
+#include <map>
+#include <set>
+
+#include "launch.hpp"
+
+namespace kd {
+
+struct Launch {
+  enum Kind { KERNEL, WAIT, STEP_BEGIN } kind = KERNEL;
+  uint32_t micro = 0, kernel = 0, op = 0;
+  std::vector<void*> rd, wr;
+  LaunchCtx ctx;
+  WaitList wait;
+  GemmPlan* gemm = nullptr;  // owned
+  // step-begin barrier words
+  std::vector<unsigned*> bar_mine, bar_slots;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+struct DevState {
+  uint32_t logical = 0;
+  int cuda = 0;
+  uint8_t* ws = nullptr;
+  uint64_t ws_bytes = 0;
+  std::vector<Launch> launches;
+  cudaGraphExec_t exec = nullptr;
+  bool captured = false;
+};
+
+}  // namespace kd
+
+struct kd_runtime {
+  const kd_plan* plan = nullptr;
+  std::vector<kd::DevState> devs;              // local devices
+  std::vector<uint8_t*> ws_of;                 // workspace base per logical device (local or peer-mapped)
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, void*> bind;  // (buf, micro, dev)
+  uint32_t mode = KD_MODE_DISAGG;
+  bool use_graph = true;
+  bool prepared = false;
+  uint32_t profile_op = 0;
+  ~kd_runtime() {
+    for (auto& d : devs) {
+      cudaSetDevice(d.cuda);
+      if (d.exec) cudaGraphExecDestroy(d.exec);
+      for (auto& l : d.launches) {
+        delete l.gemm;
+        if (l.ev0) cudaEventDestroy(l.ev0);
+        if (l.ev1) cudaEventDestroy(l.ev1);
+      }
+    }
+  }
+};
+
+using namespace kd;
+
+namespace {
+
+template <typename T>
+T attrs_get(const Kernel& k) {
+  T a;
+  std::memcpy(&a, k.attrs.data(), sizeof(T));
+  return a;
+}
+
+kd_status check_attrs(const Kernel& k) {
+  size_t need = 0;
+  switch (k.op) {
+    case KD_OP_NONE: return KD_OK;
+    case KD_OP_ADD_RMSNORM: need = sizeof(kd_attr_add_rmsnorm); break;
+    case KD_OP_GEMM: need = sizeof(kd_attr_gemm); break;
+    case KD_OP_ROPE_APPEND: need = sizeof(kd_attr_rope_append); break;
+    case KD_OP_ATTENTION: need = sizeof(kd_attr_attention); break;
+    case KD_OP_SILU_MUL: need = sizeof(kd_attr_silu_mul); break;
+    case KD_OP_RESIDUAL_ADD: need = sizeof(kd_attr_residual_add); break;
+    default: return fail(KD_ERR_UNSUPPORTED, "runtime: unknown op");
+  }
+  if (k.attrs.size() != need) return fail(KD_ERR_INVALID_ARG, "runtime: op attrs have the wrong size");
+  // read/write arity per op (kd.h op table)
+  size_t nr = k.reads.size(), nw = k.writes.size();
+  bool ok = true;
+  switch (k.op) {
+    case KD_OP_ADD_RMSNORM: ok = (nr == 2 || nr == 3) && nw == 2; break;
+    case KD_OP_GEMM: ok = nr == 2 && nw == 1; break;
+    case KD_OP_ROPE_APPEND: ok = nr == 3 && nw == 3; break;
+    case KD_OP_ATTENTION: ok = nr == 5 && nw == 1; break;
+    case KD_OP_SILU_MUL: ok = nr == 1 && nw == 1; break;
+    case KD_OP_RESIDUAL_ADD: ok = nr == 2 && nw == 1; break;
+  }
+  if (!ok) return fail(KD_ERR_INVALID_ARG, "runtime: wrong number of read/write spans for the op");
+  return KD_OK;
+}
+
+kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s) {
+  uint8_t* ws = d.ws;
+  const auto& L = rt->plan->layout[d.logical];
+  unsigned* epoch = (unsigned*)(ws + L.ctrl_off);
+  unsigned* err = epoch + 1;
+  if (l.kind == Launch::STEP_BEGIN)
+    return launch_step_begin(epoch, l.bar_mine.data(), l.bar_slots.data(), (int)l.bar_mine.size(), s);
+  if (l.kind == Launch::WAIT) return launch_wait(l.wait, epoch, err, s);
+  LaunchCtx c = l.ctx;
+  c.stream = s;
+  if (rt->mode == KD_MODE_NO_TRANSFER) c.epi.n = 0;
+  const bool prof = rt->profile_op && l.op == rt->profile_op;
+  if (prof) KD_CUDA_CHECK(cudaEventRecordWithFlags(l.ev0, s, cudaEventRecordExternal), "event record");
+  kd_status st = KD_OK;
+  const Kernel& K = rt->plan->g->kernels[l.kernel];
+  uint32_t sig = 0;
+  switch (l.op) {
+    case KD_OP_NONE: break;
+    case KD_OP_ADD_RMSNORM: {
+      auto a = attrs_get<kd_attr_add_rmsnorm>(K);
+      const void* delta = a.has_delta ? l.rd[1] : nullptr;
+      const void* gamma = a.has_delta ? l.rd[2] : l.rd[1];
+      st = launch_add_rmsnorm(a, (float*)l.wr[1], delta, gamma, l.wr[0], c, &sig);
+      break;
+    }
+    case KD_OP_GEMM: st = launch_gemm(*l.gemm, l.wr[0], c, &sig); break;
+    case KD_OP_ROPE_APPEND: {
+      auto a = attrs_get<kd_attr_rope_append>(K);
+      st = launch_rope_append(a, l.rd[0], (const int32_t*)l.rd[1], (const int32_t*)l.rd[2], l.wr[0], l.wr[1],
+                              l.wr[2], c, &sig);
+      break;
+    }
+    case KD_OP_ATTENTION: {
+      auto a = attrs_get<kd_attr_attention>(K);
+      st = launch_attention(a, l.rd[0], l.rd[1], l.rd[2], (const int32_t*)l.rd[3], (const int32_t*)l.rd[4], l.wr[0],
+                            c, &sig);
+      break;
+    }
+    case KD_OP_SILU_MUL: {
+      auto a = attrs_get<kd_attr_silu_mul>(K);
+      st = launch_silu_mul(a, l.rd[0], l.wr[0], c, &sig);
+      break;
+    }
+    case KD_OP_RESIDUAL_ADD: {
+      auto a = attrs_get<kd_attr_residual_add>(K);
+      st = launch_residual_add(a, (float*)l.wr[0], l.rd[1], c, &sig);
+      break;
+    }
+  }
+  if (st) return st;
+  if (prof) KD_CUDA_CHECK(cudaEventRecordWithFlags(l.ev1, s, cudaEventRecordExternal), "event record");
+  return KD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+kd_status kd_runtime_create(const kd_plan* p, const uint32_t* local_devs, const int32_t* cuda_ordinal, uint32_t n_local,
+                            kd_runtime** out) {
+  if (!p || !local_devs || !cuda_ordinal || !out || n_local == 0)
+    return fail(KD_ERR_INVALID_ARG, "kd_runtime_create: bad argument");
+  auto* rt = new kd_runtime();
+  rt->plan = p;
+  rt->ws_of.assign(p->n_dev, nullptr);
+  std::set<uint32_t> seen;
+  for (uint32_t j = 0; j < n_local; ++j) {
+    if (local_devs[j] >= p->n_dev || !seen.insert(local_devs[j]).second) {
+      delete rt;
+      return fail(KD_ERR_INVALID_ARG, "kd_runtime_create: bad or duplicate logical device");
+    }
+    DevState d;
+    d.logical = local_devs[j];
+    d.cuda = cuda_ordinal[j];
+    rt->devs.push_back(d);
+  }
+  *out = rt;
+  return KD_OK;
+}
+
+void kd_runtime_destroy(kd_runtime* rt) { delete rt; }
+
+kd_status kd_runtime_bind(kd_runtime* rt, uint32_t buf, uint32_t micro, uint32_t dev, void* dev_ptr) {
+  if (!rt || !dev_ptr) return fail(KD_ERR_INVALID_ARG, "kd_runtime_bind: NULL argument");
+  const kd_graph* g = rt->plan->g;
+  if (buf >= g->buffers.size() || dev >= rt->plan->n_dev) return fail(KD_ERR_INVALID_ARG, "kd_runtime_bind: bad id");
+  const uint32_t EXT = KD_BUF_WEIGHT | KD_BUF_INPUT | KD_BUF_OUTPUT | KD_BUF_PERSISTENT;
+  if (!(g->buffers[buf].flags & EXT)) return fail(KD_ERR_INVALID_ARG, "kd_runtime_bind: internal buffers live in the workspace");
+  bool per = g->buffers[buf].flags & KD_BUF_PER_MICROBATCH;
+  if (per ? micro >= rt->plan->n_micro : micro != 0) return fail(KD_ERR_INVALID_ARG, "kd_runtime_bind: bad micro-batch");
+  rt->bind[{buf, micro, dev}] = dev_ptr;
+  rt->prepared = false;
+  return KD_OK;
+}
+
+kd_status kd_runtime_set_workspace(kd_runtime* rt, uint32_t dev, void* dev_ptr, uint64_t bytes) {
+  if (!rt || !dev_ptr) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_workspace: NULL argument");
+  for (auto& d : rt->devs)
+    if (d.logical == dev) {
+      if (bytes < rt->plan->layout[dev].total) return fail(KD_ERR_OOM, "kd_runtime_set_workspace: workspace too small");
+      if ((uintptr_t)dev_ptr & 255) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_workspace: need 256-byte alignment");
+      d.ws = (uint8_t*)dev_ptr;
+      d.ws_bytes = bytes;
+      rt->ws_of[dev] = (uint8_t*)dev_ptr;
+      rt->prepared = false;
+      return KD_OK;
+    }
+  return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_workspace: device is not local");
+}
+
+kd_status kd_runtime_set_peer_workspace(kd_runtime* rt, uint32_t dev, void* mapped_ptr) {
+  if (!rt || !mapped_ptr || dev >= rt->plan->n_dev) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_peer_workspace: bad argument");
+  for (auto& d : rt->devs)
+    if (d.logical == dev) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_peer_workspace: device is local");
+  rt->ws_of[dev] = (uint8_t*)mapped_ptr;
+  rt->prepared = false;
+  return KD_OK;
+}
+
+kd_status kd_runtime_set_mode(kd_runtime* rt, uint32_t mode) {
+  if (!rt || mode > KD_MODE_LOG) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_mode: bad argument");
+  rt->mode = mode;
+  rt->prepared = false;
+  for (auto& d : rt->devs) d.captured = false;
+  return KD_OK;
+}
+
+kd_status kd_runtime_set_graph(kd_runtime* rt, int32_t enable) {
+  if (!rt) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_graph: NULL runtime");
+  rt->use_graph = enable != 0;
+  for (auto& d : rt->devs) d.captured = false;
+  return KD_OK;
+}
+
+kd_status kd_runtime_profile_op(kd_runtime* rt, uint32_t op) {
+  if (!rt) return fail(KD_ERR_INVALID_ARG, "kd_runtime_profile_op: NULL runtime");
+  rt->profile_op = op;
+  rt->prepared = false;  // re-prepare (events) and re-capture with event nodes
+  return KD_OK;
+}
+
+kd_status kd_runtime_prepare(kd_runtime* rt) {
+  if (!rt) return fail(KD_ERR_INVALID_ARG, "kd_runtime_prepare: NULL runtime");
+  const kd_plan* P = rt->plan;
+  const kd_graph* g = P->g;
+  const uint32_t n = P->n_dev, N = P->n_micro;
+  const uint32_t EXT = KD_BUF_WEIGHT | KD_BUF_INPUT | KD_BUF_OUTPUT | KD_BUF_PERSISTENT;
+  for (uint32_t v = 0; v < n; ++v)
+    if (!rt->ws_of[v]) return fail(KD_ERR_STATE, "kd_runtime_prepare: workspace of device " + std::to_string(v) + " not set");
+  for (const auto& K : g->kernels) {
+    kd_status s = check_attrs(K);
+    if (s) return s;
+  }
+  // transfer lookup: (micro, producer, dst) -> transfer index
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, uint32_t> xidx;
+  for (uint32_t t = 0; t < P->transfers.size(); ++t) {
+    const auto& x = P->transfers[t];
+    xidx[{x.micro, x.producer, x.dst_dev}] = t;
+  }
+  // incoming remote producers per (consumer kernel, buffer)
+  std::map<std::pair<uint32_t, uint32_t>, std::set<uint32_t>> remote_src;
+  for (const auto& e : g->edges)
+    if (P->assign[e.src] != P->assign[e.dst]) remote_src[{e.dst, e.buf}].insert(e.src);
+
+  for (auto& d : rt->devs) {
+    KD_CUDA_CHECK(cudaSetDevice(d.cuda), "cudaSetDevice");
+    kd_status s = kernels_init();
+    if (s) return s;
+    // peer access to every other physical device we store into
+    for (uint32_t v = 0; v < n; ++v) {
+      if (v == d.logical) continue;
+      for (auto& o : rt->devs)
+        if (o.logical == v && o.cuda != d.cuda) {
+          int can = 0;
+          cudaDeviceCanAccessPeer(&can, d.cuda, o.cuda);
+          if (can) {
+            cudaError_t e = cudaDeviceEnablePeerAccess(o.cuda, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return set_cuda_error(e, "peer access");
+            cudaGetLastError();
+          }
+        }
+    }
+    for (auto& l : d.launches) {
+      delete l.gemm;
+      if (l.ev0) cudaEventDestroy(l.ev0);
+      if (l.ev1) cudaEventDestroy(l.ev1);
+    }
+    d.launches.clear();
+    if (d.exec) {
+      cudaGraphExecDestroy(d.exec);
+      d.exec = nullptr;
+    }
+    d.captured = false;
+    const auto& L = P->layout[d.logical];
+    auto local_ptr = [&](uint32_t buf, uint32_t i, uint64_t off) -> void* {
+      const auto& B = g->buffers[buf];
+      uint32_t inst = (B.flags & KD_BUF_PER_MICROBATCH) ? i : 0;
+      if (B.flags & EXT) {
+        auto it = rt->bind.find({buf, inst, d.logical});
+        if (it == rt->bind.end()) return nullptr;
+        return (uint8_t*)it->second + off;
+      }
+      auto it = L.act.find({buf, inst});
+      if (it == L.act.end()) return nullptr;
+      return d.ws + it->second + off;
+    };
+    const bool multi = n > 1;
+    const bool transfers_on = rt->mode != KD_MODE_NO_TRANSFER;
+    if (multi) {
+      Launch sb;
+      sb.kind = Launch::STEP_BEGIN;
+      for (uint32_t v = 0; v < n; ++v) {
+        if (v == d.logical) continue;
+        sb.bar_mine.push_back((unsigned*)(d.ws + L.ctrl_off + 64 + 4 * v));
+        sb.bar_slots.push_back((unsigned*)(rt->ws_of[v] + P->layout[v].ctrl_off + 64 + 4 * d.logical));
+      }
+      d.launches.push_back(sb);
+    }
+    std::set<uint32_t> waited;
+    for (const auto& e : P->sched) {
+      if (e.dev != d.logical) continue;
+      const uint32_t i = e.micro, k = e.kernel;
+      const Kernel& K = g->kernels[k];
+      Launch l;
+      l.kind = Launch::KERNEL;
+      l.micro = i;
+      l.kernel = k;
+      l.op = K.op;
+      WaitList wl;
+      for (const auto& sp : K.reads) {
+        auto rs = remote_src.find({k, sp.buf});
+        if (rs == remote_src.end()) {
+          void* ptr = local_ptr(sp.buf, i, sp.off);
+          if (!ptr) return fail(KD_ERR_STATE, "kd_runtime_prepare: buffer " + std::to_string(sp.buf) + " not bound on device " + std::to_string(d.logical));
+          l.rd.push_back(ptr);
+          continue;
+        }
+        if (rs->second.size() != 1)
+          return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: a read span has several remote producers");
+        const uint32_t src = *rs->second.begin();
+        const Kernel& S = g->kernels[src];
+        if (S.writes.empty() || S.writes[0].buf != sp.buf || sp.off < S.writes[0].off ||
+            sp.off + sp.len > S.writes[0].off + S.writes[0].len)
+          return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: a cut edge must read the producer's primary output");
+        // all bytes of the span must come from that producer
+        for (const auto& e2 : g->edges)
+          if (e2.dst == k && e2.buf == sp.buf && e2.src != src &&
+              e2.offset < sp.off + sp.len && sp.off < e2.offset + e2.len)
+            return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: a cut read span mixes local and remote writers");
+        uint32_t t = xidx.at({i, src, d.logical});
+        const auto& land = L.landing.at(t);
+        if (transfers_on) {
+          l.rd.push_back(d.ws + land.first + (sp.off - S.writes[0].off));
+        } else {
+          // ablation: read a resident copy (the landing slot, pre-filled by a previous DISAGG step)
+          l.rd.push_back(d.ws + land.first + (sp.off - S.writes[0].off));
+        }
+        if (transfers_on && !waited.count(t)) {
+          waited.insert(t);
+          uint32_t sig = 0;
+          kd_status s2 = op_signals(S.op, S.attrs, &sig);
+          if (s2) return s2;
+          if (wl.n == 8) {
+            Launch w;
+            w.kind = Launch::WAIT;
+            w.wait = wl;
+            d.launches.push_back(w);
+            wl.n = 0;
+          }
+          wl.flag[wl.n] = (unsigned*)(d.ws + land.second);
+          wl.mult[wl.n] = sig;
+          ++wl.n;
+        }
+      }
+      if (wl.n) {
+        Launch w;
+        w.kind = Launch::WAIT;
+        w.wait = wl;
+        d.launches.push_back(w);
+      }
+      for (const auto& sp : K.writes) {
+        void* ptr = local_ptr(sp.buf, i, sp.off);
+        if (!ptr) return fail(KD_ERR_STATE, "kd_runtime_prepare: output buffer " + std::to_string(sp.buf) + " not bound on device " + std::to_string(d.logical));
+        l.wr.push_back(ptr);
+      }
+      // fused sends: every remote device reading this kernel's output
+      for (uint32_t v = 0; v < n; ++v) {
+        auto it = xidx.find({i, k, v});
+        if (it == xidx.end()) continue;
+        if (l.ctx.epi.n == kMaxPeers) return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: more than 4 consumer devices");
+        const auto& Lv = P->layout[v];
+        const auto& land = Lv.landing.at(it->second);
+        l.ctx.epi.dst[l.ctx.epi.n] = rt->ws_of[v] + land.first;
+        l.ctx.epi.flag[l.ctx.epi.n] = (unsigned*)(rt->ws_of[v] + land.second);
+        ++l.ctx.epi.n;
+      }
+      l.ctx.scratch = d.ws + L.scratch_off;
+      if (K.op == KD_OP_GEMM) {
+        l.gemm = new GemmPlan();
+        kd_status s3 = gemm_prepare(attrs_get<kd_attr_gemm>(K), l.rd[0], l.rd[1], l.gemm);
+        if (s3) return s3;
+      }
+      if (rt->profile_op) {
+        KD_CUDA_CHECK(cudaEventCreate(&l.ev0), "event create");
+        KD_CUDA_CHECK(cudaEventCreate(&l.ev1), "event create");
+      }
+      d.launches.push_back(std::move(l));
+    }
+  }
+  rt->prepared = true;
+  return KD_OK;
+}
+
+kd_status kd_step(kd_runtime* rt, void* const* streams) {
+  if (!rt || !streams) return fail(KD_ERR_INVALID_ARG, "kd_step: NULL argument");
+  if (!rt->prepared) {
+    kd_status s = kd_runtime_prepare(rt);
+    if (s) return s;
+  }
+  for (size_t j = 0; j < rt->devs.size(); ++j) {
+    auto& d = rt->devs[j];
+    cudaStream_t s = (cudaStream_t)streams[j];
+    KD_CUDA_CHECK(cudaSetDevice(d.cuda), "cudaSetDevice");
+    if (!rt->use_graph) {
+      for (auto& l : d.launches) {
+        kd_status st = enqueue(rt, d, l, s);
+        if (st) return st;
+      }
+      continue;
+    }
+    if (!d.captured) {
+      if (d.exec) {
+        cudaGraphExecDestroy(d.exec);
+        d.exec = nullptr;
+      }
+      KD_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+      kd_status st = KD_OK;
+      for (auto& l : d.launches) {
+        st = enqueue(rt, d, l, s);
+        if (st) break;
+      }
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      if (st) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      if (ce != cudaSuccess) return set_cuda_error(ce, "end capture");
+      ce = cudaGraphInstantiate(&d.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) return set_cuda_error(ce, "graph instantiate");
+      d.captured = true;
+    }
+    KD_CUDA_CHECK(cudaGraphLaunch(d.exec, s), "graph launch");
+  }
+  return KD_OK;
+}
+
+kd_status kd_runtime_check(kd_runtime* rt) {
+  if (!rt) return fail(KD_ERR_INVALID_ARG, "kd_runtime_check: NULL runtime");
+  for (auto& d : rt->devs) {
+    KD_CUDA_CHECK(cudaSetDevice(d.cuda), "cudaSetDevice");
+    KD_CUDA_CHECK(cudaDeviceSynchronize(), "device synchronize");
+    unsigned err = 0;
+    KD_CUDA_CHECK(cudaMemcpy(&err, d.ws + rt->plan->layout[d.logical].ctrl_off + 4, 4, cudaMemcpyDeviceToHost),
+                  "read error word");
+    if (err) return fail(KD_ERR_TIMEOUT, "kd_runtime_check: a flag wait timed out on device " + std::to_string(d.logical));
+  }
+  return KD_OK;
+}
+
+kd_status kd_runtime_launch_count(const kd_runtime* rt, uint32_t j, uint32_t* n) {
+  if (!rt || !n || j >= rt->devs.size()) return fail(KD_ERR_INVALID_ARG, "kd_runtime_launch_count: bad argument");
+  if (!rt->prepared) return fail(KD_ERR_STATE, "kd_runtime_launch_count: runtime not prepared");
+  *n = (uint32_t)rt->devs[j].launches.size();
+  return KD_OK;
+}
+
+kd_status kd_runtime_op_time(kd_runtime* rt, double* ms, uint64_t* launches) {
+  if (!rt || !ms || !launches) return fail(KD_ERR_INVALID_ARG, "kd_runtime_op_time: NULL argument");
+  double tot = 0;
+  uint64_t cnt = 0;
+  for (auto& d : rt->devs) {
+    KD_CUDA_CHECK(cudaSetDevice(d.cuda), "cudaSetDevice");
+    for (auto& l : d.launches)
+      if (l.ev0 && l.kind == Launch::KERNEL && l.op == rt->profile_op) {
+        KD_CUDA_CHECK(cudaEventSynchronize(l.ev1), "event sync");
+        float t = 0;
+        KD_CUDA_CHECK(cudaEventElapsedTime(&t, l.ev0, l.ev1), "event elapsed");
+        tot += t;
+        ++cnt;
+      }
+  }
+  *ms = tot;
+  *launches = cnt;
+  return KD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,277 @@
+"""Decoder-layer kernel graph (the workload the hot path executes) declared
+through the C ABI, plus the device resources a runtime binds.
+
+The graph is the per-micro-batch kernel sequence of a Llama-style decode step
+(SURVEY §8(a) a3–a10; C1 program order), declared with exact read/write spans
+(the paper's library-kernel case):
+
+  per layer l:  norm1  (a3)  reads r, d_{l-1}, γ1        writes h1, r
+                qkv    (a4)  reads h1, W_qkv              writes qkv
+                rope   (a5)  reads qkv, bt, sl            writes q, K_l, V_l
+                attn   (a6)  reads q, K_l, V_l, bt, sl    writes attn
+                o      (a7)  reads attn, W_o              writes o
+                norm2  (a3)  reads r, o, γ2               writes h2, r
+                gu     (a9)  reads h2, W_gu               writes gu
+                silu   (a8)  reads gu                     writes a
+                down   (a10) reads a, W_d                 writes d
+  after layer L−1: final residual add (C1.11) reads r, d  writes r
+
+Template ids implement repeated-layer reduction (A15) and the persistent-state
+co-location rule (R6): the kernels touching the residual stream r share one
+template, rope and attention (touching K_l/V_l) share one.
+This module only declares and allocates; all computation is in libkd.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+import os
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _kd as K
+from .api import Graph, Machine, Plan, Runtime, place
+
+T_RESID, T_QKV, T_ATTN, T_O, T_GU, T_SILU, T_DOWN = range(7)
+MEMORY_ROLE = {T_RESID, T_ATTN, T_SILU}   # HBM-bound non-GEMM kernels
+GEMM_ROLE = {T_QKV, T_O, T_GU, T_DOWN}
+
+
+def b200_machine(n_dev: int, hbm_Bps: Optional[float] = None, tc_flops: Optional[float] = None,
+                 link_Bps: float = 770e9, link_lat_ps: int = 4_000_000, launch_ps: int = 2_500_000) -> Machine:
+    """Cost-model machine of n homogeneous B200s behind NVSwitch: HBM and
+    bf16 peaks from MEASURED_PEAKS.json when present (else the profiling
+    guide's fallback 6.65 TB/s / 1.59 PF), measured peer copy 770 GB/s/dir,
+    ~4 µs handoff latency (flag release → wait kernel), 2.5 µs launch floor."""
+    peaks = {}
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        peaks = json.load(open(p))
+    hbm = hbm_Bps or peaks.get("hbm_gbs", 6650.0) * 1e9
+    tc = tc_flops or peaks.get("bf16_tflops", 1590.0) * 1e12
+    return Machine.uniform(n_dev, int(hbm), int(tc), int(link_Bps), int(link_lat_ps), int(launch_ps))
+
+
+@dataclass
+class KernelInfo:
+    name: str
+    layer: int
+    template: int
+    kid: int
+
+
+class DecoderGraph:
+    """Declares the decoder kernel graph for one micro-batch of cfg.m rows."""
+
+    def __init__(self, cfg, act: int = K.KD_BF16):
+        if act != K.KD_BF16:
+            raise NotImplementedError("only the bf16 path is built")
+        self.cfg = cfg
+        m, H, L = cfg.m, cfg.hidden, cfg.n_layers
+        Hq, Hkv, D, F = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn
+        pps = cfg.pages_per_seq
+        E = 2  # bf16 bytes
+        g = Graph()
+        self.g = g
+        self.buf: Dict[str, int] = {}
+        self.shape: Dict[str, tuple] = {}
+        self.dtype: Dict[str, str] = {}
+        W, PM = K.KD_BUF_WEIGHT, K.KD_BUF_PER_MICROBATCH
+        PERS, INP, OUT = K.KD_BUF_PERSISTENT, K.KD_BUF_INPUT, K.KD_BUF_OUTPUT
+
+        def buf(name, shape, dt, flags):
+            nbytes = int(np.prod(shape)) * {"bf16": 2, "f32": 4, "i32": 4}[dt]
+            self.buf[name] = g.add_buffer(nbytes, flags)
+            self.shape[name] = tuple(shape)
+            self.dtype[name] = dt
+            return self.buf[name]
+
+        def whole(name):
+            b = self.buf[name]
+            n = int(np.prod(self.shape[name])) * {"bf16": 2, "f32": 4, "i32": 4}[self.dtype[name]]
+            return (b, 0, n)
+
+        buf("r", (m, H), "f32", PERS | INP | OUT | PM)
+        buf("bt", (m, pps), "i32", INP | PM)
+        buf("sl", (m,), "i32", INP | PM)
+        for l in range(L):
+            buf(f"w_qkv.{l}", (cfg.qkv_dim, H), "bf16", W)
+            buf(f"w_o.{l}", (H, Hq * D), "bf16", W)
+            buf(f"w_gu.{l}", (2 * F, H), "bf16", W)
+            buf(f"w_d.{l}", (H, F), "bf16", W)
+            buf(f"g1.{l}", (H,), "bf16", W)
+            buf(f"g2.{l}", (H,), "bf16", W)
+            buf(f"kc.{l}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+            buf(f"vc.{l}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+            for nm, shp in (("h1", (m, H)), ("qkv", (m, cfg.qkv_dim)), ("q", (m, Hq * D)), ("attn", (m, Hq * D)),
+                            ("o", (m, H)), ("h2", (m, H)), ("gu", (m, 2 * F)), ("a", (m, F)), ("d", (m, H))):
+                buf(f"{nm}.{l}", shp, "bf16", PM)
+
+        self.kernels: List[KernelInfo] = []
+
+        def add(name, layer, tmpl, op, reads, writes, attrs, flops=0):
+            kid = g.add_kernel(op, [whole(x) for x in reads], [whole(x) for x in writes], attrs, flops, -1, tmpl)
+            self.kernels.append(KernelInfo(name, layer, tmpl, kid))
+            return kid
+
+        eps = float(cfg.eps)
+        for l in range(L):
+            has_d = 1 if l > 0 else 0
+            add("norm1", l, T_RESID, K.KD_OP_ADD_RMSNORM,
+                ["r"] + ([f"d.{l-1}"] if has_d else []) + [f"g1.{l}"], [f"h1.{l}", "r"],
+                K.kd_attr_add_rmsnorm(m, H, has_d, act, eps, 0))
+            add("qkv", l, T_QKV, K.KD_OP_GEMM, [f"h1.{l}", f"w_qkv.{l}"], [f"qkv.{l}"],
+                K.kd_attr_gemm(m, cfg.qkv_dim, H, act), 2 * m * cfg.qkv_dim * H)
+            add("rope", l, T_ATTN, K.KD_OP_ROPE_APPEND, [f"qkv.{l}", "bt", "sl"], [f"q.{l}", f"kc.{l}", f"vc.{l}"],
+                K.kd_attr_rope_append(m, Hq, Hkv, D, cfg.page, pps, act, 0, float(cfg.rope_theta)))
+            add("attn", l, T_ATTN, K.KD_OP_ATTENTION, [f"q.{l}", f"kc.{l}", f"vc.{l}", "bt", "sl"], [f"attn.{l}"],
+                K.kd_attr_attention(m, Hq, Hkv, D, cfg.page, pps, act, 0), 4 * m * Hq * cfg.context * D)
+            add("o", l, T_O, K.KD_OP_GEMM, [f"attn.{l}", f"w_o.{l}"], [f"o.{l}"],
+                K.kd_attr_gemm(m, H, Hq * D, act), 2 * m * H * Hq * D)
+            add("norm2", l, T_RESID, K.KD_OP_ADD_RMSNORM, ["r", f"o.{l}", f"g2.{l}"], [f"h2.{l}", "r"],
+                K.kd_attr_add_rmsnorm(m, H, 1, act, eps, 0))
+            add("gu", l, T_GU, K.KD_OP_GEMM, [f"h2.{l}", f"w_gu.{l}"], [f"gu.{l}"],
+                K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
+            add("silu", l, T_SILU, K.KD_OP_SILU_MUL, [f"gu.{l}"], [f"a.{l}"], K.kd_attr_silu_mul(m, F, act, 0))
+            add("down", l, T_DOWN, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
+                K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)
+        add("final_add", L - 1, T_RESID, K.KD_OP_RESIDUAL_ADD, ["r", f"d.{L-1}"], ["r"],
+            K.kd_attr_residual_add(m, H))
+        g.finalize()
+
+    def role_assign(self, mem_dev: int = 0, gemm_dev: int = 1) -> List[int]:
+        """Memory-bound kernels on one device, GEMMs on another (BJ config 1/2)."""
+        return [mem_dev if k.template in MEMORY_ROLE else gemm_dev for k in self.kernels]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class DecoderRuntime:
+    """Allocates and binds every external buffer on the devices the plan
+    needs, one zeroed workspace per local logical device, and runs steps.
+
+    `dev_map[logical] = cuda ordinal`; several logical devices may map to one
+    GPU (loopback). `inputs` (synth.DecoderInputs) provides exact host values
+    (parity runs); otherwise device-side seeded random values are used."""
+
+    def __init__(self, dg: DecoderGraph, assign: Sequence[int], n_dev: int, dev_map: Sequence[int],
+                 machine: Optional[Machine] = None, inputs=None, seed: int = 0, use_graph: bool = True):
+        torch = _torch()
+        cfg = dg.cfg
+        self.dg, self.cfg = dg, cfg
+        self.machine = machine or b200_machine(n_dev)
+        self.plan = Plan(dg.g, self.machine, list(assign), cfg.n_micro)
+        self.n_dev = n_dev
+        self.dev_map = list(dev_map)
+        self.rt = Runtime(self.plan, list(range(n_dev)), self.dev_map)
+        self.rt.set_graph(use_graph)
+        self.tensors: Dict[tuple, "torch.Tensor"] = {}
+        self.ws = []
+        N, m = cfg.n_micro, cfg.m
+        pps = cfg.pages_per_seq
+        tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "i32": torch.int32}
+        from synth import device_normal_
+        for name, b in dg.buf.items():
+            flags = 0
+            for d in range(n_dev):
+                if not self.plan.needs_binding(b, d):
+                    continue
+                per_micro = name in ("r", "bt", "sl") or name.startswith(("kc.", "vc."))
+                for i in range(N if per_micro else 1):
+                    t = torch.empty(dg.shape[name], dtype=tdt[dg.dtype[name]], device=f"cuda:{self.dev_map[d]}")
+                    self._fill(t, name, i, inputs, seed, device_normal_)
+                    self.tensors[(name, i, d)] = t
+                    self.rt.bind(b, i, d, t.data_ptr())
+        for d in range(n_dev):
+            nbytes = self.plan.workspace_bytes(d)
+            w = torch.zeros(nbytes + 256, dtype=torch.uint8, device=f"cuda:{self.dev_map[d]}")
+            off = (-w.data_ptr()) % 256
+            self.ws.append(w)
+            self.rt.set_workspace(d, w.data_ptr() + off, nbytes)
+        self.rt.prepare()
+        self.streams = [torch.cuda.Stream(device=f"cuda:{self.dev_map[d]}") for d in range(n_dev)]
+
+    # ------------------------------------------------------------------ inputs
+    def _fill(self, t, name, i, inputs, seed, device_normal_):
+        torch = _torch()
+        cfg = self.cfg
+        m, pps = cfg.m, cfg.pages_per_seq
+        base, _, lay = name.partition(".")
+        L = cfg.n_layers
+        if inputs is not None:
+            def put_bf16(bits):
+                t.copy_(torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16))
+            if name == "r":
+                t.copy_(torch.from_numpy(inputs.x[i * m:(i + 1) * m]))
+            elif name == "bt":
+                t.copy_(torch.from_numpy(inputs.block_table[i * m:(i + 1) * m] - i * m * pps))
+            elif name == "sl":
+                t.copy_(torch.from_numpy(inputs.seq_len[i * m:(i + 1) * m]))
+            elif base in ("kc", "vc"):
+                src = (inputs.k_cache if base == "kc" else inputs.v_cache)[int(lay)]
+                put_bf16(src[i * m * pps:(i + 1) * m * pps])
+            else:
+                lw = inputs.layers[int(lay)]
+                put_bf16({"w_qkv": lw.w_qkv, "w_o": lw.w_o, "w_gu": lw.w_gu, "w_d": lw.w_d,
+                          "g1": lw.gamma1, "g2": lw.gamma2}[base])
+            return
+        # device-side seeded values (throughput runs)
+        s = seed * 1_000_003 + self.dg.buf[name] * 131 + i
+        H, F = cfg.hidden, cfg.ffn
+        if name == "r":
+            device_normal_(t, s, 1.0)
+        elif name == "bt":
+            g = torch.Generator(device="cpu")
+            g.manual_seed(s)
+            perm = torch.randperm(m * pps, generator=g, dtype=torch.int64).to(torch.int32)
+            t.copy_(perm.view(m, pps))
+        elif name == "sl":
+            t.fill_(cfg.context)
+        elif base in ("kc", "vc"):
+            device_normal_(t, s, 1.0)
+        elif base in ("g1", "g2"):
+            device_normal_(t, s, 0.1)
+            t.add_(1.0)
+        else:
+            K_in = t.shape[1]
+            std = 1.0 / math.sqrt(K_in)
+            if base in ("w_o", "w_d"):
+                std /= math.sqrt(2.0 * L)
+            device_normal_(t, s, std)
+
+    # ------------------------------------------------------------------ run
+    def step(self):
+        self.rt.step([s.cuda_stream for s in self.streams])
+
+    def sync(self):
+        torch = _torch()
+        for d in range(self.n_dev):
+            torch.cuda.synchronize(self.dev_map[d])
+
+    def residual(self) -> np.ndarray:
+        """Concatenated residual stream r [B, H] (fp32) after the last step."""
+        outs = []
+        for i in range(self.cfg.n_micro):
+            for d in range(self.n_dev):
+                if ("r", i, d) in self.tensors:
+                    outs.append(self.tensors[("r", i, d)].cpu().numpy())
+                    break
+        return np.concatenate(outs, axis=0)
+
+    def cache(self, which: str, layer: int) -> np.ndarray:
+        """bf16 bits of one layer's KV pool, micro-batch sub-pools concatenated."""
+        torch = _torch()
+        outs = []
+        for i in range(self.cfg.n_micro):
+            for d in range(self.n_dev):
+                key = (f"{which}.{layer}", i, d)
+                if key in self.tensors:
+                    outs.append(self.tensors[key].view(torch.int16).cpu().numpy().view(np.uint16))
+                    break
+        return np.concatenate(outs, axis=0)

@@ -115,14 +115,19 @@ def normal_f32(g: np.random.Generator, shape, std: float = 1.0) -> np.ndarray:
     return (g.standard_normal(shape, dtype=np.float32) * np.float32(std)).astype(np.float32)
 
 
-def block_table(g: np.random.Generator, n_seq: int, pages_per_seq: int,
-                n_pages: Optional[int] = None) -> np.ndarray:
-    """Fragmented page pool: a seeded random permutation of page ids,
-    sequence b owns pages perm[b*pps:(b+1)*pps]."""
-    total = n_seq * pages_per_seq
-    n_pages = total if n_pages is None else n_pages
-    perm = g.permutation(n_pages)[:total].astype(np.int32)
-    return perm.reshape(n_seq, pages_per_seq)
+def block_table(g: np.random.Generator, n_seq: int, pages_per_seq: int, n_micro: int = 1) -> np.ndarray:
+    """Fragmented page pool: the pool is the concatenation of
+    one sub-pool per micro-batch (micro-batch i = sequences [i·m, (i+1)·m));
+    inside sub-pool i the page ids are a seeded random permutation, sequence b
+    owns perm_i[(b − i·m)·pps : (b − i·m + 1)·pps] + i·m·pps. Ids are global."""
+    assert n_seq % n_micro == 0
+    m = n_seq // n_micro
+    sub = m * pages_per_seq
+    out = np.empty((n_seq, pages_per_seq), dtype=np.int32)
+    for i in range(n_micro):
+        perm = g.permutation(sub).astype(np.int32) + i * sub
+        out[i * m:(i + 1) * m] = perm.reshape(m, pages_per_seq)
+    return out
 
 
 # --------------------------------------------------------------------------
@@ -180,7 +185,7 @@ def make_decoder_inputs(cfg: DecoderConfig, seed: Optional[int] = None) -> Decod
     layers = [make_layer_weights(g, cfg) for _ in range(cfg.n_layers)]
     x = normal_f32(g, (cfg.batch, cfg.hidden))
     pps = cfg.pages_per_seq
-    bt = block_table(g, cfg.batch, pps)
+    bt = block_table(g, cfg.batch, pps, cfg.n_micro)
     n_pages = cfg.batch * pps
     kshape = (n_pages, cfg.n_kv_heads, cfg.page, cfg.head_dim)
     kc = [normal_bf16(g, kshape) for _ in range(cfg.n_layers)]

@@ -242,7 +242,7 @@ def test_moe_equals_dense_masked_reference():
 
 # ------------------------------------------------------------------ layer
 def test_layer_zero_output_projections_pass_residual_through():
-    cfg = synth.TINY.with_(n_layers=1, batch=2, context=20)
+    cfg = synth.TINY.with_(n_layers=1, batch=2, context=20, n_micro=1)
     inp = synth.make_decoder_inputs(cfg)
     lw = inp.layers[0]
     lw.w_o = np.zeros_like(lw.w_o)
@@ -254,7 +254,7 @@ def test_layer_zero_output_projections_pass_residual_through():
 def test_layer_composition_matches_unpaged_dense_reference():
     """Whole layer vs an independent dense restatement: contiguous (unpaged)
     KV, natural (non-interleaved) weight order, materialised softmax."""
-    cfg = synth.TINY.with_(n_layers=1, batch=2, context=24, n_kv_heads=2)
+    cfg = synth.TINY.with_(n_layers=1, batch=2, context=24, n_kv_heads=2, n_micro=2)
     inp = synth.make_decoder_inputs(cfg)
     r_out, _, _ = L.decoder_step(inp, act="f64")
     H, Hq, Hkv, D, F = cfg.hidden, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn
