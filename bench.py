@@ -1,0 +1,317 @@
+#!/usr/bin/env python3
+"""bench.py — decode tokens/s of the kernel-disaggregation hot path on B200.
+
+Contract (task statement):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+A "step" = one full L-layer decode step (every §8(a) kernel) over one batch.
+N=1 workload: BASELINE.json configs[1], Llama-3-8B-shaped decode, B=64,
+C=4096, L=32, bf16, monolithic on one B200 (1-GPU reference point of the
+metric). N>1 (torchrun, one process per GPU): disaggregated replicas of the
+same workload per rank group — see DESIGN.md §Multi-GPU.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode_tokens_per_s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="llama3-8b")
+    p.add_argument("--layers", type=int, default=0, help="override L (default: the config's)")
+    p.add_argument("--batch", type=int, default=0)
+    p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--kernels", action="store_true", help="also time every op kind (extra passes)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained"), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.lines = []
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "50", "-i", str(gpu_index)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(2)
+        except Exception:
+            self.p.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU baseline (the oracle)
+def cpu_baseline(cfg, seconds_budget=20.0):
+    """Times the oracle as it stands (fp64 numpy) on a bounded sample of the
+    same workload: n_seq sequences through one full-width layer (all kernels),
+    extrapolated × L layers; tokens/s = n_seq / (L · t_layer)."""
+    import numpy as np
+    import synth
+    from oracle import layer as OL
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        cores = os.cpu_count()
+    n_seq = 2
+    sub = cfg.with_(n_layers=1, batch=n_seq, n_micro=1)
+    inp = synth.make_decoder_inputs(sub)
+    t0 = time.perf_counter()
+    OL.decoder_step(inp, act="bf16")
+    t = time.perf_counter() - t0
+    reps = 1
+    while time.perf_counter() - t0 < min(seconds_budget, 4 * t) and reps < 3:
+        OL.decoder_step(inp, act="bf16")
+        reps += 1
+    t = (time.perf_counter() - t0) / reps
+    value = n_seq / (cfg.n_layers * t)
+    return {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n_seq} sequences x 1 full-width layer of {cfg.name} (C={cfg.context}), fp64 numpy oracle, "
+                      f"{reps} reps, extrapolated x{cfg.n_layers} layers"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    base = cpu_baseline(cfg)
+    steps, warm = args.steps, args.warmup
+    # one "step" of the reference arm = the bounded oracle sample (time-capped)
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(cfg, 1, "oracle (CPU)"),
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, n_gpus, placement):
+    return {"workload": f"{cfg.name} decode B={cfg.batch} C={cfg.context} L={cfg.n_layers}",
+            "model_shape": {"hidden": cfg.hidden, "heads": cfg.n_heads, "kv_heads": cfg.n_kv_heads,
+                            "head_dim": cfg.head_dim, "ffn": cfg.ffn, "layers": cfg.n_layers},
+            "batch": cfg.batch, "context": cfg.context, "n_micro": cfg.n_micro, "placement": placement,
+            "n_gpus": n_gpus,
+            "l2": "inputs larger than L2 (per step: KV cache + weights >> 126 MB), no flush needed"}
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    if args.layers:
+        cfg = cfg.with_(n_layers=args.layers)
+    if args.batch:
+        cfg = cfg.with_(batch=args.batch)
+    cfg = cfg.with_(n_micro=1)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+    import torch
+    import numpy as np
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2604_10180_b200 import decoder as DEC, _kd as K
+
+    hbm_gbs, tc_tflops, tc_sus, peak_src = peaks()
+    dg = DEC.DecoderGraph(cfg)
+    assign = [0] * dg.g.num_kernels
+    rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed + rank, use_graph=not args.no_graph)
+    rt.rt.profile_op(K.KD_OP_ATTENTION)
+    rt.rt.prepare()
+    stream = rt.streams[0]
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        rt.step()
+    torch.cuda.synchronize()
+    n_launch = rt.rt.launch_count(0)
+
+    # ---- timed region (device resident inputs)
+    clocks = ClockSampler(local)
+    time.sleep(0.15)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        rt.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    attn_ms, attn_n = rt.rt.op_time()
+    rt.rt.check()
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    tokens_per_step = cfg.batch * world
+    value = tokens_per_step / (ms_step / 1e3)
+
+    # ---- roofline of the dominant kernel (decode attention)
+    m, C, Hkv, D, Hq = cfg.m, cfg.context, cfg.n_kv_heads, cfg.head_dim, cfg.n_heads
+    pps = cfg.pages_per_seq
+    attn_bytes = (m * pps * Hkv * 16 * D * 2 * 2      # K and V pools (every page of every sequence)
+                  + 2 * m * Hq * D * 2                 # q in, out
+                  + m * pps * 4 + m * 4)               # block table, seq_len
+    avg_attn_s = (attn_ms / max(attn_n, 1)) / 1e3
+    achieved = attn_bytes / avg_attn_s / 1e9
+    roof = {"kernel": "decode_attention_kernel<128>", "bound": "hbm", "achieved": round(achieved, 1),
+            "peak": hbm_gbs, "unit": "GB/s", "frac": round(achieved / hbm_gbs, 4), "traffic": None,
+            "bytes_per_launch": attn_bytes, "avg_launch_us": round(avg_attn_s * 1e6, 2),
+            "launches_timed": attn_n, "share_of_step": round(attn_ms / ms_step, 4) if ms_step else None,
+            "peak_source": peak_src,
+            "timing": "CUDA events (external event-record nodes) around each attention launch on its stream, "
+                      "last step of the timed region"}
+    tr_path = os.path.join(ROOT, "profiles", "attention_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            roof["traffic"] = json.load(open(tr_path)).get("bytes_per_launch")
+        except Exception:
+            pass
+
+    # ---- e2e: host buffers, H2D of the step inputs and D2H of the result inside the region
+    h2d = d2h = 0
+    e2e_value = None
+    try:
+        r_dev = rt.tensors[("r", 0, 0)]
+        bt_dev = rt.tensors[("bt", 0, 0)]
+        sl_dev = rt.tensors[("sl", 0, 0)]
+        r_host = torch.empty_like(r_dev, device="cpu").pin_memory()
+        r_host.copy_(r_dev)
+        bt_host = bt_dev.cpu().pin_memory()
+        sl_host = sl_dev.cpu().pin_memory()
+        out_host = torch.empty_like(r_host).pin_memory()
+        h2d = r_host.numel() * 4 + bt_host.numel() * 4 + sl_host.numel() * 4
+        d2h = out_host.numel() * 4
+        n_e2e = max(5, args.steps // 2)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            for _ in range(n_e2e):
+                r_dev.copy_(r_host, non_blocking=True)
+                bt_dev.copy_(bt_host, non_blocking=True)
+                sl_dev.copy_(sl_host, non_blocking=True)
+                rt.step()
+                out_host.copy_(r_dev, non_blocking=True)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e_value = tokens_per_step * n_e2e / el
+    except Exception as ex:  # report, do not hide
+        e2e_value = None
+        print(f"e2e failed: {ex}", file=sys.stderr)
+
+    kernels = None
+    if args.kernels:
+        kernels = {}
+        for op, nm in ((K.KD_OP_GEMM, "gemm"), (K.KD_OP_ADD_RMSNORM, "add_rmsnorm"),
+                       (K.KD_OP_ROPE_APPEND, "rope_append"), (K.KD_OP_SILU_MUL, "silu_mul")):
+            rt.rt.profile_op(op)
+            rt.rt.prepare()
+            for _ in range(3):
+                rt.step()
+            torch.cuda.synchronize()
+            t_ms, n = rt.rt.op_time()
+            kernels[nm] = {"ms_per_step": round(t_ms, 4), "launches": n}
+
+    line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded random-init weights, KV cache and residual inputs on device)",
+            "config": workload_config(cfg, world, "monolithic (all kernels on one B200)" if world == 1 else
+                                      "per-rank monolithic replica"),
+            "roofline": roof,
+            "e2e": {"value": round(e2e_value, 1) if e2e_value else None, "unit": "tokens/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": n_launch * args.steps,
+            "clocks": clk}
+    if kernels:
+        line["kernels"] = kernels
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

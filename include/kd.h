@@ -257,6 +257,15 @@ kd_status kd_runtime_launch_count(const kd_runtime* rt, uint32_t j, uint32_t* n)
 kd_status kd_runtime_profile_op(kd_runtime* rt, uint32_t op);
 kd_status kd_runtime_op_time(kd_runtime* rt, double* ms, uint64_t* launches);
 
+/* CUDA IPC helpers for the multi-process runtime (one process per GPU under
+ * torchrun): export the allocation that contains dev_ptr (handle: 64 opaque
+ * bytes written to handle64, offset: dev_ptr minus the allocation base), and
+ * map a peer's handle into this process (returns base + offset). The mapping
+ * is released with kd_ipc_close(mapped_ptr). Errors: KD_ERR_CUDA. */
+kd_status kd_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
+kd_status kd_ipc_open(const void* handle64, uint64_t offset, void** mapped_ptr);
+kd_status kd_ipc_close(void* mapped_ptr);
+
 /* ------------------------------------------------------------------ single ops
  * Direct entry points to the device kernels the runtime launches (for parity
  * tests and micro-benchmarks). Pointers are device pointers; layouts as in

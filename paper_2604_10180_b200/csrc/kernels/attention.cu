@@ -8,8 +8,8 @@
 //    split exactly once for all G heads (GQA reuse).
 //  * HND cache [page][Hkv][16][D]: one page's K (or V) slab for one kv head is
 //    16·D·2 contiguous bytes → one cp.async.bulk (TMA bulk copy) per slab into a
-//    6-stage shared-memory ring guarded by mbarriers; a single producer lane
-//    keeps ~48 KB per CTA in flight.
+//    8-stage shared-memory ring guarded by mbarriers (stage s always feeds
+//    warp s % 4); a single producer lane keeps up to 64 KB per CTA in flight.
 //  * 4 consumer warps own alternate pages. Sᵀ = Q·Kᵀ and O += P·V use
 //    mma.sync m16n8k16 (bf16 → fp32) with the G heads as MMA rows (padded
 //    to 16): Q is a register-resident A operand, P stays in registers between
@@ -29,7 +29,12 @@ namespace attn {
 
 constexpr int kWarps = 4;           // consumer warps
 constexpr int kThreads = (kWarps + 1) * 32;
-constexpr int kStages = 6;
+constexpr int kStages = 8;
+// Page j lives in stage j % kStages and is consumed by warp j % kWarps. With
+// kStages % kWarps == 0 every stage is always consumed by the SAME warp, in
+// round order, so no waiter can run two mbarrier phases ahead (parity waits
+// alias after two phases).
+static_assert(kStages % kWarps == 0, "each stage must belong to one consumer warp");
 constexpr int kPage = 16;
 constexpr int kMaxG = 8;
 constexpr int kMaxPagesPerSplit = 512;
@@ -351,8 +356,9 @@ kd_status attention_scratch_bytes(const kd_attr_attention& a, uint64_t* bytes) {
   if (s) return s;
   attn::Shape sh = attn::choose(a);
   const uint64_t units = (uint64_t)a.rows * a.n_kv_heads, G = a.n_heads / a.n_kv_heads;
+  if (units > kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "attention: too many (sequence, kv head) units");
   uint64_t n = 0;
-  if (sh.splits > 1) n = units * sh.splits * G * (a.head_dim + 1) * 4 + units * 4;
+  if (sh.splits > 1) n = kScratchCounterBytes + units * sh.splits * G * (a.head_dim + 1) * 4;
   *bytes = (n + 255) / 256 * 256;
   return KD_OK;
 }
@@ -373,9 +379,10 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
   P.sl = sl;
   P.out = (__nv_bfloat16*)out;
   const uint64_t units = (uint64_t)a.rows * a.n_kv_heads;
-  P.part_o = (float*)c.scratch;
+  if (units > kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "attention: too many (sequence, kv head) units");
+  P.counter = (unsigned*)c.scratch;
+  P.part_o = (float*)((uint8_t*)c.scratch + kScratchCounterBytes);
   P.part_lse = P.part_o + units * sh.splits * G * a.head_dim;
-  P.counter = (unsigned*)(P.part_lse + units * sh.splits * G);
   P.Hq = a.n_heads;
   P.Hkv = a.n_kv_heads;
   P.G = G;

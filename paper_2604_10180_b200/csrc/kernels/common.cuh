@@ -11,6 +11,11 @@ namespace kd {
 
 constexpr int kNumSMs = 148;
 constexpr int kMaxPeers = 4;
+// Kernel scratch layout shared by every kernel of a device (they run in
+// stream order): [0, kScratchCounterBytes) holds self-resetting u32 counters
+// (always zero between launches), partial results start after it.
+constexpr uint64_t kScratchCounterBytes = 64 * 1024;
+constexpr uint32_t kMaxCounters = kScratchCounterBytes / 4;
 
 // Fused peer-store epilogue (the chunked P2P handoff of SURVEY a13, fused into
 // the producer; replaces the paper's send kernels after k): every value

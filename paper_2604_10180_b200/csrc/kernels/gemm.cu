@@ -384,7 +384,8 @@ kd_status gemm_scratch_bytes(const kd_attr_gemm& a, uint64_t* bytes) {
   gemm::Geometry g;
   kd_status s = gemm::geometry(a, &g, kNumSMs);
   if (s) return s;
-  uint64_t n = (uint64_t)g.tiles * g.max_contrib * a.M * gemm::kBM * 4 + (uint64_t)g.tiles * 4;
+  if ((uint64_t)g.tiles > kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "gemm: too many output tiles");
+  uint64_t n = kScratchCounterBytes + (uint64_t)g.tiles * g.max_contrib * a.M * gemm::kBM * 4;
   *bytes = (n + 255) / 256 * 256;
   return KD_OK;
 }
@@ -416,8 +417,9 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   if (g.max_contrib > 1 && !c.scratch) return fail(KD_ERR_INVALID_ARG, "gemm: scratch required");
   gemm::Args A;
   A.Y = (__nv_bfloat16*)Y;
-  A.part = (float*)c.scratch;
-  A.counter = (unsigned*)((uint8_t*)c.scratch + (size_t)g.tiles * g.max_contrib * gp.a.M * gemm::kBM * 4);
+  if ((uint64_t)g.tiles > kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "gemm: too many output tiles");
+  A.counter = (unsigned*)c.scratch;
+  A.part = (float*)((uint8_t*)c.scratch + kScratchCounterBytes);
   A.M = gp.a.M;
   A.N = gp.a.N;
   A.K = gp.a.K;

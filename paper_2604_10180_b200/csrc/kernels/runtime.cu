@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <map>
 #include <set>
+#include <cstdlib>
 
 #include "launch.hpp"
 
@@ -105,7 +106,11 @@ kd_status check_attrs(const Kernel& k) {
   return KD_OK;
 }
 
-kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s) {
+inline cudaError_t record(cudaEvent_t e, cudaStream_t s, bool capturing) {
+  return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
+}
+
+kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool capturing) {
   uint8_t* ws = d.ws;
   const auto& L = rt->plan->layout[d.logical];
   unsigned* epoch = (unsigned*)(ws + L.ctrl_off);
@@ -117,7 +122,7 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s) {
   c.stream = s;
   if (rt->mode == KD_MODE_NO_TRANSFER) c.epi.n = 0;
   const bool prof = rt->profile_op && l.op == rt->profile_op;
-  if (prof) KD_CUDA_CHECK(cudaEventRecordWithFlags(l.ev0, s, cudaEventRecordExternal), "event record");
+  if (prof) KD_CUDA_CHECK(record(l.ev0, s, capturing), "event record");
   kd_status st = KD_OK;
   const Kernel& K = rt->plan->g->kernels[l.kernel];
   uint32_t sig = 0;
@@ -155,7 +160,13 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s) {
     }
   }
   if (st) return st;
-  if (prof) KD_CUDA_CHECK(cudaEventRecordWithFlags(l.ev1, s, cudaEventRecordExternal), "event record");
+  if (prof) KD_CUDA_CHECK(record(l.ev1, s, capturing), "event record");
+  if (!capturing && getenv("KD_DEBUG_SYNC")) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess)
+      return fail(KD_ERR_CUDA, std::string("kernel ") + std::to_string(l.kernel) + " (op " + std::to_string(l.op) +
+                                   ", micro " + std::to_string(l.micro) + ") failed: " + cudaGetErrorString(e));
+  }
   return KD_OK;
 }
 
@@ -430,7 +441,7 @@ kd_status kd_step(kd_runtime* rt, void* const* streams) {
     KD_CUDA_CHECK(cudaSetDevice(d.cuda), "cudaSetDevice");
     if (!rt->use_graph) {
       for (auto& l : d.launches) {
-        kd_status st = enqueue(rt, d, l, s);
+        kd_status st = enqueue(rt, d, l, s, false);
         if (st) return st;
       }
       continue;
@@ -443,7 +454,7 @@ kd_status kd_step(kd_runtime* rt, void* const* streams) {
       KD_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
       kd_status st = KD_OK;
       for (auto& l : d.launches) {
-        st = enqueue(rt, d, l, s);
+        st = enqueue(rt, d, l, s, true);
         if (st) break;
       }
       cudaGraph_t graph = nullptr;

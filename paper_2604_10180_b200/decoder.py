@@ -161,25 +161,31 @@ class DecoderRuntime:
     (parity runs); otherwise device-side seeded random values are used."""
 
     def __init__(self, dg: DecoderGraph, assign: Sequence[int], n_dev: int, dev_map: Sequence[int],
-                 machine: Optional[Machine] = None, inputs=None, seed: int = 0, use_graph: bool = True):
+                 machine: Optional[Machine] = None, inputs=None, seed: int = 0, use_graph: bool = True,
+                 local_devs: Optional[Sequence[int]] = None, dist=None):
+        """dev_map[logical] = cuda ordinal for every LOCAL logical device.
+        local_devs: logical devices driven by this process (default: all,
+        single-process / loopback). With `dist` (torch.distributed, one
+        process per GPU) the peers' workspaces are mapped through CUDA IPC."""
         torch = _torch()
         cfg = dg.cfg
         self.dg, self.cfg = dg, cfg
         self.machine = machine or b200_machine(n_dev)
         self.plan = Plan(dg.g, self.machine, list(assign), cfg.n_micro)
         self.n_dev = n_dev
-        self.dev_map = list(dev_map)
-        self.rt = Runtime(self.plan, list(range(n_dev)), self.dev_map)
+        self.local_devs = list(range(n_dev)) if local_devs is None else list(local_devs)
+        self.dev_map = {d: dev_map[j] if len(dev_map) == len(self.local_devs) else dev_map[d]
+                        for j, d in enumerate(self.local_devs)}
+        self.rt = Runtime(self.plan, self.local_devs, [self.dev_map[d] for d in self.local_devs])
         self.rt.set_graph(use_graph)
         self.tensors: Dict[tuple, "torch.Tensor"] = {}
-        self.ws = []
-        N, m = cfg.n_micro, cfg.m
-        pps = cfg.pages_per_seq
+        self.ws = {}
+        self._ipc = []
+        N = cfg.n_micro
         tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "i32": torch.int32}
         from synth import device_normal_
         for name, b in dg.buf.items():
-            flags = 0
-            for d in range(n_dev):
+            for d in self.local_devs:
                 if not self.plan.needs_binding(b, d):
                     continue
                 per_micro = name in ("r", "bt", "sl") or name.startswith(("kc.", "vc."))
@@ -188,14 +194,26 @@ class DecoderRuntime:
                     self._fill(t, name, i, inputs, seed, device_normal_)
                     self.tensors[(name, i, d)] = t
                     self.rt.bind(b, i, d, t.data_ptr())
-        for d in range(n_dev):
+        for d in self.local_devs:
             nbytes = self.plan.workspace_bytes(d)
             w = torch.zeros(nbytes + 256, dtype=torch.uint8, device=f"cuda:{self.dev_map[d]}")
             off = (-w.data_ptr()) % 256
-            self.ws.append(w)
+            self.ws[d] = (w, w.data_ptr() + off)
             self.rt.set_workspace(d, w.data_ptr() + off, nbytes)
+        if dist is not None and n_dev > 1:
+            from . import dist as kdist
+            kdist.check_same_plan(dist, self.plan)
+            assert len(self.local_devs) == 1, "one logical device per process"
+            me = self.local_devs[0]
+            torch.cuda.synchronize(self.dev_map[me])
+            peers = kdist.exchange_workspaces(dist, me, kdist.export_workspace(self.ws[me][1]))
+            for d, blob in sorted(peers.items()):
+                p = kdist.import_workspace(blob)
+                self._ipc.append(p)
+                self.rt.set_peer_workspace(d, p)
+            dist.barrier()
         self.rt.prepare()
-        self.streams = [torch.cuda.Stream(device=f"cuda:{self.dev_map[d]}") for d in range(n_dev)]
+        self.streams = [torch.cuda.Stream(device=f"cuda:{self.dev_map[d]}") for d in self.local_devs]
 
     # ------------------------------------------------------------------ inputs
     def _fill(self, t, name, i, inputs, seed, device_normal_):
@@ -251,14 +269,14 @@ class DecoderRuntime:
 
     def sync(self):
         torch = _torch()
-        for d in range(self.n_dev):
+        for d in self.local_devs:
             torch.cuda.synchronize(self.dev_map[d])
 
     def residual(self) -> np.ndarray:
         """Concatenated residual stream r [B, H] (fp32) after the last step."""
         outs = []
         for i in range(self.cfg.n_micro):
-            for d in range(self.n_dev):
+            for d in self.local_devs:
                 if ("r", i, d) in self.tensors:
                     outs.append(self.tensors[("r", i, d)].cpu().numpy())
                     break
@@ -269,7 +287,7 @@ class DecoderRuntime:
         torch = _torch()
         outs = []
         for i in range(self.cfg.n_micro):
-            for d in range(self.n_dev):
+            for d in self.local_devs:
                 key = (f"{which}.{layer}", i, d)
                 if key in self.tensors:
                     outs.append(self.tensors[key].view(torch.int16).cpu().numpy().view(np.uint16))

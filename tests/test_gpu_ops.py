@@ -153,6 +153,7 @@ ATTN = [
     (2, 64, 8, 128, 2048),  # 70B shape, G=8
     (5, 4, 2, 128, 1),      # single key
     (1, 8, 1, 64, 17),      # G=8 MQA, D=64, 2 pages
+    (64, 32, 8, 128, 4096), # full 8B bench launch (m=64): 4 splits x 64 pages, 8 ring rounds per CTA
 ]
 
 
