@@ -266,6 +266,12 @@ kd_status kd_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offse
 kd_status kd_ipc_open(const void* handle64, uint64_t offset, void** mapped_ptr);
 kd_status kd_ipc_close(void* mapped_ptr);
 
+/* Debug: when dev_buf is non-NULL, every subsequent GEMM launch writes 16
+ * %globaltimer stamps per CTA (entry, setup, first/last TMA, first full wait,
+ * last commit, per-segment epilogue start/end, fixup start/end, exit) to
+ * dev_buf[cta*32 + slot] (u64, >= 148*32 entries). NULL disables (default). */
+kd_status kd_debug_gemm_trace(void* dev_buf);
+
 /* ------------------------------------------------------------------ single ops
  * Direct entry points to the device kernels the runtime launches (for parity
  * tests and micro-benchmarks). Pointers are device pointers; layouts as in

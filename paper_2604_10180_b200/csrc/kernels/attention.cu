@@ -287,13 +287,13 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(Params P) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned prev = atomicAdd(&P.counter[unit], 1u);
+    fence_acq_rel_gpu();
+    unsigned prev = atom_add_acq_rel_gpu(&P.counter[unit], 1u);
     s_last = (prev == (unsigned)P.splits - 1);
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
+  fence_acq_rel_gpu();
   for (int e = threadIdx.x; e < G * D; e += blockDim.x) {
     const int h = e / D, d = e % D;
     float M = -INFINITY;
@@ -417,6 +417,12 @@ kd_status attention_init_attrs() {
   KD_CUDA_CHECK(cudaFuncSetAttribute(attn::decode_attention_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)attn::smem_bytes<64>()),
                 "attention smem attr");
+  // one carveout (max shared memory) for every kernel of the step: the SM never
+  // has to drain and re-split L1/shared memory between consecutive launches
+  KD_CUDA_CHECK(cudaFuncSetAttribute(attn::decode_attention_kernel<128>, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                "attention carveout");
+  KD_CUDA_CHECK(cudaFuncSetAttribute(attn::decode_attention_kernel<64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                "attention carveout");
   return KD_OK;
 }
 

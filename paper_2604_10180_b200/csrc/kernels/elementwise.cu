@@ -314,6 +314,14 @@ kd_status launch_wait(const WaitList& w, const unsigned* epoch, unsigned* err, c
   return KD_OK;
 }
 
+kd_status elementwise_init_attrs() {
+  const void* fns[] = {(const void*)add_rmsnorm_kernel, (const void*)residual_add_kernel, (const void*)silu_mul_kernel,
+                       (const void*)rope_append_kernel, (const void*)step_begin_kernel2, (const void*)wait_kernel};
+  for (const void* f : fns)
+    KD_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+  return KD_OK;
+}
+
 template <typename T>
 static kd_status attrs_of(const std::vector<uint8_t>& v, T* out) {
   if (v.size() != sizeof(T)) return fail(KD_ERR_INVALID_ARG, "op attrs have the wrong size for the op");

@@ -18,6 +18,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "launch.hpp"
@@ -40,7 +41,19 @@ struct Args {
   int M, N, K, mma_n, stages, kblocks, tiles, max_contrib;
   long long units;
   Epi epi;
+  unsigned long long* trace;  // debug: 32 %globaltimer stamps per CTA (nullable)
+  int dbg;                    // debug A/B knob (KD_GEMM_DBG): 1 skip owner Y stores, 2 skip owner fold
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define KD_TRACE(slot) \
+  do {                 \
+    if (A.trace) A.trace[blockIdx.x * 32 + (slot)] = gtimer(); \
+  } while (0)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned c) {
@@ -110,6 +123,31 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t saddr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
+  return v;
+}
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 // unit range of CTA c: [c·U/G, (c+1)·U/G); owner of unit u: ⌈(u+1)·G/U⌉ − 1
@@ -130,10 +168,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;        // [2]
   uint64_t* tempty = tfull + 2;                // [2]
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  int* s_flag = (int*)(tmem_slot + 1);
+  uint64_t* fixbar = tempty + 2;               // owner's partial bulk loads
+  uint32_t* tmem_slot = (uint32_t*)(fixbar + 1);
+  __nv_bfloat16* ystage = (__nv_bfloat16*)(fixbar + 2);  // 2 x [16][128] bf16 epilogue transpose
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) KD_TRACE(0);
   const long long U = A.units, G = gridDim.x, c = blockIdx.x;
   const long long u0 = unit_begin(c, U, G), u1 = unit_begin(c + 1, U, G);
   const int KB = A.kblocks;
@@ -148,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
+    mbar_init(fixbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
@@ -161,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) KD_TRACE(1);
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -176,7 +218,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(&full[s], tx);
         tma_load_2d(sa + (size_t)s * kStageA, &tmap_w, kb * kBK, t * kBM, &full[s], pw);
         tma_load_2d(sb + (size_t)s * stage_b, &tmap_x, kb * kBK, 0, &full[s], px);
+        if (i == 0) KD_TRACE(2);
       }
+      KD_TRACE(3);
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
@@ -197,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (; u < seg_end; ++u, ++i) {
           const int s = (int)(i % S);
           mbar_wait(&full[s], (unsigned)((i / S) & 1));
+          if (i == 0) KD_TRACE(4);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t a_addr = smem_u32(sa + (size_t)s * kStageA);
           const uint32_t b_addr = smem_u32(sb + (size_t)s * stage_b);
@@ -212,12 +257,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&tfull[a]);    // accumulator ready for the epilogue
         ++seg;
       }
+      KD_TRACE(5);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue (TMEM → HBM / peers)
+    // Split tiles (stream-K): every contributor c of tile t publishes its fp32
+    // partial [M][128] to slot (c - first contributor), release-increments
+    // arrive[t], waits until all n_contrib partials are published, then folds
+    // ITS 1/n slice of the tile (fixed contributor order → bitwise
+    // deterministic) and stores it. depart[t] lets the last leaver reset both
+    // counters for the next launch. Contributors only wait for partials that
+    // are published before anyone waits, so this cannot deadlock.
     const int q = warp - 4;                 // TMEM lane quarter
     const int row_in_tile = q * 32 + lane;  // output feature within the tile
     const int ep_tid = threadIdx.x - 128;
+    const size_t part_elems = (size_t)A.M * kBM;
     int seg = 0;
     long long u = u0;
     while (u < u1) {
@@ -227,72 +281,156 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool whole = (u == t_begin && seg_end == t_end);
       const int a = seg & 1;
       mbar_wait(&tfull[a], (unsigned)((seg >> 1) & 1));
+      if (ep_tid == 0 && seg < 3) KD_TRACE(6 + 2 * seg);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const int n = t * kBM + row_in_tile;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * A.mma_n);
-      const long long first_owner = unit_owner(t_begin, U, G);
-      const int my_idx = (int)(c - first_owner);
-      const int n_contrib = (int)(unit_owner(t_end - 1, U, G) - first_owner + 1);
-      float* my_part = A.part + ((size_t)t * A.max_contrib + my_idx) * (size_t)A.M * kBM;
-      // columns in chunks of 16 (tokens)
-      for (int j0 = 0; j0 < A.M; j0 += kChunk) {
-        float v[kChunk];
-        tmem_ld16(tbase + j0, v);
-        const int jn = min(kChunk, A.M - j0);
-        if (whole) {
-          if (n < A.N)
-            for (int j = 0; j < jn; ++j) {
-              __nv_bfloat16 o = __float2bfloat16_rn(v[j]);
-              A.Y[(size_t)(j0 + j) * A.N + n] = o;
-              for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[(size_t)(j0 + j) * A.N + n] = o;
-            }
-        } else {
-          for (int j = 0; j < jn; ++j) my_part[(size_t)(j0 + j) * kBM + row_in_tile] = v[j];
-        }
-      }
-      // accumulator drained: hand it back to the MMA warp
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[a]);
       if (!whole) {
-        named_bar(1, 128);
-        if (ep_tid == 0) {
-          __threadfence();
-          unsigned prev = atomicAdd(&A.counter[t], 1u);
-          *s_flag = (prev == (unsigned)n_contrib - 1);
+        const long long first = unit_owner(t_begin, U, G);
+        const long long lastc = unit_owner(t_end - 1, U, G);
+        const int n_contrib = (int)(lastc - first + 1);
+        const int my_idx = (int)(c - first);
+        // participants fold: contributors for which this tile is their LAST
+        // segment. Only the last contributor can have more work after this
+        // tile (a "tail" part at the start of its range); it publishes only.
+        const bool tail_exists = unit_begin(lastc + 1, U, G) > t_end;
+        const int n_part = n_contrib - (tail_exists ? 1 : 0);
+        const bool participant = (seg_end == u1);
+        const float* parts = A.part + (size_t)t * A.max_contrib * part_elems;
+        float* my_part = A.part + ((size_t)t * A.max_contrib + my_idx) * part_elems;
+        for (int j0 = 0; j0 < A.M; j0 += kChunk) {
+          float v[kChunk];
+          tmem_ld16(tbase + j0, v);
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j)
+            if (j0 + j < A.M) my_part[(size_t)(j0 + j) * kBM + row_in_tile] = v[j];
         }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[a]);
         named_bar(1, 128);
-        if (*s_flag) {
-          __threadfence();
-          if (n < A.N)
-            for (int j = 0; j < A.M; ++j) {
-              float acc = 0.f;
-              for (int ci = 0; ci < n_contrib; ++ci) {
-                const float* pp = A.part + ((size_t)t * A.max_contrib + ci) * (size_t)A.M * kBM;
-                float x = __ldcg(&pp[(size_t)j * kBM + row_in_tile]);
-                acc = (ci == 0) ? x : acc + x;
-              }
-              __nv_bfloat16 o = __float2bfloat16_rn(acc);
-              A.Y[(size_t)j * A.N + n] = o;
-              for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[(size_t)j * A.N + n] = o;
-            }
-          named_bar(1, 128);
-          if (ep_tid == 0) {
-            A.counter[t] = 0u;
-            if (A.epi.n) {
-              fence_acq_rel_sys();
-              for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
+        unsigned* arrive = A.counter + 2 * t;
+        unsigned* depart = arrive + 1;
+        if (ep_tid == 0) {
+          KD_TRACE(18);
+          fence_acq_rel_gpu();
+          atom_add_acq_rel_gpu(arrive, 1u);
+          if (participant) {
+            long long spins = 0;
+            while (ld_acquire_gpu(arrive) < (unsigned)n_contrib)
+              if (++spins > 64) __nanosleep(32);
+            KD_TRACE(16);
+            if (atom_add_acq_rel_gpu(depart, 1u) == (unsigned)n_part - 1) {
+              *arrive = 0u;  // every participant has left the wait: reset for the next launch
+              *depart = 0u;
             }
           }
         }
         named_bar(1, 128);
-      } else if (A.epi.n) {
+        // fold my slice: float4 elements [e0, e1) of the [M][128] tile
+        const int n4 = participant ? (int)(part_elems / 4) : 0;
+        const int e0 = (int)((long long)n4 * my_idx / n_part), e1 = (int)((long long)n4 * (my_idx + 1) / n_part);
+        // 4 elements per thread per round: all (element, contributor) loads of a
+        // round are in flight together (memory-level parallelism for the L2 reads)
+        constexpr int EB = 4;
+        for (int eb = e0 + ep_tid; eb < e1; eb += 128 * EB) {
+          float4 acc[EB];
+          for (int c0 = 0; c0 < n_contrib; c0 += 8) {
+            const int cn = min(8, n_contrib - c0);
+            float4 xs[EB][8];
+#pragma unroll
+            for (int k = 0; k < EB; ++k)
+#pragma unroll
+              for (int ci = 0; ci < 8; ++ci) {
+                const int e = eb + k * 128;
+                if (ci < cn && e < e1)
+                  xs[k][ci] = __ldcg(reinterpret_cast<const float4*>(parts + (size_t)(c0 + ci) * part_elems) + e);
+              }
+#pragma unroll
+            for (int k = 0; k < EB; ++k)
+#pragma unroll
+              for (int ci = 0; ci < 8; ++ci)
+                if (ci < cn) {
+                  if (c0 + ci == 0) {
+                    acc[k] = xs[k][ci];
+                  } else {
+                    acc[k].x += xs[k][ci].x;
+                    acc[k].y += xs[k][ci].y;
+                    acc[k].z += xs[k][ci].z;
+                    acc[k].w += xs[k][ci].w;
+                  }
+                }
+          }
+#pragma unroll
+          for (int k = 0; k < EB; ++k) {
+            const int e = eb + k * 128;
+            if (e >= e1) break;
+            const int j = (e * 4) / kBM, r = (e * 4) % kBM;
+            const int nn = t * kBM + r;
+            if (nn < A.N) {
+              uint2 o;
+              o.x = pack_bf16(acc[k].x, acc[k].y);
+              o.y = pack_bf16(acc[k].z, acc[k].w);
+              const size_t yo = (size_t)j * A.N + nn;
+              if (nn + 4 <= A.N && (A.N & 3) == 0) {
+                *reinterpret_cast<uint2*>(A.Y + yo) = o;
+                for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+              } else {
+                const float vv[4] = {acc[k].x, acc[k].y, acc[k].z, acc[k].w};
+                for (int x = 0; x < 4 && nn + x < A.N; ++x) {
+                  A.Y[yo + x] = __float2bfloat16_rn(vv[x]);
+                  for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = __float2bfloat16_rn(vv[x]);
+                }
+              }
+            }
+          }
+        }
+        if (ep_tid == 0) KD_TRACE(13);
+      } else {
+        // ---- whole tile: TMEM → bf16 → smem transpose → 16-byte stores
+        for (int j0 = 0; j0 < A.M; j0 += kChunk) {
+          float v[kChunk];
+          tmem_ld16(tbase + j0, v);
+          __nv_bfloat16* st = ystage + (size_t)((j0 / kChunk) & 1) * kChunk * kBM;
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j) st[j * kBM + row_in_tile] = __float2bfloat16_rn(v[j]);
+          named_bar(2, 128);
+          const int jn = min(kChunk, A.M - j0);
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int e = ep_tid + r * 128;  // 256 vectors of 8 bf16 per chunk
+            const int j = e >> 4, col = (e & 15) * 8;
+            const int nn = t * kBM + col;
+            if (j < jn && nn < A.N) {
+              const uint4 val = *reinterpret_cast<const uint4*>(st + j * kBM + col);
+              const size_t yo = (size_t)(j0 + j) * A.N + nn;
+              if (nn + 8 <= A.N && (A.N & 7) == 0) {
+                *reinterpret_cast<uint4*>(A.Y + yo) = val;
+                for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint4*>((__nv_bfloat16*)A.epi.dst[p] + yo) = val;
+              } else {
+                const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(&val);
+                for (int x = 0; x < 8 && nn + x < A.N; ++x) {
+                  A.Y[yo + x] = sv[x];
+                  for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = sv[x];
+                }
+              }
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[a]);
+      }
+      // publish this segment's share of the output to consumer devices
+      // (whole tiles and fold participants; a tail contributor stored nothing)
+      const bool stored = whole || seg_end == u1;
+      if (A.epi.n && stored) {
         named_bar(1, 128);
         if (ep_tid == 0) {
           fence_acq_rel_sys();
           for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
         }
       }
+      if (ep_tid == 0 && seg < 3) KD_TRACE(7 + 2 * seg);
       u = seg_end;
       ++seg;
     }
@@ -303,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
   }
+  if (threadIdx.x == 0) KD_TRACE(15);
 }
 
 // ------------------------------------------------------------------ host side
@@ -359,7 +498,7 @@ static kd_status geometry(const kd_attr_gemm& a, Geometry* g, int sms) {
   if (a.K % 8) return fail(KD_ERR_UNSUPPORTED, "gemm: K must be a multiple of 8 (16-byte TMA rows)");
   g->mma_n = (int)((a.M + 15) / 16 * 16);
   const int stage_bytes = kStageA + g->mma_n * kBK * 2;
-  g->stages = std::min(kMaxStages, kSmemBudget / stage_bytes);
+  g->stages = std::min(kMaxStages, (kSmemBudget - 2 * kChunk * kBM * 2) / stage_bytes);
   g->kblocks = (int)((a.K + kBK - 1) / kBK);
   g->tiles = (int)((a.N + kBM - 1) / kBM);
   g->units = (long long)g->tiles * g->kblocks;
@@ -375,7 +514,7 @@ static kd_status geometry(const kd_attr_gemm& a, Geometry* g, int sms) {
 }
 
 static size_t smem_bytes(const Geometry& g) {
-  return 1024 + (size_t)g.stages * (kStageA + g.mma_n * kBK * 2) + (2 * kMaxStages + 4) * 8 + 16;
+  return 1024 + (size_t)g.stages * (kStageA + g.mma_n * kBK * 2) + (2 * kMaxStages + 6) * 8 + 2 * kChunk * kBM * 2 + 16;
 }
 
 }  // namespace gemm
@@ -384,7 +523,7 @@ kd_status gemm_scratch_bytes(const kd_attr_gemm& a, uint64_t* bytes) {
   gemm::Geometry g;
   kd_status s = gemm::geometry(a, &g, kNumSMs);
   if (s) return s;
-  if ((uint64_t)g.tiles > kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "gemm: too many output tiles");
+  if (2ull * g.tiles > kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "gemm: too many output tiles");
   uint64_t n = kScratchCounterBytes + (uint64_t)g.tiles * g.max_contrib * a.M * gemm::kBM * 4;
   *bytes = (n + 255) / 256 * 256;
   return KD_OK;
@@ -409,6 +548,8 @@ kd_status gemm_prepare(const kd_attr_gemm& a, const void* X, const void* W, Gemm
   return KD_OK;
 }
 
+static unsigned long long* g_gemm_trace = nullptr;
+
 kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t* signals) {
   gemm::Geometry g;
   kd_status s = gemm::geometry(gp.a, &g, kNumSMs);
@@ -417,7 +558,7 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   if (g.max_contrib > 1 && !c.scratch) return fail(KD_ERR_INVALID_ARG, "gemm: scratch required");
   gemm::Args A;
   A.Y = (__nv_bfloat16*)Y;
-  if ((uint64_t)g.tiles > kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "gemm: too many output tiles");
+  if (2ull * g.tiles > kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "gemm: too many output tiles");
   A.counter = (unsigned*)c.scratch;
   A.part = (float*)((uint8_t*)c.scratch + kScratchCounterBytes);
   A.M = gp.a.M;
@@ -430,30 +571,58 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   A.max_contrib = g.max_contrib;
   A.units = g.units;
   A.epi = c.epi;
+  A.trace = g_gemm_trace;
+  {
+    static int dbg = -1;
+    if (dbg < 0) dbg = getenv("KD_GEMM_DBG") ? atoi(getenv("KD_GEMM_DBG")) : 0;
+    A.dbg = dbg;
+  }
   size_t sm = gemm::smem_bytes(g);
   kd_status ks = kernels_init();
   if (ks) return ks;
   gemm::gemm_kernel<<<g.grid, gemm::kThreads, sm, c.stream>>>(gp.tmap_w, gp.tmap_x, A);
   KD_CUDA_CHECK(cudaGetLastError(), "gemm launch");
-  if (signals) *signals = (uint32_t)g.tiles;
+  if (signals) return gemm_signals(gp.a, signals);
   return KD_OK;
 }
+
+}  // namespace kd
+
+extern "C" kd_status kd_debug_gemm_trace(void* dev_buf) {  // 32 u64 stamps per CTA
+  kd::g_gemm_trace = (unsigned long long*)dev_buf;
+  return KD_OK;
+}
+
+namespace kd {
 
 kd_status gemm_signals(const kd_attr_gemm& a, uint32_t* s) {
   gemm::Geometry g;
   kd_status st = gemm::geometry(a, &g, kNumSMs);
   if (st) return st;
-  *s = (uint32_t)g.tiles;  // one finisher per output tile
+  // one flag increment per (tile, contributing CTA) segment: whole tiles count
+  // once, a split tile once per contributor (each stores its slice)
+  uint64_t n = 0;
+  for (int t = 0; t < g.tiles; ++t) {
+    const long long tb = (long long)t * g.kblocks, te = tb + g.kblocks;
+    long long f = gemm::unit_owner(tb, g.units, g.grid);
+    long long l = gemm::unit_owner(te - 1, g.units, g.grid);
+    const bool tail = gemm::unit_begin(l + 1, g.units, g.grid) > te;
+    n += (uint64_t)(l - f + 1) - (l > f && tail ? 1 : 0);
+  }
+  *s = (uint32_t)n;
   return KD_OK;
 }
 
 kd_status gemm_init_attrs() {
   KD_CUDA_CHECK(cudaFuncSetAttribute(gemm::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
                 "gemm smem attr");
+  KD_CUDA_CHECK(cudaFuncSetAttribute(gemm::gemm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                "gemm carveout");
   return KD_OK;
 }
 
-kd_status attention_init_attrs();  // attention.cu
+kd_status attention_init_attrs();    // attention.cu
+kd_status elementwise_init_attrs();  // elementwise.cu
 
 kd_status kernels_init() {
   static std::mutex mu;
@@ -466,6 +635,8 @@ kd_status kernels_init() {
   kd_status s = gemm_init_attrs();
   if (s) return s;
   s = attention_init_attrs();
+  if (s) return s;
+  s = elementwise_init_attrs();
   if (s) return s;
   done.push_back(dev);
   return KD_OK;

@@ -1,0 +1,94 @@
+#!/usr/bin/env python3
+"""Per-kernel microbenchmark through the C ABI (CUDA events, warm L2 flushed by
+rotating through distinct weight copies larger than L2). Prints one JSON line
+per kernel: algorithmic bytes, avg µs, GB/s and fraction of measured HBM peak."""
+import argparse
+import json
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2604_10180_b200 import _kd as K, api  # noqa: E402
+
+
+def peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(p))["hbm_gbs"] if os.path.exists(p) else 6650.0
+
+
+def timeit(fn, iters=20, warm=3):
+    """Device time per launch: the launches are captured in a CUDA graph so the
+    host (ctypes, descriptor encoding) never starves the GPU."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(warm):
+            fn(0)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(iters):
+            fn(i)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        e0.record()
+        g.replay()
+        e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters * 1e3  # µs
+
+
+def gemm(M, N, Kd, copies):
+    a = K.kd_attr_gemm(M, N, Kd, K.KD_BF16)
+    X = torch.randn(M, Kd, device="cuda").to(torch.bfloat16)
+    Ws = [torch.randn(N, Kd, device="cuda").to(torch.bfloat16) * (1 / math.sqrt(Kd)) for _ in range(copies)]
+    Y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    scr = torch.zeros(api.op_scratch_bytes(K.KD_OP_GEMM, a), dtype=torch.uint8, device="cuda")
+    us = timeit(lambda i: api.gemm(a, X, Ws[i % copies], Y, scr))
+    b = N * Kd * 2 + M * Kd * 2 + M * N * 2
+    return us, b
+
+
+def attention(rows, Hq, Hkv, D, C):
+    pps = (C + 15) // 16
+    a = K.kd_attr_attention(rows, Hq, Hkv, D, 16, pps, K.KD_BF16, 0)
+    kc = torch.randn(rows * pps, Hkv, 16, D, device="cuda").to(torch.bfloat16)
+    vc = torch.randn(rows * pps, Hkv, 16, D, device="cuda").to(torch.bfloat16)
+    bt = torch.randperm(rows * pps, device="cuda").to(torch.int32).view(rows, pps)
+    sl = torch.full((rows,), C, dtype=torch.int32, device="cuda")
+    q = torch.randn(rows, Hq * D, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    scr = torch.zeros(max(256, api.op_scratch_bytes(K.KD_OP_ATTENTION, a)), dtype=torch.uint8, device="cuda")
+    us = timeit(lambda i: api.attention(a, q, kc, vc, bt, sl, out, scr))
+    b = rows * pps * Hkv * 16 * D * 2 * 2 + 2 * rows * Hq * D * 2 + rows * pps * 4 + rows * 4
+    return us, b
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--m", type=int, default=64)
+    p.add_argument("--only", default="")
+    args = p.parse_args()
+    pk = peak()
+    m = args.m
+    cases = [("gemm_qkv", lambda: gemm(m, 6144, 4096, 4)), ("gemm_o", lambda: gemm(m, 4096, 4096, 5)),
+             ("gemm_gu", lambda: gemm(m, 28672, 4096, 2)), ("gemm_down", lambda: gemm(m, 4096, 14336, 2)),
+             ("attention", lambda: attention(m, 32, 8, 128, 4096)),
+             ("gemm_overhead_1kb", lambda: gemm(m, 128 * 148, 64, 2))]
+    for name, fn in cases:
+        if args.only and args.only not in name:
+            continue
+        us, b = fn()
+        gbs = b / us / 1e3
+        print(json.dumps({"kernel": name, "m": m, "us": round(us, 2), "bytes": b, "GBps": round(gbs, 1),
+                          "frac": round(gbs / pk, 3)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
