@@ -266,6 +266,13 @@ kd_status kd_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offse
 kd_status kd_ipc_open(const void* handle64, uint64_t offset, void** mapped_ptr);
 kd_status kd_ipc_close(void* mapped_ptr);
 
+/* Programmatic dependent launch for every kernel of the path (default on):
+ * each kernel lets its successor launch early and waits for its predecessor
+ * with griddepcontrol.wait before touching dependent memory; the GEMM streams
+ * its first ring of weight tiles before that wait. Takes effect for launches
+ * (and graph captures) made after the call. */
+kd_status kd_set_pdl(int32_t enable);
+
 /* Debug: when dev_buf is non-NULL, every subsequent GEMM launch writes 16
  * %globaltimer stamps per CTA (entry, setup, first/last TMA, first full wait,
  * last commit, per-segment epilogue start/end, fixup start/end, exit) to

@@ -151,6 +151,7 @@ _PROTOS = {
     "kd_ipc_open": (kd_status, [P, u64, C.POINTER(P)]),
     "kd_ipc_close": (kd_status, [P]),
     "kd_debug_gemm_trace": (kd_status, [P]),
+    "kd_set_pdl": (kd_status, [i32]),
     "kd_op_scratch_bytes": (kd_status, [u32, P, PU64]),
     "kd_op_add_rmsnorm": (kd_status, [C.POINTER(kd_attr_add_rmsnorm), P, P, P, P, P]),
     "kd_op_gemm": (kd_status, [C.POINTER(kd_attr_gemm), P, P, P, P, P]),

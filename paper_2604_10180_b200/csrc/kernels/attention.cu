@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(Params P) {
   uint64_t* empty = full + kStages;
   __shared__ int s_last;
 
+  pdl_launch_dependents();
+  pdl_wait();
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int G = P.G, Hkv = P.Hkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -395,10 +397,13 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
   kd_status ks = kernels_init();
   if (ks) return ks;
   if (a.head_dim == 128)
-    attn::decode_attention_kernel<128><<<grid, attn::kThreads, attn::smem_bytes<128>(), c.stream>>>(P);
+    KD_CUDA_CHECK(kd_launch(attn::decode_attention_kernel<128>, grid, dim3(attn::kThreads), attn::smem_bytes<128>(),
+                            c.stream, P),
+                  "attention launch");
   else
-    attn::decode_attention_kernel<64><<<grid, attn::kThreads, attn::smem_bytes<64>(), c.stream>>>(P);
-  KD_CUDA_CHECK(cudaGetLastError(), "attention launch");
+    KD_CUDA_CHECK(kd_launch(attn::decode_attention_kernel<64>, grid, dim3(attn::kThreads), attn::smem_bytes<64>(),
+                            c.stream, P),
+                  "attention launch");
   if (signals) return attention_signals(a, signals);
   return KD_OK;
 }

@@ -60,6 +60,14 @@ __device__ __forceinline__ void epi_signal(const Epi& epi) {
   }
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every kernel lets its dependent grid launch early and waits for its
+// prerequisite grid before touching memory the prerequisite may write (or
+// read). Every CTA executes the wait, so no grid can complete before its
+// predecessor (keeps the dependency chain transitive). No-ops without PDL.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ bf16 helpers
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }

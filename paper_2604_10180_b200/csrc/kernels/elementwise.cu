@@ -6,10 +6,17 @@
 // plus the runtime's step-begin barrier and flag-wait kernels (a13/a15).
 // All are HBM- or launch-bound: 16-byte vector loads, fp32 math, one pass.
 #include <math.h>
+#include <cstdlib>
 
 #include "launch.hpp"
 
 namespace kd {
+
+static bool pdl_default() {
+  const char* e = getenv("KD_PDL");
+  return e ? atoi(e) != 0 : true;
+}
+bool g_pdl = pdl_default();
 
 kd_status set_cuda_error(cudaError_t e, const char* where) {
   return fail(KD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -25,8 +32,18 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __rest
                                                                   const __nv_bfloat16* __restrict__ gamma,
                                                                   __nv_bfloat16* __restrict__ h, int H, float eps,
                                                                   Epi epi) {
+  pdl_launch_dependents();
   const int row = blockIdx.x, tid = threadIdx.x;
   const int nch = H / 8;
+  // gamma is a weight (never written in a step): fetch it before the
+  // dependency wait so it is in registers when the reduction finishes
+  uint4 gm[kNormChunks];
+#pragma unroll
+  for (int c = 0; c < kNormChunks; ++c) {
+    int ch = tid + c * kNormThreads;
+    if (ch < nch) gm[c] = reinterpret_cast<const uint4*>(gamma)[ch];
+  }
+  pdl_wait();
   float v[kNormChunks][8];
   float ss = 0.f;
   float* rr = r + (size_t)row * H;
@@ -63,12 +80,12 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __rest
   for (int c = 0; c < kNormChunks; ++c) {
     int ch = tid + c * kNormThreads;
     if (ch < nch) {
-      uint4 gm = reinterpret_cast<const uint4*>(gamma)[ch];
+      const uint4 g = gm[c];
       uint4 o;
-      o.x = pack_bf16(v[c][0] * inv * bf16lo(gm.x), v[c][1] * inv * bf16hi(gm.x));
-      o.y = pack_bf16(v[c][2] * inv * bf16lo(gm.y), v[c][3] * inv * bf16hi(gm.y));
-      o.z = pack_bf16(v[c][4] * inv * bf16lo(gm.z), v[c][5] * inv * bf16hi(gm.z));
-      o.w = pack_bf16(v[c][6] * inv * bf16lo(gm.w), v[c][7] * inv * bf16hi(gm.w));
+      o.x = pack_bf16(v[c][0] * inv * bf16lo(g.x), v[c][1] * inv * bf16hi(g.x));
+      o.y = pack_bf16(v[c][2] * inv * bf16lo(g.y), v[c][3] * inv * bf16hi(g.y));
+      o.z = pack_bf16(v[c][4] * inv * bf16lo(g.z), v[c][5] * inv * bf16hi(g.z));
+      o.w = pack_bf16(v[c][6] * inv * bf16lo(g.w), v[c][7] * inv * bf16hi(g.w));
       size_t e = (size_t)row * nch + ch;
       reinterpret_cast<uint4*>(h)[e] = o;
       for (int p = 0; p < epi.n; ++p) reinterpret_cast<uint4*>(epi.dst[p])[e] = o;
@@ -83,10 +100,10 @@ kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const void*
   if (a.rows == 0 || a.hidden == 0 || a.hidden % 8 || a.hidden > 8 * kNormThreads * kNormChunks)
     return fail(KD_ERR_UNSUPPORTED, "add_rmsnorm: hidden must be a multiple of 8 and <= 8192");
   if (!r || !gamma || !h || (a.has_delta && !delta)) return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: NULL pointer");
-  add_rmsnorm_kernel<<<a.rows, kNormThreads, 0, c.stream>>>(
-      r, a.has_delta ? (const __nv_bfloat16*)delta : nullptr, (const __nv_bfloat16*)gamma, (__nv_bfloat16*)h,
-      (int)a.hidden, a.eps, c.epi);
-  KD_CUDA_CHECK(cudaGetLastError(), "add_rmsnorm launch");
+  KD_CUDA_CHECK(kd_launch(add_rmsnorm_kernel, dim3(a.rows), dim3(kNormThreads), 0, c.stream, r,
+                          a.has_delta ? (const __nv_bfloat16*)delta : nullptr, (const __nv_bfloat16*)gamma,
+                          (__nv_bfloat16*)h, (int)a.hidden, a.eps, c.epi),
+                "add_rmsnorm launch");
   if (signals) *signals = a.rows;
   return KD_OK;
 }
@@ -94,6 +111,8 @@ kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const void*
 // ------------------------------------------------------------------ C1.11
 __global__ void residual_add_kernel(float* __restrict__ r, const __nv_bfloat16* __restrict__ d, size_t n8,
                                     Epi epi) {
+  pdl_launch_dependents();
+  pdl_wait();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x) {
     float4 a = reinterpret_cast<float4*>(r)[2 * i];
     float4 b = reinterpret_cast<float4*>(r)[2 * i + 1];
@@ -122,8 +141,9 @@ kd_status launch_residual_add(const kd_attr_residual_add& a, float* r, const voi
   if (!r || !delta) return fail(KD_ERR_INVALID_ARG, "residual_add: NULL pointer");
   size_t n8 = n / 8;
   int grid = residual_grid(a);
-  residual_add_kernel<<<grid, 256, 0, c.stream>>>(r, (const __nv_bfloat16*)delta, n8, c.epi);
-  KD_CUDA_CHECK(cudaGetLastError(), "residual_add launch");
+  KD_CUDA_CHECK(kd_launch(residual_add_kernel, dim3(grid), dim3(256), 0, c.stream, r, (const __nv_bfloat16*)delta,
+                          n8, c.epi),
+                "residual_add launch");
   if (signals) *signals = grid;
   return KD_OK;
 }
@@ -133,6 +153,8 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloa
                                 int F, Epi epi) {
   // one thread = 8 consecutive outputs; block j of 64 outputs reads gate
   // columns [128j, 128j+64) and up columns [128j+64, 128j+128)
+  pdl_launch_dependents();
+  pdl_wait();
   const int per_row = F / 8;
   const size_t n = (size_t)rows * per_row;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
@@ -169,9 +191,9 @@ kd_status launch_silu_mul(const kd_attr_silu_mul& a, const void* gu, void* out, 
   if (a.rows == 0 || a.ffn == 0 || a.ffn % 64) return fail(KD_ERR_UNSUPPORTED, "silu_mul: ffn must be a multiple of 64");
   if (!gu || !out) return fail(KD_ERR_INVALID_ARG, "silu_mul: NULL pointer");
   int grid = silu_grid(a);
-  silu_mul_kernel<<<grid, 256, 0, c.stream>>>((const __nv_bfloat16*)gu, (__nv_bfloat16*)out, (int)a.rows,
-                                             (int)a.ffn, c.epi);
-  KD_CUDA_CHECK(cudaGetLastError(), "silu_mul launch");
+  KD_CUDA_CHECK(kd_launch(silu_mul_kernel, dim3(grid), dim3(256), 0, c.stream, (const __nv_bfloat16*)gu,
+                          (__nv_bfloat16*)out, (int)a.rows, (int)a.ffn, c.epi),
+                "silu_mul launch");
   if (signals) *signals = grid;
   return KD_OK;
 }
@@ -184,14 +206,22 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, const 
                                    __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int Hq, int Hkv,
                                    int D, int page, int pps, double theta, Epi epi) {
   extern __shared__ float cs[];  // [D/2] cos, [D/2] sin
+  pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.x, half = D / 2, G = Hq / Hkv;
   const int pos = sl[b] - 1;
+  // angle = pos·θ^(−2i/D) in fp64, reduced exactly enough to [−π, π] in fp64,
+  // then an fp32 sincos of the small reduced angle (≈ the fp64 value rounded
+  // to fp32, R12) — far cheaper than fp64 sincos of a 4K-radian argument
+  const double l2t = log2(theta);
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
-    double ang = (double)pos * pow(theta, -2.0 * (double)i / (double)D);
-    double s, c;
-    sincos(ang, &s, &c);
-    cs[i] = (float)c;
-    cs[half + i] = (float)s;
+    const double ang = (double)pos * exp2(-2.0 * (double)i / (double)D * l2t);
+    const double k = rint(ang * 0.15915494309189535);  // 1/(2π)
+    const double red = fma(-k, 6.283185307179586, fma(-k, 2.4492935982947064e-16, ang));
+    float sf, cf;
+    sincosf((float)red, &sf, &cf);
+    cs[i] = cf;
+    cs[half + i] = sf;
   }
   __syncthreads();
   const int32_t pg = bt[(size_t)b * pps + pos / page];
@@ -250,10 +280,10 @@ kd_status launch_rope_append(const kd_attr_rope_append& a, const void* qkv, cons
     return fail(KD_ERR_UNSUPPORTED, "rope_append: unsupported shape");
   if (!qkv || !bt || !sl || !q_out || !kc || !vc) return fail(KD_ERR_INVALID_ARG, "rope_append: NULL pointer");
   size_t smem = sizeof(float) * a.head_dim;
-  rope_append_kernel<<<a.rows, 256, smem, c.stream>>>(
-      (const __nv_bfloat16*)qkv, bt, sl, (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc,
-      (int)a.n_heads, (int)a.n_kv_heads, (int)a.head_dim, (int)a.page, (int)a.pages_per_seq, a.theta, c.epi);
-  KD_CUDA_CHECK(cudaGetLastError(), "rope_append launch");
+  KD_CUDA_CHECK(kd_launch(rope_append_kernel, dim3(a.rows), dim3(256), smem, c.stream, (const __nv_bfloat16*)qkv, bt,
+                          sl, (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (int)a.n_heads,
+                          (int)a.n_kv_heads, (int)a.head_dim, (int)a.page, (int)a.pages_per_seq, a.theta, c.epi),
+                "rope_append launch");
   if (signals) *signals = a.rows;
   return KD_OK;
 }
@@ -347,3 +377,8 @@ kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s
 }
 
 }  // namespace kd
+
+extern "C" kd_status kd_set_pdl(int32_t enable) {
+  kd::g_pdl = enable != 0;
+  return KD_OK;
+}

@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) KD_TRACE(0);
+  pdl_launch_dependents();
   const long long U = A.units, G = gridDim.x, c = blockIdx.x;
   const long long u0 = unit_begin(c, U, G), u1 = unit_begin(c + 1, U, G);
   const int KB = A.kblocks;
@@ -209,8 +210,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint64_t pw = policy_evict_first(), px = policy_evict_last();
       const unsigned tx = kStageA + stage_b;
-      long long i = 0;
-      for (long long u = u0; u < u1; ++u, ++i) {
+      // weights never depend on the previous kernel: fill the first ring of W
+      // tiles before the grid-dependency wait (overlaps the previous kernel's
+      // tail), then the activations of those stages, then steady state
+      const long long n_pre = std::min<long long>(S, u1 - u0);
+      for (long long i = 0; i < n_pre; ++i) {
+        const long long u = u0 + i;
+        const int t = (int)(u / KB), kb = (int)(u % KB);
+        mbar_expect_tx(&full[i], tx);
+        tma_load_2d(sa + (size_t)i * kStageA, &tmap_w, kb * kBK, t * kBM, &full[i], pw);
+        if (i == 0) KD_TRACE(2);
+      }
+      pdl_wait();
+      for (long long i = 0; i < n_pre; ++i) {
+        const long long u = u0 + i;
+        tma_load_2d(sb + (size_t)i * stage_b, &tmap_x, (int)(u % KB) * kBK, 0, &full[i], px);
+      }
+      long long i = n_pre;
+      for (long long u = u0 + n_pre; u < u1; ++u, ++i) {
         const int s = (int)(i % S);
         const long long r = i / S;
         if (r > 0) mbar_wait(&empty[s], (unsigned)((r - 1) & 1));
@@ -218,13 +235,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(&full[s], tx);
         tma_load_2d(sa + (size_t)s * kStageA, &tmap_w, kb * kBK, t * kBM, &full[s], pw);
         tma_load_2d(sb + (size_t)s * stage_b, &tmap_x, kb * kBK, 0, &full[s], px);
-        if (i == 0) KD_TRACE(2);
       }
       KD_TRACE(3);
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
+      pdl_wait();
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(A.mma_n >> 3) << 17) |
                              ((uint32_t)(kBM >> 4) << 24);
       long long i = 0;
@@ -272,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row_in_tile = q * 32 + lane;  // output feature within the tile
     const int ep_tid = threadIdx.x - 128;
     const size_t part_elems = (size_t)A.M * kBM;
+    pdl_wait();  // scratch and Y may still be in use by the previous kernel
     int seg = 0;
     long long u = u0;
     while (u < u1) {
@@ -580,8 +598,8 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   size_t sm = gemm::smem_bytes(g);
   kd_status ks = kernels_init();
   if (ks) return ks;
-  gemm::gemm_kernel<<<g.grid, gemm::kThreads, sm, c.stream>>>(gp.tmap_w, gp.tmap_x, A);
-  KD_CUDA_CHECK(cudaGetLastError(), "gemm launch");
+  KD_CUDA_CHECK(kd_launch(gemm::gemm_kernel, dim3(g.grid), dim3(gemm::kThreads), sm, c.stream, gp.tmap_w, gp.tmap_x, A),
+                "gemm launch");
   if (signals) return gemm_signals(gp.a, signals);
   return KD_OK;
 }

@@ -17,6 +17,26 @@ struct LaunchCtx {
 };
 
 kd_status set_cuda_error(cudaError_t e, const char* where);
+
+// PDL switch (kd_set_pdl); read at launch time
+extern bool g_pdl;
+
+// cudaLaunchKernelEx with programmatic stream serialization when enabled
+template <typename... KArgs, typename... Args>
+inline cudaError_t kd_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 #define KD_CUDA_CHECK(call, where)                     \
   do {                                                 \
     cudaError_t _e = (call);                           \

@@ -70,6 +70,32 @@ def attention(rows, Hq, Hkv, D, C):
     return us, b
 
 
+def small_ops(m):
+    H, F, Hq, Hkv, D, C = 4096, 14336, 32, 8, 128, 4096
+    pps = C // 16
+    out = []
+    r = torch.randn(m, H, device="cuda")
+    d = torch.randn(m, H, device="cuda").to(torch.bfloat16)
+    gm = torch.ones(H, device="cuda").to(torch.bfloat16)
+    h = torch.empty(m, H, device="cuda", dtype=torch.bfloat16)
+    a = K.kd_attr_add_rmsnorm(m, H, 1, K.KD_BF16, 1e-5, 0)
+    out.append(("add_rmsnorm", timeit(lambda i: api.add_rmsnorm(a, r, d, gm, h)), m * H * (4 * 2 + 2 * 2) + H * 2))
+    qkv = torch.randn(m, (Hq + 2 * Hkv) * D, device="cuda").to(torch.bfloat16)
+    kc = torch.randn(m * pps, Hkv, 16, D, device="cuda").to(torch.bfloat16)
+    vc = torch.randn(m * pps, Hkv, 16, D, device="cuda").to(torch.bfloat16)
+    bt = torch.randperm(m * pps, device="cuda").to(torch.int32).view(m, pps)
+    sl = torch.full((m,), C, dtype=torch.int32, device="cuda")
+    q = torch.empty(m, Hq * D, device="cuda", dtype=torch.bfloat16)
+    ra = K.kd_attr_rope_append(m, Hq, Hkv, D, 16, pps, K.KD_BF16, 0, 5e5)
+    out.append(("rope_append", timeit(lambda i: api.rope_append(ra, qkv, bt, sl, q, kc, vc)),
+                qkv.numel() * 2 + q.numel() * 2 + m * Hkv * D * 2 * 2))
+    gu = torch.randn(m, 2 * F, device="cuda").to(torch.bfloat16)
+    ao = torch.empty(m, F, device="cuda", dtype=torch.bfloat16)
+    sa = K.kd_attr_silu_mul(m, F, K.KD_BF16, 0)
+    out.append(("silu_mul", timeit(lambda i: api.silu_mul(sa, gu, ao)), m * F * 2 * 3))
+    return out
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--m", type=int, default=64)
@@ -81,6 +107,12 @@ def main():
              ("gemm_gu", lambda: gemm(m, 28672, 4096, 2)), ("gemm_down", lambda: gemm(m, 4096, 14336, 2)),
              ("attention", lambda: attention(m, 32, 8, 128, 4096)),
              ("gemm_overhead_1kb", lambda: gemm(m, 128 * 148, 64, 2))]
+    if not args.only or args.only == "small":
+        for name, us, b in small_ops(m):
+            print(json.dumps({"kernel": name, "m": m, "us": round(us, 2), "bytes": b,
+                              "GBps": round(b / us / 1e3, 1), "frac": round(b / us / 1e3 / pk, 3)}), flush=True)
+        if args.only == "small":
+            return
     for name, fn in cases:
         if args.only and args.only not in name:
             continue
