@@ -172,17 +172,43 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    # test hooks: exercise the N>1 code path on a 1-GPU box (all ranks on cuda:0,
+    # gloo process group); never set by the driver
+    if os.environ.get("KD_BENCH_ONE_GPU"):
+        local = 0
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("KD_BENCH_ONE_GPU"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     from paper_2604_10180_b200 import decoder as DEC, _kd as K
 
     hbm_gbs, tc_tflops, tc_sus, peak_src = peaks()
-    dg = DEC.DecoderGraph(cfg)
-    assign = [0] * dg.g.num_kernels
-    rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed + rank, use_graph=not args.no_graph)
+    if world == 1:
+        # 1 GPU: the monolithic reference point of the metric (all kernels on one B200)
+        dg = DEC.DecoderGraph(cfg)
+        assign = [0] * dg.g.num_kernels
+        rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed, use_graph=not args.no_graph)
+        placement = "monolithic (all kernels on one B200)"
+    else:
+        # N GPUs: N/2 independent disaggregated pairs (BASELINE config 2: memory-bound
+        # kernels on the even rank, GEMMs on the odd rank), each decoding its own batch
+        # of B sequences with 2 micro-batches; cut edges are streamed by the producers'
+        # fused peer stores into the partner's HBM (CUDA IPC over NVLink). No collective.
+        if world % 2:
+            raise SystemExit("bench.py: --gpus must be 1 or even (disaggregated pairs)")
+        pair, role = rank // 2, rank % 2
+        groups = [dist.new_group([2 * p, 2 * p + 1]) for p in range(world // 2)]
+        cfg = cfg.with_(n_micro=2)
+        dg = DEC.DecoderGraph(cfg)
+        assign = dg.role_assign(0, 1)
+        rt = DEC.DecoderRuntime(dg, assign, 2, [local], seed=cfg.seed + pair, use_graph=not args.no_graph,
+                                local_devs=[role], dist=dist, dist_group=groups[pair])
+        placement = (f"{world // 2} disaggregated pair(s): memory-role kernels (norms, RoPE+append, attention, "
+                     f"SiLU) on even ranks, GEMMs on odd ranks, N=2 micro-batches")
     stream = rt.streams[0]
 
     def barrier():
@@ -229,11 +255,11 @@ def main():
     rt.rt.profile_op(0)
     rt.rt.prepare()
     if dist is not None:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cpu" if os.environ.get("KD_BENCH_ONE_GPU") else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    tokens_per_step = cfg.batch * world
+    tokens_per_step = cfg.batch * (1 if world == 1 else world // 2)
     value = tokens_per_step / (ms_step / 1e3)
 
     # ---- roofline of the dominant kernel (decode attention)
@@ -243,7 +269,7 @@ def main():
                   + 2 * m * Hq * D * 2                 # q in, out
                   + m * pps * 4 + m * 4)               # block table, seq_len
     avg_attn_s = (attn_ms / max(attn_n, 1)) / 1e3
-    achieved = attn_bytes / avg_attn_s / 1e9
+    achieved = attn_bytes / avg_attn_s / 1e9 if attn_n else 0.0
     roof = {"kernel": "decode_attention_kernel<128>", "bound": "hbm", "achieved": round(achieved, 1),
             "peak": hbm_gbs, "unit": "GB/s", "frac": round(achieved / hbm_gbs, 4), "traffic": None,
             "bytes_per_launch": attn_bytes, "avg_launch_us": round(avg_attn_s * 1e6, 2),
@@ -254,8 +280,10 @@ def main():
                       "stream, averaged over K profiled steps run right after the timed region"}
     tr_path = os.path.join(ROOT, "profiles", "attention_traffic.json")
     if os.path.exists(tr_path):
-        try:
-            roof["traffic"] = json.load(open(tr_path)).get("bytes_per_launch")
+        try:  # ncu dram bytes of the same launch shape (profiles/), else null
+            tr = json.load(open(tr_path))
+            if tr.get("algorithmic_bytes_per_launch") == attn_bytes:
+                roof["traffic"] = tr.get("bytes_per_launch")
         except Exception:
             pass
 
@@ -263,9 +291,12 @@ def main():
     h2d = d2h = 0
     e2e_value = None
     try:
-        r_dev = rt.tensors[("r", 0, 0)]
-        bt_dev = rt.tensors[("bt", 0, 0)]
-        sl_dev = rt.tensors[("sl", 0, 0)]
+        me = rt.local_devs[0]
+        r_dev = rt.tensors.get(("r", 0, me))
+        if r_dev is None:  # GEMM-role rank: its inputs arrive from the partner
+            r_dev = torch.zeros(1, device="cuda")
+        bt_dev = rt.tensors.get(("bt", 0, me), torch.zeros(1, dtype=torch.int32, device="cuda"))
+        sl_dev = rt.tensors.get(("sl", 0, me), torch.zeros(1, dtype=torch.int32, device="cuda"))
         r_host = torch.empty_like(r_dev, device="cpu").pin_memory()
         r_host.copy_(r_dev)
         bt_host = bt_dev.cpu().pin_memory()
@@ -287,7 +318,7 @@ def main():
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         if dist is not None:
-            t = torch.tensor([el], device="cuda")
+            t = torch.tensor([el], device="cpu" if os.environ.get("KD_BENCH_ONE_GPU") else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         e2e_value = tokens_per_step * n_e2e / el
@@ -312,8 +343,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded random-init weights, KV cache and residual inputs on device)",
-            "config": workload_config(cfg, world, "monolithic (all kernels on one B200)" if world == 1 else
-                                      "per-rank monolithic replica"),
+            "config": workload_config(cfg, world, placement),
             "roofline": roof,
             "e2e": {"value": round(e2e_value, 1) if e2e_value else None, "unit": "tokens/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

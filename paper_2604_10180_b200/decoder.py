@@ -162,7 +162,7 @@ class DecoderRuntime:
 
     def __init__(self, dg: DecoderGraph, assign: Sequence[int], n_dev: int, dev_map: Sequence[int],
                  machine: Optional[Machine] = None, inputs=None, seed: int = 0, use_graph: bool = True,
-                 local_devs: Optional[Sequence[int]] = None, dist=None):
+                 local_devs: Optional[Sequence[int]] = None, dist=None, dist_group=None):
         """dev_map[logical] = cuda ordinal for every LOCAL logical device.
         local_devs: logical devices driven by this process (default: all,
         single-process / loopback). With `dist` (torch.distributed, one
@@ -202,16 +202,16 @@ class DecoderRuntime:
             self.rt.set_workspace(d, w.data_ptr() + off, nbytes)
         if dist is not None and n_dev > 1:
             from . import dist as kdist
-            kdist.check_same_plan(dist, self.plan)
+            kdist.check_same_plan(dist, self.plan, dist_group)
             assert len(self.local_devs) == 1, "one logical device per process"
             me = self.local_devs[0]
             torch.cuda.synchronize(self.dev_map[me])
-            peers = kdist.exchange_workspaces(dist, me, kdist.export_workspace(self.ws[me][1]))
+            peers = kdist.exchange_workspaces(dist, me, kdist.export_workspace(self.ws[me][1]), dist_group)
             for d, blob in sorted(peers.items()):
                 p = kdist.import_workspace(blob)
                 self._ipc.append(p)
                 self.rt.set_peer_workspace(d, p)
-            dist.barrier()
+            dist.barrier(group=dist_group)
         self.rt.prepare()
         self.streams = [torch.cuda.Stream(device=f"cuda:{self.dev_map[d]}") for d in self.local_devs]
 

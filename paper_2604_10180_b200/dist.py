@@ -29,15 +29,15 @@ def plan_digest(plan) -> str:
     return h.hexdigest()
 
 
-def all_gather_bytes(dist, payload: bytes) -> List[bytes]:
-    """all_gather of one small byte string per rank (gloo or nccl groups)."""
-    out: List = [None] * dist.get_world_size()
-    dist.all_gather_object(out, payload)
+def all_gather_bytes(dist, payload: bytes, group=None) -> List[bytes]:
+    """all_gather of one small byte string per rank of `group` (gloo or nccl)."""
+    out: List = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, payload, group=group)
     return out
 
 
-def check_same_plan(dist, plan):
-    digests = all_gather_bytes(dist, plan_digest(plan).encode())
+def check_same_plan(dist, plan, group=None):
+    digests = all_gather_bytes(dist, plan_digest(plan).encode(), group)
     if len(set(digests)) != 1:
         raise RuntimeError(f"ranks derived different plans: {digests}")
 
@@ -58,15 +58,15 @@ def import_workspace(blob: bytes) -> int:
     return p.value
 
 
-def exchange_workspaces(dist, my_dev: int, blob: bytes) -> Dict[int, bytes]:
-    """Every rank contributes (logical device, exported blob); returns the
-    peers' blobs keyed by logical device."""
-    got = all_gather_bytes(dist, struct.pack("<I", my_dev) + blob)
+def exchange_workspaces(dist, my_dev: int, blob: bytes, group=None) -> Dict[int, bytes]:
+    """Every rank of `group` contributes (logical device, exported blob);
+    returns the peers' blobs keyed by logical device."""
+    got = all_gather_bytes(dist, struct.pack("<I", my_dev) + blob, group)
     out = {}
     for g in got:
         (d,) = struct.unpack("<I", g[:4])
         if d != my_dev:
             out[d] = g[4:]
-    if len(out) != dist.get_world_size() - 1:
+    if len(out) != dist.get_world_size(group) - 1:
         raise RuntimeError("duplicate logical devices across ranks")
     return out
