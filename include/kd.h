@@ -88,7 +88,11 @@ enum {
   KD_OP_ROPE_APPEND = 3,   /* a5  reads [qkv, block_table, seq_len] writes [q, Kc, Vc] */
   KD_OP_ATTENTION = 4,     /* a6  reads [q, Kc, Vc, block_table, seq_len] writes [out] */
   KD_OP_SILU_MUL = 5,      /* a8  reads [gu] writes [a]                          */
-  KD_OP_RESIDUAL_ADD = 6   /* C1.11 reads [r, delta] writes [r]                  */
+  KD_OP_RESIDUAL_ADD = 6,  /* C1.11 reads [r, delta] writes [r]                  */
+  KD_OP_MOE_ROUTE = 7,     /* a11 reads [h, W_router] writes [route]            */
+  KD_OP_MOE_DISPATCH = 8,  /* a11 reads [h, route] writes [xg, meta]            */
+  KD_OP_GROUPED_GEMM = 9,  /* a11 reads [xg, W_experts, meta] writes [yg]       */
+  KD_OP_MOE_COMBINE = 10   /* a11 reads [yg, route, meta] writes [out]          */
 };
 
 /* element types of activations / KV */
@@ -108,6 +112,20 @@ typedef struct {
 } kd_attr_attention;
 typedef struct { uint32_t rows, ffn, dtype, pad_; } kd_attr_silu_mul;  /* gu [rows, 2F] 64-col gate/up blocks */
 typedef struct { uint32_t rows, hidden; } kd_attr_residual_add;       /* r fp32 [rows,H] += delta (act dtype) */
+/* MoE. route buffer: int32 idx[rows][top_k] then fp32
+ * w[rows][top_k]; meta buffer: int32 count[E], offset[E], slot_of[rows][top_k]
+ * (grouped row of each (row, choice)), row_of[rows*top_k]; grouped rows are
+ * expert-major, ascending row index inside an expert. */
+typedef struct { uint32_t rows, hidden, experts, top_k; } kd_attr_moe_route;    /* h bf16 [rows,H], W_r fp32 [E,H] */
+typedef struct { uint32_t rows, hidden, experts, top_k; } kd_attr_moe_dispatch; /* xg bf16 [rows*top_k, H] */
+typedef struct {
+  uint32_t rows_total;  /* rows of xg / yg (= rows * top_k) */
+  uint32_t N, K;        /* per-expert W [N, K]; W_experts [E, N, K] row-major */
+  uint32_t experts;
+  uint32_t rows_cap;    /* static bound on rows per expert (<= 256) */
+  uint32_t dtype;
+} kd_attr_grouped_gemm;                                                          /* yg bf16 [rows_total, N] */
+typedef struct { uint32_t rows, hidden, experts, top_k; } kd_attr_moe_combine;  /* out bf16 [rows, H] */
 
 typedef struct {
   uint32_t op;              /* KD_OP_* */
@@ -303,6 +321,24 @@ kd_status kd_op_attention(const kd_attr_attention* a, const void* q, const void*
 kd_status kd_op_silu_mul(const kd_attr_silu_mul* a, const void* gu, void* out, void* stream);
 /* C1.11: r += delta */
 kd_status kd_op_residual_add(const kd_attr_residual_add* a, float* r, const void* delta, void* stream);
+/* a11 router: logits = h·W_rᵀ in fp32 (fixed-order warp reduction), top_k by
+ * logit (ties → lower expert index), weights = softmax over the selected. */
+kd_status kd_op_moe_route(const kd_attr_moe_route* a, const void* h, const float* w_router, void* route, void* stream);
+/* a11 dispatch: slot map (meta) + gather of h rows into expert-major xg. */
+kd_status kd_op_moe_dispatch(const kd_attr_moe_dispatch* a, const void* h, const void* route, void* xg, void* meta,
+                             void* stream);
+/* Bytes of the dispatch meta block (256-byte aligned). In a kernel graph the
+ * dispatch op writes ONE buffer [meta | xg] (its primary output, so both cross
+ * devices together); xg starts at this offset. */
+kd_status kd_moe_meta_bytes(uint32_t rows, uint32_t experts, uint32_t top_k, uint64_t* bytes);
+/* a11 grouped GEMM: for every expert e, yg[off_e + j] = xg[off_e + j]·W_eᵀ for
+ * j < count_e (off/count from meta, read on device). tcgen05 stream-K over all
+ * experts' tiles in one launch. */
+kd_status kd_op_grouped_gemm(const kd_attr_grouped_gemm* a, const void* xg, const void* w_experts, const void* meta,
+                             void* yg, void* scratch, void* stream);
+/* a11 combine: out[b] = Σ_j w[b][j]·yg[slot_of[b][j]], ascending expert order. */
+kd_status kd_op_moe_combine(const kd_attr_moe_combine* a, const void* yg, const void* route, const void* meta,
+                            void* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -370,7 +370,11 @@ kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s
     case KD_OP_SILU_MUL: { kd_attr_silu_mul a; if ((st = attrs_of(attrs, &a))) return st; *signals = silu_grid(a); return KD_OK; }
     case KD_OP_RESIDUAL_ADD: { kd_attr_residual_add a; if ((st = attrs_of(attrs, &a))) return st; *signals = residual_grid(a); return KD_OK; }
     case KD_OP_ATTENTION: { kd_attr_attention a; if ((st = attrs_of(attrs, &a))) return st; return attention_signals(a, signals); }
-    case KD_OP_GEMM: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(a, signals); }
+    case KD_OP_GEMM: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
+    case KD_OP_GROUPED_GEMM: { kd_attr_grouped_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
+    case KD_OP_MOE_ROUTE:
+    case KD_OP_MOE_DISPATCH:
+    case KD_OP_MOE_COMBINE: return moe_signals(op, attrs, signals);
   }
   *signals = 0;
   return KD_OK;

@@ -42,6 +42,10 @@ struct Args {
   long long units;
   Epi epi;
   unsigned long long* trace;  // debug: 32 %globaltimer stamps per CTA (nullable)
+  // grouped (MoE expert) mode: groups > 0; tile t → group t / tpg, n-tile t % tpg;
+  // meta = int32 count[groups], offset[groups] (rows of X/Y), read on device
+  int groups, tpg;
+  const int* meta;
   int dbg;                    // debug A/B knob (KD_GEMM_DBG): 1 skip owner Y stores, 2 skip owner fold
 };
 
@@ -214,17 +218,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       // tiles before the grid-dependency wait (overlaps the previous kernel's
       // tail), then the activations of those stages, then steady state
       const long long n_pre = std::min<long long>(S, u1 - u0);
+      auto w_row = [&](int t) { return A.groups ? (t / A.tpg) * A.N + (t % A.tpg) * kBM : t * kBM; };
       for (long long i = 0; i < n_pre; ++i) {
         const long long u = u0 + i;
         const int t = (int)(u / KB), kb = (int)(u % KB);
         mbar_expect_tx(&full[i], tx);
-        tma_load_2d(sa + (size_t)i * kStageA, &tmap_w, kb * kBK, t * kBM, &full[i], pw);
+        tma_load_2d(sa + (size_t)i * kStageA, &tmap_w, kb * kBK, w_row(t), &full[i], pw);
         if (i == 0) KD_TRACE(2);
       }
       pdl_wait();
+      auto x_row = [&](int t) { return A.groups ? __ldg(A.meta + A.groups + t / A.tpg) : 0; };
       for (long long i = 0; i < n_pre; ++i) {
         const long long u = u0 + i;
-        tma_load_2d(sb + (size_t)i * stage_b, &tmap_x, (int)(u % KB) * kBK, 0, &full[i], px);
+        tma_load_2d(sb + (size_t)i * stage_b, &tmap_x, (int)(u % KB) * kBK, x_row((int)(u / KB)), &full[i], px);
       }
       long long i = n_pre;
       for (long long u = u0 + n_pre; u < u1; ++u, ++i) {
@@ -233,8 +239,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (r > 0) mbar_wait(&empty[s], (unsigned)((r - 1) & 1));
         const int t = (int)(u / KB), kb = (int)(u % KB);
         mbar_expect_tx(&full[s], tx);
-        tma_load_2d(sa + (size_t)s * kStageA, &tmap_w, kb * kBK, t * kBM, &full[s], pw);
-        tma_load_2d(sb + (size_t)s * stage_b, &tmap_x, kb * kBK, 0, &full[s], px);
+        tma_load_2d(sa + (size_t)s * kStageA, &tmap_w, kb * kBK, w_row(t), &full[s], pw);
+        tma_load_2d(sb + (size_t)s * stage_b, &tmap_x, kb * kBK, x_row(t), &full[s], px);
       }
       KD_TRACE(3);
     }
@@ -302,6 +308,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ep_tid == 0 && seg < 3) KD_TRACE(6 + 2 * seg);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * A.mma_n);
+      // output coordinates of tile t: column base nb0, row base y0, valid rows mv
+      const int grp = A.groups ? t / A.tpg : 0;
+      const int nb0 = (A.groups ? t % A.tpg : t) * kBM;
+      const int y0 = A.groups ? __ldg(A.meta + A.groups + grp) : 0;
+      const int mv = A.groups ? min(__ldg(A.meta + grp), A.M) : A.M;
       if (!whole) {
         const long long first = unit_owner(t_begin, U, G);
         const long long lastc = unit_owner(t_end - 1, U, G);
@@ -383,12 +394,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int e = eb + k * 128;
             if (e >= e1) break;
             const int j = (e * 4) / kBM, r = (e * 4) % kBM;
-            const int nn = t * kBM + r;
-            if (nn < A.N) {
+            const int nn = nb0 + r;
+            if (nn < A.N && j < mv) {
               uint2 o;
               o.x = pack_bf16(acc[k].x, acc[k].y);
               o.y = pack_bf16(acc[k].z, acc[k].w);
-              const size_t yo = (size_t)j * A.N + nn;
+              const size_t yo = (size_t)(y0 + j) * A.N + nn;
               if (nn + 4 <= A.N && (A.N & 3) == 0) {
                 *reinterpret_cast<uint2*>(A.Y + yo) = o;
                 for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
@@ -412,15 +423,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < kChunk; ++j) st[j * kBM + row_in_tile] = __float2bfloat16_rn(v[j]);
           named_bar(2, 128);
-          const int jn = min(kChunk, A.M - j0);
+          const int jn = min(kChunk, mv - j0);
 #pragma unroll
           for (int r = 0; r < 2; ++r) {
             const int e = ep_tid + r * 128;  // 256 vectors of 8 bf16 per chunk
             const int j = e >> 4, col = (e & 15) * 8;
-            const int nn = t * kBM + col;
+            const int nn = nb0 + col;
             if (j < jn && nn < A.N) {
               const uint4 val = *reinterpret_cast<const uint4*>(st + j * kBM + col);
-              const size_t yo = (size_t)(j0 + j) * A.N + nn;
+              const size_t yo = (size_t)(y0 + j0 + j) * A.N + nn;
               if (nn + 8 <= A.N && (A.N & 7) == 0) {
                 *reinterpret_cast<uint4*>(A.Y + yo) = val;
                 for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint4*>((__nv_bfloat16*)A.epi.dst[p] + yo) = val;
@@ -509,16 +520,17 @@ static int num_sms() {
   return n;
 }
 
-static kd_status geometry(const kd_attr_gemm& a, Geometry* g, int sms) {
+static kd_status geometry(const GemmShape& a, Geometry* g, int sms) {
   if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "gemm: only bf16 (fp32 path not built)");
-  if (a.M == 0 || a.N == 0 || a.K == 0) return fail(KD_ERR_INVALID_ARG, "gemm: empty shape");
-  if (a.M > 256) return fail(KD_ERR_UNSUPPORTED, "gemm: decode GEMM supports M <= 256");
+  if (a.M == 0 || a.N == 0 || a.K == 0 || a.rows_total == 0) return fail(KD_ERR_INVALID_ARG, "gemm: empty shape");
+  if (a.M > 256) return fail(KD_ERR_UNSUPPORTED, "gemm: decode GEMM supports M <= 256 rows (per group)");
   if (a.K % 8) return fail(KD_ERR_UNSUPPORTED, "gemm: K must be a multiple of 8 (16-byte TMA rows)");
+  if (a.groups && a.N % kBM) return fail(KD_ERR_UNSUPPORTED, "grouped gemm: N must be a multiple of 128");
   g->mma_n = (int)((a.M + 15) / 16 * 16);
   const int stage_bytes = kStageA + g->mma_n * kBK * 2;
   g->stages = std::min(kMaxStages, (kSmemBudget - 2 * kChunk * kBM * 2) / stage_bytes);
   g->kblocks = (int)((a.K + kBK - 1) / kBK);
-  g->tiles = (int)((a.N + kBM - 1) / kBM);
+  g->tiles = (int)((a.N + kBM - 1) / kBM) * (int)std::max<uint32_t>(1, a.groups);
   g->units = (long long)g->tiles * g->kblocks;
   g->grid = (int)std::min<long long>(sms, g->units);
   int mc = 1;
@@ -537,7 +549,29 @@ static size_t smem_bytes(const Geometry& g) {
 
 }  // namespace gemm
 
-kd_status gemm_scratch_bytes(const kd_attr_gemm& a, uint64_t* bytes) {
+GemmShape gemm_shape(const kd_attr_gemm& a) {
+  GemmShape s;
+  s.M = a.M;
+  s.rows_total = a.M;
+  s.N = a.N;
+  s.K = a.K;
+  s.groups = 0;
+  s.dtype = a.dtype;
+  return s;
+}
+
+GemmShape gemm_shape(const kd_attr_grouped_gemm& a) {
+  GemmShape s;
+  s.M = a.rows_cap;
+  s.rows_total = a.rows_total;
+  s.N = a.N;
+  s.K = a.K;
+  s.groups = a.experts;
+  s.dtype = a.dtype;
+  return s;
+}
+
+kd_status gemm_scratch_bytes(const GemmShape& a, uint64_t* bytes) {
   gemm::Geometry g;
   kd_status s = gemm::geometry(a, &g, kNumSMs);
   if (s) return s;
@@ -547,22 +581,18 @@ kd_status gemm_scratch_bytes(const kd_attr_gemm& a, uint64_t* bytes) {
   return KD_OK;
 }
 
-kd_status gemm_prepare(const kd_attr_gemm& a, const void* X, const void* W, GemmPlan* gp) {
+kd_status gemm_prepare(const GemmShape& a, const void* X, const void* W, const void* meta, GemmPlan* gp) {
   gemm::Geometry g;
   kd_status s = gemm::geometry(a, &g, kNumSMs);
   if (s) return s;
-  if (!X || !W) return fail(KD_ERR_INVALID_ARG, "gemm: NULL operand");
+  if (!X || !W || (a.groups && !meta)) return fail(KD_ERR_INVALID_ARG, "gemm: NULL operand");
   if (((uintptr_t)X | (uintptr_t)W) & 15) return fail(KD_ERR_INVALID_ARG, "gemm: operands must be 16-byte aligned");
-  s = gemm::encode(&gp->tmap_w, W, a.K, a.N, gemm::kBM);
+  s = gemm::encode(&gp->tmap_w, W, a.K, (uint64_t)a.N * std::max<uint32_t>(1, a.groups), gemm::kBM);
   if (s) return s;
-  s = gemm::encode(&gp->tmap_x, X, a.K, a.M, (uint32_t)g.mma_n);
+  s = gemm::encode(&gp->tmap_x, X, a.K, a.rows_total, (uint32_t)g.mma_n);
   if (s) return s;
-  gp->a = a;
-  gp->grid = g.grid;
-  gp->mma_n = g.mma_n;
-  gp->units = (uint32_t)g.units;
-  gp->kblocks = g.kblocks;
-  gp->tiles = g.tiles;
+  gp->sh = a;
+  gp->meta = (const int*)meta;
   return KD_OK;
 }
 
@@ -570,7 +600,7 @@ static unsigned long long* g_gemm_trace = nullptr;
 
 kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t* signals) {
   gemm::Geometry g;
-  kd_status s = gemm::geometry(gp.a, &g, kNumSMs);
+  kd_status s = gemm::geometry(gp.sh, &g, kNumSMs);
   if (s) return s;
   if (!Y) return fail(KD_ERR_INVALID_ARG, "gemm: NULL output");
   if (g.max_contrib > 1 && !c.scratch) return fail(KD_ERR_INVALID_ARG, "gemm: scratch required");
@@ -579,9 +609,12 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   if (2ull * g.tiles > kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "gemm: too many output tiles");
   A.counter = (unsigned*)c.scratch;
   A.part = (float*)((uint8_t*)c.scratch + kScratchCounterBytes);
-  A.M = gp.a.M;
-  A.N = gp.a.N;
-  A.K = gp.a.K;
+  A.M = gp.sh.M;
+  A.N = gp.sh.N;
+  A.K = gp.sh.K;
+  A.groups = (int)gp.sh.groups;
+  A.tpg = (int)((gp.sh.N + gemm::kBM - 1) / gemm::kBM);
+  A.meta = gp.meta;
   A.mma_n = g.mma_n;
   A.stages = g.stages;
   A.kblocks = g.kblocks;
@@ -600,7 +633,7 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   if (ks) return ks;
   KD_CUDA_CHECK(kd_launch(gemm::gemm_kernel, dim3(g.grid), dim3(gemm::kThreads), sm, c.stream, gp.tmap_w, gp.tmap_x, A),
                 "gemm launch");
-  if (signals) return gemm_signals(gp.a, signals);
+  if (signals) return gemm_signals(gp.sh, signals);
   return KD_OK;
 }
 
@@ -613,7 +646,7 @@ extern "C" kd_status kd_debug_gemm_trace(void* dev_buf) {  // 32 u64 stamps per 
 
 namespace kd {
 
-kd_status gemm_signals(const kd_attr_gemm& a, uint32_t* s) {
+kd_status gemm_signals(const GemmShape& a, uint32_t* s) {
   gemm::Geometry g;
   kd_status st = gemm::geometry(a, &g, kNumSMs);
   if (st) return st;

@@ -56,14 +56,21 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
                            const int32_t* bt, const int32_t* sl, void* out, const LaunchCtx& c, uint32_t* signals);
 
 // GEMM: TMA descriptors are encoded once per (X, W) pointer pair
+// shape of a (possibly grouped) decode GEMM: M = rows per group bound (MMA N,
+// partial layout), rows_total = rows of X/Y, groups = 0 for a plain GEMM
+struct GemmShape {
+  uint32_t M = 0, rows_total = 0, N = 0, K = 0, groups = 0, dtype = 0;
+};
+GemmShape gemm_shape(const kd_attr_gemm& a);
+GemmShape gemm_shape(const kd_attr_grouped_gemm& a);
 struct GemmPlan {
   alignas(64) CUtensorMap tmap_w;
   alignas(64) CUtensorMap tmap_x;
-  kd_attr_gemm a{};
-  uint32_t grid = 0, mma_n = 0, units = 0, kblocks = 0, tiles = 0;
+  GemmShape sh;
+  const int* meta = nullptr;  // grouped: int32 count[groups], offset[groups]
 };
-kd_status gemm_scratch_bytes(const kd_attr_gemm& a, uint64_t* bytes);
-kd_status gemm_prepare(const kd_attr_gemm& a, const void* X, const void* W, GemmPlan* gp);
+kd_status gemm_scratch_bytes(const GemmShape& sh, uint64_t* bytes);
+kd_status gemm_prepare(const GemmShape& sh, const void* X, const void* W, const void* meta, GemmPlan* gp);
 kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t* signals);
 
 // runtime support kernels
@@ -73,7 +80,15 @@ kd_status launch_step_begin(unsigned* epoch, unsigned* const* mine, unsigned* co
                             cudaStream_t s);
 // flag increments per launch (must equal what the launcher reports)
 kd_status attention_signals(const kd_attr_attention& a, uint32_t* s);
-kd_status gemm_signals(const kd_attr_gemm& a, uint32_t* s);
+kd_status gemm_signals(const GemmShape& sh, uint32_t* s);
+// MoE kernels (moe.cu)
+kd_status launch_moe_route(const kd_attr_moe_route& a, const void* h, const float* wr, void* route, const LaunchCtx& c,
+                           uint32_t* signals);
+kd_status launch_moe_dispatch(const kd_attr_moe_dispatch& a, const void* h, const void* route, void* xg, void* meta,
+                              const LaunchCtx& c, uint32_t* signals);
+kd_status launch_moe_combine(const kd_attr_moe_combine& a, const void* yg, const void* route, const void* meta,
+                             void* out, const LaunchCtx& c, uint32_t* signals);
+kd_status moe_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s);
 kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* signals);
 // one-time per-device kernel attributes (dynamic smem opt-in); call outside graph capture
 kd_status kernels_init();

@@ -18,7 +18,13 @@ kd_status op_scratch_bytes(uint32_t op, const std::vector<uint8_t>& attrs, u64* 
       kd_attr_gemm a;
       kd_status s = attrs_as(attrs, &a);
       if (s) return s;
-      return gemm_scratch_bytes(a, bytes);
+      return gemm_scratch_bytes(gemm_shape(a), bytes);
+    }
+    case KD_OP_GROUPED_GEMM: {
+      kd_attr_grouped_gemm a;
+      kd_status s = attrs_as(attrs, &a);
+      if (s) return s;
+      return gemm_scratch_bytes(gemm_shape(a), bytes);
     }
     case KD_OP_ATTENTION: {
       kd_attr_attention a;
@@ -40,7 +46,11 @@ extern "C" {
 kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes) {
   if (!attrs || !bytes) return fail(KD_ERR_INVALID_ARG, "kd_op_scratch_bytes: NULL argument");
   switch (op) {
-    case KD_OP_GEMM: return gemm_scratch_bytes(*(const kd_attr_gemm*)attrs, bytes);
+    case KD_OP_GEMM: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_gemm*)attrs), bytes);
+    case KD_OP_GROUPED_GEMM: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_grouped_gemm*)attrs), bytes);
+    case KD_OP_MOE_ROUTE:
+    case KD_OP_MOE_DISPATCH:
+    case KD_OP_MOE_COMBINE: *bytes = 0; return KD_OK;
     case KD_OP_ATTENTION: return attention_scratch_bytes(*(const kd_attr_attention*)attrs, bytes);
     case KD_OP_ADD_RMSNORM:
     case KD_OP_ROPE_APPEND:
@@ -61,7 +71,7 @@ kd_status kd_op_add_rmsnorm(const kd_attr_add_rmsnorm* a, float* r, const void* 
 kd_status kd_op_gemm(const kd_attr_gemm* a, const void* X, const void* W, void* Y, void* scratch, void* stream) {
   if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_gemm: NULL attrs");
   GemmPlan gp;
-  kd_status s = gemm_prepare(*a, X, W, &gp);
+  kd_status s = gemm_prepare(gemm_shape(*a), X, W, nullptr, &gp);
   if (s) return s;
   LaunchCtx c;
   c.stream = (cudaStream_t)stream;
@@ -99,6 +109,41 @@ kd_status kd_op_residual_add(const kd_attr_residual_add* a, float* r, const void
   LaunchCtx c;
   c.stream = (cudaStream_t)stream;
   return launch_residual_add(*a, r, delta, c, nullptr);
+}
+
+kd_status kd_op_grouped_gemm(const kd_attr_grouped_gemm* a, const void* xg, const void* w_experts, const void* meta,
+                             void* yg, void* scratch, void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_grouped_gemm: NULL attrs");
+  GemmPlan gp;
+  kd_status s = gemm_prepare(gemm_shape(*a), xg, w_experts, meta, &gp);
+  if (s) return s;
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  c.scratch = scratch;
+  return launch_gemm(gp, yg, c, nullptr);
+}
+
+kd_status kd_op_moe_route(const kd_attr_moe_route* a, const void* h, const float* w_router, void* route, void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_moe_route: NULL attrs");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  return launch_moe_route(*a, h, w_router, route, c, nullptr);
+}
+
+kd_status kd_op_moe_dispatch(const kd_attr_moe_dispatch* a, const void* h, const void* route, void* xg, void* meta,
+                             void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_moe_dispatch: NULL attrs");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  return launch_moe_dispatch(*a, h, route, xg, meta, c, nullptr);
+}
+
+kd_status kd_op_moe_combine(const kd_attr_moe_combine* a, const void* yg, const void* route, const void* meta,
+                            void* out, void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_moe_combine: NULL attrs");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  return launch_moe_combine(*a, yg, route, meta, out, c, nullptr);
 }
 
 }  // extern "C"

@@ -88,6 +88,10 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_ATTENTION: need = sizeof(kd_attr_attention); break;
     case KD_OP_SILU_MUL: need = sizeof(kd_attr_silu_mul); break;
     case KD_OP_RESIDUAL_ADD: need = sizeof(kd_attr_residual_add); break;
+    case KD_OP_MOE_ROUTE: need = sizeof(kd_attr_moe_route); break;
+    case KD_OP_MOE_DISPATCH: need = sizeof(kd_attr_moe_dispatch); break;
+    case KD_OP_GROUPED_GEMM: need = sizeof(kd_attr_grouped_gemm); break;
+    case KD_OP_MOE_COMBINE: need = sizeof(kd_attr_moe_combine); break;
     default: return fail(KD_ERR_UNSUPPORTED, "runtime: unknown op");
   }
   if (k.attrs.size() != need) return fail(KD_ERR_INVALID_ARG, "runtime: op attrs have the wrong size");
@@ -101,6 +105,10 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_ATTENTION: ok = nr == 5 && nw == 1; break;
     case KD_OP_SILU_MUL: ok = nr == 1 && nw == 1; break;
     case KD_OP_RESIDUAL_ADD: ok = nr == 2 && nw == 1; break;
+    case KD_OP_MOE_ROUTE: ok = nr == 2 && nw == 1; break;
+    case KD_OP_MOE_DISPATCH: ok = nr == 2 && nw == 1; break;  // writes [meta | xg]
+    case KD_OP_GROUPED_GEMM: ok = nr == 3 && nw == 1; break;  // reads [xg, W, meta]
+    case KD_OP_MOE_COMBINE: ok = nr == 3 && nw == 1; break;   // reads [yg, route, meta]
   }
   if (!ok) return fail(KD_ERR_INVALID_ARG, "runtime: wrong number of read/write spans for the op");
   return KD_OK;
@@ -156,6 +164,24 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
     case KD_OP_RESIDUAL_ADD: {
       auto a = attrs_get<kd_attr_residual_add>(K);
       st = launch_residual_add(a, (float*)l.wr[0], l.rd[1], c, &sig);
+      break;
+    }
+    case KD_OP_MOE_ROUTE: {
+      auto a = attrs_get<kd_attr_moe_route>(K);
+      st = launch_moe_route(a, l.rd[0], (const float*)l.rd[1], l.wr[0], c, &sig);
+      break;
+    }
+    case KD_OP_MOE_DISPATCH: {
+      auto a = attrs_get<kd_attr_moe_dispatch>(K);
+      uint64_t mb = 0;
+      kd_moe_meta_bytes(a.rows, a.experts, a.top_k, &mb);
+      st = launch_moe_dispatch(a, l.rd[0], l.rd[1], (uint8_t*)l.wr[0] + mb, l.wr[0], c, &sig);
+      break;
+    }
+    case KD_OP_GROUPED_GEMM: st = launch_gemm(*l.gemm, l.wr[0], c, &sig); break;
+    case KD_OP_MOE_COMBINE: {
+      auto a = attrs_get<kd_attr_moe_combine>(K);
+      st = launch_moe_combine(a, l.rd[0], l.rd[1], l.rd[2], l.wr[0], c, &sig);
       break;
     }
   }
@@ -413,9 +439,14 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
         ++l.ctx.epi.n;
       }
       l.ctx.scratch = d.ws + L.scratch_off;
+      if (K.op == KD_OP_GROUPED_GEMM) {
+        l.gemm = new GemmPlan();
+        kd_status s3 = gemm_prepare(gemm_shape(attrs_get<kd_attr_grouped_gemm>(K)), l.rd[0], l.rd[1], l.rd[2], l.gemm);
+        if (s3) return s3;
+      }
       if (K.op == KD_OP_GEMM) {
         l.gemm = new GemmPlan();
-        kd_status s3 = gemm_prepare(attrs_get<kd_attr_gemm>(K), l.rd[0], l.rd[1], l.gemm);
+        kd_status s3 = gemm_prepare(gemm_shape(attrs_get<kd_attr_gemm>(K)), l.rd[0], l.rd[1], nullptr, l.gemm);
         if (s3) return s3;
       }
       if (rt->profile_op) {

@@ -35,9 +35,9 @@ import numpy as np
 from . import _kd as K
 from .api import Graph, Machine, Plan, Runtime, place
 
-T_RESID, T_QKV, T_ATTN, T_O, T_GU, T_SILU, T_DOWN = range(7)
-MEMORY_ROLE = {T_RESID, T_ATTN, T_SILU}   # HBM-bound non-GEMM kernels
-GEMM_ROLE = {T_QKV, T_O, T_GU, T_DOWN}
+T_RESID, T_QKV, T_ATTN, T_O, T_GU, T_SILU, T_DOWN, T_ROUTE, T_DISPATCH, T_ESILU, T_COMBINE = range(11)
+MEMORY_ROLE = {T_RESID, T_ATTN, T_SILU, T_ROUTE, T_DISPATCH, T_COMBINE}   # HBM-bound non-GEMM kernels
+GEMM_ROLE = {T_QKV, T_O, T_GU, T_DOWN, T_ESILU}                           # GEMMs (+ the experts' SiLU)
 
 
 def b200_machine(n_dev: int, hbm_Bps: Optional[float] = None, tc_flops: Optional[float] = None,
@@ -83,7 +83,7 @@ class DecoderGraph:
         PERS, INP, OUT = K.KD_BUF_PERSISTENT, K.KD_BUF_INPUT, K.KD_BUF_OUTPUT
 
         def buf(name, shape, dt, flags):
-            nbytes = int(np.prod(shape)) * {"bf16": 2, "f32": 4, "i32": 4}[dt]
+            nbytes = int(np.prod(shape)) * {"bf16": 2, "f32": 4, "i32": 4, "u8": 1}[dt]
             self.buf[name] = g.add_buffer(nbytes, flags)
             self.shape[name] = tuple(shape)
             self.dtype[name] = dt
@@ -91,8 +91,14 @@ class DecoderGraph:
 
         def whole(name):
             b = self.buf[name]
-            n = int(np.prod(self.shape[name])) * {"bf16": 2, "f32": 4, "i32": 4}[self.dtype[name]]
+            n = int(np.prod(self.shape[name])) * {"bf16": 2, "f32": 4, "i32": 4, "u8": 1}[self.dtype[name]]
             return (b, 0, n)
+
+        E, k = cfg.n_experts, cfg.top_k
+        if E:
+            mb = C.c_uint64()
+            K.check(K.kd_moe_meta_bytes(m, E, k, C.byref(mb)), "kd_moe_meta_bytes")
+            self.meta_bytes = mb.value
 
         buf("r", (m, H), "f32", PERS | INP | OUT | PM)
         buf("bt", (m, pps), "i32", INP | PM)
@@ -100,20 +106,34 @@ class DecoderGraph:
         for l in range(L):
             buf(f"w_qkv.{l}", (cfg.qkv_dim, H), "bf16", W)
             buf(f"w_o.{l}", (H, Hq * D), "bf16", W)
-            buf(f"w_gu.{l}", (2 * F, H), "bf16", W)
-            buf(f"w_d.{l}", (H, F), "bf16", W)
+            if E:
+                buf(f"w_router.{l}", (E, H), "f32", W)
+                buf(f"w_gu_e.{l}", (E, 2 * F, H), "bf16", W)
+                buf(f"w_d_e.{l}", (E, H, F), "bf16", W)
+                buf(f"route.{l}", (2 * m * k,), "i32", PM)
+                buf(f"xgm.{l}", (self.meta_bytes + m * k * H * 2,), "u8", PM)
+                buf(f"gue.{l}", (m * k, 2 * F), "bf16", PM)
+                buf(f"ae.{l}", (m * k, F), "bf16", PM)
+                buf(f"ye.{l}", (m * k, H), "bf16", PM)
+            else:
+                buf(f"w_gu.{l}", (2 * F, H), "bf16", W)
+                buf(f"w_d.{l}", (H, F), "bf16", W)
             buf(f"g1.{l}", (H,), "bf16", W)
             buf(f"g2.{l}", (H,), "bf16", W)
             buf(f"kc.{l}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
             buf(f"vc.{l}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
-            for nm, shp in (("h1", (m, H)), ("qkv", (m, cfg.qkv_dim)), ("q", (m, Hq * D)), ("attn", (m, Hq * D)),
-                            ("o", (m, H)), ("h2", (m, H)), ("gu", (m, 2 * F)), ("a", (m, F)), ("d", (m, H))):
+            acts = [("h1", (m, H)), ("qkv", (m, cfg.qkv_dim)), ("q", (m, Hq * D)), ("attn", (m, Hq * D)),
+                    ("o", (m, H)), ("h2", (m, H)), ("d", (m, H))]
+            if not E:
+                acts += [("gu", (m, 2 * F)), ("a", (m, F))]
+            for nm, shp in acts:
                 buf(f"{nm}.{l}", shp, "bf16", PM)
 
         self.kernels: List[KernelInfo] = []
 
         def add(name, layer, tmpl, op, reads, writes, attrs, flops=0):
-            kid = g.add_kernel(op, [whole(x) for x in reads], [whole(x) for x in writes], attrs, flops, -1, tmpl)
+            span = lambda x: x if isinstance(x, tuple) else whole(x)
+            kid = g.add_kernel(op, [span(x) for x in reads], [span(x) for x in writes], attrs, flops, -1, tmpl)
             self.kernels.append(KernelInfo(name, layer, tmpl, kid))
             return kid
 
@@ -133,11 +153,28 @@ class DecoderGraph:
                 K.kd_attr_gemm(m, H, Hq * D, act), 2 * m * H * Hq * D)
             add("norm2", l, T_RESID, K.KD_OP_ADD_RMSNORM, ["r", f"o.{l}", f"g2.{l}"], [f"h2.{l}", "r"],
                 K.kd_attr_add_rmsnorm(m, H, 1, act, eps, 0))
-            add("gu", l, T_GU, K.KD_OP_GEMM, [f"h2.{l}", f"w_gu.{l}"], [f"gu.{l}"],
-                K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
-            add("silu", l, T_SILU, K.KD_OP_SILU_MUL, [f"gu.{l}"], [f"a.{l}"], K.kd_attr_silu_mul(m, F, act, 0))
-            add("down", l, T_DOWN, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
-                K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)
+            if E:
+                xgm = self.buf[f"xgm.{l}"]
+                meta_span = (xgm, 0, self.meta_bytes)
+                xg_span = (xgm, self.meta_bytes, m * k * H * 2)
+                am = K.kd_attr_moe(m, H, E, k)
+                add("route", l, T_ROUTE, K.KD_OP_MOE_ROUTE, [f"h2.{l}", f"w_router.{l}"], [f"route.{l}"], am,
+                    2 * m * E * H)
+                add("dispatch", l, T_DISPATCH, K.KD_OP_MOE_DISPATCH, [f"h2.{l}", f"route.{l}"], [f"xgm.{l}"], am)
+                add("gu", l, T_GU, K.KD_OP_GROUPED_GEMM, [xg_span, f"w_gu_e.{l}", meta_span], [f"gue.{l}"],
+                    K.kd_attr_grouped_gemm(m * k, 2 * F, H, E, m, act), 2 * m * k * 2 * F * H)
+                add("silu", l, T_ESILU, K.KD_OP_SILU_MUL, [f"gue.{l}"], [f"ae.{l}"],
+                    K.kd_attr_silu_mul(m * k, F, act, 0))
+                add("down", l, T_DOWN, K.KD_OP_GROUPED_GEMM, [f"ae.{l}", f"w_d_e.{l}", meta_span], [f"ye.{l}"],
+                    K.kd_attr_grouped_gemm(m * k, H, F, E, m, act), 2 * m * k * H * F)
+                add("combine", l, T_COMBINE, K.KD_OP_MOE_COMBINE, [f"ye.{l}", f"route.{l}", meta_span], [f"d.{l}"],
+                    am)
+            else:
+                add("gu", l, T_GU, K.KD_OP_GEMM, [f"h2.{l}", f"w_gu.{l}"], [f"gu.{l}"],
+                    K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
+                add("silu", l, T_SILU, K.KD_OP_SILU_MUL, [f"gu.{l}"], [f"a.{l}"], K.kd_attr_silu_mul(m, F, act, 0))
+                add("down", l, T_DOWN, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
+                    K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)
         add("final_add", L - 1, T_RESID, K.KD_OP_RESIDUAL_ADD, ["r", f"d.{L-1}"], ["r"],
             K.kd_attr_residual_add(m, H))
         g.finalize()
@@ -234,10 +271,12 @@ class DecoderRuntime:
             elif base in ("kc", "vc"):
                 src = (inputs.k_cache if base == "kc" else inputs.v_cache)[int(lay)]
                 put_bf16(src[i * m * pps:(i + 1) * m * pps])
+            elif base == "w_router":
+                t.copy_(torch.from_numpy(inputs.layers[int(lay)].w_router))
             else:
                 lw = inputs.layers[int(lay)]
                 put_bf16({"w_qkv": lw.w_qkv, "w_o": lw.w_o, "w_gu": lw.w_gu, "w_d": lw.w_d,
-                          "g1": lw.gamma1, "g2": lw.gamma2}[base])
+                          "g1": lw.gamma1, "g2": lw.gamma2, "w_gu_e": lw.w_gu_e, "w_d_e": lw.w_d_e}[base])
             return
         # device-side seeded values (throughput runs)
         s = seed * 1_000_003 + self.dg.buf[name] * 131 + i
@@ -257,9 +296,9 @@ class DecoderRuntime:
             device_normal_(t, s, 0.1)
             t.add_(1.0)
         else:
-            K_in = t.shape[1]
+            K_in = t.shape[-1]
             std = 1.0 / math.sqrt(K_in)
-            if base in ("w_o", "w_d"):
+            if base in ("w_o", "w_d", "w_d_e"):
                 std /= math.sqrt(2.0 * L)
             device_normal_(t, s, std)
 

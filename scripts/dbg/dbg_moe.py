@@ -1,0 +1,9 @@
+import sys; sys.path.insert(0, "/root/repo")
+import synth
+from paper_2604_10180_b200 import decoder as DEC
+cfg = synth.TINY.with_(n_experts=4, top_k=2, n_micro=2)
+inp = synth.make_decoder_inputs(cfg)
+dg = DEC.DecoderGraph(cfg)
+for k in dg.kernels[:14]: print(k)
+rt = DEC.DecoderRuntime(dg, [0]*dg.g.num_kernels, 1, [0], inputs=inp, use_graph=False)
+rt.step(); rt.sync(); print("ok")

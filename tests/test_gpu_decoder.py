@@ -110,3 +110,20 @@ def test_full_width_8b_layers_vs_oracle_sampled(mod):
     rt = run(DEC, cfg, inp, lambda dg: [0] * dg.g.num_kernels, 1)
     r_ref, _, _ = OL.decoder_step(inp, act="bf16")
     assert relerr(rt.residual(), r_ref) < 2e-2
+
+
+TINY_MOE = synth.TINY.with_(n_experts=4, top_k=2, n_micro=2)
+
+
+def test_moe_decoder_monolithic_vs_oracle_and_disaggregated_bitwise(mod):
+    """Mixtral-style layers (router/dispatch/combine on the memory role, grouped
+    expert GEMMs on the GEMM role): monolithic vs the oracle, disaggregated
+    loopback bitwise equal to monolithic."""
+    DEC, K = mod
+    cfg = TINY_MOE
+    inp = synth.make_decoder_inputs(cfg)
+    mono = run(DEC, cfg, inp, lambda dg: [0] * dg.g.num_kernels, 1)
+    r_ref, _, _ = OL.decoder_step(inp, act="bf16")
+    assert relerr(mono.residual(), r_ref) < 2e-2
+    dis = run(DEC, cfg, inp, lambda dg: dg.role_assign(0, 1), 2)
+    assert np.array_equal(mono.residual(), dis.residual())
