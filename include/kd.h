@@ -92,7 +92,10 @@ enum {
   KD_OP_MOE_ROUTE = 7,     /* a11 reads [h, W_router] writes [route]            */
   KD_OP_MOE_DISPATCH = 8,  /* a11 reads [h, route] writes [xg, meta]            */
   KD_OP_GROUPED_GEMM = 9,  /* a11 reads [xg, W_experts, meta] writes [yg]       */
-  KD_OP_MOE_COMBINE = 10   /* a11 reads [yg, route, meta] writes [out]          */
+  KD_OP_MOE_COMBINE = 10,  /* a11 reads [yg, route, meta] writes [out]          */
+  KD_OP_SSM_CONV = 11,     /* a12 reads [zxbcdt, conv_w, conv_b, conv_state] writes [xbc, conv_state] */
+  KD_OP_SSM_UPDATE = 12,   /* a12 reads [xbc, zxbcdt, dt_bias, A_log, D, ssm_state] writes [y, ssm_state] */
+  KD_OP_GATED_NORM = 13    /* a12 reads [y, zxbcdt, norm_w] writes [yn]          */
 };
 
 /* element types of activations / KV */
@@ -126,6 +129,17 @@ typedef struct {
   uint32_t dtype;
 } kd_attr_grouped_gemm;                                                          /* yg bf16 [rows_total, N] */
 typedef struct { uint32_t rows, hidden, experts, top_k; } kd_attr_moe_combine;  /* out bf16 [rows, H] */
+/* Mamba-2 decode. zxbcdt = in_proj output bf16 [rows, P_in]
+ * with columns [z (d_inner) | xBC (d_inner + 2·G·N) | dt (nheads)], P_in =
+ * 2·d_inner + 2·G·N + nheads, d_inner = nheads·head_dim. conv_state bf16
+ * [rows, d_inner + 2GN, d_conv-1] (oldest first), conv_w bf16 [ch, d_conv],
+ * conv_b bf16 [ch]; ssm_state fp32 [rows, nheads, head_dim, N]; dt_bias,
+ * A_log, D fp32 [nheads]; norm_w bf16 [d_inner]; xbc bf16 [rows, ch]; y, yn
+ * bf16 [rows, d_inner]. The gated norm normalises groups of d_inner/G. */
+typedef struct {
+  uint32_t rows, nheads, head_dim, d_state, ngroups, d_conv, dtype;
+  float eps;
+} kd_attr_ssm;
 
 typedef struct {
   uint32_t op;              /* KD_OP_* */
@@ -321,6 +335,15 @@ kd_status kd_op_attention(const kd_attr_attention* a, const void* q, const void*
 kd_status kd_op_silu_mul(const kd_attr_silu_mul* a, const void* gu, void* out, void* stream);
 /* C1.11: r += delta */
 kd_status kd_op_residual_add(const kd_attr_residual_add* a, float* r, const void* delta, void* stream);
+/* a12: conv step: window = [state, x]; xbc = silu(window·w + b); state ← window[1:] (in place) */
+kd_status kd_op_ssm_conv(const kd_attr_ssm* a, const void* zxbcdt, const void* conv_w, const void* conv_b,
+                         void* conv_state, void* xbc, void* stream);
+/* a12: S ← S·exp(softplus(dt+b)·(−e^{A_log})) + softplus(dt+b)·x⊗B; y = S·C + D·x (in place on S) */
+kd_status kd_op_ssm_update(const kd_attr_ssm* a, const void* xbc, const void* zxbcdt, const float* dt_bias,
+                           const float* A_log, const float* D, float* ssm_state, void* y, void* stream);
+/* a12: yn = groupwise RMSNorm(y · silu(z)) · norm_w */
+kd_status kd_op_gated_norm(const kd_attr_ssm* a, const void* y, const void* zxbcdt, const void* norm_w, void* yn,
+                           void* stream);
 /* a11 router: logits = h·W_rᵀ in fp32 (fixed-order warp reduction), top_k by
  * logit (ties → lower expert index), weights = softmax over the selected. */
 kd_status kd_op_moe_route(const kd_attr_moe_route* a, const void* h, const float* w_router, void* route, void* stream);

@@ -210,6 +210,78 @@ def moe_ffn(h, idx, wts, w_gu_e, w_d_e, act="bf16"):
     return store(out, act)
 
 
+# ---------------------------------------------------------------- a12 (SSM)
+def softplus(x):
+    x = np.asarray(x, np.float64)
+    return np.where(x > 20.0, x, np.log1p(np.exp(np.minimum(x, 20.0))))
+
+
+def mamba_conv_step(xbc, conv_state, conv_w, conv_b, act="bf16"):
+    """Causal depthwise conv1d, one decode step (C1.13, SURVEY a12 "conv: shift
+    state, 4-tap dot, SiLU"). xbc [m, Ch] new inputs; conv_state [m, Ch, W-1]
+    previous inputs oldest first; conv_w [Ch, W]; conv_b [Ch].
+    window = [state, x]; out = silu(Σ_w window_w · conv_w[:, w] + b);
+    new_state = window[1:]. Returns (out stored in act, new_state stored in act)."""
+    win = np.concatenate([np.asarray(conv_state, np.float64), np.asarray(xbc, np.float64)[:, :, None]], axis=2)
+    pre = np.einsum("mcw,cw->mc", win, np.asarray(conv_w, np.float64)) + np.asarray(conv_b, np.float64)
+    return store(silu(pre), act), store(win[:, :, 1:], act)
+
+
+def mamba_ssm_step(x, Bm, Cm, dt, dt_bias, A_log, D, state, nheads, headdim, dstate, ngroups, act="bf16"):
+    """Mamba-2 selective-state update, one decode step (C1.13):
+    for sequence b, head h, group g(h) = ⌊h / (nheads/ngroups)⌋:
+      dt_h = softplus(dt[b,h] + dt_bias[h]);  A_h = −exp(A_log[h]);  dA = exp(dt_h·A_h)
+      S ← S·dA + dt_h · x[b,h,:] ⊗ B[b,g,:]        (S: [headdim, dstate], fp32 storage)
+      y[b,h,:] = S · C[b,g,:] + D[h] · x[b,h,:]
+    x [m, nheads·headdim]; Bm, Cm [m, ngroups·dstate]; dt [m, nheads];
+    state [m, nheads, headdim, dstate]. Returns (y stored in act, new state fp32)."""
+    m = x.shape[0]
+    hpg = nheads // ngroups
+    X = np.asarray(x, np.float64).reshape(m, nheads, headdim)
+    Bv = np.asarray(Bm, np.float64).reshape(m, ngroups, dstate)
+    Cv = np.asarray(Cm, np.float64).reshape(m, ngroups, dstate)
+    S = np.asarray(state, np.float64).copy()
+    y = np.zeros((m, nheads, headdim))
+    for b in range(m):
+        for h in range(nheads):
+            g = h // hpg
+            dth = softplus(dt[b, h] + dt_bias[h])
+            dA = np.exp(dth * -np.exp(A_log[h]))
+            S[b, h] = S[b, h] * dA + dth * np.outer(X[b, h], Bv[b, g])
+            y[b, h] = S[b, h] @ Cv[b, g] + D[h] * X[b, h]
+    return store(y.reshape(m, nheads * headdim), act), round_f32(S)
+
+
+def gated_rmsnorm(y, z, weight, group_size, eps, act="bf16"):
+    """Gated RMSNorm of Mamba-2 (C1.13): g = y · silu(z); per group of
+    `group_size` channels, out = g / sqrt(mean(g²) + eps) · weight."""
+    g = np.asarray(y, np.float64) * silu(z)
+    m, n = g.shape
+    gg = g.reshape(m, n // group_size, group_size)
+    out = gg / np.sqrt(np.mean(gg * gg, axis=-1, keepdims=True) + eps)
+    return store(out.reshape(m, n) * np.asarray(weight, np.float64), act)
+
+
+def mamba_layer(r, delta_prev, mw, conv_state, ssm_state, cfg, act="bf16"):
+    """One Mamba-2 decode layer in program order (C1.13): add+RMSNorm →
+    in_proj → conv step → SSM step → gated RMSNorm → out_proj. in_proj columns
+    are [z (d_inner) | xBC (d_inner + 2·G·N) | dt (nheads)] (Mamba-2 order).
+    Returns (r, d, conv_state', ssm_state')."""
+    dec = bf16_to_f64
+    di, G, N, nh, P = cfg.d_inner, cfg.ssm_groups, cfg.d_state, cfg.ssm_heads, cfg.ssm_head_dim
+    r, h = add_rmsnorm(r, delta_prev, dec(mw.gamma), cfg.eps, act)
+    zxbcdt = linear(h, dec(mw.w_in), act)
+    z = zxbcdt[:, :di]
+    xbc = zxbcdt[:, di:2 * di + 2 * G * N]
+    dt = zxbcdt[:, 2 * di + 2 * G * N:]
+    xc, conv_state = mamba_conv_step(xbc, conv_state, dec(mw.conv_w), dec(mw.conv_b), act)
+    y, ssm_state = mamba_ssm_step(xc[:, :di], xc[:, di:di + G * N], xc[:, di + G * N:], dt, mw.dt_bias, mw.A_log,
+                                  mw.D, ssm_state, nh, P, N, G, act)
+    yn = gated_rmsnorm(y, z, dec(mw.norm_w), di // G, cfg.eps, act)
+    d = linear(yn, dec(mw.w_out), act)
+    return r, d, conv_state, ssm_state
+
+
 # ---------------------------------------------------------------- layer
 def decoder_layer(r, delta_prev, lw, k_cache, v_cache, block_table, seq_len,
                   cfg, act="bf16"):
@@ -236,6 +308,28 @@ def decoder_layer(r, delta_prev, lw, k_cache, v_cache, block_table, seq_len,
         a = silu_mul_blocked(gu, act=act)
         d = linear(a, dec(lw.w_d), act)
     return r, d
+
+
+def hybrid_step(inp, act="bf16"):
+    """Hybrid decode step: layer l is attention
+    (Llama-shaped incl. MLP) when cfg.is_attn_layer(l), else Mamba-2.
+    Returns (r_out, conv_states, ssm_states)."""
+    cfg = inp.cfg
+    r = np.asarray(inp.x, np.float64)
+    d = None
+    convs, ssms = [], []
+    for l in range(cfg.n_layers):
+        if cfg.is_attn_layer(l):
+            kc = store(bf16_to_f64(inp.k_cache[l]), act)
+            vc = store(bf16_to_f64(inp.v_cache[l]), act)
+            r, d = decoder_layer(r, d, inp.layers[l], kc, vc, inp.block_table, inp.seq_len, cfg, act)
+        else:
+            mw = inp.layers[l]
+            r, d, cs, ss = mamba_layer(r, d, mw, store(bf16_to_f64(inp.conv_state[l]), act),
+                                       round_f32(inp.ssm_state[l]), cfg, act)
+            convs.append(cs)
+            ssms.append(ss)
+    return residual_add(r, d), convs, ssms
 
 
 def decoder_step(inp, act="bf16", layers=None):

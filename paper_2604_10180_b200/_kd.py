@@ -24,7 +24,8 @@ KD_OK, KD_ERR_INVALID_ARG, KD_ERR_RANGE, KD_ERR_STATE, KD_ERR_PIN_CONFLICT, KD_E
 KD_BUF_WEIGHT, KD_BUF_INPUT, KD_BUF_OUTPUT, KD_BUF_PERSISTENT, KD_BUF_PER_MICROBATCH = 1, 2, 4, 8, 16
 # ops
 KD_OP_NONE, KD_OP_ADD_RMSNORM, KD_OP_GEMM, KD_OP_ROPE_APPEND, KD_OP_ATTENTION, KD_OP_SILU_MUL, \
-    KD_OP_RESIDUAL_ADD, KD_OP_MOE_ROUTE, KD_OP_MOE_DISPATCH, KD_OP_GROUPED_GEMM, KD_OP_MOE_COMBINE = range(11)
+    KD_OP_RESIDUAL_ADD, KD_OP_MOE_ROUTE, KD_OP_MOE_DISPATCH, KD_OP_GROUPED_GEMM, KD_OP_MOE_COMBINE, \
+    KD_OP_SSM_CONV, KD_OP_SSM_UPDATE, KD_OP_GATED_NORM = range(14)
 KD_BF16, KD_F32 = 0, 1
 KD_OBJ_AUTO, KD_OBJ_THROUGHPUT, KD_OBJ_LATENCY = 0, 1, 2
 KD_MODE_DISAGG, KD_MODE_NO_TRANSFER, KD_MODE_LOG = 0, 1, 2
@@ -85,6 +86,11 @@ kd_attr_moe_route = kd_attr_moe_dispatch = kd_attr_moe_combine = kd_attr_moe
 class kd_attr_grouped_gemm(C.Structure):
     _fields_ = [("rows_total", C.c_uint32), ("N", C.c_uint32), ("K", C.c_uint32), ("experts", C.c_uint32),
                 ("rows_cap", C.c_uint32), ("dtype", C.c_uint32)]
+
+
+class kd_attr_ssm(C.Structure):
+    _fields_ = [("rows", C.c_uint32), ("nheads", C.c_uint32), ("head_dim", C.c_uint32), ("d_state", C.c_uint32),
+                ("ngroups", C.c_uint32), ("d_conv", C.c_uint32), ("dtype", C.c_uint32), ("eps", C.c_float)]
 
 
 class kd_kernel_desc(C.Structure):
@@ -170,6 +176,9 @@ _PROTOS = {
     "kd_op_moe_dispatch": (kd_status, [C.POINTER(kd_attr_moe), P, P, P, P, P]),
     "kd_op_grouped_gemm": (kd_status, [C.POINTER(kd_attr_grouped_gemm), P, P, P, P, P, P]),
     "kd_op_moe_combine": (kd_status, [C.POINTER(kd_attr_moe), P, P, P, P, P]),
+    "kd_op_ssm_conv": (kd_status, [C.POINTER(kd_attr_ssm), P, P, P, P, P, P]),
+    "kd_op_ssm_update": (kd_status, [C.POINTER(kd_attr_ssm), P, P, P, P, P, P, P, P]),
+    "kd_op_gated_norm": (kd_status, [C.POINTER(kd_attr_ssm), P, P, P, P, P]),
     "kd_op_add_rmsnorm": (kd_status, [C.POINTER(kd_attr_add_rmsnorm), P, P, P, P, P]),
     "kd_op_gemm": (kd_status, [C.POINTER(kd_attr_gemm), P, P, P, P, P]),
     "kd_op_rope_append": (kd_status, [C.POINTER(kd_attr_rope_append), P, P, P, P, P, P, P]),

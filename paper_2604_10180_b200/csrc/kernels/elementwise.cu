@@ -344,12 +344,14 @@ kd_status launch_wait(const WaitList& w, const unsigned* epoch, unsigned* err, c
   return KD_OK;
 }
 
+kd_status ssm_init_attrs();  // ssm.cu
+
 kd_status elementwise_init_attrs() {
   const void* fns[] = {(const void*)add_rmsnorm_kernel, (const void*)residual_add_kernel, (const void*)silu_mul_kernel,
                        (const void*)rope_append_kernel, (const void*)step_begin_kernel2, (const void*)wait_kernel};
   for (const void* f : fns)
     KD_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-  return KD_OK;
+  return ssm_init_attrs();
 }
 
 template <typename T>
@@ -375,6 +377,9 @@ kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s
     case KD_OP_MOE_ROUTE:
     case KD_OP_MOE_DISPATCH:
     case KD_OP_MOE_COMBINE: return moe_signals(op, attrs, signals);
+    case KD_OP_SSM_CONV:
+    case KD_OP_SSM_UPDATE:
+    case KD_OP_GATED_NORM: return ssm_signals(op, attrs, signals);
   }
   *signals = 0;
   return KD_OK;

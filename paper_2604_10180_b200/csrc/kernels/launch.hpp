@@ -89,6 +89,15 @@ kd_status launch_moe_dispatch(const kd_attr_moe_dispatch& a, const void* h, cons
 kd_status launch_moe_combine(const kd_attr_moe_combine& a, const void* yg, const void* route, const void* meta,
                              void* out, const LaunchCtx& c, uint32_t* signals);
 kd_status moe_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s);
+// Mamba-2 kernels (ssm.cu)
+kd_status launch_ssm_conv(const kd_attr_ssm& a, const void* zx, const void* w, const void* bias, void* state,
+                          void* out, const LaunchCtx& c, uint32_t* signals);
+kd_status launch_ssm_update(const kd_attr_ssm& a, const void* xbc, const void* zx, const float* dt_bias,
+                            const float* A_log, const float* D, float* state, void* y, const LaunchCtx& c,
+                            uint32_t* signals);
+kd_status launch_gated_norm(const kd_attr_ssm& a, const void* y, const void* zx, const void* w, void* out,
+                            const LaunchCtx& c, uint32_t* signals);
+kd_status ssm_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s);
 kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* signals);
 // one-time per-device kernel attributes (dynamic smem opt-in); call outside graph capture
 kd_status kernels_init();

@@ -50,7 +50,10 @@ kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes) {
     case KD_OP_GROUPED_GEMM: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_grouped_gemm*)attrs), bytes);
     case KD_OP_MOE_ROUTE:
     case KD_OP_MOE_DISPATCH:
-    case KD_OP_MOE_COMBINE: *bytes = 0; return KD_OK;
+    case KD_OP_MOE_COMBINE:
+    case KD_OP_SSM_CONV:
+    case KD_OP_SSM_UPDATE:
+    case KD_OP_GATED_NORM: *bytes = 0; return KD_OK;
     case KD_OP_ATTENTION: return attention_scratch_bytes(*(const kd_attr_attention*)attrs, bytes);
     case KD_OP_ADD_RMSNORM:
     case KD_OP_ROPE_APPEND:

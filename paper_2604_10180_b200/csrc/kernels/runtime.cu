@@ -92,6 +92,9 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_MOE_DISPATCH: need = sizeof(kd_attr_moe_dispatch); break;
     case KD_OP_GROUPED_GEMM: need = sizeof(kd_attr_grouped_gemm); break;
     case KD_OP_MOE_COMBINE: need = sizeof(kd_attr_moe_combine); break;
+    case KD_OP_SSM_CONV:
+    case KD_OP_SSM_UPDATE:
+    case KD_OP_GATED_NORM: need = sizeof(kd_attr_ssm); break;
     default: return fail(KD_ERR_UNSUPPORTED, "runtime: unknown op");
   }
   if (k.attrs.size() != need) return fail(KD_ERR_INVALID_ARG, "runtime: op attrs have the wrong size");
@@ -109,6 +112,9 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_MOE_DISPATCH: ok = nr == 2 && nw == 1; break;  // writes [meta | xg]
     case KD_OP_GROUPED_GEMM: ok = nr == 3 && nw == 1; break;  // reads [xg, W, meta]
     case KD_OP_MOE_COMBINE: ok = nr == 3 && nw == 1; break;   // reads [yg, route, meta]
+    case KD_OP_SSM_CONV: ok = nr == 4 && nw == 2; break;      // reads [zx, w, b, state] writes [xbc, state]
+    case KD_OP_SSM_UPDATE: ok = nr == 6 && nw == 2; break;    // reads [xbc, zx, dt_b, A_log, D, S] writes [y, S]
+    case KD_OP_GATED_NORM: ok = nr == 3 && nw == 1; break;    // reads [y, zx, w]
   }
   if (!ok) return fail(KD_ERR_INVALID_ARG, "runtime: wrong number of read/write spans for the op");
   return KD_OK;
@@ -179,6 +185,22 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
       break;
     }
     case KD_OP_GROUPED_GEMM: st = launch_gemm(*l.gemm, l.wr[0], c, &sig); break;
+    case KD_OP_SSM_CONV: {
+      auto a = attrs_get<kd_attr_ssm>(K);
+      st = launch_ssm_conv(a, l.rd[0], l.rd[1], l.rd[2], l.wr[1], l.wr[0], c, &sig);
+      break;
+    }
+    case KD_OP_SSM_UPDATE: {
+      auto a = attrs_get<kd_attr_ssm>(K);
+      st = launch_ssm_update(a, l.rd[0], l.rd[1], (const float*)l.rd[2], (const float*)l.rd[3], (const float*)l.rd[4],
+                             (float*)l.wr[1], l.wr[0], c, &sig);
+      break;
+    }
+    case KD_OP_GATED_NORM: {
+      auto a = attrs_get<kd_attr_ssm>(K);
+      st = launch_gated_norm(a, l.rd[0], l.rd[1], l.rd[2], l.wr[0], c, &sig);
+      break;
+    }
     case KD_OP_MOE_COMBINE: {
       auto a = attrs_get<kd_attr_moe_combine>(K);
       st = launch_moe_combine(a, l.rd[0], l.rd[1], l.rd[2], l.wr[0], c, &sig);

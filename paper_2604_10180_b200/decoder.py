@@ -35,9 +35,10 @@ import numpy as np
 from . import _kd as K
 from .api import Graph, Machine, Plan, Runtime, place
 
-T_RESID, T_QKV, T_ATTN, T_O, T_GU, T_SILU, T_DOWN, T_ROUTE, T_DISPATCH, T_ESILU, T_COMBINE = range(11)
-MEMORY_ROLE = {T_RESID, T_ATTN, T_SILU, T_ROUTE, T_DISPATCH, T_COMBINE}   # HBM-bound non-GEMM kernels
-GEMM_ROLE = {T_QKV, T_O, T_GU, T_DOWN, T_ESILU}                           # GEMMs (+ the experts' SiLU)
+(T_RESID, T_QKV, T_ATTN, T_O, T_GU, T_SILU, T_DOWN, T_ROUTE, T_DISPATCH, T_ESILU, T_COMBINE,
+ T_INPROJ, T_SSM, T_OUTPROJ) = range(14)
+MEMORY_ROLE = {T_RESID, T_ATTN, T_SILU, T_ROUTE, T_DISPATCH, T_COMBINE, T_SSM}  # HBM-bound non-GEMM kernels
+GEMM_ROLE = {T_QKV, T_O, T_GU, T_DOWN, T_ESILU, T_INPROJ, T_OUTPROJ}           # GEMMs (+ the experts' SiLU)
 
 
 def b200_machine(n_dev: int, hbm_Bps: Optional[float] = None, tc_flops: Optional[float] = None,
@@ -104,6 +105,24 @@ class DecoderGraph:
         buf("bt", (m, pps), "i32", INP | PM)
         buf("sl", (m,), "i32", INP | PM)
         for l in range(L):
+            if not cfg.is_attn_layer(l):
+                di, pin, ch = cfg.d_inner, cfg.in_proj_dim, cfg.conv_channels
+                nh = cfg.ssm_heads
+                buf(f"g1.{l}", (H,), "bf16", W)
+                buf(f"w_in.{l}", (pin, H), "bf16", W)
+                buf(f"conv_w.{l}", (ch, cfg.d_conv), "bf16", W)
+                buf(f"conv_b.{l}", (ch,), "bf16", W)
+                buf(f"dt_bias.{l}", (nh,), "f32", W)
+                buf(f"A_log.{l}", (nh,), "f32", W)
+                buf(f"Dp.{l}", (nh,), "f32", W)
+                buf(f"norm_w.{l}", (di,), "bf16", W)
+                buf(f"w_out.{l}", (H, di), "bf16", W)
+                buf(f"conv_st.{l}", (m, ch, cfg.d_conv - 1), "bf16", PERS | PM)
+                buf(f"ssm_st.{l}", (m, nh, cfg.ssm_head_dim, cfg.d_state), "f32", PERS | PM)
+                for nm, shp in (("h1", (m, H)), ("zx", (m, pin)), ("xbc", (m, ch)), ("y", (m, di)),
+                                ("yn", (m, di)), ("d", (m, H))):
+                    buf(f"{nm}.{l}", shp, "bf16", PM)
+                continue
             buf(f"w_qkv.{l}", (cfg.qkv_dim, H), "bf16", W)
             buf(f"w_o.{l}", (H, Hq * D), "bf16", W)
             if E:
@@ -140,6 +159,24 @@ class DecoderGraph:
         eps = float(cfg.eps)
         for l in range(L):
             has_d = 1 if l > 0 else 0
+            if not cfg.is_attn_layer(l):
+                di, pin = cfg.d_inner, cfg.in_proj_dim
+                sa = K.kd_attr_ssm(m, cfg.ssm_heads, cfg.ssm_head_dim, cfg.d_state, cfg.ssm_groups, cfg.d_conv,
+                                   act, eps)
+                add("norm1", l, T_RESID, K.KD_OP_ADD_RMSNORM,
+                    ["r"] + ([f"d.{l-1}"] if has_d else []) + [f"g1.{l}"], [f"h1.{l}", "r"],
+                    K.kd_attr_add_rmsnorm(m, H, has_d, act, eps, 0))
+                add("in_proj", l, T_INPROJ, K.KD_OP_GEMM, [f"h1.{l}", f"w_in.{l}"], [f"zx.{l}"],
+                    K.kd_attr_gemm(m, pin, H, act), 2 * m * pin * H)
+                add("ssm_conv", l, T_SSM, K.KD_OP_SSM_CONV, [f"zx.{l}", f"conv_w.{l}", f"conv_b.{l}", f"conv_st.{l}"],
+                    [f"xbc.{l}", f"conv_st.{l}"], sa)
+                add("ssm_update", l, T_SSM, K.KD_OP_SSM_UPDATE,
+                    [f"xbc.{l}", f"zx.{l}", f"dt_bias.{l}", f"A_log.{l}", f"Dp.{l}", f"ssm_st.{l}"],
+                    [f"y.{l}", f"ssm_st.{l}"], sa, 6 * m * cfg.ssm_heads * cfg.ssm_head_dim * cfg.d_state)
+                add("gated_norm", l, T_SSM, K.KD_OP_GATED_NORM, [f"y.{l}", f"zx.{l}", f"norm_w.{l}"], [f"yn.{l}"], sa)
+                add("out_proj", l, T_OUTPROJ, K.KD_OP_GEMM, [f"yn.{l}", f"w_out.{l}"], [f"d.{l}"],
+                    K.kd_attr_gemm(m, H, di, act), 2 * m * H * di)
+                continue
             add("norm1", l, T_RESID, K.KD_OP_ADD_RMSNORM,
                 ["r"] + ([f"d.{l-1}"] if has_d else []) + [f"g1.{l}"], [f"h1.{l}", "r"],
                 K.kd_attr_add_rmsnorm(m, H, has_d, act, eps, 0))
@@ -225,7 +262,7 @@ class DecoderRuntime:
             for d in self.local_devs:
                 if not self.plan.needs_binding(b, d):
                     continue
-                per_micro = name in ("r", "bt", "sl") or name.startswith(("kc.", "vc."))
+                per_micro = name in ("r", "bt", "sl") or name.startswith(("kc.", "vc.", "conv_st.", "ssm_st."))
                 for i in range(N if per_micro else 1):
                     t = torch.empty(dg.shape[name], dtype=tdt[dg.dtype[name]], device=f"cuda:{self.dev_map[d]}")
                     self._fill(t, name, i, inputs, seed, device_normal_)
@@ -271,6 +308,18 @@ class DecoderRuntime:
             elif base in ("kc", "vc"):
                 src = (inputs.k_cache if base == "kc" else inputs.v_cache)[int(lay)]
                 put_bf16(src[i * m * pps:(i + 1) * m * pps])
+            elif base == "conv_st":
+                put_bf16(inputs.conv_state[int(lay)][i * m:(i + 1) * m])
+            elif base == "ssm_st":
+                t.copy_(torch.from_numpy(inputs.ssm_state[int(lay)][i * m:(i + 1) * m]))
+            elif base in ("dt_bias", "A_log", "Dp"):
+                mw = inputs.layers[int(lay)]
+                t.copy_(torch.from_numpy({"dt_bias": mw.dt_bias, "A_log": mw.A_log, "Dp": mw.D}[base]))
+            elif base in ("w_in", "conv_w", "conv_b", "norm_w", "w_out") or (
+                    base == "g1" and not self.cfg.is_attn_layer(int(lay))):
+                mw = inputs.layers[int(lay)]
+                put_bf16({"w_in": mw.w_in, "conv_w": mw.conv_w, "conv_b": mw.conv_b, "norm_w": mw.norm_w,
+                          "w_out": mw.w_out, "g1": mw.gamma}[base])
             elif base == "w_router":
                 t.copy_(torch.from_numpy(inputs.layers[int(lay)].w_router))
             else:
@@ -292,13 +341,30 @@ class DecoderRuntime:
             t.fill_(cfg.context)
         elif base in ("kc", "vc"):
             device_normal_(t, s, 1.0)
-        elif base in ("g1", "g2"):
+        elif base == "conv_st":
+            device_normal_(t, s, 1.0)
+        elif base == "ssm_st":
+            device_normal_(t, s, 0.1)
+        elif base == "dt_bias":
+            g = torch.Generator(device="cpu")
+            g.manual_seed(s)
+            u = torch.rand(t.shape, generator=g) * (0.1 - 1e-3) + 1e-3
+            t.copy_(torch.log(torch.expm1(u)))
+        elif base == "A_log":
+            g = torch.Generator(device="cpu")
+            g.manual_seed(s)
+            t.copy_(torch.log(torch.rand(t.shape, generator=g) * 15.0 + 1.0))
+        elif base == "Dp":
+            t.fill_(1.0)
+        elif base == "conv_w" or base == "conv_b":
+            device_normal_(t, s, 0.5)
+        elif base in ("g1", "g2", "norm_w"):
             device_normal_(t, s, 0.1)
             t.add_(1.0)
         else:
             K_in = t.shape[-1]
             std = 1.0 / math.sqrt(K_in)
-            if base in ("w_o", "w_d", "w_d_e"):
+            if base in ("w_o", "w_d", "w_d_e", "w_out"):
                 std /= math.sqrt(2.0 * L)
             device_normal_(t, s, std)
 

@@ -45,6 +45,29 @@ class DecoderConfig:
     # MoE (a11); 0 = dense
     n_experts: int = 0
     top_k: int = 2
+    # Mamba-2 hybrid (a12); attn_every = 0 → all layers attention
+    attn_every: int = 0
+    ssm_heads: int = 128
+    ssm_head_dim: int = 64
+    d_state: int = 128
+    ssm_groups: int = 8
+    d_conv: int = 4
+
+    def is_attn_layer(self, l: int) -> bool:
+        """R19: attention at layers l ≡ attn_every−1 (mod attn_every), Mamba-2 elsewhere."""
+        return self.attn_every == 0 or l % self.attn_every == self.attn_every - 1
+
+    @property
+    def d_inner(self) -> int:
+        return self.ssm_heads * self.ssm_head_dim
+
+    @property
+    def conv_channels(self) -> int:
+        return self.d_inner + 2 * self.ssm_groups * self.d_state
+
+    @property
+    def in_proj_dim(self) -> int:
+        return 2 * self.d_inner + 2 * self.ssm_groups * self.d_state + self.ssm_heads
 
     @property
     def group(self) -> int:
@@ -85,7 +108,14 @@ MIXTRAL = DecoderConfig("mixtral-8x7b", hidden=4096, n_heads=32, n_kv_heads=8,
                         context=4096, rope_theta=1e6, n_micro=1, config_index=3,
                         n_experts=8, top_k=2)
 
-CONFIGS = {c.name: c for c in (TINY, LLAMA8B, LLAMA70B, MIXTRAL)}
+HYBRID = DecoderConfig("hybrid-mamba2", hidden=4096, n_heads=32, n_kv_heads=8, head_dim=128, ffn=14336,
+                       n_layers=32, batch=64, context=4096, rope_theta=5e5, n_micro=1, config_index=4,
+                       attn_every=8, ssm_heads=128, ssm_head_dim=64, d_state=128, ssm_groups=8, d_conv=4)
+TINY_HYBRID = DecoderConfig("tiny-hybrid", hidden=256, n_heads=4, n_kv_heads=2, head_dim=64, ffn=512,
+                            n_layers=4, batch=4, context=64, rope_theta=1e4, n_micro=2, config_index=5,
+                            attn_every=2, ssm_heads=8, ssm_head_dim=32, d_state=32, ssm_groups=2, d_conv=4)
+
+CONFIGS = {c.name: c for c in (TINY, LLAMA8B, LLAMA70B, MIXTRAL, HYBRID, TINY_HYBRID)}
 
 
 # --------------------------------------------------------------------------
@@ -148,6 +178,36 @@ class LayerWeights:
 
 
 @dataclass
+class MambaWeights:
+    gamma: np.ndarray    # bf16 bits [H]   pre-norm
+    w_in: np.ndarray     # bf16 bits [2·d_inner + 2·G·N + nheads, H]  rows [z | xBC | dt]
+    conv_w: np.ndarray   # bf16 bits [conv_channels, d_conv]
+    conv_b: np.ndarray   # bf16 bits [conv_channels]
+    dt_bias: np.ndarray  # f32 [nheads]
+    A_log: np.ndarray    # f32 [nheads]
+    D: np.ndarray        # f32 [nheads]
+    norm_w: np.ndarray   # bf16 bits [d_inner]  gated RMSNorm weight
+    w_out: np.ndarray    # bf16 bits [H, d_inner]
+
+
+def make_mamba_weights(g: np.random.Generator, cfg: DecoderConfig) -> MambaWeights:
+    H, di, L = cfg.hidden, cfg.d_inner, cfg.n_layers
+    nh = cfg.ssm_heads
+    u = g.uniform(1e-3, 0.1, nh)
+    return MambaWeights(
+        gamma=f32_to_bf16_bits(1.0 + 0.1 * g.standard_normal(H, dtype=np.float32)),
+        w_in=normal_bf16(g, (cfg.in_proj_dim, H), 1.0 / math.sqrt(H)),
+        conv_w=normal_bf16(g, (cfg.conv_channels, cfg.d_conv), 0.5),
+        conv_b=normal_bf16(g, (cfg.conv_channels,), 0.5),
+        dt_bias=np.log(np.expm1(u)).astype(np.float32),          # softplus⁻¹(U[1e-3, 0.1])
+        A_log=np.log(g.uniform(1.0, 16.0, nh)).astype(np.float32),
+        D=np.ones(nh, np.float32),
+        norm_w=f32_to_bf16_bits(1.0 + 0.1 * g.standard_normal(di, dtype=np.float32)),
+        w_out=normal_bf16(g, (H, di), 1.0 / math.sqrt(2.0 * L) / math.sqrt(di)),
+    )
+
+
+@dataclass
 class DecoderInputs:
     cfg: DecoderConfig
     layers: list
@@ -156,6 +216,8 @@ class DecoderInputs:
     v_cache: list
     block_table: np.ndarray   # int32 [B, pages_per_seq]
     seq_len: np.ndarray       # int32 [B] (= C, R15)
+    conv_state: Optional[list] = None  # per layer (Mamba layers) bf16 bits [B, conv_channels, d_conv-1]
+    ssm_state: Optional[list] = None   # per layer (Mamba layers) f32 [B, nheads, head_dim, d_state]
 
 
 def make_layer_weights(g: np.random.Generator, cfg: DecoderConfig) -> LayerWeights:
@@ -182,16 +244,24 @@ def make_layer_weights(g: np.random.Generator, cfg: DecoderConfig) -> LayerWeigh
 
 def make_decoder_inputs(cfg: DecoderConfig, seed: Optional[int] = None) -> DecoderInputs:
     g = rng(cfg.seed if seed is None else seed)
-    layers = [make_layer_weights(g, cfg) for _ in range(cfg.n_layers)]
+    layers = [make_layer_weights(g, cfg) if cfg.is_attn_layer(l) else make_mamba_weights(g, cfg)
+              for l in range(cfg.n_layers)]
     x = normal_f32(g, (cfg.batch, cfg.hidden))
     pps = cfg.pages_per_seq
     bt = block_table(g, cfg.batch, pps, cfg.n_micro)
     n_pages = cfg.batch * pps
     kshape = (n_pages, cfg.n_kv_heads, cfg.page, cfg.head_dim)
-    kc = [normal_bf16(g, kshape) for _ in range(cfg.n_layers)]
-    vc = [normal_bf16(g, kshape) for _ in range(cfg.n_layers)]
+    kc = [normal_bf16(g, kshape) if cfg.is_attn_layer(l) else None for l in range(cfg.n_layers)]
+    vc = [normal_bf16(g, kshape) if cfg.is_attn_layer(l) else None for l in range(cfg.n_layers)]
     seq_len = np.full(cfg.batch, cfg.context, dtype=np.int32)
-    return DecoderInputs(cfg, layers, x, kc, vc, bt, seq_len)
+    conv = ssm = None
+    if cfg.attn_every:
+        conv = [None if cfg.is_attn_layer(l) else normal_bf16(g, (cfg.batch, cfg.conv_channels, cfg.d_conv - 1))
+                for l in range(cfg.n_layers)]
+        ssm = [None if cfg.is_attn_layer(l) else
+               normal_f32(g, (cfg.batch, cfg.ssm_heads, cfg.ssm_head_dim, cfg.d_state), 0.1)
+               for l in range(cfg.n_layers)]
+    return DecoderInputs(cfg, layers, x, kc, vc, bt, seq_len, conv, ssm)
 
 
 # --------------------------------------------------------------------------
