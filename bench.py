@@ -193,6 +193,17 @@ def main():
         assign = [0] * dg.g.num_kernels
         rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed, use_graph=not args.no_graph)
         placement = "monolithic (all kernels on one B200)"
+    elif cfg.name == "llama3-70b":
+        # BASELINE config 3: GEMMs TP-sharded over N/2 GPUs, attention partners on the
+        # other N/2 (head-sharded); row-parallel partials streamed to every partner by
+        # the GEMM epilogue and reduced in the partners' norms (fused all-reduce, a14)
+        T = world // 2
+        cfg = cfg.with_(n_micro=2)
+        dg = DEC.TPDecoderGraph(cfg, T)
+        rt = DEC.DecoderRuntime(dg, dg.assign(), 2 * T, [local], seed=cfg.seed, use_graph=not args.no_graph,
+                                local_devs=[rank], dist=dist)
+        placement = (f"TP={T}: GEMM ranks {T}..{2 * T - 1}, attention partners 0..{T - 1} (head-sharded), "
+                     f"fused peer-store all-reduce, N=2 micro-batches")
     else:
         # N GPUs: N/2 independent disaggregated pairs (BASELINE config 2: memory-bound
         # kernels on the even rank, GEMMs on the odd rank), each decoding its own batch
@@ -259,7 +270,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    tokens_per_step = cfg.batch * (1 if world == 1 else world // 2)
+    tokens_per_step = cfg.batch * (1 if world == 1 or cfg.name == "llama3-70b" else world // 2)
     value = tokens_per_step / (ms_step / 1e3)
 
     # ---- roofline of the dominant kernel (decode attention)
@@ -292,7 +303,7 @@ def main():
     e2e_value = None
     try:
         me = rt.local_devs[0]
-        r_dev = rt.tensors.get(("r", 0, me))
+        r_dev = rt.tensors.get(("r", 0, me), rt.tensors.get(("r.0", 0, me)))
         if r_dev is None:  # GEMM-role rank: its inputs arrive from the partner
             r_dev = torch.zeros(1, device="cuda")
         bt_dev = rt.tensors.get(("bt", 0, me), torch.zeros(1, dtype=torch.int32, device="cuda"))

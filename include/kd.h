@@ -83,12 +83,12 @@ typedef struct {
 /* op codes: the kernels of the decoder-layer graph */
 enum {
   KD_OP_NONE = 0,          /* bookkeeping node: costs a launch, executes nothing */
-  KD_OP_ADD_RMSNORM = 1,   /* a3  reads [r, delta?, gamma] writes [h, r]          */
+  KD_OP_ADD_RMSNORM = 1,   /* a3  reads [r, delta_0..delta_{n-1}, gamma] writes [h, r] */
   KD_OP_GEMM = 2,          /* a4/a7/a9/a10 reads [X, W] writes [Y]: Y = X·Wᵀ       */
   KD_OP_ROPE_APPEND = 3,   /* a5  reads [qkv, block_table, seq_len] writes [q, Kc, Vc] */
   KD_OP_ATTENTION = 4,     /* a6  reads [q, Kc, Vc, block_table, seq_len] writes [out] */
   KD_OP_SILU_MUL = 5,      /* a8  reads [gu] writes [a]                          */
-  KD_OP_RESIDUAL_ADD = 6,  /* C1.11 reads [r, delta] writes [r]                  */
+  KD_OP_RESIDUAL_ADD = 6,  /* C1.11 reads [r, delta_0..delta_{n-1}] writes [r]   */
   KD_OP_MOE_ROUTE = 7,     /* a11 reads [h, W_router] writes [route]            */
   KD_OP_MOE_DISPATCH = 8,  /* a11 reads [h, route] writes [xg, meta]            */
   KD_OP_GROUPED_GEMM = 9,  /* a11 reads [xg, W_experts, meta] writes [yg]       */
@@ -104,7 +104,11 @@ enum { KD_BF16 = 0, KD_F32 = 1 };
 /* Op attributes (the op's "API signature"). The FIRST write span of
  * every op is its primary output: the only output the runtime may stream to
  * another device (other outputs must stay co-located with their readers). */
-typedef struct { uint32_t rows, hidden, has_delta, dtype; float eps; uint32_t pad_; } kd_attr_add_rmsnorm;
+/* n_delta (0..8) residual deltas are added to r in index order in fp32:
+ * r' = ((r + δ_0) + δ_1) + … — with n_delta > 1 this is the reduction half of
+ * a tensor-parallel all-reduce whose partials were streamed in by the
+ * row-parallel GEMMs' fused peer stores. */
+typedef struct { uint32_t rows, hidden, n_delta, dtype; float eps; uint32_t pad_; } kd_attr_add_rmsnorm;
 typedef struct { uint32_t M, N, K, dtype; } kd_attr_gemm;            /* X [M,K], W [N,K] row-major, Y [M,N] */
 typedef struct {
   uint32_t rows, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype, pad_;
@@ -114,7 +118,7 @@ typedef struct {
   uint32_t rows, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype, pad_;
 } kd_attr_attention;
 typedef struct { uint32_t rows, ffn, dtype, pad_; } kd_attr_silu_mul;  /* gu [rows, 2F] 64-col gate/up blocks */
-typedef struct { uint32_t rows, hidden; } kd_attr_residual_add;       /* r fp32 [rows,H] += delta (act dtype) */
+typedef struct { uint32_t rows, hidden, n_delta, pad_; } kd_attr_residual_add; /* r fp32 [rows,H] += Σ deltas (bf16) */
 /* MoE. route buffer: int32 idx[rows][top_k] then fp32
  * w[rows][top_k]; meta buffer: int32 count[E], offset[E], slot_of[rows][top_k]
  * (grouped row of each (row, choice)), row_of[rows*top_k]; grouped rows are
@@ -317,8 +321,9 @@ kd_status kd_debug_gemm_trace(void* dev_buf);
  * the kd_attr_* comments. `scratch` is a ZERO-initialised device buffer of at
  * least kd_op_scratch_bytes(op, attrs) bytes (left zeroed on return). */
 kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes);
-/* a3: r' = r + delta (fp32, in place; delta may be NULL), h = r'/sqrt(mean r'^2 + eps)·gamma */
-kd_status kd_op_add_rmsnorm(const kd_attr_add_rmsnorm* a, float* r, const void* delta,
+/* a3: r' = r + Σ_i deltas[i] (fp32, in place, index order; deltas is a host array of
+ * n_delta device pointers, may be NULL when n_delta == 0), h = r'/sqrt(mean r'^2 + eps)·gamma */
+kd_status kd_op_add_rmsnorm(const kd_attr_add_rmsnorm* a, float* r, const void* const* deltas,
                             const void* gamma, void* h, void* stream);
 /* a4/a7/a9/a10: Y[M,N] = X[M,K]·W[N,K]ᵀ, bf16 in, fp32 accumulate (tcgen05, TMEM), bf16 out. */
 kd_status kd_op_gemm(const kd_attr_gemm* a, const void* X, const void* W, void* Y,
@@ -333,8 +338,8 @@ kd_status kd_op_attention(const kd_attr_attention* a, const void* q, const void*
                           void* scratch, void* stream);
 /* a8: a[:, 64j+i] = silu(gu[:, 128j+i]) · gu[:, 128j+64+i] */
 kd_status kd_op_silu_mul(const kd_attr_silu_mul* a, const void* gu, void* out, void* stream);
-/* C1.11: r += delta */
-kd_status kd_op_residual_add(const kd_attr_residual_add* a, float* r, const void* delta, void* stream);
+/* C1.11: r += Σ_i deltas[i] (index order) */
+kd_status kd_op_residual_add(const kd_attr_residual_add* a, float* r, const void* const* deltas, void* stream);
 /* a12: conv step: window = [state, x]; xbc = silu(window·w + b); state ← window[1:] (in place) */
 kd_status kd_op_ssm_conv(const kd_attr_ssm* a, const void* zxbcdt, const void* conv_w, const void* conv_b,
                          void* conv_state, void* xbc, void* stream);

@@ -242,8 +242,15 @@ def op_scratch_bytes(op: int, attrs) -> int:
     return v.value
 
 
-def add_rmsnorm(attrs, r, delta, gamma, h, stream=None):
-    check(K.kd_op_add_rmsnorm(C.byref(attrs), _p(r), _p(delta), _p(gamma), _p(h), _stream(stream)), "kd_op_add_rmsnorm")
+def _ptr_array(ts):
+    ts = [] if ts is None else (list(ts) if isinstance(ts, (list, tuple)) else [ts])
+    return (C.c_void_p * max(1, len(ts)))(*[C.c_void_p(t.data_ptr()) for t in ts]), len(ts)
+
+
+def add_rmsnorm(attrs, r, deltas, gamma, h, stream=None):
+    """deltas: None, one tensor, or a list of tensors (attrs.n_delta must match)."""
+    arr, _ = _ptr_array(deltas)
+    check(K.kd_op_add_rmsnorm(C.byref(attrs), _p(r), arr, _p(gamma), _p(h), _stream(stream)), "kd_op_add_rmsnorm")
 
 
 def gemm(attrs, X, W, Y, scratch, stream=None):
@@ -264,5 +271,6 @@ def silu_mul(attrs, gu, out, stream=None):
     check(K.kd_op_silu_mul(C.byref(attrs), _p(gu), _p(out), _stream(stream)), "kd_op_silu_mul")
 
 
-def residual_add(attrs, r, delta, stream=None):
-    check(K.kd_op_residual_add(C.byref(attrs), _p(r), _p(delta), _stream(stream)), "kd_op_residual_add")
+def residual_add(attrs, r, deltas, stream=None):
+    arr, _ = _ptr_array(deltas)
+    check(K.kd_op_residual_add(C.byref(attrs), _p(r), arr, _stream(stream)), "kd_op_residual_add")

@@ -27,8 +27,7 @@ kd_status set_cuda_error(cudaError_t e, const char* where) {
 constexpr int kNormThreads = 256;
 constexpr int kNormChunks = 4;  // H <= 8 * 256 * 4 = 8192
 
-__global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __restrict__ r,
-                                                                  const __nv_bfloat16* __restrict__ delta,
+__global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __restrict__ r, Deltas deltas,
                                                                   const __nv_bfloat16* __restrict__ gamma,
                                                                   __nv_bfloat16* __restrict__ h, int H, float eps,
                                                                   Epi epi) {
@@ -55,12 +54,16 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __rest
       float4 b = reinterpret_cast<const float4*>(rr)[2 * ch + 1];
       v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
       v[c][4] = b.x; v[c][5] = b.y; v[c][6] = b.z; v[c][7] = b.w;
-      if (delta) {
-        uint4 d = reinterpret_cast<const uint4*>(delta + (size_t)row * H)[ch];
-        v[c][0] += bf16lo(d.x); v[c][1] += bf16hi(d.x);
-        v[c][2] += bf16lo(d.y); v[c][3] += bf16hi(d.y);
-        v[c][4] += bf16lo(d.z); v[c][5] += bf16hi(d.z);
-        v[c][6] += bf16lo(d.w); v[c][7] += bf16hi(d.w);
+      if (deltas.n) {
+        uint4 dv[kMaxDeltas];
+        for (int i = 0; i < deltas.n; ++i) dv[i] = reinterpret_cast<const uint4*>(deltas.p[i] + (size_t)row * H)[ch];
+        for (int i = 0; i < deltas.n; ++i) {  // index order: bitwise reproducible
+          const uint4 d = dv[i];
+          v[c][0] += bf16lo(d.x); v[c][1] += bf16hi(d.x);
+          v[c][2] += bf16lo(d.y); v[c][3] += bf16hi(d.y);
+          v[c][4] += bf16lo(d.z); v[c][5] += bf16hi(d.z);
+          v[c][6] += bf16lo(d.w); v[c][7] += bf16hi(d.w);
+        }
         reinterpret_cast<float4*>(rr)[2 * ch] = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
         reinterpret_cast<float4*>(rr)[2 * ch + 1] = make_float4(v[c][4], v[c][5], v[c][6], v[c][7]);
       }
@@ -94,31 +97,35 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __rest
   epi_signal(epi);
 }
 
-kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const void* delta, const void* gamma, void* h,
+kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const Deltas& d, const void* gamma, void* h,
                              const LaunchCtx& c, uint32_t* signals) {
   if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "add_rmsnorm: only bf16 activations");
   if (a.rows == 0 || a.hidden == 0 || a.hidden % 8 || a.hidden > 8 * kNormThreads * kNormChunks)
     return fail(KD_ERR_UNSUPPORTED, "add_rmsnorm: hidden must be a multiple of 8 and <= 8192");
-  if (!r || !gamma || !h || (a.has_delta && !delta)) return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: NULL pointer");
-  KD_CUDA_CHECK(kd_launch(add_rmsnorm_kernel, dim3(a.rows), dim3(kNormThreads), 0, c.stream, r,
-                          a.has_delta ? (const __nv_bfloat16*)delta : nullptr, (const __nv_bfloat16*)gamma,
-                          (__nv_bfloat16*)h, (int)a.hidden, a.eps, c.epi),
+  if (a.n_delta > (uint32_t)kMaxDeltas || (int)a.n_delta != d.n)
+    return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: n_delta must match the deltas given (<= 8)");
+  for (int i = 0; i < d.n; ++i)
+    if (!d.p[i]) return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: NULL delta");
+  if (!r || !gamma || !h) return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: NULL pointer");
+  KD_CUDA_CHECK(kd_launch(add_rmsnorm_kernel, dim3(a.rows), dim3(kNormThreads), 0, c.stream, r, d,
+                          (const __nv_bfloat16*)gamma, (__nv_bfloat16*)h, (int)a.hidden, a.eps, c.epi),
                 "add_rmsnorm launch");
   if (signals) *signals = a.rows;
   return KD_OK;
 }
 
 // ------------------------------------------------------------------ C1.11
-__global__ void residual_add_kernel(float* __restrict__ r, const __nv_bfloat16* __restrict__ d, size_t n8,
-                                    Epi epi) {
+__global__ void residual_add_kernel(float* __restrict__ r, Deltas d, size_t n8, Epi epi) {
   pdl_launch_dependents();
   pdl_wait();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x) {
     float4 a = reinterpret_cast<float4*>(r)[2 * i];
     float4 b = reinterpret_cast<float4*>(r)[2 * i + 1];
-    uint4 x = reinterpret_cast<const uint4*>(d)[i];
-    a.x += bf16lo(x.x); a.y += bf16hi(x.x); a.z += bf16lo(x.y); a.w += bf16hi(x.y);
-    b.x += bf16lo(x.z); b.y += bf16hi(x.z); b.z += bf16lo(x.w); b.w += bf16hi(x.w);
+    for (int k = 0; k < d.n; ++k) {  // index order
+      const uint4 x = reinterpret_cast<const uint4*>(d.p[k])[i];
+      a.x += bf16lo(x.x); a.y += bf16hi(x.x); a.z += bf16lo(x.y); a.w += bf16hi(x.y);
+      b.x += bf16lo(x.z); b.y += bf16hi(x.z); b.z += bf16lo(x.w); b.w += bf16hi(x.w);
+    }
     reinterpret_cast<float4*>(r)[2 * i] = a;
     reinterpret_cast<float4*>(r)[2 * i + 1] = b;
     for (int p = 0; p < epi.n; ++p) {
@@ -134,15 +141,18 @@ static int residual_grid(const kd_attr_residual_add& a) {
   return (int)std::max<size_t>(1, std::min<size_t>((n8 + 255) / 256, 4 * kNumSMs));
 }
 
-kd_status launch_residual_add(const kd_attr_residual_add& a, float* r, const void* delta, const LaunchCtx& c,
+kd_status launch_residual_add(const kd_attr_residual_add& a, float* r, const Deltas& d, const LaunchCtx& c,
                               uint32_t* signals) {
   size_t n = (size_t)a.rows * a.hidden;
   if (n == 0 || a.hidden % 8) return fail(KD_ERR_UNSUPPORTED, "residual_add: hidden must be a multiple of 8");
-  if (!r || !delta) return fail(KD_ERR_INVALID_ARG, "residual_add: NULL pointer");
+  if (a.n_delta == 0 || a.n_delta > (uint32_t)kMaxDeltas || (int)a.n_delta != d.n)
+    return fail(KD_ERR_INVALID_ARG, "residual_add: need 1..8 deltas matching n_delta");
+  for (int i = 0; i < d.n; ++i)
+    if (!d.p[i]) return fail(KD_ERR_INVALID_ARG, "residual_add: NULL delta");
+  if (!r) return fail(KD_ERR_INVALID_ARG, "residual_add: NULL pointer");
   size_t n8 = n / 8;
   int grid = residual_grid(a);
-  KD_CUDA_CHECK(kd_launch(residual_add_kernel, dim3(grid), dim3(256), 0, c.stream, r, (const __nv_bfloat16*)delta,
-                          n8, c.epi),
+  KD_CUDA_CHECK(kd_launch(residual_add_kernel, dim3(grid), dim3(256), 0, c.stream, r, d, n8, c.epi),
                 "residual_add launch");
   if (signals) *signals = grid;
   return KD_OK;

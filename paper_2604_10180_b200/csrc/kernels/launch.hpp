@@ -43,9 +43,14 @@ inline cudaError_t kd_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, si
     if (_e != cudaSuccess) return set_cuda_error(_e, where); \
   } while (0)
 
-kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const void* delta, const void* gamma, void* h,
+constexpr int kMaxDeltas = 8;
+struct Deltas {
+  int n = 0;
+  const __nv_bfloat16* p[kMaxDeltas] = {};
+};
+kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const Deltas& d, const void* gamma, void* h,
                              const LaunchCtx& c, uint32_t* signals);
-kd_status launch_residual_add(const kd_attr_residual_add& a, float* r, const void* delta, const LaunchCtx& c,
+kd_status launch_residual_add(const kd_attr_residual_add& a, float* r, const Deltas& d, const LaunchCtx& c,
                               uint32_t* signals);
 kd_status launch_silu_mul(const kd_attr_silu_mul& a, const void* gu, void* out, const LaunchCtx& c,
                           uint32_t* signals);

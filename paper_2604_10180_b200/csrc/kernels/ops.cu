@@ -63,12 +63,22 @@ kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes) {
   return fail(KD_ERR_INVALID_ARG, "kd_op_scratch_bytes: unknown op");
 }
 
-kd_status kd_op_add_rmsnorm(const kd_attr_add_rmsnorm* a, float* r, const void* delta, const void* gamma, void* h,
-                            void* stream) {
+static kd_status to_deltas(uint32_t n, const void* const* ptrs, Deltas* d) {
+  if (n > (uint32_t)kMaxDeltas || (n && !ptrs)) return fail(KD_ERR_INVALID_ARG, "deltas: bad count or NULL array");
+  d->n = (int)n;
+  for (uint32_t i = 0; i < n; ++i) d->p[i] = (const __nv_bfloat16*)ptrs[i];
+  return KD_OK;
+}
+
+kd_status kd_op_add_rmsnorm(const kd_attr_add_rmsnorm* a, float* r, const void* const* deltas, const void* gamma,
+                            void* h, void* stream) {
   if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_add_rmsnorm: NULL attrs");
+  Deltas d;
+  kd_status s = to_deltas(a->n_delta, deltas, &d);
+  if (s) return s;
   LaunchCtx c;
   c.stream = (cudaStream_t)stream;
-  return launch_add_rmsnorm(*a, r, delta, gamma, h, c, nullptr);
+  return launch_add_rmsnorm(*a, r, d, gamma, h, c, nullptr);
 }
 
 kd_status kd_op_gemm(const kd_attr_gemm* a, const void* X, const void* W, void* Y, void* scratch, void* stream) {
@@ -107,11 +117,14 @@ kd_status kd_op_silu_mul(const kd_attr_silu_mul* a, const void* gu, void* out, v
   return launch_silu_mul(*a, gu, out, c, nullptr);
 }
 
-kd_status kd_op_residual_add(const kd_attr_residual_add* a, float* r, const void* delta, void* stream) {
+kd_status kd_op_residual_add(const kd_attr_residual_add* a, float* r, const void* const* deltas, void* stream) {
   if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_residual_add: NULL attrs");
+  Deltas d;
+  kd_status s = to_deltas(a->n_delta, deltas, &d);
+  if (s) return s;
   LaunchCtx c;
   c.stream = (cudaStream_t)stream;
-  return launch_residual_add(*a, r, delta, c, nullptr);
+  return launch_residual_add(*a, r, d, c, nullptr);
 }
 
 kd_status kd_op_grouped_gemm(const kd_attr_grouped_gemm* a, const void* xg, const void* w_experts, const void* meta,

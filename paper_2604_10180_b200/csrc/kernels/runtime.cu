@@ -102,12 +102,22 @@ kd_status check_attrs(const Kernel& k) {
   size_t nr = k.reads.size(), nw = k.writes.size();
   bool ok = true;
   switch (k.op) {
-    case KD_OP_ADD_RMSNORM: ok = (nr == 2 || nr == 3) && nw == 2; break;
+    case KD_OP_ADD_RMSNORM: {
+      kd_attr_add_rmsnorm a;
+      std::memcpy(&a, k.attrs.data(), sizeof a);
+      ok = a.n_delta <= (uint32_t)kMaxDeltas && nr == 2 + a.n_delta && nw == 2;
+      break;
+    }
     case KD_OP_GEMM: ok = nr == 2 && nw == 1; break;
     case KD_OP_ROPE_APPEND: ok = nr == 3 && nw == 3; break;
     case KD_OP_ATTENTION: ok = nr == 5 && nw == 1; break;
     case KD_OP_SILU_MUL: ok = nr == 1 && nw == 1; break;
-    case KD_OP_RESIDUAL_ADD: ok = nr == 2 && nw == 1; break;
+    case KD_OP_RESIDUAL_ADD: {
+      kd_attr_residual_add a;
+      std::memcpy(&a, k.attrs.data(), sizeof a);
+      ok = a.n_delta >= 1 && a.n_delta <= (uint32_t)kMaxDeltas && nr == 1 + a.n_delta && nw == 1;
+      break;
+    }
     case KD_OP_MOE_ROUTE: ok = nr == 2 && nw == 1; break;
     case KD_OP_MOE_DISPATCH: ok = nr == 2 && nw == 1; break;  // writes [meta | xg]
     case KD_OP_GROUPED_GEMM: ok = nr == 3 && nw == 1; break;  // reads [xg, W, meta]
@@ -144,9 +154,10 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
     case KD_OP_NONE: break;
     case KD_OP_ADD_RMSNORM: {
       auto a = attrs_get<kd_attr_add_rmsnorm>(K);
-      const void* delta = a.has_delta ? l.rd[1] : nullptr;
-      const void* gamma = a.has_delta ? l.rd[2] : l.rd[1];
-      st = launch_add_rmsnorm(a, (float*)l.wr[1], delta, gamma, l.wr[0], c, &sig);
+      Deltas d;
+      d.n = (int)a.n_delta;
+      for (int i = 0; i < d.n; ++i) d.p[i] = (const __nv_bfloat16*)l.rd[1 + i];
+      st = launch_add_rmsnorm(a, (float*)l.wr[1], d, l.rd[1 + a.n_delta], l.wr[0], c, &sig);
       break;
     }
     case KD_OP_GEMM: st = launch_gemm(*l.gemm, l.wr[0], c, &sig); break;
@@ -169,7 +180,10 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
     }
     case KD_OP_RESIDUAL_ADD: {
       auto a = attrs_get<kd_attr_residual_add>(K);
-      st = launch_residual_add(a, (float*)l.wr[0], l.rd[1], c, &sig);
+      Deltas d;
+      d.n = (int)a.n_delta;
+      for (int i = 0; i < d.n; ++i) d.p[i] = (const __nv_bfloat16*)l.rd[1 + i];
+      st = launch_residual_add(a, (float*)l.wr[0], d, c, &sig);
       break;
     }
     case KD_OP_MOE_ROUTE: {

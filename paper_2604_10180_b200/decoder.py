@@ -213,12 +213,152 @@ class DecoderGraph:
                 add("down", l, T_DOWN, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
                     K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)
         add("final_add", L - 1, T_RESID, K.KD_OP_RESIDUAL_ADD, ["r", f"d.{L-1}"], ["r"],
-            K.kd_attr_residual_add(m, H))
+            K.kd_attr_residual_add(m, H, 1, 0))
         g.finalize()
 
     def role_assign(self, mem_dev: int = 0, gemm_dev: int = 1) -> List[int]:
         """Memory-bound kernels on one device, GEMMs on another (BJ config 1/2)."""
         return [mem_dev if k.template in MEMORY_ROLE else gemm_dev for k in self.kernels]
+
+
+class TPDecoderGraph:
+    """Tensor-parallel disaggregated decoder graph (BJ config 3):
+    T GEMM ranks (logical devices T..2T−1) each paired with a memory-role
+    partner (devices 0..T−1) holding 1/T of the kv heads (attention sharded by
+    heads, "pair each TP rank with another GPU"). QKV and gate_up are
+    column-parallel, O and down row-parallel. The TP all-reduce (a14) is fused:
+    every row-parallel GEMM rank streams its fp32-accumulated, bf16-rounded
+    partial into all T partners' landing slots from its epilogue, and each
+    partner's add+RMSNorm sums the T partials in rank order (n_delta = T); the
+    residual stream is replicated (bitwise identical) on the partners.
+    Dense (non-MoE, all-attention) configs only."""
+
+    def __init__(self, cfg, tp: int, act: int = K.KD_BF16):
+        assert cfg.n_experts == 0 and cfg.attn_every == 0, "TP graph: dense attention layers only"
+        T = tp
+        assert cfg.n_kv_heads % T == 0 and cfg.ffn % (64 * T) == 0 and T <= 4
+        self.cfg, self.tp = cfg, T
+        m, H, L = cfg.m, cfg.hidden, cfg.n_layers
+        Hq, Hkv, D, F = cfg.n_heads // T, cfg.n_kv_heads // T, cfg.head_dim, cfg.ffn // T
+        pps = cfg.pages_per_seq
+        qkv_dim = (Hq + 2 * Hkv) * D
+        g = Graph()
+        self.g = g
+        self.buf, self.shape, self.dtype = {}, {}, {}
+        W, PM = K.KD_BUF_WEIGHT, K.KD_BUF_PER_MICROBATCH
+        PERS, INP, OUT = K.KD_BUF_PERSISTENT, K.KD_BUF_INPUT, K.KD_BUF_OUTPUT
+        nb = {"bf16": 2, "f32": 4, "i32": 4}
+
+        def buf(name, shape, dt, flags):
+            self.buf[name] = g.add_buffer(int(np.prod(shape)) * nb[dt], flags)
+            self.shape[name], self.dtype[name] = tuple(shape), dt
+
+        def whole(name):
+            return (self.buf[name], 0, int(np.prod(self.shape[name])) * nb[self.dtype[name]])
+
+        for r in range(T):
+            buf(f"r.{r}", (m, H), "f32", PERS | INP | OUT | PM)
+        buf("bt", (m, pps), "i32", INP | PM)
+        buf("sl", (m,), "i32", INP | PM)
+        for l in range(L):
+            buf(f"g1.{l}", (H,), "bf16", W)
+            buf(f"g2.{l}", (H,), "bf16", W)
+            for r in range(T):
+                buf(f"w_qkv.{l}.{r}", (qkv_dim, H), "bf16", W)
+                buf(f"w_o.{l}.{r}", (H, Hq * D), "bf16", W)
+                buf(f"w_gu.{l}.{r}", (2 * F, H), "bf16", W)
+                buf(f"w_d.{l}.{r}", (H, F), "bf16", W)
+                buf(f"kc.{l}.{r}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+                buf(f"vc.{l}.{r}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+                for nm, shp in (("h1", (m, H)), ("qkv", (m, qkv_dim)), ("q", (m, Hq * D)), ("attn", (m, Hq * D)),
+                                ("o", (m, H)), ("h2", (m, H)), ("gu", (m, 2 * F)), ("a", (m, F)), ("d", (m, H))):
+                    buf(f"{nm}.{l}.{r}", shp, "bf16", PM)
+        self.kernels: List[KernelInfo] = []
+        self.dev_of: List[int] = []
+
+        def add(name, layer, r, mem, op, reads, writes, attrs, flops=0):
+            kid = g.add_kernel(op, [whole(x) for x in reads], [whole(x) for x in writes], attrs, flops, -1, -1)
+            self.kernels.append(KernelInfo(f"{name}.{r}", layer, -1, kid))
+            self.dev_of.append(r if mem else T + r)
+
+        eps = float(cfg.eps)
+        for l in range(L):
+            nd = T if l > 0 else 0
+            for r in range(T):
+                add("norm1", l, r, True, K.KD_OP_ADD_RMSNORM,
+                    [f"r.{r}"] + [f"d.{l-1}.{s}" for s in range(nd)] + [f"g1.{l}"], [f"h1.{l}.{r}", f"r.{r}"],
+                    K.kd_attr_add_rmsnorm(m, H, nd, act, eps, 0))
+            for r in range(T):
+                add("qkv", l, r, False, K.KD_OP_GEMM, [f"h1.{l}.{r}", f"w_qkv.{l}.{r}"], [f"qkv.{l}.{r}"],
+                    K.kd_attr_gemm(m, qkv_dim, H, act), 2 * m * qkv_dim * H)
+            for r in range(T):
+                add("rope", l, r, True, K.KD_OP_ROPE_APPEND, [f"qkv.{l}.{r}", "bt", "sl"],
+                    [f"q.{l}.{r}", f"kc.{l}.{r}", f"vc.{l}.{r}"],
+                    K.kd_attr_rope_append(m, Hq, Hkv, D, cfg.page, pps, act, 0, float(cfg.rope_theta)))
+                add("attn", l, r, True, K.KD_OP_ATTENTION, [f"q.{l}.{r}", f"kc.{l}.{r}", f"vc.{l}.{r}", "bt", "sl"],
+                    [f"attn.{l}.{r}"], K.kd_attr_attention(m, Hq, Hkv, D, cfg.page, pps, act, 0),
+                    4 * m * Hq * cfg.context * D)
+            for r in range(T):
+                add("o", l, r, False, K.KD_OP_GEMM, [f"attn.{l}.{r}", f"w_o.{l}.{r}"], [f"o.{l}.{r}"],
+                    K.kd_attr_gemm(m, H, Hq * D, act), 2 * m * H * Hq * D)
+            for r in range(T):
+                add("norm2", l, r, True, K.KD_OP_ADD_RMSNORM,
+                    [f"r.{r}"] + [f"o.{l}.{s}" for s in range(T)] + [f"g2.{l}"], [f"h2.{l}.{r}", f"r.{r}"],
+                    K.kd_attr_add_rmsnorm(m, H, T, act, eps, 0))
+            for r in range(T):
+                add("gu", l, r, False, K.KD_OP_GEMM, [f"h2.{l}.{r}", f"w_gu.{l}.{r}"], [f"gu.{l}.{r}"],
+                    K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
+            for r in range(T):
+                add("silu", l, r, True, K.KD_OP_SILU_MUL, [f"gu.{l}.{r}"], [f"a.{l}.{r}"],
+                    K.kd_attr_silu_mul(m, F, act, 0))
+            for r in range(T):
+                add("down", l, r, False, K.KD_OP_GEMM, [f"a.{l}.{r}", f"w_d.{l}.{r}"], [f"d.{l}.{r}"],
+                    K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)
+        for r in range(T):
+            add("final_add", L - 1, r, True, K.KD_OP_RESIDUAL_ADD, [f"r.{r}"] + [f"d.{L-1}.{s}" for s in range(T)],
+                [f"r.{r}"], K.kd_attr_residual_add(m, H, T, 0))
+        g.finalize()
+
+    def assign(self) -> List[int]:
+        """Partners 0..T−1 (memory role), GEMM ranks T..2T−1."""
+        return list(self.dev_of)
+
+    def host_value(self, name, i, inputs):
+        """Host bf16 bits / fp32 array for buffer `name`, micro-batch i: the
+        unsharded synthetic model sliced into this shard."""
+        cfg, T = self.cfg, self.tp
+        m, pps = cfg.m, cfg.pages_per_seq
+        parts = name.split(".")
+        base = parts[0]
+        if base == "r":
+            return inputs.x[i * m:(i + 1) * m]
+        if base == "bt":
+            return inputs.block_table[i * m:(i + 1) * m] - i * m * pps
+        if base == "sl":
+            return inputs.seq_len[i * m:(i + 1) * m]
+        l = int(parts[1])
+        lw = inputs.layers[l]
+        if base in ("g1", "g2"):
+            return lw.gamma1 if base == "g1" else lw.gamma2
+        r = int(parts[2])
+        Hkv, G, D = cfg.n_kv_heads, cfg.group, cfg.head_dim
+        hs = Hkv // T
+        if base == "w_qkv":
+            rows = (G + 2) * D
+            return lw.w_qkv[r * hs * rows:(r + 1) * hs * rows]
+        if base == "w_o":
+            c = cfg.n_heads * D // T
+            return lw.w_o[:, r * c:(r + 1) * c]
+        if base == "w_gu":
+            n = 2 * cfg.ffn // T
+            return lw.w_gu[r * n:(r + 1) * n]
+        if base == "w_d":
+            n = cfg.ffn // T
+            return lw.w_d[:, r * n:(r + 1) * n]
+        if base in ("kc", "vc"):
+            src = (inputs.k_cache if base == "kc" else inputs.v_cache)[l]
+            return src[i * m * pps:(i + 1) * m * pps, r * hs:(r + 1) * hs]
+        raise KeyError(name)
 
 
 def _torch():
@@ -262,7 +402,7 @@ class DecoderRuntime:
             for d in self.local_devs:
                 if not self.plan.needs_binding(b, d):
                     continue
-                per_micro = name in ("r", "bt", "sl") or name.startswith(("kc.", "vc.", "conv_st.", "ssm_st."))
+                per_micro = name in ("r", "bt", "sl") or name.startswith(("kc.", "vc.", "conv_st.", "ssm_st.", "r."))
                 for i in range(N if per_micro else 1):
                     t = torch.empty(dg.shape[name], dtype=tdt[dg.dtype[name]], device=f"cuda:{self.dev_map[d]}")
                     self._fill(t, name, i, inputs, seed, device_normal_)
@@ -293,6 +433,15 @@ class DecoderRuntime:
     def _fill(self, t, name, i, inputs, seed, device_normal_):
         torch = _torch()
         cfg = self.cfg
+        if hasattr(self.dg, "host_value"):
+            if inputs is not None:
+                v = np.ascontiguousarray(self.dg.host_value(name, i, inputs))
+                if v.dtype == np.uint16:
+                    t.copy_(torch.from_numpy(v.view(np.int16)).view(torch.bfloat16))
+                else:
+                    t.copy_(torch.from_numpy(v))
+                return
+            name = ".".join(name.split(".")[:2]) if name.split(".")[0] not in ("r",) else "r"
         m, pps = cfg.m, cfg.pages_per_seq
         base, _, lay = name.partition(".")
         L = cfg.n_layers
@@ -380,10 +529,11 @@ class DecoderRuntime:
     def residual(self) -> np.ndarray:
         """Concatenated residual stream r [B, H] (fp32) after the last step."""
         outs = []
+        rname = "r.0" if hasattr(self.dg, "host_value") else "r"
         for i in range(self.cfg.n_micro):
             for d in self.local_devs:
-                if ("r", i, d) in self.tensors:
-                    outs.append(self.tensors[("r", i, d)].cpu().numpy())
+                if (rname, i, d) in self.tensors:
+                    outs.append(self.tensors[(rname, i, d)].cpu().numpy())
                     break
         return np.concatenate(outs, axis=0)
 

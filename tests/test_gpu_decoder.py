@@ -127,3 +127,28 @@ def test_moe_decoder_monolithic_vs_oracle_and_disaggregated_bitwise(mod):
     assert relerr(mono.residual(), r_ref) < 2e-2
     dis = run(DEC, cfg, inp, lambda dg: dg.role_assign(0, 1), 2)
     assert np.array_equal(mono.residual(), dis.residual())
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tp_pairs_fused_allreduce_vs_oracle_and_bitwise(mod, tp):
+    """a14: T GEMM ranks + T memory partners (head-sharded attention). The
+    row-parallel partials are streamed to every partner by the GEMM epilogue
+    and reduced in the partners' norms (n_delta = T). TP-sharded math vs the
+    unsharded oracle (tolerance: only rounding differs), and the T×2-device
+    loopback run bitwise equal to the same sharded kernels on one device."""
+    DEC, K = mod
+    cfg = synth.TINY.with_(n_kv_heads=4, n_micro=2)
+    inp = synth.make_decoder_inputs(cfg)
+    dg = DEC.TPDecoderGraph(cfg, tp)
+    mono = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp)
+    mono.step()
+    mono.sync()
+    r_ref, _, _ = OL.decoder_step(inp, act="bf16")
+    assert relerr(mono.residual(), r_ref) < 2e-2
+    dg2 = DEC.TPDecoderGraph(cfg, tp)
+    dis = DEC.DecoderRuntime(dg2, dg2.assign(), 2 * tp, [0] * (2 * tp), inputs=inp)
+    for _ in range(1):
+        dis.step()
+    dis.sync()
+    dis.rt.check()
+    assert np.array_equal(mono.residual(), dis.residual())

@@ -206,6 +206,33 @@ def test_residual_add(kd):
     r = synth.normal_f32(g, (3, 4096))
     d = synth.normal_bf16(g, (3, 4096))
     rt = torch.from_numpy(r).cuda()
-    api.residual_add(K.kd_attr_residual_add(3, 4096), rt, dev_bf16(d))
+    api.residual_add(K.kd_attr_residual_add(3, 4096, 1, 0), rt, dev_bf16(d))
     torch.cuda.synchronize()
     assert np.array_equal(host_f64(rt), OL.residual_add(r, OL.bf16_to_f64(d)))
+
+
+def test_add_rmsnorm_multi_delta_is_tp_reduction(kd):
+    """n_delta = 4: r' = (((r + δ0) + δ1) + δ2) + δ3 in fp32 (index order), the
+    reduction half of the fused TP all-reduce (a14)."""
+    api, K = kd
+    torch = _torch()
+    rows, H, n = 5, 4096, 4
+    g = synth.rng(77)
+    r = synth.normal_f32(g, (rows, H))
+    ds = [synth.normal_bf16(g, (rows, H)) for _ in range(n)]
+    gam = synth.f32_to_bf16_bits(1 + 0.1 * g.standard_normal(H, dtype=np.float32))
+    r_t = torch.from_numpy(r).cuda()
+    h_t = torch.empty(rows, H, dtype=torch.bfloat16, device="cuda")
+    dts = [dev_bf16(d) for d in ds]
+    api.add_rmsnorm(K.kd_attr_add_rmsnorm(rows, H, n, K.KD_BF16, 1e-5, 0), r_t, dts, dev_bf16(gam), h_t)
+    torch.cuda.synchronize()
+    acc = r.copy()
+    for d in ds:                                   # fp32 sequential adds, index order
+        acc = (acc + OL.bf16_to_f64(d).astype(np.float32)).astype(np.float32)
+    assert np.array_equal(r_t.cpu().numpy(), acc)
+    _, h_ref = OL.add_rmsnorm(r, sum(OL.bf16_to_f64(d) for d in ds), OL.bf16_to_f64(gam), 1e-5, "bf16")
+    assert relerr(host_f64(h_t), h_ref) < 5e-3
+    rr = torch.from_numpy(r).cuda()
+    api.residual_add(K.kd_attr_residual_add(rows, H, n, 0), rr, dts)
+    torch.cuda.synchronize()
+    assert np.array_equal(rr.cpu().numpy(), acc)
