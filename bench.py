@@ -247,6 +247,35 @@ def main():
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
     rt.rt.check()
+    # exposed transfer (N>1): same plan and schedule with the peer stores and
+    # flag waits removed (KD_MODE_NO_TRANSFER; consumers read their landing
+    # slots as left by the previous steps) — exposed = T(DISAGG) − T(NO_TRANSFER)
+    exposed = None
+    if world > 1:
+        rt.rt.set_mode(K.KD_MODE_NO_TRANSFER)
+        rt.rt.prepare()
+        for _ in range(2):
+            rt.step()
+        torch.cuda.synchronize()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            rt.step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_nt = f0.elapsed_time(f1)
+        if dist is not None:
+            t = torch.tensor([ms_nt], device="cpu" if os.environ.get("KD_BENCH_ONE_GPU") else "cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_nt = float(t.item())
+        exposed = {"ms_per_step": round(ms / args.steps - ms_nt / args.steps, 4),
+                   "no_transfer_ms_per_step": round(ms_nt / args.steps, 4),
+                   "fraction_of_step": round(1 - ms_nt / ms, 4)}
+        rt.rt.set_mode(K.KD_MODE_DISAGG)
+        rt.rt.prepare()
     # per-kernel CUDA-event timing: a second pass of the same K steps whose
     # graph carries event-record nodes around every attention launch (events
     # split programmatic launch edges, so they are kept out of the headline)
@@ -359,6 +388,7 @@ def main():
             "e2e": {"value": round(e2e_value, 1) if e2e_value else None, "unit": "tokens/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": n_launch * args.steps,
+            "exposed_transfer": exposed,
             "clocks": clk}
     if kernels:
         line["kernels"] = kernels
