@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkd.so")
+LIB_PATH = os.environ.get("KD_LIB") or os.path.join(_HERE, "libkd.so")  # KD_LIB: A/B experiments
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2604_10180_b200.build` "

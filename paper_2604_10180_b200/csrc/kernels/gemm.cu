@@ -491,18 +491,46 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-static kd_status encode(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_rows) {
-  EncodeTiledFn fn = get_encode();
-  if (!fn) return fail(KD_ERR_CUDA, "gemm: cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+}  // namespace gemm
+
+kd_status encode_bf16_2d_sw128(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                               uint32_t box_rows) {
+  gemm::EncodeTiledFn fn = gemm::get_encode();
+  if (!fn) return fail(KD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {inner * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+  cuuint32_t box[2] = {box_inner, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(KD_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  if (r != CUDA_SUCCESS) return fail(KD_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return KD_OK;
+}
+
+kd_status encode_bf16_sw128(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims,
+                            const uint64_t* strides_bytes, const uint32_t* box) {
+  gemm::EncodeTiledFn fn = gemm::get_encode();
+  if (!fn) return fail(KD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i) st[i - 1] = strides_bytes[i - 1];
+  }
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), d, st, b, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(KD_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return KD_OK;
+}
+
+namespace gemm {
+
+static kd_status encode(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_rows) {
+  return encode_bf16_2d_sw128(map, ptr, inner, outer, (uint32_t)kBK, box_rows);
 }
 
 struct Geometry {
