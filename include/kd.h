@@ -315,6 +315,15 @@ kd_status kd_set_pdl(int32_t enable);
  * dev_buf[cta*32 + slot] (u64, >= 148*32 entries). NULL disables (default). */
 kd_status kd_debug_gemm_trace(void* dev_buf);
 
+/* Tiling the library picks for a plain decode GEMM Y[M,N] = X[M,K]·W[N,K]ᵀ on
+ * the current device (a4/a7/a9/a10): out[0] = kernel (1 = dense tokens-as-rows
+ * cluster split-K, 0 = stream-K), out[1] = split (cluster size), out[2] = n_t
+ * (output columns per tile), out[3] = tiles, out[4] = pipeline stages,
+ * out[5] = dynamic smem bytes. Needs a CUDA device (queries co-resident
+ * clusters). Environment overrides for tuning: KD_GEMM_TILE="split,n_t",
+ * KD_GEMM_STREAMK=1. Errors: KD_ERR_INVALID_ARG (NULL), KD_ERR_UNSUPPORTED. */
+kd_status kd_gemm_tiling(uint32_t M, uint32_t N, uint32_t K, int32_t* out6);
+
 /* ------------------------------------------------------------------ single ops
  * Direct entry points to the device kernels the runtime launches (for parity
  * tests and micro-benchmarks). Pointers are device pointers; layouts as in

@@ -169,6 +169,7 @@ _PROTOS = {
     "kd_ipc_open": (kd_status, [P, u64, C.POINTER(P)]),
     "kd_ipc_close": (kd_status, [P]),
     "kd_debug_gemm_trace": (kd_status, [P]),
+    "kd_gemm_tiling": (kd_status, [u32, u32, u32, C.POINTER(C.c_int32)]),
     "kd_set_pdl": (kd_status, [i32]),
     "kd_op_scratch_bytes": (kd_status, [u32, P, PU64]),
     "kd_moe_meta_bytes": (kd_status, [u32, u32, u32, PU64]),

@@ -19,9 +19,12 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <vector>
 
 #include "launch.hpp"
+#include "tcgen05.cuh"
 
 namespace kd {
 namespace gemm {
@@ -39,6 +42,10 @@ struct Args {
   float* part;       // [tiles][max_contrib][M][128]
   unsigned* counter; // [tiles]
   int M, N, K, mma_n, stages, kblocks, tiles, max_contrib;
+  int kbs;           // 64-column boxes per pipeline stage (k-block = 64·kbs columns)
+  int split_tiles;   // any tile cut between CTAs
+  int fold_grid;     // split tiles folded after a grid barrier by all CTAs (many
+                     // contributors per tile) instead of by their last arriver
   long long units;
   Epi epi;
   unsigned long long* trace;  // debug: 32 %globaltimer stamps per CTA (nullable)
@@ -49,110 +56,15 @@ struct Args {
   int dbg;                    // debug A/B knob (KD_GEMM_DBG): 1 skip owner Y stores, 2 skip owner fold
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 #define KD_TRACE(slot) \
   do {                 \
     if (A.trace) A.trace[blockIdx.x * 32 + (slot)] = gtimer(); \
   } while (0)
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "W_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra W_%=;\n\t}" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
-                                            uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-// K-major operand tile in smem, 128-byte swizzle: 8-row atoms of 1024 B (SBO),
-// descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
-      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
-      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
-      : "memory");
-}
-__device__ __forceinline__ float4 lds128(uint32_t saddr) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
-  return v;
-}
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+// cycle-resolution stamps (clock64) into slots 16..31 (csk epilogue sub-phases)
+#define KD_CTRACE(slot) \
+  do {                 \
+    if (A.trace) A.trace[blockIdx.x * 32 + (slot)] = (unsigned long long)clock64(); \
+  } while (0)
 
 // unit range of CTA c: [c·U/G, (c+1)·U/G); owner of unit u: ⌈(u+1)·G/U⌉ − 1
 __host__ __device__ __forceinline__ long long unit_begin(long long c, long long U, long long G) { return c * U / G; }
@@ -161,19 +73,21 @@ __host__ __device__ __forceinline__ long long unit_owner(long long u, long long 
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, Args A) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Args A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const int S = A.stages;
-  const int stage_b = A.mma_n * kBK * 2;
-  uint8_t* sa = smem;                          // S × 16 KB
-  uint8_t* sb = smem + (size_t)S * kStageA;    // S × mma_n·128 B
-  uint64_t* full = (uint64_t*)(sb + (size_t)S * stage_b);
+  const int S = A.stages, kbs = A.kbs;
+  const int xbox = A.mma_n * kBK * 2;          // one 64-column X box
+  const int wst = kbs * kStageA, xst = kbs * xbox;
+  uint8_t* sa = smem;                          // S × kbs × 16 KB (W)
+  uint8_t* sb = smem + (size_t)S * wst;        // S × kbs × mma_n·128 B (X)
+  uint64_t* full = (uint64_t*)(sb + (size_t)S * xst);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;        // [2]
   uint64_t* tempty = tfull + 2;                // [2]
-  uint64_t* fixbar = tempty + 2;               // owner's partial bulk loads
+  uint64_t* fixbar = tempty + 2;               // last arriver's bulk loads of the partials
   uint32_t* tmem_slot = (uint32_t*)(fixbar + 1);
+  volatile unsigned* s_flag = (volatile unsigned*)(tmem_slot + 1);
   __nv_bfloat16* ystage = (__nv_bfloat16*)(fixbar + 2);  // 2 x [16][128] bf16 epilogue transpose
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -209,88 +123,98 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) KD_TRACE(1);
 
+  auto w_row = [&](int t) { return A.groups ? (t / A.tpg) * A.N + (t % A.tpg) * kBM : t * kBM; };
   if (warp == 0) {
-    // ------------------------------------------------ TMA producer
+    // ------------------------------------------------ TMA producer (warp-uniform loop, lane 0 issues)
+    const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+    const unsigned tx = (unsigned)(wst + xst);
+    const long long n_pre = std::min<long long>(S, u1 - u0);
+    auto load_w = [&](long long u, int s) {
+      const int t = (int)(u / KB), kb = (int)(u % KB);
+      for (int b = 0; b < kbs; ++b)
+        tma_load_2d(sa + (size_t)s * wst + b * kStageA, &tmap_w, (kb * kbs + b) * kBK, w_row(t), &full[s], pw);
+    };
+    auto load_x = [&](long long u, int s) {
+      const int t = (int)(u / KB), kb = (int)(u % KB);
+      const int xr = A.groups ? __ldg(A.meta + A.groups + t / A.tpg) : 0;
+      for (int b = 0; b < kbs; ++b)
+        tma_load_2d(sb + (size_t)s * xst + b * xbox, &tmap_x, (kb * kbs + b) * kBK, xr, &full[s], px);
+    };
     if (lane == 0) {
-      const uint64_t pw = policy_evict_first(), px = policy_evict_last();
-      const unsigned tx = kStageA + stage_b;
       // weights never depend on the previous kernel: fill the first ring of W
       // tiles before the grid-dependency wait (overlaps the previous kernel's
       // tail), then the activations of those stages, then steady state
-      const long long n_pre = std::min<long long>(S, u1 - u0);
-      auto w_row = [&](int t) { return A.groups ? (t / A.tpg) * A.N + (t % A.tpg) * kBM : t * kBM; };
       for (long long i = 0; i < n_pre; ++i) {
-        const long long u = u0 + i;
-        const int t = (int)(u / KB), kb = (int)(u % KB);
         mbar_expect_tx(&full[i], tx);
-        tma_load_2d(sa + (size_t)i * kStageA, &tmap_w, kb * kBK, w_row(t), &full[i], pw);
-        if (i == 0) KD_TRACE(2);
+        load_w(u0 + i, (int)i);
       }
+      KD_TRACE(2);
       pdl_wait();
-      auto x_row = [&](int t) { return A.groups ? __ldg(A.meta + A.groups + t / A.tpg) : 0; };
-      for (long long i = 0; i < n_pre; ++i) {
-        const long long u = u0 + i;
-        tma_load_2d(sb + (size_t)i * stage_b, &tmap_x, (int)(u % KB) * kBK, x_row((int)(u / KB)), &full[i], px);
-      }
-      long long i = n_pre;
-      for (long long u = u0 + n_pre; u < u1; ++u, ++i) {
-        const int s = (int)(i % S);
-        const long long r = i / S;
-        if (r > 0) mbar_wait(&empty[s], (unsigned)((r - 1) & 1));
-        const int t = (int)(u / KB), kb = (int)(u % KB);
-        mbar_expect_tx(&full[s], tx);
-        tma_load_2d(sa + (size_t)s * kStageA, &tmap_w, kb * kBK, w_row(t), &full[s], pw);
-        tma_load_2d(sb + (size_t)s * stage_b, &tmap_x, kb * kBK, x_row(t), &full[s], px);
-      }
-      KD_TRACE(3);
+      for (long long i = 0; i < n_pre; ++i) load_x(u0 + i, (int)i);
     }
+    __syncwarp();
+    long long i = n_pre;
+    for (long long u = u0 + n_pre; u < u1; ++u, ++i) {
+      const int s = (int)(i % S);
+      mbar_wait(&empty[s], (unsigned)(((i / S) - 1) & 1));
+      if (lane == 0) {
+        mbar_expect_tx(&full[s], tx);
+        load_w(u, s);
+        load_x(u, s);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) KD_TRACE(3);
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      pdl_wait();
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(A.mma_n >> 3) << 17) |
-                             ((uint32_t)(kBM >> 4) << 24);
-      long long i = 0;
-      int seg = 0;
-      long long u = u0;
-      while (u < u1) {
-        const int t = (int)(u / KB);
-        const long long seg_end = std::min<long long>(u1, (long long)(t + 1) * KB);
-        const int a = seg & 1, use = seg >> 1;
-        if (use > 0) mbar_wait(&tempty[a], (unsigned)((use - 1) & 1));
+    // ------------------------------------------------ MMA issuer (warp-uniform loop, lane 0 issues)
+    if (lane == 0) pdl_wait();
+    __syncwarp();
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(A.mma_n >> 3) << 17) |
+                           ((uint32_t)(kBM >> 4) << 24);
+    long long i = 0;
+    int seg = 0;
+    long long u = u0;
+    while (u < u1) {
+      const int t = (int)(u / KB);
+      const long long seg_end = std::min<long long>(u1, (long long)(t + 1) * KB);
+      const int a = seg & 1, use = seg >> 1;
+      if (use > 0) mbar_wait(&tempty[a], (unsigned)((use - 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tmem_d = tmem_base + (uint32_t)(a * A.mma_n);
+      bool first = true;
+      for (; u < seg_end; ++u, ++i) {
+        const int s = (int)(i % S);
+        mbar_wait(&full[s], (unsigned)((i / S) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t tmem_d = tmem_base + (uint32_t)(a * A.mma_n);
-        bool first = true;
-        for (; u < seg_end; ++u, ++i) {
-          const int s = (int)(i % S);
-          mbar_wait(&full[s], (unsigned)((i / S) & 1));
+        if (lane == 0) {
           if (i == 0) KD_TRACE(4);
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t a_addr = smem_u32(sa + (size_t)s * kStageA);
-          const uint32_t b_addr = smem_u32(sb + (size_t)s * stage_b);
+          const uint32_t a_addr = smem_u32(sa + (size_t)s * wst);
+          const uint32_t b_addr = smem_u32(sb + (size_t)s * xst);
+          for (int b = 0; b < kbs; ++b)
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            // advance 16 bf16 = 32 B inside the 128 B swizzle row
-            mma_bf16(tmem_d, sw128_desc(a_addr + 32 * k), sw128_desc(b_addr + 32 * k), idesc,
-                     (first && k == 0) ? 0u : 1u);
-          }
-          first = false;
+            for (int k = 0; k < kBK / 16; ++k)
+              // advance 16 bf16 = 32 B inside the 128 B swizzle row
+              mma_bf16(tmem_d, sw128_desc(a_addr + b * kStageA + 32 * k), sw128_desc(b_addr + b * xbox + 32 * k), idesc,
+                       (first && b == 0 && k == 0) ? 0u : 1u);
           mma_commit(&empty[s]);  // smem stage free once these MMAs retire
         }
-        mma_commit(&tfull[a]);    // accumulator ready for the epilogue
-        ++seg;
+        __syncwarp();
+        first = false;
       }
-      KD_TRACE(5);
+      if (lane == 0) mma_commit(&tfull[a]);  // accumulator ready for the epilogue
+      __syncwarp();
+      ++seg;
     }
+    if (lane == 0) KD_TRACE(5);
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue (TMEM → HBM / peers)
-    // Split tiles (stream-K): every contributor c of tile t publishes its fp32
-    // partial [M][128] to slot (c - first contributor), release-increments
-    // arrive[t], waits until all n_contrib partials are published, then folds
-    // ITS 1/n slice of the tile (fixed contributor order → bitwise
-    // deterministic) and stores it. depart[t] lets the last leaver reset both
-    // counters for the next launch. Contributors only wait for partials that
-    // are published before anyone waits, so this cannot deadlock.
+    // Whole tiles are stored straight from TMEM. A split tile's contributors
+    // each publish their fp32 partial [M][128] (slot = contributor − first
+    // contributor); after a grid-wide barrier every CTA folds an equal slice
+    // of all split tiles, summing the partials in contributor order (bitwise
+    // deterministic). A single CTA folding a whole tile was measured at
+    // ≈5 µs (one SM reads ≈40-60 GB/s); spread over the grid the fold is
+    // ≈32 KB per CTA. Every CTA releases the consumer flags once, at the end.
     const int q = warp - 4;                 // TMEM lane quarter
     const int row_in_tile = q * 32 + lane;  // output feature within the tile
     const int ep_tid = threadIdx.x - 128;
@@ -298,122 +222,87 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_wait();  // scratch and Y may still be in use by the previous kernel
     int seg = 0;
     long long u = u0;
+    auto out_coords = [&](int t, int* nb0, int* y0, int* mv) {
+      const int grp = A.groups ? t / A.tpg : 0;
+      *nb0 = (A.groups ? t % A.tpg : t) * kBM;
+      *y0 = A.groups ? __ldg(A.meta + A.groups + grp) : 0;
+      *mv = A.groups ? min(__ldg(A.meta + grp), A.M) : A.M;
+    };
     while (u < u1) {
       const int t = (int)(u / KB);
       const long long t_begin = (long long)t * KB, t_end = t_begin + KB;
       const long long seg_end = std::min<long long>(u1, t_end);
       const bool whole = (u == t_begin && seg_end == t_end);
       const int a = seg & 1;
-      mbar_wait(&tfull[a], (unsigned)((seg >> 1) & 1));
+      mbar_wait_sleep(&tfull[a], (unsigned)((seg >> 1) & 1), 128);
       if (ep_tid == 0 && seg < 3) KD_TRACE(6 + 2 * seg);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * A.mma_n);
-      // output coordinates of tile t: column base nb0, row base y0, valid rows mv
-      const int grp = A.groups ? t / A.tpg : 0;
-      const int nb0 = (A.groups ? t % A.tpg : t) * kBM;
-      const int y0 = A.groups ? __ldg(A.meta + A.groups + grp) : 0;
-      const int mv = A.groups ? min(__ldg(A.meta + grp), A.M) : A.M;
+      int nb0, y0, mv;
+      out_coords(t, &nb0, &y0, &mv);
       if (!whole) {
         const long long first = unit_owner(t_begin, U, G);
-        const long long lastc = unit_owner(t_end - 1, U, G);
-        const int n_contrib = (int)(lastc - first + 1);
-        const int my_idx = (int)(c - first);
-        // participants fold: contributors for which this tile is their LAST
-        // segment. Only the last contributor can have more work after this
-        // tile (a "tail" part at the start of its range); it publishes only.
-        const bool tail_exists = unit_begin(lastc + 1, U, G) > t_end;
-        const int n_part = n_contrib - (tail_exists ? 1 : 0);
-        const bool participant = (seg_end == u1);
-        const float* parts = A.part + (size_t)t * A.max_contrib * part_elems;
-        float* my_part = A.part + ((size_t)t * A.max_contrib + my_idx) * part_elems;
+        float* my_part = A.part + ((size_t)t * A.max_contrib + (c - first)) * part_elems;
         for (int j0 = 0; j0 < A.M; j0 += kChunk) {
           float v[kChunk];
           tmem_ld16(tbase + j0, v);
 #pragma unroll
           for (int j = 0; j < kChunk; ++j)
-            if (j0 + j < A.M) my_part[(size_t)(j0 + j) * kBM + row_in_tile] = v[j];
+            if (j0 + j < A.M) __stcg(my_part + (size_t)(j0 + j) * kBM + row_in_tile, v[j]);
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[a]);
-        named_bar(1, 128);
-        unsigned* arrive = A.counter + 2 * t;
-        unsigned* depart = arrive + 1;
-        if (ep_tid == 0) {
-          KD_TRACE(18);
-          fence_acq_rel_gpu();
-          atom_add_acq_rel_gpu(arrive, 1u);
-          if (participant) {
-            long long spins = 0;
-            while (ld_acquire_gpu(arrive) < (unsigned)n_contrib)
-              if (++spins > 64) __nanosleep(32);
-            KD_TRACE(16);
-            if (atom_add_acq_rel_gpu(depart, 1u) == (unsigned)n_part - 1) {
-              *arrive = 0u;  // every participant has left the wait: reset for the next launch
-              *depart = 0u;
-            }
+        if (!A.fold_grid) {
+          // few contributors per tile: the LAST to arrive folds the tile alone
+          // (contributor order → deterministic) and resets the counter
+          const long long lastc = unit_owner(t_end - 1, U, G);
+          const int n_contrib = (int)(lastc - first + 1);
+          unsigned* arrive = A.counter + 2 + t;
+          named_bar(1, 128);
+          if (ep_tid == 0) {
+            fence_acq_rel_gpu();
+            s_flag[0] = atom_add_acq_rel_gpu(arrive, 1u);
           }
-        }
-        named_bar(1, 128);
-        // fold my slice: float4 elements [e0, e1) of the [M][128] tile
-        const int n4 = participant ? (int)(part_elems / 4) : 0;
-        const int e0 = (int)((long long)n4 * my_idx / n_part), e1 = (int)((long long)n4 * (my_idx + 1) / n_part);
-        // 4 elements per thread per round: all (element, contributor) loads of a
-        // round are in flight together (memory-level parallelism for the L2 reads)
-        constexpr int EB = 4;
-        for (int eb = e0 + ep_tid; eb < e1; eb += 128 * EB) {
-          float4 acc[EB];
-          for (int c0 = 0; c0 < n_contrib; c0 += 8) {
-            const int cn = min(8, n_contrib - c0);
-            float4 xs[EB][8];
+          named_bar(1, 128);
+          if (s_flag[0] == (unsigned)(n_contrib - 1)) {
+            if (ep_tid == 0) *arrive = 0u;
+            const float4* parts = reinterpret_cast<const float4*>(A.part + (size_t)t * A.max_contrib * part_elems);
+            const int per = (int)(part_elems / 4);
+            for (int w = ep_tid; w < per; w += 128) {
+              float4 xs[4];
 #pragma unroll
-            for (int k = 0; k < EB; ++k)
-#pragma unroll
-              for (int ci = 0; ci < 8; ++ci) {
-                const int e = eb + k * 128;
-                if (ci < cn && e < e1)
-                  xs[k][ci] = __ldcg(reinterpret_cast<const float4*>(parts + (size_t)(c0 + ci) * part_elems) + e);
+              for (int k = 0; k < 4; ++k)
+                if (k < n_contrib) xs[k] = __ldcg(parts + (size_t)k * per + w);
+              float4 acc = xs[0];
+              for (int k = 1; k < n_contrib; ++k) {  // contributor order → deterministic
+                const float4 x = k < 4 ? xs[k] : __ldcg(parts + (size_t)k * per + w);
+                acc.x += x.x;
+                acc.y += x.y;
+                acc.z += x.z;
+                acc.w += x.w;
               }
-#pragma unroll
-            for (int k = 0; k < EB; ++k)
-#pragma unroll
-              for (int ci = 0; ci < 8; ++ci)
-                if (ci < cn) {
-                  if (c0 + ci == 0) {
-                    acc[k] = xs[k][ci];
-                  } else {
-                    acc[k].x += xs[k][ci].x;
-                    acc[k].y += xs[k][ci].y;
-                    acc[k].z += xs[k][ci].z;
-                    acc[k].w += xs[k][ci].w;
+              const int j = (w * 4) / kBM, r = (w * 4) % kBM;
+              const int nn = nb0 + r;
+              if (nn < A.N && j < mv) {
+                uint2 o;
+                o.x = pack_bf16(acc.x, acc.y);
+                o.y = pack_bf16(acc.z, acc.w);
+                const size_t yo = (size_t)(y0 + j) * A.N + nn;
+                if (nn + 4 <= A.N && (A.N & 3) == 0) {
+                  *reinterpret_cast<uint2*>(A.Y + yo) = o;
+                  for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+                } else {
+                  const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
+                  for (int x = 0; x < 4 && nn + x < A.N; ++x) {
+                    A.Y[yo + x] = __float2bfloat16_rn(vv[x]);
+                    for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = __float2bfloat16_rn(vv[x]);
                   }
                 }
-          }
-#pragma unroll
-          for (int k = 0; k < EB; ++k) {
-            const int e = eb + k * 128;
-            if (e >= e1) break;
-            const int j = (e * 4) / kBM, r = (e * 4) % kBM;
-            const int nn = nb0 + r;
-            if (nn < A.N && j < mv) {
-              uint2 o;
-              o.x = pack_bf16(acc[k].x, acc[k].y);
-              o.y = pack_bf16(acc[k].z, acc[k].w);
-              const size_t yo = (size_t)(y0 + j) * A.N + nn;
-              if (nn + 4 <= A.N && (A.N & 3) == 0) {
-                *reinterpret_cast<uint2*>(A.Y + yo) = o;
-                for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
-              } else {
-                const float vv[4] = {acc[k].x, acc[k].y, acc[k].z, acc[k].w};
-                for (int x = 0; x < 4 && nn + x < A.N; ++x) {
-                  A.Y[yo + x] = __float2bfloat16_rn(vv[x]);
-                  for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = __float2bfloat16_rn(vv[x]);
-                }
               }
             }
           }
         }
-        if (ep_tid == 0) KD_TRACE(13);
       } else {
         // ---- whole tile: TMEM → bf16 → smem transpose → 16-byte stores
         for (int j0 = 0; j0 < A.M; j0 += kChunk) {
@@ -449,19 +338,114 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[a]);
       }
-      // publish this segment's share of the output to consumer devices
-      // (whole tiles and fold participants; a tail contributor stored nothing)
-      const bool stored = whole || seg_end == u1;
-      if (A.epi.n && stored) {
-        named_bar(1, 128);
-        if (ep_tid == 0) {
-          fence_acq_rel_sys();
-          for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
-        }
-      }
       if (ep_tid == 0 && seg < 3) KD_TRACE(7 + 2 * seg);
       u = seg_end;
       ++seg;
+    }
+  }
+  if (A.split_tiles && A.fold_grid) {
+    // ---- grid barrier (all CTAs are co-resident: grid ≤ #SMs, 1 CTA/SM),
+    // self-resetting: the last CTA to leave zeroes both words
+    __syncthreads();
+    if (threadIdx.x == 128) {
+      unsigned* arrive = A.counter;
+      unsigned* depart = A.counter + 1;
+      KD_TRACE(18);
+      fence_acq_rel_gpu();
+      atom_add_acq_rel_gpu(arrive, 1u);
+      while (ld_acquire_gpu(arrive) < (unsigned)G) {
+      }
+      KD_TRACE(16);
+      if (atom_add_acq_rel_gpu(depart, 1u) == (unsigned)G - 1) {
+        *arrive = 0u;
+        *depart = 0u;
+      }
+    }
+    __syncthreads();
+    // ---- fold my slice of the flat [tile][M][128] float4 space with all 256
+    // threads; every (element, contributor) load of a round is in flight at once
+    const long long per_tile = (long long)A.M * kBM / 4;
+    const long long E = (long long)A.tiles * per_tile;
+    const long long e0 = c * E / G, e1 = (c + 1) * E / G;
+    constexpr int kE = 2, kC = 8;
+    for (long long f0 = e0; f0 < e1; f0 += kE * kThreads) {
+      float4 xs[kE][kC];
+      int ncs[kE];
+      long long fs[kE];
+#pragma unroll
+      for (int k = 0; k < kE; ++k) {
+        const long long f = f0 + threadIdx.x + (long long)k * kThreads;
+        fs[k] = f;
+        ncs[k] = 0;
+        if (f < e1) {
+          const int t = (int)(f / per_tile);
+          const long long tb = (long long)t * KB;
+          const long long first = unit_owner(tb, U, G), lastc = unit_owner(tb + KB - 1, U, G);
+          if (lastc > first) {  // split tile (whole tiles were stored from TMEM)
+            ncs[k] = (int)(lastc - first + 1);
+            const float4* parts = reinterpret_cast<const float4*>(A.part + (size_t)t * A.max_contrib * A.M * kBM);
+            const int w = (int)(f - (long long)t * per_tile);
+#pragma unroll
+            for (int ci = 0; ci < kC; ++ci)
+              if (ci < ncs[k]) xs[k][ci] = __ldcg(parts + (size_t)ci * per_tile + w);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kE; ++k) {
+        if (ncs[k] == 0) continue;
+        const long long f = fs[k];
+        const int t = (int)(f / per_tile);
+        const float4* parts = reinterpret_cast<const float4*>(A.part + (size_t)t * A.max_contrib * A.M * kBM);
+        const int w = (int)(f - (long long)t * per_tile);
+        float4 acc = xs[k][0];
+#pragma unroll
+        for (int ci = 1; ci < kC; ++ci)  // contributor order → deterministic
+          if (ci < ncs[k]) {
+            acc.x += xs[k][ci].x;
+            acc.y += xs[k][ci].y;
+            acc.z += xs[k][ci].z;
+            acc.w += xs[k][ci].w;
+          }
+        for (int ci = kC; ci < ncs[k]; ++ci) {
+          const float4 x = __ldcg(parts + (size_t)ci * per_tile + w);
+          acc.x += x.x;
+          acc.y += x.y;
+          acc.z += x.z;
+          acc.w += x.w;
+        }
+        const int grp = A.groups ? t / A.tpg : 0;
+        const int nb0 = (A.groups ? t % A.tpg : t) * kBM;
+        const int y0 = A.groups ? __ldg(A.meta + A.groups + grp) : 0;
+        const int mv = A.groups ? min(__ldg(A.meta + grp), A.M) : A.M;
+        const int j = (w * 4) / kBM, r = (w * 4) % kBM;
+        const int nn = nb0 + r;
+        if (nn < A.N && j < mv) {
+          uint2 o;
+          o.x = pack_bf16(acc.x, acc.y);
+          o.y = pack_bf16(acc.z, acc.w);
+          const size_t yo = (size_t)(y0 + j) * A.N + nn;
+          if (nn + 4 <= A.N && (A.N & 3) == 0) {
+            *reinterpret_cast<uint2*>(A.Y + yo) = o;
+            for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+          } else {
+            const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
+            for (int x = 0; x < 4 && nn + x < A.N; ++x) {
+              A.Y[yo + x] = __float2bfloat16_rn(vv[x]);
+              for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = __float2bfloat16_rn(vv[x]);
+            }
+          }
+        }
+      }
+    }
+    if (threadIdx.x == 128) KD_TRACE(13);
+  }
+  // publish this CTA's stores to the consumer devices (one release per CTA)
+  if (A.epi.n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_acq_rel_sys();
+      for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -490,6 +474,284 @@ static EncodeTiledFn get_encode() {
   });
   return fn;
 }
+
+
+// ============================================================================
+// Cluster split-K decode GEMM (weights on MMA M = 128, tokens on MMA N, the
+// stream-K kernel's orientation): tile t = 128 weight rows, its K range cut
+// into `split` equal parts over the CTAs of one thread-block cluster. Each
+// rank stages its fp32 partial [M][128] in shared memory grouped by owner
+// (rank o owns weight rows [o·rpo, (o+1)·rpo)) and pushes every owner its
+// block with ONE bulk shared::cta → shared::cluster copy completing on the
+// owner's mbarrier; owners sum the split blocks in rank order (bitwise
+// deterministic) and store bf16. Replaces stream-K's global fold (grid
+// barrier + L2 round trips, ≈5 µs measured) for the skinny GEMMs whose
+// 32-48 tiles cannot fill 148 SMs without splitting K.
+namespace csk {
+
+constexpr int kThreads = 256;  // w0 TMA, w1 MMA + TMEM alloc, w4..w7 epilogue
+constexpr int kSmemMax = 227 * 1024;
+
+struct Args {
+  __nv_bfloat16* Y;
+  int M, N, K;
+  int mma_n;     // tokens rounded up to 16 (MMA N)
+  int split;     // cluster size
+  int kbs;       // 64-column boxes per stage
+  int kblocks;   // ⌈K / (64·kbs)⌉
+  int stages;
+  int rpo;       // weight rows owned per rank (split > 1)
+  Epi epi;
+  unsigned long long* trace;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_csk_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Args A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int S = A.stages, kbs = A.kbs, split = A.split, M = A.M;
+  const int xbox = A.mma_n * kBK * 2;
+  const int wst = kbs * kStageA, xst = kbs * xbox;
+  uint8_t* sa = smem;                                 // S × kbs × 16 KB (W)
+  uint8_t* sb = smem + (size_t)S * wst;               // S × kbs × mma_n·128 B (X)
+  float* recv = (float*)(sb + (size_t)S * xst);       // split × [M][rpo] fp32 (peers' blocks of my rows)
+  const size_t blk = (size_t)M * A.rpo;               // floats per (rank, owner) block
+  const size_t recv_bytes = split > 1 ? (size_t)split * blk * 4 : 0;
+  uint64_t* full = (uint64_t*)((uint8_t*)recv + recv_bytes);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tfull = empty + kMaxStages;
+  uint64_t* rbar = tfull + 1;
+  uint32_t* tmem_slot = (uint32_t*)(rbar + 1);
+  float* send = (float*)smem;  // split × [M][rpo] fp32 staging, reuses the idle ring after the last MMA
+  __nv_bfloat16* ystage = (__nv_bfloat16*)smem;  // split == 1: [M][128] bf16 staging (same reuse)
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) KD_TRACE(0);
+  pdl_launch_dependents();
+  const int rank = split > 1 ? (int)cluster_ctarank() : 0;
+  const int tile = blockIdx.x / split;
+  const int n0 = tile * kBM;
+  const int kb0 = (int)((long long)A.kblocks * rank / split);
+  const int nk = (int)((long long)A.kblocks * (rank + 1) / split) - kb0;
+  const int my_rows = split > 1 ? max(0, min(kBM, (rank + 1) * A.rpo) - rank * A.rpo) : 0;
+  const uint32_t ncols = A.mma_n <= 32 ? 32 : (A.mma_n <= 64 ? 64 : (A.mma_n <= 128 ? 128 : 256));
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(rbar, 1);
+    if (split > 1) mbar_expect_tx(rbar, my_rows ? (unsigned)((split - 1) * blk * 4) : 0u);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (split > 1) cluster_arrive_release();  // every rank's rbar is armed once this barrier completes
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) KD_TRACE(1);
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (warp-uniform loop, lane 0 issues)
+    const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+    const unsigned tx = (unsigned)(wst + xst);
+    auto load_w = [&](int i, int s) {
+      for (int b = 0; b < kbs; ++b)
+        tma_load_2d(sa + (size_t)s * wst + b * kStageA, &tmap_w, ((kb0 + i) * kbs + b) * kBK, n0, &full[s], pw);
+    };
+    auto load_x = [&](int i, int s) {
+      for (int b = 0; b < kbs; ++b)
+        tma_load_2d(sb + (size_t)s * xst + b * xbox, &tmap_x, ((kb0 + i) * kbs + b) * kBK, 0, &full[s], px);
+    };
+    const int n_pre = min(S, nk);
+    if (lane == 0) {
+      for (int i = 0; i < n_pre; ++i) {  // weights before the grid-dependency wait
+        mbar_expect_tx(&full[i], tx);
+        load_w(i, i);
+      }
+      KD_TRACE(2);
+      pdl_wait();
+      for (int i = 0; i < n_pre; ++i) load_x(i, i);
+    }
+    __syncwarp();
+    for (int i = n_pre; i < nk; ++i) {
+      const int s = i % S;
+      mbar_wait(&empty[s], (unsigned)(((i / S) - 1) & 1));
+      if (lane == 0) {
+        mbar_expect_tx(&full[s], tx);
+        load_w(i, s);
+        load_x(i, s);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) KD_TRACE(3);
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (warp-uniform loop, lane 0 issues)
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(A.mma_n >> 3) << 17) |
+                           ((uint32_t)(kBM >> 4) << 24);
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % S;
+      mbar_wait(&full[s], (unsigned)((i / S) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (lane == 0) {
+        if (i == 0) KD_TRACE(4);
+        const uint32_t a_addr = smem_u32(sa + (size_t)s * wst);
+        const uint32_t b_addr = smem_u32(sb + (size_t)s * xst);
+        for (int b = 0; b < kbs; ++b)
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            mma_bf16(tmem_base, sw128_desc(a_addr + b * kStageA + 32 * k), sw128_desc(b_addr + b * xbox + 32 * k), idesc,
+                     (i > 0 || b > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      mma_commit(tfull);
+      KD_TRACE(5);
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue
+    const int q = warp - 4, ep = threadIdx.x - 128;
+    const int row = q * 32 + lane;  // weight row within the tile = TMEM lane
+    mbar_wait_sleep(tfull, 0, 128);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (ep == 0) { KD_TRACE(6); KD_CTRACE(20); }
+    const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16);
+    auto store1 = [&](size_t yo, float v) {
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      A.Y[yo] = h;
+      for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo] = h;
+    };
+    auto store_y = [&](int j, int col, float v0, float v1, float v2, float v3) {  // 4 consecutive outputs of token j
+      const size_t yo = (size_t)j * A.N + col;
+      if (col + 4 <= A.N && (A.N & 3) == 0) {
+        uint2 o;
+        o.x = pack_bf16(v0, v1);
+        o.y = pack_bf16(v2, v3);
+        *reinterpret_cast<uint2*>(A.Y + yo) = o;
+        for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+      } else {
+        if (col < A.N) store1(yo, v0);
+        if (col + 1 < A.N) store1(yo + 1, v1);
+        if (col + 2 < A.N) store1(yo + 2, v2);
+        if (col + 3 < A.N) store1(yo + 3, v3);
+      }
+    };
+    bool stored = false;
+    if (split == 1) {
+      // TMEM → fp32 staging [M][128] (thread = row: conflict-free) → 4-wide bf16 stores
+      float* st = send;
+      for (int j0 = 0; j0 < M; j0 += kChunk) {
+        float v[kChunk];
+        tmem_ld16(tbase + j0, v);
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j)
+          if (j0 + j < M) st[(size_t)(j0 + j) * kBM + row] = v[j];
+      }
+      named_bar(1, 128);
+      pdl_wait();
+      for (int e = ep; e < M * (kBM / 4); e += 128) {
+        const int j = e / (kBM / 4), r4 = (e % (kBM / 4)) * 4;
+        const float4 v = *reinterpret_cast<const float4*>(st + (size_t)j * kBM + r4);
+        if (n0 + r4 < A.N) store_y(j, n0 + r4, v.x, v.y, v.z, v.w);
+      }
+      stored = true;
+    } else {
+      // partial → send[owner][j][row − owner·rpo] (owner-major staging)
+      cluster_wait_acquire();  // every owner's rbar is armed (phase 1)
+      if (ep == 0) { KD_TRACE(12); KD_CTRACE(21); }
+      const int rpo = A.rpo;
+      const int o = row / rpo, lr = row - o * rpo;
+      for (int j0 = 0; j0 < M; j0 += 4 * kChunk) {
+        uint32_t v[4][kChunk];  // up to 64 columns in flight, one wait
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (j0 + b * kChunk < A.mma_n) tmem_ld16_nowait(tbase + j0 + b * kChunk, v[b]);
+        tmem_ld_wait();
+        float* dst = send + (size_t)o * blk + lr;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j)
+            if (j0 + b * kChunk + j < M) dst[(size_t)(j0 + b * kChunk + j) * rpo] = __uint_as_float(v[b][j]);
+      }
+      named_bar(1, 128);
+      if (ep == 0) { KD_TRACE(7); KD_CTRACE(22); }
+      // push each peer owner its block: 16-byte st.async into the owner's
+      // recv[rank], completing bytes on the owner's rbar
+      for (int d = 1; d < split; ++d) {
+        const int ow = (rank + d) % split;  // stagger destinations
+        const int orows = max(0, min(kBM, (ow + 1) * rpo) - ow * rpo);
+        if (orows == 0) continue;
+        const int nv = M * rpo / 4;         // the whole [M][rpo] block (row pitch rpo)
+        const uint32_t dst = mapa_shared(smem_u32(recv + (size_t)rank * blk), (uint32_t)ow);
+        const uint32_t rb = mapa_shared(smem_u32(rbar), (uint32_t)ow);
+        const float4* src = reinterpret_cast<const float4*>(send + (size_t)ow * blk);
+        for (int e = ep; e < nv; e += 128) {
+          const float4 v = src[e];
+          st_async_v4(dst + (uint32_t)e * 16, v.x, v.y, v.z, v.w, rb);
+        }
+      }
+      if (ep == 0) { KD_TRACE(10); KD_CTRACE(23); }
+      mbar_wait_cluster(rbar, 0);  // the peers' blocks of my rows have landed
+      if (ep == 0) { KD_TRACE(8); KD_CTRACE(24); }
+      pdl_wait();
+      // my rows [rank·rpo, +my_rows): Σ over ranks in order; 4 rows per thread
+      const int r4n = my_rows / 4;  // rpo and 128 are multiples of 4
+      for (int e = ep; e < M * r4n; e += 128) {
+        const int j = e / r4n, lr4 = (e - j * r4n) * 4;
+        const size_t off = (size_t)j * rpo + lr4;
+        float4 acc = *reinterpret_cast<const float4*>((rank == 0 ? send : recv) + off);
+        for (int cr = 1; cr < split; ++cr) {  // rank order → deterministic
+          const float4 x = *reinterpret_cast<const float4*>((cr == rank ? send : recv) + (size_t)cr * blk + off);
+          acc.x += x.x;
+          acc.y += x.y;
+          acc.z += x.z;
+          acc.w += x.w;
+        }
+        const int col = n0 + rank * rpo + lr4;
+        if (col < A.N) store_y(j, col, acc.x, acc.y, acc.z, acc.w);
+      }
+      stored = my_rows > 0;
+      if (ep == 0) { KD_TRACE(11); KD_CTRACE(25); }
+    }
+    if (A.epi.n && stored) {  // publish this CTA's stores to the consumer devices
+      named_bar(1, 128);
+      if (ep == 0) {
+        fence_acq_rel_sys();
+        for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
+      }
+    }
+    if (ep == 0) { KD_TRACE(9); KD_CTRACE(26); }
+  }
+  if (split > 1) {
+    // phase 1 waits (epilogue warps did theirs before sending), then a second
+    // cluster barrier so no CTA exits while a peer may still address it
+    if (warp < 4) cluster_wait_acquire();
+    cluster_arrive_release();
+    cluster_wait_acquire();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
+  }
+  if (threadIdx.x == 0) KD_TRACE(15);
+}
+
+}  // namespace csk
 
 }  // namespace gemm
 
@@ -534,7 +796,7 @@ static kd_status encode(CUtensorMap* map, const void* ptr, uint64_t inner, uint6
 }
 
 struct Geometry {
-  int mma_n, stages, kblocks, tiles, grid, max_contrib;
+  int mma_n, stages, kblocks, tiles, grid, max_contrib, kbs;
   long long units;
 };
 
@@ -555,9 +817,13 @@ static kd_status geometry(const GemmShape& a, Geometry* g, int sms) {
   if (a.K % 8) return fail(KD_ERR_UNSUPPORTED, "gemm: K must be a multiple of 8 (16-byte TMA rows)");
   if (a.groups && a.N % kBM) return fail(KD_ERR_UNSUPPORTED, "grouped gemm: N must be a multiple of 128");
   g->mma_n = (int)((a.M + 15) / 16 * 16);
-  const int stage_bytes = kStageA + g->mma_n * kBK * 2;
+  // two 64-column boxes per stage halve the per-stage barrier/MMA-issue
+  // overhead (measured ≈0.3 µs per stage at one box) while ≥ 4 stages fit
+  g->kbs = g->mma_n <= 128 ? 2 : 1;
+  if (const char* e = getenv("KD_GEMM_KBS")) g->kbs = std::max(1, std::min(2, atoi(e)));
+  const int stage_bytes = g->kbs * (kStageA + g->mma_n * kBK * 2);
   g->stages = std::min(kMaxStages, (kSmemBudget - 2 * kChunk * kBM * 2) / stage_bytes);
-  g->kblocks = (int)((a.K + kBK - 1) / kBK);
+  g->kblocks = (int)((a.K + kBK * g->kbs - 1) / (kBK * g->kbs));
   g->tiles = (int)((a.N + kBM - 1) / kBM) * (int)std::max<uint32_t>(1, a.groups);
   g->units = (long long)g->tiles * g->kblocks;
   g->grid = (int)std::min<long long>(sms, g->units);
@@ -572,8 +838,125 @@ static kd_status geometry(const GemmShape& a, Geometry* g, int sms) {
 }
 
 static size_t smem_bytes(const Geometry& g) {
-  return 1024 + (size_t)g.stages * (kStageA + g.mma_n * kBK * 2) + (2 * kMaxStages + 6) * 8 + 2 * kChunk * kBM * 2 + 16;
+  return 1024 + (size_t)g.stages * g.kbs * (kStageA + g.mma_n * kBK * 2) + (2 * kMaxStages + 6) * 8 +
+         2 * kChunk * kBM * 2 + 16;
 }
+
+// ---------------------------------------------------------------- dense GEMM kernel choice
+namespace csk {
+
+static size_t smem_for(int mma_n, int kbs, int stages, int split, int rpo, int M) {
+  const size_t recv = split > 1 ? (size_t)split * M * rpo * 4 : 0;
+  return 1024 + (size_t)stages * kbs * (kStageA + (size_t)mma_n * kBK * 2) + recv + (2 * kMaxStages + 4) * 8 + 16;
+}
+
+// co-resident clusters of `split` CTAs (one CTA per SM at this kernel's smem),
+// per device; ⌊SMs / split⌋ when the query is unavailable
+static int max_clusters(int split) {
+  static std::mutex mu;
+  static std::map<int, std::vector<int>> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return kNumSMs / split;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& v = cache[dev];
+  if (v.empty()) {
+    int sms = kNumSMs;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(gemm_csk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+    v.assign(9, 0);
+    for (int c = 1; c <= 8; ++c) {
+      int n = 0;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c * (sms / c));
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = 160 * 1024;
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = c;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = 1;
+      if (c == 1) n = sms;
+      else if (cudaOccupancyMaxActiveClusters(&n, gemm_csk_kernel, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+      }
+      v[c] = n;
+    }
+  }
+  return v[split];
+}
+
+// Modelled time (ns) of the cluster kernel at split s: the largest per-CTA
+// weight slab at min(per-SM TMA rate, HBM share), + the DSMEM reduction; and
+// of stream-K: all weights at HBM rate + its fold tail. Constants measured on
+// B200 (scripts/bench_ops.py, scratch sweeps): ≈60 GB/s per SM with 2-box
+// stages, 6.45 TB/s HBM, ≈1 µs cluster reduction, stream-K tails ≈2 µs (≤3
+// contributors per tile, last-arriver fold) / ≈6 µs (grid fold).
+constexpr double kSmBps = 60e9, kHbmBps = 6.45e12;
+
+static kd_status choose(const GemmShape& a, GemmTile* t, double* best_ns) {
+  const int M = (int)a.M, mma_n = (M + 15) / 16 * 16;
+  const int tiles = (int)((a.N + kBM - 1) / kBM);
+  int force_s = 0;
+  if (const char* e = getenv("KD_GEMM_TILE")) sscanf(e, "%d", &force_s);
+  double best = -1;
+  for (int s = 1; s <= 8; ++s) {
+    if (force_s && s != force_s) continue;
+    const int maxc = max_clusters(s);
+    if (tiles > maxc) continue;
+    const int kbs = mma_n <= 128 ? 2 : 1;
+    const int KB = (int)((a.K + kBK * kbs - 1) / (kBK * kbs));
+    if (s > KB) continue;
+    const int rpo = s > 1 ? ((kBM + s - 1) / s + 3) / 4 * 4 : 0;
+    if (s > 1 && (rpo * (s - 1) >= kBM)) continue;  // every rank must own rows
+    int stages = kMaxStages;
+    while (stages >= 2 && smem_for(mma_n, kbs, stages, s, rpo, M) > (size_t)kSmemMax) --stages;
+    if (stages < 2) continue;
+    const size_t ring = (size_t)stages * kbs * (kStageA + (size_t)mma_n * kBK * 2);
+    if ((size_t)M * kBM * 4 > ring) continue;  // fp32 staging reuses the ring
+    const double bytes = (double)kBM * ((KB + s - 1) / s) * kbs * kBK * 2;
+    const double rate = std::min(kSmBps, kHbmBps / (tiles * s));
+    const double ns = bytes / rate * 1e9 + (s > 1 ? 1000.0 : 0.0);
+    if (best < 0 || ns < best) {
+      best = ns;
+      t->split = s;
+      t->kbs = kbs;
+      t->kblocks = KB;
+      t->tiles = tiles;
+      t->stages = stages;
+      t->rpo = rpo;
+      t->mt = mma_n;
+      t->smem = (uint32_t)smem_for(mma_n, kbs, stages, s, rpo, M);
+    }
+  }
+  if (best < 0) return fail(KD_ERR_UNSUPPORTED, "gemm: no feasible cluster tiling for this shape");
+  *best_ns = best;
+  return KD_OK;
+}
+
+}  // namespace csk
+
+static double streamk_ns(const GemmShape& a) {
+  Geometry g;
+  if (geometry(a, &g, kNumSMs)) return 1e30;
+  const double w = (double)a.N * a.K * 2;
+  return w / csk::kHbmBps * 1e9 + (g.max_contrib <= 3 ? 2000.0 : 6000.0);
+}
+
+// plain GEMMs: the cluster kernel unless stream-K is modelled faster (or forced)
+static bool use_dense(const GemmShape& a) {
+  if (a.groups) return false;
+  const char* e = getenv("KD_GEMM_STREAMK");
+  if (e && atoi(e)) return false;
+  if (getenv("KD_GEMM_TILE")) return true;
+  GemmTile t;
+  double ns = 0;
+  if (csk::choose(a, &t, &ns)) return false;
+  return ns <= streamk_ns(a);
+}
+
 
 }  // namespace gemm
 
@@ -615,18 +998,53 @@ kd_status gemm_prepare(const GemmShape& a, const void* X, const void* W, const v
   if (s) return s;
   if (!X || !W || (a.groups && !meta)) return fail(KD_ERR_INVALID_ARG, "gemm: NULL operand");
   if (((uintptr_t)X | (uintptr_t)W) & 15) return fail(KD_ERR_INVALID_ARG, "gemm: operands must be 16-byte aligned");
+  gp->sh = a;
+  gp->meta = (const int*)meta;
+  gp->dense = gemm::use_dense(a);
+  if (gp->dense) {
+    double ns = 0;
+    s = gemm::csk::choose(a, &gp->tile, &ns);
+    if (s) return s;
+    s = gemm::encode(&gp->tmap_w, W, a.K, a.N, gemm::kBM);
+    if (s) return s;
+    return gemm::encode(&gp->tmap_x, X, a.K, a.rows_total, (uint32_t)gp->tile.mt);
+  }
   s = gemm::encode(&gp->tmap_w, W, a.K, (uint64_t)a.N * std::max<uint32_t>(1, a.groups), gemm::kBM);
   if (s) return s;
   s = gemm::encode(&gp->tmap_x, X, a.K, a.rows_total, (uint32_t)g.mma_n);
   if (s) return s;
-  gp->sh = a;
-  gp->meta = (const int*)meta;
   return KD_OK;
 }
 
 static unsigned long long* g_gemm_trace = nullptr;
 
+static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t* signals) {
+  const GemmTile& t = gp.tile;
+  gemm::csk::Args A;
+  A.Y = (__nv_bfloat16*)Y;
+  A.M = (int)gp.sh.M;
+  A.N = (int)gp.sh.N;
+  A.K = (int)gp.sh.K;
+  A.mma_n = t.mt;
+  A.split = t.split;
+  A.kbs = t.kbs;
+  A.kblocks = t.kblocks;
+  A.stages = t.stages;
+  A.rpo = t.rpo;
+  A.epi = c.epi;
+  A.trace = g_gemm_trace;
+  kd_status ks = kernels_init();
+  if (ks) return ks;
+  KD_CUDA_CHECK(kd_launch_cluster(gemm::csk::gemm_csk_kernel, dim3(t.tiles * t.split), dim3(gemm::csk::kThreads),
+                                  t.smem, c.stream, (unsigned)t.split, gp.tmap_w, gp.tmap_x, A),
+                "gemm (cluster split-K) launch");
+  if (signals) return gemm_signals(gp.sh, signals);
+  return KD_OK;
+}
+
 kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t* signals) {
+  if (!Y) return fail(KD_ERR_INVALID_ARG, "gemm: NULL output");
+  if (gp.dense) return launch_gemm_dense(gp, Y, c, signals);
   gemm::Geometry g;
   kd_status s = gemm::geometry(gp.sh, &g, kNumSMs);
   if (s) return s;
@@ -646,6 +1064,10 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   A.mma_n = g.mma_n;
   A.stages = g.stages;
   A.kblocks = g.kblocks;
+  A.kbs = g.kbs;
+  A.split_tiles = g.max_contrib > 1 ? 1 : 0;
+  A.fold_grid = g.max_contrib > 3 ? 1 : 0;
+  if (const char* e = getenv("KD_GEMM_FOLD")) A.fold_grid = atoi(e);
   A.tiles = g.tiles;
   A.max_contrib = g.max_contrib;
   A.units = g.units;
@@ -667,6 +1089,35 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
 
 }  // namespace kd
 
+extern "C" kd_status kd_gemm_tiling(uint32_t M, uint32_t N, uint32_t K, int32_t* out) {
+  if (!out) return kd::fail(KD_ERR_INVALID_ARG, "kd_gemm_tiling: NULL out");
+  kd_attr_gemm a;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.dtype = KD_BF16;
+  const kd::GemmShape sh = kd::gemm_shape(a);
+  kd::gemm::Geometry g;
+  kd_status gs = kd::gemm::geometry(sh, &g, kd::kNumSMs);  // shape validation
+  if (gs) return gs;
+  if (!kd::gemm::use_dense(sh)) {
+    out[0] = 0;
+    out[1] = out[2] = out[3] = out[4] = out[5] = 0;
+    return KD_OK;
+  }
+  kd::GemmTile t;
+  double ns = 0;
+  kd_status s = kd::gemm::csk::choose(sh, &t, &ns);
+  if (s) return s;
+  out[0] = 1;
+  out[1] = t.split;
+  out[2] = kd::gemm::kBM;
+  out[3] = t.tiles;
+  out[4] = t.stages;
+  out[5] = (int32_t)t.smem;
+  return KD_OK;
+}
+
 extern "C" kd_status kd_debug_gemm_trace(void* dev_buf) {  // 32 u64 stamps per CTA
   kd::g_gemm_trace = (unsigned long long*)dev_buf;
   return KD_OK;
@@ -675,20 +1126,24 @@ extern "C" kd_status kd_debug_gemm_trace(void* dev_buf) {  // 32 u64 stamps per 
 namespace kd {
 
 kd_status gemm_signals(const GemmShape& a, uint32_t* s) {
+  if (gemm::use_dense(a)) {
+    // one release per storing CTA: every tile once (split 1), else every
+    // cluster rank that owns at least one token row
+    // one release per storing CTA: every tile once (split 1), else every
+    // cluster rank that owns weight rows
+    GemmTile t;
+    double ns = 0;
+    kd_status st = gemm::csk::choose(a, &t, &ns);
+    if (st) return st;
+    const int owners = t.split == 1 ? 1 : (gemm::kBM + t.rpo - 1) / t.rpo;
+    *s = (uint32_t)(t.tiles * owners);
+    return KD_OK;
+  }
   gemm::Geometry g;
   kd_status st = gemm::geometry(a, &g, kNumSMs);
   if (st) return st;
-  // one flag increment per (tile, contributing CTA) segment: whole tiles count
-  // once, a split tile once per contributor (each stores its slice)
-  uint64_t n = 0;
-  for (int t = 0; t < g.tiles; ++t) {
-    const long long tb = (long long)t * g.kblocks, te = tb + g.kblocks;
-    long long f = gemm::unit_owner(tb, g.units, g.grid);
-    long long l = gemm::unit_owner(te - 1, g.units, g.grid);
-    const bool tail = gemm::unit_begin(l + 1, g.units, g.grid) > te;
-    n += (uint64_t)(l - f + 1) - (l > f && tail ? 1 : 0);
-  }
-  *s = (uint32_t)n;
+  // one flag increment per CTA, after its whole tiles and its fold slice
+  *s = (uint32_t)g.grid;
   return KD_OK;
 }
 
@@ -697,6 +1152,11 @@ kd_status gemm_init_attrs() {
                 "gemm smem attr");
   KD_CUDA_CHECK(cudaFuncSetAttribute(gemm::gemm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
                 "gemm carveout");
+  KD_CUDA_CHECK(cudaFuncSetAttribute(gemm::csk::gemm_csk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     gemm::csk::kSmemMax),
+                "gemm dense smem attr");
+  KD_CUDA_CHECK(cudaFuncSetAttribute(gemm::csk::gemm_csk_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                "gemm dense carveout");
   return KD_OK;
 }
 

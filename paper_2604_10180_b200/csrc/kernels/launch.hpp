@@ -37,6 +37,33 @@ inline cudaError_t kd_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, si
   cfg.numAttrs = g_pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+// same, launched as clusters of `cluster` CTAs along x
+template <typename... KArgs, typename... Args>
+inline cudaError_t kd_launch_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                     unsigned cluster, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (g_pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 #define KD_CUDA_CHECK(call, where)                     \
   do {                                                 \
     cudaError_t _e = (call);                           \
@@ -76,11 +103,18 @@ struct GemmShape {
 };
 GemmShape gemm_shape(const kd_attr_gemm& a);
 GemmShape gemm_shape(const kd_attr_grouped_gemm& a);
+// dense (non-grouped) GEMM tiling, chosen per shape and device (gemm.cu)
+struct GemmTile {
+  int split = 0, kbs = 0, kblocks = 0, mt = 0 /* MMA N (tokens rounded to 16) */, stages = 0, rpo = 0, tiles = 0;
+  uint32_t tx = 0, smem = 0;
+};
 struct GemmPlan {
   alignas(64) CUtensorMap tmap_w;
   alignas(64) CUtensorMap tmap_x;
   GemmShape sh;
   const int* meta = nullptr;  // grouped: int32 count[groups], offset[groups]
+  bool dense = false;         // cluster split-K kernel (else stream-K)
+  GemmTile tile;
 };
 kd_status gemm_scratch_bytes(const GemmShape& sh, uint64_t* bytes);
 kd_status gemm_prepare(const GemmShape& sh, const void* X, const void* W, const void* meta, GemmPlan* gp);

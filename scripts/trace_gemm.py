@@ -28,7 +28,7 @@ for name in (sys.argv[1:] or list(shapes)):
     rel[:, 20:] = float("nan")
     import numpy as np
     labels = ["entry", "setup", "tma0", "tmaN", "full0", "commitN", "seg0.wait", "seg0.done", "seg1.wait", "seg1.done",
-              "seg2.wait", "seg2.done", "fix.start", "fix.end", "fix.chunk0", "exit", "all.arrived", "own.bulk", "ctb.stored", "ctb.atom"] + ["-"] * 12
+              "seg2.wait", "seg2.done", "-", "fold.end", "-", "exit", "gbar.pass", "-", "gbar.arrive", "-"] + ["-"] * 12
     print(f"== {name} M={M} N={N} K={Kd}: span {np.nanmax(rel):.2f} us")
     raw = tr.view(148, 32).cpu().numpy()
     own_rows = raw[raw[:, 21] > 0]
