@@ -75,7 +75,10 @@ __host__ __device__ __forceinline__ long long unit_owner(long long u, long long 
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Args A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // align by offsetting the __shared__ array itself (a uintptr_t round trip
+  // loses the address space: the epilogue's staging stores compiled to
+  // generic ST.E with 64-bit address math, measured ≈35 cycles each)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = A.stages, kbs = A.kbs;
   const int xbox = A.mma_n * kBK * 2;          // one 64-column X box
   const int wst = kbs * kStageA, xst = kbs * xbox;
@@ -501,6 +504,7 @@ struct Args {
   int kblocks;   // ⌈K / (64·kbs)⌉
   int stages;
   int rpo;       // weight rows owned per rank (split > 1)
+  int dbg;       // debug A/B (KD_GEMM_DBG)
   Epi epi;
   unsigned long long* trace;
 };
@@ -508,22 +512,25 @@ struct Args {
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_csk_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Args A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // align by offsetting the __shared__ array itself (a uintptr_t round trip
+  // loses the address space: the epilogue's staging stores compiled to
+  // generic ST.E with 64-bit address math, measured ≈35 cycles each)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = A.stages, kbs = A.kbs, split = A.split, M = A.M;
   const int xbox = A.mma_n * kBK * 2;
   const int wst = kbs * kStageA, xst = kbs * xbox;
   uint8_t* sa = smem;                                 // S × kbs × 16 KB (W)
   uint8_t* sb = smem + (size_t)S * wst;               // S × kbs × mma_n·128 B (X)
   float* recv = (float*)(sb + (size_t)S * xst);       // split × [M][rpo] fp32 (peers' blocks of my rows)
-  const size_t blk = (size_t)M * A.rpo;               // floats per (rank, owner) block
+  const int P = (M + 3) / 4 * 4 + 4;                  // recv row pitch (floats): 16-byte rows + pad
+  const size_t blk = (size_t)P * A.rpo;               // floats per (rank, owner) block: rpo rows
   const size_t recv_bytes = split > 1 ? (size_t)split * blk * 4 : 0;
   uint64_t* full = (uint64_t*)((uint8_t*)recv + recv_bytes);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* rbar = tfull + 1;
   uint32_t* tmem_slot = (uint32_t*)(rbar + 1);
-  float* send = (float*)smem;  // split × [M][rpo] fp32 staging, reuses the idle ring after the last MMA
-  __nv_bfloat16* ystage = (__nv_bfloat16*)smem;  // split == 1: [M][128] bf16 staging (same reuse)
+  float* send = (float*)smem;  // split == 1: [M][128] fp32 staging, reuses the idle ring after the last MMA
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) KD_TRACE(0);
@@ -543,7 +550,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(tfull, 1);
     mbar_init(rbar, 1);
-    if (split > 1) mbar_expect_tx(rbar, my_rows ? (unsigned)((split - 1) * blk * 4) : 0u);
+    // each peer rank sends my_rows rows of ⌈M/4⌉ 16-byte groups
+    if (split > 1) mbar_expect_tx(rbar, (unsigned)((split - 1) * my_rows * ((M + 3) / 4) * 16));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
@@ -556,7 +564,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (split > 1) cluster_arrive_release();  // every rank's rbar is armed once this barrier completes
+  if (split > 1) {
+    // every rank's rbar is armed once this completes. Waited here, at the
+    // start: a cluster-scope acquire invalidates L1 (CCTL.IVALL), which was
+    // measured to stall the epilogue's shared-memory work by ≈2-3K cycles
+    // when done after the main loop.
+    cluster_arrive_release();
+    cluster_wait_acquire();
+  }
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) KD_TRACE(1);
 
@@ -668,60 +683,57 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       stored = true;
     } else {
-      // partial → send[owner][j][row − owner·rpo] (owner-major staging)
-      cluster_wait_acquire();  // every owner's rbar is armed (phase 1)
+      // Each thread owns one weight row of the partial (its TMEM lane) and
+      // sends it, 64 token columns at a time, straight from registers to the
+      // row's owner: recv[rank][lr][0..M) (row pitch P = ⌈M/4⌉·4 + 4 floats) with
+      // 16-byte st.async (peers) or st.shared (itself). No staging pass.
       if (ep == 0) { KD_TRACE(12); KD_CTRACE(21); }
       const int rpo = A.rpo;
       const int o = row / rpo, lr = row - o * rpo;
+      const uint32_t my_off = (uint32_t)(((size_t)rank * rpo + lr) * P * 4);  // recv[rank][lr][·] in the owner
+      const uint32_t dst = o == rank ? smem_u32(recv) + my_off : mapa_shared(smem_u32(recv) + my_off, (uint32_t)o);
+      const uint32_t rb = o == rank ? 0u : mapa_shared(smem_u32(rbar), (uint32_t)o);
       for (int j0 = 0; j0 < M; j0 += 4 * kChunk) {
         uint32_t v[4][kChunk];  // up to 64 columns in flight, one wait
 #pragma unroll
         for (int b = 0; b < 4; ++b)
           if (j0 + b * kChunk < A.mma_n) tmem_ld16_nowait(tbase + j0 + b * kChunk, v[b]);
         tmem_ld_wait();
-        float* dst = send + (size_t)o * blk + lr;
 #pragma unroll
         for (int b = 0; b < 4; ++b)
 #pragma unroll
-          for (int j = 0; j < kChunk; ++j)
-            if (j0 + b * kChunk + j < M) dst[(size_t)(j0 + b * kChunk + j) * rpo] = __uint_as_float(v[b][j]);
+          for (int x = 0; x < kChunk / 4; ++x) {
+            const int j = j0 + b * kChunk + 4 * x;
+            if (j < M) {  // the last 16-byte group may run past M into the pad
+              const uint32_t ad = dst + (uint32_t)j * 4;
+              if (o == rank)
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ad), "r"(v[b][4 * x]), "r"(v[b][4 * x + 1]),
+                             "r"(v[b][4 * x + 2]), "r"(v[b][4 * x + 3])
+                             : "memory");
+              else
+                st_async_v4(ad, __uint_as_float(v[b][4 * x]), __uint_as_float(v[b][4 * x + 1]),
+                            __uint_as_float(v[b][4 * x + 2]), __uint_as_float(v[b][4 * x + 3]), rb);
+            }
+          }
       }
-      named_bar(1, 128);
-      if (ep == 0) { KD_TRACE(7); KD_CTRACE(22); }
-      // push each peer owner its block: 16-byte st.async into the owner's
-      // recv[rank], completing bytes on the owner's rbar
-      for (int d = 1; d < split; ++d) {
-        const int ow = (rank + d) % split;  // stagger destinations
-        const int orows = max(0, min(kBM, (ow + 1) * rpo) - ow * rpo);
-        if (orows == 0) continue;
-        const int nv = M * rpo / 4;         // the whole [M][rpo] block (row pitch rpo)
-        const uint32_t dst = mapa_shared(smem_u32(recv + (size_t)rank * blk), (uint32_t)ow);
-        const uint32_t rb = mapa_shared(smem_u32(rbar), (uint32_t)ow);
-        const float4* src = reinterpret_cast<const float4*>(send + (size_t)ow * blk);
-        for (int e = ep; e < nv; e += 128) {
-          const float4 v = src[e];
-          st_async_v4(dst + (uint32_t)e * 16, v.x, v.y, v.z, v.w, rb);
-        }
-      }
-      if (ep == 0) { KD_TRACE(10); KD_CTRACE(23); }
-      mbar_wait_cluster(rbar, 0);  // the peers' blocks of my rows have landed
+      if (ep == 0) { KD_TRACE(7); KD_CTRACE(22); KD_TRACE(10); KD_CTRACE(23); }
+      named_bar(1, 128);           // my own rows are in recv[rank]
+      mbar_wait(rbar, 0);          // the peers' rows have landed (st.async complete_tx)
       if (ep == 0) { KD_TRACE(8); KD_CTRACE(24); }
       pdl_wait();
-      // my rows [rank·rpo, +my_rows): Σ over ranks in order; 4 rows per thread
+      // my rows [rank·rpo, +my_rows): Σ over ranks in order; lanes walk tokens
+      // (conflict-free column reads), each thread 4 consecutive weight rows
       const int r4n = my_rows / 4;  // rpo and 128 are multiples of 4
       for (int e = ep; e < M * r4n; e += 128) {
-        const int j = e / r4n, lr4 = (e - j * r4n) * 4;
-        const size_t off = (size_t)j * rpo + lr4;
-        float4 acc = *reinterpret_cast<const float4*>((rank == 0 ? send : recv) + off);
-        for (int cr = 1; cr < split; ++cr) {  // rank order → deterministic
-          const float4 x = *reinterpret_cast<const float4*>((cr == rank ? send : recv) + (size_t)cr * blk + off);
-          acc.x += x.x;
-          acc.y += x.y;
-          acc.z += x.z;
-          acc.w += x.w;
-        }
+        const int lr4 = (e / M) * 4, j = e - (e / M) * M;
+        float acc[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) acc[x] = recv[((size_t)0 * rpo + lr4 + x) * P + j];
+        for (int cr = 1; cr < split; ++cr)  // rank order → deterministic
+#pragma unroll
+          for (int x = 0; x < 4; ++x) acc[x] += recv[((size_t)cr * rpo + lr4 + x) * P + j];
         const int col = n0 + rank * rpo + lr4;
-        if (col < A.N) store_y(j, col, acc.x, acc.y, acc.z, acc.w);
+        if (col < A.N) store_y(j, col, acc[0], acc[1], acc[2], acc[3]);
       }
       stored = my_rows > 0;
       if (ep == 0) { KD_TRACE(11); KD_CTRACE(25); }
@@ -735,13 +747,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (ep == 0) { KD_TRACE(9); KD_CTRACE(26); }
   }
-  if (split > 1) {
-    // phase 1 waits (epilogue warps did theirs before sending), then a second
-    // cluster barrier so no CTA exits while a peer may still address it
-    if (warp < 4) cluster_wait_acquire();
-    cluster_arrive_release();
-    cluster_wait_acquire();
-  }
+  // No closing cluster barrier: peers only ever WRITE into this CTA's recv
+  // (st.async), and the epilogue waits for all of those bytes on rbar before
+  // the CTA can exit; nothing reads another CTA's shared memory.
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1) {
@@ -846,7 +854,7 @@ static size_t smem_bytes(const Geometry& g) {
 namespace csk {
 
 static size_t smem_for(int mma_n, int kbs, int stages, int split, int rpo, int M) {
-  const size_t recv = split > 1 ? (size_t)split * M * rpo * 4 : 0;
+  const size_t recv = split > 1 ? (size_t)split * ((M + 3) / 4 * 4 + 4) * rpo * 4 : 0;
   return 1024 + (size_t)stages * kbs * (kStageA + (size_t)mma_n * kBK * 2) + recv + (2 * kMaxStages + 4) * 8 + 16;
 }
 
@@ -1031,6 +1039,7 @@ static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx&
   A.kblocks = t.kblocks;
   A.stages = t.stages;
   A.rpo = t.rpo;
+  A.dbg = getenv("KD_GEMM_DBG") ? atoi(getenv("KD_GEMM_DBG")) : 0;
   A.epi = c.epi;
   A.trace = g_gemm_trace;
   kd_status ks = kernels_init();
