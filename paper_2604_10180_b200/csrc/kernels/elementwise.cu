@@ -6,6 +6,7 @@
 // plus the runtime's step-begin barrier and flag-wait kernels (a13/a15).
 // All are HBM- or launch-bound: 16-byte vector loads, fp32 math, one pass.
 #include <math.h>
+#include <cmath>
 #include <cstdlib>
 
 #include "launch.hpp"
@@ -209,92 +210,111 @@ kd_status launch_silu_mul(const kd_attr_silu_mul& a, const void* gu, void* out, 
 }
 
 // ------------------------------------------------------------------ a5
-// one CTA per token row; cos/sin of pos·θ^(−2i/D) computed once per row in
-// fp64 (R12) into shared memory; threads own (head, pair of dims) work items.
-__global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ bt,
-                                   const int32_t* __restrict__ sl, __nv_bfloat16* __restrict__ q_out,
-                                   __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int Hq, int Hkv,
-                                   int D, int page, int pps, double theta, Epi epi) {
-  extern __shared__ float cs[];  // [D/2] cos, [D/2] sin
+// grid (row, head group of 8): 16 threads per head. A rotated head (q or k)
+// uses threads 0..D/16-1, each rotating 8 dims i..i+7 of the first half with
+// their partners i+D/2.. (two 16-byte loads, two 16-byte stores); a v head is
+// a 16-byte-vector copy into the cache slot. cos/sin of pos·θ^(−2i/D) are
+// formed per thread in fp64 (R12), overlapping the loads.
+constexpr int kRopeHeadsPerCta = 8;
+struct RopeFreq {  // θ^(−2i/D), i < D/2, fp64, formed once per launch on the host
+  double f[128];
+};
+
+__global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
+    rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ bt,
+                       const int32_t* __restrict__ sl, __nv_bfloat16* __restrict__ q_out,
+                       __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int Hq, int Hkv, int D,
+                       int page, int pps, const __grid_constant__ RopeFreq fr, Epi epi) {
   pdl_launch_dependents();
-  pdl_wait();
   const int b = blockIdx.x, half = D / 2, G = Hq / Hkv;
-  const int pos = sl[b] - 1;
-  // angle = pos·θ^(−2i/D) in fp64, reduced exactly enough to [−π, π] in fp64,
-  // then an fp32 sincos of the small reduced angle (≈ the fp64 value rounded
-  // to fp32, R12) — far cheaper than fp64 sincos of a 4K-radian argument
-  const double l2t = log2(theta);
-  for (int i = threadIdx.x; i < half; i += blockDim.x) {
-    const double ang = (double)pos * exp2(-2.0 * (double)i / (double)D * l2t);
-    const double k = rint(ang * 0.15915494309189535);  // 1/(2π)
-    const double red = fma(-k, 6.283185307179586, fma(-k, 2.4492935982947064e-16, ang));
-    float sf, cf;
-    sincosf((float)red, &sf, &cf);
-    cs[i] = cf;
-    cs[half + i] = sf;
-  }
-  __syncthreads();
-  const int32_t pg = bt[(size_t)b * pps + pos / page];
-  const int off = pos % page;
-  const __nv_bfloat16* src = qkv + (size_t)b * (Hq + 2 * Hkv) * D;
-  const int pairs = half / 2;  // bf16x2 items per rotated head
-  // rotated heads: Hq q heads then Hkv k heads
-  const int n_rot = (Hq + Hkv) * pairs;
-  for (int t = threadIdx.x; t < n_rot; t += blockDim.x) {
-    int hh = t / pairs, i = (t % pairs) * 2;
+  const int hh = blockIdx.y * kRopeHeadsPerCta + (int)(threadIdx.x >> 4), t16 = threadIdx.x & 15;
+  const int n_rot = Hq + Hkv;
+  pdl_wait();
+  if (hh < n_rot && t16 * 8 < half) {
+    const int i0 = t16 * 8;
+    const int pos = sl[b] - 1;
+    const __nv_bfloat16* src = qkv + (size_t)b * (Hq + 2 * Hkv) * D;
     const __nv_bfloat16* x;
     __nv_bfloat16* dst;
-    size_t qoff = 0;
     bool is_q = hh < Hq;
+    size_t qoff = 0;
     if (is_q) {
-      int g = hh / G, j = hh % G;
+      const int g = hh / G, j = hh % G;
       x = src + (size_t)g * (G + 2) * D + (size_t)j * D;
       qoff = (size_t)b * Hq * D + (size_t)hh * D;
       dst = q_out + qoff;
     } else {
-      int g = hh - Hq;
+      const int g = hh - Hq;
+      const int32_t pg = bt[(size_t)b * pps + pos / page];
       x = src + (size_t)g * (G + 2) * D + (size_t)G * D;
-      dst = kc + (((size_t)pg * Hkv + g) * page + off) * D;
+      dst = kc + (((size_t)pg * Hkv + g) * page + pos % page) * D;
     }
-    uint32_t a = *reinterpret_cast<const uint32_t*>(x + i);
-    uint32_t bb = *reinterpret_cast<const uint32_t*>(x + half + i);
-    float x0 = bf16lo(a), x1 = bf16hi(a), y0 = bf16lo(bb), y1 = bf16hi(bb);
-    float c0 = cs[i], c1 = cs[i + 1], s0 = cs[half + i], s1 = cs[half + i + 1];
-    uint32_t lo = pack_bf16(x0 * c0 - y0 * s0, x1 * c1 - y1 * s1);
-    uint32_t hi = pack_bf16(y0 * c0 + x0 * s0, y1 * c1 + x1 * s1);
-    *reinterpret_cast<uint32_t*>(dst + i) = lo;
-    *reinterpret_cast<uint32_t*>(dst + half + i) = hi;
+    const uint4 xa = *reinterpret_cast<const uint4*>(x + i0);
+    const uint4 xb = *reinterpret_cast<const uint4*>(x + half + i0);
+    // angle = pos·θ^(−2i/D) in fp64, reduced to [−π, π] in fp64, then fp32
+    // sincos of the small reduced angle (≈ the fp64 value rounded to fp32)
+    float c[8], sn[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double ang = (double)pos * fr.f[i0 + k];
+      const double kk = rint(ang * 0.15915494309189535);  // 1/(2π)
+      const double red = fma(-kk, 6.283185307179586, fma(-kk, 2.4492935982947064e-16, ang));
+      sincosf((float)red, &sn[k], &c[k]);
+    }
+    const uint32_t* pa = &xa.x;
+    const uint32_t* pb = &xb.x;
+    uint4 lo, hi;
+    uint32_t* plo = &lo.x;
+    uint32_t* phi = &hi.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float x0 = bf16lo(pa[q]), x1 = bf16hi(pa[q]), y0 = bf16lo(pb[q]), y1 = bf16hi(pb[q]);
+      const float c0 = c[2 * q], c1 = c[2 * q + 1], s0 = sn[2 * q], s1 = sn[2 * q + 1];
+      plo[q] = pack_bf16(x0 * c0 - y0 * s0, x1 * c1 - y1 * s1);
+      phi[q] = pack_bf16(y0 * c0 + x0 * s0, y1 * c1 + x1 * s1);
+    }
+    *reinterpret_cast<uint4*>(dst + i0) = lo;
+    *reinterpret_cast<uint4*>(dst + half + i0) = hi;
     if (is_q)
       for (int p = 0; p < epi.n; ++p) {
         __nv_bfloat16* pd = (__nv_bfloat16*)epi.dst[p] + qoff;
-        *reinterpret_cast<uint32_t*>(pd + i) = lo;
-        *reinterpret_cast<uint32_t*>(pd + half + i) = hi;
+        *reinterpret_cast<uint4*>(pd + i0) = lo;
+        *reinterpret_cast<uint4*>(pd + half + i0) = hi;
       }
-  }
-  // v: plain copy into the cache slot
-  const int n_v = Hkv * (D / 8);
-  for (int t = threadIdx.x; t < n_v; t += blockDim.x) {
-    int g = t / (D / 8), c8 = (t % (D / 8)) * 8;
-    const __nv_bfloat16* x = src + (size_t)g * (G + 2) * D + (size_t)(G + 1) * D + c8;
-    __nv_bfloat16* dst = vc + (((size_t)pg * Hkv + g) * page + off) * D + c8;
-    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(x);
+  } else if (hh >= n_rot && hh < n_rot + Hkv) {
+    // v: plain copy into the cache slot, 16 threads × 8 dims per pass
+    const int g = hh - n_rot;
+    const int pos = sl[b] - 1;
+    const int32_t pg = bt[(size_t)b * pps + pos / page];
+    const __nv_bfloat16* x = qkv + (size_t)b * (Hq + 2 * Hkv) * D + (size_t)g * (G + 2) * D + (size_t)(G + 1) * D;
+    __nv_bfloat16* dst = vc + (((size_t)pg * Hkv + g) * page + pos % page) * D;
+    for (int c8 = t16 * 8; c8 < D; c8 += 128)
+      *reinterpret_cast<uint4*>(dst + c8) = *reinterpret_cast<const uint4*>(x + c8);
   }
   epi_signal(epi);
+}
+
+static dim3 rope_grid(const kd_attr_rope_append& a) {
+  const int heads = (int)(a.n_heads + 2 * a.n_kv_heads);
+  return dim3(a.rows, (heads + kRopeHeadsPerCta - 1) / kRopeHeadsPerCta);
 }
 
 kd_status launch_rope_append(const kd_attr_rope_append& a, const void* qkv, const int32_t* bt, const int32_t* sl,
                              void* q_out, void* kc, void* vc, const LaunchCtx& c, uint32_t* signals) {
   if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "rope_append: only bf16 activations");
-  if (a.rows == 0 || a.n_kv_heads == 0 || a.n_heads % a.n_kv_heads || a.head_dim % 8 || a.head_dim < 8 ||
-      a.page == 0 || a.pages_per_seq == 0)
-    return fail(KD_ERR_UNSUPPORTED, "rope_append: unsupported shape");
+  if (a.rows == 0 || a.n_kv_heads == 0 || a.n_heads % a.n_kv_heads || a.head_dim % 16 || a.head_dim < 16 ||
+      a.head_dim > 256 || a.page == 0 || a.pages_per_seq == 0)
+    return fail(KD_ERR_UNSUPPORTED, "rope_append: unsupported shape (head_dim a multiple of 16, <= 256)");
   if (!qkv || !bt || !sl || !q_out || !kc || !vc) return fail(KD_ERR_INVALID_ARG, "rope_append: NULL pointer");
-  size_t smem = sizeof(float) * a.head_dim;
-  KD_CUDA_CHECK(kd_launch(rope_append_kernel, dim3(a.rows), dim3(256), smem, c.stream, (const __nv_bfloat16*)qkv, bt,
-                          sl, (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (int)a.n_heads,
-                          (int)a.n_kv_heads, (int)a.head_dim, (int)a.page, (int)a.pages_per_seq, a.theta, c.epi),
+  const dim3 grid = rope_grid(a);
+  RopeFreq fr;
+  const double l2t = std::log2(a.theta);
+  for (uint32_t i = 0; i < a.head_dim / 2; ++i) fr.f[i] = std::exp2(-2.0 * (double)i / (double)a.head_dim * l2t);
+  KD_CUDA_CHECK(kd_launch(rope_append_kernel, grid, dim3(kRopeHeadsPerCta * 16), 0, c.stream, (const __nv_bfloat16*)qkv,
+                          bt, sl, (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (int)a.n_heads,
+                          (int)a.n_kv_heads, (int)a.head_dim, (int)a.page, (int)a.pages_per_seq, fr, c.epi),
                 "rope_append launch");
-  if (signals) *signals = a.rows;
+  if (signals) *signals = grid.x * grid.y;
   return KD_OK;
 }
 
@@ -378,7 +398,13 @@ kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s
   kd_status st = KD_OK;
   switch (op) {
     case KD_OP_ADD_RMSNORM: { kd_attr_add_rmsnorm a; if ((st = attrs_of(attrs, &a))) return st; *signals = a.rows; return KD_OK; }
-    case KD_OP_ROPE_APPEND: { kd_attr_rope_append a; if ((st = attrs_of(attrs, &a))) return st; *signals = a.rows; return KD_OK; }
+    case KD_OP_ROPE_APPEND: {
+      kd_attr_rope_append a;
+      if ((st = attrs_of(attrs, &a))) return st;
+      const dim3 g = rope_grid(a);
+      *signals = g.x * g.y;
+      return KD_OK;
+    }
     case KD_OP_SILU_MUL: { kd_attr_silu_mul a; if ((st = attrs_of(attrs, &a))) return st; *signals = silu_grid(a); return KD_OK; }
     case KD_OP_RESIDUAL_ADD: { kd_attr_residual_add a; if ((st = attrs_of(attrs, &a))) return st; *signals = residual_grid(a); return KD_OK; }
     case KD_OP_ATTENTION: { kd_attr_attention a; if ((st = attrs_of(attrs, &a))) return st; return attention_signals(a, signals); }
