@@ -118,7 +118,7 @@ typedef struct {
   uint32_t rows, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype, pad_;
 } kd_attr_attention;
 typedef struct { uint32_t rows, ffn, dtype, pad_; } kd_attr_silu_mul;  /* gu [rows, 2F] 64-col gate/up blocks */
-typedef struct { uint32_t rows, hidden, n_delta, pad_; } kd_attr_residual_add; /* r fp32 [rows,H] += Σ deltas (bf16) */
+typedef struct { uint32_t rows, hidden, n_delta, dtype; } kd_attr_residual_add; /* r fp32 [rows,H] += Σ deltas (dtype: bf16 or fp32) */
 /* MoE. route buffer: int32 idx[rows][top_k] then fp32
  * w[rows][top_k]; meta buffer: int32 count[E], offset[E], slot_of[rows][top_k]
  * (grouped row of each (row, choice)), row_of[rows*top_k]; grouped rows are

@@ -73,7 +73,7 @@ class kd_attr_silu_mul(C.Structure):
 
 
 class kd_attr_residual_add(C.Structure):
-    _fields_ = [("rows", C.c_uint32), ("hidden", C.c_uint32), ("n_delta", C.c_uint32), ("pad_", C.c_uint32)]
+    _fields_ = [("rows", C.c_uint32), ("hidden", C.c_uint32), ("n_delta", C.c_uint32), ("dtype", C.c_uint32)]
 
 
 class kd_attr_moe(C.Structure):  # kd_attr_moe_route / _dispatch / _combine

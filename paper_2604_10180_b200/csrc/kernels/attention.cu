@@ -658,6 +658,10 @@ static kd_status validate(const kd_attr_attention& a) {
 }  // namespace attn
 
 kd_status attention_scratch_bytes(const kd_attr_attention& a, uint64_t* bytes) {
+  if (a.dtype == KD_F32) {  // fp32 parity kernel: no scratch
+    *bytes = 256;
+    return KD_OK;
+  }
   kd_status s = attn::validate(a);
   if (s) return s;
   attn::Shape sh = attn::choose(a);
@@ -671,6 +675,14 @@ kd_status attention_scratch_bytes(const kd_attr_attention& a, uint64_t* bytes) {
 
 kd_status launch_attention(const kd_attr_attention& a, const void* q, const void* kc, const void* vc,
                            const int32_t* bt, const int32_t* sl, void* out, const LaunchCtx& c, uint32_t* signals) {
+  if (a.dtype == KD_F32) {
+    if (!q || !kc || !vc || !bt || !sl || !out) return fail(KD_ERR_INVALID_ARG, "attention: NULL pointer");
+    if (a.rows == 0 || a.n_kv_heads == 0 || a.n_heads % a.n_kv_heads || a.head_dim == 0 || a.page == 0)
+      return fail(KD_ERR_UNSUPPORTED, "attention (fp32): unsupported shape");
+    kd_status st = launch_attention_f32(a, (const float*)q, (const float*)kc, (const float*)vc, bt, sl, (float*)out, c);
+    if (!st && signals) *signals = attention_f32_signals(a);
+    return st;
+  }
   kd_status s = attn::validate(a);
   if (s) return s;
   if (!q || !kc || !vc || !bt || !sl || !out) return fail(KD_ERR_INVALID_ARG, "attention: NULL pointer");
@@ -776,6 +788,10 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
 }
 
 kd_status attention_signals(const kd_attr_attention& a, uint32_t* s) {
+  if (a.dtype == KD_F32) {
+    *s = attention_f32_signals(a);
+    return KD_OK;
+  }
   kd_status st = attn::validate(a);
   if (st) return st;
   *s = (uint32_t)a.rows * a.n_kv_heads;  // one finishing CTA per (sequence, kv head)

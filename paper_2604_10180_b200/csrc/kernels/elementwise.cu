@@ -98,9 +98,21 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __rest
   epi_signal(epi);
 }
 
+static DeltasF as_f32(const Deltas& d) {
+  DeltasF f;
+  f.n = d.n;
+  for (int i = 0; i < d.n; ++i) f.p[i] = reinterpret_cast<const float*>(d.p[i]);
+  return f;
+}
+
 kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const Deltas& d, const void* gamma, void* h,
                              const LaunchCtx& c, uint32_t* signals) {
-  if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "add_rmsnorm: only bf16 activations");
+  if (a.dtype != KD_BF16 && a.dtype != KD_F32) return fail(KD_ERR_UNSUPPORTED, "add_rmsnorm: dtype must be bf16 or fp32");
+  if (a.n_delta > (uint32_t)kMaxDeltas || (int)a.n_delta != d.n)
+    return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: n_delta must match the deltas given (<= 8)");
+  for (int i = 0; i < d.n; ++i)
+    if (!d.p[i]) return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: NULL delta");
+  if (a.dtype == KD_F32) return launch_add_rmsnorm_f32(a, r, as_f32(d), (const float*)gamma, (float*)h, c, signals);
   if (a.rows == 0 || a.hidden == 0 || a.hidden % 8 || a.hidden > 8 * kNormThreads * kNormChunks)
     return fail(KD_ERR_UNSUPPORTED, "add_rmsnorm: hidden must be a multiple of 8 and <= 8192");
   if (a.n_delta > (uint32_t)kMaxDeltas || (int)a.n_delta != d.n)
@@ -151,8 +163,14 @@ kd_status launch_residual_add(const kd_attr_residual_add& a, float* r, const Del
   for (int i = 0; i < d.n; ++i)
     if (!d.p[i]) return fail(KD_ERR_INVALID_ARG, "residual_add: NULL delta");
   if (!r) return fail(KD_ERR_INVALID_ARG, "residual_add: NULL pointer");
+  if (a.dtype != KD_BF16 && a.dtype != KD_F32) return fail(KD_ERR_UNSUPPORTED, "residual_add: deltas bf16 or fp32");
   size_t n8 = n / 8;
   int grid = residual_grid(a);
+  if (a.dtype == KD_F32) {
+    kd_status st = launch_residual_add_f32(r, as_f32(d), n, grid, c);
+    if (!st && signals) *signals = grid;
+    return st;
+  }
   KD_CUDA_CHECK(kd_launch(residual_add_kernel, dim3(grid), dim3(256), 0, c.stream, r, d, n8, c.epi),
                 "residual_add launch");
   if (signals) *signals = grid;
@@ -198,10 +216,15 @@ static int silu_grid(const kd_attr_silu_mul& a) {
 
 kd_status launch_silu_mul(const kd_attr_silu_mul& a, const void* gu, void* out, const LaunchCtx& c,
                           uint32_t* signals) {
-  if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "silu_mul: only bf16 activations");
+  if (a.dtype != KD_BF16 && a.dtype != KD_F32) return fail(KD_ERR_UNSUPPORTED, "silu_mul: dtype must be bf16 or fp32");
   if (a.rows == 0 || a.ffn == 0 || a.ffn % 64) return fail(KD_ERR_UNSUPPORTED, "silu_mul: ffn must be a multiple of 64");
   if (!gu || !out) return fail(KD_ERR_INVALID_ARG, "silu_mul: NULL pointer");
   int grid = silu_grid(a);
+  if (a.dtype == KD_F32) {
+    kd_status st = launch_silu_mul_f32(a, (const float*)gu, (float*)out, grid, c);
+    if (!st && signals) *signals = grid;
+    return st;
+  }
   KD_CUDA_CHECK(kd_launch(silu_mul_kernel, dim3(grid), dim3(256), 0, c.stream, (const __nv_bfloat16*)gu,
                           (__nv_bfloat16*)out, (int)a.rows, (int)a.ffn, c.epi),
                 "silu_mul launch");
@@ -301,12 +324,17 @@ static dim3 rope_grid(const kd_attr_rope_append& a) {
 
 kd_status launch_rope_append(const kd_attr_rope_append& a, const void* qkv, const int32_t* bt, const int32_t* sl,
                              void* q_out, void* kc, void* vc, const LaunchCtx& c, uint32_t* signals) {
-  if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "rope_append: only bf16 activations");
+  if (a.dtype != KD_BF16 && a.dtype != KD_F32) return fail(KD_ERR_UNSUPPORTED, "rope_append: dtype must be bf16 or fp32");
   if (a.rows == 0 || a.n_kv_heads == 0 || a.n_heads % a.n_kv_heads || a.head_dim % 16 || a.head_dim < 16 ||
       a.head_dim > 256 || a.page == 0 || a.pages_per_seq == 0)
     return fail(KD_ERR_UNSUPPORTED, "rope_append: unsupported shape (head_dim a multiple of 16, <= 256)");
   if (!qkv || !bt || !sl || !q_out || !kc || !vc) return fail(KD_ERR_INVALID_ARG, "rope_append: NULL pointer");
   const dim3 grid = rope_grid(a);
+  if (a.dtype == KD_F32) {
+    kd_status st = launch_rope_append_f32(a, (const float*)qkv, bt, sl, (float*)q_out, (float*)kc, (float*)vc, grid, c);
+    if (!st && signals) *signals = grid.x * grid.y;
+    return st;
+  }
   RopeFreq fr;
   const double l2t = std::log2(a.theta);
   for (uint32_t i = 0; i < a.head_dim / 2; ++i) fr.f[i] = std::exp2(-2.0 * (double)i / (double)a.head_dim * l2t);

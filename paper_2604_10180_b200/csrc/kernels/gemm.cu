@@ -991,6 +991,11 @@ GemmShape gemm_shape(const kd_attr_grouped_gemm& a) {
 }
 
 kd_status gemm_scratch_bytes(const GemmShape& a, uint64_t* bytes) {
+  if (a.dtype == KD_F32) {  // fp32 path: SIMT kernel, no scratch
+    if (a.groups) return fail(KD_ERR_UNSUPPORTED, "grouped gemm: bf16 only");
+    *bytes = 256;
+    return KD_OK;
+  }
   gemm::Geometry g;
   kd_status s = gemm::geometry(a, &g, kNumSMs);
   if (s) return s;
@@ -1001,6 +1006,16 @@ kd_status gemm_scratch_bytes(const GemmShape& a, uint64_t* bytes) {
 }
 
 kd_status gemm_prepare(const GemmShape& a, const void* X, const void* W, const void* meta, GemmPlan* gp) {
+  if (a.dtype == KD_F32) {
+    if (a.groups) return fail(KD_ERR_UNSUPPORTED, "grouped gemm: bf16 only");
+    if (a.M == 0 || a.N == 0 || a.K == 0) return fail(KD_ERR_INVALID_ARG, "gemm: empty shape");
+    if (!X || !W) return fail(KD_ERR_INVALID_ARG, "gemm: NULL operand");
+    gp->sh = a;
+    gp->X = X;
+    gp->W = W;
+    gp->dense = false;
+    return KD_OK;
+  }
   gemm::Geometry g;
   kd_status s = gemm::geometry(a, &g, kNumSMs);
   if (s) return s;
@@ -1053,6 +1068,12 @@ static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx&
 
 kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t* signals) {
   if (!Y) return fail(KD_ERR_INVALID_ARG, "gemm: NULL output");
+  if (gp.sh.dtype == KD_F32) {
+    kd_status st = launch_gemm_f32((const float*)gp.X, (const float*)gp.W, (float*)Y, (int)gp.sh.M, (int)gp.sh.N,
+                                   (int)gp.sh.K, c);
+    if (!st && signals) *signals = gemm_f32_signals(gp.sh.N);
+    return st;
+  }
   if (gp.dense) return launch_gemm_dense(gp, Y, c, signals);
   gemm::Geometry g;
   kd_status s = gemm::geometry(gp.sh, &g, kNumSMs);
@@ -1135,6 +1156,10 @@ extern "C" kd_status kd_debug_gemm_trace(void* dev_buf) {  // 32 u64 stamps per 
 namespace kd {
 
 kd_status gemm_signals(const GemmShape& a, uint32_t* s) {
+  if (a.dtype == KD_F32) {
+    *s = gemm_f32_signals(a.N);
+    return KD_OK;
+  }
   if (gemm::use_dense(a)) {
     // one release per storing CTA: every tile once (split 1), else every
     // cluster rank that owns at least one token row

@@ -75,6 +75,23 @@ struct Deltas {
   int n = 0;
   const __nv_bfloat16* p[kMaxDeltas] = {};
 };
+// fp32 path (f32.cu): reached from the launchers below when attrs.dtype == KD_F32
+struct DeltasF {
+  int n = 0;
+  const float* p[kMaxDeltas] = {};
+};
+kd_status launch_add_rmsnorm_f32(const kd_attr_add_rmsnorm& a, float* r, const DeltasF& d, const float* gamma,
+                                 float* h, const LaunchCtx& c, uint32_t* signals);
+kd_status launch_residual_add_f32(float* r, const DeltasF& d, size_t n, int grid, const LaunchCtx& c);
+kd_status launch_silu_mul_f32(const kd_attr_silu_mul& a, const float* gu, float* out, int grid, const LaunchCtx& c);
+kd_status launch_rope_append_f32(const kd_attr_rope_append& a, const float* qkv, const int32_t* bt, const int32_t* sl,
+                                 float* q_out, float* kc, float* vc, dim3 grid, const LaunchCtx& c);
+uint32_t attention_f32_signals(const kd_attr_attention& a);
+kd_status launch_attention_f32(const kd_attr_attention& a, const float* q, const float* kc, const float* vc,
+                               const int32_t* bt, const int32_t* sl, float* out, const LaunchCtx& c);
+uint32_t gemm_f32_signals(uint32_t N);
+kd_status launch_gemm_f32(const float* X, const float* W, float* Y, int M, int N, int K, const LaunchCtx& c);
+
 kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const Deltas& d, const void* gamma, void* h,
                              const LaunchCtx& c, uint32_t* signals);
 kd_status launch_residual_add(const kd_attr_residual_add& a, float* r, const Deltas& d, const LaunchCtx& c,
@@ -114,6 +131,8 @@ struct GemmPlan {
   GemmShape sh;
   const int* meta = nullptr;  // grouped: int32 count[groups], offset[groups]
   bool dense = false;         // cluster split-K kernel (else stream-K)
+  const void* X = nullptr;    // fp32 path: plain operand pointers (SIMT kernel)
+  const void* W = nullptr;
   GemmTile tile;
 };
 kd_status gemm_scratch_bytes(const GemmShape& sh, uint64_t* bytes);

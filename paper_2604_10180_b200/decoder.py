@@ -68,8 +68,14 @@ class DecoderGraph:
     """Declares the decoder kernel graph for one micro-batch of cfg.m rows."""
 
     def __init__(self, cfg, act: int = K.KD_BF16):
-        if act != K.KD_BF16:
-            raise NotImplementedError("only the bf16 path is built")
+        """act: KD_BF16 (throughput path) or KD_F32 (the 1e-5 parity path,
+        R13: fp32 weights, activations and KV cache; dense attention layers)."""
+        if act not in (K.KD_BF16, K.KD_F32):
+            raise ValueError("act must be KD_BF16 or KD_F32")
+        if act == K.KD_F32 and (cfg.n_experts or cfg.attn_every):
+            raise NotImplementedError("the fp32 path covers the dense decoder (no MoE / SSM layers)")
+        self.act = act
+        adt = "bf16" if act == K.KD_BF16 else "f32"  # storage of weights, activations and KV cache
         self.cfg = cfg
         m, H, L = cfg.m, cfg.hidden, cfg.n_layers
         Hq, Hkv, D, F = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn
@@ -123,30 +129,30 @@ class DecoderGraph:
                                 ("yn", (m, di)), ("d", (m, H))):
                     buf(f"{nm}.{l}", shp, "bf16", PM)
                 continue
-            buf(f"w_qkv.{l}", (cfg.qkv_dim, H), "bf16", W)
-            buf(f"w_o.{l}", (H, Hq * D), "bf16", W)
+            buf(f"w_qkv.{l}", (cfg.qkv_dim, H), adt, W)
+            buf(f"w_o.{l}", (H, Hq * D), adt, W)
             if E:
                 buf(f"w_router.{l}", (E, H), "f32", W)
-                buf(f"w_gu_e.{l}", (E, 2 * F, H), "bf16", W)
-                buf(f"w_d_e.{l}", (E, H, F), "bf16", W)
+                buf(f"w_gu_e.{l}", (E, 2 * F, H), adt, W)
+                buf(f"w_d_e.{l}", (E, H, F), adt, W)
                 buf(f"route.{l}", (2 * m * k,), "i32", PM)
                 buf(f"xgm.{l}", (self.meta_bytes + m * k * H * 2,), "u8", PM)
-                buf(f"gue.{l}", (m * k, 2 * F), "bf16", PM)
-                buf(f"ae.{l}", (m * k, F), "bf16", PM)
-                buf(f"ye.{l}", (m * k, H), "bf16", PM)
+                buf(f"gue.{l}", (m * k, 2 * F), adt, PM)
+                buf(f"ae.{l}", (m * k, F), adt, PM)
+                buf(f"ye.{l}", (m * k, H), adt, PM)
             else:
-                buf(f"w_gu.{l}", (2 * F, H), "bf16", W)
-                buf(f"w_d.{l}", (H, F), "bf16", W)
-            buf(f"g1.{l}", (H,), "bf16", W)
-            buf(f"g2.{l}", (H,), "bf16", W)
-            buf(f"kc.{l}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
-            buf(f"vc.{l}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+                buf(f"w_gu.{l}", (2 * F, H), adt, W)
+                buf(f"w_d.{l}", (H, F), adt, W)
+            buf(f"g1.{l}", (H,), adt, W)
+            buf(f"g2.{l}", (H,), adt, W)
+            buf(f"kc.{l}", (m * pps, Hkv, cfg.page, D), adt, PERS | PM)
+            buf(f"vc.{l}", (m * pps, Hkv, cfg.page, D), adt, PERS | PM)
             acts = [("h1", (m, H)), ("qkv", (m, cfg.qkv_dim)), ("q", (m, Hq * D)), ("attn", (m, Hq * D)),
                     ("o", (m, H)), ("h2", (m, H)), ("d", (m, H))]
             if not E:
                 acts += [("gu", (m, 2 * F)), ("a", (m, F))]
             for nm, shp in acts:
-                buf(f"{nm}.{l}", shp, "bf16", PM)
+                buf(f"{nm}.{l}", shp, adt, PM)
 
         self.kernels: List[KernelInfo] = []
 
@@ -213,7 +219,7 @@ class DecoderGraph:
                 add("down", l, T_DOWN, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
                     K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)
         add("final_add", L - 1, T_RESID, K.KD_OP_RESIDUAL_ADD, ["r", f"d.{L-1}"], ["r"],
-            K.kd_attr_residual_add(m, H, 1, 0))
+            K.kd_attr_residual_add(m, H, 1, act))
         g.finalize()
 
     def role_assign(self, mem_dev: int = 0, gemm_dev: int = 1) -> List[int]:
@@ -447,6 +453,10 @@ class DecoderRuntime:
         L = cfg.n_layers
         if inputs is not None:
             def put_bf16(bits):
+                if t.dtype == torch.float32:  # fp32 path: the same bf16-valued inputs, stored fp32 (exact)
+                    from synth import bf16_bits_to_f32
+                    t.copy_(torch.from_numpy(np.ascontiguousarray(bf16_bits_to_f32(np.asarray(bits)))))
+                    return
                 t.copy_(torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16))
             if name == "r":
                 t.copy_(torch.from_numpy(inputs.x[i * m:(i + 1) * m]))
@@ -538,13 +548,18 @@ class DecoderRuntime:
         return np.concatenate(outs, axis=0)
 
     def cache(self, which: str, layer: int) -> np.ndarray:
-        """bf16 bits of one layer's KV pool, micro-batch sub-pools concatenated."""
+        """One layer's KV pool, micro-batch sub-pools concatenated: bf16 bits
+        (uint16) on the bf16 path, fp32 values on the fp32 path."""
         torch = _torch()
         outs = []
         for i in range(self.cfg.n_micro):
             for d in self.local_devs:
                 key = (f"{which}.{layer}", i, d)
                 if key in self.tensors:
-                    outs.append(self.tensors[key].view(torch.int16).cpu().numpy().view(np.uint16))
+                    t = self.tensors[key]
+                    if t.dtype == torch.float32:
+                        outs.append(t.cpu().numpy())
+                    else:
+                        outs.append(t.view(torch.int16).cpu().numpy().view(np.uint16))
                     break
         return np.concatenate(outs, axis=0)

@@ -26,8 +26,8 @@ def relerr(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
 
 
-def run(DEC, cfg, inputs, assign, n_dev, steps=1, use_graph=True):
-    dg = DEC.DecoderGraph(cfg)
+def run(DEC, cfg, inputs, assign, n_dev, steps=1, use_graph=True, act=None):
+    dg = DEC.DecoderGraph(cfg) if act is None else DEC.DecoderGraph(cfg, act)
     a = assign(dg) if callable(assign) else assign
     rt = DEC.DecoderRuntime(dg, a, n_dev, [0] * n_dev, inputs=inputs, use_graph=use_graph)
     for _ in range(steps):
@@ -68,6 +68,35 @@ def test_disaggregated_loopback_bitwise_equals_monolithic(mod, cfg):
     # eager (no CUDA graph) path gives the same bits
     eager = run(DEC, cfg, inp, lambda dg: dg.role_assign(0, 1), 2, steps=2, use_graph=False)
     assert np.array_equal(mono.residual(), eager.residual())
+
+
+# ------------------------------------------------------------------ the fp32 path (R13)
+# BASELINE north star: "match fp32 oracle outputs within a relative tolerance
+# of ... 1e-5 for the fp32 path". fp32 weights (the same bf16-valued draws),
+# activations and KV cache; SIMT FFMA GEMMs and a plain fp32 softmax.
+@pytest.mark.parametrize("cfg", [TINY, TINY_GQA], ids=["tiny", "tiny_gqa_ragged"])
+def test_fp32_path_step_vs_oracle_1e5(mod, cfg):
+    DEC, K = mod
+    inp = synth.make_decoder_inputs(cfg)
+    rt = run(DEC, cfg, inp, lambda dg: [0] * dg.g.num_kernels, 1, act=K.KD_F32)
+    r_ref, kcs, vcs = OL.decoder_step(inp, act="fp32")
+    r = rt.residual()
+    assert relerr(r, r_ref) < 1e-5
+    for l in range(cfg.n_layers):
+        assert relerr(rt.cache("kc", l), kcs[l]) < 1e-5
+        assert relerr(rt.cache("vc", l), vcs[l]) < 1e-5
+
+
+def test_fp32_path_disaggregated_bitwise(mod):
+    DEC, K = mod
+    cfg = TINY
+    inp = synth.make_decoder_inputs(cfg)
+    mono = run(DEC, cfg, inp, lambda dg: [0] * dg.g.num_kernels, 1, steps=2, act=K.KD_F32)
+    dis = run(DEC, cfg, inp, lambda dg: dg.role_assign(0, 1), 2, steps=2, act=K.KD_F32)
+    assert len(dis.plan.transfers()) > 0
+    assert np.array_equal(mono.residual(), dis.residual())
+    for l in range(cfg.n_layers):
+        assert np.array_equal(mono.cache("kc", l), dis.cache("kc", l))
 
 
 def test_placement_search_plan_runs_bitwise(mod):

@@ -245,3 +245,46 @@ def test_add_rmsnorm_multi_delta_is_tp_reduction(kd):
     api.residual_add(K.kd_attr_residual_add(rows, H, n, 0), rr, dts)
     torch.cuda.synchronize()
     assert np.array_equal(rr.cpu().numpy(), acc)
+
+
+# ------------------------------------------------------------------ the fp32 path (R13): 1e-5 vs the oracle
+def dev_f32(bits):
+    """bf16-valued draws stored fp32 (exact) on the device."""
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(synth.bf16_bits_to_f32(bits))).cuda()
+
+
+@pytest.mark.parametrize("M,N,K_", [(1, 768, 256), (4, 2048, 1024), (33, 100, 1000)])
+def test_gemm_fp32_1e5(kd, M, N, K_):
+    api, K = kd
+    torch = _torch()
+    g = synth.rng(M * 13 + N + K_)
+    X = synth.normal_bf16(g, (M, K_))
+    W = synth.normal_bf16(g, (N, K_), 1 / math.sqrt(K_))
+    a = K.kd_attr_gemm(M, N, K_, K.KD_F32)
+    Y = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    api.gemm(a, dev_f32(X), dev_f32(W), Y, scratch_for(api, K.KD_OP_GEMM, a))
+    torch.cuda.synchronize()
+    ref = OL.linear(OL.bf16_to_f64(X), OL.bf16_to_f64(W), "fp32")
+    assert relerr(host_f64(Y), ref) < 1e-5
+
+
+@pytest.mark.parametrize("rows,Hq,Hkv,D,C", [(4, 4, 4, 64, 128), (3, 8, 2, 128, 37)])
+def test_attention_fp32_1e5(kd, rows, Hq, Hkv, D, C):
+    api, K = kd
+    torch = _torch()
+    g = synth.rng(rows * 17 + Hq + C)
+    pps = (C + 15) // 16
+    bt = synth.block_table(g, rows, pps)
+    sl = np.full(rows, C, np.int32)
+    kc = synth.normal_bf16(g, (rows * pps, Hkv, 16, D))
+    vc = synth.normal_bf16(g, (rows * pps, Hkv, 16, D))
+    q = synth.normal_bf16(g, (rows, Hq * D))
+    out = torch.empty(rows, Hq * D, dtype=torch.float32, device="cuda")
+    a = K.kd_attr_attention(rows, Hq, Hkv, D, 16, pps, K.KD_F32, 0)
+    args = (dev_f32(q), dev_f32(kc), dev_f32(vc), torch.from_numpy(bt).cuda(), torch.from_numpy(sl).cuda())
+    api.attention(a, *args, out, scratch_for(api, K.KD_OP_ATTENTION, a))
+    torch.cuda.synchronize()
+    ref = OL.paged_decode_attention(OL.bf16_to_f64(q), OL.bf16_to_f64(kc), OL.bf16_to_f64(vc), bt, sl, Hq, Hkv, D,
+                                    16, "fp32")
+    assert relerr(host_f64(out), ref) < 1e-5
