@@ -382,9 +382,9 @@ kd_status launch_step_begin(unsigned* epoch, unsigned* const* mine, unsigned* co
   return KD_OK;
 }
 
-__global__ void wait_kernel(WaitList w, const unsigned* epoch, unsigned* err) {
+__global__ void wait_kernel(WaitList w, const unsigned* epoch, unsigned base, unsigned* err) {
   if (threadIdx.x >= w.n) return;
-  const unsigned target = (*epoch) * w.mult[threadIdx.x];
+  const unsigned target = (*epoch - base) * w.mult[threadIdx.x];
   long long spins = 0;
   while (ld_acquire_sys(w.flag[threadIdx.x]) < target) {
     if (++spins > (1ll << 30)) {  // watchdog: record and give up (KD_ERR_TIMEOUT at kd_runtime_check)
@@ -395,9 +395,9 @@ __global__ void wait_kernel(WaitList w, const unsigned* epoch, unsigned* err) {
   }
 }
 
-kd_status launch_wait(const WaitList& w, const unsigned* epoch, unsigned* err, cudaStream_t s) {
+kd_status launch_wait(const WaitList& w, const unsigned* epoch, unsigned base, unsigned* err, cudaStream_t s) {
   if (w.n <= 0) return KD_OK;
-  wait_kernel<<<1, 32, 0, s>>>(w, epoch, err);
+  wait_kernel<<<1, 32, 0, s>>>(w, epoch, base, err);
   KD_CUDA_CHECK(cudaGetLastError(), "wait launch");
   return KD_OK;
 }

@@ -167,12 +167,13 @@ kd_status ssm_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* 
 kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* signals);
 // one-time per-device kernel attributes (dynamic smem opt-in); call outside graph capture
 kd_status kernels_init();
-// wait until every flag[i] >= epoch * mult[i] (ld.acquire.sys); watchdog sets *err
+// wait until every flag[i] >= (epoch − base) * mult[i] (ld.acquire.sys); watchdog sets *err
 struct WaitList {
   int n = 0;
   unsigned* flag[8];
   unsigned mult[8];
 };
-kd_status launch_wait(const WaitList& w, const unsigned* epoch, unsigned* err, cudaStream_t s);
+// base = steps the runtime ran with transfers off (their epochs carry no releases)
+kd_status launch_wait(const WaitList& w, const unsigned* epoch, unsigned base, unsigned* err, cudaStream_t s);
 
 }  // namespace kd

@@ -54,6 +54,9 @@ struct kd_runtime {
   bool use_graph = true;
   bool prepared = false;
   uint32_t profile_op = 0;
+  // steps run in KD_MODE_NO_TRANSFER: their epochs advanced without any flag
+  // release, so the DISAGG wait target is (epoch − nt_steps) × signals
+  uint32_t nt_steps = 0;
   ~kd_runtime() {
     for (auto& d : devs) {
       cudaSetDevice(d.cuda);
@@ -141,7 +144,7 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
   unsigned* err = epoch + 1;
   if (l.kind == Launch::STEP_BEGIN)
     return launch_step_begin(epoch, l.bar_mine.data(), l.bar_slots.data(), (int)l.bar_mine.size(), s);
-  if (l.kind == Launch::WAIT) return launch_wait(l.wait, epoch, err, s);
+  if (l.kind == Launch::WAIT) return launch_wait(l.wait, epoch, rt->nt_steps, err, s);
   LaunchCtx c = l.ctx;
   c.stream = s;
   if (rt->mode == KD_MODE_NO_TRANSFER) c.epi.n = 0;
@@ -538,6 +541,7 @@ kd_status kd_step(kd_runtime* rt, void* const* streams) {
     }
     KD_CUDA_CHECK(cudaGraphLaunch(d.exec, s), "graph launch");
   }
+  if (rt->mode == KD_MODE_NO_TRANSFER) ++rt->nt_steps;  // graphs re-capture on the next mode switch
   return KD_OK;
 }
 

@@ -181,3 +181,24 @@ def test_tp_pairs_fused_allreduce_vs_oracle_and_bitwise(mod, tp):
     dis.sync()
     dis.rt.check()
     assert np.array_equal(mono.residual(), dis.residual())
+
+
+def test_mode_switch_no_transfer_then_disagg(mod):
+    """The exposed-transfer ablation runs KD_MODE_NO_TRANSFER steps (epochs
+    advance, no flag releases) between DISAGG steps; the following DISAGG
+    steps must wait for (epoch − no-transfer steps) × signals, not hang."""
+    DEC, K = mod
+    cfg = TINY
+    inp = synth.make_decoder_inputs(cfg)
+    dis = run(DEC, cfg, inp, lambda dg: dg.role_assign(0, 1), 2, steps=1)
+    dis.rt.set_mode(K.KD_MODE_NO_TRANSFER)
+    dis.rt.prepare()
+    for _ in range(2):
+        dis.step()
+    dis.sync()
+    dis.rt.set_mode(K.KD_MODE_DISAGG)
+    dis.rt.prepare()
+    for _ in range(2):
+        dis.step()
+    dis.sync()
+    dis.rt.check()  # KD_ERR_TIMEOUT if a wait missed its target
