@@ -439,6 +439,7 @@ class DecoderRuntime:
     def _fill(self, t, name, i, inputs, seed, device_normal_):
         torch = _torch()
         cfg = self.cfg
+        bid = self.dg.buf[name]  # seed stream per graph buffer (the TP graph renames shards below)
         if hasattr(self.dg, "host_value"):
             if inputs is not None:
                 v = np.ascontiguousarray(self.dg.host_value(name, i, inputs))
@@ -487,7 +488,7 @@ class DecoderRuntime:
                           "g1": lw.gamma1, "g2": lw.gamma2, "w_gu_e": lw.w_gu_e, "w_d_e": lw.w_d_e}[base])
             return
         # device-side seeded values (throughput runs)
-        s = seed * 1_000_003 + self.dg.buf[name] * 131 + i
+        s = seed * 1_000_003 + bid * 131 + i
         H, F = cfg.hidden, cfg.ffn
         if name == "r":
             device_normal_(t, s, 1.0)
