@@ -188,8 +188,10 @@ def main():
 
     hbm_gbs, tc_tflops, tc_sus, peak_src = peaks()
     if world == 1:
-        # 1 GPU: the monolithic reference point of the metric (all kernels on one B200)
-        dg = DEC.DecoderGraph(cfg)
+        # 1 GPU: the monolithic reference point of the metric (all kernels on one B200);
+        # gate_up and SiLU·mul share the device, so they are declared as one fused
+        # kernel (KD_OP_GEMM_SILU, same bits as the pair; KD_BENCH_NO_FUSE=1 for the A/B)
+        dg = DEC.DecoderGraph(cfg, fuse_silu=not os.environ.get("KD_BENCH_NO_FUSE"))
         assign = [0] * dg.g.num_kernels
         rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed, use_graph=not args.no_graph)
         placement = "monolithic (all kernels on one B200)"

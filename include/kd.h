@@ -95,7 +95,10 @@ enum {
   KD_OP_MOE_COMBINE = 10,  /* a11 reads [yg, route, meta] writes [out]          */
   KD_OP_SSM_CONV = 11,     /* a12 reads [zxbcdt, conv_w, conv_b, conv_state] writes [xbc, conv_state] */
   KD_OP_SSM_UPDATE = 12,   /* a12 reads [xbc, zxbcdt, dt_bias, A_log, D, ssm_state] writes [y, ssm_state] */
-  KD_OP_GATED_NORM = 13    /* a12 reads [y, zxbcdt, norm_w] writes [yn]          */
+  KD_OP_GATED_NORM = 13,   /* a12 reads [y, zxbcdt, norm_w] writes [yn]          */
+  KD_OP_GEMM_SILU = 14     /* a9+a8 fused (co-located gate_up and SiLU·mul): reads [X, W_gu] writes [a]:
+                            * a = silu_mul_blocked(bf16(X·W_guᵀ)) with kd_attr_gemm, N = 2F weight rows
+                            * (64-row gate/up blocks, R12), a [M, F]; bits identical to a9 then a8 */
 };
 
 /* element types of activations / KV */
@@ -335,6 +338,11 @@ kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes);
 kd_status kd_op_add_rmsnorm(const kd_attr_add_rmsnorm* a, float* r, const void* const* deltas,
                             const void* gamma, void* h, void* stream);
 /* a4/a7/a9/a10: Y[M,N] = X[M,K]·W[N,K]ᵀ, bf16 in, fp32 accumulate (tcgen05, TMEM), bf16 out. */
+/* a9+a8 fused: a [M, N/2] = silu(g)·u of the bf16-rounded gate/up GEMM output
+ * (same bits as kd_op_gemm then kd_op_silu_mul). bf16 only; scratch as for the
+ * plain GEMM of the same attrs. */
+kd_status kd_op_gemm_silu(const kd_attr_gemm* a, const void* X, const void* W, void* out, void* scratch,
+                          void* stream);
 kd_status kd_op_gemm(const kd_attr_gemm* a, const void* X, const void* W, void* Y,
                      void* scratch, void* stream);
 /* a5: NeoX RoPE of q and k at pos = seq_len[b]-1, append (k_rot, v) to the

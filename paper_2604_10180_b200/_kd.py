@@ -25,7 +25,7 @@ KD_BUF_WEIGHT, KD_BUF_INPUT, KD_BUF_OUTPUT, KD_BUF_PERSISTENT, KD_BUF_PER_MICROB
 # ops
 KD_OP_NONE, KD_OP_ADD_RMSNORM, KD_OP_GEMM, KD_OP_ROPE_APPEND, KD_OP_ATTENTION, KD_OP_SILU_MUL, \
     KD_OP_RESIDUAL_ADD, KD_OP_MOE_ROUTE, KD_OP_MOE_DISPATCH, KD_OP_GROUPED_GEMM, KD_OP_MOE_COMBINE, \
-    KD_OP_SSM_CONV, KD_OP_SSM_UPDATE, KD_OP_GATED_NORM = range(14)
+    KD_OP_SSM_CONV, KD_OP_SSM_UPDATE, KD_OP_GATED_NORM, KD_OP_GEMM_SILU = range(15)
 KD_BF16, KD_F32 = 0, 1
 KD_OBJ_AUTO, KD_OBJ_THROUGHPUT, KD_OBJ_LATENCY = 0, 1, 2
 KD_MODE_DISAGG, KD_MODE_NO_TRANSFER, KD_MODE_LOG = 0, 1, 2
@@ -182,6 +182,7 @@ _PROTOS = {
     "kd_op_gated_norm": (kd_status, [C.POINTER(kd_attr_ssm), P, P, P, P, P]),
     "kd_op_add_rmsnorm": (kd_status, [C.POINTER(kd_attr_add_rmsnorm), P, P, P, P, P]),
     "kd_op_gemm": (kd_status, [C.POINTER(kd_attr_gemm), P, P, P, P, P]),
+    "kd_op_gemm_silu": (kd_status, [C.POINTER(kd_attr_gemm), P, P, P, P, P]),
     "kd_op_rope_append": (kd_status, [C.POINTER(kd_attr_rope_append), P, P, P, P, P, P, P]),
     "kd_op_attention": (kd_status, [C.POINTER(kd_attr_attention), P, P, P, P, P, P, P, P]),
     "kd_op_silu_mul": (kd_status, [C.POINTER(kd_attr_silu_mul), P, P, P]),

@@ -257,6 +257,11 @@ def gemm(attrs, X, W, Y, scratch, stream=None):
     check(K.kd_op_gemm(C.byref(attrs), _p(X), _p(W), _p(Y), _p(scratch), _stream(stream)), "kd_op_gemm")
 
 
+def gemm_silu(attrs, X, W, out, scratch, stream=None):
+    """a9+a8 fused: out [M, N/2] = silu·mul of the 64-row gate/up blocks of X·Wᵀ."""
+    check(K.kd_op_gemm_silu(C.byref(attrs), _p(X), _p(W), _p(out), _p(scratch), _stream(stream)), "kd_op_gemm_silu")
+
+
 def rope_append(attrs, qkv, block_table, seq_len, q_out, k_cache, v_cache, stream=None):
     check(K.kd_op_rope_append(C.byref(attrs), _p(qkv), _p(block_table), _p(seq_len), _p(q_out), _p(k_cache),
                               _p(v_cache), _stream(stream)), "kd_op_rope_append")

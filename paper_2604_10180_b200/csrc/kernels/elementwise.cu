@@ -437,6 +437,7 @@ kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s
     case KD_OP_RESIDUAL_ADD: { kd_attr_residual_add a; if ((st = attrs_of(attrs, &a))) return st; *signals = residual_grid(a); return KD_OK; }
     case KD_OP_ATTENTION: { kd_attr_attention a; if ((st = attrs_of(attrs, &a))) return st; return attention_signals(a, signals); }
     case KD_OP_GEMM: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
+    case KD_OP_GEMM_SILU: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a, true), signals); }
     case KD_OP_GROUPED_GEMM: { kd_attr_grouped_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
     case KD_OP_MOE_ROUTE:
     case KD_OP_MOE_DISPATCH:

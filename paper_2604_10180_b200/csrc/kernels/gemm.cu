@@ -43,6 +43,8 @@ struct Args {
   unsigned* counter; // [tiles]
   int M, N, K, mma_n, stages, kblocks, tiles, max_contrib;
   int kbs;           // 64-column boxes per pipeline stage (k-block = 64·kbs columns)
+  int silu;          // fused SiLU·mul epilogue: tile t = gate block t (rows 0-63) + up block t
+                     // (rows 64-127) → a[j][64t + i] (row stride N/2), bits of a9 then a8
   int split_tiles;   // any tile cut between CTAs
   int fold_grid;     // split tiles folded after a grid barrier by all CTAs (many
                      // contributors per tile) instead of by their last arriver
@@ -70,6 +72,23 @@ struct Args {
 __host__ __device__ __forceinline__ long long unit_begin(long long c, long long U, long long G) { return c * U / G; }
 __host__ __device__ __forceinline__ long long unit_owner(long long u, long long U, long long G) {
   return ((u + 1) * G + U - 1) / U - 1;
+}
+
+// fused a8 on the GEMM output (KD_OP_GEMM_SILU): gate/up sums rounded to bf16
+// (the plain GEMM's output) then exactly silu_mul_kernel's fp32 math
+__device__ __forceinline__ float rbf(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ uint32_t silu2(float g0, float g1, float u0, float u1) {
+  g0 = rbf(g0), g1 = rbf(g1), u0 = rbf(u0), u1 = rbf(u1);
+  const float s0 = g0 / (1.f + __expf(-g0)), s1 = g1 / (1.f + __expf(-g1));
+  return pack_bf16(s0 * u0, s1 * u1);
+}
+// store 4 fused outputs a[row][col..col+3] (row stride ldy) to Y and every peer copy
+__device__ __forceinline__ void store_silu4(const Args& A, size_t yo, const float4& g, const float4& u) {
+  uint2 o;
+  o.x = silu2(g.x, g.y, u.x, u.y);
+  o.y = silu2(g.z, g.w, u.z, u.w);
+  *reinterpret_cast<uint2*>(A.Y + yo) = o;
+  for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -272,7 +291,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (ep_tid == 0) *arrive = 0u;
             const float4* parts = reinterpret_cast<const float4*>(A.part + (size_t)t * A.max_contrib * part_elems);
             const int per = (int)(part_elems / 4);
-            for (int w = ep_tid; w < per; w += 128) {
+            if (A.silu) {  // gate float4 (rows r..r+3 < 64) with its up partner 16 float4s on
+              for (int w = ep_tid; w < A.M * 16; w += 128) {
+                const int j = w >> 4, wg = j * 32 + (w & 15);
+                float4 g = __ldcg(parts + wg), uu = __ldcg(parts + wg + 16);
+                for (int k = 1; k < n_contrib; ++k) {  // contributor order → deterministic
+                  const float4 x = __ldcg(parts + (size_t)k * per + wg), y = __ldcg(parts + (size_t)k * per + wg + 16);
+                  g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
+                  uu.x += y.x; uu.y += y.y; uu.z += y.z; uu.w += y.w;
+                }
+                if (j < mv) store_silu4(A, (size_t)(y0 + j) * (A.N / 2) + (nb0 / 2) + (w & 15) * 4, g, uu);
+              }
+            }
+            for (int w = ep_tid; w < (A.silu ? 0 : per); w += 128) {
               float4 xs[4];
 #pragma unroll
               for (int k = 0; k < 4; ++k)
@@ -316,8 +347,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < kChunk; ++j) st[j * kBM + row_in_tile] = __float2bfloat16_rn(v[j]);
           named_bar(2, 128);
           const int jn = min(kChunk, mv - j0);
+          if (A.silu) {  // 16 tokens x 8 groups of 8 outputs: gate cols c8.., up cols 64 + c8..
+            const int j = ep_tid >> 3, c8 = (ep_tid & 7) * 8;
+            if (j < jn) {
+              const uint4 gv = *reinterpret_cast<const uint4*>(st + j * kBM + c8);
+              const uint4 uv = *reinterpret_cast<const uint4*>(st + j * kBM + 64 + c8);
+              const uint32_t* gp = &gv.x;
+              const uint32_t* up = &uv.x;
+              uint4 o;
+              uint32_t* op = &o.x;
 #pragma unroll
-          for (int r = 0; r < 2; ++r) {
+              for (int qd = 0; qd < 4; ++qd) op[qd] = silu2(bf16lo(gp[qd]), bf16hi(gp[qd]), bf16lo(up[qd]), bf16hi(up[qd]));
+              const size_t yo = (size_t)(y0 + j0 + j) * (A.N / 2) + nb0 / 2 + c8;
+              *reinterpret_cast<uint4*>(A.Y + yo) = o;
+              for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint4*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < (A.silu ? 0 : 2); ++r) {
             const int e = ep_tid + r * 128;  // 256 vectors of 8 bf16 per chunk
             const int j = e >> 4, col = (e & 15) * 8;
             const int nn = nb0 + col;
@@ -824,6 +871,7 @@ static kd_status geometry(const GemmShape& a, Geometry* g, int sms) {
   if (a.M > 256) return fail(KD_ERR_UNSUPPORTED, "gemm: decode GEMM supports M <= 256 rows (per group)");
   if (a.K % 8) return fail(KD_ERR_UNSUPPORTED, "gemm: K must be a multiple of 8 (16-byte TMA rows)");
   if (a.groups && a.N % kBM) return fail(KD_ERR_UNSUPPORTED, "grouped gemm: N must be a multiple of 128");
+  if (a.silu && (a.groups || a.N % kBM)) return fail(KD_ERR_UNSUPPORTED, "gemm+silu: plain GEMM with N (= 2F) a multiple of 128");
   g->mma_n = (int)((a.M + 15) / 16 * 16);
   // two 64-column boxes per stage halve the per-stage barrier/MMA-issue
   // overhead (measured ≈0.3 µs per stage at one box) while ≥ 4 stages fit
@@ -955,7 +1003,7 @@ static double streamk_ns(const GemmShape& a) {
 
 // plain GEMMs: the cluster kernel unless stream-K is modelled faster (or forced)
 static bool use_dense(const GemmShape& a) {
-  if (a.groups) return false;
+  if (a.groups || a.silu) return false;
   const char* e = getenv("KD_GEMM_STREAMK");
   if (e && atoi(e)) return false;
   if (getenv("KD_GEMM_TILE")) return true;
@@ -968,8 +1016,9 @@ static bool use_dense(const GemmShape& a) {
 
 }  // namespace gemm
 
-GemmShape gemm_shape(const kd_attr_gemm& a) {
+GemmShape gemm_shape(const kd_attr_gemm& a, bool silu) {
   GemmShape s;
+  s.silu = silu ? 1u : 0u;
   s.M = a.M;
   s.rows_total = a.M;
   s.N = a.N;
@@ -1095,9 +1144,11 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   A.stages = g.stages;
   A.kblocks = g.kblocks;
   A.kbs = g.kbs;
+  A.silu = (int)gp.sh.silu;
   A.split_tiles = g.max_contrib > 1 ? 1 : 0;
   A.fold_grid = g.max_contrib > 3 ? 1 : 0;
   if (const char* e = getenv("KD_GEMM_FOLD")) A.fold_grid = atoi(e);
+  if (A.silu) A.fold_grid = 0;  // the fused SiLU epilogue is built for the last-arriver fold
   A.tiles = g.tiles;
   A.max_contrib = g.max_contrib;
   A.units = g.units;

@@ -117,8 +117,9 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
 // partial layout), rows_total = rows of X/Y, groups = 0 for a plain GEMM
 struct GemmShape {
   uint32_t M = 0, rows_total = 0, N = 0, K = 0, groups = 0, dtype = 0;
+  uint32_t silu = 0;  // KD_OP_GEMM_SILU: output a [M, N/2] = silu·mul of the 64-row gate/up blocks
 };
-GemmShape gemm_shape(const kd_attr_gemm& a);
+GemmShape gemm_shape(const kd_attr_gemm& a, bool silu = false);
 GemmShape gemm_shape(const kd_attr_grouped_gemm& a);
 // dense (non-grouped) GEMM tiling, chosen per shape and device (gemm.cu)
 struct GemmTile {

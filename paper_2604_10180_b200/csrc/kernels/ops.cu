@@ -14,11 +14,12 @@ static kd_status attrs_as(const std::vector<uint8_t>& v, T* out) {
 kd_status op_scratch_bytes(uint32_t op, const std::vector<uint8_t>& attrs, u64* bytes) {
   *bytes = 0;
   switch (op) {
-    case KD_OP_GEMM: {
+    case KD_OP_GEMM:
+    case KD_OP_GEMM_SILU: {
       kd_attr_gemm a;
       kd_status s = attrs_as(attrs, &a);
       if (s) return s;
-      return gemm_scratch_bytes(gemm_shape(a), bytes);
+      return gemm_scratch_bytes(gemm_shape(a, op == KD_OP_GEMM_SILU), bytes);
     }
     case KD_OP_GROUPED_GEMM: {
       kd_attr_grouped_gemm a;
@@ -47,6 +48,7 @@ kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes) {
   if (!attrs || !bytes) return fail(KD_ERR_INVALID_ARG, "kd_op_scratch_bytes: NULL argument");
   switch (op) {
     case KD_OP_GEMM: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_gemm*)attrs), bytes);
+    case KD_OP_GEMM_SILU: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_gemm*)attrs, true), bytes);
     case KD_OP_GROUPED_GEMM: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_grouped_gemm*)attrs), bytes);
     case KD_OP_MOE_ROUTE:
     case KD_OP_MOE_DISPATCH:
@@ -90,6 +92,19 @@ kd_status kd_op_gemm(const kd_attr_gemm* a, const void* X, const void* W, void* 
   c.stream = (cudaStream_t)stream;
   c.scratch = scratch;
   return launch_gemm(gp, Y, c, nullptr);
+}
+
+kd_status kd_op_gemm_silu(const kd_attr_gemm* a, const void* X, const void* W, void* out, void* scratch,
+                          void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_gemm_silu: NULL attrs");
+  if (a->dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "kd_op_gemm_silu: bf16 only");
+  GemmPlan gp;
+  kd_status s = gemm_prepare(gemm_shape(*a, true), X, W, nullptr, &gp);
+  if (s) return s;
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  c.scratch = scratch;
+  return launch_gemm(gp, out, c, nullptr);
 }
 
 kd_status kd_op_rope_append(const kd_attr_rope_append* a, const void* qkv, const int32_t* block_table,

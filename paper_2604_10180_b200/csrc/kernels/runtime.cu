@@ -86,7 +86,8 @@ kd_status check_attrs(const Kernel& k) {
   switch (k.op) {
     case KD_OP_NONE: return KD_OK;
     case KD_OP_ADD_RMSNORM: need = sizeof(kd_attr_add_rmsnorm); break;
-    case KD_OP_GEMM: need = sizeof(kd_attr_gemm); break;
+    case KD_OP_GEMM:
+    case KD_OP_GEMM_SILU: need = sizeof(kd_attr_gemm); break;
     case KD_OP_ROPE_APPEND: need = sizeof(kd_attr_rope_append); break;
     case KD_OP_ATTENTION: need = sizeof(kd_attr_attention); break;
     case KD_OP_SILU_MUL: need = sizeof(kd_attr_silu_mul); break;
@@ -111,7 +112,8 @@ kd_status check_attrs(const Kernel& k) {
       ok = a.n_delta <= (uint32_t)kMaxDeltas && nr == 2 + a.n_delta && nw == 2;
       break;
     }
-    case KD_OP_GEMM: ok = nr == 2 && nw == 1; break;
+    case KD_OP_GEMM:
+    case KD_OP_GEMM_SILU: ok = nr == 2 && nw == 1; break;
     case KD_OP_ROPE_APPEND: ok = nr == 3 && nw == 3; break;
     case KD_OP_ATTENTION: ok = nr == 5 && nw == 1; break;
     case KD_OP_SILU_MUL: ok = nr == 1 && nw == 1; break;
@@ -163,7 +165,8 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
       st = launch_add_rmsnorm(a, (float*)l.wr[1], d, l.rd[1 + a.n_delta], l.wr[0], c, &sig);
       break;
     }
-    case KD_OP_GEMM: st = launch_gemm(*l.gemm, l.wr[0], c, &sig); break;
+    case KD_OP_GEMM:
+    case KD_OP_GEMM_SILU: st = launch_gemm(*l.gemm, l.wr[0], c, &sig); break;
     case KD_OP_ROPE_APPEND: {
       auto a = attrs_get<kd_attr_rope_append>(K);
       st = launch_rope_append(a, l.rd[0], (const int32_t*)l.rd[1], (const int32_t*)l.rd[2], l.wr[0], l.wr[1],
@@ -483,9 +486,10 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
         kd_status s3 = gemm_prepare(gemm_shape(attrs_get<kd_attr_grouped_gemm>(K)), l.rd[0], l.rd[1], l.rd[2], l.gemm);
         if (s3) return s3;
       }
-      if (K.op == KD_OP_GEMM) {
+      if (K.op == KD_OP_GEMM || K.op == KD_OP_GEMM_SILU) {
         l.gemm = new GemmPlan();
-        kd_status s3 = gemm_prepare(gemm_shape(attrs_get<kd_attr_gemm>(K)), l.rd[0], l.rd[1], nullptr, l.gemm);
+        kd_status s3 = gemm_prepare(gemm_shape(attrs_get<kd_attr_gemm>(K), K.op == KD_OP_GEMM_SILU), l.rd[0], l.rd[1],
+                                    nullptr, l.gemm);
         if (s3) return s3;
       }
       if (rt->profile_op) {

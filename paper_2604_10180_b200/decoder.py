@@ -67,14 +67,19 @@ class KernelInfo:
 class DecoderGraph:
     """Declares the decoder kernel graph for one micro-batch of cfg.m rows."""
 
-    def __init__(self, cfg, act: int = K.KD_BF16):
+    def __init__(self, cfg, act: int = K.KD_BF16, fuse_silu: bool = False):
         """act: KD_BF16 (throughput path) or KD_F32 (the 1e-5 parity path,
-        R13: fp32 weights, activations and KV cache; dense attention layers)."""
+        R13: fp32 weights, activations and KV cache; dense attention layers).
+        fuse_silu: declare gate_up and SiLU·mul as ONE kernel (KD_OP_GEMM_SILU,
+        same bits as the pair) — for placements that co-locate them (the
+        1-GPU monolithic step); the gu activation then never exists."""
         if act not in (K.KD_BF16, K.KD_F32):
             raise ValueError("act must be KD_BF16 or KD_F32")
         if act == K.KD_F32 and (cfg.n_experts or cfg.attn_every):
             raise NotImplementedError("the fp32 path covers the dense decoder (no MoE / SSM layers)")
         self.act = act
+        fuse_silu = bool(fuse_silu) and act == K.KD_BF16 and not cfg.n_experts
+        self.fuse_silu = fuse_silu
         adt = "bf16" if act == K.KD_BF16 else "f32"  # storage of weights, activations and KV cache
         self.cfg = cfg
         m, H, L = cfg.m, cfg.hidden, cfg.n_layers
@@ -150,7 +155,7 @@ class DecoderGraph:
             acts = [("h1", (m, H)), ("qkv", (m, cfg.qkv_dim)), ("q", (m, Hq * D)), ("attn", (m, Hq * D)),
                     ("o", (m, H)), ("h2", (m, H)), ("d", (m, H))]
             if not E:
-                acts += [("gu", (m, 2 * F)), ("a", (m, F))]
+                acts += ([] if fuse_silu else [("gu", (m, 2 * F))]) + [("a", (m, F))]
             for nm, shp in acts:
                 buf(f"{nm}.{l}", shp, adt, PM)
 
@@ -213,9 +218,13 @@ class DecoderGraph:
                 add("combine", l, T_COMBINE, K.KD_OP_MOE_COMBINE, [f"ye.{l}", f"route.{l}", meta_span], [f"d.{l}"],
                     am)
             else:
-                add("gu", l, T_GU, K.KD_OP_GEMM, [f"h2.{l}", f"w_gu.{l}"], [f"gu.{l}"],
-                    K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
-                add("silu", l, T_SILU, K.KD_OP_SILU_MUL, [f"gu.{l}"], [f"a.{l}"], K.kd_attr_silu_mul(m, F, act, 0))
+                if fuse_silu:
+                    add("gu_silu", l, T_GU, K.KD_OP_GEMM_SILU, [f"h2.{l}", f"w_gu.{l}"], [f"a.{l}"],
+                        K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
+                else:
+                    add("gu", l, T_GU, K.KD_OP_GEMM, [f"h2.{l}", f"w_gu.{l}"], [f"gu.{l}"],
+                        K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
+                    add("silu", l, T_SILU, K.KD_OP_SILU_MUL, [f"gu.{l}"], [f"a.{l}"], K.kd_attr_silu_mul(m, F, act, 0))
                 add("down", l, T_DOWN, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
                     K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)
         add("final_add", L - 1, T_RESID, K.KD_OP_RESIDUAL_ADD, ["r", f"d.{L-1}"], ["r"],

@@ -202,3 +202,34 @@ def test_mode_switch_no_transfer_then_disagg(mod):
         dis.step()
     dis.sync()
     dis.rt.check()  # KD_ERR_TIMEOUT if a wait missed its target
+
+
+def test_fused_silu_graph_vs_oracle_and_disaggregated(mod):
+    """The monolithic-placement graph with gate_up+SiLU fused (KD_OP_GEMM_SILU)
+    is within tolerance of the oracle and runs disaggregated bitwise equal to
+    its own monolithic run."""
+    DEC, K = mod
+    cfg = TINY
+    inp = synth.make_decoder_inputs(cfg)
+
+    def runf(assign, n_dev):
+        dg = DEC.DecoderGraph(cfg, fuse_silu=True)
+        assert any(k.name == "gu_silu" for k in dg.kernels)
+        rt = DEC.DecoderRuntime(dg, assign(dg), n_dev, [0] * n_dev, inputs=inp)
+        for _ in range(2):
+            rt.step()
+        rt.sync()
+        rt.rt.check()
+        return rt
+
+    mono = runf(lambda dg: [0] * dg.g.num_kernels, 1)
+    dis = runf(lambda dg: dg.role_assign(0, 1), 2)
+    assert np.array_equal(mono.residual(), dis.residual())
+    one = run(DEC, cfg, inp, lambda dg: [0] * dg.g.num_kernels, 1, steps=1)
+    r_ref, _, _ = OL.decoder_step(inp, act="bf16")
+    dg = DEC.DecoderGraph(cfg, fuse_silu=True)
+    rt = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp)
+    rt.step()
+    rt.sync()
+    assert relerr(rt.residual(), r_ref) < 5e-3
+    assert relerr(one.residual(), r_ref) < 5e-3

@@ -288,3 +288,30 @@ def test_attention_fp32_1e5(kd, rows, Hq, Hkv, D, C):
     ref = OL.paged_decode_attention(OL.bf16_to_f64(q), OL.bf16_to_f64(kc), OL.bf16_to_f64(vc), bt, sl, Hq, Hkv, D,
                                     16, "fp32")
     assert relerr(host_f64(out), ref) < 1e-5
+
+
+# ------------------------------------------------------------------ a9+a8 fused (KD_OP_GEMM_SILU)
+@pytest.mark.parametrize("M,F,K_", [(1, 1024, 256), (64, 14336, 4096), (33, 512, 1000)])
+def test_gemm_silu_fused_equals_pair(kd, M, F, K_, monkeypatch):
+    """Fused gate_up + SiLU·mul: within tolerance of the oracle's a9 → a8, and
+    bit-identical to the GPU pair when both GEMMs run the same stream-K split."""
+    api, K = kd
+    torch = _torch()
+    monkeypatch.setenv("KD_GEMM_STREAMK", "1")
+    g = synth.rng(M * 5 + F + K_)
+    X = synth.normal_bf16(g, (M, K_))
+    W = synth.normal_bf16(g, (2 * F, K_), 1 / math.sqrt(K_))
+    a = K.kd_attr_gemm(M, 2 * F, K_, K.KD_BF16)
+    scr = scratch_for(api, K.KD_OP_GEMM_SILU, a)
+    Xd, Wd = dev_bf16(X), dev_bf16(W)
+    out = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    api.gemm_silu(a, Xd, Wd, out, scr)
+    gu = torch.empty(M, 2 * F, dtype=torch.bfloat16, device="cuda")
+    api.gemm(a, Xd, Wd, gu, scratch_for(api, K.KD_OP_GEMM, a))
+    pair = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    api.silu_mul(K.kd_attr_silu_mul(M, F, K.KD_BF16, 0), gu, pair)
+    torch.cuda.synchronize()
+    assert torch.equal(out, pair), "fused gate_up+SiLU differs from the GEMM → SiLU pair"
+    rows = np.arange(M) if M * F * K_ <= 2 ** 28 else np.array([0, M // 2, M - 1])
+    ref = OL.silu_mul_blocked(OL.linear(OL.bf16_to_f64(X[rows]), OL.bf16_to_f64(W), "bf16"), act="bf16")
+    assert relerr(host_f64(out)[rows], ref) < 5e-3
