@@ -371,7 +371,7 @@ def main():
     kernels = None
     if args.kernels:
         kernels = {}
-        for op, nm in ((K.KD_OP_GEMM, "gemm"), (K.KD_OP_ADD_RMSNORM, "add_rmsnorm"),
+        for op, nm in ((K.KD_OP_GEMM, "gemm"), (K.KD_OP_GEMM_SILU, "gemm_silu"), (K.KD_OP_ADD_RMSNORM, "add_rmsnorm"),
                        (K.KD_OP_ROPE_APPEND, "rope_append"), (K.KD_OP_SILU_MUL, "silu_mul")):
             rt.rt.profile_op(op)
             rt.rt.prepare()
