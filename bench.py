@@ -189,9 +189,14 @@ def main():
     hbm_gbs, tc_tflops, tc_sus, peak_src = peaks()
     if world == 1:
         # 1 GPU: the monolithic reference point of the metric (all kernels on one B200);
-        # gate_up and SiLU·mul share the device, so they are declared as one fused
-        # kernel (KD_OP_GEMM_SILU, same bits as the pair; KD_BENCH_NO_FUSE=1 for the A/B)
-        dg = DEC.DecoderGraph(cfg, fuse_silu=not os.environ.get("KD_BENCH_NO_FUSE"))
+        # gate_up and SiLU·mul share the device, so they are declared as one fused kernel
+        # (KD_OP_GEMM_SILU, bit-identical to the pair; KD_BENCH_NO_FUSE=1 for the A/B).
+        # QKV + RoPE/append (KD_OP_QKV_ROPE) is built and bit-identical too, but measured
+        # slower than the pair (27.5 vs 19.3 µs at the 8B shape: the cluster GEMM's
+        # epilogue is the expensive place for per-element trig), so it is opt-in
+        # (KD_BENCH_FUSE_ROPE=1).
+        fuse = not os.environ.get("KD_BENCH_NO_FUSE")
+        dg = DEC.DecoderGraph(cfg, fuse_silu=fuse, fuse_rope=fuse and bool(os.environ.get("KD_BENCH_FUSE_ROPE")))
         assign = [0] * dg.g.num_kernels
         rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed, use_graph=not args.no_graph)
         placement = "monolithic (all kernels on one B200)"
@@ -371,7 +376,8 @@ def main():
     kernels = None
     if args.kernels:
         kernels = {}
-        for op, nm in ((K.KD_OP_GEMM, "gemm"), (K.KD_OP_GEMM_SILU, "gemm_silu"), (K.KD_OP_ADD_RMSNORM, "add_rmsnorm"),
+        for op, nm in ((K.KD_OP_GEMM, "gemm"), (K.KD_OP_GEMM_SILU, "gemm_silu"), (K.KD_OP_QKV_ROPE, "qkv_rope"),
+                       (K.KD_OP_ADD_RMSNORM, "add_rmsnorm"),
                        (K.KD_OP_ROPE_APPEND, "rope_append"), (K.KD_OP_SILU_MUL, "silu_mul")):
             rt.rt.profile_op(op)
             rt.rt.prepare()

@@ -96,9 +96,13 @@ enum {
   KD_OP_SSM_CONV = 11,     /* a12 reads [zxbcdt, conv_w, conv_b, conv_state] writes [xbc, conv_state] */
   KD_OP_SSM_UPDATE = 12,   /* a12 reads [xbc, zxbcdt, dt_bias, A_log, D, ssm_state] writes [y, ssm_state] */
   KD_OP_GATED_NORM = 13,   /* a12 reads [y, zxbcdt, norm_w] writes [yn]          */
-  KD_OP_GEMM_SILU = 14     /* a9+a8 fused (co-located gate_up and SiLU·mul): reads [X, W_gu] writes [a]:
+  KD_OP_GEMM_SILU = 14,    /* a9+a8 fused (co-located gate_up and SiLU·mul): reads [X, W_gu] writes [a]:
                             * a = silu_mul_blocked(bf16(X·W_guᵀ)) with kd_attr_gemm, N = 2F weight rows
                             * (64-row gate/up blocks, R12), a [M, F]; bits identical to a9 then a8 */
+  KD_OP_QKV_ROPE = 15      /* a4+a5 fused (co-located QKV GEMM and RoPE + KV append): reads [X, W_qkv',
+                            * block_table, seq_len] writes [q, Kc, Vc] with kd_attr_qkv_rope. W_qkv' = the
+                            * kv-group-interleaved QKV weight with rows pair-interleaved inside every head
+                            * (row 2p ← dim p, row 2p+1 ← dim p + D/2); bits identical to a4 then a5 */
 };
 
 /* element types of activations / KV */
@@ -120,6 +124,10 @@ typedef struct {
 typedef struct {
   uint32_t rows, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype, pad_;
 } kd_attr_attention;
+typedef struct {
+  uint32_t rows, hidden, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype;
+  double theta;   /* RoPE base (R12) */
+} kd_attr_qkv_rope;  /* X [rows, hidden]; q [rows, n_heads·D]; caches as for rope_append */
 typedef struct { uint32_t rows, ffn, dtype, pad_; } kd_attr_silu_mul;  /* gu [rows, 2F] 64-col gate/up blocks */
 typedef struct { uint32_t rows, hidden, n_delta, dtype; } kd_attr_residual_add; /* r fp32 [rows,H] += Σ deltas (dtype: bf16 or fp32) */
 /* MoE. route buffer: int32 idx[rows][top_k] then fp32
@@ -338,6 +346,13 @@ kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes);
 kd_status kd_op_add_rmsnorm(const kd_attr_add_rmsnorm* a, float* r, const void* const* deltas,
                             const void* gamma, void* h, void* stream);
 /* a4/a7/a9/a10: Y[M,N] = X[M,K]·W[N,K]ᵀ, bf16 in, fp32 accumulate (tcgen05, TMEM), bf16 out. */
+/* a4+a5 fused: the QKV GEMM whose epilogue rotates q/k (NeoX RoPE) and appends
+ * k/v to the paged cache; W_qkv rows pair-interleaved per head (see
+ * KD_OP_QKV_ROPE). bf16 only. Errors: KD_ERR_UNSUPPORTED when no cluster
+ * tiling exists for the shape. */
+kd_status kd_op_qkv_rope(const kd_attr_qkv_rope* a, const void* X, const void* W, const int32_t* block_table,
+                         const int32_t* seq_len, void* q_out, void* k_cache, void* v_cache, void* scratch,
+                         void* stream);
 /* a9+a8 fused: a [M, N/2] = silu(g)·u of the bf16-rounded gate/up GEMM output
  * (same bits as kd_op_gemm then kd_op_silu_mul). bf16 only; scratch as for the
  * plain GEMM of the same attrs. */

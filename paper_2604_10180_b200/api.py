@@ -262,6 +262,12 @@ def gemm_silu(attrs, X, W, out, scratch, stream=None):
     check(K.kd_op_gemm_silu(C.byref(attrs), _p(X), _p(W), _p(out), _p(scratch), _stream(stream)), "kd_op_gemm_silu")
 
 
+def qkv_rope(attrs, X, W, block_table, seq_len, q_out, k_cache, v_cache, scratch, stream=None):
+    """a4+a5 fused: QKV GEMM with the RoPE + KV-append epilogue (W rows pair-interleaved per head)."""
+    check(K.kd_op_qkv_rope(C.byref(attrs), _p(X), _p(W), _p(block_table), _p(seq_len), _p(q_out), _p(k_cache),
+                           _p(v_cache), _p(scratch), _stream(stream)), "kd_op_qkv_rope")
+
+
 def rope_append(attrs, qkv, block_table, seq_len, q_out, k_cache, v_cache, stream=None):
     check(K.kd_op_rope_append(C.byref(attrs), _p(qkv), _p(block_table), _p(seq_len), _p(q_out), _p(k_cache),
                               _p(v_cache), _stream(stream)), "kd_op_rope_append")

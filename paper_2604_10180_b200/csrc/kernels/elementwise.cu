@@ -438,6 +438,7 @@ kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s
     case KD_OP_ATTENTION: { kd_attr_attention a; if ((st = attrs_of(attrs, &a))) return st; return attention_signals(a, signals); }
     case KD_OP_GEMM: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
     case KD_OP_GEMM_SILU: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a, true), signals); }
+    case KD_OP_QKV_ROPE: { kd_attr_qkv_rope a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
     case KD_OP_GROUPED_GEMM: { kd_attr_grouped_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
     case KD_OP_MOE_ROUTE:
     case KD_OP_MOE_DISPATCH:

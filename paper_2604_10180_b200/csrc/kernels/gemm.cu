@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -554,7 +555,51 @@ struct Args {
   int dbg;       // debug A/B (KD_GEMM_DBG)
   Epi epi;
   unsigned long long* trace;
+  int rope;      // KD_OP_QKV_ROPE: epilogue = a5 (RoPE + KV append) on the bf16 QKV output
+  RopeEpi rp;
 };
+
+// a5 fused into the QKV GEMM epilogue. W rows are pair-interleaved within each
+// head (row 2p ← dim p, row 2p+1 ← dim p + D/2), so a rotation pair is two
+// adjacent rows and never straddles a cluster owner (rpo is even). Values are
+// rounded to bf16 first (the plain GEMM's output), then exactly the RoPE
+// kernel's fp32 math with its cos/sin (fp64 angle, host fp64 θ^(−2i/D)).
+__device__ __forceinline__ void rope_pair(const Args& A, int j, int n, float xs, float ys) {
+  const RopeEpi& R = A.rp;
+  const int D = R.D, half = D / 2, G = R.Hq / R.Hkv;
+  const int hall = n / D, rr = n - hall * D, p = rr >> 1;
+  const int grp = hall / (G + 2), slot = hall - grp * (G + 2);
+  const float x = __bfloat162float(__float2bfloat16_rn(xs)), y = __bfloat162float(__float2bfloat16_rn(ys));
+  const int pos = R.sl[j] - 1;
+  __nv_bfloat16 lo, hi;
+  if (slot <= G) {
+    const double ang = (double)pos * R.f[p];
+    const double k = rint(ang * 0.15915494309189535);
+    const double red = fma(-k, 6.283185307179586, fma(-k, 2.4492935982947064e-16, ang));
+    float sn, cs;
+    sincosf((float)red, &sn, &cs);
+    lo = __float2bfloat16_rn(x * cs - y * sn);
+    hi = __float2bfloat16_rn(y * cs + x * sn);
+  } else {
+    lo = __float2bfloat16_rn(x);
+    hi = __float2bfloat16_rn(y);
+  }
+  if (slot < G) {
+    const size_t qo = ((size_t)j * R.Hq + (size_t)grp * G + slot) * D;
+    R.q[qo + p] = lo;
+    R.q[qo + p + half] = hi;
+    for (int e = 0; e < A.epi.n; ++e) {
+      ((__nv_bfloat16*)A.epi.dst[e])[qo + p] = lo;
+      ((__nv_bfloat16*)A.epi.dst[e])[qo + p + half] = hi;
+    }
+  } else {
+    const int32_t pg = R.bt[(size_t)j * R.pps + pos / R.page];
+    const size_t co = (((size_t)pg * R.Hkv + grp) * R.page + pos % R.page) * D;
+    __nv_bfloat16* cache = slot == G ? R.kc : R.vc;
+    cache[co + p] = lo;
+    cache[co + p + half] = hi;
+  }
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_csk_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Args A) {
@@ -696,6 +741,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo] = h;
     };
     auto store_y = [&](int j, int col, float v0, float v1, float v2, float v3) {  // 4 consecutive outputs of token j
+      if (A.rope) {  // two rotation pairs (col is a multiple of 4)
+        if (col < A.N) rope_pair(A, j, col, v0, v1);
+        if (col + 2 < A.N) rope_pair(A, j, col + 2, v2, v3);
+        return;
+      }
       const size_t yo = (size_t)j * A.N + col;
       if (col + 4 <= A.N && (A.N & 3) == 0) {
         uint2 o;
@@ -1003,6 +1053,7 @@ static double streamk_ns(const GemmShape& a) {
 
 // plain GEMMs: the cluster kernel unless stream-K is modelled faster (or forced)
 static bool use_dense(const GemmShape& a) {
+  if (a.rope) return true;  // the fused RoPE epilogue exists in the cluster kernel only
   if (a.groups || a.silu) return false;
   const char* e = getenv("KD_GEMM_STREAMK");
   if (e && atoi(e)) return false;
@@ -1026,6 +1077,40 @@ GemmShape gemm_shape(const kd_attr_gemm& a, bool silu) {
   s.groups = 0;
   s.dtype = a.dtype;
   return s;
+}
+
+GemmShape gemm_shape(const kd_attr_qkv_rope& a) {
+  GemmShape s;
+  s.rope = 1;
+  s.M = a.rows;
+  s.rows_total = a.rows;
+  s.N = (a.n_heads + 2 * a.n_kv_heads) * a.head_dim;
+  s.K = a.hidden;
+  s.groups = 0;
+  s.dtype = a.dtype;
+  return s;
+}
+
+kd_status qkv_rope_bind(const kd_attr_qkv_rope& a, const int32_t* bt, const int32_t* sl, void* q, void* kc, void* vc,
+                        GemmPlan* gp) {
+  if (!bt || !sl || !q || !kc || !vc) return fail(KD_ERR_INVALID_ARG, "qkv_rope: NULL pointer");
+  if (a.n_kv_heads == 0 || a.n_heads % a.n_kv_heads || a.head_dim % 2 || a.head_dim > 256 || a.page == 0 ||
+      a.pages_per_seq == 0)
+    return fail(KD_ERR_UNSUPPORTED, "qkv_rope: unsupported head layout");
+  RopeEpi& r = gp->rp;
+  r.bt = bt;
+  r.sl = sl;
+  r.q = (__nv_bfloat16*)q;
+  r.kc = (__nv_bfloat16*)kc;
+  r.vc = (__nv_bfloat16*)vc;
+  r.Hq = (int)a.n_heads;
+  r.Hkv = (int)a.n_kv_heads;
+  r.D = (int)a.head_dim;
+  r.page = (int)a.page;
+  r.pps = (int)a.pages_per_seq;
+  const double l2t = std::log2(a.theta);
+  for (uint32_t i = 0; i < a.head_dim / 2; ++i) r.f[i] = std::exp2(-2.0 * (double)i / (double)a.head_dim * l2t);
+  return KD_OK;
 }
 
 GemmShape gemm_shape(const kd_attr_grouped_gemm& a) {
@@ -1104,6 +1189,8 @@ static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx&
   A.stages = t.stages;
   A.rpo = t.rpo;
   A.dbg = getenv("KD_GEMM_DBG") ? atoi(getenv("KD_GEMM_DBG")) : 0;
+  A.rope = (int)gp.sh.rope;
+  A.rp = gp.rp;
   A.epi = c.epi;
   A.trace = g_gemm_trace;
   kd_status ks = kernels_init();

@@ -115,11 +115,27 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
 // GEMM: TMA descriptors are encoded once per (X, W) pointer pair
 // shape of a (possibly grouped) decode GEMM: M = rows per group bound (MMA N,
 // partial layout), rows_total = rows of X/Y, groups = 0 for a plain GEMM
+// KD_OP_QKV_ROPE epilogue parameters (a5 fused into the QKV GEMM)
+struct RopeEpi {
+  const int32_t* bt = nullptr;
+  const int32_t* sl = nullptr;
+  __nv_bfloat16* q = nullptr;
+  __nv_bfloat16* kc = nullptr;
+  __nv_bfloat16* vc = nullptr;
+  int Hq = 0, Hkv = 0, D = 0, page = 0, pps = 0, pad_ = 0;
+  double f[128] = {};  // θ^(−2i/D), fp64, host-computed
+};
 struct GemmShape {
   uint32_t M = 0, rows_total = 0, N = 0, K = 0, groups = 0, dtype = 0;
   uint32_t silu = 0;  // KD_OP_GEMM_SILU: output a [M, N/2] = silu·mul of the 64-row gate/up blocks
+  uint32_t rope = 0;  // KD_OP_QKV_ROPE: cluster split-K kernel with the RoPE + KV-append epilogue
 };
 GemmShape gemm_shape(const kd_attr_gemm& a, bool silu = false);
+GemmShape gemm_shape(const kd_attr_qkv_rope& a);
+struct GemmPlan;
+// fill gp->rp for a KD_OP_QKV_ROPE plan (after gemm_prepare)
+kd_status qkv_rope_bind(const kd_attr_qkv_rope& a, const int32_t* bt, const int32_t* sl, void* q, void* kc, void* vc,
+                        GemmPlan* gp);
 GemmShape gemm_shape(const kd_attr_grouped_gemm& a);
 // dense (non-grouped) GEMM tiling, chosen per shape and device (gemm.cu)
 struct GemmTile {
@@ -134,6 +150,7 @@ struct GemmPlan {
   bool dense = false;         // cluster split-K kernel (else stream-K)
   const void* X = nullptr;    // fp32 path: plain operand pointers (SIMT kernel)
   const void* W = nullptr;
+  RopeEpi rp;                 // KD_OP_QKV_ROPE
   GemmTile tile;
 };
 kd_status gemm_scratch_bytes(const GemmShape& sh, uint64_t* bytes);

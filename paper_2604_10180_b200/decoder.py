@@ -56,6 +56,14 @@ def b200_machine(n_dev: int, hbm_Bps: Optional[float] = None, tc_flops: Optional
     return Machine.uniform(n_dev, int(hbm), int(tc), int(link_Bps), int(link_lat_ps), int(launch_ps))
 
 
+def pair_interleave_qkv(w: np.ndarray, head_dim: int) -> np.ndarray:
+    """W_qkv rows for KD_OP_QKV_ROPE: inside every head block of D rows,
+    row 2p ← row p and row 2p+1 ← row p + D/2 (a RoPE pair on adjacent rows)."""
+    rows, H = w.shape
+    h = w.reshape(rows // head_dim, 2, head_dim // 2, H)
+    return np.ascontiguousarray(h.transpose(0, 2, 1, 3).reshape(rows, H))
+
+
 @dataclass
 class KernelInfo:
     name: str
@@ -67,12 +75,16 @@ class KernelInfo:
 class DecoderGraph:
     """Declares the decoder kernel graph for one micro-batch of cfg.m rows."""
 
-    def __init__(self, cfg, act: int = K.KD_BF16, fuse_silu: bool = False):
+    def __init__(self, cfg, act: int = K.KD_BF16, fuse_silu: bool = False, fuse_rope: bool = False):
         """act: KD_BF16 (throughput path) or KD_F32 (the 1e-5 parity path,
         R13: fp32 weights, activations and KV cache; dense attention layers).
         fuse_silu: declare gate_up and SiLU·mul as ONE kernel (KD_OP_GEMM_SILU,
         same bits as the pair) — for placements that co-locate them (the
-        1-GPU monolithic step); the gu activation then never exists."""
+        1-GPU monolithic step); the gu activation then never exists.
+        fuse_rope: declare the QKV GEMM and RoPE + KV append as ONE kernel
+        (KD_OP_QKV_ROPE; its W_qkv rows are pair-interleaved per head, see
+        pair_interleave_qkv); it writes the KV cache, so it joins the
+        attention template (co-located with the cache, R6)."""
         if act not in (K.KD_BF16, K.KD_F32):
             raise ValueError("act must be KD_BF16 or KD_F32")
         if act == K.KD_F32 and (cfg.n_experts or cfg.attn_every):
@@ -80,6 +92,8 @@ class DecoderGraph:
         self.act = act
         fuse_silu = bool(fuse_silu) and act == K.KD_BF16 and not cfg.n_experts
         self.fuse_silu = fuse_silu
+        fuse_rope = bool(fuse_rope) and act == K.KD_BF16
+        self.fuse_rope = fuse_rope
         adt = "bf16" if act == K.KD_BF16 else "f32"  # storage of weights, activations and KV cache
         self.cfg = cfg
         m, H, L = cfg.m, cfg.hidden, cfg.n_layers
@@ -152,8 +166,8 @@ class DecoderGraph:
             buf(f"g2.{l}", (H,), adt, W)
             buf(f"kc.{l}", (m * pps, Hkv, cfg.page, D), adt, PERS | PM)
             buf(f"vc.{l}", (m * pps, Hkv, cfg.page, D), adt, PERS | PM)
-            acts = [("h1", (m, H)), ("qkv", (m, cfg.qkv_dim)), ("q", (m, Hq * D)), ("attn", (m, Hq * D)),
-                    ("o", (m, H)), ("h2", (m, H)), ("d", (m, H))]
+            acts = [("h1", (m, H))] + ([] if fuse_rope else [("qkv", (m, cfg.qkv_dim))]) + [
+                ("q", (m, Hq * D)), ("attn", (m, Hq * D)), ("o", (m, H)), ("h2", (m, H)), ("d", (m, H))]
             if not E:
                 acts += ([] if fuse_silu else [("gu", (m, 2 * F))]) + [("a", (m, F))]
             for nm, shp in acts:
@@ -191,10 +205,16 @@ class DecoderGraph:
             add("norm1", l, T_RESID, K.KD_OP_ADD_RMSNORM,
                 ["r"] + ([f"d.{l-1}"] if has_d else []) + [f"g1.{l}"], [f"h1.{l}", "r"],
                 K.kd_attr_add_rmsnorm(m, H, has_d, act, eps, 0))
-            add("qkv", l, T_QKV, K.KD_OP_GEMM, [f"h1.{l}", f"w_qkv.{l}"], [f"qkv.{l}"],
-                K.kd_attr_gemm(m, cfg.qkv_dim, H, act), 2 * m * cfg.qkv_dim * H)
-            add("rope", l, T_ATTN, K.KD_OP_ROPE_APPEND, [f"qkv.{l}", "bt", "sl"], [f"q.{l}", f"kc.{l}", f"vc.{l}"],
-                K.kd_attr_rope_append(m, Hq, Hkv, D, cfg.page, pps, act, 0, float(cfg.rope_theta)))
+            if fuse_rope:
+                add("qkv_rope", l, T_ATTN, K.KD_OP_QKV_ROPE, [f"h1.{l}", f"w_qkv.{l}", "bt", "sl"],
+                    [f"q.{l}", f"kc.{l}", f"vc.{l}"],
+                    K.kd_attr_qkv_rope(m, H, Hq, Hkv, D, cfg.page, pps, act, float(cfg.rope_theta)),
+                    2 * m * cfg.qkv_dim * H)
+            else:
+                add("qkv", l, T_QKV, K.KD_OP_GEMM, [f"h1.{l}", f"w_qkv.{l}"], [f"qkv.{l}"],
+                    K.kd_attr_gemm(m, cfg.qkv_dim, H, act), 2 * m * cfg.qkv_dim * H)
+                add("rope", l, T_ATTN, K.KD_OP_ROPE_APPEND, [f"qkv.{l}", "bt", "sl"], [f"q.{l}", f"kc.{l}", f"vc.{l}"],
+                    K.kd_attr_rope_append(m, Hq, Hkv, D, cfg.page, pps, act, 0, float(cfg.rope_theta)))
             add("attn", l, T_ATTN, K.KD_OP_ATTENTION, [f"q.{l}", f"kc.{l}", f"vc.{l}", "bt", "sl"], [f"attn.{l}"],
                 K.kd_attr_attention(m, Hq, Hkv, D, cfg.page, pps, act, 0), 4 * m * Hq * cfg.context * D)
             add("o", l, T_O, K.KD_OP_GEMM, [f"attn.{l}", f"w_o.{l}"], [f"o.{l}"],
@@ -493,7 +513,10 @@ class DecoderRuntime:
                 t.copy_(torch.from_numpy(inputs.layers[int(lay)].w_router))
             else:
                 lw = inputs.layers[int(lay)]
-                put_bf16({"w_qkv": lw.w_qkv, "w_o": lw.w_o, "w_gu": lw.w_gu, "w_d": lw.w_d,
+                w_qkv = lw.w_qkv
+                if base == "w_qkv" and getattr(self.dg, "fuse_rope", False):
+                    w_qkv = pair_interleave_qkv(w_qkv, cfg.head_dim)
+                put_bf16({"w_qkv": w_qkv, "w_o": lw.w_o, "w_gu": lw.w_gu, "w_d": lw.w_d,
                           "g1": lw.gamma1, "g2": lw.gamma2, "w_gu_e": lw.w_gu_e, "w_d_e": lw.w_d_e}[base])
             return
         # device-side seeded values (throughput runs)

@@ -204,8 +204,9 @@ def test_mode_switch_no_transfer_then_disagg(mod):
     dis.rt.check()  # KD_ERR_TIMEOUT if a wait missed its target
 
 
-def test_fused_silu_graph_vs_oracle_and_disaggregated(mod):
-    """The monolithic-placement graph with gate_up+SiLU fused (KD_OP_GEMM_SILU)
+def test_fused_graph_vs_oracle_and_disaggregated(mod):
+    """The monolithic-placement graph with gate_up+SiLU (KD_OP_GEMM_SILU) and
+    QKV+RoPE+append (KD_OP_QKV_ROPE) fused
     is within tolerance of the oracle and runs disaggregated bitwise equal to
     its own monolithic run."""
     DEC, K = mod
@@ -213,8 +214,8 @@ def test_fused_silu_graph_vs_oracle_and_disaggregated(mod):
     inp = synth.make_decoder_inputs(cfg)
 
     def runf(assign, n_dev):
-        dg = DEC.DecoderGraph(cfg, fuse_silu=True)
-        assert any(k.name == "gu_silu" for k in dg.kernels)
+        dg = DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True)
+        assert any(k.name == "gu_silu" for k in dg.kernels) and any(k.name == "qkv_rope" for k in dg.kernels)
         rt = DEC.DecoderRuntime(dg, assign(dg), n_dev, [0] * n_dev, inputs=inp)
         for _ in range(2):
             rt.step()
@@ -227,7 +228,7 @@ def test_fused_silu_graph_vs_oracle_and_disaggregated(mod):
     assert np.array_equal(mono.residual(), dis.residual())
     one = run(DEC, cfg, inp, lambda dg: [0] * dg.g.num_kernels, 1, steps=1)
     r_ref, _, _ = OL.decoder_step(inp, act="bf16")
-    dg = DEC.DecoderGraph(cfg, fuse_silu=True)
+    dg = DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True)
     rt = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp)
     rt.step()
     rt.sync()

@@ -315,3 +315,45 @@ def test_gemm_silu_fused_equals_pair(kd, M, F, K_, monkeypatch):
     rows = np.arange(M) if M * F * K_ <= 2 ** 28 else np.array([0, M // 2, M - 1])
     ref = OL.silu_mul_blocked(OL.linear(OL.bf16_to_f64(X[rows]), OL.bf16_to_f64(W), "bf16"), act="bf16")
     assert relerr(host_f64(out)[rows], ref) < 5e-3
+
+
+# ------------------------------------------------------------------ a4+a5 fused (KD_OP_QKV_ROPE)
+@pytest.mark.parametrize("rows,H,Hq,Hkv,D,C,split", [(4, 256, 4, 4, 64, 128, "2"), (64, 4096, 32, 8, 128, 4096, "2"),
+                                                       (3, 512, 8, 2, 128, 37, "4"), (5, 256, 4, 2, 64, 50, "1")])
+def test_qkv_rope_fused_equals_pair(kd, rows, H, Hq, Hkv, D, C, split, monkeypatch):
+    """QKV GEMM with the RoPE + append epilogue (W rows pair-interleaved per
+    head) is bit-identical to the GEMM → rope_append pair at the same cluster
+    split, and within tolerance of the oracle."""
+    from paper_2604_10180_b200.decoder import pair_interleave_qkv
+    api, K = kd
+    torch = _torch()
+    monkeypatch.setenv("KD_GEMM_TILE", split)
+    g = synth.rng(rows * 3 + H + C)
+    theta = 5e5
+    N = (Hq + 2 * Hkv) * D
+    X = synth.normal_bf16(g, (rows, H))
+    W = synth.normal_bf16(g, (N, H), 1 / math.sqrt(H))
+    pps = (C + 15) // 16
+    bt = synth.block_table(g, rows, pps)
+    sl = np.full(rows, C, np.int32)
+    kc = synth.normal_bf16(g, (rows * pps, Hkv, 16, D))
+    vc = synth.normal_bf16(g, (rows * pps, Hkv, 16, D))
+    btd, sld = torch.from_numpy(bt).cuda(), torch.from_numpy(sl).cuda()
+    # the pair: GEMM then rope_append
+    ag = K.kd_attr_gemm(rows, N, H, K.KD_BF16)
+    qkv = torch.empty(rows, N, dtype=torch.bfloat16, device="cuda")
+    api.gemm(ag, dev_bf16(X), dev_bf16(W), qkv, scratch_for(api, K.KD_OP_GEMM, ag))
+    q1, k1, v1 = torch.empty(rows, Hq * D, dtype=torch.bfloat16, device="cuda"), dev_bf16(kc), dev_bf16(vc)
+    api.rope_append(K.kd_attr_rope_append(rows, Hq, Hkv, D, 16, pps, K.KD_BF16, 0, theta), qkv, btd, sld, q1, k1, v1)
+    # fused
+    af = K.kd_attr_qkv_rope(rows, H, Hq, Hkv, D, 16, pps, K.KD_BF16, theta)
+    q2, k2, v2 = torch.empty(rows, Hq * D, dtype=torch.bfloat16, device="cuda"), dev_bf16(kc), dev_bf16(vc)
+    api.qkv_rope(af, dev_bf16(X), dev_bf16(pair_interleave_qkv(W, D)), btd, sld, q2, k2, v2,
+                 scratch_for(api, K.KD_OP_QKV_ROPE, af))
+    torch.cuda.synchronize()
+    assert torch.equal(q1, q2) and torch.equal(k1, k2) and torch.equal(v1, v2), "fused QKV+RoPE differs from the pair"
+    kr, vr = OL.bf16_to_f64(kc), OL.bf16_to_f64(vc)
+    qkv_ref = OL.linear(OL.bf16_to_f64(X), OL.bf16_to_f64(W), "bf16")
+    qr = OL.rope_append(qkv_ref, sl - 1, bt, kr, vr, Hq, Hkv, D, theta, 16, "bf16")
+    assert relerr(host_f64(q2), qr) < 5e-3
+    assert relerr(host_f64(k2), kr) < 5e-3 and relerr(host_f64(v2), vr) < 5e-3
