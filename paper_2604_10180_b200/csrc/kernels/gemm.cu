@@ -601,6 +601,32 @@ __device__ __forceinline__ void rope_pair(const Args& A, int j, int n, float xs,
   }
 }
 
+// 4 consecutive outputs (weight rows col..col+3) of token j → Y (+ peers), or
+// the fused RoPE/append epilogue
+__device__ __forceinline__ void csk_store4(const Args& A, int j, int col, float v0, float v1, float v2, float v3) {
+  if (A.rope) {
+    if (col < A.N) rope_pair(A, j, col, v0, v1);
+    if (col + 2 < A.N) rope_pair(A, j, col + 2, v2, v3);
+    return;
+  }
+  const size_t yo = (size_t)j * A.N + col;
+  if (col + 4 <= A.N && (A.N & 3) == 0) {
+    uint2 o;
+    o.x = pack_bf16(v0, v1);
+    o.y = pack_bf16(v2, v3);
+    *reinterpret_cast<uint2*>(A.Y + yo) = o;
+    for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+  } else {
+    const float vv[4] = {v0, v1, v2, v3};
+    for (int x = 0; x < 4; ++x)
+      if (col + x < A.N) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(vv[x]);
+        A.Y[yo + x] = h;
+        for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = h;
+      }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_csk_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Args A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -814,26 +840,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
       }
       if (ep == 0) { KD_TRACE(7); KD_CTRACE(22); KD_TRACE(10); KD_CTRACE(23); }
-      named_bar(1, 128);           // my own rows are in recv[rank]
-      mbar_wait(rbar, 0);          // the peers' rows have landed (st.async complete_tx)
-      if (ep == 0) { KD_TRACE(8); KD_CTRACE(24); }
-      pdl_wait();
-      // my rows [rank·rpo, +my_rows): Σ over ranks in order; lanes walk tokens
-      // (conflict-free column reads), each thread 4 consecutive weight rows
-      const int r4n = my_rows / 4;  // rpo and 128 are multiples of 4
-      for (int e = ep; e < M * r4n; e += 128) {
-        const int lr4 = (e / M) * 4, j = e - (e / M) * M;
-        float acc[4];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) acc[x] = recv[((size_t)0 * rpo + lr4 + x) * P + j];
-        for (int cr = 1; cr < split; ++cr)  // rank order → deterministic
-#pragma unroll
-          for (int x = 0; x < 4; ++x) acc[x] += recv[((size_t)cr * rpo + lr4 + x) * P + j];
-        const int col = n0 + rank * rpo + lr4;
-        if (col < A.N) store_y(j, col, acc[0], acc[1], acc[2], acc[3]);
-      }
-      stored = my_rows > 0;
-      if (ep == 0) { KD_TRACE(11); KD_CTRACE(25); }
+      // the owner's sum runs after the role branches with all 8 warps
     }
     if (A.epi.n && stored) {  // publish this CTA's stores to the consumer devices
       named_bar(1, 128);
@@ -843,6 +850,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (ep == 0) { KD_TRACE(9); KD_CTRACE(26); }
+  }
+  if (split > 1) {
+    // ---- owner sum with all 256 threads (the TMA/MMA warps are idle by now):
+    // my rows [rank·rpo, +my_rows), Σ over ranks in order; lanes walk tokens
+    // (conflict-free column reads), each thread 4 consecutive weight rows
+    __syncthreads();            // my own rows are in recv[rank]
+    mbar_wait(rbar, 0);         // the peers' rows have landed (st.async complete_tx)
+    if (threadIdx.x == 128) { KD_TRACE(8); KD_CTRACE(24); }
+    pdl_wait();
+    const int rpo = A.rpo, r4n = my_rows / 4;  // rpo and 128 are multiples of 4
+    for (int e = threadIdx.x; e < M * r4n; e += kThreads) {
+      const int lr4 = (e / M) * 4, j = e - (e / M) * M;
+      float acc[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) acc[x] = recv[((size_t)lr4 + x) * P + j];
+      for (int cr = 1; cr < split; ++cr)  // rank order → deterministic
+#pragma unroll
+        for (int x = 0; x < 4; ++x) acc[x] += recv[((size_t)cr * rpo + lr4 + x) * P + j];
+      csk_store4(A, j, n0 + rank * rpo + lr4, acc[0], acc[1], acc[2], acc[3]);
+    }
+    if (threadIdx.x == 128) { KD_TRACE(11); KD_CTRACE(25); }
+    if (A.epi.n && my_rows > 0) {  // publish this CTA's stores to the consumer devices
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_acq_rel_sys();
+        for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
+      }
+    }
   }
   // No closing cluster barrier: peers only ever WRITE into this CTA's recv
   // (st.async), and the epilogue waits for all of those bytes on rbar before
