@@ -540,7 +540,8 @@ static EncodeTiledFn get_encode() {
 // 32-48 tiles cannot fill 148 SMs without splitting K.
 namespace csk {
 
-constexpr int kThreads = 256;  // w0 TMA, w1 MMA + TMEM alloc, w4..w7 epilogue
+constexpr int kThreads = 384;  // w0 TMA, w1 MMA + TMEM alloc, w4..w11 epilogue (2 warps per TMEM lane quarter)
+constexpr int kEpi = kThreads - 128;
 constexpr int kSmemMax = 227 * 1024;
 
 struct Args {
@@ -755,7 +756,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
-    const int q = warp - 4, ep = threadIdx.x - 128;
+    // 8 warps: warp w reads TMEM lane quarter (w − 4) mod 4 (its hardware
+    // quarter), token-column chunks of 16 alternating between the two halves
+    const int q = (warp - 4) & 3, half = (warp - 4) >> 2, ep = threadIdx.x - 128;
     const int row = q * 32 + lane;  // weight row within the tile = TMEM lane
     mbar_wait_sleep(tfull, 0, 128);
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -790,16 +793,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (split == 1) {
       // TMEM → fp32 staging [M][128] (thread = row: conflict-free) → 4-wide bf16 stores
       float* st = send;
-      for (int j0 = 0; j0 < M; j0 += kChunk) {
+      for (int j0 = half * kChunk; j0 < M; j0 += 2 * kChunk) {
         float v[kChunk];
         tmem_ld16(tbase + j0, v);
 #pragma unroll
         for (int j = 0; j < kChunk; ++j)
           if (j0 + j < M) st[(size_t)(j0 + j) * kBM + row] = v[j];
       }
-      named_bar(1, 128);
+      named_bar(1, kEpi);
       pdl_wait();
-      for (int e = ep; e < M * (kBM / 4); e += 128) {
+      for (int e = ep; e < M * (kBM / 4); e += kEpi) {
         const int j = e / (kBM / 4), r4 = (e % (kBM / 4)) * 4;
         const float4 v = *reinterpret_cast<const float4*>(st + (size_t)j * kBM + r4);
         if (n0 + r4 < A.N) store_y(j, n0 + r4, v.x, v.y, v.z, v.w);
@@ -816,14 +819,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t my_off = (uint32_t)(((size_t)rank * rpo + lr) * P * 4);  // recv[rank][lr][·] in the owner
       const uint32_t dst = o == rank ? smem_u32(recv) + my_off : mapa_shared(smem_u32(recv) + my_off, (uint32_t)o);
       const uint32_t rb = o == rank ? 0u : mapa_shared(smem_u32(rbar), (uint32_t)o);
-      for (int j0 = 0; j0 < M; j0 += 4 * kChunk) {
-        uint32_t v[4][kChunk];  // up to 64 columns in flight, one wait
+      for (int j0 = half * 2 * kChunk; j0 < M; j0 += 4 * kChunk) {
+        uint32_t v[2][kChunk];  // this half's 2 chunks of 16 columns in flight, one wait
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < 2; ++b)
           if (j0 + b * kChunk < A.mma_n) tmem_ld16_nowait(tbase + j0 + b * kChunk, v[b]);
         tmem_ld_wait();
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < 2; ++b)
 #pragma unroll
           for (int x = 0; x < kChunk / 4; ++x) {
             const int j = j0 + b * kChunk + 4 * x;
@@ -840,10 +843,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
       }
       if (ep == 0) { KD_TRACE(7); KD_CTRACE(22); KD_TRACE(10); KD_CTRACE(23); }
-      // the owner's sum runs after the role branches with all 8 warps
+      // the owner's sum runs after the role branches with all warps
     }
     if (A.epi.n && stored) {  // publish this CTA's stores to the consumer devices
-      named_bar(1, 128);
+      named_bar(1, kEpi);
       if (ep == 0) {
         fence_acq_rel_sys();
         for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
@@ -852,7 +855,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (ep == 0) { KD_TRACE(9); KD_CTRACE(26); }
   }
   if (split > 1) {
-    // ---- owner sum with all 256 threads (the TMA/MMA warps are idle by now):
+    // ---- owner sum with all 384 threads (the TMA/MMA warps are idle by now):
     // my rows [rank·rpo, +my_rows), Σ over ranks in order; lanes walk tokens
     // (conflict-free column reads), each thread 4 consecutive weight rows
     __syncthreads();            // my own rows are in recv[rank]
