@@ -144,6 +144,23 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def placement_search(cfg, DEC):
+    """a1 on the host ("report search time", "solves
+    each DDG in about 20 ms"): kd_place over the unfused graph of this config
+    (N=2 micro-batches) on 2/4/8 B200s; wall time of the exact search."""
+    from paper_2604_10180_b200.api import place
+    if cfg.n_experts or cfg.attn_every:
+        return None
+    dg = DEC.DecoderGraph(cfg.with_(n_micro=2))
+    out = {"kernels": dg.g.num_kernels, "n_micro": 2}
+    for n in (2, 4, 8):
+        t0 = time.perf_counter()
+        a, obj, nodes = place(dg.g, DEC.b200_machine(n), 2)
+        out[f"{n}gpu"] = {"search_ms": round((time.perf_counter() - t0) * 1e3, 2), "objective_us": round(obj / 1e6, 1),
+                          "nodes": nodes, "devices_used": len(set(a))}
+    return out
+
+
 def workload_config(cfg, n_gpus, placement):
     return {"workload": f"{cfg.name} decode B={cfg.batch} C={cfg.context} L={cfg.n_layers}",
             "model_shape": {"hidden": cfg.hidden, "heads": cfg.n_heads, "kv_heads": cfg.n_kv_heads,
@@ -400,6 +417,8 @@ def main():
             "clocks": clk}
     if kernels:
         line["kernels"] = kernels
+    if rank == 0:
+        line["placement_search"] = placement_search(cfg, DEC)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0:
