@@ -230,6 +230,26 @@ kd_status kd_objective(const kd_graph* g, const kd_machine* m, const int32_t* as
 kd_status kd_place(const kd_graph* g, const kd_machine* m, const kd_place_opts* opts,
                    int32_t* assign, int64_t* objective_ps, uint64_t* nodes_visited);
 
+/* ------------------------------------------------------------------ online monitor
+ * Queueing-aware policy switching (§3.4): requests are
+ * attributed to the fixed window ⌊t_end/W⌋ in which they finish; at each window
+ * boundary the ratio L̄_req / L̄_exec of mean request latency to mean pure
+ * execution latency (compute + communication, queueing excluded)
+ * selects KD_OBJ_THROUGHPUT when > β, else KD_OBJ_LATENCY; an empty window
+ * keeps the policy. Paper defaults W = 300 ms, β = 1.5. Times are
+ * integer ns, β = beta_num/beta_den: decisions are exact. Switching itself
+ * (re-planning, synchronising the workers at an iteration boundary) is
+ * the caller's: it keeps one plan per policy. Errors: KD_ERR_INVALID_ARG;
+ * KD_ERR_STATE when a request finishes in a window already evaluated. */
+typedef struct kd_monitor kd_monitor;
+kd_status kd_monitor_create(uint64_t window_ns, uint32_t beta_num, uint32_t beta_den, uint32_t initial_policy,
+                            kd_monitor** out);
+kd_status kd_monitor_destroy(kd_monitor* m);
+kd_status kd_monitor_record(kd_monitor* m, uint64_t t_end_ns, uint64_t req_latency_ns, uint64_t exec_latency_ns);
+/* evaluates every window that ended before now_ns, in order; *policy = current
+ * policy, *switches (nullable) = switches so far */
+kd_status kd_monitor_poll(kd_monitor* m, uint64_t now_ns, uint32_t* policy, uint32_t* switches);
+
 /* Chunk partition (R10): q = ⌈⌈len/unit⌉/n⌉·unit; chunk c = [c·q, min((c+1)·q, len)),
  * empty chunks dropped. begin_end receives 2·(*n_out) values; cap in chunks. */
 kd_status kd_chunks(uint64_t len, uint64_t unit, uint32_t n, uint64_t* begin_end, uint32_t cap, uint32_t* n_out);

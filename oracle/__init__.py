@@ -16,8 +16,10 @@ S:n = SPEC.md line n, R# = the readings listed in SURVEY.md §8(c) and DESIGN.md
               exhaustive enumeration (C3)
   schedule  — discrete-event list schedule + chunk partition (P:380, P:401-402,
               C4, R10, R11)
+  monitor   — online monitor's windowed queueing-ratio policy switch
+              (P:405-420, P:597, R21)
 
 Parity pins live in tests/test_oracle_*.py. Functions without an independent
 pin say "parity unpinned" in their docstring (none at present).
 """
-from . import layer, ddg, placement, schedule  # noqa: F401
+from . import layer, ddg, placement, schedule, monitor  # noqa: F401

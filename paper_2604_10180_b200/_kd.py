@@ -175,6 +175,10 @@ _PROTOS = {
     "kd_ipc_open": (kd_status, [P, u64, C.POINTER(P)]),
     "kd_ipc_close": (kd_status, [P]),
     "kd_debug_gemm_trace": (kd_status, [P]),
+    "kd_monitor_create": (kd_status, [u64, u32, u32, u32, C.POINTER(P)]),
+    "kd_monitor_destroy": (kd_status, [P]),
+    "kd_monitor_record": (kd_status, [P, u64, u64, u64]),
+    "kd_monitor_poll": (kd_status, [P, u64, PU32, PU32]),
     "kd_gemm_tiling": (kd_status, [u32, u32, u32, C.POINTER(C.c_int32)]),
     "kd_set_pdl": (kd_status, [i32]),
     "kd_op_scratch_bytes": (kd_status, [u32, P, PU64]),

@@ -116,6 +116,29 @@ def place(g: Graph, m: Machine, n_micro: int, obj: int = K.KD_OBJ_AUTO, max_node
     return list(a), o.value, nodes.value
 
 
+class Monitor:
+    """Online monitor: record finished requests, poll at any time
+    for the current policy (KD_OBJ_LATENCY / KD_OBJ_THROUGHPUT)."""
+
+    def __init__(self, window_ns: int = 300_000_000, beta=(3, 2), initial_policy: int = K.KD_OBJ_LATENCY):
+        h = C.c_void_p()
+        check(K.kd_monitor_create(window_ns, beta[0], beta[1], initial_policy, C.byref(h)), "kd_monitor_create")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            K.kd_monitor_destroy(self.h)
+            self.h = None
+
+    def record(self, t_end_ns: int, req_latency_ns: int, exec_latency_ns: int):
+        check(K.kd_monitor_record(self.h, t_end_ns, req_latency_ns, exec_latency_ns), "kd_monitor_record")
+
+    def poll(self, now_ns: int):
+        p, n = C.c_uint32(), C.c_uint32()
+        check(K.kd_monitor_poll(self.h, now_ns, C.byref(p), C.byref(n)), "kd_monitor_poll")
+        return p.value, n.value
+
+
 def chunks(length: int, unit: int, n: int):
     out = (C.c_uint64 * (2 * n))()
     cnt = C.c_uint32()
