@@ -99,10 +99,11 @@ enum {
   KD_OP_GEMM_SILU = 14,    /* a9+a8 fused (co-located gate_up and SiLU·mul): reads [X, W_gu] writes [a]:
                             * a = silu_mul_blocked(bf16(X·W_guᵀ)) with kd_attr_gemm, N = 2F weight rows
                             * (64-row gate/up blocks, R12), a [M, F]; bits identical to a9 then a8 */
-  KD_OP_QKV_ROPE = 15      /* a4+a5 fused (co-located QKV GEMM and RoPE + KV append): reads [X, W_qkv',
+  KD_OP_QKV_ROPE = 15,     /* a4+a5 fused (co-located QKV GEMM and RoPE + KV append): reads [X, W_qkv',
                             * block_table, seq_len] writes [q, Kc, Vc] with kd_attr_qkv_rope. W_qkv' = the
                             * kv-group-interleaved QKV weight with rows pair-interleaved inside every head
                             * (row 2p ← dim p, row 2p+1 ← dim p + D/2); bits identical to a4 then a5 */
+  KD_OP_ATTN_MERGE = 16    /* f2 reads [part_0 .. part_{n-1}] ([out|lse] of KD_ATTN_LSE attentions) writes [out] */
 };
 
 /* element types of activations / KV */
@@ -117,13 +118,26 @@ enum { KD_BF16 = 0, KD_F32 = 1 };
  * row-parallel GEMMs' fused peer stores. */
 typedef struct { uint32_t rows, hidden, n_delta, dtype; float eps; uint32_t pad_; } kd_attr_add_rmsnorm;
 typedef struct { uint32_t M, N, K, dtype; } kd_attr_gemm;            /* X [M,K], W [N,K] row-major, Y [M,N] */
+/* slot_offset: tokens of each sequence held by earlier KV shards (f2, long
+ * context split over devices): the rotation angle uses the absolute position
+ * seq_len − 1, the appended slot is (seq_len − 1 − slot_offset) in this
+ * shard's block table. 0 for an unsharded cache. */
 typedef struct {
-  uint32_t rows, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype, pad_;
+  uint32_t rows, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype, slot_offset;
   double theta;   /* RoPE base (R12) */
 } kd_attr_rope_append;
+/* flags: KD_ATTN_LSE → the output buffer is [out bf16 rows×Hq×D | lse fp32
+ * rows×Hq], lse = log2 Σ_t 2^(s_t·log2e) (the base-2 log-sum-exp of the
+ * scaled scores; −inf for an empty context): one KV shard's partial for
+ * KD_OP_ATTN_MERGE (f2). */
+enum { KD_ATTN_LSE = 1 };
 typedef struct {
-  uint32_t rows, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype, pad_;
+  uint32_t rows, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype, flags;
 } kd_attr_attention;
+/* f2: merge of n_parts attention partials of the
+ * same queries over disjoint KV shards: out = Σ_s 2^(lse_s − M)·out_s /
+ * Σ_s 2^(lse_s − M), M = max_s lse_s, shards in index order (deterministic). */
+typedef struct { uint32_t rows, n_heads, head_dim, n_parts; } kd_attr_attn_merge;
 typedef struct {
   uint32_t rows, hidden, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype;
   double theta;   /* RoPE base (R12) */
@@ -388,6 +402,9 @@ kd_status kd_op_rope_append(const kd_attr_rope_append* a, const void* qkv, const
 kd_status kd_op_attention(const kd_attr_attention* a, const void* q, const void* k_cache, const void* v_cache,
                           const int32_t* block_table, const int32_t* seq_len, void* out,
                           void* scratch, void* stream);
+/* f2: merge n_parts KD_ATTN_LSE partials (parts: n_parts device pointers to
+ * [out|lse] buffers) into out bf16 [rows, n_heads·head_dim]. */
+kd_status kd_op_attn_merge(const kd_attr_attn_merge* a, const void* const* parts, void* out, void* stream);
 /* a8: a[:, 64j+i] = silu(gu[:, 128j+i]) · gu[:, 128j+64+i] */
 kd_status kd_op_silu_mul(const kd_attr_silu_mul* a, const void* gu, void* out, void* stream);
 /* C1.11: r += Σ_i deltas[i] (index order) */

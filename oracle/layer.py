@@ -152,6 +152,48 @@ def paged_decode_attention(q, k_cache, v_cache, block_table, seq_len,
     return store(out, act)
 
 
+def paged_decode_attention_lse(q, k_cache, v_cache, block_table, seq_len, n_heads, n_kv, D, page=16):
+    """C1.5 plus the base-2 log-sum-exp of the scaled scores per (row, head):
+    lse2 = log2 Σ_t exp(s_t), s_t = q·k_t/√D (−inf for an empty context, whose
+    output is 0). Exact fp64; the KV-shard partial of f2."""
+    m = q.shape[0]
+    G = n_heads // n_kv
+    out = np.zeros((m, n_heads * D))
+    lse = np.full((m, n_heads), -np.inf)
+    scale = 1.0 / math.sqrt(D)
+    for b in range(m):
+        C = int(seq_len[b])
+        if C == 0:
+            continue
+        pages = [int(block_table[b][t // page]) for t in range(C)]
+        offs = [t % page for t in range(C)]
+        for g in range(n_kv):
+            K = np.asarray(k_cache[pages, g, offs, :], np.float64)
+            V = np.asarray(v_cache[pages, g, offs, :], np.float64)
+            for j in range(G):
+                h = g * G + j
+                s = (K @ np.asarray(q[b, h * D:(h + 1) * D], np.float64)) * scale
+                mx = s.max()
+                e = np.exp(s - mx)
+                out[b, h * D:(h + 1) * D] = (e / e.sum()) @ V
+                lse[b, h] = (mx + math.log(e.sum())) / math.log(2.0)
+    return out, lse
+
+
+def lse_merge(outs, lses, D):
+    """Merge attention partials over disjoint key sets (f2): with weights
+    w_s = 2^(lse_s − max_s lse_s), out = Σ_s w_s·out_s / Σ_s w_s — the softmax
+    over the union of the key sets written out (shards in index order)."""
+    lses = np.asarray(lses, np.float64)           # [S, m, H]
+    outs = np.asarray(outs, np.float64)           # [S, m, H*D]
+    S, m, H = lses.shape
+    M = lses.max(axis=0)
+    w = np.where(np.isfinite(lses), np.exp2(lses - np.where(np.isfinite(M), M, 0.0)), 0.0)
+    num = (w[:, :, :, None] * outs.reshape(S, m, H, D)).sum(axis=0)
+    den = w.sum(axis=0)[:, :, None]
+    return np.where(den > 0, num / np.where(den > 0, den, 1.0), 0.0).reshape(m, H * D)
+
+
 # ---------------------------------------------------------------- a8
 def silu(x):
     x = np.asarray(x, np.float64)

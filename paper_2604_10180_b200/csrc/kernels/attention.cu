@@ -46,6 +46,8 @@ struct Params {
   const int32_t* bt;
   const int32_t* sl;
   __nv_bfloat16* out;
+  float* lse;         // KD_ATTN_LSE: [rows][Hq] base-2 LSE after the [rows][Hq][D] bf16 out (nullable)
+  size_t lse_off;     // byte offset of lse inside the output buffer (for the peer copies)
   float* part_o;      // [rows][Hkv][splits][G][D]
   float* part_lse;    // [rows][Hkv][splits][G]
   unsigned* counter;  // [rows][Hkv]
@@ -130,6 +132,12 @@ __device__ __forceinline__ void store_out4(const Params& P, size_t oi, float4 v)
   pk.y = pack_bf16(v.z, v.w);
   *reinterpret_cast<uint2*>(P.out + oi) = pk;
   for (int pp = 0; pp < P.epi.n; ++pp) *reinterpret_cast<uint2*>((__nv_bfloat16*)P.epi.dst[pp] + oi) = pk;
+}
+
+// one (row, head) base-2 LSE of a KD_ATTN_LSE partial, mirrored to the peers
+__device__ __forceinline__ void store_lse(const Params& P, size_t li, float v) {
+  P.lse[li] = v;
+  for (int pp = 0; pp < P.epi.n; ++pp) reinterpret_cast<float*>((uint8_t*)P.epi.dst[pp] + P.lse_off)[li] = v;
 }
 
 // Stage tile of one page slab: [16 tokens][D/64 halves][64 dims] bf16 (the
@@ -348,6 +356,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
         acc.x *= inv, acc.y *= inv, acc.z *= inv, acc.w *= inv;
         if (single) {
           store_out4(P, (size_t)b * P.Hq * D + (size_t)(g * G + h) * D + d0, acc);
+          if (P.lse && d0 == 0) store_lse(P, (size_t)b * P.Hq + g * G + h, L > 0.f ? s_M[h] + log2f(L) : -INFINITY);
         } else {
           const size_t pi = (((size_t)unit * P.splits + split) * G + h);
           *reinterpret_cast<float4*>(P.part_o + pi * D + d0) = acc;
@@ -410,6 +419,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
             const float inv = L > 0.f ? 1.f / L : 0.f;
             acc.x *= inv, acc.y *= inv, acc.z *= inv, acc.w *= inv;
             store_out4(P, (size_t)b * P.Hq * D + (size_t)(g * G + h) * D + d0, acc);
+            if (P.lse && d0 == 0) store_lse(P, (size_t)b * P.Hq + g * G + h, L > 0.f ? Mu + log2f(L) : -INFINITY);
           }
           if (lane == 0) P.counter[unit] = 0u;  // ready for the next launch
         }
@@ -652,6 +662,7 @@ static kd_status validate(const kd_attr_attention& a) {
   if (a.n_kv_heads == 0 || a.n_heads % a.n_kv_heads || a.n_heads / a.n_kv_heads > kMaxG)
     return fail(KD_ERR_UNSUPPORTED, "attention: need Hq % Hkv == 0 and Hq/Hkv <= 8");
   if (a.rows == 0 || a.pages_per_seq == 0) return fail(KD_ERR_INVALID_ARG, "attention: empty shape");
+  if (a.flags & ~(uint32_t)KD_ATTN_LSE) return fail(KD_ERR_INVALID_ARG, "attention: unknown flags");
   return KD_OK;
 }
 
@@ -677,6 +688,7 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
                            const int32_t* bt, const int32_t* sl, void* out, const LaunchCtx& c, uint32_t* signals) {
   if (a.dtype == KD_F32) {
     if (!q || !kc || !vc || !bt || !sl || !out) return fail(KD_ERR_INVALID_ARG, "attention: NULL pointer");
+    if (a.flags) return fail(KD_ERR_UNSUPPORTED, "attention (fp32): KD_ATTN_LSE partials are bf16-path only");
     if (a.rows == 0 || a.n_kv_heads == 0 || a.n_heads % a.n_kv_heads || a.head_dim == 0 || a.page == 0)
       return fail(KD_ERR_UNSUPPORTED, "attention (fp32): unsupported shape");
     kd_status st = launch_attention_f32(a, (const float*)q, (const float*)kc, (const float*)vc, bt, sl, (float*)out, c);
@@ -696,6 +708,8 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
   P.bt = bt;
   P.sl = sl;
   P.out = (__nv_bfloat16*)out;
+  P.lse_off = (size_t)a.rows * a.n_heads * a.head_dim * 2;
+  P.lse = (a.flags & KD_ATTN_LSE) ? (float*)((uint8_t*)out + P.lse_off) : nullptr;
   const uint64_t units = (uint64_t)a.rows * a.n_kv_heads;
   if (units >= kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "attention: too many (sequence, kv head) units");
   P.counter = (unsigned*)c.scratch;

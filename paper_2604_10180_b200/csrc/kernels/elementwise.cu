@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
     rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ bt,
                        const int32_t* __restrict__ sl, __nv_bfloat16* __restrict__ q_out,
                        __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int Hq, int Hkv, int D,
-                       int page, int pps, const __grid_constant__ RopeFreq fr, Epi epi) {
+                       int page, int pps, int slot_offset, const __grid_constant__ RopeFreq fr, Epi epi) {
   pdl_launch_dependents();
   const int b = blockIdx.x, half = D / 2, G = Hq / Hkv;
   const int hh = blockIdx.y * kRopeHeadsPerCta + (int)(threadIdx.x >> 4), t16 = threadIdx.x & 15;
@@ -267,10 +267,10 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
       qoff = (size_t)b * Hq * D + (size_t)hh * D;
       dst = q_out + qoff;
     } else {
-      const int g = hh - Hq;
-      const int32_t pg = bt[(size_t)b * pps + pos / page];
+      const int g = hh - Hq, slot = pos - slot_offset;  // this shard's slot of the absolute position
+      const int32_t pg = bt[(size_t)b * pps + slot / page];
       x = src + (size_t)g * (G + 2) * D + (size_t)G * D;
-      dst = kc + (((size_t)pg * Hkv + g) * page + pos % page) * D;
+      dst = kc + (((size_t)pg * Hkv + g) * page + slot % page) * D;
     }
     const uint4 xa = *reinterpret_cast<const uint4*>(x + i0);
     const uint4 xb = *reinterpret_cast<const uint4*>(x + half + i0);
@@ -307,10 +307,10 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
   } else if (hh >= n_rot && hh < n_rot + Hkv) {
     // v: plain copy into the cache slot, 16 threads × 8 dims per pass
     const int g = hh - n_rot;
-    const int pos = sl[b] - 1;
-    const int32_t pg = bt[(size_t)b * pps + pos / page];
+    const int slot = sl[b] - 1 - slot_offset;
+    const int32_t pg = bt[(size_t)b * pps + slot / page];
     const __nv_bfloat16* x = qkv + (size_t)b * (Hq + 2 * Hkv) * D + (size_t)g * (G + 2) * D + (size_t)(G + 1) * D;
-    __nv_bfloat16* dst = vc + (((size_t)pg * Hkv + g) * page + pos % page) * D;
+    __nv_bfloat16* dst = vc + (((size_t)pg * Hkv + g) * page + slot % page) * D;
     for (int c8 = t16 * 8; c8 < D; c8 += 128)
       *reinterpret_cast<uint4*>(dst + c8) = *reinterpret_cast<const uint4*>(x + c8);
   }
@@ -330,7 +330,9 @@ kd_status launch_rope_append(const kd_attr_rope_append& a, const void* qkv, cons
     return fail(KD_ERR_UNSUPPORTED, "rope_append: unsupported shape (head_dim a multiple of 16, <= 256)");
   if (!qkv || !bt || !sl || !q_out || !kc || !vc) return fail(KD_ERR_INVALID_ARG, "rope_append: NULL pointer");
   const dim3 grid = rope_grid(a);
+  if (a.slot_offset % a.page) return fail(KD_ERR_INVALID_ARG, "rope_append: slot_offset must be a multiple of the page");
   if (a.dtype == KD_F32) {
+    if (a.slot_offset) return fail(KD_ERR_UNSUPPORTED, "rope_append (fp32): sharded caches are bf16-path only");
     kd_status st = launch_rope_append_f32(a, (const float*)qkv, bt, sl, (float*)q_out, (float*)kc, (float*)vc, grid, c);
     if (!st && signals) *signals = grid.x * grid.y;
     return st;
@@ -340,9 +342,71 @@ kd_status launch_rope_append(const kd_attr_rope_append& a, const void* qkv, cons
   for (uint32_t i = 0; i < a.head_dim / 2; ++i) fr.f[i] = std::exp2(-2.0 * (double)i / (double)a.head_dim * l2t);
   KD_CUDA_CHECK(kd_launch(rope_append_kernel, grid, dim3(kRopeHeadsPerCta * 16), 0, c.stream, (const __nv_bfloat16*)qkv,
                           bt, sl, (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (int)a.n_heads,
-                          (int)a.n_kv_heads, (int)a.head_dim, (int)a.page, (int)a.pages_per_seq, fr, c.epi),
+                          (int)a.n_kv_heads, (int)a.head_dim, (int)a.page, (int)a.pages_per_seq, (int)a.slot_offset,
+                          fr, c.epi),
                 "rope_append launch");
   if (signals) *signals = grid.x * grid.y;
+  return KD_OK;
+}
+
+// ------------------------------------------------------------------ f2: KV-shard merge
+// out = Σ_s 2^(lse_s − M)·out_s / Σ_s 2^(lse_s − M), M = max_s lse_s, shards in
+// index order (deterministic); a shard with an empty context has lse = −inf
+constexpr int kMaxParts = 8;
+struct Parts {
+  const uint8_t* p[kMaxParts];
+};
+
+__global__ void attn_merge_kernel(Parts ps, int n, __nv_bfloat16* __restrict__ out, int rows, int Hq, int D, Epi epi) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const size_t lse_off = (size_t)rows * Hq * D * 2;
+  const int d4n = D / 4;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)rows * Hq * d4n;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const size_t rh = e / d4n;
+    const int d0 = (int)(e % d4n) * 4;
+    float M = -INFINITY;
+    for (int s = 0; s < n; ++s) M = fmaxf(M, reinterpret_cast<const float*>(ps.p[s] + lse_off)[rh]);
+    float ax = 0.f, ay = 0.f, az = 0.f, aw = 0.f, wsum = 0.f;
+    for (int s = 0; s < n; ++s) {
+      const float l = reinterpret_cast<const float*>(ps.p[s] + lse_off)[rh];
+      const float w = (M == -INFINITY || l == -INFINITY) ? 0.f : exp2f(l - M);
+      const uint2 v = *reinterpret_cast<const uint2*>(ps.p[s] + (rh * D + d0) * 2);
+      ax += w * bf16lo(v.x), ay += w * bf16hi(v.x), az += w * bf16lo(v.y), aw += w * bf16hi(v.y);
+      wsum += w;
+    }
+    const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+    uint2 o;
+    o.x = pack_bf16(ax * inv, ay * inv);
+    o.y = pack_bf16(az * inv, aw * inv);
+    const size_t oi = rh * D + d0;
+    *reinterpret_cast<uint2*>(out + oi) = o;
+    for (int p = 0; p < epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)epi.dst[p] + oi) = o;
+  }
+  epi_signal(epi);
+}
+
+static int merge_grid(const kd_attr_attn_merge& a) {
+  const size_t n = (size_t)a.rows * a.n_heads * (a.head_dim / 4);
+  return (int)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 4 * kNumSMs));
+}
+
+kd_status launch_attn_merge(const kd_attr_attn_merge& a, const void* const* parts, void* out, const LaunchCtx& c,
+                            uint32_t* signals) {
+  if (a.n_parts == 0 || a.n_parts > (uint32_t)kMaxParts) return fail(KD_ERR_INVALID_ARG, "attn_merge: 1..8 parts");
+  if (a.rows == 0 || a.n_heads == 0 || a.head_dim % 4) return fail(KD_ERR_UNSUPPORTED, "attn_merge: unsupported shape");
+  if (!out) return fail(KD_ERR_INVALID_ARG, "attn_merge: NULL output");
+  Parts ps{};
+  for (uint32_t s = 0; s < a.n_parts; ++s) {
+    if (!parts[s]) return fail(KD_ERR_INVALID_ARG, "attn_merge: NULL part");
+    ps.p[s] = (const uint8_t*)parts[s];
+  }
+  const int grid = merge_grid(a);
+  KD_CUDA_CHECK(kd_launch(attn_merge_kernel, dim3(grid), dim3(256), 0, c.stream, ps, (int)a.n_parts,
+                          (__nv_bfloat16*)out, (int)a.rows, (int)a.n_heads, (int)a.head_dim, c.epi),
+                "attn_merge launch");
+  if (signals) *signals = grid;
   return KD_OK;
 }
 
@@ -426,6 +490,12 @@ kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s
   kd_status st = KD_OK;
   switch (op) {
     case KD_OP_ADD_RMSNORM: { kd_attr_add_rmsnorm a; if ((st = attrs_of(attrs, &a))) return st; *signals = a.rows; return KD_OK; }
+    case KD_OP_ATTN_MERGE: {
+      kd_attr_attn_merge a;
+      if ((st = attrs_of(attrs, &a))) return st;
+      *signals = merge_grid(a);
+      return KD_OK;
+    }
     case KD_OP_ROPE_APPEND: {
       kd_attr_rope_append a;
       if ((st = attrs_of(attrs, &a))) return st;

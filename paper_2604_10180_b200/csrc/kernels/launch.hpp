@@ -101,6 +101,8 @@ kd_status launch_silu_mul(const kd_attr_silu_mul& a, const void* gu, void* out, 
 kd_status launch_rope_append(const kd_attr_rope_append& a, const void* qkv, const int32_t* bt, const int32_t* sl,
                              void* q_out, void* kc, void* vc, const LaunchCtx& c, uint32_t* signals);
 kd_status attention_scratch_bytes(const kd_attr_attention& a, uint64_t* bytes);
+kd_status launch_attn_merge(const kd_attr_attn_merge& a, const void* const* parts, void* out, const LaunchCtx& c,
+                            uint32_t* signals);
 // 2-D bf16 tensor map, row-major [outer][inner], 128-byte swizzle, box
 // {box_inner, box_rows} (box_inner·2 ≤ 128). Defined in gemm.cu.
 kd_status encode_bf16_2d_sw128(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,

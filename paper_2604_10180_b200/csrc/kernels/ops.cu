@@ -57,6 +57,7 @@ kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes) {
     case KD_OP_GEMM_SILU: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_gemm*)attrs, true), bytes);
     case KD_OP_QKV_ROPE: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_qkv_rope*)attrs), bytes);
     case KD_OP_GROUPED_GEMM: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_grouped_gemm*)attrs), bytes);
+    case KD_OP_ATTN_MERGE:
     case KD_OP_MOE_ROUTE:
     case KD_OP_MOE_DISPATCH:
     case KD_OP_MOE_COMBINE:
@@ -99,6 +100,13 @@ kd_status kd_op_gemm(const kd_attr_gemm* a, const void* X, const void* W, void* 
   c.stream = (cudaStream_t)stream;
   c.scratch = scratch;
   return launch_gemm(gp, Y, c, nullptr);
+}
+
+kd_status kd_op_attn_merge(const kd_attr_attn_merge* a, const void* const* parts, void* out, void* stream) {
+  if (!a || !parts) return fail(KD_ERR_INVALID_ARG, "kd_op_attn_merge: NULL argument");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  return launch_attn_merge(*a, parts, out, c, nullptr);
 }
 
 kd_status kd_op_qkv_rope(const kd_attr_qkv_rope* a, const void* X, const void* W, const int32_t* block_table,

@@ -89,6 +89,7 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_GEMM:
     case KD_OP_GEMM_SILU: need = sizeof(kd_attr_gemm); break;
     case KD_OP_QKV_ROPE: need = sizeof(kd_attr_qkv_rope); break;
+    case KD_OP_ATTN_MERGE: need = sizeof(kd_attr_attn_merge); break;
     case KD_OP_ROPE_APPEND: need = sizeof(kd_attr_rope_append); break;
     case KD_OP_ATTENTION: need = sizeof(kd_attr_attention); break;
     case KD_OP_SILU_MUL: need = sizeof(kd_attr_silu_mul); break;
@@ -116,6 +117,12 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_GEMM:
     case KD_OP_GEMM_SILU: ok = nr == 2 && nw == 1; break;
     case KD_OP_QKV_ROPE: ok = nr == 4 && nw == 3; break;  // reads [X, W', bt, sl] writes [q, Kc, Vc]
+    case KD_OP_ATTN_MERGE: {
+      kd_attr_attn_merge a;
+      std::memcpy(&a, k.attrs.data(), sizeof a);
+      ok = a.n_parts >= 1 && a.n_parts <= 8 && nr == a.n_parts && nw == 1;
+      break;
+    }
     case KD_OP_ROPE_APPEND: ok = nr == 3 && nw == 3; break;
     case KD_OP_ATTENTION: ok = nr == 5 && nw == 1; break;
     case KD_OP_SILU_MUL: ok = nr == 1 && nw == 1; break;
@@ -185,6 +192,11 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
     case KD_OP_SILU_MUL: {
       auto a = attrs_get<kd_attr_silu_mul>(K);
       st = launch_silu_mul(a, l.rd[0], l.wr[0], c, &sig);
+      break;
+    }
+    case KD_OP_ATTN_MERGE: {
+      auto a = attrs_get<kd_attr_attn_merge>(K);
+      st = launch_attn_merge(a, (const void* const*)l.rd.data(), l.wr[0], c, &sig);
       break;
     }
     case KD_OP_RESIDUAL_ADD: {

@@ -401,6 +401,136 @@ def _torch():
     return torch
 
 
+T_ATTN_SHARD = 32  # template ids 32 + s: attention (and, for the last shard, RoPE/append) of KV shard s
+
+
+class ShardedKVDecoderGraph:
+    """Long-context decode with every sequence's KV cache split over S
+    memory-role devices ("the KV cache ... can be
+    partitioned"): shard s holds tokens [s·T, (s+1)·T) (T = C/S, a page
+    multiple) in its own paged pool; each shard's attention returns its
+    normalised partial and base-2 log-sum-exp (KD_ATTN_LSE), a merge kernel
+    combines them in shard order (KD_OP_ATTN_MERGE); RoPE/append writes the new
+    token into the last shard (absolute position for the angle, slot_offset =
+    (S−1)·T). Logical devices: 0..S−1 the shards (norms, SiLU and the merge on
+    0), S the GEMMs. Dense bf16 configs; sequences at exactly C."""
+
+    def __init__(self, cfg, shards: int, act: int = K.KD_BF16):
+        assert act == K.KD_BF16 and not cfg.n_experts and not cfg.attn_every
+        S = shards
+        assert cfg.context % (S * cfg.page) == 0, "context must split into page-aligned shards"
+        self.cfg, self.shards = cfg, S
+        m, H, L = cfg.m, cfg.hidden, cfg.n_layers
+        Hq, Hkv, D, F = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn
+        T = cfg.context // S
+        ps = T // cfg.page  # pages per sequence per shard
+        self.T, self.ps = T, ps
+        g = Graph()
+        self.g = g
+        self.buf, self.shape, self.dtype = {}, {}, {}
+        W, PM = K.KD_BUF_WEIGHT, K.KD_BUF_PER_MICROBATCH
+        PERS, INP, OUT = K.KD_BUF_PERSISTENT, K.KD_BUF_INPUT, K.KD_BUF_OUTPUT
+        nb = {"bf16": 2, "f32": 4, "i32": 4, "u8": 1}
+
+        def buf(name, shape, dt, flags):
+            self.buf[name] = g.add_buffer(int(np.prod(shape)) * nb[dt], flags)
+            self.shape[name], self.dtype[name] = tuple(shape), dt
+
+        def whole(name):
+            return (self.buf[name], 0, int(np.prod(self.shape[name])) * nb[self.dtype[name]])
+
+        part_bytes = m * Hq * D * 2 + m * Hq * 4  # [out bf16 | lse fp32]
+        buf("r", (m, H), "f32", PERS | INP | OUT | PM)
+        buf("sl", (m,), "i32", INP | PM)
+        for s_ in range(S):
+            buf(f"bt.{s_}", (m, ps), "i32", INP | PM)
+            buf(f"sl.{s_}", (m,), "i32", INP | PM)
+        for l in range(L):
+            buf(f"w_qkv.{l}", (cfg.qkv_dim, H), "bf16", W)
+            buf(f"w_o.{l}", (H, Hq * D), "bf16", W)
+            buf(f"w_gu.{l}", (2 * F, H), "bf16", W)
+            buf(f"w_d.{l}", (H, F), "bf16", W)
+            buf(f"g1.{l}", (H,), "bf16", W)
+            buf(f"g2.{l}", (H,), "bf16", W)
+            for s_ in range(S):
+                buf(f"kc.{l}.{s_}", (m * ps, Hkv, cfg.page, D), "bf16", PERS | PM)
+                buf(f"vc.{l}.{s_}", (m * ps, Hkv, cfg.page, D), "bf16", PERS | PM)
+                buf(f"ap.{l}.{s_}", (part_bytes,), "u8", PM)
+            for nm, shp in (("h1", (m, H)), ("qkv", (m, cfg.qkv_dim)), ("q", (m, Hq * D)), ("attn", (m, Hq * D)),
+                            ("o", (m, H)), ("h2", (m, H)), ("gu", (m, 2 * F)), ("a", (m, F)), ("d", (m, H))):
+                buf(f"{nm}.{l}", shp, "bf16", PM)
+        self.kernels: List[KernelInfo] = []
+        self.dev_of: List[int] = []
+
+        def add(name, layer, tmpl, dev, op, reads, writes, attrs, flops=0):
+            kid = g.add_kernel(op, [whole(x) for x in reads], [whole(x) for x in writes], attrs, flops, -1, tmpl)
+            self.kernels.append(KernelInfo(name, layer, tmpl, kid))
+            self.dev_of.append(dev)
+
+        eps = float(cfg.eps)
+        for l in range(L):
+            has_d = 1 if l > 0 else 0
+            add("norm1", l, T_RESID, 0, K.KD_OP_ADD_RMSNORM, ["r"] + ([f"d.{l-1}"] if has_d else []) + [f"g1.{l}"],
+                [f"h1.{l}", "r"], K.kd_attr_add_rmsnorm(m, H, has_d, act, eps, 0))
+            add("qkv", l, T_QKV, S, K.KD_OP_GEMM, [f"h1.{l}", f"w_qkv.{l}"], [f"qkv.{l}"],
+                K.kd_attr_gemm(m, cfg.qkv_dim, H, act), 2 * m * cfg.qkv_dim * H)
+            add("rope", l, T_ATTN_SHARD + S - 1, S - 1, K.KD_OP_ROPE_APPEND, [f"qkv.{l}", f"bt.{S-1}", "sl"],
+                [f"q.{l}", f"kc.{l}.{S-1}", f"vc.{l}.{S-1}"],
+                K.kd_attr_rope_append(m, Hq, Hkv, D, cfg.page, ps, act, (S - 1) * T, float(cfg.rope_theta)))
+            for s_ in range(S):
+                add(f"attn{s_}", l, T_ATTN_SHARD + s_, s_, K.KD_OP_ATTENTION,
+                    [f"q.{l}", f"kc.{l}.{s_}", f"vc.{l}.{s_}", f"bt.{s_}", f"sl.{s_}"], [f"ap.{l}.{s_}"],
+                    K.kd_attr_attention(m, Hq, Hkv, D, cfg.page, ps, act, K.KD_ATTN_LSE), 4 * m * Hq * T * D)
+            add("merge", l, T_RESID, 0, K.KD_OP_ATTN_MERGE, [f"ap.{l}.{s_}" for s_ in range(S)], [f"attn.{l}"],
+                K.kd_attr_attn_merge(m, Hq, D, S))
+            add("o", l, T_O, S, K.KD_OP_GEMM, [f"attn.{l}", f"w_o.{l}"], [f"o.{l}"],
+                K.kd_attr_gemm(m, H, Hq * D, act), 2 * m * H * Hq * D)
+            add("norm2", l, T_RESID, 0, K.KD_OP_ADD_RMSNORM, ["r", f"o.{l}", f"g2.{l}"], [f"h2.{l}", "r"],
+                K.kd_attr_add_rmsnorm(m, H, 1, act, eps, 0))
+            add("gu", l, T_GU, S, K.KD_OP_GEMM, [f"h2.{l}", f"w_gu.{l}"], [f"gu.{l}"],
+                K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
+            add("silu", l, T_SILU, 0, K.KD_OP_SILU_MUL, [f"gu.{l}"], [f"a.{l}"], K.kd_attr_silu_mul(m, F, act, 0))
+            add("down", l, T_DOWN, S, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
+                K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)
+        add("final_add", L - 1, T_RESID, 0, K.KD_OP_RESIDUAL_ADD, ["r", f"d.{L-1}"], ["r"],
+            K.kd_attr_residual_add(m, H, 1, 0))
+        g.finalize()
+
+    def assign(self) -> List[int]:
+        """Shards on devices 0..S−1, GEMMs on device S."""
+        return list(self.dev_of)
+
+    def host_value(self, name, i, inputs):
+        """Host values of buffer `name` for micro-batch i, carved out of the
+        unsharded synthetic inputs: shard s's pool holds, for local sequence b,
+        the global pages of tokens [s·T, (s+1)·T) at local page ids b·ps + j."""
+        cfg, S, T, ps = self.cfg, self.shards, self.T, self.ps
+        m, pps = cfg.m, cfg.pages_per_seq
+        parts = name.split(".")
+        base = parts[0]
+        rows = slice(i * m, (i + 1) * m)
+        if base == "r":
+            return inputs.x[rows]
+        if base == "sl":
+            if len(parts) == 1:
+                return inputs.seq_len[rows]
+            s_ = int(parts[1])
+            ln = inputs.seq_len[rows].astype(np.int64)
+            hi = T if s_ < S - 1 else cfg.context  # the last shard takes every remaining token
+            return np.clip(ln - s_ * T, 0, hi).astype(np.int32)
+        if base == "bt":
+            return (np.arange(m, dtype=np.int32)[:, None] * ps + np.arange(ps, dtype=np.int32)[None, :])
+        l = int(parts[1])
+        lw = inputs.layers[l]
+        if base in ("kc", "vc"):
+            s_ = int(parts[2])
+            pool = (inputs.k_cache if base == "kc" else inputs.v_cache)[l]
+            gpages = inputs.block_table[rows][:, s_ * ps:(s_ + 1) * ps].reshape(-1)
+            return pool[gpages]
+        return {"w_qkv": lw.w_qkv, "w_o": lw.w_o, "w_gu": lw.w_gu, "w_d": lw.w_d, "g1": lw.gamma1,
+                "g2": lw.gamma2}[base]
+
+
 class DecoderRuntime:
     """Allocates and binds every external buffer on the devices the plan
     needs, one zeroed workspace per local logical device, and runs steps.
@@ -437,7 +567,8 @@ class DecoderRuntime:
             for d in self.local_devs:
                 if not self.plan.needs_binding(b, d):
                     continue
-                per_micro = name in ("r", "bt", "sl") or name.startswith(("kc.", "vc.", "conv_st.", "ssm_st.", "r."))
+                per_micro = name in ("r", "bt", "sl") or name.startswith(("kc.", "vc.", "conv_st.", "ssm_st.", "r.",
+                                                                          "bt.", "sl."))
                 for i in range(N if per_micro else 1):
                     t = torch.empty(dg.shape[name], dtype=tdt[dg.dtype[name]], device=f"cuda:{self.dev_map[d]}")
                     self._fill(t, name, i, inputs, seed, device_normal_)
@@ -572,7 +703,7 @@ class DecoderRuntime:
     def residual(self) -> np.ndarray:
         """Concatenated residual stream r [B, H] (fp32) after the last step."""
         outs = []
-        rname = "r.0" if hasattr(self.dg, "host_value") else "r"
+        rname = "r.0" if "r.0" in self.dg.buf else "r"
         for i in range(self.cfg.n_micro):
             for d in self.local_devs:
                 if (rname, i, d) in self.tensors:

@@ -357,3 +357,48 @@ def test_qkv_rope_fused_equals_pair(kd, rows, H, Hq, Hkv, D, C, split, monkeypat
     qr = OL.rope_append(qkv_ref, sl - 1, bt, kr, vr, Hq, Hkv, D, theta, 16, "bf16")
     assert relerr(host_f64(q2), qr) < 5e-3
     assert relerr(host_f64(k2), kr) < 5e-3 and relerr(host_f64(v2), vr) < 5e-3
+
+
+# ------------------------------------------------------------------ f2: attention partials + LSE merge
+def test_attention_lse_partials_and_merge(kd):
+    api, K = kd
+    torch = _torch()
+    g = synth.rng(4242)
+    rows, Hq, Hkv, D, C, S = 5, 32, 8, 128, 1024, 3
+    pps = C // 16
+    bt = synth.block_table(g, rows, pps)
+    kc = synth.normal_bf16(g, (rows * pps, Hkv, 16, D))
+    vc = synth.normal_bf16(g, (rows * pps, Hkv, 16, D))
+    q = synth.normal_bf16(g, (rows, Hq * D))
+    sl = np.array([1024, 1000, 700, 341, 17], np.int32)  # ragged; some shards empty for some rows
+    bounds = [0, 336, 672, 1024]                        # page-aligned, unequal shards
+    parts, ref_outs, ref_lses = [], [], []
+    for s in range(S):
+        p0, p1 = bounds[s] // 16, bounds[s + 1] // 16
+        bts = np.ascontiguousarray(bt[:, p0:p1])
+        sls = np.clip(sl - bounds[s], 0, bounds[s + 1] - bounds[s]).astype(np.int32)
+        a = K.kd_attr_attention(rows, Hq, Hkv, D, 16, p1 - p0, K.KD_BF16, K.KD_ATTN_LSE)
+        buf = torch.empty(rows * Hq * D * 2 + rows * Hq * 4, dtype=torch.uint8, device="cuda")
+        api.attention(a, dev_bf16(q), dev_bf16(kc), dev_bf16(vc), torch.from_numpy(bts).cuda(),
+                      torch.from_numpy(sls).cuda(), buf, scratch_for(api, K.KD_OP_ATTENTION, a))
+        parts.append(buf)
+        o, l = OL.paged_decode_attention_lse(OL.bf16_to_f64(q), OL.bf16_to_f64(kc), OL.bf16_to_f64(vc), bts, sls,
+                                             Hq, Hkv, D)
+        ref_outs.append(o)
+        ref_lses.append(l)
+    torch.cuda.synchronize()
+    for s in range(S):
+        lse = parts[s][rows * Hq * D * 2:].view(torch.float32).cpu().numpy().reshape(rows, Hq)
+        fin = np.isfinite(ref_lses[s])
+        assert np.array_equal(np.isfinite(lse), fin)
+        assert np.allclose(lse[fin], ref_lses[s][fin], atol=2e-3)
+    out = torch.empty(rows, Hq * D, dtype=torch.bfloat16, device="cuda")
+    import ctypes as C
+    ptrs = (C.c_void_p * S)(*[p.data_ptr() for p in parts])
+    K.check(K.kd_op_attn_merge(C.byref(K.kd_attr_attn_merge(rows, Hq, D, S)), ptrs, C.c_void_p(out.data_ptr()),
+                               None), "kd_op_attn_merge")
+    torch.cuda.synchronize()
+    full = OL.paged_decode_attention(OL.bf16_to_f64(q), OL.bf16_to_f64(kc), OL.bf16_to_f64(vc), bt, sl, Hq, Hkv, D,
+                                     16, "bf16")
+    assert relerr(host_f64(out), OL.lse_merge(ref_outs, ref_lses, D)) < 1e-2
+    assert relerr(host_f64(out), full) < 1e-2

@@ -292,3 +292,38 @@ def test_layer_composition_matches_unpaged_dense_reference():
         d = dec(lw.w_d) @ (gg / (1 + np.exp(-gg)) * uu)
         ref = np.float32(r2 + d).astype(np.float64)
         assert np.allclose(r_out[b], ref, rtol=1e-6, atol=1e-6)
+
+
+# ------------------------------------------------------------------ f2: KV shards + LSE merge
+def test_lse_merge_of_shards_equals_full_attention():
+    from oracle import layer as OL
+    """Splitting every sequence's keys into disjoint shards and merging the
+    shard partials by their log-sum-exp is the softmax over the union (exact
+    in fp64), including a shard that holds no key of a sequence."""
+    import synth
+    g = synth.rng(77)
+    m, Hq, Hkv, D, C, S = 3, 4, 2, 32, 48, 3
+    pps = C // 16
+    bt = synth.block_table(g, m, pps)
+    kc = OL.bf16_to_f64(synth.normal_bf16(g, (m * pps, Hkv, 16, D)))
+    vc = OL.bf16_to_f64(synth.normal_bf16(g, (m * pps, Hkv, 16, D)))
+    q = OL.bf16_to_f64(synth.normal_bf16(g, (m, Hq * D)))
+    sl = np.array([48, 20, 33], np.int32)           # sequence 1 has no key in shard 2
+    full = OL.paged_decode_attention(q, kc, vc, bt, sl, Hq, Hkv, D, 16, "f64")
+    T = C // S
+    outs, lses = [], []
+    for s in range(S):
+        bts = bt[:, s * T // 16:(s + 1) * T // 16]
+        sls = np.clip(sl - s * T, 0, T)
+        o, l = OL.paged_decode_attention_lse(q, kc, vc, bts, sls, Hq, Hkv, D)
+        outs.append(o)
+        lses.append(l)
+    assert np.isneginf(lses[2][1]).all()
+    merged = OL.lse_merge(outs, lses, D)
+    assert np.allclose(merged, full, rtol=0, atol=1e-12)
+    # lse of one shard over everything: log2 Σ exp(s) by brute force for one (row, head)
+    o1, l1 = OL.paged_decode_attention_lse(q, kc, vc, bt, sl, Hq, Hkv, D)
+    b, h = 0, 3
+    kv = h // (Hq // Hkv)
+    s_t = [float(kc[bt[b][t // 16], kv, t % 16] @ q[b, h * D:(h + 1) * D]) / np.sqrt(D) for t in range(sl[b])]
+    assert abs(l1[b, h] - np.log2(np.sum(np.exp(s_t)))) < 1e-12
