@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
     uint64_t pol = 0;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     uint32_t gj = 0;
-    long long pw = 0, p_tot = 0, p_item = 0, p_issue = 0;
+    long long pw = 0, p_item = 0, p_issue = 0;
     const long long p_start = P.prof ? clock64() : 0;
     unsigned long long p_gt0 = 0;
     if (P.prof) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(p_gt0));

@@ -943,16 +943,6 @@ struct Geometry {
   long long units;
 };
 
-static int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      n = kNumSMs;
-  }
-  return n;
-}
-
 static kd_status geometry(const GemmShape& a, Geometry* g, int sms) {
   if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "gemm: only bf16 (fp32 path not built)");
   if (a.M == 0 || a.N == 0 || a.K == 0 || a.rows_total == 0) return fail(KD_ERR_INVALID_ARG, "gemm: empty shape");

@@ -344,7 +344,7 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
   if (!rt) return fail(KD_ERR_INVALID_ARG, "kd_runtime_prepare: NULL runtime");
   const kd_plan* P = rt->plan;
   const kd_graph* g = P->g;
-  const uint32_t n = P->n_dev, N = P->n_micro;
+  const uint32_t n = P->n_dev;
   const uint32_t EXT = KD_BUF_WEIGHT | KD_BUF_INPUT | KD_BUF_OUTPUT | KD_BUF_PERSISTENT;
   for (uint32_t v = 0; v < n; ++v)
     if (!rt->ws_of[v]) return fail(KD_ERR_STATE, "kd_runtime_prepare: workspace of device " + std::to_string(v) + " not set");
