@@ -21,7 +21,15 @@ def _port():
     return p
 
 
-def _rank(rank, world, port, q, steps):
+def _graph(DEC, kind, cfg):
+    if kind == "sharded":  # f2: 2 KV shards (devices 0, 1) + GEMMs (device 2), LSE partials streamed to the merge
+        dg = DEC.ShardedKVDecoderGraph(cfg, 2)
+        return dg, dg.assign(), 3
+    dg = DEC.DecoderGraph(cfg)
+    return dg, dg.role_assign(0, 1), 2
+
+
+def _rank(rank, world, port, q, steps, kind="pair"):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -33,8 +41,8 @@ def _rank(rank, world, port, q, steps):
         from paper_2604_10180_b200 import decoder as DEC
         cfg = synth.TINY
         inp = synth.make_decoder_inputs(cfg)
-        dg = DEC.DecoderGraph(cfg)
-        rt = DEC.DecoderRuntime(dg, dg.role_assign(0, 1), 2, [0], inputs=inp, local_devs=[rank], dist=dist)
+        dg, assign, n_dev = _graph(DEC, kind, cfg)
+        rt = DEC.DecoderRuntime(dg, assign, n_dev, [0], inputs=inp, local_devs=[rank], dist=dist)
         for _ in range(steps):
             rt.step()
         rt.sync()
@@ -46,15 +54,16 @@ def _rank(rank, world, port, q, steps):
         dist.destroy_process_group()
 
 
-def test_two_processes_ipc_bitwise_equals_monolithic(cuda_ok):
+@pytest.mark.parametrize("kind,world", [("pair", 2), ("sharded", 3)])
+def test_processes_ipc_bitwise_equals_monolithic(cuda_ok, kind, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
     steps = 2
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, q, steps)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q, steps, kind)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict((r, (x, n)) for r, x, n in [q.get(timeout=600) for _ in range(2)])
+    res = dict((r, (x, n)) for r, x, n in [q.get(timeout=600) for _ in range(world)])
     for p in procs:
         p.join(120)
         assert p.exitcode == 0
@@ -62,7 +71,7 @@ def test_two_processes_ipc_bitwise_equals_monolithic(cuda_ok):
     from paper_2604_10180_b200 import decoder as DEC
     cfg = synth.TINY
     inp = synth.make_decoder_inputs(cfg)
-    dg = DEC.DecoderGraph(cfg)
+    dg, _, _ = _graph(DEC, kind, cfg)
     mono = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp)
     for _ in range(steps):
         mono.step()
