@@ -54,6 +54,7 @@ struct Params {
   unsigned* work;     // item ticket counter (last word of the counter region)
   unsigned long long* prof;  // KD_ATTN_PROF experiments: [0] producer empty-wait cycles, [1] consumer full-wait, [2] consumer busy, [3] pages
   int Hq, Hkv, G, pps, splits, pages_per_split;
+  int prefetch;       // stream the first item's safe pages before griddepcontrol.wait (KD_ATTN_PREFETCH=0 disables)
   float scale_log2;   // log2(e)/sqrt(D)
   Epi epi;
 };
@@ -196,7 +197,6 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
   __shared__ float s_w[kWarps * kMaxG], s_M[kMaxG], s_L[kMaxG];  // epilogue merge weights
 
   pdl_launch_dependents();
-  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -216,6 +216,10 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // every warp but the producer waits for the previous grid here; the
+  // producer first streams the K/V pages of its statically assigned first
+  // item that the previous kernels cannot be writing (see the producer)
+  if (warp != kWarps) pdl_wait();
   const bool single = (P.splits == 1);
   auto next_item = [&](int k) -> int {  // consumer / epilogue side of the item ring
     const int is = k & 3;
@@ -234,14 +238,19 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
       const int j = j0 + lane, pg = split * P.pages_per_split + j;
       return (j < P.pages_per_split && pg < P.pps) ? __ldg(P.bt + (size_t)b * P.pps + pg) : 0;
     };
+    // CTA c's first item is c (static); tickets t ≥ 0 hand out items
+    // gridDim.x + t. Every CTA draws exactly one failing ticket, so the last
+    // ticket value is max(0, n_items − grid) + grid − 1: its drawer resets the
+    // counter for the next launch.
+    const unsigned n_dyn = n_items > (int)gridDim.x ? (unsigned)(n_items - (int)gridDim.x) : 0u;
     auto fetch = [&]() -> int {
       unsigned t = 0;
       if (lane == 0) {
         t = atomicAdd(P.work, 1u);
-        if (t == (unsigned)(n_items + gridDim.x - 1)) atomicExch(P.work, 0u);  // last ticket: reset
+        if (t == n_dyn + gridDim.x - 1) atomicExch(P.work, 0u);  // last ticket: reset
       }
       t = __shfl_sync(0xffffffffu, t, 0);
-      return t < (unsigned)n_items ? (int)t : -1;
+      return t < n_dyn ? (int)(gridDim.x + t) : -1;
     };
     uint64_t pol = 0;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -250,8 +259,36 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
     const long long p_start = P.prof ? clock64() : 0;
     unsigned long long p_gt0 = 0;
     if (P.prof) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(p_gt0));
-    int it = fetch();
-    int mine = ids_of(it, 0);
+    // ---- before the grid-dependency wait: the first item (static) and its
+    // first min(S, pages) K/V slabs, all strictly before the page holding
+    // position len−1 — the only page of a sequence this step's RoPE/append
+    // writes. The block table and lengths are step inputs (not written by
+    // the previous kernels). The ticket counter is only touched after the wait.
+    const int it0 = (int)blockIdx.x < n_items ? (int)blockIdx.x : -2;  // −2: draw after the wait
+    int n_pre = 0;
+    int mine = ids_of(it0 < 0 ? -1 : it0, 0);
+    if (it0 >= 0 && P.prefetch) {
+      const int split = it0 % P.splits, unit = it0 / P.splits;
+      const int g = unit % Hkv, b = unit / Hkv;
+      const int len = __ldg(P.sl + b);
+      const int p0 = split * P.pages_per_split;
+      const int np = max(0, min((len + kPage - 1) / kPage, p0 + P.pages_per_split) - p0);
+      const int safe = max(0, min(np, (len - 1) / kPage - p0));  // pages before the appended one
+      n_pre = min(min(S, 32), safe);
+      for (int t = 0; t < n_pre; ++t) {
+        const int pid = __shfl_sync(0xffffffffu, mine, t);
+        if (lane == 0) {
+          const int row = (pid * Hkv + g) * kPage;
+          mbar_expect_tx(&full[t], 2u * SLAB_B);
+          tma_3d(ks + t * SLAB_B, &tk, 0, 0, row, &full[t], pol);
+          tma_3d(vs + t * SLAB_B, &tv, 0, 0, row, &full[t], pol);
+        }
+      }
+      gj = (uint32_t)n_pre;
+    }
+    pdl_wait();
+    int it = it0 == -2 ? fetch() : it0;
+    if (it0 == -2) mine = ids_of(it, 0);
     for (int k = 0;; ++k) {
       if (lane == 0) {  // publish the item (or the end marker -1)
         const int is = k & 3;
@@ -278,7 +315,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
         const bool more = j0 + 32 < np;
         const int nxt = more ? ids_of(it, j0 + 32) : ids_of(it_next, 0);
         const int cnt = min(32, np - j0);
-        for (int t = 0; t < cnt; ++t, ++gj) {
+        for (int t = (k == 0 && j0 == 0) ? n_pre : 0; t < cnt; ++t, ++gj) {  // slabs already in flight skipped
           const int pid = __shfl_sync(0xffffffffu, mine, t);
           const long long tq = P.prof ? clock64() : 0;
           if (lane == 0) {
@@ -709,6 +746,10 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
   P.sl = sl;
   P.out = (__nv_bfloat16*)out;
   P.lse_off = (size_t)a.rows * a.n_heads * a.head_dim * 2;
+  {
+    const char* e = getenv("KD_ATTN_PREFETCH");
+    P.prefetch = e ? atoi(e) : 1;
+  }
   P.lse = (a.flags & KD_ATTN_LSE) ? (float*)((uint8_t*)out + P.lse_off) : nullptr;
   const uint64_t units = (uint64_t)a.rows * a.n_kv_heads;
   if (units >= kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "attention: too many (sequence, kv head) units");
