@@ -293,15 +293,43 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float4* parts = reinterpret_cast<const float4*>(A.part + (size_t)t * A.max_contrib * part_elems);
             const int per = (int)(part_elems / 4);
             if (A.silu) {  // gate float4 (rows r..r+3 < 64) with its up partner 16 float4s on
-              for (int w = ep_tid; w < A.M * 16; w += 128) {
-                const int j = w >> 4, wg = j * 32 + (w & 15);
-                float4 g = __ldcg(parts + wg), uu = __ldcg(parts + wg + 16);
-                for (int k = 1; k < n_contrib; ++k) {  // contributor order → deterministic
-                  const float4 x = __ldcg(parts + (size_t)k * per + wg), y = __ldcg(parts + (size_t)k * per + wg + 16);
-                  g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
-                  uu.x += y.x; uu.y += y.y; uu.z += y.z; uu.w += y.w;
+              // 4 items per round with every (item, contributor) load in flight
+              // together: the fold is L2-latency-bound, not bandwidth-bound
+              constexpr int kI = 4;
+              for (int w0 = ep_tid; w0 < A.M * 16; w0 += 128 * kI) {
+                float4 g[kI], uu[kI];
+#pragma unroll
+                for (int i = 0; i < kI; ++i) {
+                  const int w = w0 + 128 * i;
+                  if (w < A.M * 16) {
+                    const int wg = (w >> 4) * 32 + (w & 15);
+                    g[i] = __ldcg(parts + wg);
+                    uu[i] = __ldcg(parts + wg + 16);
+                  }
                 }
-                if (j < mv) store_silu4(A, (size_t)(y0 + j) * (A.N / 2) + (nb0 / 2) + (w & 15) * 4, g, uu);
+                for (int k = 1; k < n_contrib; ++k) {  // contributor order → deterministic
+                  float4 x[kI], y[kI];
+#pragma unroll
+                  for (int i = 0; i < kI; ++i) {
+                    const int w = w0 + 128 * i;
+                    if (w < A.M * 16) {
+                      const int wg = (w >> 4) * 32 + (w & 15);
+                      x[i] = __ldcg(parts + (size_t)k * per + wg);
+                      y[i] = __ldcg(parts + (size_t)k * per + wg + 16);
+                    }
+                  }
+#pragma unroll
+                  for (int i = 0; i < kI; ++i) {
+                    g[i].x += x[i].x; g[i].y += x[i].y; g[i].z += x[i].z; g[i].w += x[i].w;
+                    uu[i].x += y[i].x; uu[i].y += y[i].y; uu[i].z += y[i].z; uu[i].w += y[i].w;
+                  }
+                }
+#pragma unroll
+                for (int i = 0; i < kI; ++i) {
+                  const int w = w0 + 128 * i, j = w >> 4;
+                  if (w < A.M * 16 && j < mv)
+                    store_silu4(A, (size_t)(y0 + j) * (A.N / 2) + (nb0 / 2) + (w & 15) * 4, g[i], uu[i]);
+                }
               }
             }
             for (int w = ep_tid; w < (A.silu ? 0 : per); w += 128) {
