@@ -338,8 +338,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int k = 0; k < 4; ++k)
                 if (k < n_contrib) xs[k] = __ldcg(parts + (size_t)k * per + w);
               float4 acc = xs[0];
-              for (int k = 1; k < n_contrib; ++k) {  // contributor order → deterministic
-                const float4 x = k < 4 ? xs[k] : __ldcg(parts + (size_t)k * per + w);
+#pragma unroll
+              for (int k = 1; k < 4; ++k)  // contributor order → deterministic (static indices: no local memory)
+                if (k < n_contrib) {
+                  acc.x += xs[k].x;
+                  acc.y += xs[k].y;
+                  acc.z += xs[k].z;
+                  acc.w += xs[k].w;
+                }
+              for (int k = 4; k < n_contrib; ++k) {
+                const float4 x = __ldcg(parts + (size_t)k * per + w);
                 acc.x += x.x;
                 acc.y += x.y;
                 acc.z += x.z;
