@@ -84,6 +84,11 @@ __device__ __forceinline__ float from_f<float>(float x) { return x; }
 template <>
 __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 
+// silu(x) = x·sigmoid(x) with the fast divide (≈2 ulp; outputs are bf16): the
+// one definition shared by the SiLU kernel and the fused gate_up+SiLU epilogue,
+// so the two produce identical bits
+__device__ __forceinline__ float silu_fast(float x) { return __fdividef(x, 1.f + __expf(-x)); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -199,7 +199,7 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloa
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       float g0 = bf16lo(gp[q]), g1 = bf16hi(gp[q]);
-      float s0 = g0 / (1.f + __expf(-g0)), s1 = g1 / (1.f + __expf(-g1));
+      float s0 = silu_fast(g0), s1 = silu_fast(g1);
       op[q] = pack_bf16(s0 * bf16lo(up[q]), s1 * bf16hi(up[q]));
     }
     size_t e = (size_t)row * per_row + c8;

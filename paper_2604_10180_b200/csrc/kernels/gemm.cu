@@ -80,7 +80,7 @@ __host__ __device__ __forceinline__ long long unit_owner(long long u, long long 
 __device__ __forceinline__ float rbf(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 __device__ __forceinline__ uint32_t silu2(float g0, float g1, float u0, float u1) {
   g0 = rbf(g0), g1 = rbf(g1), u0 = rbf(u0), u1 = rbf(u1);
-  const float s0 = g0 / (1.f + __expf(-g0)), s1 = g1 / (1.f + __expf(-g1));
+  const float s0 = silu_fast(g0), s1 = silu_fast(g1);
   return pack_bf16(s0 * u0, s1 * u1);
 }
 // store 4 fused outputs a[row][col..col+3] (row stride ldy) to Y and every peer copy
