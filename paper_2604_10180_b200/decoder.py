@@ -592,6 +592,11 @@ class DecoderRuntime:
                 self._ipc.append(p)
                 self.rt.set_peer_workspace(d, p)
             dist.barrier(group=dist_group)
+        # the fills and zeroed workspaces above ran on the default stream; the
+        # step runs on its own streams — order them (a step must never see an
+        # unfilled input or a non-zero flag/counter word)
+        for d in self.local_devs:
+            torch.cuda.synchronize(self.dev_map[d])
         self.rt.prepare()
         self.streams = [torch.cuda.Stream(device=f"cuda:{self.dev_map[d]}") for d in self.local_devs]
 

@@ -25,6 +25,8 @@ def timeit(fn, iters=20, warm=3):
     """Device time per launch: the launches are captured in a CUDA graph so the
     host (ctypes, descriptor encoding) never starves the GPU."""
     s = torch.cuda.Stream()
+    torch.cuda.synchronize()  # inputs were produced on the default stream
+    s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
         for _ in range(warm):
             fn(0)
