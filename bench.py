@@ -211,9 +211,13 @@ def main():
         # QKV + RoPE/append (KD_OP_QKV_ROPE) is built and bit-identical too, but measured
         # slower than the pair (27.5 vs 19.3 µs at the 8B shape: the cluster GEMM's
         # epilogue is the expensive place for per-element trig), so it is opt-in
-        # (KD_BENCH_FUSE_ROPE=1).
+        # (KD_BENCH_FUSE_ROPE=1). The O GEMM with norm2 and the down GEMM with the next
+        # layer's norm1 run as one kernel each (KD_OP_GEMM_RMSNORM: the per-token Σr² is
+        # finished across the grid after an in-kernel barrier), measured 9.13 vs 9.17 ms
+        # per step (KD_BENCH_NO_FUSE_NORM=1 for the A/B).
         fuse = not os.environ.get("KD_BENCH_NO_FUSE")
-        dg = DEC.DecoderGraph(cfg, fuse_silu=fuse, fuse_rope=fuse and bool(os.environ.get("KD_BENCH_FUSE_ROPE")))
+        dg = DEC.DecoderGraph(cfg, fuse_silu=fuse, fuse_rope=fuse and bool(os.environ.get("KD_BENCH_FUSE_ROPE")),
+                              fuse_norm=fuse and not os.environ.get("KD_BENCH_NO_FUSE_NORM"))
         assign = [0] * dg.g.num_kernels
         rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed, use_graph=not args.no_graph)
         placement = "monolithic (all kernels on one B200)"
@@ -394,6 +398,7 @@ def main():
     if args.kernels:
         kernels = {}
         for op, nm in ((K.KD_OP_GEMM, "gemm"), (K.KD_OP_GEMM_SILU, "gemm_silu"), (K.KD_OP_QKV_ROPE, "qkv_rope"),
+                       (K.KD_OP_GEMM_RMSNORM, "gemm_rmsnorm"),
                        (K.KD_OP_ADD_RMSNORM, "add_rmsnorm"),
                        (K.KD_OP_ROPE_APPEND, "rope_append"), (K.KD_OP_SILU_MUL, "silu_mul")):
             rt.rt.profile_op(op)

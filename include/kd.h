@@ -103,7 +103,11 @@ enum {
                             * block_table, seq_len] writes [q, Kc, Vc] with kd_attr_qkv_rope. W_qkv' = the
                             * kv-group-interleaved QKV weight with rows pair-interleaved inside every head
                             * (row 2p ← dim p, row 2p+1 ← dim p + D/2); bits identical to a4 then a5 */
-  KD_OP_ATTN_MERGE = 16    /* f2 reads [part_0 .. part_{n-1}] ([out|lse] of KD_ATTN_LSE attentions) writes [out] */
+  KD_OP_ATTN_MERGE = 16,   /* f2 reads [part_0 .. part_{n-1}] ([out|lse] of KD_ATTN_LSE attentions) writes [out] */
+  KD_OP_GEMM_RMSNORM = 17  /* a7+a3 / a10+a3 fused (co-located O or down GEMM and the next residual add +
+                            * RMSNorm): reads [X, W, r, gamma] writes [h, r] with kd_attr_gemm_rmsnorm:
+                            * r' = r + bf16(X·Wᵀ) (bits identical to a GEMM then a3's add), h =
+                            * r'/sqrt(mean r'² + eps)·gamma (Σr'² in another order than a3: not bitwise) */
 };
 
 /* element types of activations / KV */
@@ -118,6 +122,8 @@ enum { KD_BF16 = 0, KD_F32 = 1 };
  * row-parallel GEMMs' fused peer stores. */
 typedef struct { uint32_t rows, hidden, n_delta, dtype; float eps; uint32_t pad_; } kd_attr_add_rmsnorm;
 typedef struct { uint32_t M, N, K, dtype; } kd_attr_gemm;            /* X [M,K], W [N,K] row-major, Y [M,N] */
+/* X [M,K], W [N,K] (N = hidden), r fp32 [M,N], gamma [N], h [M,N]; bf16 only */
+typedef struct { uint32_t M, N, K, dtype; float eps; uint32_t pad_; } kd_attr_gemm_rmsnorm;
 /* slot_offset: tokens of each sequence held by earlier KV shards (f2, long
  * context split over devices): the rotation angle uses the absolute position
  * seq_len − 1, the appended slot is (seq_len − 1 − slot_offset) in this
@@ -394,6 +400,14 @@ kd_status kd_op_gemm_silu(const kd_attr_gemm* a, const void* X, const void* W, v
                           void* stream);
 kd_status kd_op_gemm(const kd_attr_gemm* a, const void* X, const void* W, void* Y,
                      void* scratch, void* stream);
+/* a7/a10 + a3 fused (KD_OP_GEMM_RMSNORM): r (fp32 [M,N], in place) += bf16(X·Wᵀ),
+ * h [M,N] = RMSNorm(r)·gamma. One cluster split-K launch; the per-token Σr² is
+ * completed across its CTAs after an in-kernel grid barrier (all CTAs are
+ * co-resident by construction). bf16 only, N % 8 == 0; r and gamma 16-byte
+ * aligned; scratch as kd_op_scratch_bytes(KD_OP_GEMM_RMSNORM). Errors:
+ * KD_ERR_UNSUPPORTED when no co-resident cluster tiling exists for the shape. */
+kd_status kd_op_gemm_rmsnorm(const kd_attr_gemm_rmsnorm* a, const void* X, const void* W, float* r,
+                             const void* gamma, void* h, void* scratch, void* stream);
 /* a5: NeoX RoPE of q and k at pos = seq_len[b]-1, append (k_rot, v) to the
  * HND paged cache [pages][Hkv][page][D]; q_out [rows, Hq·D]. */
 kd_status kd_op_rope_append(const kd_attr_rope_append* a, const void* qkv, const int32_t* block_table,

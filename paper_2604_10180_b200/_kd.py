@@ -25,7 +25,8 @@ KD_BUF_WEIGHT, KD_BUF_INPUT, KD_BUF_OUTPUT, KD_BUF_PERSISTENT, KD_BUF_PER_MICROB
 # ops
 KD_OP_NONE, KD_OP_ADD_RMSNORM, KD_OP_GEMM, KD_OP_ROPE_APPEND, KD_OP_ATTENTION, KD_OP_SILU_MUL, \
     KD_OP_RESIDUAL_ADD, KD_OP_MOE_ROUTE, KD_OP_MOE_DISPATCH, KD_OP_GROUPED_GEMM, KD_OP_MOE_COMBINE, \
-    KD_OP_SSM_CONV, KD_OP_SSM_UPDATE, KD_OP_GATED_NORM, KD_OP_GEMM_SILU, KD_OP_QKV_ROPE, KD_OP_ATTN_MERGE = range(17)
+    KD_OP_SSM_CONV, KD_OP_SSM_UPDATE, KD_OP_GATED_NORM, KD_OP_GEMM_SILU, KD_OP_QKV_ROPE, KD_OP_ATTN_MERGE, \
+    KD_OP_GEMM_RMSNORM = range(18)
 KD_BF16, KD_F32 = 0, 1
 KD_OBJ_AUTO, KD_OBJ_THROUGHPUT, KD_OBJ_LATENCY = 0, 1, 2
 KD_MODE_DISAGG, KD_MODE_NO_TRANSFER, KD_MODE_LOG = 0, 1, 2
@@ -76,6 +77,11 @@ class kd_attr_qkv_rope(C.Structure):
     _fields_ = [("rows", C.c_uint32), ("hidden", C.c_uint32), ("n_heads", C.c_uint32), ("n_kv_heads", C.c_uint32),
                 ("head_dim", C.c_uint32), ("page", C.c_uint32), ("pages_per_seq", C.c_uint32), ("dtype", C.c_uint32),
                 ("theta", C.c_double)]
+
+
+class kd_attr_gemm_rmsnorm(C.Structure):
+    _fields_ = [("M", C.c_uint32), ("N", C.c_uint32), ("K", C.c_uint32), ("dtype", C.c_uint32),
+                ("eps", C.c_float), ("pad_", C.c_uint32)]
 
 
 class kd_attr_attn_merge(C.Structure):
@@ -200,6 +206,7 @@ _PROTOS = {
     "kd_op_add_rmsnorm": (kd_status, [C.POINTER(kd_attr_add_rmsnorm), P, P, P, P, P]),
     "kd_op_gemm": (kd_status, [C.POINTER(kd_attr_gemm), P, P, P, P, P]),
     "kd_op_gemm_silu": (kd_status, [C.POINTER(kd_attr_gemm), P, P, P, P, P]),
+    "kd_op_gemm_rmsnorm": (kd_status, [C.POINTER(kd_attr_gemm_rmsnorm), P, P, P, P, P, P, P]),
     "kd_op_attn_merge": (kd_status, [C.POINTER(kd_attr_attn_merge), P, P, P]),
     "kd_op_qkv_rope": (kd_status, [C.POINTER(kd_attr_qkv_rope), P, P, P, P, P, P, P, P, P]),
     "kd_op_rope_append": (kd_status, [C.POINTER(kd_attr_rope_append), P, P, P, P, P, P, P]),

@@ -285,6 +285,12 @@ def gemm_silu(attrs, X, W, out, scratch, stream=None):
     check(K.kd_op_gemm_silu(C.byref(attrs), _p(X), _p(W), _p(out), _p(scratch), _stream(stream)), "kd_op_gemm_silu")
 
 
+def gemm_rmsnorm(attrs, X, W, r, gamma, h, scratch, stream=None):
+    """a7/a10 + a3 fused: r += bf16(X·Wᵀ) (fp32, in place); h = RMSNorm(r)·gamma."""
+    check(K.kd_op_gemm_rmsnorm(C.byref(attrs), _p(X), _p(W), _p(r), _p(gamma), _p(h), _p(scratch),
+                               _stream(stream)), "kd_op_gemm_rmsnorm")
+
+
 def qkv_rope(attrs, X, W, block_table, seq_len, q_out, k_cache, v_cache, scratch, stream=None):
     """a4+a5 fused: QKV GEMM with the RoPE + KV-append epilogue (W rows pair-interleaved per head)."""
     check(K.kd_op_qkv_rope(C.byref(attrs), _p(X), _p(W), _p(block_table), _p(seq_len), _p(q_out), _p(k_cache),

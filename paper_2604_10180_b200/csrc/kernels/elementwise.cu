@@ -115,10 +115,6 @@ kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const Delta
   if (a.dtype == KD_F32) return launch_add_rmsnorm_f32(a, r, as_f32(d), (const float*)gamma, (float*)h, c, signals);
   if (a.rows == 0 || a.hidden == 0 || a.hidden % 8 || a.hidden > 8 * kNormThreads * kNormChunks)
     return fail(KD_ERR_UNSUPPORTED, "add_rmsnorm: hidden must be a multiple of 8 and <= 8192");
-  if (a.n_delta > (uint32_t)kMaxDeltas || (int)a.n_delta != d.n)
-    return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: n_delta must match the deltas given (<= 8)");
-  for (int i = 0; i < d.n; ++i)
-    if (!d.p[i]) return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: NULL delta");
   if (!r || !gamma || !h) return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: NULL pointer");
   KD_CUDA_CHECK(kd_launch(add_rmsnorm_kernel, dim3(a.rows), dim3(kNormThreads), 0, c.stream, r, d,
                           (const __nv_bfloat16*)gamma, (__nv_bfloat16*)h, (int)a.hidden, a.eps, c.epi),
@@ -484,7 +480,6 @@ static kd_status attrs_of(const std::vector<uint8_t>& v, T* out) {
 }
 
 kd_status attention_signals(const kd_attr_attention& a, uint32_t* s);  // attention.cu
-kd_status gemm_signals(const kd_attr_gemm& a, uint32_t* s);            // gemm.cu
 
 kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* signals) {
   kd_status st = KD_OK;
@@ -509,6 +504,7 @@ kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s
     case KD_OP_GEMM: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
     case KD_OP_GEMM_SILU: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a, true), signals); }
     case KD_OP_QKV_ROPE: { kd_attr_qkv_rope a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
+    case KD_OP_GEMM_RMSNORM: { kd_attr_gemm_rmsnorm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
     case KD_OP_GROUPED_GEMM: { kd_attr_grouped_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_signals(gemm_shape(a), signals); }
     case KD_OP_MOE_ROUTE:
     case KD_OP_MOE_DISPATCH:

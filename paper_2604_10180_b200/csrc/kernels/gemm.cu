@@ -594,6 +594,14 @@ struct Args {
   unsigned long long* trace;
   int rope;      // KD_OP_QKV_ROPE: epilogue = a5 (RoPE + KV append) on the bf16 QKV output
   RopeEpi rp;
+  // KD_OP_GEMM_RMSNORM: epilogue = a3 on the bf16 output across the whole grid
+  // (r += bf16(X·Wᵀ); Y = RMSNorm(r)·γ), per-token Σr² completed after a grid barrier
+  int norm;
+  float* r;                     // [M][N] fp32 residual (read + written)
+  const __nv_bfloat16* gamma;   // [N]
+  float eps;
+  unsigned* bar;                // 2 self-resetting words (scratch)
+  float* ssq;                   // [M][gridDim.x] per-CTA partial Σr² (scratch)
 };
 
 // a5 fused into the QKV GEMM epilogue. W rows are pair-interleaved within each
@@ -664,6 +672,198 @@ __device__ __forceinline__ void csk_store4(const Args& A, int j, int col, float 
   }
 }
 
+// a3 fused into the GEMM epilogue (KD_OP_GEMM_RMSNORM). Each CTA owns weight
+// rows [c0, c0 + rows) of every token. While the main loop streams, the idle
+// warps 2-3 stage this slice of r (fp32) and gamma into shared memory (rs,
+// gs), so the epilogue's only global round trips are the grid barrier and one
+// batch of partial-sum loads (measured ≈0.5-1 µs per dependent global round
+// trip in this phase). After the role branches, all 384 threads:
+//   A: v = Σ partials (rank order); r' = r + bf16(v) → r (global) and rs
+//   B: per token, this CTA's Σ r'² (warp per token, fixed shuffle tree) → ssq[j][cta]
+//   grid barrier (all CTAs co-resident: tiles ≤ max co-resident clusters)
+//   C: per token, Σ over CTAs (fixed order) → inv = rsqrt(Σ/N + eps);
+//   D: Y = bf16(r'·inv·γ), exactly a3's rounding.
+struct NormSmem {
+  float* rs;            // [M][Tp] fp32: r slice, then r'
+  __nv_bfloat16* gs;    // [rows] gamma slice
+  float* invs;          // [M] 1/rms
+  int Tp;
+};
+
+__device__ __forceinline__ int norm_rows(const Args& A, int rank, int n0, int my_rows, int* c0) {
+  *c0 = A.split > 1 ? n0 + rank * A.rpo : n0;
+  return A.split > 1 ? max(0, min(my_rows, A.N - *c0)) : min(kBM, A.N - n0);  // valid rows of the tail tile
+}
+
+// warps 2-3 during the main loop
+__device__ __forceinline__ void norm_stage(const Args& A, const NormSmem& ns, int rank, int n0, int my_rows) {
+  const int t = threadIdx.x - 64;
+  int c0;
+  const int rows = norm_rows(A, rank, n0, my_rows, &c0), r4n = rows / 4, M = A.M;
+  for (int i = t; i < r4n; i += 64)  // gamma is a weight: before the dependency wait
+    *reinterpret_cast<uint2*>(ns.gs + 4 * i) = __ldg(reinterpret_cast<const uint2*>(A.gamma + c0 + 4 * i));
+  pdl_wait();  // r is written by earlier kernels
+  constexpr int kB = 8;  // loads in flight per thread
+  for (int e0 = t; e0 < M * r4n; e0 += 64 * kB) {
+    float4 v[kB];
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const int e = e0 + 64 * b, j = e / r4n, l4 = e - j * r4n;
+      if (e < M * r4n) v[b] = __ldcg(reinterpret_cast<const float4*>(A.r + (size_t)j * A.N + c0 + 4 * l4));
+    }
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const int e = e0 + 64 * b, j = e / r4n, l4 = e - j * r4n;
+      if (e < M * r4n) *reinterpret_cast<float4*>(ns.rs + (size_t)j * ns.Tp + 4 * l4) = v[b];
+    }
+  }
+}
+
+__device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns, const float* st, const float* recv,
+                                              uint64_t* rbar, int rank, int n0, int my_rows) {
+  const int split = A.split, M = A.M, N = A.N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* const ssq = A.ssq;
+  float* const rs = ns.rs;
+  const int Tp = ns.Tp;
+  const int G = gridDim.x, Gp = (G + 15) / 16 * 16;  // ssq row pitch
+  __syncthreads();  // staging (split 1) and the r/gamma slices are complete; my own rows are in recv[rank]
+  if (split > 1) mbar_wait(rbar, 0);
+  pdl_wait();
+  if (threadIdx.x == 0) { KD_TRACE(8); KD_CTRACE(22); }
+  int c0;
+  const int rows = norm_rows(A, rank, n0, my_rows, &c0);
+  const int P = (M + 3) / 4 * 4 + 4, r4n = rows / 4;
+  for (int e = threadIdx.x; e < M * r4n; e += kThreads) {
+    int lr4, j;
+    float acc[4];
+    if (split > 1) {  // lanes walk tokens: conflict-free recv column reads
+      lr4 = (e / M) * 4;
+      j = e - (e / M) * M;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) acc[x] = recv[((size_t)lr4 + x) * P + j];
+      for (int cr = 1; cr < split; ++cr)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) acc[x] += recv[((size_t)cr * A.rpo + lr4 + x) * P + j];
+    } else {
+      j = e / r4n;
+      lr4 = (e - j * r4n) * 4;
+      const float4 v = *reinterpret_cast<const float4*>(st + (size_t)j * kBM + lr4);
+      acc[0] = v.x; acc[1] = v.y; acc[2] = v.z; acc[3] = v.w;
+    }
+    float4* sp = reinterpret_cast<float4*>(rs + (size_t)j * Tp + lr4);
+    float4 rv = *sp;
+    rv.x += __bfloat162float(__float2bfloat16_rn(acc[0]));
+    rv.y += __bfloat162float(__float2bfloat16_rn(acc[1]));
+    rv.z += __bfloat162float(__float2bfloat16_rn(acc[2]));
+    rv.w += __bfloat162float(__float2bfloat16_rn(acc[3]));
+    *sp = rv;  // (r' reaches global memory in D, with coalesced stores)
+  }
+  if (threadIdx.x == 0) KD_CTRACE(16);
+  __syncthreads();
+  if (threadIdx.x == 0) KD_CTRACE(17);
+  for (int j = threadIdx.x; j < M; j += kThreads) {  // thread per token, 16-byte reads, l order
+    float ss = 0.f;
+    for (int l4 = 0; l4 < r4n; ++l4) {
+      const float4 v = *reinterpret_cast<const float4*>(rs + (size_t)j * Tp + 4 * l4);
+      ss += v.x * v.x;
+      ss += v.y * v.y;
+      ss += v.z * v.z;
+      ss += v.w * v.w;
+    }
+    ssq[(size_t)j * Gp + blockIdx.x] = ss;
+  }
+  if (threadIdx.x == 0) KD_CTRACE(18);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // grid barrier (self-resetting: see the departure at the end)
+    KD_TRACE(13);
+    KD_CTRACE(24);
+    fence_acq_rel_gpu();
+    atom_add_acq_rel_gpu(A.bar, 1u);
+    while (ld_acquire_gpu(A.bar) < (unsigned)G) {
+    }
+    KD_TRACE(14);
+    KD_CTRACE(23);
+  }
+  __syncthreads();
+  // per token Σ over CTAs: a warp takes kTpw tokens; each lane loads 16-byte
+  // chunks lane and lane + 32 of every row (coalesced, all loads in flight),
+  // sums its components in c order, then the tokens' shuffle trees run
+  // interleaved. Fixed order: deterministic. Entries ≥ G are masked (the pad
+  // of a row is not ours: the scratch is shared with other kernels).
+  {
+    constexpr int kTpw = 6, kCh = (kNormMaxGrid + 127) / 128;  // ≤ 2 float4 per lane per row (G ≤ 160)
+    for (int j0 = warp * kTpw; j0 < M; j0 += kTpw * (kThreads / 32)) {
+      float4 v[kTpw][kCh];
+#pragma unroll
+      for (int t = 0; t < kTpw; ++t)
+#pragma unroll
+        for (int i = 0; i < kCh; ++i) {
+          const int c = (lane + 32 * i) * 4;
+          v[t][i] = (j0 + t < M && c < G) ? __ldcg(reinterpret_cast<const float4*>(ssq + (size_t)(j0 + t) * Gp + c))
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      float sm[kTpw];
+#pragma unroll
+      for (int t = 0; t < kTpw; ++t) {
+        sm[t] = 0.f;
+#pragma unroll
+        for (int i = 0; i < kCh; ++i) {
+          const int c = (lane + 32 * i) * 4;
+          sm[t] += v[t][i].x;
+          sm[t] += c + 1 < G ? v[t][i].y : 0.f;
+          sm[t] += c + 2 < G ? v[t][i].z : 0.f;
+          sm[t] += c + 3 < G ? v[t][i].w : 0.f;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int t = 0; t < kTpw; ++t) sm[t] += __shfl_xor_sync(0xffffffffu, sm[t], o);
+      if (lane < kTpw && j0 + lane < M) {
+        float mine = sm[0];
+#pragma unroll
+        for (int t = 1; t < kTpw; ++t) mine = lane == t ? sm[t] : mine;
+        ns.invs[j0 + lane] = rsqrtf(mine / (float)N + A.eps);
+      }
+    }
+  }
+  if (threadIdx.x == 0) KD_CTRACE(19);
+  __syncthreads();
+  if (threadIdx.x == 0) KD_CTRACE(20);
+  __nv_bfloat16* const Y = A.Y;
+  for (int e = threadIdx.x; e < M * r4n; e += kThreads) {  // lanes walk a token's rows: coalesced h stores
+    const int j = e / r4n, l4 = e - j * r4n;
+    const float inv = ns.invs[j];
+    const float4 v = *reinterpret_cast<const float4*>(rs + (size_t)j * Tp + 4 * l4);
+    const uint2 g = *reinterpret_cast<const uint2*>(ns.gs + 4 * l4);
+    uint2 o;
+    o.x = pack_bf16(v.x * inv * bf16lo(g.x), v.y * inv * bf16hi(g.x));
+    o.y = pack_bf16(v.z * inv * bf16lo(g.y), v.w * inv * bf16hi(g.y));
+    const size_t yo = (size_t)j * N + c0 + 4 * l4;
+    *reinterpret_cast<float4*>(A.r + yo) = v;
+    *reinterpret_cast<uint2*>(Y + yo) = o;
+    for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+  }
+  if (threadIdx.x == 0) {
+    KD_CTRACE(21);
+    KD_TRACE(15);
+    // departure, off the critical path: the last CTA to leave (every CTA has
+    // passed the arrival spin by then) zeroes both words for the next launch
+    if (atom_add_acq_rel_gpu(A.bar + 1, 1u) == (unsigned)G - 1) {
+      A.bar[0] = 0u;
+      A.bar[1] = 0u;
+    }
+  }
+  if (A.epi.n && (split == 1 || my_rows > 0)) {  // publish this CTA's stores (gemm_signals counts these)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_acq_rel_sys();
+      for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_csk_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Args A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -685,6 +885,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* rbar = tfull + 1;
   uint32_t* tmem_slot = (uint32_t*)(rbar + 1);
+  NormSmem ns;                                        // norm: after the barriers
+  ns.invs = (float*)(tmem_slot + 4);                  // [256]
+  ns.Tp = (split > 1 ? A.rpo : kBM) + 4;              // 16-byte rows + pad (conflict-free column walks)
+  ns.rs = ns.invs + 256;                              // [M][Tp]
+  ns.gs = (__nv_bfloat16*)(ns.rs + (size_t)M * ns.Tp);  // [128]
   float* send = (float*)smem;  // split == 1: [M][128] fp32 staging, reuses the idle ring after the last MMA
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -790,6 +995,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       KD_TRACE(5);
     }
     __syncwarp();
+  } else if (A.norm && warp < 4) {
+    // ------------------------------------------------ idle warps 2-3: stage r and gamma (norm)
+    norm_stage(A, ns, rank, n0, my_rows);
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
     // 8 warps: warp w reads TMEM lane quarter (w − 4) mod 4 (its hardware
@@ -836,14 +1044,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < kChunk; ++j)
           if (j0 + j < M) st[(size_t)(j0 + j) * kBM + row] = v[j];
       }
-      named_bar(1, kEpi);
-      pdl_wait();
-      for (int e = ep; e < M * (kBM / 4); e += kEpi) {
-        const int j = e / (kBM / 4), r4 = (e % (kBM / 4)) * 4;
-        const float4 v = *reinterpret_cast<const float4*>(st + (size_t)j * kBM + r4);
-        if (n0 + r4 < A.N) store_y(j, n0 + r4, v.x, v.y, v.z, v.w);
+      if (!A.norm) {  // (norm: the staged tile is finished after the role branches)
+        named_bar(1, kEpi);
+        pdl_wait();
+        for (int e = ep; e < M * (kBM / 4); e += kEpi) {
+          const int j = e / (kBM / 4), r4 = (e % (kBM / 4)) * 4;
+          const float4 v = *reinterpret_cast<const float4*>(st + (size_t)j * kBM + r4);
+          if (n0 + r4 < A.N) store_y(j, n0 + r4, v.x, v.y, v.z, v.w);
+        }
+        stored = true;
       }
-      stored = true;
     } else {
       // Each thread owns one weight row of the partial (its TMEM lane) and
       // sends it, 64 token columns at a time, straight from registers to the
@@ -890,7 +1100,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (ep == 0) { KD_TRACE(9); KD_CTRACE(26); }
   }
-  if (split > 1) {
+  if (A.norm) {
+    norm_epilogue(A, ns, send, recv, rbar, rank, n0, my_rows);
+  } else if (split > 1) {
     // ---- owner sum with all 384 threads (the TMA/MMA warps are idle by now):
     // my rows [rank·rpo, +my_rows), Σ over ranks in order; lanes walk tokens
     // (conflict-free column reads), each thread 4 consecutive weight rows
@@ -1015,9 +1227,14 @@ static size_t smem_bytes(const Geometry& g) {
 // ---------------------------------------------------------------- dense GEMM kernel choice
 namespace csk {
 
-static size_t smem_for(int mma_n, int kbs, int stages, int split, int rpo, int M) {
+static size_t smem_for(int mma_n, int kbs, int stages, int split, int rpo, int M, bool norm) {
   const size_t recv = split > 1 ? (size_t)split * ((M + 3) / 4 * 4 + 4) * rpo * 4 : 0;
-  return 1024 + (size_t)stages * kbs * (kStageA + (size_t)mma_n * kBK * 2) + recv + (2 * kMaxStages + 4) * 8 + 16;
+  if (norm) {  // + the r slice [M][Tp] fp32 and the gamma slice
+    const size_t tp = (split > 1 ? rpo : kBM) + 4;
+    return smem_for(mma_n, kbs, stages, split, rpo, M, false) + (size_t)M * tp * 4 + 256;
+  }
+  return 1024 + (size_t)stages * kbs * (kStageA + (size_t)mma_n * kBK * 2) + recv + (2 * kMaxStages + 4) * 8 + 16 +
+         256 * 4;  // + the norm epilogue's per-token 1/rms
 }
 
 // co-resident clusters of `split` CTAs (one CTA per SM at this kernel's smem),
@@ -1076,13 +1293,14 @@ static kd_status choose(const GemmShape& a, GemmTile* t, double* best_ns) {
     if (force_s && s != force_s) continue;
     const int maxc = max_clusters(s);
     if (tiles > maxc) continue;
+    if (a.norm && tiles * s > kNormMaxGrid) continue;  // per-CTA partial sums in scratch
     const int kbs = mma_n <= 128 ? 2 : 1;
     const int KB = (int)((a.K + kBK * kbs - 1) / (kBK * kbs));
     if (s > KB) continue;
     const int rpo = s > 1 ? ((kBM + s - 1) / s + 3) / 4 * 4 : 0;
     if (s > 1 && (rpo * (s - 1) >= kBM)) continue;  // every rank must own rows
     int stages = kMaxStages;
-    while (stages >= 2 && smem_for(mma_n, kbs, stages, s, rpo, M) > (size_t)kSmemMax) --stages;
+    while (stages >= 2 && smem_for(mma_n, kbs, stages, s, rpo, M, a.norm != 0) > (size_t)kSmemMax) --stages;
     if (stages < 2) continue;
     const size_t ring = (size_t)stages * kbs * (kStageA + (size_t)mma_n * kBK * 2);
     if ((size_t)M * kBM * 4 > ring) continue;  // fp32 staging reuses the ring
@@ -1098,7 +1316,7 @@ static kd_status choose(const GemmShape& a, GemmTile* t, double* best_ns) {
       t->stages = stages;
       t->rpo = rpo;
       t->mt = mma_n;
-      t->smem = (uint32_t)smem_for(mma_n, kbs, stages, s, rpo, M);
+      t->smem = (uint32_t)smem_for(mma_n, kbs, stages, s, rpo, M, a.norm != 0);
     }
   }
   if (best < 0) return fail(KD_ERR_UNSUPPORTED, "gemm: no feasible cluster tiling for this shape");
@@ -1117,7 +1335,7 @@ static double streamk_ns(const GemmShape& a) {
 
 // plain GEMMs: the cluster kernel unless stream-K is modelled faster (or forced)
 static bool use_dense(const GemmShape& a) {
-  if (a.rope) return true;  // the fused RoPE epilogue exists in the cluster kernel only
+  if (a.rope || a.norm) return true;  // the fused RoPE / RMSNorm epilogues exist in the cluster kernel only
   if (a.groups || a.silu) return false;
   const char* e = getenv("KD_GEMM_STREAMK");
   if (e && atoi(e)) return false;
@@ -1155,6 +1373,27 @@ GemmShape gemm_shape(const kd_attr_qkv_rope& a) {
   return s;
 }
 
+GemmShape gemm_shape(const kd_attr_gemm_rmsnorm& a) {
+  GemmShape s;
+  s.M = s.rows_total = a.M;
+  s.N = a.N;
+  s.K = a.K;
+  s.dtype = a.dtype;
+  s.norm = 1;
+  return s;
+}
+
+kd_status gemm_rmsnorm_bind(const kd_attr_gemm_rmsnorm& a, float* r, const void* gamma, GemmPlan* gp) {
+  if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "gemm_rmsnorm: bf16 only");
+  if (a.N % 8) return fail(KD_ERR_UNSUPPORTED, "gemm_rmsnorm: hidden must be a multiple of 8");
+  if (!r || !gamma) return fail(KD_ERR_INVALID_ARG, "gemm_rmsnorm: NULL r or gamma");
+  if (((uintptr_t)r | (uintptr_t)gamma) & 15) return fail(KD_ERR_INVALID_ARG, "gemm_rmsnorm: r and gamma must be 16-byte aligned");
+  gp->r = r;
+  gp->gamma = gamma;
+  gp->eps = a.eps;
+  return KD_OK;
+}
+
 kd_status qkv_rope_bind(const kd_attr_qkv_rope& a, const int32_t* bt, const int32_t* sl, void* q, void* kc, void* vc,
                         GemmPlan* gp) {
   if (!bt || !sl || !q || !kc || !vc) return fail(KD_ERR_INVALID_ARG, "qkv_rope: NULL pointer");
@@ -1189,6 +1428,10 @@ GemmShape gemm_shape(const kd_attr_grouped_gemm& a) {
 }
 
 kd_status gemm_scratch_bytes(const GemmShape& a, uint64_t* bytes) {
+  if (a.norm) {  // grid-barrier words + per-CTA partial Σr² [M][≤ kNormMaxGrid]
+    *bytes = kScratchCounterBytes + (uint64_t)a.M * kNormMaxGrid * 4;
+    return KD_OK;
+  }
   if (a.dtype == KD_F32) {  // fp32 path: SIMT kernel, no scratch
     if (a.groups) return fail(KD_ERR_UNSUPPORTED, "grouped gemm: bf16 only");
     *bytes = 256;
@@ -1255,6 +1498,15 @@ static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx&
   A.dbg = getenv("KD_GEMM_DBG") ? atoi(getenv("KD_GEMM_DBG")) : 0;
   A.rope = (int)gp.sh.rope;
   A.rp = gp.rp;
+  A.norm = (int)gp.sh.norm;
+  A.r = gp.r;
+  A.gamma = (const __nv_bfloat16*)gp.gamma;
+  A.eps = gp.eps;
+  A.bar = (unsigned*)c.scratch;
+  A.ssq = c.scratch ? (float*)((uint8_t*)c.scratch + kScratchCounterBytes) : nullptr;
+  if (A.norm && (!c.scratch || !A.r || !A.gamma))
+    return fail(KD_ERR_INVALID_ARG, "gemm_rmsnorm: scratch, r and gamma are required");
+  if (A.norm && t.tiles * t.split > kNormMaxGrid) return fail(KD_ERR_UNSUPPORTED, "gemm_rmsnorm: grid too large");
   A.epi = c.epi;
   A.trace = g_gemm_trace;
   kd_status ks = kernels_init();
@@ -1363,8 +1615,6 @@ kd_status gemm_signals(const GemmShape& a, uint32_t* s) {
     return KD_OK;
   }
   if (gemm::use_dense(a)) {
-    // one release per storing CTA: every tile once (split 1), else every
-    // cluster rank that owns at least one token row
     // one release per storing CTA: every tile once (split 1), else every
     // cluster rank that owns weight rows
     GemmTile t;

@@ -131,10 +131,15 @@ struct GemmShape {
   uint32_t M = 0, rows_total = 0, N = 0, K = 0, groups = 0, dtype = 0;
   uint32_t silu = 0;  // KD_OP_GEMM_SILU: output a [M, N/2] = silu·mul of the 64-row gate/up blocks
   uint32_t rope = 0;  // KD_OP_QKV_ROPE: cluster split-K kernel with the RoPE + KV-append epilogue
+  uint32_t norm = 0;  // KD_OP_GEMM_RMSNORM: cluster split-K kernel with the add + RMSNorm epilogue
 };
+constexpr int kNormMaxGrid = 160;  // CTAs of a KD_OP_GEMM_RMSNORM launch (partial-sum scratch bound)
 GemmShape gemm_shape(const kd_attr_gemm& a, bool silu = false);
 GemmShape gemm_shape(const kd_attr_qkv_rope& a);
+GemmShape gemm_shape(const kd_attr_gemm_rmsnorm& a);
 struct GemmPlan;
+// fill the a3 operands of a KD_OP_GEMM_RMSNORM plan (after gemm_prepare)
+kd_status gemm_rmsnorm_bind(const kd_attr_gemm_rmsnorm& a, float* r, const void* gamma, GemmPlan* gp);
 // fill gp->rp for a KD_OP_QKV_ROPE plan (after gemm_prepare)
 kd_status qkv_rope_bind(const kd_attr_qkv_rope& a, const int32_t* bt, const int32_t* sl, void* q, void* kc, void* vc,
                         GemmPlan* gp);
@@ -153,6 +158,9 @@ struct GemmPlan {
   const void* X = nullptr;    // fp32 path: plain operand pointers (SIMT kernel)
   const void* W = nullptr;
   RopeEpi rp;                 // KD_OP_QKV_ROPE
+  float* r = nullptr;         // KD_OP_GEMM_RMSNORM: residual, gamma, eps
+  const void* gamma = nullptr;
+  float eps = 0.f;
   GemmTile tile;
 };
 kd_status gemm_scratch_bytes(const GemmShape& sh, uint64_t* bytes);

@@ -33,6 +33,12 @@ kd_status op_scratch_bytes(uint32_t op, const std::vector<uint8_t>& attrs, u64* 
       if (s) return s;
       return gemm_scratch_bytes(gemm_shape(a), bytes);
     }
+    case KD_OP_GEMM_RMSNORM: {
+      kd_attr_gemm_rmsnorm a;
+      kd_status s = attrs_as(attrs, &a);
+      if (s) return s;
+      return gemm_scratch_bytes(gemm_shape(a), bytes);
+    }
     case KD_OP_ATTENTION: {
       kd_attr_attention a;
       kd_status s = attrs_as(attrs, &a);
@@ -56,6 +62,7 @@ kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes) {
     case KD_OP_GEMM: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_gemm*)attrs), bytes);
     case KD_OP_GEMM_SILU: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_gemm*)attrs, true), bytes);
     case KD_OP_QKV_ROPE: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_qkv_rope*)attrs), bytes);
+    case KD_OP_GEMM_RMSNORM: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_gemm_rmsnorm*)attrs), bytes);
     case KD_OP_GROUPED_GEMM: return gemm_scratch_bytes(gemm_shape(*(const kd_attr_grouped_gemm*)attrs), bytes);
     case KD_OP_ATTN_MERGE:
     case KD_OP_MOE_ROUTE:
@@ -123,6 +130,21 @@ kd_status kd_op_qkv_rope(const kd_attr_qkv_rope* a, const void* X, const void* W
   c.stream = (cudaStream_t)stream;
   c.scratch = scratch;
   return launch_gemm(gp, q_out, c, nullptr);
+}
+
+kd_status kd_op_gemm_rmsnorm(const kd_attr_gemm_rmsnorm* a, const void* X, const void* W, float* r,
+                             const void* gamma, void* h, void* scratch, void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_gemm_rmsnorm: NULL attrs");
+  if (a->dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "kd_op_gemm_rmsnorm: bf16 only");
+  GemmPlan gp;
+  kd_status s = gemm_prepare(gemm_shape(*a), X, W, nullptr, &gp);
+  if (s) return s;
+  s = gemm_rmsnorm_bind(*a, r, gamma, &gp);
+  if (s) return s;
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  c.scratch = scratch;
+  return launch_gemm(gp, h, c, nullptr);
 }
 
 kd_status kd_op_gemm_silu(const kd_attr_gemm* a, const void* X, const void* W, void* out, void* scratch,

@@ -89,6 +89,7 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_GEMM:
     case KD_OP_GEMM_SILU: need = sizeof(kd_attr_gemm); break;
     case KD_OP_QKV_ROPE: need = sizeof(kd_attr_qkv_rope); break;
+    case KD_OP_GEMM_RMSNORM: need = sizeof(kd_attr_gemm_rmsnorm); break;
     case KD_OP_ATTN_MERGE: need = sizeof(kd_attr_attn_merge); break;
     case KD_OP_ROPE_APPEND: need = sizeof(kd_attr_rope_append); break;
     case KD_OP_ATTENTION: need = sizeof(kd_attr_attention); break;
@@ -117,6 +118,7 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_GEMM:
     case KD_OP_GEMM_SILU: ok = nr == 2 && nw == 1; break;
     case KD_OP_QKV_ROPE: ok = nr == 4 && nw == 3; break;  // reads [X, W', bt, sl] writes [q, Kc, Vc]
+    case KD_OP_GEMM_RMSNORM: ok = nr == 4 && nw == 2; break;  // reads [X, W, r, gamma] writes [h, r]
     case KD_OP_ATTN_MERGE: {
       kd_attr_attn_merge a;
       std::memcpy(&a, k.attrs.data(), sizeof a);
@@ -176,7 +178,8 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
     }
     case KD_OP_GEMM:
     case KD_OP_GEMM_SILU:
-    case KD_OP_QKV_ROPE: st = launch_gemm(*l.gemm, l.wr[0], c, &sig); break;
+    case KD_OP_QKV_ROPE:
+    case KD_OP_GEMM_RMSNORM: st = launch_gemm(*l.gemm, l.wr[0], c, &sig); break;
     case KD_OP_ROPE_APPEND: {
       auto a = attrs_get<kd_attr_rope_append>(K);
       st = launch_rope_append(a, l.rd[0], (const int32_t*)l.rd[1], (const int32_t*)l.rd[2], l.wr[0], l.wr[1],
@@ -507,6 +510,14 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
         kd_status s3 = gemm_prepare(gemm_shape(a), l.rd[0], l.rd[1], nullptr, l.gemm);
         if (s3) return s3;
         s3 = qkv_rope_bind(a, (const int32_t*)l.rd[2], (const int32_t*)l.rd[3], l.wr[0], l.wr[1], l.wr[2], l.gemm);
+        if (s3) return s3;
+      }
+      if (K.op == KD_OP_GEMM_RMSNORM) {
+        const auto a = attrs_get<kd_attr_gemm_rmsnorm>(K);
+        l.gemm = new GemmPlan();
+        kd_status s3 = gemm_prepare(gemm_shape(a), l.rd[0], l.rd[1], nullptr, l.gemm);
+        if (s3) return s3;
+        s3 = gemm_rmsnorm_bind(a, (float*)l.wr[1], l.rd[3], l.gemm);
         if (s3) return s3;
       }
       if (K.op == KD_OP_GEMM || K.op == KD_OP_GEMM_SILU) {

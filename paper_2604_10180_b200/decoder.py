@@ -75,7 +75,8 @@ class KernelInfo:
 class DecoderGraph:
     """Declares the decoder kernel graph for one micro-batch of cfg.m rows."""
 
-    def __init__(self, cfg, act: int = K.KD_BF16, fuse_silu: bool = False, fuse_rope: bool = False):
+    def __init__(self, cfg, act: int = K.KD_BF16, fuse_silu: bool = False, fuse_rope: bool = False,
+                 fuse_norm: bool = False):
         """act: KD_BF16 (throughput path) or KD_F32 (the 1e-5 parity path,
         R13: fp32 weights, activations and KV cache; dense attention layers).
         fuse_silu: declare gate_up and SiLU·mul as ONE kernel (KD_OP_GEMM_SILU,
@@ -84,7 +85,11 @@ class DecoderGraph:
         fuse_rope: declare the QKV GEMM and RoPE + KV append as ONE kernel
         (KD_OP_QKV_ROPE; its W_qkv rows are pair-interleaved per head, see
         pair_interleave_qkv); it writes the KV cache, so it joins the
-        attention template (co-located with the cache, R6)."""
+        attention template (co-located with the cache, R6).
+        fuse_norm: declare each O GEMM with the following residual add +
+        RMSNorm (norm2), and each dense down GEMM with the next layer's norm1,
+        as ONE kernel (KD_OP_GEMM_RMSNORM) — for co-located placements; the o
+        and d activations then never exist (except the last layer's d)."""
         if act not in (K.KD_BF16, K.KD_F32):
             raise ValueError("act must be KD_BF16 or KD_F32")
         if act == K.KD_F32 and (cfg.n_experts or cfg.attn_every):
@@ -94,6 +99,8 @@ class DecoderGraph:
         self.fuse_silu = fuse_silu
         fuse_rope = bool(fuse_rope) and act == K.KD_BF16
         self.fuse_rope = fuse_rope
+        fuse_norm = bool(fuse_norm) and act == K.KD_BF16
+        self.fuse_norm = fuse_norm
         adt = "bf16" if act == K.KD_BF16 else "f32"  # storage of weights, activations and KV cache
         self.cfg = cfg
         m, H, L = cfg.m, cfg.hidden, cfg.n_layers
@@ -121,6 +128,9 @@ class DecoderGraph:
             return (b, 0, n)
 
         E, k = cfg.n_experts, cfg.top_k
+
+        def fused_down(l):  # dense attention layer whose down GEMM also runs layer l+1's norm1
+            return fuse_norm and not E and l < L - 1 and cfg.is_attn_layer(l) and cfg.is_attn_layer(l + 1)
         if E:
             mb = C.c_uint64()
             K.check(K.kd_moe_meta_bytes(m, E, k, C.byref(mb)), "kd_moe_meta_bytes")
@@ -167,7 +177,8 @@ class DecoderGraph:
             buf(f"kc.{l}", (m * pps, Hkv, cfg.page, D), adt, PERS | PM)
             buf(f"vc.{l}", (m * pps, Hkv, cfg.page, D), adt, PERS | PM)
             acts = [("h1", (m, H))] + ([] if fuse_rope else [("qkv", (m, cfg.qkv_dim))]) + [
-                ("q", (m, Hq * D)), ("attn", (m, Hq * D)), ("o", (m, H)), ("h2", (m, H)), ("d", (m, H))]
+                ("q", (m, Hq * D)), ("attn", (m, Hq * D))] + ([] if fuse_norm else [("o", (m, H))]) + [
+                ("h2", (m, H))] + ([] if fused_down(l) else [("d", (m, H))])
             if not E:
                 acts += ([] if fuse_silu else [("gu", (m, 2 * F))]) + [("a", (m, F))]
             for nm, shp in acts:
@@ -182,6 +193,7 @@ class DecoderGraph:
             return kid
 
         eps = float(cfg.eps)
+
         for l in range(L):
             has_d = 1 if l > 0 else 0
             if not cfg.is_attn_layer(l):
@@ -202,9 +214,10 @@ class DecoderGraph:
                 add("out_proj", l, T_OUTPROJ, K.KD_OP_GEMM, [f"yn.{l}", f"w_out.{l}"], [f"d.{l}"],
                     K.kd_attr_gemm(m, H, di, act), 2 * m * H * di)
                 continue
-            add("norm1", l, T_RESID, K.KD_OP_ADD_RMSNORM,
-                ["r"] + ([f"d.{l-1}"] if has_d else []) + [f"g1.{l}"], [f"h1.{l}", "r"],
-                K.kd_attr_add_rmsnorm(m, H, has_d, act, eps, 0))
+            if not (has_d and fused_down(l - 1)):
+                add("norm1", l, T_RESID, K.KD_OP_ADD_RMSNORM,
+                    ["r"] + ([f"d.{l-1}"] if has_d else []) + [f"g1.{l}"], [f"h1.{l}", "r"],
+                    K.kd_attr_add_rmsnorm(m, H, has_d, act, eps, 0))
             if fuse_rope:
                 add("qkv_rope", l, T_ATTN, K.KD_OP_QKV_ROPE, [f"h1.{l}", f"w_qkv.{l}", "bt", "sl"],
                     [f"q.{l}", f"kc.{l}", f"vc.{l}"],
@@ -217,10 +230,14 @@ class DecoderGraph:
                     K.kd_attr_rope_append(m, Hq, Hkv, D, cfg.page, pps, act, 0, float(cfg.rope_theta)))
             add("attn", l, T_ATTN, K.KD_OP_ATTENTION, [f"q.{l}", f"kc.{l}", f"vc.{l}", "bt", "sl"], [f"attn.{l}"],
                 K.kd_attr_attention(m, Hq, Hkv, D, cfg.page, pps, act, 0), 4 * m * Hq * cfg.context * D)
-            add("o", l, T_O, K.KD_OP_GEMM, [f"attn.{l}", f"w_o.{l}"], [f"o.{l}"],
-                K.kd_attr_gemm(m, H, Hq * D, act), 2 * m * H * Hq * D)
-            add("norm2", l, T_RESID, K.KD_OP_ADD_RMSNORM, ["r", f"o.{l}", f"g2.{l}"], [f"h2.{l}", "r"],
-                K.kd_attr_add_rmsnorm(m, H, 1, act, eps, 0))
+            if fuse_norm:
+                add("o_norm", l, T_O, K.KD_OP_GEMM_RMSNORM, [f"attn.{l}", f"w_o.{l}", "r", f"g2.{l}"], [f"h2.{l}", "r"],
+                    K.kd_attr_gemm_rmsnorm(m, H, Hq * D, act, eps, 0), 2 * m * H * Hq * D)
+            else:
+                add("o", l, T_O, K.KD_OP_GEMM, [f"attn.{l}", f"w_o.{l}"], [f"o.{l}"],
+                    K.kd_attr_gemm(m, H, Hq * D, act), 2 * m * H * Hq * D)
+                add("norm2", l, T_RESID, K.KD_OP_ADD_RMSNORM, ["r", f"o.{l}", f"g2.{l}"], [f"h2.{l}", "r"],
+                    K.kd_attr_add_rmsnorm(m, H, 1, act, eps, 0))
             if E:
                 xgm = self.buf[f"xgm.{l}"]
                 meta_span = (xgm, 0, self.meta_bytes)
@@ -245,8 +262,12 @@ class DecoderGraph:
                     add("gu", l, T_GU, K.KD_OP_GEMM, [f"h2.{l}", f"w_gu.{l}"], [f"gu.{l}"],
                         K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
                     add("silu", l, T_SILU, K.KD_OP_SILU_MUL, [f"gu.{l}"], [f"a.{l}"], K.kd_attr_silu_mul(m, F, act, 0))
-                add("down", l, T_DOWN, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
-                    K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)
+                if fused_down(l):
+                    add("down_norm", l, T_DOWN, K.KD_OP_GEMM_RMSNORM, [f"a.{l}", f"w_d.{l}", "r", f"g1.{l+1}"],
+                        [f"h1.{l+1}", "r"], K.kd_attr_gemm_rmsnorm(m, H, F, act, eps, 0), 2 * m * H * F)
+                else:
+                    add("down", l, T_DOWN, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
+                        K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)
         add("final_add", L - 1, T_RESID, K.KD_OP_RESIDUAL_ADD, ["r", f"d.{L-1}"], ["r"],
             K.kd_attr_residual_add(m, H, 1, act))
         g.finalize()

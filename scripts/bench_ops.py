@@ -57,6 +57,20 @@ def gemm(M, N, Kd, copies):
     return us, b
 
 
+def gemm_norm(M, N, Kd, copies):
+    """O/down GEMM with the fused residual add + RMSNorm epilogue (KD_OP_GEMM_RMSNORM)."""
+    a = K.kd_attr_gemm_rmsnorm(M, N, Kd, K.KD_BF16, 1e-5, 0)
+    X = torch.randn(M, Kd, device="cuda").to(torch.bfloat16)
+    Ws = [torch.randn(N, Kd, device="cuda").to(torch.bfloat16) * (1 / math.sqrt(Kd)) for _ in range(copies)]
+    r = torch.randn(M, N, device="cuda")
+    gam = torch.ones(N, device="cuda").to(torch.bfloat16)
+    h = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    scr = torch.zeros(api.op_scratch_bytes(K.KD_OP_GEMM_RMSNORM, a), dtype=torch.uint8, device="cuda")
+    us = timeit(lambda i: api.gemm_rmsnorm(a, X, Ws[i % copies], r, gam, h, scr))
+    b = N * Kd * 2 + M * Kd * 2 + M * N * (4 + 4 + 2) + N * 2
+    return us, b
+
+
 def attention(rows, Hq, Hkv, D, C):
     pps = (C + 15) // 16
     a = K.kd_attr_attention(rows, Hq, Hkv, D, 16, pps, K.KD_BF16, 0)
@@ -107,6 +121,8 @@ def main():
     m = args.m
     cases = [("gemm_qkv", lambda: gemm(m, 6144, 4096, 4)), ("gemm_o", lambda: gemm(m, 4096, 4096, 5)),
              ("gemm_gu", lambda: gemm(m, 28672, 4096, 2)), ("gemm_down", lambda: gemm(m, 4096, 14336, 2)),
+             ("gemm_o_norm", lambda: gemm_norm(m, 4096, 4096, 5)),
+             ("gemm_down_norm", lambda: gemm_norm(m, 4096, 14336, 2)),
              ("attention", lambda: attention(m, 32, 8, 128, 4096)),
              ("gemm_overhead_1kb", lambda: gemm(m, 128 * 148, 64, 2))]
     if not args.only or args.only == "small":

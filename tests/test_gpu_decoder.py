@@ -204,14 +204,28 @@ def test_mode_switch_no_transfer_then_disagg(mod):
     dis.rt.check()  # KD_ERR_TIMEOUT if a wait missed its target
 
 
-def test_fused_graph_vs_oracle_and_disaggregated(mod):
-    """The monolithic-placement graph with gate_up+SiLU (KD_OP_GEMM_SILU) and
-    QKV+RoPE+append (KD_OP_QKV_ROPE) fused
-    is within tolerance of the oracle and runs disaggregated bitwise equal to
-    its own monolithic run."""
+@pytest.mark.parametrize("fuse_norm", [False, True])
+def test_fused_graph_vs_oracle_and_disaggregated(mod, fuse_norm):
+    """The monolithic-placement graph with gate_up+SiLU (KD_OP_GEMM_SILU),
+    QKV+RoPE+append (KD_OP_QKV_ROPE) and (fuse_norm) O/down + residual add +
+    RMSNorm (KD_OP_GEMM_RMSNORM) fused is within tolerance of the oracle; the
+    first two run disaggregated bitwise equal to their own monolithic run (the
+    norm fusion co-locates the residual stream with the GEMMs: monolithic only)."""
     DEC, K = mod
     cfg = TINY
     inp = synth.make_decoder_inputs(cfg)
+    if fuse_norm:
+        dg = DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True, fuse_norm=True)
+        names = [k.name for k in dg.kernels]
+        assert "o_norm" in names and "down_norm" in names and "norm2" not in names
+        assert names.count("norm1") == 1  # layer 0 only
+        rt = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp)
+        rt.step()
+        rt.sync()
+        rt.rt.check()
+        r_ref, _, _ = OL.decoder_step(inp, act="bf16")
+        assert relerr(rt.residual(), r_ref) < 5e-3
+        return
 
     def runf(assign, n_dev):
         dg = DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True)

@@ -317,6 +317,56 @@ def test_gemm_silu_fused_equals_pair(kd, M, F, K_, monkeypatch):
     assert relerr(host_f64(out)[rows], ref) < 5e-3
 
 
+# ------------------------------------------------------------------ a7/a10 + a3 fused (KD_OP_GEMM_RMSNORM)
+@pytest.mark.parametrize("M,N,K_,split", [(64, 4096, 4096, None), (64, 4096, 14336, None), (5, 264, 520, "1"),
+                                          (33, 384, 320, "2"), (3, 1024, 2048, "4"), (120, 520, 264, "3"),
+                                          (64, 4096, 4096, "2")])
+def test_gemm_rmsnorm_fused(kd, M, N, K_, split, monkeypatch):
+    """O/down GEMM with the residual add + RMSNorm epilogue (per-token Σr²
+    completed across the grid after an in-kernel barrier): r bit-identical to
+    the GEMM → add_rmsnorm pair at the same cluster split, h within one bf16
+    ulp of the pair's (only the Σr² order differs), both within tolerance of
+    the oracle, and bitwise reproducible run to run."""
+    api, K = kd
+    torch = _torch()
+    if split:
+        monkeypatch.setenv("KD_GEMM_TILE", split)
+    g = synth.rng(M * 7 + N + K_)
+    X = synth.normal_bf16(g, (M, K_))
+    W = synth.normal_bf16(g, (N, K_), 1 / math.sqrt(K_))
+    r0 = synth.normal_f32(g, (M, N))
+    gam = synth.f32_to_bf16_bits(1 + 0.1 * g.standard_normal(N, dtype=np.float32))
+    Xd, Wd, gd = dev_bf16(X), dev_bf16(W), dev_bf16(gam)
+    af = K.kd_attr_gemm_rmsnorm(M, N, K_, K.KD_BF16, 1e-5, 0)
+    scr = scratch_for(api, K.KD_OP_GEMM_RMSNORM, af)
+    outs = []
+    for _ in range(2):
+        r = torch.from_numpy(r0).cuda()
+        h = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        api.gemm_rmsnorm(af, Xd, Wd, r, gd, h, scr)
+        outs.append((r, h))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1]), "not reproducible"
+    r, h = outs[0]
+    assert not scr[:8].any(), "grid-barrier words must self-reset"
+    # the pair
+    ag = K.kd_attr_gemm(M, N, K_, K.KD_BF16)
+    y = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    api.gemm(ag, Xd, Wd, y, scratch_for(api, K.KD_OP_GEMM, ag))
+    rp = torch.from_numpy(r0).cuda()
+    hp = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    api.add_rmsnorm(K.kd_attr_add_rmsnorm(M, N, 1, K.KD_BF16, 1e-5, 0), rp, y, gd, hp)
+    torch.cuda.synchronize()
+    hh, hph = host_f64(h), host_f64(hp)
+    if split:
+        assert torch.equal(r, rp), "fused residual differs from the GEMM → add pair"
+        assert np.all(np.abs(hh - hph) <= 1.01 * (np.abs(hph) * 2.0 ** -7) + 1e-30)
+    r_ref, h_ref = OL.add_rmsnorm(r0, OL.linear(OL.bf16_to_f64(X), OL.bf16_to_f64(W), "bf16"), OL.bf16_to_f64(gam),
+                                  1e-5, "bf16")
+    assert relerr(host_f64(r), r_ref) < 1e-3
+    assert relerr(hh, h_ref) < 5e-3
+
+
 # ------------------------------------------------------------------ a4+a5 fused (KD_OP_QKV_ROPE)
 @pytest.mark.parametrize("rows,H,Hq,Hkv,D,C,split", [(4, 256, 4, 4, 64, 128, "2"), (64, 4096, 32, 8, 128, 4096, "2"),
                                                        (3, 512, 8, 2, 128, 37, "4"), (5, 256, 4, 2, 64, 50, "1")])
