@@ -609,16 +609,38 @@ struct Args {
 // adjacent rows and never straddles a cluster owner (rpo is even). Values are
 // rounded to bf16 first (the plain GEMM's output), then exactly the RoPE
 // kernel's fp32 math with its cos/sin (fp64 angle, host fp64 θ^(−2i/D)).
-__device__ __forceinline__ void rope_pair(const Args& A, int j, int n, float xs, float ys) {
+// Per-token position and page, and the frequency table, are staged in shared
+// memory by the idle warps 2-3 during the main loop (RopeSmem): indexed
+// parameter-space reads (divergent across lanes) and dependent global loads
+// in this epilogue were its dominant cost.
+struct RopeSmem {
+  int* pos;      // [M] seq_len − 1
+  int* pg;       // [M] page holding pos (block_table entry)
+  double* f;     // [D/2]
+};
+
+__device__ __forceinline__ void rope_stage(const Args& A, const RopeSmem& rs) {
+  const RopeEpi& R = A.rp;
+  const int t = threadIdx.x - 64;
+  for (int i = t; i < R.D / 2; i += 64) rs.f[i] = R.f[i];
+  pdl_wait();  // block table and lengths are step inputs written before this kernel
+  for (int j = t; j < A.M; j += 64) {
+    const int pos = R.sl[j] - 1;
+    rs.pos[j] = pos;
+    rs.pg[j] = R.bt[(size_t)j * R.pps + pos / R.page];
+  }
+}
+
+__device__ __forceinline__ void rope_pair(const Args& A, const RopeSmem& rs, int j, int n, float xs, float ys) {
   const RopeEpi& R = A.rp;
   const int D = R.D, half = D / 2, G = R.Hq / R.Hkv;
   const int hall = n / D, rr = n - hall * D, p = rr >> 1;
   const int grp = hall / (G + 2), slot = hall - grp * (G + 2);
   const float x = __bfloat162float(__float2bfloat16_rn(xs)), y = __bfloat162float(__float2bfloat16_rn(ys));
-  const int pos = R.sl[j] - 1;
+  const int pos = rs.pos[j];
   __nv_bfloat16 lo, hi;
   if (slot <= G) {
-    const double ang = (double)pos * R.f[p];
+    const double ang = (double)pos * rs.f[p];
     const double k = rint(ang * 0.15915494309189535);
     const double red = fma(-k, 6.283185307179586, fma(-k, 2.4492935982947064e-16, ang));
     float sn, cs;
@@ -638,7 +660,7 @@ __device__ __forceinline__ void rope_pair(const Args& A, int j, int n, float xs,
       ((__nv_bfloat16*)A.epi.dst[e])[qo + p + half] = hi;
     }
   } else {
-    const int32_t pg = R.bt[(size_t)j * R.pps + pos / R.page];
+    const int32_t pg = rs.pg[j];
     const size_t co = (((size_t)pg * R.Hkv + grp) * R.page + pos % R.page) * D;
     __nv_bfloat16* cache = slot == G ? R.kc : R.vc;
     cache[co + p] = lo;
@@ -648,10 +670,11 @@ __device__ __forceinline__ void rope_pair(const Args& A, int j, int n, float xs,
 
 // 4 consecutive outputs (weight rows col..col+3) of token j → Y (+ peers), or
 // the fused RoPE/append epilogue
-__device__ __forceinline__ void csk_store4(const Args& A, int j, int col, float v0, float v1, float v2, float v3) {
+__device__ __forceinline__ void csk_store4(const Args& A, const RopeSmem& rs, int j, int col, float v0, float v1,
+                                           float v2, float v3) {
   if (A.rope) {
-    if (col < A.N) rope_pair(A, j, col, v0, v1);
-    if (col + 2 < A.N) rope_pair(A, j, col + 2, v2, v3);
+    if (col < A.N) rope_pair(A, rs, j, col, v0, v1);
+    if (col + 2 < A.N) rope_pair(A, rs, j, col + 2, v2, v3);
     return;
   }
   const size_t yo = (size_t)j * A.N + col;
@@ -890,6 +913,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   ns.Tp = (split > 1 ? A.rpo : kBM) + 4;              // 16-byte rows + pad (conflict-free column walks)
   ns.rs = ns.invs + 256;                              // [M][Tp]
   ns.gs = (__nv_bfloat16*)(ns.rs + (size_t)M * ns.Tp);  // [128]
+  RopeSmem ropes;                                     // rope: after the barriers (exclusive with norm)
+  ropes.pos = (int*)(ns.invs + 256);                  // [256]
+  ropes.pg = ropes.pos + 256;                         // [256]
+  ropes.f = (double*)(ropes.pg + 256);                // [128]
   float* send = (float*)smem;  // split == 1: [M][128] fp32 staging, reuses the idle ring after the last MMA
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -998,6 +1025,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (A.norm && warp < 4) {
     // ------------------------------------------------ idle warps 2-3: stage r and gamma (norm)
     norm_stage(A, ns, rank, n0, my_rows);
+  } else if (A.rope && warp < 4) {
+    // ------------------------------------------------ idle warps 2-3: stage positions, pages, θ table
+    rope_stage(A, ropes);
+    if (split == 1) asm volatile("bar.arrive 2, %0;" ::"r"(kEpi + 64) : "memory");  // hand-off to the epilogue warps
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
     // 8 warps: warp w reads TMEM lane quarter (w − 4) mod 4 (its hardware
@@ -1015,8 +1046,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     auto store_y = [&](int j, int col, float v0, float v1, float v2, float v3) {  // 4 consecutive outputs of token j
       if (A.rope) {  // two rotation pairs (col is a multiple of 4)
-        if (col < A.N) rope_pair(A, j, col, v0, v1);
-        if (col + 2 < A.N) rope_pair(A, j, col + 2, v2, v3);
+        if (col < A.N) rope_pair(A, ropes, j, col, v0, v1);
+        if (col + 2 < A.N) rope_pair(A, ropes, j, col + 2, v2, v3);
         return;
       }
       const size_t yo = (size_t)j * A.N + col;
@@ -1046,6 +1077,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (!A.norm) {  // (norm: the staged tile is finished after the role branches)
         named_bar(1, kEpi);
+        if (A.rope) named_bar(2, kEpi + 64);  // warps 2-3 staged the RoPE tables
         pdl_wait();
         for (int e = ep; e < M * (kBM / 4); e += kEpi) {
           const int j = e / (kBM / 4), r4 = (e % (kBM / 4)) * 4;
@@ -1119,7 +1151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int cr = 1; cr < split; ++cr)  // rank order → deterministic
 #pragma unroll
         for (int x = 0; x < 4; ++x) acc[x] += recv[((size_t)cr * rpo + lr4 + x) * P + j];
-      csk_store4(A, j, n0 + rank * rpo + lr4, acc[0], acc[1], acc[2], acc[3]);
+      csk_store4(A, ropes, j, n0 + rank * rpo + lr4, acc[0], acc[1], acc[2], acc[3]);
     }
     if (threadIdx.x == 128) { KD_TRACE(11); KD_CTRACE(25); }
     if (A.epi.n && my_rows > 0) {  // publish this CTA's stores to the consumer devices
@@ -1227,12 +1259,13 @@ static size_t smem_bytes(const Geometry& g) {
 // ---------------------------------------------------------------- dense GEMM kernel choice
 namespace csk {
 
-static size_t smem_for(int mma_n, int kbs, int stages, int split, int rpo, int M, bool norm) {
+static size_t smem_for(int mma_n, int kbs, int stages, int split, int rpo, int M, bool norm, bool rope) {
   const size_t recv = split > 1 ? (size_t)split * ((M + 3) / 4 * 4 + 4) * rpo * 4 : 0;
   if (norm) {  // + the r slice [M][Tp] fp32 and the gamma slice
     const size_t tp = (split > 1 ? rpo : kBM) + 4;
-    return smem_for(mma_n, kbs, stages, split, rpo, M, false) + (size_t)M * tp * 4 + 256;
+    return smem_for(mma_n, kbs, stages, split, rpo, M, false, false) + (size_t)M * tp * 4 + 256;
   }
+  if (rope) return smem_for(mma_n, kbs, stages, split, rpo, M, false, false) + 256 * 4 * 2 + 128 * 8;
   return 1024 + (size_t)stages * kbs * (kStageA + (size_t)mma_n * kBK * 2) + recv + (2 * kMaxStages + 4) * 8 + 16 +
          256 * 4;  // + the norm epilogue's per-token 1/rms
 }
@@ -1300,7 +1333,7 @@ static kd_status choose(const GemmShape& a, GemmTile* t, double* best_ns) {
     const int rpo = s > 1 ? ((kBM + s - 1) / s + 3) / 4 * 4 : 0;
     if (s > 1 && (rpo * (s - 1) >= kBM)) continue;  // every rank must own rows
     int stages = kMaxStages;
-    while (stages >= 2 && smem_for(mma_n, kbs, stages, s, rpo, M, a.norm != 0) > (size_t)kSmemMax) --stages;
+    while (stages >= 2 && smem_for(mma_n, kbs, stages, s, rpo, M, a.norm != 0, a.rope != 0) > (size_t)kSmemMax) --stages;
     if (stages < 2) continue;
     const size_t ring = (size_t)stages * kbs * (kStageA + (size_t)mma_n * kBK * 2);
     if ((size_t)M * kBM * 4 > ring) continue;  // fp32 staging reuses the ring
@@ -1316,7 +1349,7 @@ static kd_status choose(const GemmShape& a, GemmTile* t, double* best_ns) {
       t->stages = stages;
       t->rpo = rpo;
       t->mt = mma_n;
-      t->smem = (uint32_t)smem_for(mma_n, kbs, stages, s, rpo, M, a.norm != 0);
+      t->smem = (uint32_t)smem_for(mma_n, kbs, stages, s, rpo, M, a.norm != 0, a.rope != 0);
     }
   }
   if (best < 0) return fail(KD_ERR_UNSUPPORTED, "gemm: no feasible cluster tiling for this shape");

@@ -71,6 +71,24 @@ def gemm_norm(M, N, Kd, copies):
     return us, b
 
 
+def qkv_rope(M, H, Hq, Hkv, D, C, copies):
+    """QKV GEMM with the fused RoPE + KV-append epilogue (KD_OP_QKV_ROPE)."""
+    pps = (C + 15) // 16
+    N = (Hq + 2 * Hkv) * D
+    a = K.kd_attr_qkv_rope(M, H, Hq, Hkv, D, 16, pps, K.KD_BF16, 5e5)
+    X = torch.randn(M, H, device="cuda").to(torch.bfloat16)
+    Ws = [torch.randn(N, H, device="cuda").to(torch.bfloat16) * (1 / math.sqrt(H)) for _ in range(copies)]
+    bt = torch.arange(M * pps, device="cuda", dtype=torch.int32).view(M, pps)
+    sl = torch.full((M,), C, device="cuda", dtype=torch.int32)
+    q = torch.empty(M, Hq * D, device="cuda", dtype=torch.bfloat16)
+    kc = torch.zeros(M * pps, Hkv, 16, D, device="cuda", dtype=torch.bfloat16)
+    vc = torch.zeros_like(kc)
+    scr = torch.zeros(api.op_scratch_bytes(K.KD_OP_QKV_ROPE, a), dtype=torch.uint8, device="cuda")
+    us = timeit(lambda i: api.qkv_rope(a, X, Ws[i % copies], bt, sl, q, kc, vc, scr))
+    b = N * H * 2 + M * H * 2 + M * N * 2
+    return us, b
+
+
 def attention(rows, Hq, Hkv, D, C):
     pps = (C + 15) // 16
     a = K.kd_attr_attention(rows, Hq, Hkv, D, 16, pps, K.KD_BF16, 0)
@@ -122,6 +140,7 @@ def main():
     cases = [("gemm_qkv", lambda: gemm(m, 6144, 4096, 4)), ("gemm_o", lambda: gemm(m, 4096, 4096, 5)),
              ("gemm_gu", lambda: gemm(m, 28672, 4096, 2)), ("gemm_down", lambda: gemm(m, 4096, 14336, 2)),
              ("gemm_o_norm", lambda: gemm_norm(m, 4096, 4096, 5)),
+             ("gemm_qkv_rope", lambda: qkv_rope(m, 4096, 32, 8, 128, 4096, 4)),
              ("gemm_down_norm", lambda: gemm_norm(m, 4096, 14336, 2)),
              ("attention", lambda: attention(m, 32, 8, 128, 4096)),
              ("gemm_overhead_1kb", lambda: gemm(m, 128 * 148, 64, 2))]

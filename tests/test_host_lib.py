@@ -53,6 +53,25 @@ def test_error_paths(kd):
     assert e.value.status == K.KD_ERR_STATE
 
 
+def test_fused_norm_op_host_checks(kd):
+    """KD_OP_GEMM_RMSNORM host side: scratch sizing (barrier words + per-CTA
+    partial sums), dtype validation before any device work, the graph accepts
+    the op id and its 4-read / 2-write declaration."""
+    _, K, api = kd
+    a = K.kd_attr_gemm_rmsnorm(64, 4096, 4096, K.KD_BF16, 1e-5, 0)
+    assert api.op_scratch_bytes(K.KD_OP_GEMM_RMSNORM, a) == 64 * 1024 + 64 * 160 * 4
+    bad = K.kd_attr_gemm_rmsnorm(64, 4096, 4096, K.KD_F32, 1e-5, 0)
+    import ctypes as C
+    assert K.kd_op_gemm_rmsnorm(C.byref(bad), None, None, None, None, None, None, None) == K.KD_ERR_UNSUPPORTED
+    g = api.Graph()
+    X, W, r, gam, h = (g.add_buffer(n, f) for n, f in ((64, 0), (64, K.KD_BUF_WEIGHT), (64, 0),
+                                                       (16, K.KD_BUF_WEIGHT), (32, 0)))
+    g.add_kernel(K.KD_OP_GEMM_RMSNORM, [(X, 0, 64), (W, 0, 64), (r, 0, 64), (gam, 0, 16)], [(h, 0, 32), (r, 0, 64)], a)
+    with pytest.raises(K.KdError):
+        g.add_kernel(K.KD_OP_GEMM_RMSNORM + 1, [], [(h, 0, 8)])
+    g.finalize()
+
+
 def rand_trace(rng, K_, nbuf=4, maxlen=48):
     ks = []
     for _ in range(K_):
