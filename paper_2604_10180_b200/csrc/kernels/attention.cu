@@ -685,6 +685,7 @@ static Shape choose(const kd_attr_attention& a) {
   const long units = (long)a.rows * a.n_kv_heads;
   const long target = 4L * 3 * kNumSMs;
   int splits = (int)std::max<long>(1, (target + units - 1) / units);
+  if (const char* e = getenv("KD_ATTN_SPLITS")) splits = std::max(1, atoi(e));  // A/B knob
   splits = std::min(splits, std::max(1, pages / 16));
   int pps = (pages + splits - 1) / splits;
   if (pps > kMaxPagesPerSplit) pps = kMaxPagesPerSplit;
