@@ -207,16 +207,14 @@ def main():
     if world == 1:
         # 1 GPU: the monolithic reference point of the metric (all kernels on one B200);
         # gate_up and SiLU·mul share the device, so they are declared as one fused kernel
-        # (KD_OP_GEMM_SILU, bit-identical to the pair; KD_BENCH_NO_FUSE=1 for the A/B).
-        # QKV + RoPE/append (KD_OP_QKV_ROPE) is built and bit-identical too, but measured
-        # slower than the pair (27.5 vs 19.3 µs at the 8B shape: the cluster GEMM's
-        # epilogue is the expensive place for per-element trig), so it is opt-in
-        # (KD_BENCH_FUSE_ROPE=1). The O GEMM with norm2 and the down GEMM with the next
-        # layer's norm1 run as one kernel each (KD_OP_GEMM_RMSNORM: the per-token Σr² is
-        # finished across the grid after an in-kernel barrier), measured 9.13 vs 9.17 ms
-        # per step (KD_BENCH_NO_FUSE_NORM=1 for the A/B).
+        # (KD_OP_GEMM_SILU, bit-identical to the pair); so are QKV + RoPE/append
+        # (KD_OP_QKV_ROPE, bit-identical to the pair: 17.0 vs 15.0 + 3.7 µs, step 9.04 vs
+        # 9.13 ms) and the O GEMM with norm2 / the down GEMM with the next layer's norm1
+        # (KD_OP_GEMM_RMSNORM: the per-token Σr² is finished across the grid after an
+        # in-kernel barrier; step 9.13 vs 9.17 ms). A/B: KD_BENCH_NO_FUSE (all),
+        # KD_BENCH_NO_FUSE_ROPE, KD_BENCH_NO_FUSE_NORM.
         fuse = not os.environ.get("KD_BENCH_NO_FUSE")
-        dg = DEC.DecoderGraph(cfg, fuse_silu=fuse, fuse_rope=fuse and bool(os.environ.get("KD_BENCH_FUSE_ROPE")),
+        dg = DEC.DecoderGraph(cfg, fuse_silu=fuse, fuse_rope=fuse and not os.environ.get("KD_BENCH_NO_FUSE_ROPE"),
                               fuse_norm=fuse and not os.environ.get("KD_BENCH_NO_FUSE_NORM"))
         assign = [0] * dg.g.num_kernels
         rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed, use_graph=not args.no_graph)

@@ -668,6 +668,51 @@ __device__ __forceinline__ void rope_pair(const Args& A, const RopeSmem& rs, int
   }
 }
 
+// Two adjacent rotation pairs (weight rows n..n+3 → dims p, p+1 and p + D/2,
+// p + D/2 + 1 of one head; n % 4 == 0) with 4-byte stores: the cluster
+// path's second pass, where lanes walk a token's rows so that the q / cache
+// stores coalesce. Per element exactly rope_pair's arithmetic (same bits).
+__device__ __forceinline__ void rope_quad(const Args& A, const RopeSmem& rs, int j, int n, float4 a) {
+  const RopeEpi& R = A.rp;
+  const int D = R.D, half = D / 2, G = R.Hq / R.Hkv;
+  const int hall = n / D, rr = n - hall * D, p = rr >> 1;
+  const int grp = hall / (G + 2), slot = hall - grp * (G + 2);
+  const float xs[2] = {__bfloat162float(__float2bfloat16_rn(a.x)), __bfloat162float(__float2bfloat16_rn(a.z))};
+  const float ys[2] = {__bfloat162float(__float2bfloat16_rn(a.y)), __bfloat162float(__float2bfloat16_rn(a.w))};
+  const int pos = rs.pos[j];
+  __nv_bfloat16 lo[2], hi[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (slot <= G) {
+      const double ang = (double)pos * rs.f[p + u];
+      const double k = rint(ang * 0.15915494309189535);
+      const double red = fma(-k, 6.283185307179586, fma(-k, 2.4492935982947064e-16, ang));
+      float sn, cs;
+      sincosf((float)red, &sn, &cs);
+      lo[u] = __float2bfloat16_rn(xs[u] * cs - ys[u] * sn);
+      hi[u] = __float2bfloat16_rn(ys[u] * cs + xs[u] * sn);
+    } else {
+      lo[u] = __float2bfloat16_rn(xs[u]);
+      hi[u] = __float2bfloat16_rn(ys[u]);
+    }
+  }
+  const __nv_bfloat162 l2 = __halves2bfloat162(lo[0], lo[1]), h2 = __halves2bfloat162(hi[0], hi[1]);
+  if (slot < G) {
+    const size_t qo = ((size_t)j * R.Hq + (size_t)grp * G + slot) * D;
+    *reinterpret_cast<__nv_bfloat162*>(R.q + qo + p) = l2;
+    *reinterpret_cast<__nv_bfloat162*>(R.q + qo + p + half) = h2;
+    for (int e = 0; e < A.epi.n; ++e) {
+      *reinterpret_cast<__nv_bfloat162*>((__nv_bfloat16*)A.epi.dst[e] + qo + p) = l2;
+      *reinterpret_cast<__nv_bfloat162*>((__nv_bfloat16*)A.epi.dst[e] + qo + p + half) = h2;
+    }
+  } else {
+    const size_t co = (((size_t)rs.pg[j] * R.Hkv + grp) * R.page + pos % R.page) * D;
+    __nv_bfloat16* cache = slot == G ? R.kc : R.vc;
+    *reinterpret_cast<__nv_bfloat162*>(cache + co + p) = l2;
+    *reinterpret_cast<__nv_bfloat162*>(cache + co + p + half) = h2;
+  }
+}
+
 // 4 consecutive outputs (weight rows col..col+3) of token j → Y (+ peers), or
 // the fused RoPE/append epilogue
 __device__ __forceinline__ void csk_store4(const Args& A, const RopeSmem& rs, int j, int col, float v0, float v1,
@@ -1143,6 +1188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 128) { KD_TRACE(8); KD_CTRACE(24); }
     pdl_wait();
     const int rpo = A.rpo, r4n = my_rows / 4;  // rpo and 128 are multiples of 4
+    float* T = (float*)smem;                    // rope: [M][rpo + 4] sums (the idle operand ring)
+    const int Tp = rpo + 4;
     for (int e = threadIdx.x; e < M * r4n; e += kThreads) {
       const int lr4 = (e / M) * 4, j = e - (e / M) * M;
       float acc[4];
@@ -1151,7 +1198,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int cr = 1; cr < split; ++cr)  // rank order → deterministic
 #pragma unroll
         for (int x = 0; x < 4; ++x) acc[x] += recv[((size_t)cr * rpo + lr4 + x) * P + j];
-      csk_store4(A, ropes, j, n0 + rank * rpo + lr4, acc[0], acc[1], acc[2], acc[3]);
+      if (A.rope)
+        *reinterpret_cast<float4*>(T + (size_t)j * Tp + lr4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      else
+        csk_store4(A, ropes, j, n0 + rank * rpo + lr4, acc[0], acc[1], acc[2], acc[3]);
+    }
+    if (A.rope) {  // second pass: lanes walk a token's rows (coalesced q / cache stores)
+      __syncthreads();
+      for (int e = threadIdx.x; e < M * r4n; e += kThreads) {
+        const int j = e / r4n, l4 = e - j * r4n, n = n0 + rank * rpo + 4 * l4;
+        if (n < A.N) rope_quad(A, ropes, j, n, *reinterpret_cast<const float4*>(T + (size_t)j * Tp + 4 * l4));
+      }
     }
     if (threadIdx.x == 128) { KD_TRACE(11); KD_CTRACE(25); }
     if (A.epi.n && my_rows > 0) {  // publish this CTA's stores to the consumer devices

@@ -5,17 +5,28 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2604_10180_b200 import _kd as K, api
 shapes = {"qkv": (64, 6144, 4096), "o": (64, 4096, 4096), "gu": (64, 28672, 4096), "down": (64, 4096, 14336),
-          "o_norm": (64, 4096, 4096), "down_norm": (64, 4096, 14336)}
+          "o_norm": (64, 4096, 4096), "down_norm": (64, 4096, 14336), "qkv_rope": (64, 6144, 4096)}
+plain_gemm = api.gemm
 for name in (sys.argv[1:] or list(shapes)):
     M, N, Kd = shapes[name]
     norm = name.endswith("_norm")
+    rope = name == "qkv_rope"
+    api.gemm = plain_gemm
     a = K.kd_attr_gemm_rmsnorm(M, N, Kd, K.KD_BF16, 1e-5, 0) if norm else K.kd_attr_gemm(M, N, Kd, K.KD_BF16)
+    if rope:
+        a = K.kd_attr_qkv_rope(M, Kd, 32, 8, 128, 16, 256, K.KD_BF16, 5e5)
+        bt = torch.arange(M * 256, device="cuda", dtype=torch.int32).view(M, 256)
+        sl = torch.full((M,), 4096, device="cuda", dtype=torch.int32)
+        q = torch.empty(M, 32 * 128, device="cuda", dtype=torch.bfloat16)
+        kc = torch.zeros(M * 256, 8, 16, 128, device="cuda", dtype=torch.bfloat16)
+        vc = torch.zeros_like(kc)
+        api.gemm = lambda a_, X_, W_, Y_, s_: api.qkv_rope(a_, X_, W_, bt, sl, q, kc, vc, s_)
     X = torch.randn(M, Kd, device="cuda").to(torch.bfloat16)
     W = torch.randn(N, Kd, device="cuda").to(torch.bfloat16)
     W2 = torch.randn(N, Kd, device="cuda").to(torch.bfloat16)
     Y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    scr = torch.zeros(api.op_scratch_bytes(K.KD_OP_GEMM_RMSNORM if norm else K.KD_OP_GEMM, a), dtype=torch.uint8,
-                      device="cuda")
+    op = K.KD_OP_GEMM_RMSNORM if norm else (K.KD_OP_QKV_ROPE if rope else K.KD_OP_GEMM)
+    scr = torch.zeros(max(256, api.op_scratch_bytes(op, a)), dtype=torch.uint8, device="cuda")
     r = torch.randn(M, N, device="cuda")
     gam = torch.ones(N, device="cuda").to(torch.bfloat16)
     if norm:
