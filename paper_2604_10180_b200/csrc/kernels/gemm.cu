@@ -1188,7 +1188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 128) { KD_TRACE(8); KD_CTRACE(24); }
     pdl_wait();
     const int rpo = A.rpo, r4n = my_rows / 4;  // rpo and 128 are multiples of 4
-    float* T = (float*)smem;                    // rope: [M][rpo + 4] sums (the idle operand ring)
+    float* T = (float*)smem;                    // [M][rpo + 4] sums (the idle operand ring)
     const int Tp = rpo + 4;
     for (int e = threadIdx.x; e < M * r4n; e += kThreads) {
       const int lr4 = (e / M) * 4, j = e - (e / M) * M;
@@ -1198,16 +1198,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int cr = 1; cr < split; ++cr)  // rank order → deterministic
 #pragma unroll
         for (int x = 0; x < 4; ++x) acc[x] += recv[((size_t)cr * rpo + lr4 + x) * P + j];
-      if (A.rope)
-        *reinterpret_cast<float4*>(T + (size_t)j * Tp + lr4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      else
-        csk_store4(A, ropes, j, n0 + rank * rpo + lr4, acc[0], acc[1], acc[2], acc[3]);
+      *reinterpret_cast<float4*>(T + (size_t)j * Tp + lr4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
     }
-    if (A.rope) {  // second pass: lanes walk a token's rows (coalesced q / cache stores)
-      __syncthreads();
-      for (int e = threadIdx.x; e < M * r4n; e += kThreads) {
-        const int j = e / r4n, l4 = e - j * r4n, n = n0 + rank * rpo + 4 * l4;
-        if (n < A.N) rope_quad(A, ropes, j, n, *reinterpret_cast<const float4*>(T + (size_t)j * Tp + 4 * l4));
+    // second pass: lanes walk a token's rows, so the output (and peer) stores
+    // coalesce; walking tokens, as the sum must, scatters every warp store
+    // over 32 rows of Y (measured: the RoPE epilogue's 2-byte stores cost ≈4 µs)
+    __syncthreads();
+    for (int e = threadIdx.x; e < M * r4n; e += kThreads) {
+      const int j = e / r4n, l4 = e - j * r4n, n = n0 + rank * rpo + 4 * l4;
+      const float4 v = *reinterpret_cast<const float4*>(T + (size_t)j * Tp + 4 * l4);
+      if (A.rope) {
+        if (n < A.N) rope_quad(A, ropes, j, n, v);
+      } else {
+        csk_store4(A, ropes, j, n, v.x, v.y, v.z, v.w);
       }
     }
     if (threadIdx.x == 128) { KD_TRACE(11); KD_CTRACE(25); }
