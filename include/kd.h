@@ -405,7 +405,9 @@ kd_status kd_op_gemm(const kd_attr_gemm* a, const void* X, const void* W, void* 
  * completed across its CTAs after an in-kernel grid barrier (all CTAs are
  * co-resident by construction). bf16 only, N % 8 == 0; r and gamma 16-byte
  * aligned; scratch as kd_op_scratch_bytes(KD_OP_GEMM_RMSNORM). Errors:
- * KD_ERR_UNSUPPORTED when no co-resident cluster tiling exists for the shape. */
+ * KD_ERR_UNSUPPORTED when no co-resident cluster tiling exists for the shape.
+ * The in-kernel grid barrier needs every CTA of the launch resident at once:
+ * do not run it concurrently with kernels that wait on its completion. */
 kd_status kd_op_gemm_rmsnorm(const kd_attr_gemm_rmsnorm* a, const void* X, const void* W, float* r,
                              const void* gamma, void* h, void* scratch, void* stream);
 /* a5: NeoX RoPE of q and k at pos = seq_len[b]-1, append (k_rot, v) to the
