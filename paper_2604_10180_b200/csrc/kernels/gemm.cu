@@ -152,40 +152,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pw = policy_evict_first(), px = policy_evict_last();
     const unsigned tx = (unsigned)(wst + xst);
     const long long n_pre = std::min<long long>(S, u1 - u0);
-    auto load_w = [&](long long u, int s) {
-      const int t = (int)(u / KB), kb = (int)(u % KB);
+    // (tile, k-block) of a unit, advanced incrementally: a 64-bit division per
+    // stage (a ~300-cycle subroutine) was measured at ≈600 cycles of issue
+    // cost per stage in this warp
+    const int t_first = (int)(u0 / KB), kb_first = (int)(u0 - (long long)t_first * KB);
+    auto load_w = [&](int t, int kb, int s) {
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sa + (size_t)s * wst + b * kStageA, &tmap_w, (kb * kbs + b) * kBK, w_row(t), &full[s], pw);
     };
-    auto load_x = [&](long long u, int s) {
-      const int t = (int)(u / KB), kb = (int)(u % KB);
+    auto load_x = [&](int t, int kb, int s) {
       const int xr = A.groups ? __ldg(A.meta + A.groups + t / A.tpg) : 0;
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sb + (size_t)s * xst + b * xbox, &tmap_x, (kb * kbs + b) * kBK, xr, &full[s], px);
     };
+    if (lane == 0) KD_CTRACE(24);
+    int t = t_first, kb = kb_first;
     if (lane == 0) {
       // weights never depend on the previous kernel: fill the first ring of W
       // tiles before the grid-dependency wait (overlaps the previous kernel's
       // tail), then the activations of those stages, then steady state
       for (long long i = 0; i < n_pre; ++i) {
         mbar_expect_tx(&full[i], tx);
-        load_w(u0 + i, (int)i);
+        load_w(t, kb, (int)i);
+        if (i == 0) KD_CTRACE(25);
+        if (++kb == KB) kb = 0, ++t;
       }
+      KD_CTRACE(26);
       KD_TRACE(2);
       pdl_wait();
-      for (long long i = 0; i < n_pre; ++i) load_x(u0 + i, (int)i);
+      t = t_first, kb = kb_first;
+      for (long long i = 0; i < n_pre; ++i) {
+        load_x(t, kb, (int)i);
+        if (++kb == KB) kb = 0, ++t;
+      }
     }
     __syncwarp();
+    t = __shfl_sync(0xffffffffu, t, 0);
+    kb = __shfl_sync(0xffffffffu, kb, 0);
     long long i = n_pre;
+    int s = (int)(n_pre % S), ph = (int)(n_pre / S);
     for (long long u = u0 + n_pre; u < u1; ++u, ++i) {
-      const int s = (int)(i % S);
-      mbar_wait(&empty[s], (unsigned)(((i / S) - 1) & 1));
+      mbar_wait(&empty[s], (unsigned)((ph - 1) & 1));
       if (lane == 0) {
         mbar_expect_tx(&full[s], tx);
-        load_w(u, s);
-        load_x(u, s);
+        load_w(t, kb, s);
+        load_x(t, kb, s);
       }
       __syncwarp();
+      if (++kb == KB) kb = 0, ++t;
+      if (++s == S) s = 0, ++ph;
     }
     if (lane == 0) KD_TRACE(3);
   } else if (warp == 1) {
@@ -195,10 +210,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(A.mma_n >> 3) << 17) |
                            ((uint32_t)(kBM >> 4) << 24);
     long long i = 0;
-    int seg = 0;
+    int seg = 0, st = 0, ph = 0;  // ring slot / phase of unit i, advanced incrementally (no 64-bit division per stage)
     long long u = u0;
+    int t = (int)(u0 / KB);
     while (u < u1) {
-      const int t = (int)(u / KB);
       const long long seg_end = std::min<long long>(u1, (long long)(t + 1) * KB);
       const int a = seg & 1, use = seg >> 1;
       if (use > 0) mbar_wait(&tempty[a], (unsigned)((use - 1) & 1));
@@ -206,8 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tmem_d = tmem_base + (uint32_t)(a * A.mma_n);
       bool first = true;
       for (; u < seg_end; ++u, ++i) {
-        const int s = (int)(i % S);
-        mbar_wait(&full[s], (unsigned)((i / S) & 1));
+        const int s = st;
+        mbar_wait(&full[s], (unsigned)(ph & 1));
+        if (++st == S) st = 0, ++ph;
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (lane == 0) {
           if (i == 0) KD_TRACE(4);
@@ -227,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mma_commit(&tfull[a]);  // accumulator ready for the epilogue
       __syncwarp();
       ++seg;
+      ++t;
     }
     if (lane == 0) KD_TRACE(5);
   } else if (warp >= 4) {
@@ -1030,24 +1047,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < n_pre; ++i) load_x(i, i);
     }
     __syncwarp();
-    for (int i = n_pre; i < nk; ++i) {
-      const int s = i % S;
-      mbar_wait(&empty[s], (unsigned)(((i / S) - 1) & 1));
+    for (int i = n_pre, s = n_pre % S, ph = n_pre / S; i < nk; ++i) {
+      mbar_wait(&empty[s], (unsigned)((ph - 1) & 1));
       if (lane == 0) {
         mbar_expect_tx(&full[s], tx);
         load_w(i, s);
         load_x(i, s);
       }
       __syncwarp();
+      if (++s == S) s = 0, ++ph;
     }
     if (lane == 0) KD_TRACE(3);
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (warp-uniform loop, lane 0 issues)
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(A.mma_n >> 3) << 17) |
                            ((uint32_t)(kBM >> 4) << 24);
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % S;
-      mbar_wait(&full[s], (unsigned)((i / S) & 1));
+    for (int i = 0, st = 0, ph = 0; i < nk; ++i) {
+      const int s = st;
+      mbar_wait(&full[s], (unsigned)(ph & 1));
+      if (++st == S) st = 0, ++ph;
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (lane == 0) {
         if (i == 0) KD_TRACE(4);

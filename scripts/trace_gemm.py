@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2604_10180_b200 import _kd as K, api
 shapes = {"qkv": (64, 6144, 4096), "o": (64, 4096, 4096), "gu": (64, 28672, 4096), "down": (64, 4096, 14336),
-          "o_norm": (64, 4096, 4096), "down_norm": (64, 4096, 14336), "qkv_rope": (64, 6144, 4096)}
+          "o_norm": (64, 4096, 4096), "down_norm": (64, 4096, 14336), "qkv_rope": (64, 6144, 4096), "gu_silu": (64, 28672, 4096)}
 plain_gemm = api.gemm
 for name in (sys.argv[1:] or list(shapes)):
     M, N, Kd = shapes[name]
@@ -13,6 +13,8 @@ for name in (sys.argv[1:] or list(shapes)):
     rope = name == "qkv_rope"
     api.gemm = plain_gemm
     a = K.kd_attr_gemm_rmsnorm(M, N, Kd, K.KD_BF16, 1e-5, 0) if norm else K.kd_attr_gemm(M, N, Kd, K.KD_BF16)
+    if name == "gu_silu":
+        api.gemm = lambda a_, X_, W_, Y_, s_: api.gemm_silu(a_, X_, W_, Y_, s_)
     if rope:
         a = K.kd_attr_qkv_rope(M, Kd, 32, 8, 128, 16, 256, K.KD_BF16, 5e5)
         bt = torch.arange(M * 256, device="cuda", dtype=torch.int32).view(M, 256)
@@ -25,7 +27,8 @@ for name in (sys.argv[1:] or list(shapes)):
     W = torch.randn(N, Kd, device="cuda").to(torch.bfloat16)
     W2 = torch.randn(N, Kd, device="cuda").to(torch.bfloat16)
     Y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    op = K.KD_OP_GEMM_RMSNORM if norm else (K.KD_OP_QKV_ROPE if rope else K.KD_OP_GEMM)
+    op = K.KD_OP_GEMM_RMSNORM if norm else (K.KD_OP_QKV_ROPE if rope else
+                                            (K.KD_OP_GEMM_SILU if name == "gu_silu" else K.KD_OP_GEMM))
     scr = torch.zeros(max(256, api.op_scratch_bytes(op, a)), dtype=torch.uint8, device="cuda")
     r = torch.randn(M, N, device="cuda")
     gam = torch.ones(N, device="cuda").to(torch.bfloat16)
@@ -57,6 +60,9 @@ for name in (sys.argv[1:] or list(shapes)):
         print("  norm cycles: A", d(22, 16), "sync", d(16, 17), "B", d(17, 18), "sync+fence..arrive", d(18, 24),
               "barrier", d(24, 23), "C", d(23, 19), "sync", d(19, 20), "D", d(20, 21))
         continue
+    if name in ("gu", "gu_silu"):
+        d = lambda a, b: int(np.median(raw[:, b].astype(np.int64) - raw[:, a].astype(np.int64)))
+        print("  prologue cycles: first TMA issue", d(24, 25), "rest of the first ring", d(25, 26))
     own_rows = raw[raw[:, 21] > 0]
     if len(own_rows):
         print(f"  fold cycles: med {np.median(own_rows[:, 20]):.0f} max {own_rows[:, 20].max()}  nb {np.unique(own_rows[:, 21])} n4 {np.unique(own_rows[:, 22])}")
