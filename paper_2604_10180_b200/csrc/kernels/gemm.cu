@@ -863,10 +863,11 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
   if (threadIdx.x == 0) {  // grid barrier (self-resetting: see the departure at the end)
     KD_TRACE(13);
     KD_CTRACE(24);
-    fence_acq_rel_gpu();
+    // the acq_rel add releases this CTA's partial sums (ordered before it by
+    // the bar.sync: release is cumulative); polls back off to keep the line
+    // free for the other CTAs' arrivals
     atom_add_acq_rel_gpu(A.bar, 1u);
-    while (ld_acquire_gpu(A.bar) < (unsigned)G) {
-    }
+    while (ld_acquire_gpu(A.bar) < (unsigned)G) __nanosleep(64);
     KD_TRACE(14);
     KD_CTRACE(23);
   }
