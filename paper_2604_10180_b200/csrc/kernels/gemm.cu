@@ -117,6 +117,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) KD_TRACE(0);
   pdl_launch_dependents();
   const long long U = A.units, G = gridDim.x, c = blockIdx.x;
+  if (threadIdx.x == 0) {  // descriptor fetches first: the first TMA waits on them
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
+  }
   const long long u0 = unit_begin(c, U, G), u1 = unit_begin(c + 1, U, G);
   const int KB = A.kblocks;
   const uint32_t ncols = (2 * A.mma_n <= 32) ? 32 : (2 * A.mma_n <= 64 ? 64 : (2 * A.mma_n <= 128 ? 128 : (2 * A.mma_n <= 256 ? 256 : 512)));
@@ -132,8 +136,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(fixbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -983,7 +985,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* send = (float*)smem;  // split == 1: [M][128] fp32 staging, reuses the idle ring after the last MMA
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) KD_TRACE(0);
+  if (threadIdx.x == 0) {  // descriptor fetches first: the first TMA waits on them
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
+    KD_TRACE(0);
+  }
   pdl_launch_dependents();
   const int rank = split > 1 ? (int)cluster_ctarank() : 0;
   const int tile = blockIdx.x / split;
@@ -1003,8 +1009,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // each peer rank sends my_rows rows of ⌈M/4⌉ 16-byte groups
     if (split > 1) mbar_expect_tx(rbar, (unsigned)((split - 1) * my_rows * ((M + 3) / 4) * 16));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
