@@ -141,6 +141,31 @@ def test_full_width_8b_layers_vs_oracle_sampled(mod):
     assert relerr(rt.residual(), r_ref) < 2e-2
 
 
+@pytest.mark.slow
+def test_full_width_8b_fused_graph(mod):
+    """The bench's 1-GPU graph (QKV+RoPE, O+norm2, gate_up+SiLU, down+norm1
+    fused) at full 8B layer shapes: within tolerance of the oracle at B=8, and
+    of the unfused graph at the bench's B=64 (every fused epilogue at the
+    tilings the bench runs)."""
+    DEC, K = mod
+    for batch, vs_oracle in ((8, True), (64, False)):
+        cfg = synth.LLAMA8B.with_(n_layers=2, batch=batch)
+        inp = synth.make_decoder_inputs(cfg)  # host inputs: both graphs see the same weights
+        outs = []
+        for fuse in (True, False):
+            dg = DEC.DecoderGraph(cfg, fuse_silu=fuse, fuse_rope=fuse, fuse_norm=fuse)
+            rt = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp)
+            rt.step()
+            rt.sync()
+            rt.rt.check()
+            outs.append(rt.residual())
+            del rt
+        if vs_oracle:
+            r_ref, _, _ = OL.decoder_step(inp, act="bf16")
+            assert relerr(outs[0], r_ref) < 2e-2
+        assert relerr(outs[0], outs[1]) < 1e-2
+
+
 TINY_MOE = synth.TINY.with_(n_experts=4, top_k=2, n_micro=2)
 
 
