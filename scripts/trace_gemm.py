@@ -1,5 +1,9 @@
 #!/usr/bin/env python3
-"""Per-CTA phase timeline of one GEMM launch (kd_debug_gemm_trace)."""
+"""Per-CTA phase timeline of one GEMM launch (kd_debug_gemm_trace).
+
+usage: trace_gemm.py [qkv|o|gu|down|o_norm|down_norm|qkv_rope|gu_silu ...]
+(8B shapes, m=64; the traced launch streams cold weights). The fused-norm
+variants print per-phase cycle counts of the norm epilogue instead."""
 import ctypes as C, os, sys, math
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
