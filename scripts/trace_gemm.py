@@ -47,10 +47,10 @@ for name in (sys.argv[1:] or list(shapes)):
     torch.cuda.synchronize()
     K.kd_debug_gemm_trace(None)
     t = tr.view(148, 32).cpu().numpy().astype("float64")
-    t0 = t[:, 0].min()
+    t0 = t[:, 0][t[:, 0] > 0].min()  # rows past the grid are unused (0)
     rel = (t - t0) / 1000.0
     rel[t == 0] = float("nan")
-    rel[:, 20:] = float("nan")
+    rel[:, 16:] = float("nan")  # slots 16.. hold clock64 cycle stamps
     import numpy as np
     labels = ["entry", "setup", "tma0", "tmaN", "full0", "commitN", "seg0.wait", "seg0.done", "seg1.wait", "seg1.done",
               "seg2.wait", "seg2.done", "-", "fold.end|n.A", "n.bar", "exit|n.end", "gbar.pass", "-", "gbar.arrive", "-"] + ["-"] * 12
@@ -67,7 +67,7 @@ for name in (sys.argv[1:] or list(shapes)):
     if name in ("gu", "gu_silu"):
         d = lambda a, b: int(np.median(raw[:, b].astype(np.int64) - raw[:, a].astype(np.int64)))
         print("  prologue cycles: first TMA issue", d(24, 25), "rest of the first ring", d(25, 26))
-    own_rows = raw[raw[:, 21] > 0]
+    own_rows = raw[raw[:, 21] > 0] if name in ("gu", "gu_silu") else raw[:0]
     if len(own_rows):
         print(f"  fold cycles: med {np.median(own_rows[:, 20]):.0f} max {own_rows[:, 20].max()}  nb {np.unique(own_rows[:, 21])} n4 {np.unique(own_rows[:, 22])}")
     for i, l in enumerate(labels):
