@@ -117,10 +117,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) KD_TRACE(0);
   pdl_launch_dependents();
   const long long U = A.units, G = gridDim.x, c = blockIdx.x;
-  if (threadIdx.x == 0) {  // descriptor fetches first: the first TMA waits on them
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
-  }
   const long long u0 = unit_begin(c, U, G), u1 = unit_begin(c + 1, U, G);
   const int KB = A.kblocks;
   const uint32_t ncols = (2 * A.mma_n <= 32) ? 32 : (2 * A.mma_n <= 64 ? 64 : (2 * A.mma_n <= 128 ? 128 : (2 * A.mma_n <= 256 ? 256 : 512)));
@@ -136,6 +132,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(fixbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -985,12 +983,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* send = (float*)smem;  // split == 1: [M][128] fp32 staging, reuses the idle ring after the last MMA
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {  // descriptor fetches first: the first TMA waits on them
-    KD_CTRACE(30);
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
-    KD_TRACE(0);
-  }
+  if (threadIdx.x == 0) KD_TRACE(0);
   pdl_launch_dependents();
   const int rank = split > 1 ? (int)cluster_ctarank() : 0;
   const int tile = blockIdx.x / split;
@@ -1010,41 +1003,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     // each peer rank sends my_rows rows of ⌈M/4⌉ 16-byte groups
     if (split > 1) mbar_expect_tx(rbar, (unsigned)((split - 1) * my_rows * ((M + 3) / 4) * 16));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // the first ring of weight tiles right away: it needs neither TMEM nor the
-    // cluster barrier (own shared memory), and weights never depend on the
-    // previous kernel (activations follow after the dependency wait)
-    const uint64_t pw0 = policy_evict_first();
-    for (int i = 0; i < min(S, nk); ++i) {
-      mbar_expect_tx(&full[i], (unsigned)(wst + xst));
-      for (int b = 0; b < kbs; ++b)
-        tma_load_2d(sa + (size_t)i * wst + b * kStageA, &tmap_w, ((kb0 + i) * kbs + b) * kBK, n0, &full[i], pw0);
-    }
-    KD_TRACE(13);
-    KD_CTRACE(31);
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_w) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_x) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(ncols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    if (lane == 0) KD_CTRACE(27);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (threadIdx.x == 0) KD_CTRACE(28);
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (split > 1) {
     // every rank's rbar is armed once this completes. Waited here, at the
     // start: a cluster-scope acquire invalidates L1 (CCTL.IVALL), which was
     // measured to stall the epilogue's shared-memory work by ≈2-3K cycles
     // when done after the main loop.
-    // The TMA and MMA warps wait later (once their first loads are issued /
-    // before the first MMA): a CTA's peers start up to ~1 µs apart, and that
-    // skew must not delay the first activation loads.
-    cluster_arrive_relaxed();
-    if (warp >= 2) cluster_wait_acquire();
+    cluster_arrive_release();
+    cluster_wait_acquire();
   }
   const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) { KD_CTRACE(29); KD_TRACE(1); }
+  if (threadIdx.x == 0) KD_TRACE(1);
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (warp-uniform loop, lane 0 issues)
@@ -1058,14 +1037,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sb + (size_t)s * xst + b * xbox, &tmap_x, ((kb0 + i) * kbs + b) * kBK, 0, &full[s], px);
     };
-    const int n_pre = min(S, nk);  // their weight tiles were issued at barrier init
+    const int n_pre = min(S, nk);
     if (lane == 0) {
+      for (int i = 0; i < n_pre; ++i) {  // weights before the grid-dependency wait
+        mbar_expect_tx(&full[i], tx);
+        load_w(i, i);
+      }
       KD_TRACE(2);
       pdl_wait();
       for (int i = 0; i < n_pre; ++i) load_x(i, i);
     }
     __syncwarp();
-    if (split > 1) cluster_wait_acquire();
     for (int i = n_pre, s = n_pre % S, ph = n_pre / S; i < nk; ++i) {
       mbar_wait(&empty[s], (unsigned)((ph - 1) & 1));
       if (lane == 0) {
@@ -1081,7 +1063,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------ MMA issuer (warp-uniform loop, lane 0 issues)
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(A.mma_n >> 3) << 17) |
                            ((uint32_t)(kBM >> 4) << 24);
-    if (split > 1) cluster_wait_acquire();
     for (int i = 0, st = 0, ph = 0; i < nk; ++i) {
       const int s = st;
       mbar_wait(&full[s], (unsigned)(ph & 1));

@@ -164,10 +164,6 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
 }
 __device__ __forceinline__ void cluster_arrive_release() { asm volatile("barrier.cluster.arrive.release;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire;" ::: "memory"); }
-// after fence.mbarrier_init.release.cluster (which publishes the barrier
-// inits), a relaxed arrive suffices and does not wait for this thread's
-// outstanding memory operations (the TMA loads already in flight)
-__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory"); }
 // 16-byte remote store into a peer CTA's shared memory; completes `bytes` on
 // the peer's mbarrier (both addresses are shared::cluster)
 __device__ __forceinline__ void st_async_v4(uint32_t raddr, float a, float b, float c, float d, uint32_t rbar) {

@@ -64,10 +64,6 @@ for name in (sys.argv[1:] or list(shapes)):
         print("  norm cycles: A", d(22, 16), "sync", d(16, 17), "B", d(17, 18), "sync+fence..arrive", d(18, 24),
               "barrier", d(24, 23), "C", d(23, 19), "sync", d(19, 20), "D", d(20, 21))
         continue
-    if name in ("qkv", "o", "down"):
-        d = lambda a, b: int(np.median(raw[:, b].astype(np.int64) - raw[:, a].astype(np.int64)))
-        print("  setup cycles from entry: W ring issued", d(30, 31), "TMEM alloc", d(30, 27), "syncthreads", d(30, 28),
-              "cluster barrier", d(30, 29))
     if name in ("gu", "gu_silu"):
         d = lambda a, b: int(np.median(raw[:, b].astype(np.int64) - raw[:, a].astype(np.int64)))
         print("  prologue cycles: first TMA issue", d(24, 25), "rest of the first ring", d(25, 26))
