@@ -211,11 +211,12 @@ def main():
         # (KD_OP_QKV_ROPE, bit-identical to the pair: 17.0 vs 15.0 + 3.7 µs, step 9.04 vs
         # 9.13 ms) and the O GEMM with norm2 / the down GEMM with the next layer's norm1
         # (KD_OP_GEMM_RMSNORM: the per-token Σr² is finished across the grid after an
-        # in-kernel barrier; step 9.13 vs 9.17 ms). A/B: KD_BENCH_NO_FUSE (all),
-        # KD_BENCH_NO_FUSE_ROPE, KD_BENCH_NO_FUSE_NORM.
+        # in-kernel barrier; step 8.92 vs 8.95 ms). A/B: KD_BENCH_NO_FUSE (all),
+        # KD_BENCH_NO_FUSE_ROPE, KD_BENCH_NO_FUSE_NORM, KD_BENCH_FUSE_NORM=o (O+norm2 only).
         fuse = not os.environ.get("KD_BENCH_NO_FUSE")
         dg = DEC.DecoderGraph(cfg, fuse_silu=fuse, fuse_rope=fuse and not os.environ.get("KD_BENCH_NO_FUSE_ROPE"),
-                              fuse_norm=fuse and not os.environ.get("KD_BENCH_NO_FUSE_NORM"))
+                              fuse_norm=(fuse and not os.environ.get("KD_BENCH_NO_FUSE_NORM")) and
+                              (os.environ.get("KD_BENCH_FUSE_NORM") or True))
         assign = [0] * dg.g.num_kernels
         rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed, use_graph=not args.no_graph)
         placement = "monolithic (all kernels on one B200)"

@@ -89,7 +89,8 @@ class DecoderGraph:
         fuse_norm: declare each O GEMM with the following residual add +
         RMSNorm (norm2), and each dense down GEMM with the next layer's norm1,
         as ONE kernel (KD_OP_GEMM_RMSNORM) — for co-located placements; the o
-        and d activations then never exist (except the last layer's d)."""
+        and d activations then never exist (except the last layer's d).
+        fuse_norm="o" fuses only O + norm2 (A/B: measured between all and none)."""
         if act not in (K.KD_BF16, K.KD_F32):
             raise ValueError("act must be KD_BF16 or KD_F32")
         if act == K.KD_F32 and (cfg.n_experts or cfg.attn_every):
@@ -99,6 +100,7 @@ class DecoderGraph:
         self.fuse_silu = fuse_silu
         fuse_rope = bool(fuse_rope) and act == K.KD_BF16
         self.fuse_rope = fuse_rope
+        norm_o_only = fuse_norm == "o"  # fuse only O + norm2 (keep down → norm1 apart)
         fuse_norm = bool(fuse_norm) and act == K.KD_BF16
         self.fuse_norm = fuse_norm
         adt = "bf16" if act == K.KD_BF16 else "f32"  # storage of weights, activations and KV cache
@@ -130,7 +132,8 @@ class DecoderGraph:
         E, k = cfg.n_experts, cfg.top_k
 
         def fused_down(l):  # dense attention layer whose down GEMM also runs layer l+1's norm1
-            return fuse_norm and not E and l < L - 1 and cfg.is_attn_layer(l) and cfg.is_attn_layer(l + 1)
+            return (fuse_norm and not norm_o_only and not E and l < L - 1 and cfg.is_attn_layer(l)
+                    and cfg.is_attn_layer(l + 1))
         if E:
             mb = C.c_uint64()
             K.check(K.kd_moe_meta_bytes(m, E, k, C.byref(mb)), "kd_moe_meta_bytes")
