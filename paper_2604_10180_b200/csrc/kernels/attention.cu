@@ -38,6 +38,9 @@ constexpr int kThreads = (kWarps + 2) * 32;  // + producer + epilogue warp
 constexpr int kPage = 16;
 constexpr int kMaxG = 8;
 constexpr int kMaxPagesPerSplit = 512;
+// split merge fast path (all of a unit's partial loads in one batch) when
+// splits·G ≤ this and splits ≤ kFastSplits
+constexpr int kFastSplitLse = 128, kFastSplits = 4;
 
 struct Params {
   const __nv_bfloat16* q;
@@ -195,6 +198,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
   uint64_t* iempty = ifull + 4;  // [4]
   __shared__ int s_item[4];
   __shared__ float s_w[kWarps * kMaxG], s_M[kMaxG], s_L[kMaxG];  // epilogue merge weights
+  __shared__ float s_lse[kFastSplitLse];                           // split merge: every (split, head) LSE
 
   pdl_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -414,49 +418,95 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
           fence_acq_rel_gpu();
           const float* lse = P.part_lse + (size_t)unit * P.splits * G;  // [split][G]
           const float* po = P.part_o + (size_t)unit * P.splits * G * D;  // [split][G][D]
-          // per-head max / normaliser over the splits (lanes over splits)
-          for (int h = 0; h < G; ++h) {
-            float M = -INFINITY;
-            for (int sp = lane; sp < P.splits; sp += 32) M = fmaxf(M, __ldcg(lse + sp * G + h));
-#pragma unroll
-            for (int x = 16; x; x >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, x));
-            const float Mu = (M == -INFINITY) ? 0.f : M;
-            float L = 0.f;
-            for (int sp = lane; sp < P.splits; sp += 32) L += exp2f(__ldcg(lse + sp * G + h) - Mu);
-#pragma unroll
-            for (int x = 16; x; x >>= 1) L += __shfl_xor_sync(0xffffffffu, L, x);
-            if (lane == 0) s_M[h] = Mu, s_L[h] = L;
-          }
-          __syncwarp();
-          for (int e4 = lane; e4 < G * D / 4; e4 += 32) {
-            const int h = (e4 * 4) / D, d0 = (e4 * 4) % D;
-            const float Mu = s_M[h];
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            int sp = 0;
-            for (; sp + 4 <= P.splits; sp += 4) {  // 4 independent L2 round trips in flight
-              float wv[4];
-              float4 v[4];
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                wv[u] = __ldcg(lse + (sp + u) * G + h);
-                v[u] = __ldcg(reinterpret_cast<const float4*>(po + ((size_t)(sp + u) * G + h) * D + d0));
-              }
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const float sc = exp2f(wv[u] - Mu);
-                acc.x += sc * v[u].x, acc.y += sc * v[u].y, acc.z += sc * v[u].z, acc.w += sc * v[u].w;
-              }
+          const int nl = P.splits * G, n_e4 = G * D / 4;
+          if (nl <= kFastSplitLse && P.splits <= kFastSplits && n_e4 <= 32 * 4) {
+            // fast path: every LSE in one batch, then per head max / normaliser
+            // in split order from shared memory, then every partial this lane
+            // combines in one batch (a dependent L2 round trip costs ~1 µs here,
+            // and the last units' merges are the kernel's tail)
+            for (int i = lane; i < nl; i += 32) s_lse[i] = __ldcg(lse + i);
+            __syncwarp();
+            if (lane < G) {
+              float M = -INFINITY;
+              for (int sp = 0; sp < P.splits; ++sp) M = fmaxf(M, s_lse[sp * G + lane]);
+              const float Mu = (M == -INFINITY) ? 0.f : M;
+              float L = 0.f;
+              for (int sp = 0; sp < P.splits; ++sp) L += exp2f(s_lse[sp * G + lane] - Mu);
+              s_M[lane] = Mu, s_L[lane] = L;
             }
-            for (; sp < P.splits; ++sp) {
-              const float sc = exp2f(__ldcg(lse + sp * G + h) - Mu);
-              const float4 v = __ldcg(reinterpret_cast<const float4*>(po + ((size_t)sp * G + h) * D + d0));
-              acc.x += sc * v.x, acc.y += sc * v.y, acc.z += sc * v.z, acc.w += sc * v.w;
+            __syncwarp();
+            float4 v[4][kFastSplits];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int e4 = lane + 32 * k, h = (e4 * 4) / D, d0 = (e4 * 4) % D;
+#pragma unroll
+              for (int sp = 0; sp < kFastSplits; ++sp)
+                if (e4 < n_e4 && sp < P.splits)
+                  v[k][sp] = __ldcg(reinterpret_cast<const float4*>(po + ((size_t)sp * G + h) * D + d0));
             }
-            const float L = s_L[h];
-            const float inv = L > 0.f ? 1.f / L : 0.f;
-            acc.x *= inv, acc.y *= inv, acc.z *= inv, acc.w *= inv;
-            store_out4(P, (size_t)b * P.Hq * D + (size_t)(g * G + h) * D + d0, acc);
-            if (P.lse && d0 == 0) store_lse(P, (size_t)b * P.Hq + g * G + h, L > 0.f ? Mu + log2f(L) : -INFINITY);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int e4 = lane + 32 * k, h = (e4 * 4) / D, d0 = (e4 * 4) % D;
+              if (e4 >= n_e4) continue;
+              const float Mu = s_M[h];
+              float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int sp = 0; sp < kFastSplits; ++sp)
+                if (sp < P.splits) {
+                  const float sc = exp2f(s_lse[sp * G + h] - Mu);
+                  acc.x += sc * v[k][sp].x, acc.y += sc * v[k][sp].y, acc.z += sc * v[k][sp].z, acc.w += sc * v[k][sp].w;
+                }
+              const float L = s_L[h];
+              const float inv = L > 0.f ? 1.f / L : 0.f;
+              acc.x *= inv, acc.y *= inv, acc.z *= inv, acc.w *= inv;
+              store_out4(P, (size_t)b * P.Hq * D + (size_t)(g * G + h) * D + d0, acc);
+              if (P.lse && d0 == 0) store_lse(P, (size_t)b * P.Hq + g * G + h, L > 0.f ? Mu + log2f(L) : -INFINITY);
+            }
+          } else {
+            // per-head max / normaliser over the splits (lanes over splits)
+            for (int h = 0; h < G; ++h) {
+              float M = -INFINITY;
+              for (int sp = lane; sp < P.splits; sp += 32) M = fmaxf(M, __ldcg(lse + sp * G + h));
+  #pragma unroll
+              for (int x = 16; x; x >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, x));
+              const float Mu = (M == -INFINITY) ? 0.f : M;
+              float L = 0.f;
+              for (int sp = lane; sp < P.splits; sp += 32) L += exp2f(__ldcg(lse + sp * G + h) - Mu);
+  #pragma unroll
+              for (int x = 16; x; x >>= 1) L += __shfl_xor_sync(0xffffffffu, L, x);
+              if (lane == 0) s_M[h] = Mu, s_L[h] = L;
+            }
+            __syncwarp();
+            for (int e4 = lane; e4 < G * D / 4; e4 += 32) {
+              const int h = (e4 * 4) / D, d0 = (e4 * 4) % D;
+              const float Mu = s_M[h];
+              float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+              int sp = 0;
+              for (; sp + 4 <= P.splits; sp += 4) {  // 4 independent L2 round trips in flight
+                float wv[4];
+                float4 v[4];
+  #pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  wv[u] = __ldcg(lse + (sp + u) * G + h);
+                  v[u] = __ldcg(reinterpret_cast<const float4*>(po + ((size_t)(sp + u) * G + h) * D + d0));
+                }
+  #pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const float sc = exp2f(wv[u] - Mu);
+                  acc.x += sc * v[u].x, acc.y += sc * v[u].y, acc.z += sc * v[u].z, acc.w += sc * v[u].w;
+                }
+              }
+              for (; sp < P.splits; ++sp) {
+                const float sc = exp2f(__ldcg(lse + sp * G + h) - Mu);
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(po + ((size_t)sp * G + h) * D + d0));
+                acc.x += sc * v.x, acc.y += sc * v.y, acc.z += sc * v.z, acc.w += sc * v.w;
+              }
+              const float L = s_L[h];
+              const float inv = L > 0.f ? 1.f / L : 0.f;
+              acc.x *= inv, acc.y *= inv, acc.z *= inv, acc.w *= inv;
+              store_out4(P, (size_t)b * P.Hq * D + (size_t)(g * G + h) * D + d0, acc);
+              if (P.lse && d0 == 0) store_lse(P, (size_t)b * P.Hq + g * G + h, L > 0.f ? Mu + log2f(L) : -INFINITY);
+            }
           }
           if (lane == 0) P.counter[unit] = 0u;  // ready for the next launch
         }
