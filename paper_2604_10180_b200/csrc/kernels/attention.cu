@@ -409,13 +409,14 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
       bool done = true;
       if (!single) {
         unsigned prev = 0;
-        if (lane == 0) {
-          fence_acq_rel_gpu();
-          prev = atom_add_acq_rel_gpu(&P.counter[unit], 1u);
-        }
+        // the acq_rel add releases this warp's partial (its stores are ordered
+        // before lane 0's add by the __syncwarp above: release is cumulative)
+        // and acquires the other splits' partials for the last arriver; the
+        // __syncwarp after it orders the other lanes' loads behind lane 0
+        if (lane == 0) prev = atom_add_acq_rel_gpu(&P.counter[unit], 1u);
         done = __shfl_sync(0xffffffffu, prev, 0) == (unsigned)P.splits - 1;
         if (done) {
-          fence_acq_rel_gpu();
+          __syncwarp();
           const float* lse = P.part_lse + (size_t)unit * P.splits * G;  // [split][G]
           const float* po = P.part_o + (size_t)unit * P.splits * G * D;  // [split][G][D]
           const int nl = P.splits * G, n_e4 = G * D / 4;
