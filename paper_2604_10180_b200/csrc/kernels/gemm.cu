@@ -300,10 +300,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int n_contrib = (int)(lastc - first + 1);
           unsigned* arrive = A.counter + 2 + t;
           named_bar(1, 128);
-          if (ep_tid == 0) {
-            fence_acq_rel_gpu();
-            s_flag[0] = atom_add_acq_rel_gpu(arrive, 1u);
-          }
+          // the acq_rel add releases the partial (the 128 threads' stores are
+          // ordered before it by the named barrier: release is cumulative) and
+          // acquires the other contributors' for the last arriver
+          if (ep_tid == 0) s_flag[0] = atom_add_acq_rel_gpu(arrive, 1u);
           named_bar(1, 128);
           if (s_flag[0] == (unsigned)(n_contrib - 1)) {
             if (ep_tid == 0) *arrive = 0u;
