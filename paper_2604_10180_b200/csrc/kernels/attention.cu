@@ -421,11 +421,20 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
           const float* po = P.part_o + (size_t)unit * P.splits * G * D;  // [split][G][D]
           const int nl = P.splits * G, n_e4 = G * D / 4;
           if (nl <= kFastSplitLse && P.splits <= kFastSplits && n_e4 <= 32 * 4) {
-            // fast path: every LSE in one batch, then per head max / normaliser
-            // in split order from shared memory, then every partial this lane
-            // combines in one batch (a dependent L2 round trip costs ~1 µs here,
-            // and the last units' merges are the kernel's tail)
-            for (int i = lane; i < nl; i += 32) s_lse[i] = __ldcg(lse + i);
+            // fast path: every partial this lane combines and every LSE in one
+            // batch, then per head max / normaliser in split order from shared
+            // memory (a dependent L2 round trip costs ~1 µs here, and the last
+            // units' merges are the kernel's tail)
+            float4 v[4][kFastSplits];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int e4 = lane + 32 * k, h = (e4 * 4) / D, d0 = (e4 * 4) % D;
+#pragma unroll
+              for (int sp = 0; sp < kFastSplits; ++sp)
+                if (e4 < n_e4 && sp < P.splits)
+                  v[k][sp] = __ldcg(reinterpret_cast<const float4*>(po + ((size_t)sp * G + h) * D + d0));
+            }
+            for (int i = lane; i < nl; i += 32) s_lse[i] = __ldcg(lse + i);  // (both batches in flight)
             __syncwarp();
             if (lane < G) {
               float M = -INFINITY;
@@ -436,15 +445,6 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
               s_M[lane] = Mu, s_L[lane] = L;
             }
             __syncwarp();
-            float4 v[4][kFastSplits];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int e4 = lane + 32 * k, h = (e4 * 4) / D, d0 = (e4 * 4) % D;
-#pragma unroll
-              for (int sp = 0; sp < kFastSplits; ++sp)
-                if (e4 < n_e4 && sp < P.splits)
-                  v[k][sp] = __ldcg(reinterpret_cast<const float4*>(po + ((size_t)sp * G + h) * D + d0));
-            }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const int e4 = lane + 32 * k, h = (e4 * 4) / D, d0 = (e4 * 4) % D;
