@@ -98,6 +98,25 @@ def test_rope_pairs_halves_not_adjacent():
     assert np.all(y[[1, 2, 3, 5, 6, 7]] == 0)
 
 
+def test_rope_frequency_exponent_second_pair_hand_value():
+    """Pins θ^(−2i/D) for i ≥ 1 (R12; the Llama/NeoX RoPE frequency
+    schedule): D = 4, θ = 10⁴, pos = 3 → pair 0 turns by 3 rad, pair 1 by
+    3·10⁴^(−2/4) = 3·10⁻² rad. Hand values (cos 0.03, sin 0.03, cos 3, sin 3)
+    are literals, not recomputed from the oracle's formula; a wrong exponent
+    (θ^(−i/D), θ^(−2i/(D−2)), θ^(+…)) or swapped pairing fails here."""
+    c0, s0 = L.rope_freqs(3, 4, 1e4)
+    assert abs(c0[0] - (-0.9899924966004454)) < 1e-15 and abs(s0[0] - 0.1411200080598672) < 1e-15
+    assert abs(c0[1] - 0.9995500337489875) < 1e-15 and abs(s0[1] - 0.029995500202495664) < 1e-15
+    # a unit vector on the second pair's first half: (0, 1, 0, 0) -> (0, cos .03, 0, sin .03)
+    y = L.rope_neox(np.array([0.0, 1.0, 0.0, 0.0]), 3, 1e4)
+    assert np.allclose(y, [0.0, 0.9995500337489875, 0.0, 0.029995500202495664], rtol=0, atol=1e-15)
+    # D = 8, θ = 10⁴, pos = 1: angles 1, 10⁻¹, 10⁻², 10⁻³ rad (exactly θ^(−2i/8) = 10^(−i))
+    c, s = L.rope_freqs(1, 8, 1e4)
+    hand_c = [0.5403023058681398, 0.9950041652780258, 0.9999500004166653, 0.9999995000000417]
+    hand_s = [0.8414709848078965, 0.09983341664682815, 0.009999833334166664, 0.0009999998333333417]
+    assert np.allclose(c, hand_c, rtol=0, atol=1e-15) and np.allclose(s, hand_s, rtol=0, atol=1e-15)
+
+
 def test_kv_append_slot_and_grouped_split():
     Hq, Hkv, D, P = 4, 2, 4, 16
     G = Hq // Hkv

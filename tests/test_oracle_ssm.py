@@ -105,6 +105,21 @@ def test_gated_rmsnorm_constant_group_closed_form():
     assert np.all(L.gated_rmsnorm(y, np.zeros((m, n)), w, gs, 1e-5, act="f64") == 0)
 
 
+def test_gated_rmsnorm_two_groups_different_scales_hand_value():
+    """Pins the GROUPING of the gated RMSNorm (C1.13: groups of d_inner/G
+    contiguous channels, each normalised by its own RMS). z = 50 makes
+    silu(z) = 50 exactly in fp64. y = [3, 4, 1, 1] with groups of 2:
+    group [3, 4] has rms √12.5, group [1, 1] rms 1, so out = [3/√12.5,
+    4/√12.5, 1, 1]·w. Row-wise normalisation would give [1.1547, 1.5396,
+    0.3849, 0.3849]; interleaved groups ([3, 1], [4, 1]) other values."""
+    y = np.array([[3.0, 4.0, 1.0, 1.0]])
+    z = np.full((1, 4), 50.0)
+    w = np.array([1.0, 2.0, 3.0, 4.0])
+    out = L.gated_rmsnorm(y, z, w, 2, 1e-5, act="f64")
+    hand = np.array([0.848528137423857, 1.131370849898476 * 2, 1.0 * 3, 1.0 * 4])
+    assert np.allclose(out[0], hand, rtol=1e-8, atol=0)  # eps = 1e-5 against ms ≥ 2500: < 2e-9 relative
+
+
 def test_hybrid_zero_output_projections_pass_residual_and_advance_states():
     cfg = synth.TINY_HYBRID.with_(n_micro=1)
     inp = synth.make_decoder_inputs(cfg)
