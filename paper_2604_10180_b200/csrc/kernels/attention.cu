@@ -404,19 +404,23 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
           if (d0 == 0) P.part_lse[pi] = L > 0.f ? s_M[h] + log2f(L) : -INFINITY;
         }
       }
+      // every lane fences its own partial stores at gpu scope before lane 0's
+      // release-add publishes them (PTX memory model: a bar.warp.sync is not a
+      // documented morally-strong barrier, so cumulativity through it is not
+      // relied on)
+      if (!single) __threadfence();
       __syncwarp();
       if (lane == 0) mbar_arrive(&cempty[cs]);
       bool done = true;
       if (!single) {
         unsigned prev = 0;
-        // the acq_rel add releases this warp's partial (its stores are ordered
-        // before lane 0's add by the __syncwarp above: release is cumulative)
-        // and acquires the other splits' partials for the last arriver; the
-        // __syncwarp after it orders the other lanes' loads behind lane 0
+        // the acq_rel add releases this warp's (fenced) partial and acquires
+        // the other splits' partials for the last arriver
         if (lane == 0) prev = atom_add_acq_rel_gpu(&P.counter[unit], 1u);
         done = __shfl_sync(0xffffffffu, prev, 0) == (unsigned)P.splits - 1;
         if (done) {
           __syncwarp();
+          fence_acq_rel_gpu();  // each lane: its partial loads below are ordered after lane 0's acquire
           const float* lse = P.part_lse + (size_t)unit * P.splits * G;  // [split][G]
           const float* po = P.part_o + (size_t)unit * P.splits * G * D;  // [split][G][D]
           const int nl = P.splits * G, n_e4 = G * D / 4;

@@ -422,7 +422,10 @@ __global__ void step_begin_kernel2(unsigned* epoch, PeerSlots ps, int n_peers) {
   for (int p = 0; p < n_peers; ++p) {
     long long spins = 0;
     while (ld_acquire_sys(ps.mine[p]) < e) {
-      if (++spins > (1ll << 34)) break;  // watchdog (~tens of seconds); surfaces as a stuck step
+      if (++spins > (1ll << 28)) {  // watchdog (~20 s): record (KD_ERR_TIMEOUT at kd_runtime_check) and give up
+        atomicExch(epoch + 1, 3u);  // the error word follows the epoch word in the control block
+        break;
+      }
       __nanosleep(64);
     }
   }

@@ -57,6 +57,7 @@ struct Args {
   int groups, tpg;
   const int* meta;
   int dbg;                    // debug A/B knob (KD_GEMM_DBG): 1 skip owner Y stores, 2 skip owner fold
+  unsigned* err;              // runtime error word (nullable): set to 2 when the fold barrier times out
 };
 
 #define KD_TRACE(slot) \
@@ -457,7 +458,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       KD_TRACE(18);
       fence_acq_rel_gpu();
       atom_add_acq_rel_gpu(arrive, 1u);
+      // watchdog: the barrier needs all G CTAs co-resident (G = the device's
+      // SM count, 1 CTA/SM); if that ever fails, record and give up rather
+      // than hang (KD_ERR_TIMEOUT at kd_runtime_check; the output is invalid)
+      long long spins = 0;
       while (ld_acquire_gpu(arrive) < (unsigned)G) {
+        if (++spins > (1ll << 28)) {
+          if (A.err) atomicExch(A.err, 2u);
+          break;
+        }
       }
       KD_TRACE(16);
       if (atom_add_acq_rel_gpu(depart, 1u) == (unsigned)G - 1) {
@@ -619,6 +628,7 @@ struct Args {
   float eps;
   unsigned* bar;                // 2 self-resetting words (scratch)
   float* ssq;                   // [M][gridDim.x] per-CTA partial Σr² (scratch)
+  unsigned* err;                // runtime error word (nullable): set to 2 when the grid barrier times out
 };
 
 // a5 fused into the QKV GEMM epilogue. W rows are pair-interleaved within each
@@ -867,7 +877,14 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
     // the bar.sync: release is cumulative); polls back off to keep the line
     // free for the other CTAs' arrivals
     atom_add_acq_rel_gpu(A.bar, 1u);
-    while (ld_acquire_gpu(A.bar) < (unsigned)G) __nanosleep(64);
+    long long spins = 0;  // watchdog as in the stream-K fold barrier
+    while (ld_acquire_gpu(A.bar) < (unsigned)G) {
+      if (++spins > (1ll << 24)) {
+        if (A.err) atomicExch(A.err, 2u);
+        break;
+      }
+      __nanosleep(64);
+    }
     KD_TRACE(14);
     KD_CTRACE(23);
   }
@@ -1302,6 +1319,20 @@ struct Geometry {
   long long units;
 };
 
+// SMs of the current device (MIG / green contexts can expose fewer than 148):
+// the stream-K grid is one CTA per SM and its fold barrier needs every CTA
+// co-resident, so the grid comes from the device, not a constant (148 when no
+// device is visible, e.g. host-only planning)
+static int device_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      n <= 0) {
+    cudaGetLastError();
+    return kNumSMs;
+  }
+  return n;
+}
+
 static kd_status geometry(const GemmShape& a, Geometry* g, int sms) {
   if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "gemm: only bf16 (fp32 path not built)");
   if (a.M == 0 || a.N == 0 || a.K == 0 || a.rows_total == 0) return fail(KD_ERR_INVALID_ARG, "gemm: empty shape");
@@ -1440,7 +1471,7 @@ static kd_status choose(const GemmShape& a, GemmTile* t, double* best_ns) {
 
 static double streamk_ns(const GemmShape& a) {
   Geometry g;
-  if (geometry(a, &g, kNumSMs)) return 1e30;
+  if (geometry(a, &g, device_sms())) return 1e30;
   const double w = (double)a.N * a.K * 2;
   return w / csk::kHbmBps * 1e9 + (g.max_contrib <= 3 ? 2000.0 : 6000.0);
 }
@@ -1550,7 +1581,7 @@ kd_status gemm_scratch_bytes(const GemmShape& a, uint64_t* bytes) {
     return KD_OK;
   }
   gemm::Geometry g;
-  kd_status s = gemm::geometry(a, &g, kNumSMs);
+  kd_status s = gemm::geometry(a, &g, gemm::device_sms());
   if (s) return s;
   if (2ull * g.tiles > kMaxCounters) return fail(KD_ERR_UNSUPPORTED, "gemm: too many output tiles");
   uint64_t n = kScratchCounterBytes + (uint64_t)g.tiles * g.max_contrib * a.M * gemm::kBM * 4;
@@ -1570,7 +1601,7 @@ kd_status gemm_prepare(const GemmShape& a, const void* X, const void* W, const v
     return KD_OK;
   }
   gemm::Geometry g;
-  kd_status s = gemm::geometry(a, &g, kNumSMs);
+  kd_status s = gemm::geometry(a, &g, gemm::device_sms());
   if (s) return s;
   if (!X || !W || (a.groups && !meta)) return fail(KD_ERR_INVALID_ARG, "gemm: NULL operand");
   if (((uintptr_t)X | (uintptr_t)W) & 15) return fail(KD_ERR_INVALID_ARG, "gemm: operands must be 16-byte aligned");
@@ -1620,6 +1651,7 @@ static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx&
     return fail(KD_ERR_INVALID_ARG, "gemm_rmsnorm: scratch, r and gamma are required");
   if (A.norm && t.tiles * t.split > kNormMaxGrid) return fail(KD_ERR_UNSUPPORTED, "gemm_rmsnorm: grid too large");
   A.epi = c.epi;
+  A.err = c.err;
   A.trace = g_gemm_trace;
   kd_status ks = kernels_init();
   if (ks) return ks;
@@ -1640,7 +1672,7 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   }
   if (gp.dense) return launch_gemm_dense(gp, Y, c, signals);
   gemm::Geometry g;
-  kd_status s = gemm::geometry(gp.sh, &g, kNumSMs);
+  kd_status s = gemm::geometry(gp.sh, &g, gemm::device_sms());
   if (s) return s;
   if (!Y) return fail(KD_ERR_INVALID_ARG, "gemm: NULL output");
   if (g.max_contrib > 1 && !c.scratch) return fail(KD_ERR_INVALID_ARG, "gemm: scratch required");
@@ -1668,6 +1700,7 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   A.max_contrib = g.max_contrib;
   A.units = g.units;
   A.epi = c.epi;
+  A.err = c.err;
   A.trace = g_gemm_trace;
   {
     static int dbg = -1;
@@ -1694,7 +1727,7 @@ extern "C" kd_status kd_gemm_tiling(uint32_t M, uint32_t N, uint32_t K, int32_t*
   a.dtype = KD_BF16;
   const kd::GemmShape sh = kd::gemm_shape(a);
   kd::gemm::Geometry g;
-  kd_status gs = kd::gemm::geometry(sh, &g, kd::kNumSMs);  // shape validation
+  kd_status gs = kd::gemm::geometry(sh, &g, kd::gemm::device_sms());  // shape validation
   if (gs) return gs;
   if (!kd::gemm::use_dense(sh)) {
     out[0] = 0;
@@ -1738,7 +1771,7 @@ kd_status gemm_signals(const GemmShape& a, uint32_t* s) {
     return KD_OK;
   }
   gemm::Geometry g;
-  kd_status st = gemm::geometry(a, &g, kNumSMs);
+  kd_status st = gemm::geometry(a, &g, gemm::device_sms());
   if (st) return st;
   // one flag increment per CTA, after its whole tiles and its fold slice
   *s = (uint32_t)g.grid;

@@ -14,6 +14,7 @@ struct LaunchCtx {
   cudaStream_t stream = nullptr;
   void* scratch = nullptr;   // zero-initialised device scratch (left zeroed)
   Epi epi;                   // fused peer stores of the primary output
+  unsigned* err = nullptr;   // runtime error word (device; nullable): in-kernel watchdogs record timeouts here
 };
 
 kd_status set_cuda_error(cudaError_t e, const char* where);

@@ -499,6 +499,7 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
         ++l.ctx.epi.n;
       }
       l.ctx.scratch = d.ws + L.scratch_off;
+      l.ctx.err = (unsigned*)(d.ws + L.ctrl_off + 4);
       if (K.op == KD_OP_GROUPED_GEMM) {
         l.gemm = new GemmPlan();
         kd_status s3 = gemm_prepare(gemm_shape(attrs_get<kd_attr_grouped_gemm>(K)), l.rd[0], l.rd[1], l.rd[2], l.gemm);
@@ -591,7 +592,11 @@ kd_status kd_runtime_check(kd_runtime* rt) {
     unsigned err = 0;
     KD_CUDA_CHECK(cudaMemcpy(&err, d.ws + rt->plan->layout[d.logical].ctrl_off + 4, 4, cudaMemcpyDeviceToHost),
                   "read error word");
-    if (err) return fail(KD_ERR_TIMEOUT, "kd_runtime_check: a flag wait timed out on device " + std::to_string(d.logical));
+    if (err) {
+      const char* what = err == 2 ? "an in-kernel grid barrier" : err == 3 ? "the step-begin barrier" : "a flag wait";
+      return fail(KD_ERR_TIMEOUT, std::string("kd_runtime_check: ") + what + " timed out on device " +
+                                      std::to_string(d.logical));
+    }
   }
   return KD_OK;
 }

@@ -430,8 +430,9 @@ T_ATTN_SHARD = 32  # template ids 32 + s: attention (and, for the last shard, Ro
 
 class ShardedKVDecoderGraph:
     """Long-context decode with every sequence's KV cache split over S
-    memory-role devices ("the KV cache ... can be
-    partitioned"): shard s holds tokens [s·T, (s+1)·T) (T = C/S, a page
+    memory-role devices (SURVEY §8(f) f2's long-context proposal; this split
+    is NOT in the paper, whose cross-iteration buffers are instead replicated
+    per GPU with asynchronous delta transfers): shard s holds tokens [s·T, (s+1)·T) (T = C/S, a page
     multiple) in its own paged pool; each shard's attention returns its
     normalised partial and base-2 log-sum-exp (KD_ATTN_LSE), a merge kernel
     combines them in shard order (KD_OP_ATTN_MERGE); RoPE/append writes the new
