@@ -347,10 +347,15 @@ def main():
                       "stream, averaged over K profiled steps run right after the timed region"}
     tr_path = os.path.join(ROOT, "profiles", "attention_traffic.json")
     if os.path.exists(tr_path):
-        try:  # ncu dram bytes of the same launch shape (profiles/), else null
+        # ncu dram bytes of the same launch shape (profiles/), ONLY if captured
+        # from the kernel sources this build compiled (sha256 stamp), else null
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "scripts"))
+            from attention_traffic import source_sha256
             tr = json.load(open(tr_path))
-            if tr.get("algorithmic_bytes_per_launch") == attn_bytes:
+            if tr.get("algorithmic_bytes_per_launch") == attn_bytes and tr.get("source_sha256") == source_sha256():
                 roof["traffic"] = tr.get("bytes_per_launch")
+                roof["traffic_source"] = tr.get("source")
         except Exception:
             pass
 
