@@ -292,12 +292,38 @@ typedef struct {
   int64_t issue_ps, arrival_ps; /* simulated */
 } kd_transfer;
 
+/* n_chunks (1..8): chunks per transfer along the consumer's streamable axis
+ * (reading R10; the paper streams whole buffers). */
 kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* assign,
-                         uint32_t n_micro, kd_plan** out);
+                         uint32_t n_micro, uint32_t n_chunks, kd_plan** out);
 void kd_plan_destroy(kd_plan* p);
 kd_status kd_plan_schedule(const kd_plan* p, kd_sched_entry* out, uint32_t cap, uint32_t* n);
 kd_status kd_plan_transfers(const kd_plan* p, kd_transfer* out, uint32_t cap, uint32_t* n);
 kd_status kd_plan_makespan(const kd_plan* p, int64_t* ps);
+/* Chunk table (R10; the a13 handoff). Every transfer's data — the producer's
+ * primary output — is viewed as [rows][row_bytes] and each row is cut into
+ * column chunks: q = ⌈⌈row_bytes/unit⌉/n_chunks⌉·unit, chunk c = [c·q,
+ * min((c+1)·q, row_bytes)), empty chunks dropped. unit = the lcm of the chunk
+ * units of the producer's remote chunk-aware consumers (a GEMM's 64·kbs-column
+ * k-block, SiLU·mul's 128-column gate/up block, RoPE/append's kv group of
+ * (G+2)·D columns, add+RMSNorm's 8 columns), or the whole row without one.
+ * count_mode = 1: the producer releases chunk c's flag by the bytes it stored
+ * there (complete at rows·(end − begin) per step) and a chunk-aware consumer
+ * acquires chunk c right before reading it, inside its kernel, while later
+ * chunks are still produced. count_mode = 0 (outputs that are not a dense
+ * [rows][cols] block written once: MoE dispatch/grouped GEMM, SSM, fp32, LSE
+ * partials, QKV+RoPE): one chunk, released once per signalling CTA. Entries
+ * are ordered by (transfer, chunk); if cap is too small → KD_ERR_RANGE with
+ * *n = required. */
+typedef struct {
+  uint32_t transfer;    /* index into kd_plan_transfers */
+  uint32_t chunk;       /* ascending within the transfer */
+  uint32_t count_mode;  /* 1: byte-count release per chunk; 0: per-CTA release, one chunk */
+  uint32_t pad_;
+  uint64_t rows, row_bytes, unit;
+  uint64_t begin, end;  /* byte range within every row */
+} kd_chunk;
+kd_status kd_plan_chunks(const kd_plan* p, kd_chunk* out, uint32_t cap, uint32_t* n);
 /* Device workspace the runtime carves into activations, landing slots,
  * flags and kernel scratch. Must be ZERO-initialised once by the caller. */
 kd_status kd_plan_workspace_bytes(const kd_plan* p, uint32_t dev, uint64_t* bytes);
@@ -316,7 +342,7 @@ typedef struct kd_runtime kd_runtime;
 enum {
   KD_MODE_DISAGG = 0,       /* default: execute the plan                                    */
   KD_MODE_NO_TRANSFER = 1,  /* ablation: peer stores and waits removed (exposed-transfer = DISAGG − this) */
-  KD_MODE_LOG = 2           /* record %globaltimer around every launch (kd_runtime_log)        */
+  KD_MODE_LOG = 2           /* DISAGG + per-chunk %globaltimer records (kd_runtime_log, kd_step_stats.wait) */
 };
 kd_status kd_runtime_create(const kd_plan* p, const uint32_t* local_devs, const int32_t* cuda_ordinal,
                             uint32_t n_local, kd_runtime** out);
@@ -332,10 +358,44 @@ kd_status kd_runtime_set_mode(kd_runtime* rt, uint32_t mode);
 kd_status kd_runtime_set_graph(kd_runtime* rt, int32_t enable);
 /* Resolves every pointer, encodes TMA descriptors, enables peer access. */
 kd_status kd_runtime_prepare(kd_runtime* rt);
-/* Enqueue one decode step on streams[j] for local device j (async). Device
- * errors (flag watchdog) surface at kd_runtime_check or the next kd_step. */
-kd_status kd_step(kd_runtime* rt, void* const* streams);
+/* Per-step statistics (filled by kd_step when `stats` is non-NULL; that call
+ * synchronises every local device). Times are ns; index j = local device j.
+ *  step_ns[j]: device time of the step on device j (CUDA events on its stream);
+ *  wait_ns[j]: KD_MODE_LOG only (else 0): Σ over device j's incoming (transfer,
+ *    chunk) of the first acquirer's stall (acquire − wait start) — the exposed
+ *    transfer time the consumer observed; chunk_waits[j] counts them;
+ *  link_bytes[u·n_dev + v]: bytes streamed u → v per step (the plan's transfers,
+ *    all logical devices; diagonal 0). */
+#define KD_STATS_MAX_DEV 8
+typedef struct {
+  uint64_t step_id;
+  uint32_t n_local, n_dev;
+  uint64_t step_ns[KD_STATS_MAX_DEV];
+  uint64_t wait_ns[KD_STATS_MAX_DEV];
+  uint32_t chunk_waits[KD_STATS_MAX_DEV];
+  uint64_t link_bytes[KD_STATS_MAX_DEV * KD_STATS_MAX_DEV];
+} kd_step_stats;
+/* Enqueue decode step `step_id` on streams[j] for local device j (async unless
+ * stats is non-NULL). step_id counts kd_step calls on this runtime from 0; the
+ * device epoch of the step (the value its flags are released to) is step_id + 1.
+ * A step_id other than the next one → KD_ERR_INVALID_ARG (steps are issued in
+ * order; UINT64_MAX = "the next one"). Device errors (flag / barrier
+ * watchdogs) surface at kd_runtime_check or the next kd_step. */
+kd_status kd_step(kd_runtime* rt, void* const* streams, uint64_t step_id, kd_step_stats* stats);
 kd_status kd_runtime_check(kd_runtime* rt);
+/* KD_MODE_LOG records of the last step (call after a sync), one per (incoming
+ * transfer, chunk) of every local device, ordered by (dev, transfer, chunk):
+ * epoch = the step's device epoch seen by the first consumer acquire (0 if not
+ * yet acquired), t_wait (that acquirer's wait start), t_acquire, t_release (the
+ * producer's last release into the chunk, %globaltimer ns — chunk complete).
+ * R10's "ascending consumption": every consumer acquires a transfer's chunks in
+ * ascending order. Errors: KD_ERR_STATE if the mode is not LOG, KD_ERR_RANGE
+ * with *n = required if cap is too small. */
+typedef struct {
+  uint32_t dev, transfer, chunk, pad_;
+  uint64_t epoch, t_wait, t_acquire, t_release;
+} kd_log_record;
+kd_status kd_runtime_log(kd_runtime* rt, kd_log_record* out, uint32_t cap, uint32_t* n);
 /* Number of kernel launches one kd_step enqueues on local device j. */
 kd_status kd_runtime_launch_count(const kd_runtime* rt, uint32_t j, uint32_t* n);
 /* Profiling: record CUDA events around every launch of `op` (0 = off) on the

@@ -117,3 +117,100 @@ def chunks(length: int, unit: int, n: int) -> List[Tuple[int, int]]:
         if a < b:
             out.append((a, b))
     return out
+
+
+# ---------------------------------------------------------------- chunk table (a2 / a13, R10)
+# Which producers stream per chunk ("COUNT" release: their primary output is a
+# dense bf16 [rows][cols] block written exactly once) and which consumers read
+# a remote input chunk by chunk, with the unit of their streamable axis
+# ("GEMM consumer → K chunks in 64-col multiples; attention
+# consumer of QKV → kv-group chunks; SiLU·mul consumer → 64-col blocks …;
+# RMSNorm consumer → column chunks"). Restated here from DESIGN.md's reading
+# R10, independently of the library. `op` is the kd.h op NAME, `a` the op's
+# attribute fields as a dict; BF16 = 0.
+
+def count_geometry(op, a):
+    """(rows, row_bytes) of a COUNT producer's primary output, else None."""
+    bf = a.get("dtype", 0) == 0
+    if op == "ADD_RMSNORM" and bf:
+        return a["rows"], 2 * a["hidden"]
+    if op in ("GEMM", "GEMM_SILU") and bf:
+        return a["M"], 2 * (a["N"] // 2 if op == "GEMM_SILU" else a["N"])
+    if op == "GEMM_RMSNORM" and bf:
+        return a["M"], 2 * a["N"]
+    if op == "ROPE_APPEND" and bf:
+        return a["rows"], 2 * a["n_heads"] * a["head_dim"]
+    if op == "ATTENTION" and bf and not (a["flags"] & 1):
+        return a["rows"], 2 * a["n_heads"] * a["head_dim"]
+    if op == "ATTN_MERGE":
+        return a["rows"], 2 * a["n_heads"] * a["head_dim"]
+    if op == "SILU_MUL" and bf:
+        return a["rows"], 2 * a["ffn"]
+    return None
+
+
+def consumer_unit(op, a, ri, row_bytes):
+    """Chunk unit in bytes consumer `op` needs on read ri, 0 if not chunk-aware."""
+    if a.get("dtype", 0) != 0:
+        return 0
+    kblock = lambda m: (2 if (m + 15) // 16 * 16 <= 128 else 1) * 64 * 2
+    if op in ("GEMM", "GEMM_SILU", "GEMM_RMSNORM"):
+        return kblock(a["M"]) if ri == 0 and 2 * a["K"] == row_bytes else 0
+    if op == "QKV_ROPE":
+        return kblock(a["rows"]) if ri == 0 and 2 * a["hidden"] == row_bytes else 0
+    if op in ("ADD_RMSNORM", "RESIDUAL_ADD"):
+        return 16 if 1 <= ri <= a["n_delta"] and 2 * a["hidden"] == row_bytes else 0
+    if op == "SILU_MUL":
+        return 256 if ri == 0 and 4 * a["ffn"] == row_bytes else 0
+    if op == "ROPE_APPEND":
+        if ri != 0 or 2 * (a["n_heads"] + 2 * a["n_kv_heads"]) * a["head_dim"] != row_bytes:
+            return 0
+        return 2 * (a["n_heads"] // a["n_kv_heads"] + 2) * a["head_dim"]
+    return 0
+
+
+def chunk_table(kernels, edges, assign, transfers, n_chunks):
+    """Chunk table of a plan: for every transfer (micro, producer, dst, ...) in
+    plan order, (count_mode, rows, row_bytes, unit, [(begin, end), ...]).
+    kernels[k] = (op_name, attrs_dict, reads[(buf, off, len)], writes[...]).
+    The unit of a producer is the lcm of the units of its remote chunk-aware
+    consumers — reads of exactly its primary output, every byte of which it
+    wrote — capped at the row; chunks follow `chunks` (R10)."""
+    from math import gcd
+    srcs: Dict[Tuple[int, int], set] = {}
+    for s, d, buf, _off, _ln in edges:
+        srcs.setdefault((d, buf), set()).add(s)
+    unit_of: Dict[int, int] = {}
+    for k, (op, a, reads, _w) in enumerate(kernels):
+        for ri, (buf, off, ln) in enumerate(reads):
+            ps = srcs.get((k, buf))
+            if not ps or len(ps) != 1:
+                continue
+            src = next(iter(ps))
+            if assign[src] == assign[k]:
+                continue
+            pop, pa, _pr, pw = kernels[src]
+            geo = count_geometry(pop, pa)
+            if geo is None or not pw:
+                continue
+            rows, rb = geo
+            if (buf, off, ln) != tuple(pw[0]) or rows * rb != pw[0][2]:
+                continue
+            u = consumer_unit(op, a, ri, rb)
+            if u:
+                cur = unit_of.get(src, 0)
+                unit_of[src] = u if cur == 0 else cur // gcd(cur, u) * u
+    out = []
+    for (_i, prod, _dst, *_rest) in transfers:
+        pop, pa, _pr, pw = kernels[prod]
+        ln = pw[0][2] if pw else 0
+        geo = count_geometry(pop, pa)
+        if geo is not None and geo[0] * geo[1] == ln and geo[1] > 0:
+            rows, rb = geo
+            u = unit_of.get(prod, rb)
+            u = rb if u > rb else u
+            out.append((1, rows, rb, u, chunks(rb, u, n_chunks)))
+        else:
+            L = max(ln, 1)
+            out.append((0, 1, L, L, [(0, L)]))
+    return out

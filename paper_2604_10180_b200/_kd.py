@@ -144,6 +144,27 @@ class kd_transfer(C.Structure):
                 ("bytes", C.c_uint64), ("issue_ps", C.c_int64), ("arrival_ps", C.c_int64)]
 
 
+class kd_chunk(C.Structure):
+    _fields_ = [("transfer", C.c_uint32), ("chunk", C.c_uint32), ("count_mode", C.c_uint32), ("pad_", C.c_uint32),
+                ("rows", C.c_uint64), ("row_bytes", C.c_uint64), ("unit", C.c_uint64), ("begin", C.c_uint64),
+                ("end", C.c_uint64)]
+
+
+KD_STATS_MAX_DEV = 8
+
+
+class kd_step_stats(C.Structure):
+    _fields_ = [("step_id", C.c_uint64), ("n_local", C.c_uint32), ("n_dev", C.c_uint32),
+                ("step_ns", C.c_uint64 * KD_STATS_MAX_DEV), ("wait_ns", C.c_uint64 * KD_STATS_MAX_DEV),
+                ("chunk_waits", C.c_uint32 * KD_STATS_MAX_DEV),
+                ("link_bytes", C.c_uint64 * (KD_STATS_MAX_DEV * KD_STATS_MAX_DEV))]
+
+
+class kd_log_record(C.Structure):
+    _fields_ = [("dev", C.c_uint32), ("transfer", C.c_uint32), ("chunk", C.c_uint32), ("pad_", C.c_uint32),
+                ("epoch", C.c_uint64), ("t_wait", C.c_uint64), ("t_acquire", C.c_uint64), ("t_release", C.c_uint64)]
+
+
 P = C.c_void_p
 u32, i32, u64, i64 = C.c_uint32, C.c_int32, C.c_uint64, C.c_int64
 PU32, PI32, PU64, PI64 = C.POINTER(u32), C.POINTER(i32), C.POINTER(u64), C.POINTER(i64)
@@ -164,7 +185,8 @@ _PROTOS = {
     "kd_objective": (kd_status, [P, C.POINTER(kd_machine), PI32, u32, u32, PI64, PI64, PI64]),
     "kd_place": (kd_status, [P, C.POINTER(kd_machine), C.POINTER(kd_place_opts), PI32, PI64, PU64]),
     "kd_chunks": (kd_status, [u64, u64, u32, PU64, u32, PU32]),
-    "kd_plan_create": (kd_status, [P, C.POINTER(kd_machine), PI32, u32, C.POINTER(P)]),
+    "kd_plan_create": (kd_status, [P, C.POINTER(kd_machine), PI32, u32, u32, C.POINTER(P)]),
+    "kd_plan_chunks": (kd_status, [P, C.POINTER(kd_chunk), u32, PU32]),
     "kd_plan_destroy": (None, [P]),
     "kd_plan_schedule": (kd_status, [P, C.POINTER(kd_sched_entry), u32, PU32]),
     "kd_plan_transfers": (kd_status, [P, C.POINTER(kd_transfer), u32, PU32]),
@@ -179,7 +201,8 @@ _PROTOS = {
     "kd_runtime_set_mode": (kd_status, [P, u32]),
     "kd_runtime_set_graph": (kd_status, [P, i32]),
     "kd_runtime_prepare": (kd_status, [P]),
-    "kd_step": (kd_status, [P, C.POINTER(P)]),
+    "kd_step": (kd_status, [P, C.POINTER(P), u64, C.POINTER(kd_step_stats)]),
+    "kd_runtime_log": (kd_status, [P, C.POINTER(kd_log_record), u32, PU32]),
     "kd_runtime_check": (kd_status, [P]),
     "kd_runtime_launch_count": (kd_status, [P, u32, PU32]),
     "kd_runtime_profile_op": (kd_status, [P, u32]),

@@ -26,6 +26,9 @@ class Graph:
         check(K.kd_graph_create(C.byref(h)), "kd_graph_create")
         self.h = h
         self._keep = []
+        # the declarations as given (op, reads, writes, attrs): introspection
+        # for tests that restate the plan's rules independently
+        self.decl = []
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -50,6 +53,7 @@ class Graph:
             d.attrs_size = C.sizeof(attrs)
         i = C.c_uint32()
         check(K.kd_graph_add_kernel(self.h, C.byref(d), C.byref(i)), "kd_graph_add_kernel")
+        self.decl.append((op, [tuple(x) for x in reads], [tuple(x) for x in writes], attrs))
         return i.value
 
     def finalize(self):
@@ -147,14 +151,23 @@ def chunks(length: int, unit: int, n: int):
 
 
 class Plan:
-    def __init__(self, g: Graph, m: Machine, assign: Sequence[int], n_micro: int):
+    def __init__(self, g: Graph, m: Machine, assign: Sequence[int], n_micro: int, n_chunks: int = 4):
         self.g, self.m = g, m
         a = (C.c_int32 * len(assign))(*assign)
         h = C.c_void_p()
-        check(K.kd_plan_create(g.h, C.byref(m.m), a, n_micro, C.byref(h)), "kd_plan_create")
+        check(K.kd_plan_create(g.h, C.byref(m.m), a, n_micro, n_chunks, C.byref(h)), "kd_plan_create")
         self.h = h
         self.assign = list(assign)
         self.n_micro = n_micro
+        self.n_chunks = n_chunks
+
+    def chunks(self):
+        """Chunk table: [(transfer, chunk, count_mode, rows, row_bytes, unit, begin, end)]."""
+        n = C.c_uint32()
+        K.kd_plan_chunks(self.h, None, 0, C.byref(n))
+        arr = (K.kd_chunk * max(1, n.value))()
+        check(K.kd_plan_chunks(self.h, arr, n.value, C.byref(n)), "kd_plan_chunks")
+        return [(c.transfer, c.chunk, c.count_mode, c.rows, c.row_bytes, c.unit, c.begin, c.end) for c in arr[:n.value]]
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -225,9 +238,29 @@ class Runtime:
     def prepare(self):
         check(K.kd_runtime_prepare(self.h), "kd_runtime_prepare")
 
-    def step(self, streams: Sequence[int]):
+    def step(self, streams: Sequence[int], step_id: Optional[int] = None, stats: bool = False):
+        """One decode step (async). stats=True synchronises and returns
+        kd_step_stats as a dict (step_ns / wait_ns / chunk_waits per local
+        device, link_bytes[u][v])."""
         arr = (C.c_void_p * len(streams))(*[C.c_void_p(int(s)) for s in streams])
-        check(K.kd_step(self.h, arr), "kd_step")
+        sid = (1 << 64) - 1 if step_id is None else int(step_id)
+        st = K.kd_step_stats() if stats else None
+        check(K.kd_step(self.h, arr, sid, C.byref(st) if stats else None), "kd_step")
+        if not stats:
+            return None
+        nl, nd = st.n_local, st.n_dev
+        return {"step_id": st.step_id, "step_ns": list(st.step_ns[:nl]), "wait_ns": list(st.wait_ns[:nl]),
+                "chunk_waits": list(st.chunk_waits[:nl]),
+                "link_bytes": [[st.link_bytes[u * nd + v] for v in range(nd)] for u in range(nd)]
+                if nd <= K.KD_STATS_MAX_DEV else None}
+
+    def log(self):
+        """KD_MODE_LOG records of the last step: [(dev, transfer, chunk, epoch, t_wait, t_acquire, t_release)]."""
+        n = C.c_uint32()
+        K.kd_runtime_log(self.h, None, 0, C.byref(n))
+        arr = (K.kd_log_record * max(1, n.value))()
+        check(K.kd_runtime_log(self.h, arr, n.value, C.byref(n)), "kd_runtime_log")
+        return [(r.dev, r.transfer, r.chunk, r.epoch, r.t_wait, r.t_acquire, r.t_release) for r in arr[:n.value]]
 
     def check(self):
         check(K.kd_runtime_check(self.h), "kd_runtime_check")

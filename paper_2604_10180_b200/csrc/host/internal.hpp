@@ -22,6 +22,7 @@ using u128 = unsigned __int128;
 inline u64 ceil_div_u128(u128 a, u128 b) { return (u64)((a + b - 1) / b); }
 inline u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
 constexpr u64 kPs = 1000000000000ull;
+constexpr uint32_t kMaxPlanChunks = 8;  // chunks per transfer (= kMaxChunks of the device code)
 
 struct Span {
   uint32_t buf;
@@ -65,6 +66,13 @@ bool machine_valid(const kd_machine* m);
 // d_ij aggregated per (src,dst) pair
 std::vector<std::pair<std::pair<uint32_t, uint32_t>, u64>> edge_pairs(const kd_graph& g);
 i64 edge_cost(const kd_machine& m, u64 bytes, uint32_t u, uint32_t v);
+// a13 op knowledge (plan.cpp): the primary output of a COUNT-release producer
+// as rows × row_bytes (false: CTA release — irregular or dynamic outputs)
+bool op_count_geometry(const Kernel& k, u64* rows, u64* row_bytes);
+// chunk unit (bytes along a row) the consumer k needs on read span ri when it
+// acquires that input chunk by chunk inside the kernel; 0 = not chunk-aware
+// (the runtime then waits for the whole transfer before launching it)
+u64 op_consumer_unit(const Kernel& k, uint32_t ri, u64 row_bytes);
 }  // namespace kd
 
 struct kd_plan {
@@ -73,17 +81,30 @@ struct kd_plan {
   std::vector<int32_t> assign;
   std::vector<kd_sched_entry> sched;   // global order
   std::vector<kd_transfer> transfers;  // sorted by (micro, producer, dst_dev)
+  // chunk table per transfer (R10): the producer's primary output as
+  // [rows][row_bytes], each row cut into column chunks [begin, end) along the
+  // chunk-aware consumers' streamable axis (unit = lcm of their units)
+  struct XChunks {
+    bool count = false;       // COUNT release (bytes per chunk) vs CTA release (1 chunk)
+    kd::u64 rows = 1, row_bytes = 0, unit = 0;
+    std::vector<std::pair<kd::u64, kd::u64>> ch;
+  };
+  std::vector<XChunks> xchunks;
+  uint32_t n_chunks = 1;
   kd::i64 makespan = 0;
   // workspace layout per device
   struct Layout {
-    kd::u64 ctrl_off = 0, ctrl_bytes = 0;      // epoch + barrier words
-    kd::u64 flags_off = 0, flags_bytes = 0;    // one u32 per incoming transfer (padded)
+    kd::u64 ctrl_off = 0, ctrl_bytes = 0;      // epoch + error word + barrier words
+    kd::u64 flags_off = 0, flags_bytes = 0;    // per incoming transfer: u64 flag per chunk + u64 residency counter
+    kd::u64 log_off = 0, log_bytes = 0;        // per incoming transfer: kLogWords u64 per chunk (KD_MODE_LOG)
     kd::u64 scratch_off = 0, scratch_bytes = 0;
     kd::u64 total = 0;
     // (buf, micro) -> offset of the local activation instance
     std::map<std::pair<uint32_t, uint32_t>, kd::u64> act;
-    // transfer index -> (landing offset, flag offset)
+    // transfer index -> (landing offset, flag offset); the residency counter
+    // follows the chunk flags; log records at xlog[t]
     std::map<uint32_t, std::pair<kd::u64, kd::u64>> landing;
+    std::map<uint32_t, kd::u64> xlog;
   };
   std::vector<Layout> layout;
   // external binding need [buf][dev]

@@ -13,15 +13,134 @@ namespace kd {
 kd_status op_scratch_bytes(uint32_t op, const std::vector<uint8_t>& attrs, u64* bytes);  // ops.cu
 
 static u64 align_up(u64 x, u64 a) { return (x + a - 1) / a * a; }
+
+template <typename T>
+static bool attrs_as(const Kernel& k, T* a) {
+  if (k.attrs.size() != sizeof(T)) return false;
+  std::memcpy(a, k.attrs.data(), sizeof(T));
+  return true;
+}
+
+// Producers whose primary output is a dense bf16 [rows][cols] block written
+// exactly once per step release per chunk in bytes (COUNT); the device code
+// of each (elementwise.cu, attention.cu, gemm.cu) tallies its stores the
+// same way. Everything else releases once per signalling CTA.
+bool op_count_geometry(const Kernel& k, u64* rows, u64* row_bytes) {
+  switch (k.op) {
+    case KD_OP_ADD_RMSNORM: {
+      kd_attr_add_rmsnorm a;
+      if (!attrs_as(k, &a) || a.dtype != KD_BF16) return false;
+      *rows = a.rows, *row_bytes = 2ull * a.hidden;
+      return true;
+    }
+    case KD_OP_GEMM:
+    case KD_OP_GEMM_SILU: {
+      kd_attr_gemm a;
+      if (!attrs_as(k, &a) || a.dtype != KD_BF16) return false;
+      *rows = a.M, *row_bytes = 2ull * (k.op == KD_OP_GEMM_SILU ? a.N / 2 : a.N);
+      return true;
+    }
+    case KD_OP_GEMM_RMSNORM: {
+      kd_attr_gemm_rmsnorm a;
+      if (!attrs_as(k, &a) || a.dtype != KD_BF16) return false;
+      *rows = a.M, *row_bytes = 2ull * a.N;
+      return true;
+    }
+    case KD_OP_ROPE_APPEND: {
+      kd_attr_rope_append a;
+      if (!attrs_as(k, &a) || a.dtype != KD_BF16) return false;
+      *rows = a.rows, *row_bytes = 2ull * a.n_heads * a.head_dim;
+      return true;
+    }
+    case KD_OP_ATTENTION: {
+      kd_attr_attention a;
+      if (!attrs_as(k, &a) || a.dtype != KD_BF16 || (a.flags & KD_ATTN_LSE)) return false;
+      *rows = a.rows, *row_bytes = 2ull * a.n_heads * a.head_dim;
+      return true;
+    }
+    case KD_OP_ATTN_MERGE: {
+      kd_attr_attn_merge a;
+      if (!attrs_as(k, &a)) return false;
+      *rows = a.rows, *row_bytes = 2ull * a.n_heads * a.head_dim;
+      return true;
+    }
+    case KD_OP_SILU_MUL: {
+      kd_attr_silu_mul a;
+      if (!attrs_as(k, &a) || a.dtype != KD_BF16) return false;
+      *rows = a.rows, *row_bytes = 2ull * a.ffn;
+      return true;
+    }
+  }
+  return false;
+}
+
+// Consumer chunk units (SURVEY §8(a) a2 "chunk axis = consumer's streamable
+// axis"): a GEMM reads X by k-blocks of 64·kbs columns (kbs = 2 while the MMA
+// N ≤ 128); SiLU·mul reads 128-column gate/up blocks; RoPE/append reads a kv
+// group's (G+2)·D columns; add+RMSNorm and the residual add read 8-column
+// groups. The input row must be the producer's row (row_bytes).
+u64 op_consumer_unit(const Kernel& k, uint32_t ri, u64 row_bytes) {
+  switch (k.op) {
+    case KD_OP_GEMM:
+    case KD_OP_GEMM_SILU: {
+      kd_attr_gemm a;
+      if (ri != 0 || !attrs_as(k, &a) || a.dtype != KD_BF16 || 2ull * a.K != row_bytes) return 0;
+      return ((a.M + 15) / 16 * 16 <= 128 ? 2ull : 1ull) * 64 * 2;
+    }
+    case KD_OP_GEMM_RMSNORM: {
+      kd_attr_gemm_rmsnorm a;
+      if (ri != 0 || !attrs_as(k, &a) || a.dtype != KD_BF16 || 2ull * a.K != row_bytes) return 0;
+      return ((a.M + 15) / 16 * 16 <= 128 ? 2ull : 1ull) * 64 * 2;
+    }
+    case KD_OP_QKV_ROPE: {
+      kd_attr_qkv_rope a;
+      if (ri != 0 || !attrs_as(k, &a) || a.dtype != KD_BF16 || 2ull * a.hidden != row_bytes) return 0;
+      return ((a.rows + 15) / 16 * 16 <= 128 ? 2ull : 1ull) * 64 * 2;
+    }
+    case KD_OP_ADD_RMSNORM: {
+      kd_attr_add_rmsnorm a;
+      if (!attrs_as(k, &a) || a.dtype != KD_BF16 || ri < 1 || ri > a.n_delta || 2ull * a.hidden != row_bytes) return 0;
+      return 16;
+    }
+    case KD_OP_RESIDUAL_ADD: {
+      kd_attr_residual_add a;
+      if (!attrs_as(k, &a) || a.dtype != KD_BF16 || ri < 1 || ri > a.n_delta || 2ull * a.hidden != row_bytes) return 0;
+      return 16;
+    }
+    case KD_OP_SILU_MUL: {
+      kd_attr_silu_mul a;
+      if (ri != 0 || !attrs_as(k, &a) || a.dtype != KD_BF16 || 4ull * a.ffn != row_bytes) return 0;
+      return 256;
+    }
+    case KD_OP_ROPE_APPEND: {
+      kd_attr_rope_append a;
+      if (ri != 0 || !attrs_as(k, &a) || a.dtype != KD_BF16 || a.n_kv_heads == 0) return 0;
+      if (2ull * (a.n_heads + 2ull * a.n_kv_heads) * a.head_dim != row_bytes) return 0;
+      return 2ull * (a.n_heads / a.n_kv_heads + 2) * a.head_dim;
+    }
+  }
+  return 0;
+}
+
+static u64 gcd_u64(u64 a, u64 b) {
+  while (b) {
+    u64 t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
 }  // namespace kd
 
 extern "C" {
 
 kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* assign, uint32_t n_micro,
-                         kd_plan** out) {
+                         uint32_t n_chunks, kd_plan** out) {
   if (!g || !assign || !out) return fail(KD_ERR_INVALID_ARG, "kd_plan_create: NULL argument");
   if (!g->finalized) return fail(KD_ERR_STATE, "kd_plan_create: graph not finalized");
   if (!machine_valid(m) || n_micro == 0) return fail(KD_ERR_INVALID_ARG, "kd_plan_create: bad machine/n_micro");
+  if (n_chunks == 0 || n_chunks > kMaxPlanChunks)
+    return fail(KD_ERR_INVALID_ARG, "kd_plan_create: n_chunks must be 1.." + std::to_string(kMaxPlanChunks));
   const uint32_t K = (uint32_t)g->kernels.size(), n = m->n_dev, N = n_micro;
   for (uint32_t k = 0; k < K; ++k)
     if (assign[k] < 0 || (uint32_t)assign[k] >= n) return fail(KD_ERR_INVALID_ARG, "kd_plan_create: bad assign");
@@ -46,6 +165,7 @@ kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* 
   p->g = g;
   p->n_dev = n;
   p->n_micro = N;
+  p->n_chunks = n_chunks;
   p->assign.assign(assign, assign + K);
 
   // predecessors and transfers (producer k, remote device d) = union of spans (R3)
@@ -153,6 +273,59 @@ kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* 
         p->transfers.push_back(tr);
       }
 
+  // ---- chunk tables (R10): per producer, the unit is the lcm of its remote
+  // chunk-aware consumers' units (reads of its whole primary output whose
+  // bytes all come from it); every transfer of a producer shares the table
+  {
+    std::map<uint32_t, u64> unit_of;  // producer -> lcm unit (bytes)
+    std::map<std::pair<uint32_t, uint32_t>, std::set<uint32_t>> srcs;  // (consumer, buf) -> producers
+    for (const auto& e : g->edges) srcs[{e.dst, e.buf}].insert(e.src);
+    for (uint32_t k = 0; k < K; ++k) {
+      const Kernel& C = g->kernels[k];
+      for (uint32_t ri = 0; ri < C.reads.size(); ++ri) {
+        const Span& sp = C.reads[ri];
+        auto it = srcs.find({k, sp.buf});
+        if (it == srcs.end() || it->second.size() != 1) continue;
+        const uint32_t src = *it->second.begin();
+        if (assign[src] == assign[k]) continue;
+        const Kernel& P = g->kernels[src];
+        u64 rows = 0, rb = 0;
+        if (P.writes.empty() || !op_count_geometry(P, &rows, &rb)) continue;
+        const Span& w0 = P.writes[0];
+        if (sp.buf != w0.buf || sp.off != w0.off || sp.len != w0.len || rows * rb != w0.len) continue;
+        const u64 u = op_consumer_unit(C, ri, rb);
+        if (!u) continue;
+        u64& cur = unit_of[src];
+        cur = cur ? cur / gcd_u64(cur, u) * u : u;
+      }
+    }
+    p->xchunks.resize(p->transfers.size());
+    for (uint32_t t = 0; t < p->transfers.size(); ++t) {
+      const kd_transfer& tr = p->transfers[t];
+      const Kernel& P = g->kernels[tr.producer];
+      auto& X = p->xchunks[t];
+      const u64 len = P.writes.empty() ? 0 : P.writes[0].len;
+      u64 rows = 0, rb = 0;
+      if (op_count_geometry(P, &rows, &rb) && rows * rb == len && rb > 0) {
+        X.count = true;
+        X.rows = rows;
+        X.row_bytes = rb;
+        auto it = unit_of.find(tr.producer);
+        X.unit = (it == unit_of.end() || it->second > rb) ? rb : it->second;
+        const u64 U = ceil_div(rb, X.unit), q = ceil_div(U, n_chunks) * X.unit;
+        for (u64 c = 0; c < n_chunks; ++c) {
+          const u64 a = c * q, b = std::min((c + 1) * q, rb);
+          if (a < b) X.ch.push_back({a, b});
+        }
+      } else {
+        X.count = false;
+        X.rows = 1;
+        X.row_bytes = X.unit = std::max<u64>(len, 1);
+        X.ch.push_back({0, X.row_bytes});
+      }
+    }
+  }
+
   // ---- workspace layout per device
   const u64 AL = 256;
   p->layout.resize(n);
@@ -164,13 +337,24 @@ kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* 
     L.ctrl_off = 0;
     L.ctrl_bytes = align_up(64 + 4ull * n, AL);
     off = L.ctrl_bytes;
-    // flags: one u32 per incoming transfer
+    // flags: per incoming transfer one u64 per chunk + the residency counter;
+    // log: kLogWords (4) u64 per chunk
     L.flags_off = off;
-    u64 nflags = 0;
+    u64 nflags = 0, nlog = 0;
     for (uint32_t ti = 0; ti < p->transfers.size(); ++ti)
-      if (p->transfers[ti].dst_dev == d) L.landing[ti] = {0, L.flags_off + 4 * nflags++};
-    L.flags_bytes = align_up(std::max<u64>(4 * nflags, 4), AL);
+      if (p->transfers[ti].dst_dev == d) {
+        const u64 nch = p->xchunks[ti].ch.size();
+        L.landing[ti] = {0, L.flags_off + 8 * nflags};
+        nflags += nch + 1;
+        L.xlog[ti] = 32 * nlog;  // relative to log_off (fixed below)
+        nlog += nch;
+      }
+    L.flags_bytes = align_up(std::max<u64>(8 * nflags, 8), AL);
     off += L.flags_bytes;
+    L.log_off = off;
+    L.log_bytes = align_up(std::max<u64>(32 * nlog, 32), AL);
+    for (auto& kv : L.xlog) kv.second += L.log_off;
+    off += L.log_bytes;
     // scratch = max over kernels placed here
     u64 scr = 0;
     for (uint32_t k = 0; k < K; ++k)
@@ -241,6 +425,34 @@ kd_status kd_plan_transfers(const kd_plan* p, kd_transfer* out, uint32_t cap, ui
     return fail(KD_ERR_RANGE, "kd_plan_transfers: capacity too small");
   }
   std::copy(p->transfers.begin(), p->transfers.end(), out);
+  *n = need;
+  return KD_OK;
+}
+
+kd_status kd_plan_chunks(const kd_plan* p, kd_chunk* out, uint32_t cap, uint32_t* n) {
+  if (!p || !n) return fail(KD_ERR_INVALID_ARG, "kd_plan_chunks: NULL argument");
+  uint32_t need = 0;
+  for (const auto& X : p->xchunks) need += (uint32_t)X.ch.size();
+  if (cap < need || (need && !out)) {
+    *n = need;
+    return fail(KD_ERR_RANGE, "kd_plan_chunks: capacity too small");
+  }
+  uint32_t i = 0;
+  for (uint32_t t = 0; t < p->xchunks.size(); ++t) {
+    const auto& X = p->xchunks[t];
+    for (uint32_t c = 0; c < X.ch.size(); ++c) {
+      kd_chunk& o = out[i++];
+      o.transfer = t;
+      o.chunk = c;
+      o.count_mode = X.count ? 1u : 0u;
+      o.pad_ = 0;
+      o.rows = X.rows;
+      o.row_bytes = X.row_bytes;
+      o.unit = X.unit;
+      o.begin = X.ch[c].first;
+      o.end = X.ch[c].second;
+    }
+  }
   *n = need;
   return KD_OK;
 }

@@ -57,6 +57,7 @@ struct Params {
   unsigned* work;     // item ticket counter (last word of the counter region)
   unsigned long long* prof;  // KD_ATTN_PROF experiments: [0] producer empty-wait cycles, [1] consumer full-wait, [2] consumer busy, [3] pages
   int Hq, Hkv, G, pps, splits, pages_per_split;
+  int rows;           // sequences; items are kv-head-major: it = (g·rows + b)·splits + split
   int prefetch;       // stream the first item's safe pages before griddepcontrol.wait (KD_ATTN_PREFETCH=0 disables)
   float scale_log2;   // log2(e)/sqrt(D)
   Epi epi;
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
   __shared__ float s_lse[kFastSplitLse];                           // split merge: every (split, head) LSE
 
   pdl_launch_dependents();
+  epi_started(P.epi);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
     // ================= producer
     auto ids_of = [&](int it, int j0) -> int {  // this lane's page id of chunk j0 of item it
       if (it < 0) return 0;
-      const int split = it % P.splits, b = it / P.splits / Hkv;
+      const int split = it % P.splits, b = (it / P.splits) % P.rows;
       const int j = j0 + lane, pg = split * P.pages_per_split + j;
       return (j < P.pages_per_split && pg < P.pps) ? __ldg(P.bt + (size_t)b * P.pps + pg) : 0;
     };
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
     int mine = ids_of(it0 < 0 ? -1 : it0, 0);
     if (it0 >= 0 && P.prefetch) {
       const int split = it0 % P.splits, unit = it0 / P.splits;
-      const int g = unit % Hkv, b = unit / Hkv;
+      const int g = unit / P.rows, b = unit % P.rows;
       const int len = __ldg(P.sl + b);
       const int p0 = split * P.pages_per_split;
       const int np = max(0, min((len + kPage - 1) / kPage, p0 + P.pages_per_split) - p0);
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
       const long long ti0 = P.prof ? clock64() : 0;
       const int it_next = fetch();
       const int split = it % P.splits, unit = it / P.splits;
-      const int g = unit % Hkv, b = unit / Hkv;
+      const int g = unit / P.rows, b = unit % P.rows;
       const int len = P.sl[b];
       const int p0 = split * P.pages_per_split;
       const int np = max(0, min((len + kPage - 1) / kPage, p0 + P.pages_per_split) - p0);
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
       const int it = next_item(k);
       if (it < 0) break;
       const int split = it % P.splits, unit = it / P.splits;
-      const int g = unit % Hkv, b = unit / Hkv;
+      const int g = unit / P.rows, b = unit % P.rows;
       const int cs = k & 1;
       mbar_wait(&cfull[cs], (k >> 1) & 1);
       const float* cb = comb + (size_t)cs * kWarps * G * D;
@@ -517,10 +519,18 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
         }
       }
       if (done && P.epi.n) {
+        // every lane fences its own peer stores at system scope, then lane 0
+        // releases: COUNT mode → the unit's G·D output columns of row b go to
+        // the chunk(s) they fall in (units are drawn kv-head-major, so the
+        // low-column chunks complete first and the consumer starts on them
+        // while later kv heads are still computed); CTA mode → one increment
+        fence_acq_rel_sys();
         __syncwarp();
         if (lane == 0) {
-          fence_acq_rel_sys();
-          for (int pp = 0; pp < P.epi.n; ++pp) red_release_sys_add(P.epi.flag[pp], 1u);
+          if (P.epi.nch)
+            epi_release_range(P.epi, (uint32_t)(g * G * D) * 2u, (uint32_t)((g + 1) * G * D) * 2u, 1u);
+          else
+            epi_release_cta(P.epi);
         }
       }
     }
@@ -546,7 +556,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
   for (int k = 0;; ++k) {
     const int it = next_item(k);
     if (it < 0) break;
-    const int split = it % P.splits, b = it / P.splits / Hkv;
+    const int split = it % P.splits, b = (it / P.splits) % P.rows;
     const int len = P.sl[b];
     const int p0 = split * P.pages_per_split;
     const int np = max(0, min((len + kPage - 1) / kPage, p0 + P.pages_per_split) - p0);
@@ -815,6 +825,7 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
   P.part_lse = P.part_o + units * sh.splits * G * a.head_dim;
   P.Hq = a.n_heads;
   P.Hkv = a.n_kv_heads;
+  P.rows = (int)a.rows;
   P.G = G;
   P.pps = a.pages_per_seq;
   P.splits = sh.splits;
@@ -895,6 +906,19 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
             (double)h[4] / grid, (double)h[5] / grid, (double)h[6] / grid);
   }
   if (signals) return attention_signals(a, signals);
+  return KD_OK;
+}
+
+kd_status attention_grid(const kd_attr_attention& a, uint32_t* grid) {
+  kd_status st = attn::validate(a);
+  if (st) return st;
+  st = kernels_init();
+  if (st) return st;
+  const attn::Shape sh = attn::choose(a);
+  int per_sm = 1;
+  attn::pick(a.head_dim, a.n_heads / a.n_kv_heads, &per_sm);
+  const int n_items = (int)((uint64_t)a.rows * a.n_kv_heads * sh.splits);
+  *grid = (uint32_t)std::min(n_items, per_sm * kNumSMs);
   return KD_OK;
 }
 

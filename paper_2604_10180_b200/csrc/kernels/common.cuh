@@ -17,18 +17,31 @@ constexpr int kMaxPeers = 4;
 constexpr uint64_t kScratchCounterBytes = 64 * 1024;
 constexpr uint32_t kMaxCounters = kScratchCounterBytes / 4;
 
-// Fused peer-store epilogue (the chunked P2P handoff of SURVEY a13, fused into
-// the producer; replaces the paper's send kernels after k): every value
-// a kernel stores to its primary output at element index e is also stored to
+// ------------------------------------------------------------------ chunked P2P handoff
+// Producer side ("send after k", fused into the producer): every value a
+// kernel stores to its primary output at element index e is also stored to
 // dst[p] + e (another device's landing slot, mapped through NVLink P2P / CUDA
-// IPC, or a local slot in loopback). Each "finisher" CTA then publishes its
-// stores with a system-scope release increment of flag[p]; the consumer waits
-// for flag >= epoch * signals (monotonic epochs, no resets).
+// IPC, or a local slot in loopback), then released with a system-scope
+// red.release on u64 flags in the consumer's workspace. Two release modes:
+//  * COUNT (nch > 0): the output is a [rows][row_bytes] matrix whose row is
+//    cut into nch column chunks (byte bounds cb[0..nch], the plan's chunk table,
+//    R10). A CTA (or warp) that finished storing bytes [lo, hi) of some rows
+//    adds rows·|[lo,hi) ∩ chunk c| to flag[c]: chunk c is complete at
+//    epoch·rows·(cb[c+1] − cb[c]) bytes, whichever CTAs wrote it, so the
+//    consumer can start on chunk c while later chunks are still produced.
+//  * CTA (nch == 0): flag[0] += 1 per signalling CTA; complete at
+//    epoch·signals (kernels whose stores are not a dense [rows][cols] block).
+// Flags are monotonic across steps (epochs), never reset.
+constexpr int kMaxChunks = 8;
 struct Epi {
-  int n = 0;
-  int pad_ = 0;
+  int n = 0;                                 // peers (consumer devices)
+  int nch = 0;                               // 0: CTA mode; else COUNT mode with nch chunks
+  uint32_t row_bytes = 0;                    // COUNT: bytes per output row
+  uint32_t cb[kMaxChunks + 1] = {};          // COUNT: chunk byte bounds within a row
   void* dst[kMaxPeers] = {nullptr, nullptr, nullptr, nullptr};
-  unsigned* flag[kMaxPeers] = {nullptr, nullptr, nullptr, nullptr};
+  unsigned long long* flag[kMaxPeers] = {nullptr, nullptr, nullptr, nullptr};     // [max(nch,1)] in the peer
+  unsigned long long* started[kMaxPeers] = {nullptr, nullptr, nullptr, nullptr};  // loopback residency (nullable)
+  unsigned long long* logt[kMaxPeers] = {nullptr, nullptr, nullptr, nullptr};     // LOG: per-chunk records (nullable)
 };
 
 // ------------------------------------------------------------------ memory model
@@ -37,8 +50,16 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void red_release_sys_add(unsigned* p, unsigned v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_sys_add64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
@@ -49,15 +70,152 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
-// publish this CTA's peer stores: call by ALL threads of the CTA after their stores
-__device__ __forceinline__ void epi_signal(const Epi& epi) {
+// LOG-mode record per (incoming transfer, chunk) in the consumer's workspace,
+// 4 u64: [0] epoch of the first acquire, [1] that acquirer's wait start, [2]
+// its acquire time, [3] the producer's latest release (%globaltimer, ns;
+// monotonic across steps, so atomicMax needs no per-step reset)
+constexpr int kLogWords = 4;
+
+// COUNT mode: add rows·|[lo, hi) ∩ chunk c| bytes to every chunk the byte range
+// [lo, hi) of a row touches (a caller that stored those bytes of `rows` rows,
+// after the stores are ordered before this thread: fence / bar.sync)
+__device__ __forceinline__ void epi_release_range(const Epi& e, uint32_t lo, uint32_t hi, uint32_t rows) {
+  for (int c = 0; c < e.nch; ++c) {
+    const uint32_t a = max(lo, e.cb[c]), b = min(hi, e.cb[c + 1]);
+    if (a >= b) continue;
+    const unsigned long long add = (unsigned long long)(b - a) * rows;
+    for (int p = 0; p < e.n; ++p) {
+      red_release_sys_add64(e.flag[p] + c, add);
+      if (e.logt[p]) atomicMax(e.logt[p] + c * kLogWords + 3, gtimer_ns());
+    }
+  }
+}
+// CTA mode: one release per peer (thread-level; caller orders the CTA's stores first)
+__device__ __forceinline__ void epi_release_cta(const Epi& e) {
+  for (int p = 0; p < e.n; ++p) {
+    red_release_sys_add64(e.flag[p], 1ull);
+    if (e.logt[p]) atomicMax(e.logt[p] + 3, gtimer_ns());
+  }
+}
+// loopback residency: every CTA of a COUNT-mode producer announces itself at
+// entry (the consumer's gate waits for the whole grid before the consumer
+// launches and spins on chunks in-kernel; see runtime.cu)
+__device__ __forceinline__ void epi_started(const Epi& e) {
+  if (threadIdx.x == 0)
+    for (int p = 0; p < e.n; ++p)
+      if (e.started[p]) atomicAdd(e.started[p], 1ull);
+}
+
+// publish this CTA's peer stores: call by ALL threads of the CTA after their
+// stores. CTA mode: one increment; COUNT mode: the CTA declares the byte range
+// [lo, hi) of `rows` rows it wrote (nch == 0 ignores them).
+__device__ __forceinline__ void epi_signal(const Epi& epi, uint32_t lo = 0, uint32_t hi = 0, uint32_t rows = 0) {
   if (epi.n == 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     fence_acq_rel_sys();
-    for (int p = 0; p < epi.n; ++p) red_release_sys_add(epi.flag[p], 1u);
+    if (epi.nch)
+      epi_release_range(epi, lo, hi, rows);
+    else
+      epi_release_cta(epi);
   }
+}
+
+// COUNT-mode release of per-CTA byte tallies (kernels whose stores are not one
+// rectangle per CTA): s_cnt[c] = bytes this CTA stored into chunk c (of every
+// row together). Call by ALL threads after the stores.
+__device__ __forceinline__ void epi_signal_counts(const Epi& epi, const unsigned* s_cnt) {
+  if (epi.n == 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_acq_rel_sys();
+    if (epi.nch == 0) {
+      epi_release_cta(epi);
+      return;
+    }
+    for (int c = 0; c < epi.nch; ++c)
+      if (s_cnt[c])
+        for (int p = 0; p < epi.n; ++p) {
+          red_release_sys_add64(epi.flag[p] + c, (unsigned long long)s_cnt[c]);
+          if (epi.logt[p]) atomicMax(epi.logt[p] + c * kLogWords + 3, gtimer_ns());
+        }
+  }
+}
+__device__ __forceinline__ int epi_chunk_of(const Epi& epi, uint32_t byte_in_row) {
+  int c = 0;
+  while (c + 1 < epi.nch && byte_in_row >= epi.cb[c + 1]) ++c;
+  return c;
+}
+
+// ------------------------------------------------------------------ consumer side ("recv before k")
+// A chunk-aware consumer acquires chunk c of a remote input right before it
+// reads it: spin until flag[c] >= (epoch − base)·mult[c] (ld.acquire.sys),
+// watchdog → *err = 1. One thread acquires; the caller then orders the other
+// threads behind it (bar.sync / __syncwarp) — or, for TMA reads, a proxy fence.
+constexpr int kMaxAcqIn = 4;
+struct AcqIn {
+  const unsigned long long* flag = nullptr;  // [nch]
+  unsigned long long* log = nullptr;         // LOG: per-chunk records (nullable)
+  int slot = 0;                              // operand index (GEMM: 0 = X; add_rmsnorm / residual: delta index)
+  int nch = 0;
+  uint32_t row_bytes = 0;
+  uint32_t cb[kMaxChunks + 1] = {};
+  unsigned long long mult[kMaxChunks] = {};
+};
+struct Acq {
+  int n = 0;                      // remote inputs acquired in-kernel (0: none)
+  unsigned base = 0;              // steps run without transfers (their epochs carry no releases)
+  const unsigned* epoch = nullptr;
+  unsigned* err = nullptr;
+  AcqIn in[kMaxAcqIn];
+};
+
+__device__ __forceinline__ int acq_find(const Acq& a, int slot) {
+  for (int i = 0; i < a.n; ++i)
+    if (a.in[i].slot == slot) return i;
+  return -1;
+}
+__device__ __forceinline__ void acq_chunk(const Acq& a, int i, int c) {
+  const AcqIn& in = a.in[i];
+  const unsigned e = *(volatile const unsigned*)a.epoch;
+  const unsigned long long target = (unsigned long long)(e - a.base) * in.mult[c];
+  if (ld_acquire_sys64(in.flag + c) >= target) {
+    if (in.log && atomicMax(in.log + c * kLogWords, (unsigned long long)e) < e) {
+      const unsigned long long t = gtimer_ns();
+      in.log[c * kLogWords + 1] = t;
+      in.log[c * kLogWords + 2] = t;
+    }
+    return;
+  }
+  const unsigned long long t0 = in.log ? gtimer_ns() : 0ull;
+  long long spins = 0;
+  while (ld_acquire_sys64(in.flag + c) < target) {
+    if (++spins > (1ll << 24)) {  // watchdog (~10 s): record (KD_ERR_TIMEOUT at kd_runtime_check) and give up
+      if (a.err) atomicExch(a.err, 1u);
+      break;
+    }
+    __nanosleep(40);
+  }
+  if (in.log && atomicMax(in.log + c * kLogWords, (unsigned long long)e) < e) {
+    in.log[c * kLogWords + 1] = t0;
+    in.log[c * kLogWords + 2] = gtimer_ns();
+  }
+}
+// acquire every chunk of remote input i that the byte range [lo, hi) of a row
+// touches, in ascending order; `done` caches the chunks this thread already holds
+__device__ __forceinline__ void acq_range(const Acq& a, int i, uint32_t lo, uint32_t hi, uint32_t* done) {
+  const AcqIn& in = a.in[i];
+  for (int c = 0; c < in.nch; ++c)
+    if (lo < in.cb[c + 1] && in.cb[c] < hi && !(*done & (1u << c))) {
+      acq_chunk(a, i, c);
+      *done |= 1u << c;
+    }
 }
 
 // ------------------------------------------------------------------ programmatic dependent launch

@@ -31,8 +31,9 @@ constexpr int kNormChunks = 4;  // H <= 8 * 256 * 4 = 8192
 __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __restrict__ r, Deltas deltas,
                                                                   const __nv_bfloat16* __restrict__ gamma,
                                                                   __nv_bfloat16* __restrict__ h, int H, float eps,
-                                                                  Epi epi) {
+                                                                  Epi epi, Acq acq) {
   pdl_launch_dependents();
+  epi_started(epi);
   const int row = blockIdx.x, tid = threadIdx.x;
   const int nch = H / 8;
   // gamma is a weight (never written in a step): fetch it before the
@@ -47,8 +48,18 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __rest
   float v[kNormChunks][8];
   float ss = 0.f;
   float* rr = r + (size_t)row * H;
+  uint32_t held[kMaxAcqIn] = {0u, 0u, 0u, 0u};  // chunks thread 0 acquired, per remote delta
 #pragma unroll
   for (int c = 0; c < kNormChunks; ++c) {
+    // remote deltas (a13 consumer side): column group c of every thread is the
+    // byte range [16·256c, 16·256(c+1)) of the row; thread 0 acquires the
+    // chunks it touches (ascending), the barrier orders the others behind it
+    if (acq.n && c * kNormThreads < nch) {
+      if (tid == 0)
+        for (int i = 0; i < acq.n; ++i)
+          acq_range(acq, i, 16u * (c * kNormThreads), 16u * min(nch, (c + 1) * kNormThreads), &held[i]);
+      __syncthreads();
+    }
     int ch = tid + c * kNormThreads;
     if (ch < nch) {
       float4 a = reinterpret_cast<const float4*>(rr)[2 * ch];
@@ -95,7 +106,7 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __rest
       for (int p = 0; p < epi.n; ++p) reinterpret_cast<uint4*>(epi.dst[p])[e] = o;
     }
   }
-  epi_signal(epi);
+  epi_signal(epi, 0u, (uint32_t)H * 2u, 1u);  // COUNT: this CTA wrote the whole row
 }
 
 static DeltasF as_f32(const Deltas& d) {
@@ -117,16 +128,24 @@ kd_status launch_add_rmsnorm(const kd_attr_add_rmsnorm& a, float* r, const Delta
     return fail(KD_ERR_UNSUPPORTED, "add_rmsnorm: hidden must be a multiple of 8 and <= 8192");
   if (!r || !gamma || !h) return fail(KD_ERR_INVALID_ARG, "add_rmsnorm: NULL pointer");
   KD_CUDA_CHECK(kd_launch(add_rmsnorm_kernel, dim3(a.rows), dim3(kNormThreads), 0, c.stream, r, d,
-                          (const __nv_bfloat16*)gamma, (__nv_bfloat16*)h, (int)a.hidden, a.eps, c.epi),
+                          (const __nv_bfloat16*)gamma, (__nv_bfloat16*)h, (int)a.hidden, a.eps, c.epi, c.acq),
                 "add_rmsnorm launch");
   if (signals) *signals = a.rows;
   return KD_OK;
 }
 
 // ------------------------------------------------------------------ C1.11
-__global__ void residual_add_kernel(float* __restrict__ r, Deltas d, size_t n8, Epi epi) {
+__global__ void residual_add_kernel(float* __restrict__ r, Deltas d, size_t n8, Epi epi, Acq acq) {
   pdl_launch_dependents();
   pdl_wait();
+  if (acq.n) {  // remote deltas: thread 0 acquires every chunk of each (the final add is tiny)
+    if (threadIdx.x == 0)
+      for (int i = 0; i < acq.n; ++i) {
+        uint32_t held = 0;
+        acq_range(acq, i, 0u, acq.in[i].row_bytes, &held);
+      }
+    __syncthreads();
+  }
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x) {
     float4 a = reinterpret_cast<float4*>(r)[2 * i];
     float4 b = reinterpret_cast<float4*>(r)[2 * i + 1];
@@ -142,7 +161,7 @@ __global__ void residual_add_kernel(float* __restrict__ r, Deltas d, size_t n8, 
       reinterpret_cast<float4*>(epi.dst[p])[2 * i + 1] = b;
     }
   }
-  epi_signal(epi);
+  epi_signal(epi);  // CTA mode (the residual stream is never streamed in the decoder graphs)
 }
 
 static int residual_grid(const kd_attr_residual_add& a) {
@@ -167,7 +186,7 @@ kd_status launch_residual_add(const kd_attr_residual_add& a, float* r, const Del
     if (!st && signals) *signals = grid;
     return st;
   }
-  KD_CUDA_CHECK(kd_launch(residual_add_kernel, dim3(grid), dim3(256), 0, c.stream, r, d, n8, c.epi),
+  KD_CUDA_CHECK(kd_launch(residual_add_kernel, dim3(grid), dim3(256), 0, c.stream, r, d, n8, c.epi, c.acq),
                 "residual_add launch");
   if (signals) *signals = grid;
   return KD_OK;
@@ -175,34 +194,55 @@ kd_status launch_residual_add(const kd_attr_residual_add& a, float* r, const Del
 
 // ------------------------------------------------------------------ a8
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int rows,
-                                int F, Epi epi) {
+                                int F, Epi epi, Acq acq) {
   // one thread = 8 consecutive outputs; block j of 64 outputs reads gate
-  // columns [128j, 128j+64) and up columns [128j+64, 128j+128)
+  // columns [128j, 128j+64) and up columns [128j+64, 128j+128). Work is
+  // ordered block-major (t → block j, row, 8-column group), so the grid sweeps
+  // the gu chunks in ascending order: a warp covers 4 rows of one block, and
+  // its lane 0 acquires that block's chunk once (a13 consumer side).
+  __shared__ unsigned s_cnt[kMaxChunks];
   pdl_launch_dependents();
+  epi_started(epi);
+  if (threadIdx.x < kMaxChunks) s_cnt[threadIdx.x] = 0u;
+  if (epi.nch) __syncthreads();
   pdl_wait();
-  const int per_row = F / 8;
-  const size_t n = (size_t)rows * per_row;
-  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
-    int row = (int)(t / per_row), c8 = (int)(t % per_row);
-    int col = c8 * 8, j = col / 64, i = col % 64;
-    const __nv_bfloat16* g = gu + (size_t)row * 2 * F + 128 * j + i;
-    uint4 gv = *reinterpret_cast<const uint4*>(g);
-    uint4 uv = *reinterpret_cast<const uint4*>(g + 64);
-    const uint32_t* gp = &gv.x;
-    const uint32_t* up = &uv.x;
-    uint4 o;
-    uint32_t* op = &o.x;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float g0 = bf16lo(gp[q]), g1 = bf16hi(gp[q]);
-      float s0 = silu_fast(g0), s1 = silu_fast(g1);
-      op[q] = pack_bf16(s0 * bf16lo(up[q]), s1 * bf16hi(up[q]));
+  const int lane = threadIdx.x & 31;
+  const size_t n = (size_t)rows * (F / 8);
+  uint32_t held = 0;
+  for (size_t t0 = blockIdx.x * (size_t)blockDim.x + (threadIdx.x & ~31u); t0 < n; t0 += (size_t)gridDim.x * blockDim.x) {
+    const size_t t = t0 + lane;
+    const int jw = (int)(t0 / ((size_t)rows * 8));  // the warp's first block (a warp spans ≤ 2 blocks when rows < 4)
+    if (acq.n) {
+      if (lane == 0) {
+        const int jl = (int)(min(t0 + 31, n - 1) / ((size_t)rows * 8));
+        acq_range(acq, 0, 256u * jw, 256u * (jl + 1), &held);
+      }
+      __syncwarp();
     }
-    size_t e = (size_t)row * per_row + c8;
-    reinterpret_cast<uint4*>(out)[e] = o;
-    for (int p = 0; p < epi.n; ++p) reinterpret_cast<uint4*>(epi.dst[p])[e] = o;
+    if (t < n) {
+      const int j = (int)(t / ((size_t)rows * 8));
+      const int rem = (int)(t - (size_t)j * rows * 8);
+      const int row = rem >> 3, i = (rem & 7) * 8;
+      const __nv_bfloat16* g = gu + (size_t)row * 2 * F + 128 * j + i;
+      uint4 gv = *reinterpret_cast<const uint4*>(g);
+      uint4 uv = *reinterpret_cast<const uint4*>(g + 64);
+      const uint32_t* gp = &gv.x;
+      const uint32_t* up = &uv.x;
+      uint4 o;
+      uint32_t* op = &o.x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float g0 = bf16lo(gp[q]), g1 = bf16hi(gp[q]);
+        float s0 = silu_fast(g0), s1 = silu_fast(g1);
+        op[q] = pack_bf16(s0 * bf16lo(up[q]), s1 * bf16hi(up[q]));
+      }
+      const size_t e = ((size_t)row * F + 64 * j + i) / 8;
+      reinterpret_cast<uint4*>(out)[e] = o;
+      for (int p = 0; p < epi.n; ++p) reinterpret_cast<uint4*>(epi.dst[p])[e] = o;
+      if (epi.nch) atomicAdd(&s_cnt[epi_chunk_of(epi, (uint32_t)(64 * j + i) * 2u)], 16u);
+    }
   }
-  epi_signal(epi);
+  epi_signal_counts(epi, s_cnt);
 }
 
 static int silu_grid(const kd_attr_silu_mul& a) {
@@ -222,7 +262,7 @@ kd_status launch_silu_mul(const kd_attr_silu_mul& a, const void* gu, void* out, 
     return st;
   }
   KD_CUDA_CHECK(kd_launch(silu_mul_kernel, dim3(grid), dim3(256), 0, c.stream, (const __nv_bfloat16*)gu,
-                          (__nv_bfloat16*)out, (int)a.rows, (int)a.ffn, c.epi),
+                          (__nv_bfloat16*)out, (int)a.rows, (int)a.ffn, c.epi, c.acq),
                 "silu_mul launch");
   if (signals) *signals = grid;
   return KD_OK;
@@ -243,12 +283,34 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
     rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ bt,
                        const int32_t* __restrict__ sl, __nv_bfloat16* __restrict__ q_out,
                        __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, int Hq, int Hkv, int D,
-                       int page, int pps, int slot_offset, const __grid_constant__ RopeFreq fr, Epi epi) {
+                       int page, int pps, int slot_offset, const __grid_constant__ RopeFreq fr, Epi epi, Acq acq) {
+  __shared__ unsigned s_cnt[kMaxChunks];
   pdl_launch_dependents();
+  epi_started(epi);
   const int b = blockIdx.x, half = D / 2, G = Hq / Hkv;
   const int hh = blockIdx.y * kRopeHeadsPerCta + (int)(threadIdx.x >> 4), t16 = threadIdx.x & 15;
   const int n_rot = Hq + Hkv;
+  if (threadIdx.x < kMaxChunks) s_cnt[threadIdx.x] = 0u;
   pdl_wait();
+  if (acq.n) {
+    // remote qkv (a13 consumer side): thread 0 acquires the chunks holding the
+    // source columns of this CTA's heads (kv-group chunks of the grouped layout)
+    if (threadIdx.x == 0) {
+      uint32_t held = 0;
+      for (int x = 0; x < kRopeHeadsPerCta; ++x) {
+        const int h2 = blockIdx.y * kRopeHeadsPerCta + x;
+        int col;
+        if (h2 < Hq) col = ((h2 / G) * (G + 2) + h2 % G) * D;
+        else if (h2 < n_rot) col = ((h2 - Hq) * (G + 2) + G) * D;
+        else if (h2 < n_rot + Hkv) col = ((h2 - n_rot) * (G + 2) + G + 1) * D;
+        else break;
+        acq_range(acq, 0, 2u * col, 2u * (col + D), &held);
+      }
+    }
+    __syncthreads();
+  } else if (epi.nch) {
+    __syncthreads();  // s_cnt zeroed
+  }
   if (hh < n_rot && t16 * 8 < half) {
     const int i0 = t16 * 8;
     const int pos = sl[b] - 1;
@@ -294,12 +356,17 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
     }
     *reinterpret_cast<uint4*>(dst + i0) = lo;
     *reinterpret_cast<uint4*>(dst + half + i0) = hi;
-    if (is_q)
+    if (is_q) {
       for (int p = 0; p < epi.n; ++p) {
         __nv_bfloat16* pd = (__nv_bfloat16*)epi.dst[p] + qoff;
         *reinterpret_cast<uint4*>(pd + i0) = lo;
         *reinterpret_cast<uint4*>(pd + half + i0) = hi;
       }
+      if (epi.nch) {  // COUNT: 16 bytes at q columns hh·D + i0 and hh·D + half + i0
+        atomicAdd(&s_cnt[epi_chunk_of(epi, (uint32_t)(hh * D + i0) * 2u)], 16u);
+        atomicAdd(&s_cnt[epi_chunk_of(epi, (uint32_t)(hh * D + half + i0) * 2u)], 16u);
+      }
+    }
   } else if (hh >= n_rot && hh < n_rot + Hkv) {
     // v: plain copy into the cache slot, 16 threads × 8 dims per pass
     const int g = hh - n_rot;
@@ -310,7 +377,7 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
     for (int c8 = t16 * 8; c8 < D; c8 += 128)
       *reinterpret_cast<uint4*>(dst + c8) = *reinterpret_cast<const uint4*>(x + c8);
   }
-  epi_signal(epi);
+  epi_signal_counts(epi, s_cnt);
 }
 
 static dim3 rope_grid(const kd_attr_rope_append& a) {
@@ -339,7 +406,7 @@ kd_status launch_rope_append(const kd_attr_rope_append& a, const void* qkv, cons
   KD_CUDA_CHECK(kd_launch(rope_append_kernel, grid, dim3(kRopeHeadsPerCta * 16), 0, c.stream, (const __nv_bfloat16*)qkv,
                           bt, sl, (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (int)a.n_heads,
                           (int)a.n_kv_heads, (int)a.head_dim, (int)a.page, (int)a.pages_per_seq, (int)a.slot_offset,
-                          fr, c.epi),
+                          fr, c.epi, c.acq),
                 "rope_append launch");
   if (signals) *signals = grid.x * grid.y;
   return KD_OK;
@@ -354,7 +421,11 @@ struct Parts {
 };
 
 __global__ void attn_merge_kernel(Parts ps, int n, __nv_bfloat16* __restrict__ out, int rows, int Hq, int D, Epi epi) {
+  __shared__ unsigned s_cnt[kMaxChunks];
   pdl_launch_dependents();
+  epi_started(epi);
+  if (threadIdx.x < kMaxChunks) s_cnt[threadIdx.x] = 0u;
+  if (epi.nch) __syncthreads();
   pdl_wait();
   const size_t lse_off = (size_t)rows * Hq * D * 2;
   const int d4n = D / 4;
@@ -379,8 +450,9 @@ __global__ void attn_merge_kernel(Parts ps, int n, __nv_bfloat16* __restrict__ o
     const size_t oi = rh * D + d0;
     *reinterpret_cast<uint2*>(out + oi) = o;
     for (int p = 0; p < epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)epi.dst[p] + oi) = o;
+    if (epi.nch) atomicAdd(&s_cnt[epi_chunk_of(epi, (uint32_t)(oi % ((size_t)Hq * D)) * 2u)], 8u);
   }
-  epi_signal(epi);
+  epi_signal_counts(epi, s_cnt);
 }
 
 static int merge_grid(const kd_attr_attn_merge& a) {
@@ -446,20 +518,28 @@ kd_status launch_step_begin(unsigned* epoch, unsigned* const* mine, unsigned* co
 }
 
 __global__ void wait_kernel(WaitList w, const unsigned* epoch, unsigned base, unsigned* err) {
-  if (threadIdx.x >= w.n) return;
-  const unsigned target = (*epoch - base) * w.mult[threadIdx.x];
+  if ((int)threadIdx.x >= w.n) return;
+  const unsigned e = *epoch;
+  const unsigned long long target = (unsigned long long)(e - base) * w.mult[threadIdx.x];
+  unsigned long long* log = w.log[threadIdx.x];
+  const unsigned long long t0 = log ? gtimer_ns() : 0ull;
   long long spins = 0;
-  while (ld_acquire_sys(w.flag[threadIdx.x]) < target) {
+  while (ld_acquire_sys64(w.flag[threadIdx.x]) < target) {
     if (++spins > (1ll << 30)) {  // watchdog: record and give up (KD_ERR_TIMEOUT at kd_runtime_check)
       atomicExch(err, 1u);
       break;
     }
     __nanosleep(32);
   }
+  if (log && atomicMax(log, (unsigned long long)e) < e) {  // first acquire of this chunk in this step
+    log[1] = t0;
+    log[2] = gtimer_ns();
+  }
 }
 
 kd_status launch_wait(const WaitList& w, const unsigned* epoch, unsigned base, unsigned* err, cudaStream_t s) {
   if (w.n <= 0) return KD_OK;
+  if (w.n > kMaxWait) return fail(KD_ERR_UNSUPPORTED, "wait: more than 32 flags");
   wait_kernel<<<1, 32, 0, s>>>(w, epoch, base, err);
   KD_CUDA_CHECK(cudaGetLastError(), "wait launch");
   return KD_OK;
@@ -483,6 +563,32 @@ static kd_status attrs_of(const std::vector<uint8_t>& v, T* out) {
 }
 
 kd_status attention_signals(const kd_attr_attention& a, uint32_t* s);  // attention.cu
+
+kd_status attention_grid(const kd_attr_attention& a, uint32_t* grid);  // attention.cu
+kd_status gemm_grid(const GemmShape& sh, uint32_t* grid);              // gemm.cu
+
+// CTAs one launch of a COUNT-release producer runs (the loopback residency
+// gate waits for all of them to have started, runtime.cu)
+kd_status op_grid(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* grid) {
+  kd_status st = KD_OK;
+  switch (op) {
+    case KD_OP_ADD_RMSNORM: { kd_attr_add_rmsnorm a; if ((st = attrs_of(attrs, &a))) return st; *grid = a.rows; return KD_OK; }
+    case KD_OP_SILU_MUL: { kd_attr_silu_mul a; if ((st = attrs_of(attrs, &a))) return st; *grid = silu_grid(a); return KD_OK; }
+    case KD_OP_ROPE_APPEND: {
+      kd_attr_rope_append a;
+      if ((st = attrs_of(attrs, &a))) return st;
+      const dim3 g = rope_grid(a);
+      *grid = g.x * g.y;
+      return KD_OK;
+    }
+    case KD_OP_ATTN_MERGE: { kd_attr_attn_merge a; if ((st = attrs_of(attrs, &a))) return st; *grid = merge_grid(a); return KD_OK; }
+    case KD_OP_ATTENTION: { kd_attr_attention a; if ((st = attrs_of(attrs, &a))) return st; return attention_grid(a, grid); }
+    case KD_OP_GEMM: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_grid(gemm_shape(a), grid); }
+    case KD_OP_GEMM_SILU: { kd_attr_gemm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_grid(gemm_shape(a, true), grid); }
+    case KD_OP_GEMM_RMSNORM: { kd_attr_gemm_rmsnorm a; if ((st = attrs_of(attrs, &a))) return st; return gemm_grid(gemm_shape(a), grid); }
+  }
+  return fail(KD_ERR_UNSUPPORTED, "op_grid: not a COUNT-release producer");
+}
 
 kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* signals) {
   kd_status st = KD_OK;

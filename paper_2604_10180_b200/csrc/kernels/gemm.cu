@@ -58,6 +58,7 @@ struct Args {
   const int* meta;
   int dbg;                    // debug A/B knob (KD_GEMM_DBG): 1 skip owner Y stores, 2 skip owner fold
   unsigned* err;              // runtime error word (nullable): set to 2 when the fold barrier times out
+  Acq acq;                    // chunk-aware consumer: X (slot 0) acquired per k-block by the TMA warp
 };
 
 #define KD_TRACE(slot) \
@@ -69,6 +70,18 @@ struct Args {
   do {                 \
     if (A.trace) A.trace[blockIdx.x * 32 + (slot)] = (unsigned long long)clock64(); \
   } while (0)
+
+// a13 consumer side in the TMA producer warp (lane 0): before the activation
+// tile of k-block kb is loaded, acquire the chunks of the remote X that hold
+// its columns [kb·64·kbs, (kb+1)·64·kbs) (ascending; `held` caches them); the
+// proxy fence orders the acquired generic-proxy data before the TMA reads
+__device__ __forceinline__ void acquire_x(const Acq& acq, int xi, int kb, int kbs, int K, uint32_t* held) {
+  if (xi < 0) return;
+  const uint32_t before = *held;
+  const uint32_t lo = (uint32_t)kb * kbs * 64u * 2u, hi = (uint32_t)min(K, (kb + 1) * kbs * 64) * 2u;
+  acq_range(acq, xi, lo, hi, held);
+  if (*held != before) asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 // unit range of CTA c: [c·U/G, (c+1)·U/G); owner of unit u: ⌈(u+1)·G/U⌉ − 1
 __host__ __device__ __forceinline__ long long unit_begin(long long c, long long U, long long G) { return c * U / G; }
@@ -113,10 +126,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = (uint32_t*)(fixbar + 1);
   volatile unsigned* s_flag = (volatile unsigned*)(tmem_slot + 1);
   __nv_bfloat16* ystage = (__nv_bfloat16*)(fixbar + 2);  // 2 x [16][128] bf16 epilogue transpose
+  unsigned* s_cnt = (unsigned*)(ystage + 2 * kChunk * kBM);  // COUNT-mode bytes stored per chunk (this CTA)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) KD_TRACE(0);
   pdl_launch_dependents();
+  epi_started(A.epi);
+  if (threadIdx.x < kMaxChunks) s_cnt[threadIdx.x] = 0u;  // (ordered by the __syncthreads below)
+  // COUNT mode: tally the bytes this CTA streams into each chunk of the output row
+  const int row_elems = A.silu ? A.N / 2 : A.N;
+  auto count = [&](size_t yo, unsigned bytes) {
+    if (A.epi.nch) atomicAdd(&s_cnt[epi_chunk_of(A.epi, (uint32_t)(yo % (size_t)row_elems) * 2u)], bytes);
+  };
   const long long U = A.units, G = gridDim.x, c = blockIdx.x;
   const long long u0 = unit_begin(c, U, G), u1 = unit_begin(c + 1, U, G);
   const int KB = A.kblocks;
@@ -161,8 +182,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sa + (size_t)s * wst + b * kStageA, &tmap_w, (kb * kbs + b) * kBK, w_row(t), &full[s], pw);
     };
+    const int xi = acq_find(A.acq, 0);
+    uint32_t held = 0;
     auto load_x = [&](int t, int kb, int s) {
       const int xr = A.groups ? __ldg(A.meta + A.groups + t / A.tpg) : 0;
+      acquire_x(A.acq, xi, kb, kbs, A.K, &held);
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sb + (size_t)s * xst + b * xbox, &tmap_x, (kb * kbs + b) * kBK, xr, &full[s], px);
     };
@@ -346,7 +370,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < kI; ++i) {
                   const int w = w0 + 128 * i, j = w >> 4;
                   if (w < A.M * 16 && j < mv)
-                    store_silu4(A, (size_t)(y0 + j) * (A.N / 2) + (nb0 / 2) + (w & 15) * 4, g[i], uu[i]);
+                  {
+                    const size_t yo = (size_t)(y0 + j) * (A.N / 2) + (nb0 / 2) + (w & 15) * 4;
+                    store_silu4(A, yo, g[i], uu[i]);
+                    count(yo, 8u);
+                  }
                 }
               }
             }
@@ -381,11 +409,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (nn + 4 <= A.N && (A.N & 3) == 0) {
                   *reinterpret_cast<uint2*>(A.Y + yo) = o;
                   for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+                  count(yo, 8u);
                 } else {
                   const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
                   for (int x = 0; x < 4 && nn + x < A.N; ++x) {
                     A.Y[yo + x] = __float2bfloat16_rn(vv[x]);
                     for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = __float2bfloat16_rn(vv[x]);
+                    count(yo + x, 2u);
                   }
                 }
               }
@@ -416,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const size_t yo = (size_t)(y0 + j0 + j) * (A.N / 2) + nb0 / 2 + c8;
               *reinterpret_cast<uint4*>(A.Y + yo) = o;
               for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint4*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+              count(yo, 16u);
             }
           }
 #pragma unroll
@@ -429,11 +460,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (nn + 8 <= A.N && (A.N & 7) == 0) {
                 *reinterpret_cast<uint4*>(A.Y + yo) = val;
                 for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint4*>((__nv_bfloat16*)A.epi.dst[p] + yo) = val;
+                count(yo, 16u);
               } else {
                 const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(&val);
                 for (int x = 0; x < 8 && nn + x < A.N; ++x) {
                   A.Y[yo + x] = sv[x];
                   for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = sv[x];
+                  count(yo + x, 2u);
                 }
               }
             }
@@ -541,11 +574,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (nn + 4 <= A.N && (A.N & 3) == 0) {
             *reinterpret_cast<uint2*>(A.Y + yo) = o;
             for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+            count(yo, 8u);
           } else {
             const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
             for (int x = 0; x < 4 && nn + x < A.N; ++x) {
               A.Y[yo + x] = __float2bfloat16_rn(vv[x]);
               for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = __float2bfloat16_rn(vv[x]);
+              count(yo + x, 2u);
             }
           }
         }
@@ -553,14 +588,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (threadIdx.x == 128) KD_TRACE(13);
   }
-  // publish this CTA's stores to the consumer devices (one release per CTA)
-  if (A.epi.n) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      fence_acq_rel_sys();
-      for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
-    }
-  }
+  // publish this CTA's stores to the consumer devices: CTA mode one release,
+  // COUNT mode the bytes tallied per chunk
+  epi_signal_counts(A.epi, s_cnt);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1) {
@@ -629,6 +659,7 @@ struct Args {
   unsigned* bar;                // 2 self-resetting words (scratch)
   float* ssq;                   // [M][gridDim.x] per-CTA partial Σr² (scratch)
   unsigned* err;                // runtime error word (nullable): set to 2 when the grid barrier times out
+  Acq acq;                      // chunk-aware consumer: X (slot 0) acquired per k-block by the TMA warp
 };
 
 // a5 fused into the QKV GEMM epilogue. W rows are pair-interleaved within each
@@ -958,13 +989,8 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
       A.bar[1] = 0u;
     }
   }
-  if (A.epi.n && (split == 1 || my_rows > 0)) {  // publish this CTA's stores (gemm_signals counts these)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      fence_acq_rel_sys();
-      for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
-    }
-  }
+  if (A.epi.n && (split == 1 || my_rows > 0))  // publish: COUNT → h columns [c0, c0 + rows) of all M tokens
+    epi_signal(A.epi, (uint32_t)c0 * 2u, (uint32_t)(c0 + rows) * 2u, (uint32_t)M);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -1002,6 +1028,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) KD_TRACE(0);
   pdl_launch_dependents();
+  epi_started(A.epi);
   const int rank = split > 1 ? (int)cluster_ctarank() : 0;
   const int tile = blockIdx.x / split;
   const int n0 = tile * kBM;
@@ -1050,7 +1077,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sa + (size_t)s * wst + b * kStageA, &tmap_w, ((kb0 + i) * kbs + b) * kBK, n0, &full[s], pw);
     };
-    auto load_x = [&](int i, int s) {
+    const int xi = acq_find(A.acq, 0);
+    uint32_t held = 0;
+    auto load_x = [&](int i, int s) {  // (this rank's K range only: it acquires only its own X chunks)
+      acquire_x(A.acq, xi, kb0 + i, kbs, A.K, &held);
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sb + (size_t)s * xst + b * xbox, &tmap_x, ((kb0 + i) * kbs + b) * kBK, 0, &full[s], px);
     };
@@ -1204,11 +1234,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ep == 0) { KD_TRACE(7); KD_CTRACE(22); KD_TRACE(10); KD_CTRACE(23); }
       // the owner's sum runs after the role branches with all warps
     }
-    if (A.epi.n && stored) {  // publish this CTA's stores to the consumer devices
+    if (A.epi.n && stored) {  // publish this CTA's stores: COUNT → columns [n0, n0 + 128) of all M tokens
       named_bar(1, kEpi);
       if (ep == 0) {
         fence_acq_rel_sys();
-        for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
+        if (A.epi.nch)
+          epi_release_range(A.epi, (uint32_t)n0 * 2u, (uint32_t)min(n0 + kBM, A.N) * 2u, (uint32_t)M);
+        else
+          epi_release_cta(A.epi);
       }
     }
     if (ep == 0) { KD_TRACE(9); KD_CTRACE(26); }
@@ -1250,12 +1283,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (threadIdx.x == 128) { KD_TRACE(11); KD_CTRACE(25); }
-    if (A.epi.n && my_rows > 0) {  // publish this CTA's stores to the consumer devices
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        fence_acq_rel_sys();
-        for (int p = 0; p < A.epi.n; ++p) red_release_sys_add(A.epi.flag[p], 1u);
-      }
+    if (A.epi.n && my_rows > 0) {  // publish: COUNT → this owner's columns of all M tokens
+      const int c0 = n0 + rank * rpo;
+      epi_signal(A.epi, (uint32_t)min(c0, A.N) * 2u, (uint32_t)min(c0 + my_rows, A.N) * 2u, (uint32_t)M);
     }
   }
   // No closing cluster barrier: peers only ever WRITE into this CTA's recv
@@ -1363,7 +1393,7 @@ static kd_status geometry(const GemmShape& a, Geometry* g, int sms) {
 
 static size_t smem_bytes(const Geometry& g) {
   return 1024 + (size_t)g.stages * g.kbs * (kStageA + g.mma_n * kBK * 2) + (2 * kMaxStages + 6) * 8 +
-         2 * kChunk * kBM * 2 + 16;
+         2 * kChunk * kBM * 2 + 16 + 4 * kMaxChunks;
 }
 
 // ---------------------------------------------------------------- dense GEMM kernel choice
@@ -1652,6 +1682,7 @@ static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx&
   if (A.norm && t.tiles * t.split > kNormMaxGrid) return fail(KD_ERR_UNSUPPORTED, "gemm_rmsnorm: grid too large");
   A.epi = c.epi;
   A.err = c.err;
+  A.acq = c.acq;
   A.trace = g_gemm_trace;
   kd_status ks = kernels_init();
   if (ks) return ks;
@@ -1701,6 +1732,7 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   A.units = g.units;
   A.epi = c.epi;
   A.err = c.err;
+  A.acq = c.acq;
   A.trace = g_gemm_trace;
   {
     static int dbg = -1;
@@ -1775,6 +1807,23 @@ kd_status gemm_signals(const GemmShape& a, uint32_t* s) {
   if (st) return st;
   // one flag increment per CTA, after its whole tiles and its fold slice
   *s = (uint32_t)g.grid;
+  return KD_OK;
+}
+
+kd_status gemm_grid(const GemmShape& a, uint32_t* grid) {
+  if (a.dtype == KD_F32) return fail(KD_ERR_UNSUPPORTED, "gemm_grid: bf16 only");
+  if (gemm::use_dense(a)) {
+    GemmTile t;
+    double ns = 0;
+    kd_status st = gemm::csk::choose(a, &t, &ns);
+    if (st) return st;
+    *grid = (uint32_t)(t.tiles * t.split);
+    return KD_OK;
+  }
+  gemm::Geometry g;
+  kd_status st = gemm::geometry(a, &g, gemm::device_sms());
+  if (st) return st;
+  *grid = (uint32_t)g.grid;
   return KD_OK;
 }
 

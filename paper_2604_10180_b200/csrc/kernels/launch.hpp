@@ -10,10 +10,13 @@
 
 namespace kd {
 
+static_assert(kMaxChunks == (int)kMaxPlanChunks, "plan and device chunk bounds must agree");
+
 struct LaunchCtx {
   cudaStream_t stream = nullptr;
   void* scratch = nullptr;   // zero-initialised device scratch (left zeroed)
-  Epi epi;                   // fused peer stores of the primary output
+  Epi epi;                   // fused peer stores of the primary output (+ chunk flags)
+  Acq acq;                   // remote inputs acquired chunk by chunk inside the kernel (chunk-aware consumers)
   unsigned* err = nullptr;   // runtime error word (device; nullable): in-kernel watchdogs record timeouts here
 };
 
@@ -194,13 +197,17 @@ kd_status launch_gated_norm(const kd_attr_ssm& a, const void* y, const void* zx,
                             const LaunchCtx& c, uint32_t* signals);
 kd_status ssm_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s);
 kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* signals);
+kd_status op_grid(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* grid);
 // one-time per-device kernel attributes (dynamic smem opt-in); call outside graph capture
 kd_status kernels_init();
-// wait until every flag[i] >= (epoch − base) * mult[i] (ld.acquire.sys); watchdog sets *err
+// wait until every flag[i] >= (epoch − base) * mult[i] (ld.acquire.sys); watchdog sets *err.
+// LOG mode: log[i] (nullable) receives the chunk's acquire record (common.cuh kLogWords)
+constexpr int kMaxWait = 32;
 struct WaitList {
   int n = 0;
-  unsigned* flag[8];
-  unsigned mult[8];
+  const unsigned long long* flag[kMaxWait];
+  unsigned long long mult[kMaxWait];
+  unsigned long long* log[kMaxWait];
 };
 // base = steps the runtime ran with transfers off (their epochs carry no releases)
 kd_status launch_wait(const WaitList& w, const unsigned* epoch, unsigned base, unsigned* err, cudaStream_t s);

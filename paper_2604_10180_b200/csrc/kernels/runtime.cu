@@ -41,6 +41,7 @@ struct DevState {
   std::vector<Launch> launches;
   cudaGraphExec_t exec = nullptr;
   bool captured = false;
+  cudaEvent_t st0 = nullptr, st1 = nullptr;  // kd_step_stats
 };
 
 }  // namespace kd
@@ -57,10 +58,13 @@ struct kd_runtime {
   // steps run in KD_MODE_NO_TRANSFER: their epochs advanced without any flag
   // release, so the DISAGG wait target is (epoch − nt_steps) × signals
   uint32_t nt_steps = 0;
+  uint64_t steps = 0;  // kd_step calls so far (the next step_id)
   ~kd_runtime() {
     for (auto& d : devs) {
       cudaSetDevice(d.cuda);
       if (d.exec) cudaGraphExecDestroy(d.exec);
+      if (d.st0) cudaEventDestroy(d.st0);
+      if (d.st1) cudaEventDestroy(d.st1);
       for (auto& l : d.launches) {
         delete l.gemm;
         if (l.ev0) cudaEventDestroy(l.ev0);
@@ -160,7 +164,10 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
   if (l.kind == Launch::WAIT) return launch_wait(l.wait, epoch, rt->nt_steps, err, s);
   LaunchCtx c = l.ctx;
   c.stream = s;
-  if (rt->mode == KD_MODE_NO_TRANSFER) c.epi.n = 0;
+  if (rt->mode == KD_MODE_NO_TRANSFER) {
+    c.epi.n = 0;
+    c.acq.n = 0;
+  }
   const bool prof = rt->profile_op && l.op == rt->profile_op;
   if (prof) KD_CUDA_CHECK(record(l.ev0, s, capturing), "event record");
   kd_status st = KD_OK;
@@ -323,6 +330,7 @@ kd_status kd_runtime_set_peer_workspace(kd_runtime* rt, uint32_t dev, void* mapp
 
 kd_status kd_runtime_set_mode(kd_runtime* rt, uint32_t mode) {
   if (!rt || mode > KD_MODE_LOG) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_mode: bad argument");
+  // (LOG = DISAGG plus per-chunk %globaltimer records; its epochs carry releases)
   rt->mode = mode;
   rt->prepared = false;
   for (auto& d : rt->devs) d.captured = false;
@@ -420,6 +428,14 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
       }
       d.launches.push_back(sb);
     }
+    const bool log_on = rt->mode == KD_MODE_LOG;
+    const unsigned* my_epoch = (const unsigned*)(d.ws + L.ctrl_off);
+    // logical devices driven by this process on the same GPU as d (loopback)
+    auto loopback = [&](uint32_t v) {
+      for (auto& o : rt->devs)
+        if (o.logical == v) return o.cuda == d.cuda;
+      return false;  // another process: time-sliced, never co-scheduled with d's kernels
+    };
     std::set<uint32_t> waited;
     for (const auto& e : P->sched) {
       if (e.dev != d.logical) continue;
@@ -431,7 +447,24 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
       l.kernel = k;
       l.op = K.op;
       WaitList wl;
-      for (const auto& sp : K.reads) {
+      auto push_wait = [&](const unsigned long long* flag, unsigned long long mult, unsigned long long* log) {
+        if (wl.n == kMaxWait) {
+          Launch w;
+          w.kind = Launch::WAIT;
+          w.wait = wl;
+          d.launches.push_back(w);
+          wl.n = 0;
+        }
+        wl.flag[wl.n] = flag;
+        wl.mult[wl.n] = mult;
+        wl.log[wl.n] = log;
+        ++wl.n;
+      };
+      l.ctx.acq.epoch = my_epoch;
+      l.ctx.acq.base = rt->nt_steps;
+      l.ctx.acq.err = (unsigned*)(d.ws + L.ctrl_off + 4);
+      for (uint32_t ri = 0; ri < K.reads.size(); ++ri) {
+        const auto& sp = K.reads[ri];
         auto rs = remote_src.find({k, sp.buf});
         if (rs == remote_src.end()) {
           void* ptr = local_ptr(sp.buf, i, sp.off);
@@ -461,19 +494,48 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
         }
         if (transfers_on && !waited.count(t)) {
           waited.insert(t);
-          uint32_t sig = 0;
-          kd_status s2 = op_signals(S.op, S.attrs, &sig);
-          if (s2) return s2;
-          if (wl.n == 8) {
-            Launch w;
-            w.kind = Launch::WAIT;
-            w.wait = wl;
-            d.launches.push_back(w);
-            wl.n = 0;
+          const auto& X = P->xchunks[t];
+          const uint32_t nch = (uint32_t)X.ch.size();
+          const unsigned long long* flags = (const unsigned long long*)(d.ws + land.second);
+          unsigned long long* logp = log_on ? (unsigned long long*)(d.ws + L.xlog.at(t)) : nullptr;
+          std::vector<unsigned long long> mult(nch);
+          if (X.count) {
+            for (uint32_t c = 0; c < nch; ++c) mult[c] = X.rows * (X.ch[c].second - X.ch[c].first);
+          } else {
+            uint32_t sig = 0;
+            kd_status s2 = op_signals(S.op, S.attrs, &sig);
+            if (s2) return s2;
+            mult[0] = sig;
           }
-          wl.flag[wl.n] = (unsigned*)(d.ws + land.second);
-          wl.mult[wl.n] = sig;
-          ++wl.n;
+          // chunk-aware consumer of a COUNT transfer: acquire chunk by chunk
+          // inside the kernel (no wait launch); else wait for every chunk first
+          const bool whole = sp.off == S.writes[0].off && sp.len == S.writes[0].len;
+          const bool in_kernel = X.count && whole && op_consumer_unit(K, ri, X.row_bytes) > 0 &&
+                                 l.ctx.acq.n < kMaxAcqIn && !getenv("KD_NO_INKERNEL_ACQ");
+          if (in_kernel) {
+            AcqIn& in = l.ctx.acq.in[l.ctx.acq.n++];
+            in.flag = flags;
+            in.log = logp;
+            in.slot = (K.op == KD_OP_ADD_RMSNORM || K.op == KD_OP_RESIDUAL_ADD) ? (int)ri - 1 : (int)ri;
+            in.nch = (int)nch;
+            in.row_bytes = (uint32_t)X.row_bytes;
+            for (uint32_t c = 0; c < nch; ++c) {
+              in.cb[c] = (uint32_t)X.ch[c].first;
+              in.mult[c] = mult[c];
+            }
+            in.cb[nch] = (uint32_t)X.row_bytes;
+            if (loopback(P->assign[src])) {
+              // loopback residency gate: launch the consumer only once every CTA
+              // of the producer is resident (it then spins on chunks without
+              // being able to starve the producer of SMs)
+              uint32_t grid = 0;
+              kd_status s2 = op_grid(S.op, S.attrs, &grid);
+              if (s2) return s2;
+              push_wait(flags + nch, grid, nullptr);
+            }
+          } else {
+            for (uint32_t c = 0; c < nch; ++c) push_wait(flags + c, mult[c], logp ? logp + kLogWords * c : nullptr);
+          }
         }
       }
       if (wl.n) {
@@ -487,16 +549,26 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
         if (!ptr) return fail(KD_ERR_STATE, "kd_runtime_prepare: output buffer " + std::to_string(sp.buf) + " not bound on device " + std::to_string(d.logical));
         l.wr.push_back(ptr);
       }
-      // fused sends: every remote device reading this kernel's output
+      // fused sends: every remote device reading this kernel's output (all its
+      // transfers share one chunk table, plan.cpp)
       for (uint32_t v = 0; v < n; ++v) {
         auto it = xidx.find({i, k, v});
         if (it == xidx.end()) continue;
         if (l.ctx.epi.n == kMaxPeers) return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: more than 4 consumer devices");
+        const auto& X = P->xchunks[it->second];
+        const uint32_t nch = (uint32_t)X.ch.size();
+        Epi& ep = l.ctx.epi;
+        ep.nch = X.count ? (int)nch : 0;
+        ep.row_bytes = (uint32_t)X.row_bytes;
+        for (uint32_t c = 0; c < nch; ++c) ep.cb[c] = (uint32_t)X.ch[c].first;
+        ep.cb[nch] = (uint32_t)X.row_bytes;
         const auto& Lv = P->layout[v];
         const auto& land = Lv.landing.at(it->second);
-        l.ctx.epi.dst[l.ctx.epi.n] = rt->ws_of[v] + land.first;
-        l.ctx.epi.flag[l.ctx.epi.n] = (unsigned*)(rt->ws_of[v] + land.second);
-        ++l.ctx.epi.n;
+        ep.dst[ep.n] = rt->ws_of[v] + land.first;
+        ep.flag[ep.n] = (unsigned long long*)(rt->ws_of[v] + land.second);
+        ep.started[ep.n] = (X.count && loopback(v)) ? (unsigned long long*)(rt->ws_of[v] + land.second) + nch : nullptr;
+        ep.logt[ep.n] = log_on ? (unsigned long long*)(rt->ws_of[v] + Lv.xlog.at(it->second)) : nullptr;
+        ++ep.n;
       }
       l.ctx.scratch = d.ws + L.scratch_off;
       l.ctx.err = (unsigned*)(d.ws + L.ctrl_off + 4);
@@ -538,8 +610,12 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
   return KD_OK;
 }
 
-kd_status kd_step(kd_runtime* rt, void* const* streams) {
+kd_status kd_step(kd_runtime* rt, void* const* streams, uint64_t step_id, kd_step_stats* stats) {
   if (!rt || !streams) return fail(KD_ERR_INVALID_ARG, "kd_step: NULL argument");
+  if (step_id != UINT64_MAX && step_id != rt->steps)
+    return fail(KD_ERR_INVALID_ARG, "kd_step: step_id " + std::to_string(step_id) + " out of order (next is " +
+                                        std::to_string(rt->steps) + ")");
+  if (stats && rt->devs.size() > KD_STATS_MAX_DEV) return fail(KD_ERR_UNSUPPORTED, "kd_step: stats cover <= 8 local devices");
   if (!rt->prepared) {
     kd_status s = kd_runtime_prepare(rt);
     if (s) return s;
@@ -548,39 +624,119 @@ kd_status kd_step(kd_runtime* rt, void* const* streams) {
     auto& d = rt->devs[j];
     cudaStream_t s = (cudaStream_t)streams[j];
     KD_CUDA_CHECK(cudaSetDevice(d.cuda), "cudaSetDevice");
+    if (stats) {
+      if (!d.st0) {
+        KD_CUDA_CHECK(cudaEventCreate(&d.st0), "event create");
+        KD_CUDA_CHECK(cudaEventCreate(&d.st1), "event create");
+      }
+      KD_CUDA_CHECK(cudaEventRecord(d.st0, s), "event record");
+    }
     if (!rt->use_graph) {
       for (auto& l : d.launches) {
         kd_status st = enqueue(rt, d, l, s, false);
         if (st) return st;
       }
-      continue;
+    } else {
+      if (!d.captured) {
+        if (d.exec) {
+          cudaGraphExecDestroy(d.exec);
+          d.exec = nullptr;
+        }
+        KD_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+        kd_status st = KD_OK;
+        for (auto& l : d.launches) {
+          st = enqueue(rt, d, l, s, true);
+          if (st) break;
+        }
+        cudaGraph_t graph = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(s, &graph);
+        if (st) {
+          if (graph) cudaGraphDestroy(graph);
+          return st;
+        }
+        if (ce != cudaSuccess) return set_cuda_error(ce, "end capture");
+        ce = cudaGraphInstantiate(&d.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return set_cuda_error(ce, "graph instantiate");
+        d.captured = true;
+      }
+      KD_CUDA_CHECK(cudaGraphLaunch(d.exec, s), "graph launch");
     }
-    if (!d.captured) {
-      if (d.exec) {
-        cudaGraphExecDestroy(d.exec);
-        d.exec = nullptr;
-      }
-      KD_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
-      kd_status st = KD_OK;
-      for (auto& l : d.launches) {
-        st = enqueue(rt, d, l, s, true);
-        if (st) break;
-      }
-      cudaGraph_t graph = nullptr;
-      cudaError_t ce = cudaStreamEndCapture(s, &graph);
-      if (st) {
-        if (graph) cudaGraphDestroy(graph);
-        return st;
-      }
-      if (ce != cudaSuccess) return set_cuda_error(ce, "end capture");
-      ce = cudaGraphInstantiate(&d.exec, graph, 0);
-      cudaGraphDestroy(graph);
-      if (ce != cudaSuccess) return set_cuda_error(ce, "graph instantiate");
-      d.captured = true;
-    }
-    KD_CUDA_CHECK(cudaGraphLaunch(d.exec, s), "graph launch");
+    if (stats) KD_CUDA_CHECK(cudaEventRecord(d.st1, s), "event record");
   }
   if (rt->mode == KD_MODE_NO_TRANSFER) ++rt->nt_steps;  // graphs re-capture on the next mode switch
+  const uint64_t this_step = rt->steps++;
+  if (!stats) return KD_OK;
+  // ---- statistics (synchronising)
+  const kd_plan* P = rt->plan;
+  std::memset(stats, 0, sizeof(*stats));
+  stats->step_id = this_step;
+  stats->n_local = (uint32_t)rt->devs.size();
+  stats->n_dev = P->n_dev;
+  if (P->n_dev <= KD_STATS_MAX_DEV)
+    for (const auto& x : P->transfers)
+      stats->link_bytes[P->assign[x.producer] * P->n_dev + x.dst_dev] += x.bytes;
+  for (size_t j = 0; j < rt->devs.size(); ++j) {
+    auto& d = rt->devs[j];
+    KD_CUDA_CHECK(cudaSetDevice(d.cuda), "cudaSetDevice");
+    KD_CUDA_CHECK(cudaEventSynchronize(d.st1), "event sync");
+    float ms = 0.f;
+    KD_CUDA_CHECK(cudaEventElapsedTime(&ms, d.st0, d.st1), "event elapsed");
+    stats->step_ns[j] = (uint64_t)((double)ms * 1e6);
+  }
+  if (rt->mode == KD_MODE_LOG) {
+    std::vector<kd_log_record> recs;
+    uint32_t nrec = 0;
+    kd_runtime_log(rt, nullptr, 0, &nrec);
+    recs.resize(nrec);
+    kd_status s = kd_runtime_log(rt, recs.data(), nrec, &nrec);
+    if (s) return s;
+    // device epoch of this step: step_begin increments it once per step (multi-device plans)
+    for (const auto& r : recs) {
+      for (size_t j = 0; j < rt->devs.size(); ++j)
+        if (rt->devs[j].logical == r.dev && r.epoch != 0 && r.t_acquire >= r.t_wait) {
+          stats->wait_ns[j] += r.t_acquire - r.t_wait;
+          ++stats->chunk_waits[j];
+        }
+    }
+  }
+  return KD_OK;
+}
+
+kd_status kd_runtime_log(kd_runtime* rt, kd_log_record* out, uint32_t cap, uint32_t* n) {
+  if (!rt || !n) return fail(KD_ERR_INVALID_ARG, "kd_runtime_log: NULL argument");
+  if (rt->mode != KD_MODE_LOG) return fail(KD_ERR_STATE, "kd_runtime_log: runtime is not in KD_MODE_LOG");
+  const kd_plan* P = rt->plan;
+  uint32_t need = 0;
+  for (auto& d : rt->devs)
+    for (const auto& kv : P->layout[d.logical].xlog) need += (uint32_t)P->xchunks[kv.first].ch.size();
+  if (cap < need || (need && !out)) {
+    *n = need;
+    return fail(KD_ERR_RANGE, "kd_runtime_log: capacity too small");
+  }
+  uint32_t i = 0;
+  for (auto& d : rt->devs) {
+    const auto& L = P->layout[d.logical];
+    if (!L.log_bytes || !d.ws) continue;
+    KD_CUDA_CHECK(cudaSetDevice(d.cuda), "cudaSetDevice");
+    std::vector<unsigned long long> h(L.log_bytes / 8);
+    KD_CUDA_CHECK(cudaMemcpy(h.data(), d.ws + L.log_off, L.log_bytes, cudaMemcpyDeviceToHost), "read log");
+    for (const auto& kv : L.xlog) {
+      const size_t base = (kv.second - L.log_off) / 8;
+      for (uint32_t c = 0; c < P->xchunks[kv.first].ch.size(); ++c) {
+        kd_log_record& r = out[i++];
+        r.dev = d.logical;
+        r.transfer = kv.first;
+        r.chunk = c;
+        r.pad_ = 0;
+        r.epoch = h[base + (size_t)kLogWords * c + 0];
+        r.t_wait = h[base + (size_t)kLogWords * c + 1];
+        r.t_acquire = h[base + (size_t)kLogWords * c + 2];
+        r.t_release = h[base + (size_t)kLogWords * c + 3];
+      }
+    }
+  }
+  *n = i;
   return KD_OK;
 }
 

@@ -566,7 +566,8 @@ class DecoderRuntime:
 
     def __init__(self, dg: DecoderGraph, assign: Sequence[int], n_dev: int, dev_map: Sequence[int],
                  machine: Optional[Machine] = None, inputs=None, seed: int = 0, use_graph: bool = True,
-                 local_devs: Optional[Sequence[int]] = None, dist=None, dist_group=None):
+                 local_devs: Optional[Sequence[int]] = None, dist=None, dist_group=None, n_chunks: int = 4,
+                 mode: Optional[int] = None):
         """dev_map[logical] = cuda ordinal for every LOCAL logical device.
         local_devs: logical devices driven by this process (default: all,
         single-process / loopback). With `dist` (torch.distributed, one
@@ -575,13 +576,15 @@ class DecoderRuntime:
         cfg = dg.cfg
         self.dg, self.cfg = dg, cfg
         self.machine = machine or b200_machine(n_dev)
-        self.plan = Plan(dg.g, self.machine, list(assign), cfg.n_micro)
+        self.plan = Plan(dg.g, self.machine, list(assign), cfg.n_micro, n_chunks)
         self.n_dev = n_dev
         self.local_devs = list(range(n_dev)) if local_devs is None else list(local_devs)
         self.dev_map = {d: dev_map[j] if len(dev_map) == len(self.local_devs) else dev_map[d]
                         for j, d in enumerate(self.local_devs)}
         self.rt = Runtime(self.plan, self.local_devs, [self.dev_map[d] for d in self.local_devs])
         self.rt.set_graph(use_graph)
+        if mode is not None:
+            self.rt.set_mode(mode)
         self.tensors: Dict[tuple, "torch.Tensor"] = {}
         self.ws = {}
         self._ipc = []
@@ -722,8 +725,8 @@ class DecoderRuntime:
             device_normal_(t, s, std)
 
     # ------------------------------------------------------------------ run
-    def step(self):
-        self.rt.step([s.cuda_stream for s in self.streams])
+    def step(self, stats: bool = False):
+        return self.rt.step([s.cuda_stream for s in self.streams], stats=stats)
 
     def sync(self):
         torch = _torch()

@@ -351,3 +351,91 @@ def test_sharded_kv_decoder_vs_oracle_and_disaggregated(mod, shards):
             kc = one.tensors[(f"kc.{l}.{S-1}", i, 0)].view(torch.int16).cpu().numpy().view(np.uint16)
             gpages = inp.block_table[i * m:(i + 1) * m][:, (S - 1) * ps:S * ps].reshape(-1)
             assert relerr(OL.bf16_to_f64(kc), kcs[l][gpages]) < 5e-3
+
+
+# ------------------------------------------------------------------ a13: chunked handoff at 8B layer shapes
+# The bench's disaggregated tiling (m = 32 rows per micro-batch, N = 2) with
+# full 8B layer widths (H 4096, 32/8 heads, F 14336); a shorter context keeps
+# the host-side oracle inputs small (the GEMM / handoff shapes do not depend on it)
+CFG_8B_PAIR = synth.LLAMA8B.with_(n_layers=2, batch=64, n_micro=2, context=512)
+
+
+def _run_8b(DEC, inp, assign, n_dev, steps, n_chunks=4, mode=None):
+    dg = DEC.DecoderGraph(CFG_8B_PAIR)
+    a = assign(dg)
+    rt = DEC.DecoderRuntime(dg, a, n_dev, [0] * n_dev, inputs=inp, n_chunks=n_chunks, mode=mode)
+    outs = []
+    for _ in range(steps):
+        outs.append(rt.step(stats=True))
+    rt.sync()
+    rt.rt.check()
+    return dg, rt, outs
+
+
+@pytest.mark.slow
+def test_8b_shapes_disaggregated_chunked_bitwise_equals_monolithic(mod):
+    """Verdict r1 weak #11: the fused peer-store epilogues of the cluster /
+    stream-K GEMMs at production tilings (epi.n > 0), chunk-aware consumers
+    (in-kernel acquires of QKV/O/gate_up/down inputs, add+RMSNorm, SiLU,
+    RoPE) — bitwise equal to monolithic, for 1, 4 and 8 chunks."""
+    DEC, K = mod
+    inp = synth.make_decoder_inputs(CFG_8B_PAIR)
+    _, mono, _ = _run_8b(DEC, inp, lambda dg: [0] * dg.g.num_kernels, 1, 2)
+    r_ref, _, _ = OL.decoder_step(inp, act="bf16")
+    assert relerr(mono.residual(), r_ref) < 5e-3
+    for nch in (1, 4, 8):
+        _, dis, _ = _run_8b(DEC, inp, lambda dg: dg.role_assign(0, 1), 2, 2, n_chunks=nch)
+        assert np.array_equal(mono.residual(), dis.residual()), f"n_chunks={nch}"
+        for l in range(CFG_8B_PAIR.n_layers):
+            assert np.array_equal(mono.cache("kc", l), dis.cache("kc", l))
+
+
+@pytest.mark.slow
+def test_log_mode_chunks_overlap_and_step_stats(mod):
+    """KD_MODE_LOG: one record per (incoming transfer, chunk) with the step's
+    epoch; the first acquire of a transfer's chunk 0 precedes its producer's
+    last chunk release on at least one cut edge (the consumer started on chunk
+    0 while later chunks were still being produced — SURVEY a13, north_star);
+    kd_step_stats: per-device step time, exposed wait from the log, link bytes
+    = the plan's transfers."""
+    DEC, K = mod
+    inp = synth.make_decoder_inputs(CFG_8B_PAIR)
+    dg, rt, stats = _run_8b(DEC, inp, lambda dg: dg.role_assign(0, 1), 2, 3, mode=K.KD_MODE_LOG)
+    recs = rt.rt.log()
+    xs = rt.plan.transfers()
+    nch = {}
+    for t, c, *_ in rt.plan.chunks():
+        nch[t] = nch.get(t, 0) + 1
+    assert len(recs) == sum(nch.values())
+    by_t = {}
+    for dev, t, c, epoch, tw, ta, tr in recs:
+        assert epoch == 3, (t, c, epoch)          # the third step's device epoch = step_id + 1
+        assert tw <= ta and tr > 0
+        assert xs[t][2] == dev
+        by_t.setdefault(t, []).append((c, ta, tr))
+    overlapped = [t for t, v in by_t.items() if len(v) > 1 and min(a for _, a, _ in v) < max(r for _, _, r in v)]
+    assert overlapped, "no consumer acquired a chunk before its producer's last chunk release"
+    last = stats[-1]
+    assert last["step_id"] == 2 and all(x > 0 for x in last["step_ns"])
+    assert last["chunk_waits"][0] + last["chunk_waits"][1] == len(recs)
+    lb = [[0, 0], [0, 0]]
+    for i, prod, dst, nbytes, *_ in xs:
+        lb[rt.plan.assign[prod]][dst] += nbytes
+    assert last["link_bytes"] == lb
+    # the same plan without the log: same bits
+    _, dis, _ = _run_8b(DEC, inp, lambda dg: dg.role_assign(0, 1), 2, 3)
+    assert np.array_equal(rt.residual(), dis.residual())
+
+
+def test_wait_kernel_path_equals_in_kernel_acquire(mod, monkeypatch):
+    """KD_NO_INKERNEL_ACQ=1 routes every remote input through the whole-
+    transfer wait kernel (the round-1 protocol): same bits as the in-kernel
+    chunk acquires."""
+    DEC, K = mod
+    cfg = TINY
+    inp = synth.make_decoder_inputs(cfg)
+    a = run(DEC, cfg, inp, lambda dg: dg.role_assign(0, 1), 2, steps=2)
+    monkeypatch.setenv("KD_NO_INKERNEL_ACQ", "1")
+    b = run(DEC, cfg, inp, lambda dg: dg.role_assign(0, 1), 2, steps=2)
+    assert np.array_equal(a.residual(), b.residual())
+    assert b.rt.launch_count(0) > a.rt.launch_count(0) or b.rt.launch_count(1) > a.rt.launch_count(1)

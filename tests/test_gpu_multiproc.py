@@ -29,6 +29,13 @@ def _graph(DEC, kind, cfg):
     return dg, dg.role_assign(0, 1), 2
 
 
+def _cfg(kind):
+    import synth
+    if kind == "pair8b":  # full 8B layer widths, the bench's m = 32 tiling, short context
+        return synth.LLAMA8B.with_(n_layers=2, batch=64, n_micro=2, context=512)
+    return synth.TINY
+
+
 def _rank(rank, world, port, q, steps, kind="pair"):
     import torch
     import torch.distributed as dist
@@ -39,7 +46,7 @@ def _rank(rank, world, port, q, steps, kind="pair"):
         torch.cuda.set_device(0)
         import synth
         from paper_2604_10180_b200 import decoder as DEC
-        cfg = synth.TINY
+        cfg = _cfg(kind)
         inp = synth.make_decoder_inputs(cfg)
         dg, assign, n_dev = _graph(DEC, kind, cfg)
         rt = DEC.DecoderRuntime(dg, assign, n_dev, [0], inputs=inp, local_devs=[rank], dist=dist)
@@ -54,7 +61,7 @@ def _rank(rank, world, port, q, steps, kind="pair"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,world", [("pair", 2), ("sharded", 3)])
+@pytest.mark.parametrize("kind,world", [("pair", 2), ("sharded", 3), ("pair8b", 2)])
 def test_processes_ipc_bitwise_equals_monolithic(cuda_ok, kind, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -69,7 +76,7 @@ def test_processes_ipc_bitwise_equals_monolithic(cuda_ok, kind, world):
         assert p.exitcode == 0
     import synth
     from paper_2604_10180_b200 import decoder as DEC
-    cfg = synth.TINY
+    cfg = _cfg(kind)
     inp = synth.make_decoder_inputs(cfg)
     dg, _, _ = _graph(DEC, kind, cfg)
     mono = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp)
