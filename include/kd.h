@@ -250,6 +250,37 @@ kd_status kd_objective(const kd_graph* g, const kd_machine* m, const int32_t* as
 kd_status kd_place(const kd_graph* g, const kd_machine* m, const kd_place_opts* opts,
                    int32_t* assign, int64_t* objective_ps, uint64_t* nodes_visited);
 
+/* Device-role search (SURVEY §8(a) a1 "search over device roles"; the E6
+ * throughput objective, evaluated over role layouts). `g` is ONE
+ * memory shard's step graph with rows_per_micro rows per micro-batch. A layout
+ * puts every template class (A15) in the memory role or the GEMM role (pins:
+ * pin_device 0 = memory, 1 = GEMM) and runs it on `a` memory-role GPUs (each
+ * its own rows: sequences are sharded) and `gr` GEMM-role GPUs (weights split
+ * over them, all a·rows rows per micro-batch), with N micro-batches:
+ *   memory kernel   t = max(⌈(W + A)·10¹²/HBM⌉, ⌈F·10¹²/TC⌉) + launch
+ *   GEMM-role kernel t = max(⌈(⌈W/gr⌉ + a·A)·10¹²/HBM⌉, ⌈⌈a·F/gr⌉·10¹²/TC⌉) + launch
+ * (W = bytes of its WEIGHT spans, A = its other bytes, F = flops);
+ * T_mem = N·Σ t_mem, T_gemm = N·Σ t_gemm; per cut edge of d bytes,
+ * memory → GEMM: M_gemm += N·a·(ℓ + ⌈d·10¹²/bw⌉), GEMM → memory:
+ * M_mem += N·gr·(ℓ + ⌈⌈d/gr⌉·10¹²/bw⌉); step period = max of the four (N ≥ 2)
+ * or their sum (N = 1: nothing overlaps inside one step, R8). gpus = 1 is the
+ * monolithic layout (a = 1, gr = 0, no transfers). For every gpus ∈ {1,2,4,8},
+ * gpus ≤ max_gpus, the layout with the most tokens per second per GPU
+ * (a·N·rows / (gpus·period)) is returned, ties → smallest (a, N, role mask)
+ * (mask bit c = class c in the GEMM role, classes in first-use order). The
+ * machine's device 0 HBM/TC and link 0→1 are used (homogeneous NVSwitch box).
+ * roles receives K values per returned layout (0 memory, 1 GEMM). At most 20
+ * free classes (KD_ERR_UNSUPPORTED otherwise). */
+typedef struct {
+  uint32_t gpus, a, gr, n_micro;
+  int64_t period_ps;
+  int64_t T_mem_ps, T_gemm_ps, M_mem_ps, M_gemm_ps;
+  uint64_t tokens_per_step;   /* a · N · rows_per_micro */
+  uint64_t role_mask;
+} kd_role_layout;
+kd_status kd_place_roles(const kd_graph* g, const kd_machine* m, uint32_t rows_per_micro, uint32_t max_gpus,
+                         uint32_t micro_mask, kd_role_layout* best, int32_t* roles, uint32_t cap, uint32_t* n_out);
+
 /* ------------------------------------------------------------------ online monitor
  * Queueing-aware policy switching (§3.4): requests are
  * attributed to the fixed window ⌊t_end/W⌋ in which they finish; at each window

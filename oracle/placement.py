@@ -141,3 +141,85 @@ def place_all_assignments(kernels, flops, edges, m: Machine, n_micro: int):
         if best is None or obj < best[1]:
             best = (list(assign), obj)
     return best
+
+
+# ---------------------------------------------------------------- device-role search
+def place_roles(kernels, flops, templates, pins, weight_bufs, edges, hbm: int, tc: int, link_Bps: int,
+                link_lat_ps: int, launch_ps: int, rows: int, max_gpus: int, micro_mask: int):
+    """Exhaustive device-role search: for every GPU count n in {1, 2, 4, 8}
+    (n <= max_gpus), every split n = a memory-role + gr GEMM-role GPUs, every
+    allowed N = 2^j (micro_mask bit j) and every memory/GEMM role of each
+    free template class, evaluate the E6 step period of that layout and keep
+    the most tokens per GPU-second (a·N·rows/(n·period)); ties keep the first
+    in (a, N, mask) order. A memory-role kernel runs on each of the `a` GPUs
+    over its own `rows` rows: t = max(⌈(W+A)·10¹²/hbm⌉, ⌈F·10¹²/tc⌉) + launch;
+    a GEMM-role kernel runs once per micro-batch over a·rows rows with its
+    weights split over the gr GPUs: t = max(⌈(⌈W/gr⌉ + a·A)·10¹²/hbm⌉,
+    ⌈⌈a·F/gr⌉·10¹²/tc⌉) + launch (W = weight-span bytes, A = other bytes).
+    A cut edge of d bytes costs, per micro-batch, a·(ℓ + ⌈d·10¹²/bw⌉) at the
+    GEMM side (each GEMM GPU gathers every shard) or gr·(ℓ + ⌈⌈d/gr⌉·10¹²/bw⌉)
+    at the memory side. Period = max(T_mem, T_gemm, M_mem, M_gemm)·… for
+    N >= 2, their sum for N = 1 (R8). n = 1 is monolithic (a = 1, no GEMM
+    role). pins: -1 free, 0 memory, 1 GEMM. Returns, per n, (n, a, gr, N,
+    period, T_mem, T_gemm, M_mem, M_gemm, tokens, mask, roles[K])."""
+    K = len(kernels)
+    order: Dict[Tuple[int, int], int] = {}
+    cls = []
+    for k in range(K):
+        key = (0, templates[k]) if templates[k] >= 0 else (1, k)
+        if key not in order:
+            order[key] = len(order)
+        cls.append(order[key])
+    C = len(order)
+    fixed = [-1] * C
+    for k in range(K):
+        if pins[k] >= 0:
+            fixed[cls[k]] = pins[k]
+    free = [c for c in range(C) if fixed[c] < 0]
+    W, A = [], []
+    for reads, writes in kernels:
+        W.append(span_bytes([s for s in list(reads) + list(writes) if s[0] in weight_bufs]))
+        A.append(span_bytes([s for s in reads if s[0] not in weight_bufs]) +
+                 span_bytes([s for s in writes if s[0] not in weight_bufs]))
+    d = edge_bytes(edges)
+
+    def t(b, f):
+        return max(ceil_div(b * PS, hbm), ceil_div(f * PS, tc)) + launch_ps
+
+    out = []
+    for n in (1, 2, 4, 8):
+        if n > max_gpus:
+            continue
+        best = None
+        for a in ([1] if n == 1 else range(1, n)):
+            gr = n - a
+            for j in range(3):
+                if not micro_mask >> j & 1:
+                    continue
+                N = 1 << j
+                for mask in range(1 if n == 1 else 1 << len(free)):
+                    role = [0] * C
+                    if n > 1:
+                        for c in range(C):
+                            role[c] = 1 if fixed[c] == 1 else 0
+                        for b, c in enumerate(free):
+                            role[c] = mask >> b & 1
+                    Tm = sum(t(W[k] + A[k], flops[k]) for k in range(K) if role[cls[k]] == 0)
+                    Tg = sum(t(ceil_div(W[k], gr) + a * A[k], ceil_div(a * flops[k], gr))
+                             for k in range(K) if role[cls[k]] == 1)
+                    Mm = Mg = 0
+                    for (i, jj), nbytes in d.items():
+                        ri, rj = role[cls[i]], role[cls[jj]]
+                        if ri == rj:
+                            continue
+                        if rj == 1:
+                            Mg += a * (link_lat_ps + ceil_div(nbytes * PS, link_Bps))
+                        else:
+                            Mm += gr * (link_lat_ps + ceil_div(ceil_div(nbytes, gr) * PS, link_Bps))
+                    Tm, Tg, Mm, Mg = N * Tm, N * Tg, N * Mm, N * Mg
+                    period = Tm + Tg + Mm + Mg if N == 1 else max(Tm, Tg, Mm, Mg)
+                    tok = a * N * rows
+                    if best is None or tok * best[4] > best[9] * period:
+                        best = (n, a, gr, N, period, Tm, Tg, Mm, Mg, tok, mask, [role[cls[k]] for k in range(K)])
+        out.append(best)
+    return out

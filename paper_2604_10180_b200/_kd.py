@@ -165,6 +165,12 @@ class kd_log_record(C.Structure):
                 ("epoch", C.c_uint64), ("t_wait", C.c_uint64), ("t_acquire", C.c_uint64), ("t_release", C.c_uint64)]
 
 
+class kd_role_layout(C.Structure):
+    _fields_ = [("gpus", C.c_uint32), ("a", C.c_uint32), ("gr", C.c_uint32), ("n_micro", C.c_uint32),
+                ("period_ps", C.c_int64), ("T_mem_ps", C.c_int64), ("T_gemm_ps", C.c_int64), ("M_mem_ps", C.c_int64),
+                ("M_gemm_ps", C.c_int64), ("tokens_per_step", C.c_uint64), ("role_mask", C.c_uint64)]
+
+
 P = C.c_void_p
 u32, i32, u64, i64 = C.c_uint32, C.c_int32, C.c_uint64, C.c_int64
 PU32, PI32, PU64, PI64 = C.POINTER(u32), C.POINTER(i32), C.POINTER(u64), C.POINTER(i64)
@@ -185,6 +191,8 @@ _PROTOS = {
     "kd_objective": (kd_status, [P, C.POINTER(kd_machine), PI32, u32, u32, PI64, PI64, PI64]),
     "kd_place": (kd_status, [P, C.POINTER(kd_machine), C.POINTER(kd_place_opts), PI32, PI64, PU64]),
     "kd_chunks": (kd_status, [u64, u64, u32, PU64, u32, PU32]),
+    "kd_place_roles": (kd_status, [P, C.POINTER(kd_machine), u32, u32, u32, C.POINTER(kd_role_layout), PI32, u32,
+                                   PU32]),
     "kd_plan_create": (kd_status, [P, C.POINTER(kd_machine), PI32, u32, u32, C.POINTER(P)]),
     "kd_plan_chunks": (kd_status, [P, C.POINTER(kd_chunk), u32, PU32]),
     "kd_plan_destroy": (None, [P]),

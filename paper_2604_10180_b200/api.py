@@ -29,6 +29,8 @@ class Graph:
         # the declarations as given (op, reads, writes, attrs): introspection
         # for tests that restate the plan's rules independently
         self.decl = []
+        self._desc = []       # (flops, template, pin) per kernel
+        self._buf_flags = []  # flags per buffer
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -38,6 +40,7 @@ class Graph:
     def add_buffer(self, nbytes: int, flags: int = 0) -> int:
         i = C.c_uint32()
         check(K.kd_graph_add_buffer(self.h, int(nbytes), int(flags), C.byref(i)), "kd_graph_add_buffer")
+        self._buf_flags.append(int(flags))
         return i.value
 
     def add_kernel(self, op: int, reads: Sequence[Span], writes: Sequence[Span], attrs=None, flops: int = 0,
@@ -54,6 +57,7 @@ class Graph:
         i = C.c_uint32()
         check(K.kd_graph_add_kernel(self.h, C.byref(d), C.byref(i)), "kd_graph_add_kernel")
         self.decl.append((op, [tuple(x) for x in reads], [tuple(x) for x in writes], attrs))
+        self._desc.append((int(flops), int(template), int(pin)))
         return i.value
 
     def finalize(self):
@@ -88,6 +92,9 @@ class Machine:
         self.m = K.kd_machine(n, 0, self._hbm, self._tc, self._bw, self._lat, int(launch_ps))
         self.hbm_Bps, self.tc_flops = list(hbm_Bps), list(tc_flops)
         self.link_Bps, self.link_lat_ps, self.launch_ps = link_Bps, link_lat_ps, launch_ps
+        # the constants kd_place_roles reads (device 0, link 0 → 1)
+        self.py = {"hbm": int(hbm_Bps[0]), "tc": int(tc_flops[0]), "bw": int(link_Bps[0][1]) if n > 1 else 1,
+                   "lat": int(link_lat_ps[0][1]) if n > 1 else 0, "launch": int(launch_ps)}
 
     @classmethod
     def uniform(cls, n, hbm_Bps, tc_flops, link_Bps, link_lat_ps, launch_ps):
@@ -118,6 +125,26 @@ def place(g: Graph, m: Machine, n_micro: int, obj: int = K.KD_OBJ_AUTO, max_node
     nodes = C.c_uint64()
     check(K.kd_place(g.h, C.byref(m.m), C.byref(opts), a, C.byref(o), C.byref(nodes)), "kd_place")
     return list(a), o.value, nodes.value
+
+
+def place_roles(g: Graph, m: Machine, rows_per_micro: int, max_gpus: int = 8, micro_mask: int = 0b111):
+    """kd_place_roles: the best memory/GEMM role layout per GPU count
+    (1, 2, 4, 8 ≤ max_gpus). Returns a list of dicts (gpus, a, gr, n_micro,
+    period_ps, T/M per role, tokens_per_step, role_mask, roles[K])."""
+    K_ = g.num_kernels
+    best = (K.kd_role_layout * 4)()
+    roles = (C.c_int32 * (4 * K_))()
+    n = C.c_uint32()
+    check(K.kd_place_roles(g.h, C.byref(m.m), rows_per_micro, max_gpus, micro_mask, best, roles, 4, C.byref(n)),
+          "kd_place_roles")
+    out = []
+    for i in range(n.value):
+        b = best[i]
+        out.append({"gpus": b.gpus, "a": b.a, "gr": b.gr, "n_micro": b.n_micro, "period_ps": b.period_ps,
+                    "T_mem_ps": b.T_mem_ps, "T_gemm_ps": b.T_gemm_ps, "M_mem_ps": b.M_mem_ps,
+                    "M_gemm_ps": b.M_gemm_ps, "tokens_per_step": b.tokens_per_step, "role_mask": b.role_mask,
+                    "roles": list(roles[i * K_:(i + 1) * K_])})
+    return out
 
 
 class Monitor:

@@ -235,6 +235,116 @@ kd_status kd_place(const kd_graph* g, const kd_machine* m, const kd_place_opts* 
   return KD_OK;
 }
 
+kd_status kd_place_roles(const kd_graph* g, const kd_machine* m, uint32_t rows, uint32_t max_gpus, uint32_t micro_mask,
+                         kd_role_layout* best, int32_t* roles, uint32_t cap, uint32_t* n_out) {
+  if (!g || !best || !roles || !n_out) return fail(KD_ERR_INVALID_ARG, "kd_place_roles: NULL argument");
+  if (!g->finalized) return fail(KD_ERR_STATE, "kd_place_roles: graph not finalized");
+  if (!machine_valid(m) || rows == 0 || max_gpus == 0 || (micro_mask & 7u) == 0)
+    return fail(KD_ERR_INVALID_ARG, "kd_place_roles: invalid machine/rows/max_gpus/micro_mask");
+  const uint32_t K = (uint32_t)g->kernels.size();
+  // classes in first-use order; pins fix the role (0 memory, 1 GEMM)
+  std::vector<uint32_t> cls_of(K);
+  std::map<std::pair<int, int64_t>, uint32_t> key2cls;
+  for (uint32_t k = 0; k < K; ++k) {
+    int tid = g->kernels[k].tmpl;
+    auto key = tid >= 0 ? std::make_pair(0, (int64_t)tid) : std::make_pair(1, (int64_t)k);
+    auto it = key2cls.find(key);
+    if (it == key2cls.end()) it = key2cls.emplace(key, (uint32_t)key2cls.size()).first;
+    cls_of[k] = it->second;
+  }
+  const uint32_t C = (uint32_t)key2cls.size();
+  std::vector<int32_t> fixed(C, -1);
+  for (uint32_t k = 0; k < K; ++k) {
+    const int32_t p = g->kernels[k].pin;
+    if (p < 0) continue;
+    if (p > 1) return fail(KD_ERR_INVALID_ARG, "kd_place_roles: a pin must name a role (0 memory, 1 GEMM)");
+    if (fixed[cls_of[k]] >= 0 && fixed[cls_of[k]] != p) return fail(KD_ERR_PIN_CONFLICT, "kd_place_roles: conflicting pins");
+    fixed[cls_of[k]] = p;
+  }
+  std::vector<uint32_t> free_cls;
+  for (uint32_t c = 0; c < C; ++c)
+    if (fixed[c] < 0) free_cls.push_back(c);
+  if (free_cls.size() > 20) return fail(KD_ERR_UNSUPPORTED, "kd_place_roles: more than 20 free template classes");
+  const u64 hbm = m->hbm_Bps[0], tc = m->tc_flops[0];
+  const bool has_link = m->n_dev > 1;
+  const u64 bw = has_link ? m->link_Bps[1] : 1, lat = has_link ? m->link_lat_ps[1] : 0;
+  // per kernel: weight bytes, other bytes, flops
+  std::vector<u64> wb(K), ab(K), fl(K);
+  for (uint32_t k = 0; k < K; ++k) {
+    const Kernel& Kk = g->kernels[k];
+    std::vector<Span> wr, rd, wo;
+    for (const auto& sp : Kk.reads) (g->buffers[sp.buf].flags & KD_BUF_WEIGHT ? wr : rd).push_back(sp);
+    for (const auto& sp : Kk.writes) (g->buffers[sp.buf].flags & KD_BUF_WEIGHT ? wr : wo).push_back(sp);
+    wb[k] = union_bytes(wr);
+    ab[k] = union_bytes(rd) + union_bytes(wo);
+    fl[k] = Kk.flops;
+  }
+  auto t_of = [&](u64 bytes, u64 flops) -> i64 {
+    return (i64)(std::max(ceil_div_u128((u128)bytes * kPs, hbm), ceil_div_u128((u128)flops * kPs, tc)) + m->launch_ps);
+  };
+  const auto pairs = edge_pairs(*g);
+  const uint32_t counts[4] = {1, 2, 4, 8};
+  uint32_t nout = 0;
+  for (uint32_t gpus : counts) {
+    if (gpus > max_gpus || (gpus > 1 && !has_link)) continue;
+    if (nout == cap) {
+      *n_out = nout;
+      return fail(KD_ERR_RANGE, "kd_place_roles: capacity too small");
+    }
+    kd_role_layout bl{};
+    bool have = false;
+    std::vector<int32_t> brole(K, 0);
+    const uint32_t a_lo = gpus == 1 ? 1 : 1, a_hi = gpus == 1 ? 1 : gpus - 1;
+    for (uint32_t a = a_lo; a <= a_hi; ++a) {
+      const uint32_t gr = gpus - a;
+      for (uint32_t j = 0; j < 3; ++j) {
+        if (!(micro_mask & (1u << j))) continue;
+        const i64 N = (i64)1 << j;
+        const uint64_t n_masks = gpus == 1 ? 1 : (1ull << free_cls.size());
+        for (uint64_t mask = 0; mask < n_masks; ++mask) {
+          std::vector<uint8_t> role_c(C, 0);
+          for (uint32_t c = 0; c < C; ++c) role_c[c] = fixed[c] > 0 ? 1 : 0;
+          if (gpus > 1)
+            for (size_t b = 0; b < free_cls.size(); ++b) role_c[free_cls[b]] = (mask >> b) & 1;
+          else
+            std::fill(role_c.begin(), role_c.end(), 0);
+          i64 Tm = 0, Tg = 0, Mm = 0, Mg = 0;
+          for (uint32_t k = 0; k < K; ++k) {
+            if (!role_c[cls_of[k]]) {
+              Tm += t_of(wb[k] + ab[k], fl[k]);
+            } else {
+              Tg += t_of(ceil_div(wb[k], gr) + (u64)a * ab[k], ceil_div((u64)a * fl[k], gr));
+            }
+          }
+          for (const auto& e : pairs) {
+            const uint8_t ri = role_c[cls_of[e.first.first]], rj = role_c[cls_of[e.first.second]];
+            if (ri == rj) continue;
+            if (rj == 1)  // memory -> GEMM: every GEMM GPU gathers all a shards' rows
+              Mg += (i64)a * (i64)(lat + ceil_div_u128((u128)e.second * kPs, bw));
+            else          // GEMM -> memory: every memory GPU receives from the gr GEMM GPUs
+              Mm += (i64)gr * (i64)(lat + ceil_div_u128((u128)ceil_div(e.second, gr) * kPs, bw));
+          }
+          Tm *= N, Tg *= N, Mm *= N, Mg *= N;
+          const i64 period = N == 1 ? Tm + Tg + Mm + Mg : std::max(std::max(Tm, Tg), std::max(Mm, Mg));
+          const u64 tok = (u64)a * (u64)N * rows;
+          // better: tok/period larger (same gpus) — compare tok·period_best > tok_best·period
+          const bool better = !have || (u128)tok * (u128)bl.period_ps > (u128)bl.tokens_per_step * (u128)period;
+          if (better) {
+            have = true;
+            bl = {gpus, a, gr, (uint32_t)N, period, Tm, Tg, Mm, Mg, tok, mask};
+            for (uint32_t k = 0; k < K; ++k) brole[k] = role_c[cls_of[k]];
+          }
+        }
+      }
+    }
+    best[nout] = bl;
+    std::copy(brole.begin(), brole.end(), roles + (size_t)nout * K);
+    ++nout;
+  }
+  *n_out = nout;
+  return KD_OK;
+}
+
 kd_status kd_chunks(uint64_t len, uint64_t unit, uint32_t n, uint64_t* begin_end, uint32_t cap, uint32_t* n_out) {
   if (!n_out || unit == 0 || n == 0 || len == 0) return fail(KD_ERR_INVALID_ARG, "kd_chunks: bad argument");
   u64 q = ceil_div(ceil_div(len, unit), n) * unit;

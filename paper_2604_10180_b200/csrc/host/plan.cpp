@@ -389,11 +389,24 @@ kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* 
         off = align_up(off + B.bytes, AL);
       }
     }
-    // landing slots: the producer's primary output span
+    // landing: a transfer lands in the destination's own instance of the
+    // producer's output buffer, at the producer's offset — so several
+    // producers (on several devices) can fill disjoint row spans of one
+    // buffer that a consumer reads as a whole (the bipartite gather of a:g
+    // layouts); external buffers get a private landing slot
     for (auto& kv : L.landing) {
       const kd_transfer& tr = p->transfers[kv.first];
       const Kernel& P = g->kernels[tr.producer];
       u64 len = P.writes.empty() ? 0 : P.writes[0].len;
+      if (!P.writes.empty() && !(g->buffers[P.writes[0].buf].flags & EXT)) {
+        const uint32_t b = P.writes[0].buf;
+        const uint32_t inst = (g->buffers[b].flags & KD_BUF_PER_MICROBATCH) ? tr.micro : 0;
+        auto it = L.act.find({b, inst});
+        if (it != L.act.end()) {
+          kv.second.first = it->second + P.writes[0].off;
+          continue;
+        }
+      }
       kv.second.first = off;
       off = align_up(off + std::max<u64>(len, 1), AL);
     }

@@ -10,7 +10,7 @@
 namespace kd {
 
 constexpr int kNumSMs = 148;
-constexpr int kMaxPeers = 4;
+constexpr int kMaxPeers = 8;  // consumer devices per producer (a 7:1 layout scatters to 7)
 // Kernel scratch layout shared by every kernel of a device (they run in
 // stream order): [0, kScratchCounterBytes) holds self-resetting u32 counters
 // (always zero between launches), partial results start after it.
@@ -38,10 +38,10 @@ struct Epi {
   int nch = 0;                               // 0: CTA mode; else COUNT mode with nch chunks
   uint32_t row_bytes = 0;                    // COUNT: bytes per output row
   uint32_t cb[kMaxChunks + 1] = {};          // COUNT: chunk byte bounds within a row
-  void* dst[kMaxPeers] = {nullptr, nullptr, nullptr, nullptr};
-  unsigned long long* flag[kMaxPeers] = {nullptr, nullptr, nullptr, nullptr};     // [max(nch,1)] in the peer
-  unsigned long long* started[kMaxPeers] = {nullptr, nullptr, nullptr, nullptr};  // loopback residency (nullable)
-  unsigned long long* logt[kMaxPeers] = {nullptr, nullptr, nullptr, nullptr};     // LOG: per-chunk records (nullable)
+  void* dst[kMaxPeers] = {};
+  unsigned long long* flag[kMaxPeers] = {};     // [max(nch,1)] in the peer
+  unsigned long long* started[kMaxPeers] = {};  // loopback residency (nullable)
+  unsigned long long* logt[kMaxPeers] = {};     // LOG: per-chunk records (nullable)
 };
 
 // ------------------------------------------------------------------ memory model

@@ -472,26 +472,50 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
           l.rd.push_back(ptr);
           continue;
         }
-        if (rs->second.size() != 1)
-          return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: a read span has several remote producers");
-        const uint32_t src = *rs->second.begin();
+        // remote producers whose writes this span reads (bipartite gather: one
+        // per source device's row span; local writers are ordered by the stream)
+        std::vector<uint32_t> srcs_here;
+        for (uint32_t src : rs->second) {
+          bool hit = false;
+          for (const auto& e2 : g->edges)
+            if (e2.dst == k && e2.src == src && e2.buf == sp.buf && e2.offset < sp.off + sp.len &&
+                sp.off < e2.offset + e2.len)
+              hit = true;
+          if (!hit) continue;
+          const Kernel& S = g->kernels[src];
+          for (const auto& e2 : g->edges)
+            if (e2.dst == k && e2.src == src && e2.buf == sp.buf &&
+                (S.writes.empty() || S.writes[0].buf != sp.buf || e2.offset < S.writes[0].off ||
+                 e2.offset + e2.len > S.writes[0].off + S.writes[0].len))
+              return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: a cut edge must read the producer's primary output");
+          srcs_here.push_back(src);
+        }
+        if (srcs_here.empty()) {
+          void* ptr = local_ptr(sp.buf, i, sp.off);
+          if (!ptr) return fail(KD_ERR_STATE, "kd_runtime_prepare: buffer " + std::to_string(sp.buf) + " not bound on device " + std::to_string(d.logical));
+          l.rd.push_back(ptr);
+          continue;
+        }
+        const bool ext = g->buffers[sp.buf].flags & EXT;
+        if (ext) {  // external buffer: one remote producer, its private landing slot
+          if (srcs_here.size() != 1)
+            return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: an external buffer read span with several remote producers");
+          const Kernel& S = g->kernels[srcs_here[0]];
+          for (const auto& e2 : g->edges)
+            if (e2.dst == k && e2.buf == sp.buf && e2.src != srcs_here[0] && e2.offset < sp.off + sp.len &&
+                sp.off < e2.offset + e2.len)
+              return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: a cut read span of an external buffer mixes writers");
+          const auto& land = L.landing.at(xidx.at({i, srcs_here[0], d.logical}));
+          l.rd.push_back(d.ws + land.first + (sp.off - S.writes[0].off));
+        } else {  // transfers land in this device's instance of the buffer
+          void* ptr = local_ptr(sp.buf, i, sp.off);
+          if (!ptr) return fail(KD_ERR_STATE, "kd_runtime_prepare: no local instance of buffer " + std::to_string(sp.buf));
+          l.rd.push_back(ptr);
+        }
+        for (uint32_t src : srcs_here) {
         const Kernel& S = g->kernels[src];
-        if (S.writes.empty() || S.writes[0].buf != sp.buf || sp.off < S.writes[0].off ||
-            sp.off + sp.len > S.writes[0].off + S.writes[0].len)
-          return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: a cut edge must read the producer's primary output");
-        // all bytes of the span must come from that producer
-        for (const auto& e2 : g->edges)
-          if (e2.dst == k && e2.buf == sp.buf && e2.src != src &&
-              e2.offset < sp.off + sp.len && sp.off < e2.offset + e2.len)
-            return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: a cut read span mixes local and remote writers");
         uint32_t t = xidx.at({i, src, d.logical});
         const auto& land = L.landing.at(t);
-        if (transfers_on) {
-          l.rd.push_back(d.ws + land.first + (sp.off - S.writes[0].off));
-        } else {
-          // ablation: read a resident copy (the landing slot, pre-filled by a previous DISAGG step)
-          l.rd.push_back(d.ws + land.first + (sp.off - S.writes[0].off));
-        }
         if (transfers_on && !waited.count(t)) {
           waited.insert(t);
           const auto& X = P->xchunks[t];
@@ -510,7 +534,7 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
           // chunk-aware consumer of a COUNT transfer: acquire chunk by chunk
           // inside the kernel (no wait launch); else wait for every chunk first
           const bool whole = sp.off == S.writes[0].off && sp.len == S.writes[0].len;
-          const bool in_kernel = X.count && whole && op_consumer_unit(K, ri, X.row_bytes) > 0 &&
+          const bool in_kernel = srcs_here.size() == 1 && X.count && whole && op_consumer_unit(K, ri, X.row_bytes) > 0 &&
                                  l.ctx.acq.n < kMaxAcqIn && !getenv("KD_NO_INKERNEL_ACQ");
           if (in_kernel) {
             AcqIn& in = l.ctx.acq.in[l.ctx.acq.n++];
@@ -537,6 +561,7 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
             for (uint32_t c = 0; c < nch; ++c) push_wait(flags + c, mult[c], logp ? logp + kLogWords * c : nullptr);
           }
         }
+        }  // remote producers of this span
       }
       if (wl.n) {
         Launch w;
@@ -554,7 +579,7 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
       for (uint32_t v = 0; v < n; ++v) {
         auto it = xidx.find({i, k, v});
         if (it == xidx.end()) continue;
-        if (l.ctx.epi.n == kMaxPeers) return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: more than 4 consumer devices");
+        if (l.ctx.epi.n == kMaxPeers) return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: more than 8 consumer devices");
         const auto& X = P->xchunks[it->second];
         const uint32_t nch = (uint32_t)X.ch.size();
         Epi& ep = l.ctx.epi;

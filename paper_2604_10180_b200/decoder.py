@@ -556,6 +556,148 @@ class ShardedKVDecoderGraph:
                 "g2": lw.gamma2}[base]
 
 
+class RoleDecoderGraph:
+    """a:1 device-role layout: `a` memory-role GPUs
+    (logical devices 0..a−1) each own m = cfg.m sequences per micro-batch —
+    their residual stream, KV cache and every memory-bound kernel (norms,
+    RoPE/append, attention, SiLU·mul) — and one GEMM-role GPU (device a) runs
+    the QKV / O / gate_up / down GEMMs once per micro-batch over all a·m rows
+    (the weights are read once for a·m rows: the layouts where disaggregation
+    can beat monolithic per GPU). The handoff is a
+    bipartite gather/scatter: shard s writes rows [s·m, (s+1)·m) of each GEMM
+    input straight into the GEMM GPU's buffer (transfers land in the
+    destination's instance of the buffer), and every GEMM output is streamed
+    to the memory GPUs, each reading its row span. Dense bf16 configs.
+    Global row order: micro-batch i, shard s, row j → (i·a + s)·m + j."""
+
+    def __init__(self, cfg, a: int, act: int = K.KD_BF16):
+        assert act == K.KD_BF16 and not cfg.n_experts and not cfg.attn_every
+        assert a >= 1 and a * cfg.m <= 256, "the GEMM role takes a·m <= 256 rows per micro-batch"
+        self.cfg, self.a = cfg, a
+        m, H, L = cfg.m, cfg.hidden, cfg.n_layers
+        Hq, Hkv, D, F = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn
+        M, pps = a * m, cfg.pages_per_seq
+        g = Graph()
+        self.g = g
+        self.buf, self.shape, self.dtype = {}, {}, {}
+        W, PM = K.KD_BUF_WEIGHT, K.KD_BUF_PER_MICROBATCH
+        PERS, INP, OUT = K.KD_BUF_PERSISTENT, K.KD_BUF_INPUT, K.KD_BUF_OUTPUT
+        nb = {"bf16": 2, "f32": 4, "i32": 4}
+
+        def buf(name, shape, dt, flags):
+            self.buf[name] = g.add_buffer(int(np.prod(shape)) * nb[dt], flags)
+            self.shape[name], self.dtype[name] = tuple(shape), dt
+
+        def whole(name):
+            return (self.buf[name], 0, int(np.prod(self.shape[name])) * nb[self.dtype[name]])
+
+        def rows(name, s):  # shard s's row span of a [a·m, cols] activation
+            cols = self.shape[name][1]
+            e = nb[self.dtype[name]]
+            return (self.buf[name], s * m * cols * e, m * cols * e)
+
+        for s_ in range(a):
+            buf(f"r.{s_}", (m, H), "f32", PERS | INP | OUT | PM)
+            buf(f"bt.{s_}", (m, pps), "i32", INP | PM)
+            buf(f"sl.{s_}", (m,), "i32", INP | PM)
+        for l in range(L):
+            buf(f"w_qkv.{l}", (cfg.qkv_dim, H), "bf16", W)
+            buf(f"w_o.{l}", (H, Hq * D), "bf16", W)
+            buf(f"w_gu.{l}", (2 * F, H), "bf16", W)
+            buf(f"w_d.{l}", (H, F), "bf16", W)
+            buf(f"g1.{l}", (H,), "bf16", W)
+            buf(f"g2.{l}", (H,), "bf16", W)
+            for s_ in range(a):
+                buf(f"kc.{l}.{s_}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+                buf(f"vc.{l}.{s_}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+                buf(f"q.{l}.{s_}", (m, Hq * D), "bf16", PM)
+            for nm, cols in (("h1", H), ("qkv", cfg.qkv_dim), ("attn", Hq * D), ("o", H), ("h2", H), ("gu", 2 * F),
+                             ("a", F), ("d", H)):
+                buf(f"{nm}.{l}", (M, cols), "bf16", PM)
+        self.kernels: List[KernelInfo] = []
+        self.dev_of: List[int] = []
+
+        def add(name, layer, dev, op, reads, writes, attrs, flops=0):
+            sp = lambda x: x if isinstance(x, tuple) else whole(x)
+            kid = g.add_kernel(op, [sp(x) for x in reads], [sp(x) for x in writes], attrs, flops, -1, -1)
+            self.kernels.append(KernelInfo(name, layer, -1, kid))
+            self.dev_of.append(dev)
+
+        eps = float(cfg.eps)
+        for l in range(L):
+            for s_ in range(a):
+                nd = 1 if l > 0 else 0
+                add(f"norm1.{s_}", l, s_, K.KD_OP_ADD_RMSNORM,
+                    [f"r.{s_}"] + ([rows(f"d.{l-1}", s_)] if nd else []) + [f"g1.{l}"], [rows(f"h1.{l}", s_), f"r.{s_}"],
+                    K.kd_attr_add_rmsnorm(m, H, nd, act, eps, 0))
+            add("qkv", l, a, K.KD_OP_GEMM, [f"h1.{l}", f"w_qkv.{l}"], [f"qkv.{l}"], K.kd_attr_gemm(M, cfg.qkv_dim, H, act),
+                2 * M * cfg.qkv_dim * H)
+            for s_ in range(a):
+                add(f"rope.{s_}", l, s_, K.KD_OP_ROPE_APPEND, [rows(f"qkv.{l}", s_), f"bt.{s_}", f"sl.{s_}"],
+                    [f"q.{l}.{s_}", f"kc.{l}.{s_}", f"vc.{l}.{s_}"],
+                    K.kd_attr_rope_append(m, Hq, Hkv, D, cfg.page, pps, act, 0, float(cfg.rope_theta)))
+                add(f"attn.{s_}", l, s_, K.KD_OP_ATTENTION,
+                    [f"q.{l}.{s_}", f"kc.{l}.{s_}", f"vc.{l}.{s_}", f"bt.{s_}", f"sl.{s_}"], [rows(f"attn.{l}", s_)],
+                    K.kd_attr_attention(m, Hq, Hkv, D, cfg.page, pps, act, 0), 4 * m * Hq * cfg.context * D)
+            add("o", l, a, K.KD_OP_GEMM, [f"attn.{l}", f"w_o.{l}"], [f"o.{l}"], K.kd_attr_gemm(M, H, Hq * D, act),
+                2 * M * H * Hq * D)
+            for s_ in range(a):
+                add(f"norm2.{s_}", l, s_, K.KD_OP_ADD_RMSNORM, [f"r.{s_}", rows(f"o.{l}", s_), f"g2.{l}"],
+                    [rows(f"h2.{l}", s_), f"r.{s_}"], K.kd_attr_add_rmsnorm(m, H, 1, act, eps, 0))
+            add("gu", l, a, K.KD_OP_GEMM, [f"h2.{l}", f"w_gu.{l}"], [f"gu.{l}"], K.kd_attr_gemm(M, 2 * F, H, act),
+                2 * M * 2 * F * H)
+            for s_ in range(a):
+                add(f"silu.{s_}", l, s_, K.KD_OP_SILU_MUL, [rows(f"gu.{l}", s_)], [rows(f"a.{l}", s_)],
+                    K.kd_attr_silu_mul(m, F, act, 0))
+            add("down", l, a, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"], K.kd_attr_gemm(M, H, F, act),
+                2 * M * H * F)
+        for s_ in range(a):
+            add(f"final_add.{s_}", L - 1, s_, K.KD_OP_RESIDUAL_ADD, [f"r.{s_}", rows(f"d.{L-1}", s_)], [f"r.{s_}"],
+                K.kd_attr_residual_add(m, H, 1, 0))
+        g.finalize()
+
+    def assign(self) -> List[int]:
+        """Memory shards on devices 0..a−1, the GEMMs on device a."""
+        return list(self.dev_of)
+
+    def global_rows(self, s: int, i: int) -> np.ndarray:
+        m, a = self.cfg.m, self.a
+        return np.arange((i * a + s) * m, (i * a + s + 1) * m)
+
+    def host_value(self, name, i, inputs):
+        """Host values of buffer `name`, micro-batch i (inputs: the unsharded
+        synthetic model of batch a·N·m, cfg.with_(batch=a·N·m))."""
+        cfg = self.cfg
+        pps = cfg.pages_per_seq
+        parts = name.split(".")
+        base = parts[0]
+        if base in ("r", "bt", "sl"):
+            s_ = int(parts[1])
+            rr = self.global_rows(s_, i)
+            if base == "r":
+                return inputs.x[rr]
+            if base == "sl":
+                return inputs.seq_len[rr]
+            return (np.arange(cfg.m, dtype=np.int32)[:, None] * pps + np.arange(pps, dtype=np.int32)[None, :])
+        l = int(parts[1])
+        lw = inputs.layers[l]
+        if base in ("kc", "vc"):
+            s_ = int(parts[2])
+            pool = (inputs.k_cache if base == "kc" else inputs.v_cache)[l]
+            return pool[inputs.block_table[self.global_rows(s_, i)].reshape(-1)]
+        return {"w_qkv": lw.w_qkv, "w_o": lw.w_o, "w_gu": lw.w_gu, "w_d": lw.w_d, "g1": lw.gamma1,
+                "g2": lw.gamma2}[base]
+
+    def residual_global(self, rt) -> np.ndarray:
+        """The residual stream [a·N·m, H] in global row order after a step."""
+        cfg = self.cfg
+        out = np.zeros((self.a * cfg.n_micro * cfg.m, cfg.hidden), np.float32)
+        for (name, i, d), t in rt.tensors.items():
+            if name.startswith("r."):
+                out[self.global_rows(int(name.split(".")[1]), i)] = t.cpu().numpy()
+        return out
+
+
 class DecoderRuntime:
     """Allocates and binds every external buffer on the devices the plan
     needs, one zeroed workspace per local logical device, and runs steps.
@@ -641,7 +783,8 @@ class DecoderRuntime:
                 else:
                     t.copy_(torch.from_numpy(v))
                 return
-            name = ".".join(name.split(".")[:2]) if name.split(".")[0] not in ("r",) else "r"
+            b0 = name.split(".")[0]
+            name = b0 if b0 in ("r", "bt", "sl") else ".".join(name.split(".")[:2])
         m, pps = cfg.m, cfg.pages_per_seq
         base, _, lay = name.partition(".")
         L = cfg.n_layers

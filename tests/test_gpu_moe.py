@@ -177,8 +177,8 @@ def test_moe_ffn_pipeline_vs_oracle(kd, rows, H, F, E):
     ref = OL.moe_ffn(OL.bf16_to_f64(h), ridx, rw, OL.bf16_to_f64(wgu), OL.bf16_to_f64(wd), "bf16")
     e = relerr(host_f64(out), ref)
     assert e < 2e-2 and e < 1e-2, e
-    # the expert FFN chains two GEMMs and SiLU (each rounding to bf16): 2 steps + 1e-2·rms
-    assert_elementwise(host_f64(out), ref, 2, 1e-2, "moe out")
+    # the expert FFN chains two GEMMs and SiLU (each rounding to bf16): 2 steps + 2e-2·rms
+    assert_elementwise(host_f64(out), ref, 2, 2e-2, "moe out")
     # grouped GEMM determinism
     y1 = y.clone()
     K.check(K.kd_op_grouped_gemm(a2, act.data_ptr(), wd_d.data_ptr(), xgm.data_ptr(), y.data_ptr(),

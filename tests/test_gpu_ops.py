@@ -84,6 +84,9 @@ GEMM_SHAPES = [
     (33, 384, 320),     # ragged M (mma_n 48), K not a multiple of 128
     (32, 6144, 4096),   # 8B QKV at m=32
     (64, 4096, 4096),   # 8B O at m=64 (split across SMs)
+    (32, 4096, 4096),   # 8B O at the disaggregated pair's m=32 (N=2)
+    (32, 4096, 14336),  # 8B down at m=32
+    (32, 28672, 4096),  # 8B gate_up at m=32
     (64, 4096, 14336),  # 8B down (stream-K fixup)
     (64, 28672, 4096),  # 8B gate_up
     (128, 1024, 2048),  # m=128
@@ -251,9 +254,9 @@ def test_attention_ragged_lengths(kd, rows, Hq, Hkv, D, C, lens):
     ref = OL.paged_decode_attention(OL.bf16_to_f64(q), OL.bf16_to_f64(kc), OL.bf16_to_f64(vc), bt, sl, Hq, Hkv, D,
                                     16, "bf16")
     assert relerr(host_f64(out), ref) < 1e-2
-    assert_elementwise(host_f64(out), ref, 2, 1e-2, "attention out (ragged)")
-    for b in range(rows):  # and per row: a short row cannot hide behind the long ones' norm
+    for b in range(rows):  # per row (a short row's outputs are larger than a long row's: own rms)
         assert relerr(host_f64(out)[b], ref[b]) < 1e-2, f"row {b} (len {sl[b]})"
+        assert_elementwise(host_f64(out)[b], ref[b], 2, 1e-2, f"attention out row {b} (len {sl[b]})")
 
 
 # ------------------------------------------------------------------ a8
@@ -433,7 +436,9 @@ def test_gemm_rmsnorm_fused(kd, M, N, K_, split, monkeypatch):
                                   1e-5, "bf16")
     assert relerr(host_f64(r), r_ref) < 1e-3
     assert relerr(hh, h_ref) < 5e-3
-    assert_elementwise(hh, h_ref, 2, 2e-3, "gemm_rmsnorm h")
+    # a GEMM sum rounding to the neighbouring bf16 value moves r' by one ulp of
+    # the GEMM output (|Y| ~ rms 1 → 2^-7), which h carries through the norm
+    assert_elementwise(hh, h_ref, 2, 1e-2, "gemm_rmsnorm h")
 
 
 # ------------------------------------------------------------------ a4+a5 fused (KD_OP_QKV_ROPE)
@@ -476,8 +481,9 @@ def test_qkv_rope_fused_equals_pair(kd, rows, H, Hq, Hkv, D, C, split, monkeypat
     qr = OL.rope_append(qkv_ref, sl - 1, bt, kr, vr, Hq, Hkv, D, theta, 16, "bf16")
     assert relerr(host_f64(q2), qr) < 5e-3
     assert relerr(host_f64(k2), kr) < 5e-3 and relerr(host_f64(v2), vr) < 5e-3
-    assert_elementwise(host_f64(q2), qr, 2, 2e-3, "qkv_rope q")
-    assert_elementwise(host_f64(k2), kr, 2, 2e-3, "qkv_rope k cache")
+    # (a rotation pair mixes two GEMM outputs: one rounding step of either, 2^-7·rms)
+    assert_elementwise(host_f64(q2), qr, 2, 1e-2, "qkv_rope q")
+    assert_elementwise(host_f64(k2), kr, 2, 1e-2, "qkv_rope k cache")
     assert_elementwise(host_f64(v2), vr, 1, 1e-3, "qkv_rope v cache")
 
 
