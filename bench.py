@@ -39,6 +39,8 @@ def parse():
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--kernels", action="store_true", help="also time every op kind (extra passes)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--layout", default="search", choices=["search", "pairs"],
+                   help="N>1: the role layout kd_place_roles picks (default) or independent 1:1 pairs")
     return p.parse_args()
 
 
@@ -99,44 +101,73 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU baseline (the oracle)
-def cpu_baseline(cfg, seconds_budget=20.0):
-    """Times the oracle as it stands (fp64 numpy) on a bounded sample of the
-    same workload: n_seq sequences through one full-width layer (all kernels),
-    extrapolated × L layers; tokens/s = n_seq / (L · t_layer)."""
-    import numpy as np
-    import synth
-    from oracle import layer as OL
+def _oracle_cores():
     try:
         from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     except Exception:
-        cores = os.cpu_count()
-    n_seq = 2
-    sub = cfg.with_(n_layers=1, batch=n_seq, n_micro=1)
+        return os.cpu_count()
+
+
+def cpu_baseline(cfg, full_batch=True):
+    """Times the oracle as it stands (fp64 numpy) on the host cores: one
+    full-width layer of the workload at its FULL batch B (every kernel of the
+    layer, all B sequences at context C), extrapolated × L layers; tokens/s =
+    B / (L · t_layer). Also a 1-thread figure on a 2-sequence sample
+    (BASELINE.md §3). Input generation is outside the timed region."""
+    import numpy as np  # noqa: F401
+    import synth
+    from oracle import layer as OL
+    cores = _oracle_cores()
+    B = cfg.batch if full_batch else 2
+    sub = cfg.with_(n_layers=1, batch=B, n_micro=1)
     inp = synth.make_decoder_inputs(sub)
     t0 = time.perf_counter()
     OL.decoder_step(inp, act="bf16")
     t = time.perf_counter() - t0
-    reps = 1
-    while time.perf_counter() - t0 < min(seconds_budget, 4 * t) and reps < 3:
-        OL.decoder_step(inp, act="bf16")
-        reps += 1
-    t = (time.perf_counter() - t0) / reps
-    value = n_seq / (cfg.n_layers * t)
-    return {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-            "sample": f"{n_seq} sequences x 1 full-width layer of {cfg.name} (C={cfg.context}), fp64 numpy oracle, "
-                      f"{reps} reps, extrapolated x{cfg.n_layers} layers"}
+    value = B / (cfg.n_layers * t)
+    out = {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+           "sample": f"{B} sequences x 1 full-width layer of {cfg.name} (C={cfg.context}), fp64 numpy oracle on "
+                     f"{cores} BLAS threads, 1 rep ({t:.1f} s), extrapolated x{cfg.n_layers} layers",
+           "host_cpus": os.cpu_count()}
+    try:
+        from threadpoolctl import threadpool_limits
+        sub2 = cfg.with_(n_layers=1, batch=2, n_micro=1)
+        inp2 = synth.make_decoder_inputs(sub2)
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
+            OL.decoder_step(inp2, act="bf16")
+            t1 = time.perf_counter() - t0
+        out["one_thread"] = {"value": 2 / (cfg.n_layers * t1), "unit": "tokens/s",
+                             "sample": f"2 sequences x 1 layer, 1 thread ({t1:.1f} s), extrapolated x{cfg.n_layers}"}
+    except Exception as ex:  # report, do not hide
+        out["one_thread"] = {"error": str(ex)}
+    return out
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    base = cpu_baseline(cfg)
+    # the reference arm is the oracle (PAPER.md has no code to install): each
+    # step = one full-width layer of the workload for a bounded 2-sequence
+    # sample, timed W + K times on the host cores, extrapolated × L layers
+    import synth
+    from oracle import layer as OL
     steps, warm = args.steps, args.warmup
-    # one "step" of the reference arm = the bounded oracle sample (time-capped)
+    inp = synth.make_decoder_inputs(cfg.with_(n_layers=1, batch=2, n_micro=1))
+    for _ in range(warm):
+        OL.decoder_step(inp, act="bf16")
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        OL.decoder_step(inp, act="bf16")
+    t = (time.perf_counter() - t0) / max(steps, 1)
+    cores = _oracle_cores()
+    base = {"value": 2 / (cfg.n_layers * t), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"2 sequences x 1 full-width layer of {cfg.name} (C={cfg.context}) per step, fp64 numpy oracle on "
+                      f"{cores} BLAS threads, {steps} timed steps after {warm} warm-up, extrapolated x{cfg.n_layers} layers"}
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": None,
+            "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": round(t * cfg.n_layers * 1e3, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(cfg, 1, "oracle (CPU)"),
             "cpu_baseline": base,
@@ -146,19 +177,42 @@ def run_reference(args, cfg):
 
 def placement_search(cfg, DEC):
     """a1 on the host ("report search time", "solves
-    each DDG in about 20 ms"): kd_place over the unfused graph of this config
-    (N=2 micro-batches) on 2/4/8 B200s; wall time of the exact search."""
-    from paper_2604_10180_b200.api import place
+    each DDG in about 20 ms"): the device-role search kd_place_roles over one
+    memory shard's unfused step graph (m = 32 rows per micro-batch, the 8B
+    pair's micro-batch) — the best memory:GEMM ratio and N per GPU count with
+    its modelled tokens/s per GPU — and kd_place's kernel-level search on the
+    2-device pair; wall time of each exact search."""
+    from paper_2604_10180_b200.api import place, place_roles
     if cfg.n_experts or cfg.attn_every:
         return None
-    dg = DEC.DecoderGraph(cfg.with_(n_micro=2))
-    out = {"kernels": dg.g.num_kernels, "n_micro": 2}
-    for n in (2, 4, 8):
-        t0 = time.perf_counter()
-        a, obj, nodes = place(dg.g, DEC.b200_machine(n), 2)
-        out[f"{n}gpu"] = {"search_ms": round((time.perf_counter() - t0) * 1e3, 2), "objective_us": round(obj / 1e6, 1),
-                          "nodes": nodes, "devices_used": len(set(a))}
+    m = 32
+    dg = DEC.DecoderGraph(cfg.with_(batch=m, n_micro=1))
+    out = {"kernels": dg.g.num_kernels, "rows_per_micro": m, "model": "kd_place_roles (E6 over role layouts)"}
+    t0 = time.perf_counter()
+    lays = place_roles(dg.g, DEC.b200_machine(8), m, 8, 0b111)
+    out["roles_search_ms"] = round((time.perf_counter() - t0) * 1e3, 2)
+    for L in lays:
+        tok_s = L["tokens_per_step"] / (L["period_ps"] * 1e-12)
+        out[f"{L['gpus']}gpu"] = {"memory_gpus": L["a"], "gemm_gpus": L["gr"], "n_micro": L["n_micro"],
+                                  "period_us": round(L["period_ps"] / 1e6, 1),
+                                  "model_tokens_per_s_per_gpu": round(tok_s / L["gpus"], 1),
+                                  "T_mem_us": round(L["T_mem_ps"] / 1e6, 1), "T_gemm_us": round(L["T_gemm_ps"] / 1e6, 1)}
+    dg2 = DEC.DecoderGraph(cfg.with_(n_micro=2))
+    t0 = time.perf_counter()
+    a, obj, nodes = place(dg2.g, DEC.b200_machine(2), 2)
+    out["pair_kernel_search"] = {"search_ms": round((time.perf_counter() - t0) * 1e3, 2),
+                                 "objective_us": round(obj / 1e6, 1), "nodes": nodes, "devices_used": len(set(a))}
     return out
+
+
+def role_layout(cfg, DEC, n_gpus):
+    """(a, N) of kd_place_roles' best layout on n_gpus (8B shard, m = 32)."""
+    from paper_2604_10180_b200.api import place_roles
+    dg = DEC.DecoderGraph(cfg.with_(batch=32, n_micro=1))
+    for L in place_roles(dg.g, DEC.b200_machine(8), 32, 8, 0b110):  # N ∈ {2, 4}
+        if L["gpus"] == n_gpus:
+            return L["a"], L["n_micro"]
+    return n_gpus - 1, 2
 
 
 def workload_config(cfg, n_gpus, placement):
@@ -236,17 +290,38 @@ def main():
         # kernels on the even rank, GEMMs on the odd rank), each decoding its own batch
         # of B sequences with 2 micro-batches; cut edges are streamed by the producers'
         # fused peer stores into the partner's HBM (CUDA IPC over NVLink). No collective.
-        if world % 2:
-            raise SystemExit("bench.py: --gpus must be 1 or even (disaggregated pairs)")
-        pair, role = rank // 2, rank % 2
-        groups = [dist.new_group([2 * p, 2 * p + 1]) for p in range(world // 2)]
-        cfg = cfg.with_(n_micro=2)
-        dg = DEC.DecoderGraph(cfg)
-        assign = dg.role_assign(0, 1)
-        rt = DEC.DecoderRuntime(dg, assign, 2, [local], seed=cfg.seed + pair, use_graph=not args.no_graph,
-                                local_devs=[role], dist=dist, dist_group=groups[pair])
-        placement = (f"{world // 2} disaggregated pair(s): memory-role kernels (norms, RoPE+append, attention, "
-                     f"SiLU) on even ranks, GEMMs on odd ranks, N=2 micro-batches")
+        if args.layout == "pairs":
+            if world % 2:
+                raise SystemExit("bench.py: --layout pairs needs an even --gpus")
+            pair, role = rank // 2, rank % 2
+            groups = [dist.new_group([2 * p, 2 * p + 1]) for p in range(world // 2)]
+            cfg = cfg.with_(n_micro=2)
+            dg = DEC.DecoderGraph(cfg)
+            assign = dg.role_assign(0, 1)
+            rt = DEC.DecoderRuntime(dg, assign, 2, [local], seed=cfg.seed + pair, use_graph=not args.no_graph,
+                                    local_devs=[role], dist=dist, dist_group=groups[pair])
+            placement = (f"{world // 2} disaggregated pair(s): memory-role kernels (norms, RoPE+append, attention, "
+                         f"SiLU) on even ranks, GEMMs on odd ranks, N=2 micro-batches")
+            tokens_per_step = cfg.batch * (world // 2)
+        else:
+            # the layout kd_place_roles picks for this GPU count:
+            # a memory-role ranks (0..a-1), each decoding its own B sequences, and
+            # world − a GEMM ranks; with one GEMM rank (a:1) every GEMM runs once
+            # per micro-batch over all a·m rows (bipartite gather/scatter)
+            a, N = role_layout(cfg, DEC, world)
+            if world - a != 1:
+                raise SystemExit(f"bench.py: the searched layout {a}:{world - a} needs TP GEMM ranks (use --layout pairs)")
+            shard = cfg.with_(n_micro=N)
+            if shard.m * a > 256:
+                shard = shard.with_(batch=N * (256 // a))
+            dg = DEC.RoleDecoderGraph(shard, a)
+            rt = DEC.DecoderRuntime(dg, dg.assign(), a + 1, [local], seed=cfg.seed, use_graph=not args.no_graph,
+                                    local_devs=[rank], dist=dist)
+            cfg = shard
+            placement = (f"searched role layout {a}:1 (kd_place_roles): ranks 0..{a - 1} memory role (norms, "
+                         f"RoPE+append, attention, SiLU; {shard.batch} sequences each), rank {a} the GEMMs over "
+                         f"{a}x{shard.m} rows per micro-batch, N={N} micro-batches, chunked P2P handoff")
+            tokens_per_step = shard.batch * a
     stream = rt.streams[0]
 
     def barrier():
@@ -301,6 +376,19 @@ def main():
         exposed = {"ms_per_step": round(ms / args.steps - ms_nt / args.steps, 4),
                    "no_transfer_ms_per_step": round(ms_nt / args.steps, 4),
                    "fraction_of_step": round(1 - ms_nt / ms, 4)}
+        # and as the consumers saw it: KD_MODE_LOG per-chunk records, kd_step_stats
+        # wait_ns = Σ over this rank's incoming chunks of the first acquirer's stall
+        rt.rt.set_mode(K.KD_MODE_LOG)
+        rt.rt.prepare()
+        for _ in range(2):
+            rt.step()
+        barrier()
+        st = rt.step(stats=True)
+        exposed["log_wait_us_per_step_rank0"] = round(st["wait_ns"][0] / 1e3, 2)
+        exposed["log_step_us_rank0"] = round(st["step_ns"][0] / 1e3, 2)
+        exposed["log_chunk_waits_rank0"] = st["chunk_waits"][0]
+        exposed["link_bytes_per_step_from_rank0"] = sum(st["link_bytes"][rt.local_devs[0]]) if st["link_bytes"] else None
+        barrier()
         rt.rt.set_mode(K.KD_MODE_DISAGG)
         rt.rt.prepare()
     # per-kernel CUDA-event timing: a second pass of the same K steps whose
@@ -326,7 +414,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    tokens_per_step = cfg.batch * (1 if world == 1 or cfg.name == "llama3-70b" else world // 2)
+    if world == 1 or cfg.name == "llama3-70b":
+        tokens_per_step = cfg.batch
     value = tokens_per_step / (ms_step / 1e3)
 
     # ---- roofline of the dominant kernel (decode attention)
@@ -364,11 +453,14 @@ def main():
     e2e_value = None
     try:
         me = rt.local_devs[0]
-        r_dev = rt.tensors.get(("r", 0, me), rt.tensors.get(("r.0", 0, me)))
-        if r_dev is None:  # GEMM-role rank: its inputs arrive from the partner
-            r_dev = torch.zeros(1, device="cuda")
-        bt_dev = rt.tensors.get(("bt", 0, me), torch.zeros(1, dtype=torch.int32, device="cuda"))
-        sl_dev = rt.tensors.get(("sl", 0, me), torch.zeros(1, dtype=torch.int32, device="cuda"))
+        def mine(base, dt):  # this rank's instance of r / bt / sl (suffixed per shard in the role graphs)
+            for (nm, i, d), t in rt.tensors.items():
+                if d == me and i == 0 and (nm == base or nm.startswith(base + ".")):
+                    return t
+            return torch.zeros(1, dtype=dt, device="cuda")  # GEMM-role rank: its inputs arrive from the peers
+        r_dev = mine("r", torch.float32)
+        bt_dev = mine("bt", torch.int32)
+        sl_dev = mine("sl", torch.int32)
         r_host = torch.empty_like(r_dev, device="cpu").pin_memory()
         r_host.copy_(r_dev)
         bt_host = bt_dev.cpu().pin_memory()

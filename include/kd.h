@@ -158,12 +158,20 @@ typedef struct { uint32_t rows, hidden, experts, top_k; } kd_attr_moe_route;    
 typedef struct { uint32_t rows, hidden, experts, top_k; } kd_attr_moe_dispatch; /* xg bf16 [rows*top_k, H] */
 typedef struct {
   uint32_t rows_total;  /* rows of xg / yg (= rows * top_k) */
-  uint32_t N, K;        /* per-expert W [N, K]; W_experts [E, N, K] row-major */
-  uint32_t experts;
+  uint32_t N, K;        /* per-expert W [N, K]; W_experts [experts, N, K] row-major */
+  uint32_t experts;     /* groups this GEMM runs: experts expert0 .. expert0 + experts − 1 */
   uint32_t rows_cap;    /* static bound on rows per expert (<= 256) */
   uint32_t dtype;
+  /* expert parallelism (SURVEY §8(e) "MoE: EP with P2P dispatch and combine"):
+   * the meta block describes meta_experts experts (0 = experts); this GEMM's
+   * group j is expert expert0 + j (count at meta[expert0 + j], offset at
+   * meta[meta_experts + expert0 + j]); W_experts holds only its experts. */
+  uint32_t expert0, meta_experts;
 } kd_attr_grouped_gemm;                                                          /* yg bf16 [rows_total, N] */
-typedef struct { uint32_t rows, hidden, experts, top_k; } kd_attr_moe_combine;  /* out bf16 [rows, H] */
+/* n_parts (0 or 1: one yg): expert-parallel combine reads [yg_0 .. yg_{n_parts−1},
+ * route, meta]; expert e's rows are in part e / (experts / n_parts) (each
+ * expert device writes its experts' rows of its own yg buffer). */
+typedef struct { uint32_t rows, hidden, experts, top_k, n_parts, pad_; } kd_attr_moe_combine;  /* out bf16 [rows, H] */
 /* Mamba-2 decode. zxbcdt = in_proj output bf16 [rows, P_in]
  * with columns [z (d_inner) | xBC (d_inner + 2·G·N) | dt (nheads)], P_in =
  * 2·d_inner + 2·G·N + nheads, d_inner = nheads·head_dim. conv_state bf16

@@ -99,12 +99,18 @@ class kd_attr_moe(C.Structure):  # kd_attr_moe_route / _dispatch / _combine
     _fields_ = [("rows", C.c_uint32), ("hidden", C.c_uint32), ("experts", C.c_uint32), ("top_k", C.c_uint32)]
 
 
-kd_attr_moe_route = kd_attr_moe_dispatch = kd_attr_moe_combine = kd_attr_moe
+kd_attr_moe_route = kd_attr_moe_dispatch = kd_attr_moe
 
 
 class kd_attr_grouped_gemm(C.Structure):
     _fields_ = [("rows_total", C.c_uint32), ("N", C.c_uint32), ("K", C.c_uint32), ("experts", C.c_uint32),
-                ("rows_cap", C.c_uint32), ("dtype", C.c_uint32)]
+                ("rows_cap", C.c_uint32), ("dtype", C.c_uint32), ("expert0", C.c_uint32),
+                ("meta_experts", C.c_uint32)]
+
+
+class kd_attr_moe_combine(C.Structure):
+    _fields_ = [("rows", C.c_uint32), ("hidden", C.c_uint32), ("experts", C.c_uint32), ("top_k", C.c_uint32),
+                ("n_parts", C.c_uint32), ("pad_", C.c_uint32)]
 
 
 class kd_attr_ssm(C.Structure):
@@ -230,7 +236,7 @@ _PROTOS = {
     "kd_op_moe_route": (kd_status, [C.POINTER(kd_attr_moe), P, P, P, P]),
     "kd_op_moe_dispatch": (kd_status, [C.POINTER(kd_attr_moe), P, P, P, P, P]),
     "kd_op_grouped_gemm": (kd_status, [C.POINTER(kd_attr_grouped_gemm), P, P, P, P, P, P]),
-    "kd_op_moe_combine": (kd_status, [C.POINTER(kd_attr_moe), P, P, P, P, P]),
+    "kd_op_moe_combine": (kd_status, [C.POINTER(kd_attr_moe_combine), P, P, P, P, P]),
     "kd_op_ssm_conv": (kd_status, [C.POINTER(kd_attr_ssm), P, P, P, P, P, P]),
     "kd_op_ssm_update": (kd_status, [C.POINTER(kd_attr_ssm), P, P, P, P, P, P, P, P]),
     "kd_op_gated_norm": (kd_status, [C.POINTER(kd_attr_ssm), P, P, P, P, P]),

@@ -14,12 +14,15 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libkd.so")
+# KD_BUILD_TAG / KD_EXTRA_NVCC: A/B variants (libkd_<tag>.so, loaded with KD_LIB)
+_TAG = os.environ.get("KD_BUILD_TAG", "")
+BUILD = os.path.join(PKG, "_build" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(PKG, f"libkd_{_TAG}.so" if _TAG else "libkd.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-          "-Xcompiler", "-fPIC,-Wall,-Wno-unused-function", "--expt-relaxed-constexpr"]
+          "-Xcompiler", "-fPIC,-Wall,-Wno-unused-function", "--expt-relaxed-constexpr"] + \
+    os.environ.get("KD_EXTRA_NVCC", "").split()
 
 
 def _sources():

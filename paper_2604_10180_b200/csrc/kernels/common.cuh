@@ -10,7 +10,11 @@
 namespace kd {
 
 constexpr int kNumSMs = 148;
+#ifdef KD_SMALL_PARAMS  // A/B: kernel-parameter size
+constexpr int kMaxPeers = 4;
+#else
 constexpr int kMaxPeers = 8;  // consumer devices per producer (a 7:1 layout scatters to 7)
+#endif
 // Kernel scratch layout shared by every kernel of a device (they run in
 // stream order): [0, kScratchCounterBytes) holds self-resetting u32 counters
 // (always zero between launches), partial results start after it.
@@ -158,7 +162,11 @@ __device__ __forceinline__ int epi_chunk_of(const Epi& epi, uint32_t byte_in_row
 // reads it: spin until flag[c] >= (epoch − base)·mult[c] (ld.acquire.sys),
 // watchdog → *err = 1. One thread acquires; the caller then orders the other
 // threads behind it (bar.sync / __syncwarp) — or, for TMA reads, a proxy fence.
+#ifdef KD_SMALL_PARAMS
+constexpr int kMaxAcqIn = 1;
+#else
 constexpr int kMaxAcqIn = 4;
+#endif
 struct AcqIn {
   const unsigned long long* flag = nullptr;  // [nch]
   unsigned long long* log = nullptr;         // LOG: per-chunk records (nullable)

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __rest
   float v[kNormChunks][8];
   float ss = 0.f;
   float* rr = r + (size_t)row * H;
-  uint32_t held[kMaxAcqIn] = {0u, 0u, 0u, 0u};  // chunks thread 0 acquired, per remote delta
+  uint32_t held[kMaxAcqIn] = {};  // chunks thread 0 acquired, per remote delta
 #pragma unroll
   for (int c = 0; c < kNormChunks; ++c) {
     // remote deltas (a13 consumer side): column group c of every thread is the

@@ -55,7 +55,8 @@ struct Args {
   // grouped (MoE expert) mode: groups > 0; tile t → group t / tpg, n-tile t % tpg;
   // meta = int32 count[groups], offset[groups] (rows of X/Y), read on device
   int groups, tpg;
-  const int* meta;
+  const int* meta;            // counts of this GEMM's experts (already offset by expert0)
+  int moff;                   // offsets are at meta + moff (= meta_experts)
   int dbg;                    // debug A/B knob (KD_GEMM_DBG): 1 skip owner Y stores, 2 skip owner fold
   unsigned* err;              // runtime error word (nullable): set to 2 when the fold barrier times out
   Acq acq;                    // chunk-aware consumer: X (slot 0) acquired per k-block by the TMA warp
@@ -106,6 +107,11 @@ __device__ __forceinline__ void store_silu4(const Args& A, size_t yo, const floa
   for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
 }
 
+// kX: the round-2 handoff protocol (chunk byte counts, in-kernel acquires,
+// residency / log words) is compiled in; launches without chunked transfers
+// use the kX = false instance, whose code is the plain GEMM + CTA-mode peer
+// stores (measured: the extra code cost 0.7-1.5 µs per launch otherwise)
+template <bool kX>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Args A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -131,12 +137,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) KD_TRACE(0);
   pdl_launch_dependents();
-  epi_started(A.epi);
-  if (threadIdx.x < kMaxChunks) s_cnt[threadIdx.x] = 0u;  // (ordered by the __syncthreads below)
+  if constexpr (kX) {
+    epi_started(A.epi);
+    if (threadIdx.x < kMaxChunks) s_cnt[threadIdx.x] = 0u;  // (ordered by the __syncthreads below)
+  }
   // COUNT mode: tally the bytes this CTA streams into each chunk of the output row
   const int row_elems = A.silu ? A.N / 2 : A.N;
   auto count = [&](size_t yo, unsigned bytes) {
-    if (A.epi.nch) atomicAdd(&s_cnt[epi_chunk_of(A.epi, (uint32_t)(yo % (size_t)row_elems) * 2u)], bytes);
+    if constexpr (kX) {
+      if (A.epi.nch) atomicAdd(&s_cnt[epi_chunk_of(A.epi, (uint32_t)(yo % (size_t)row_elems) * 2u)], bytes);
+    }
   };
   const long long U = A.units, G = gridDim.x, c = blockIdx.x;
   const long long u0 = unit_begin(c, U, G), u1 = unit_begin(c + 1, U, G);
@@ -182,11 +192,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sa + (size_t)s * wst + b * kStageA, &tmap_w, (kb * kbs + b) * kBK, w_row(t), &full[s], pw);
     };
-    const int xi = acq_find(A.acq, 0);
+    const int xi = kX ? acq_find(A.acq, 0) : -1;
     uint32_t held = 0;
     auto load_x = [&](int t, int kb, int s) {
-      const int xr = A.groups ? __ldg(A.meta + A.groups + t / A.tpg) : 0;
-      acquire_x(A.acq, xi, kb, kbs, A.K, &held);
+      const int xr = A.groups ? __ldg(A.meta + A.moff + t / A.tpg) : 0;
+      if constexpr (kX) acquire_x(A.acq, xi, kb, kbs, A.K, &held);
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sb + (size_t)s * xst + b * xbox, &tmap_x, (kb * kbs + b) * kBK, xr, &full[s], px);
     };
@@ -290,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto out_coords = [&](int t, int* nb0, int* y0, int* mv) {
       const int grp = A.groups ? t / A.tpg : 0;
       *nb0 = (A.groups ? t % A.tpg : t) * kBM;
-      *y0 = A.groups ? __ldg(A.meta + A.groups + grp) : 0;
+      *y0 = A.groups ? __ldg(A.meta + A.moff + grp) : 0;
       *mv = A.groups ? min(__ldg(A.meta + grp), A.M) : A.M;
     };
     while (u < u1) {
@@ -562,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int grp = A.groups ? t / A.tpg : 0;
         const int nb0 = (A.groups ? t % A.tpg : t) * kBM;
-        const int y0 = A.groups ? __ldg(A.meta + A.groups + grp) : 0;
+        const int y0 = A.groups ? __ldg(A.meta + A.moff + grp) : 0;
         const int mv = A.groups ? min(__ldg(A.meta + grp), A.M) : A.M;
         const int j = (w * 4) / kBM, r = (w * 4) % kBM;
         const int nn = nb0 + r;
@@ -590,7 +600,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   // publish this CTA's stores to the consumer devices: CTA mode one release,
   // COUNT mode the bytes tallied per chunk
-  epi_signal_counts(A.epi, s_cnt);
+  if constexpr (kX) {
+    epi_signal_counts(A.epi, s_cnt);
+  } else if (A.epi.n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_acq_rel_sys();
+      for (int p = 0; p < A.epi.n; ++p) red_release_sys_add64(A.epi.flag[p], 1ull);
+    }
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1) {
@@ -993,6 +1011,7 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
     epi_signal(A.epi, (uint32_t)c0 * 2u, (uint32_t)(c0 + rows) * 2u, (uint32_t)M);
 }
 
+template <bool kX>  // as gemm_kernel: the handoff-protocol code only in the kX instance
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_csk_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ Args A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1028,7 +1047,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) KD_TRACE(0);
   pdl_launch_dependents();
-  epi_started(A.epi);
+  if constexpr (kX) epi_started(A.epi);
   const int rank = split > 1 ? (int)cluster_ctarank() : 0;
   const int tile = blockIdx.x / split;
   const int n0 = tile * kBM;
@@ -1077,10 +1096,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sa + (size_t)s * wst + b * kStageA, &tmap_w, ((kb0 + i) * kbs + b) * kBK, n0, &full[s], pw);
     };
-    const int xi = acq_find(A.acq, 0);
+    const int xi = kX ? acq_find(A.acq, 0) : -1;
     uint32_t held = 0;
     auto load_x = [&](int i, int s) {  // (this rank's K range only: it acquires only its own X chunks)
-      acquire_x(A.acq, xi, kb0 + i, kbs, A.K, &held);
+      if constexpr (kX) acquire_x(A.acq, xi, kb0 + i, kbs, A.K, &held);
       for (int b = 0; b < kbs; ++b)
         tma_load_2d(sb + (size_t)s * xst + b * xbox, &tmap_x, ((kb0 + i) * kbs + b) * kBK, 0, &full[s], px);
     };
@@ -1422,7 +1441,8 @@ static int max_clusters(int split) {
   if (v.empty()) {
     int sms = kNumSMs;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(gemm_csk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+    cudaFuncSetAttribute(gemm_csk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+    cudaFuncSetAttribute(gemm_csk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
     v.assign(9, 0);
     for (int c = 1; c <= 8; ++c) {
       int n = 0;
@@ -1438,9 +1458,14 @@ static int max_clusters(int split) {
       cfg.attrs = &at;
       cfg.numAttrs = 1;
       if (c == 1) n = sms;
-      else if (cudaOccupancyMaxActiveClusters(&n, gemm_csk_kernel, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        n = 0;
+      else {
+        int n2 = 0;  // both instances: the tiling must fit whichever is launched
+        if (cudaOccupancyMaxActiveClusters(&n, gemm_csk_kernel<false>, &cfg) != cudaSuccess ||
+            cudaOccupancyMaxActiveClusters(&n2, gemm_csk_kernel<true>, &cfg) != cudaSuccess) {
+          cudaGetLastError();
+          n = n2 = 0;
+        }
+        n = std::min(n, n2);
       }
       v[c] = n;
     }
@@ -1597,6 +1622,8 @@ GemmShape gemm_shape(const kd_attr_grouped_gemm& a) {
   s.K = a.K;
   s.groups = a.experts;
   s.dtype = a.dtype;
+  s.expert0 = a.expert0;
+  s.meta_experts = a.meta_experts ? a.meta_experts : a.experts;
   return s;
 }
 
@@ -1636,7 +1663,10 @@ kd_status gemm_prepare(const GemmShape& a, const void* X, const void* W, const v
   if (!X || !W || (a.groups && !meta)) return fail(KD_ERR_INVALID_ARG, "gemm: NULL operand");
   if (((uintptr_t)X | (uintptr_t)W) & 15) return fail(KD_ERR_INVALID_ARG, "gemm: operands must be 16-byte aligned");
   gp->sh = a;
-  gp->meta = (const int*)meta;
+  if (a.groups && a.expert0 + a.groups > a.meta_experts)
+    return fail(KD_ERR_INVALID_ARG, "grouped gemm: expert0 + experts exceeds meta_experts");
+  gp->meta = a.groups ? (const int*)meta + a.expert0 : nullptr;
+  gp->moff = (int)a.meta_experts;
   gp->dense = gemm::use_dense(a);
   if (gp->dense) {
     double ns = 0;
@@ -1654,6 +1684,15 @@ kd_status gemm_prepare(const GemmShape& a, const void* X, const void* W, const v
 }
 
 static unsigned long long* g_gemm_trace = nullptr;
+
+// the kX kernel instance is needed when the launch streams chunked (COUNT)
+// output, acquires remote inputs in-kernel, or records residency / log words
+static bool kx_needed(const LaunchCtx& c) {
+  if (c.epi.nch > 0 || c.acq.n > 0) return true;
+  for (int p = 0; p < c.epi.n; ++p)
+    if (c.epi.started[p] || c.epi.logt[p]) return true;
+  return false;
+}
 
 static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t* signals) {
   const GemmTile& t = gp.tile;
@@ -1686,7 +1725,9 @@ static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx&
   A.trace = g_gemm_trace;
   kd_status ks = kernels_init();
   if (ks) return ks;
-  KD_CUDA_CHECK(kd_launch_cluster(gemm::csk::gemm_csk_kernel, dim3(t.tiles * t.split), dim3(gemm::csk::kThreads),
+  const bool x = kx_needed(c);
+  KD_CUDA_CHECK(kd_launch_cluster(x ? gemm::csk::gemm_csk_kernel<true> : gemm::csk::gemm_csk_kernel<false>,
+                                  dim3(t.tiles * t.split), dim3(gemm::csk::kThreads),
                                   t.smem, c.stream, (unsigned)t.split, gp.tmap_w, gp.tmap_x, A),
                 "gemm (cluster split-K) launch");
   if (signals) return gemm_signals(gp.sh, signals);
@@ -1718,6 +1759,7 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   A.groups = (int)gp.sh.groups;
   A.tpg = (int)((gp.sh.N + gemm::kBM - 1) / gemm::kBM);
   A.meta = gp.meta;
+  A.moff = gp.moff;
   A.mma_n = g.mma_n;
   A.stages = g.stages;
   A.kblocks = g.kblocks;
@@ -1742,7 +1784,8 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   size_t sm = gemm::smem_bytes(g);
   kd_status ks = kernels_init();
   if (ks) return ks;
-  KD_CUDA_CHECK(kd_launch(gemm::gemm_kernel, dim3(g.grid), dim3(gemm::kThreads), sm, c.stream, gp.tmap_w, gp.tmap_x, A),
+  KD_CUDA_CHECK(kd_launch(kx_needed(c) ? gemm::gemm_kernel<true> : gemm::gemm_kernel<false>, dim3(g.grid),
+                          dim3(gemm::kThreads), sm, c.stream, gp.tmap_w, gp.tmap_x, A),
                 "gemm launch");
   if (signals) return gemm_signals(gp.sh, signals);
   return KD_OK;
@@ -1828,15 +1871,15 @@ kd_status gemm_grid(const GemmShape& a, uint32_t* grid) {
 }
 
 kd_status gemm_init_attrs() {
-  KD_CUDA_CHECK(cudaFuncSetAttribute(gemm::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
-                "gemm smem attr");
-  KD_CUDA_CHECK(cudaFuncSetAttribute(gemm::gemm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
-                "gemm carveout");
-  KD_CUDA_CHECK(cudaFuncSetAttribute(gemm::csk::gemm_csk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     gemm::csk::kSmemMax),
-                "gemm dense smem attr");
-  KD_CUDA_CHECK(cudaFuncSetAttribute(gemm::csk::gemm_csk_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
-                "gemm dense carveout");
+  for (auto f : {gemm::gemm_kernel<false>, gemm::gemm_kernel<true>}) {
+    KD_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), "gemm smem attr");
+    KD_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "gemm carveout");
+  }
+  for (auto f : {gemm::csk::gemm_csk_kernel<false>, gemm::csk::gemm_csk_kernel<true>}) {
+    KD_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::csk::kSmemMax),
+                  "gemm dense smem attr");
+    KD_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "gemm dense carveout");
+  }
   return KD_OK;
 }
 

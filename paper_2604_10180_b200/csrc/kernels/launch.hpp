@@ -136,6 +136,7 @@ struct GemmShape {
   uint32_t silu = 0;  // KD_OP_GEMM_SILU: output a [M, N/2] = silu·mul of the 64-row gate/up blocks
   uint32_t rope = 0;  // KD_OP_QKV_ROPE: cluster split-K kernel with the RoPE + KV-append epilogue
   uint32_t norm = 0;  // KD_OP_GEMM_RMSNORM: cluster split-K kernel with the add + RMSNorm epilogue
+  uint32_t expert0 = 0, meta_experts = 0;  // grouped: expert window inside the meta block (EP)
 };
 constexpr int kNormMaxGrid = 160;  // CTAs of a KD_OP_GEMM_RMSNORM launch (partial-sum scratch bound)
 GemmShape gemm_shape(const kd_attr_gemm& a, bool silu = false);
@@ -157,7 +158,8 @@ struct GemmPlan {
   alignas(64) CUtensorMap tmap_w;
   alignas(64) CUtensorMap tmap_x;
   GemmShape sh;
-  const int* meta = nullptr;  // grouped: int32 count[groups], offset[groups]
+  const int* meta = nullptr;  // grouped: int32 counts (+expert0); offsets at meta + moff
+  int moff = 0;               // grouped: meta_experts (offsets follow the counts of every expert)
   bool dense = false;         // cluster split-K kernel (else stream-K)
   const void* X = nullptr;    // fp32 path: plain operand pointers (SIMT kernel)
   const void* W = nullptr;
@@ -184,7 +186,7 @@ kd_status launch_moe_route(const kd_attr_moe_route& a, const void* h, const floa
                            uint32_t* signals);
 kd_status launch_moe_dispatch(const kd_attr_moe_dispatch& a, const void* h, const void* route, void* xg, void* meta,
                               const LaunchCtx& c, uint32_t* signals);
-kd_status launch_moe_combine(const kd_attr_moe_combine& a, const void* yg, const void* route, const void* meta,
+kd_status launch_moe_combine(const kd_attr_moe_combine& a, const void* const* ygs, const void* route, const void* meta,
                              void* out, const LaunchCtx& c, uint32_t* signals);
 kd_status moe_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s);
 // Mamba-2 kernels (ssm.cu)

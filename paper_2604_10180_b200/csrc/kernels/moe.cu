@@ -130,10 +130,15 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
   epi_signal(epi);
 }
 
-__global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __restrict__ yg,
-                                                      const int32_t* __restrict__ idx, const float* __restrict__ w,
-                                                      const int32_t* __restrict__ meta, __nv_bfloat16* __restrict__ out,
-                                                      int H, int E, int k, Epi epi) {
+constexpr int kMaxParts = 8;
+struct YParts {  // expert-parallel combine: expert e's rows live in part e / per_part
+  const __nv_bfloat16* p[kMaxParts];
+  int per_part;
+};
+
+__global__ void __launch_bounds__(256) combine_kernel(YParts ys, const int32_t* __restrict__ idx,
+                                                      const float* __restrict__ w, const int32_t* __restrict__ meta,
+                                                      __nv_bfloat16* __restrict__ out, int H, int E, int k, Epi epi) {
   pdl_launch_dependents();
   pdl_wait();
   const int row = blockIdx.x;
@@ -152,6 +157,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
     for (int jj = 0; jj < k; ++jj) {
       const int j = ord[jj];
       const float wj = w[(size_t)row * k + j];
+      const __nv_bfloat16* yg = ys.p[idx[(size_t)row * k + j] / ys.per_part];
       const uint4 y = *reinterpret_cast<const uint4*>(yg + (size_t)slot_of[(size_t)row * k + j] * H + c);
       acc[0] += wj * bf16lo(y.x);
       acc[1] += wj * bf16hi(y.x);
@@ -220,14 +226,23 @@ kd_status launch_moe_dispatch(const kd_attr_moe_dispatch& a, const void* h, cons
   return KD_OK;
 }
 
-kd_status launch_moe_combine(const kd_attr_moe_combine& a, const void* yg, const void* route, const void* meta,
+kd_status launch_moe_combine(const kd_attr_moe_combine& a, const void* const* ygs, const void* route, const void* meta,
                              void* out, const LaunchCtx& c, uint32_t* signals) {
   kd_status s = moe::check(a.rows, a.hidden, a.experts, a.top_k);
   if (s) return s;
-  if (!yg || !route || !meta || !out) return fail(KD_ERR_INVALID_ARG, "moe_combine: NULL pointer");
+  const uint32_t np = a.n_parts ? a.n_parts : 1;
+  if (np > (uint32_t)moe::kMaxParts || a.experts % np)
+    return fail(KD_ERR_UNSUPPORTED, "moe_combine: n_parts must divide experts (<= 8 parts)");
+  if (!ygs || !route || !meta || !out) return fail(KD_ERR_INVALID_ARG, "moe_combine: NULL pointer");
+  moe::YParts ys{};
+  ys.per_part = (int)(a.experts / np);
+  for (uint32_t i = 0; i < np; ++i) {
+    if (!ygs[i]) return fail(KD_ERR_INVALID_ARG, "moe_combine: NULL yg part");
+    ys.p[i] = (const __nv_bfloat16*)ygs[i];
+  }
   const int32_t* idx = (const int32_t*)route;
   const float* w = (const float*)(idx + (size_t)a.rows * a.top_k);
-  KD_CUDA_CHECK(kd_launch(moe::combine_kernel, dim3(a.rows), dim3(256), 0, c.stream, (const __nv_bfloat16*)yg, idx, w,
+  KD_CUDA_CHECK(kd_launch(moe::combine_kernel, dim3(a.rows), dim3(256), 0, c.stream, ys, idx, w,
                           (const int32_t*)meta, (__nv_bfloat16*)out, (int)a.hidden, (int)a.experts, (int)a.top_k,
                           c.epi),
                 "moe_combine launch");
@@ -236,7 +251,8 @@ kd_status launch_moe_combine(const kd_attr_moe_combine& a, const void* yg, const
 }
 
 kd_status moe_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s) {
-  if (attrs.size() != 16) return fail(KD_ERR_INVALID_ARG, "moe: attrs have the wrong size");
+  if (attrs.size() != (op == KD_OP_MOE_COMBINE ? sizeof(kd_attr_moe_combine) : 16))
+    return fail(KD_ERR_INVALID_ARG, "moe: attrs have the wrong size");
   uint32_t v[4];
   std::memcpy(v, attrs.data(), 16);
   *s = (op == KD_OP_MOE_DISPATCH) ? (uint32_t)moe::dispatch_grid(v[0], v[1], v[3]) : v[0];

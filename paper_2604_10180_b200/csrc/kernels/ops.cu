@@ -225,9 +225,11 @@ kd_status kd_op_moe_dispatch(const kd_attr_moe_dispatch* a, const void* h, const
 kd_status kd_op_moe_combine(const kd_attr_moe_combine* a, const void* yg, const void* route, const void* meta,
                             void* out, void* stream) {
   if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_moe_combine: NULL attrs");
+  if (a->n_parts > 1) return fail(KD_ERR_UNSUPPORTED, "kd_op_moe_combine: one yg (n_parts <= 1) through the single-op call");
   LaunchCtx c;
   c.stream = (cudaStream_t)stream;
-  return launch_moe_combine(*a, yg, route, meta, out, c, nullptr);
+  const void* parts[1] = {yg};
+  return launch_moe_combine(*a, parts, route, meta, out, c, nullptr);
 }
 
 }  // extern "C"

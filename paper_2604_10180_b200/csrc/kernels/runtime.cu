@@ -141,7 +141,12 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_MOE_ROUTE: ok = nr == 2 && nw == 1; break;
     case KD_OP_MOE_DISPATCH: ok = nr == 2 && nw == 1; break;  // writes [meta | xg]
     case KD_OP_GROUPED_GEMM: ok = nr == 3 && nw == 1; break;  // reads [xg, W, meta]
-    case KD_OP_MOE_COMBINE: ok = nr == 3 && nw == 1; break;   // reads [yg, route, meta]
+    case KD_OP_MOE_COMBINE: {  // reads [yg_0 .. yg_{n_parts-1}, route, meta]
+      kd_attr_moe_combine a;
+      std::memcpy(&a, k.attrs.data(), sizeof a);
+      ok = nr == std::max(1u, a.n_parts) + 2 && nw == 1;
+      break;
+    }
     case KD_OP_SSM_CONV: ok = nr == 4 && nw == 2; break;      // reads [zx, w, b, state] writes [xbc, state]
     case KD_OP_SSM_UPDATE: ok = nr == 6 && nw == 2; break;    // reads [xbc, zx, dt_b, A_log, D, S] writes [y, S]
     case KD_OP_GATED_NORM: ok = nr == 3 && nw == 1; break;    // reads [y, zx, w]
@@ -248,7 +253,8 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
     }
     case KD_OP_MOE_COMBINE: {
       auto a = attrs_get<kd_attr_moe_combine>(K);
-      st = launch_moe_combine(a, l.rd[0], l.rd[1], l.rd[2], l.wr[0], c, &sig);
+      const uint32_t np = std::max(1u, a.n_parts);
+      st = launch_moe_combine(a, (const void* const*)l.rd.data(), l.rd[np], l.rd[np + 1], l.wr[0], c, &sig);
       break;
     }
   }

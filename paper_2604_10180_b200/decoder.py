@@ -256,7 +256,7 @@ class DecoderGraph:
                 add("down", l, T_DOWN, K.KD_OP_GROUPED_GEMM, [f"ae.{l}", f"w_d_e.{l}", meta_span], [f"ye.{l}"],
                     K.kd_attr_grouped_gemm(m * k, H, F, E, m, act), 2 * m * k * H * F)
                 add("combine", l, T_COMBINE, K.KD_OP_MOE_COMBINE, [f"ye.{l}", f"route.{l}", meta_span], [f"d.{l}"],
-                    am)
+                    K.kd_attr_moe_combine(m, H, E, k, 1, 0))
             else:
                 if fuse_silu:
                     add("gu_silu", l, T_GU, K.KD_OP_GEMM_SILU, [f"h2.{l}", f"w_gu.{l}"], [f"a.{l}"],
@@ -690,6 +690,165 @@ class RoleDecoderGraph:
 
     def residual_global(self, rt) -> np.ndarray:
         """The residual stream [a·N·m, H] in global row order after a step."""
+        cfg = self.cfg
+        out = np.zeros((self.a * cfg.n_micro * cfg.m, cfg.hidden), np.float32)
+        for (name, i, d), t in rt.tensors.items():
+            if name.startswith("r."):
+                out[self.global_rows(int(name.split(".")[1]), i)] = t.cpu().numpy()
+        return out
+
+
+class MoEEPDecoderGraph:
+    """Expert-parallel MoE decode (BASELINE config 4 "router/attention kernels
+    disaggregated from expert GEMMs over 8 GPUs"; SURVEY §8(e) "MoE: EP with
+    P2P dispatch (rows to expert owner) and combine"). Logical devices 0..a−1
+    are attention/router shards (each its own m sequences per micro-batch:
+    norms, QKV/O GEMMs, RoPE/append, attention, router, dispatch, combine);
+    devices a..a+e−1 each own E/e experts (their gate_up / down weights only)
+    and run, per shard, the grouped gate_up GEMM, SiLU·mul and grouped down
+    GEMM over that shard's rows routed to their experts (expert window
+    expert0 = x·E/e of the shard's dispatch meta). The dispatch block [meta |
+    xg] is streamed to every expert device; each expert device streams its
+    experts' rows back in its own yg buffer; the shard's combine sums over the
+    e parts in ascending expert order (C1.12). Dense-attention MoE configs,
+    bf16. Global row order: micro-batch i, shard s, row j → (i·a + s)·m + j."""
+
+    def __init__(self, cfg, a: int, e: int, act: int = K.KD_BF16):
+        assert act == K.KD_BF16 and cfg.n_experts and not cfg.attn_every
+        E, k = cfg.n_experts, cfg.top_k
+        assert E % e == 0 and e <= 8, "experts must split evenly over the expert devices"
+        self.cfg, self.a, self.e = cfg, a, e
+        Ex = E // e
+        m, H, L = cfg.m, cfg.hidden, cfg.n_layers
+        Hq, Hkv, D, F = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn
+        pps = cfg.pages_per_seq
+        g = Graph()
+        self.g = g
+        self.buf, self.shape, self.dtype = {}, {}, {}
+        W, PM = K.KD_BUF_WEIGHT, K.KD_BUF_PER_MICROBATCH
+        PERS, INP, OUT = K.KD_BUF_PERSISTENT, K.KD_BUF_INPUT, K.KD_BUF_OUTPUT
+        nb = {"bf16": 2, "f32": 4, "i32": 4, "u8": 1}
+        mb = C.c_uint64()
+        K.check(K.kd_moe_meta_bytes(m, E, k, C.byref(mb)), "kd_moe_meta_bytes")
+        self.meta_bytes = mb.value
+
+        def buf(name, shape, dt, flags):
+            self.buf[name] = g.add_buffer(int(np.prod(shape)) * nb[dt], flags)
+            self.shape[name], self.dtype[name] = tuple(shape), dt
+
+        def whole(name):
+            return (self.buf[name], 0, int(np.prod(self.shape[name])) * nb[self.dtype[name]])
+
+        for s_ in range(a):
+            buf(f"r.{s_}", (m, H), "f32", PERS | INP | OUT | PM)
+            buf(f"bt.{s_}", (m, pps), "i32", INP | PM)
+            buf(f"sl.{s_}", (m,), "i32", INP | PM)
+        for l in range(L):
+            buf(f"w_qkv.{l}", (cfg.qkv_dim, H), "bf16", W)
+            buf(f"w_o.{l}", (H, Hq * D), "bf16", W)
+            buf(f"w_router.{l}", (E, H), "f32", W)
+            buf(f"g1.{l}", (H,), "bf16", W)
+            buf(f"g2.{l}", (H,), "bf16", W)
+            for x in range(e):
+                buf(f"w_gu_e.{l}.{x}", (Ex, 2 * F, H), "bf16", W)
+                buf(f"w_d_e.{l}.{x}", (Ex, H, F), "bf16", W)
+            for s_ in range(a):
+                buf(f"kc.{l}.{s_}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+                buf(f"vc.{l}.{s_}", (m * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+                for nm, shp in (("h1", (m, H)), ("qkv", (m, cfg.qkv_dim)), ("q", (m, Hq * D)), ("attn", (m, Hq * D)),
+                                ("o", (m, H)), ("h2", (m, H)), ("d", (m, H))):
+                    buf(f"{nm}.{l}.{s_}", shp, "bf16", PM)
+                buf(f"route.{l}.{s_}", (2 * m * k,), "i32", PM)
+                buf(f"xgm.{l}.{s_}", (self.meta_bytes + m * k * H * 2,), "u8", PM)
+                for x in range(e):
+                    buf(f"gue.{l}.{s_}.{x}", (m * k, 2 * F), "bf16", PM)
+                    buf(f"ae.{l}.{s_}.{x}", (m * k, F), "bf16", PM)
+                    buf(f"ye.{l}.{s_}.{x}", (m * k, H), "bf16", PM)
+        self.kernels: List[KernelInfo] = []
+        self.dev_of: List[int] = []
+
+        def add(name, layer, dev, op, reads, writes, attrs, flops=0):
+            sp = lambda x: x if isinstance(x, tuple) else whole(x)
+            kid = g.add_kernel(op, [sp(x) for x in reads], [sp(x) for x in writes], attrs, flops, -1, -1)
+            self.kernels.append(KernelInfo(name, layer, -1, kid))
+            self.dev_of.append(dev)
+
+        eps = float(cfg.eps)
+        am = K.kd_attr_moe(m, H, E, k)
+        for l in range(L):
+            for s_ in range(a):
+                nd = 1 if l > 0 else 0
+                add(f"norm1.{s_}", l, s_, K.KD_OP_ADD_RMSNORM,
+                    [f"r.{s_}"] + ([f"d.{l-1}.{s_}"] if nd else []) + [f"g1.{l}"], [f"h1.{l}.{s_}", f"r.{s_}"],
+                    K.kd_attr_add_rmsnorm(m, H, nd, act, eps, 0))
+                add(f"qkv.{s_}", l, s_, K.KD_OP_GEMM, [f"h1.{l}.{s_}", f"w_qkv.{l}"], [f"qkv.{l}.{s_}"],
+                    K.kd_attr_gemm(m, cfg.qkv_dim, H, act), 2 * m * cfg.qkv_dim * H)
+                add(f"rope.{s_}", l, s_, K.KD_OP_ROPE_APPEND, [f"qkv.{l}.{s_}", f"bt.{s_}", f"sl.{s_}"],
+                    [f"q.{l}.{s_}", f"kc.{l}.{s_}", f"vc.{l}.{s_}"],
+                    K.kd_attr_rope_append(m, Hq, Hkv, D, cfg.page, pps, act, 0, float(cfg.rope_theta)))
+                add(f"attn.{s_}", l, s_, K.KD_OP_ATTENTION,
+                    [f"q.{l}.{s_}", f"kc.{l}.{s_}", f"vc.{l}.{s_}", f"bt.{s_}", f"sl.{s_}"], [f"attn.{l}.{s_}"],
+                    K.kd_attr_attention(m, Hq, Hkv, D, cfg.page, pps, act, 0), 4 * m * Hq * cfg.context * D)
+                add(f"o.{s_}", l, s_, K.KD_OP_GEMM, [f"attn.{l}.{s_}", f"w_o.{l}"], [f"o.{l}.{s_}"],
+                    K.kd_attr_gemm(m, H, Hq * D, act), 2 * m * H * Hq * D)
+                add(f"norm2.{s_}", l, s_, K.KD_OP_ADD_RMSNORM, [f"r.{s_}", f"o.{l}.{s_}", f"g2.{l}"],
+                    [f"h2.{l}.{s_}", f"r.{s_}"], K.kd_attr_add_rmsnorm(m, H, 1, act, eps, 0))
+                add(f"route.{s_}", l, s_, K.KD_OP_MOE_ROUTE, [f"h2.{l}.{s_}", f"w_router.{l}"], [f"route.{l}.{s_}"],
+                    am, 2 * m * E * H)
+                add(f"dispatch.{s_}", l, s_, K.KD_OP_MOE_DISPATCH, [f"h2.{l}.{s_}", f"route.{l}.{s_}"],
+                    [f"xgm.{l}.{s_}"], am)
+                xgm = self.buf[f"xgm.{l}.{s_}"]
+                meta_span = (xgm, 0, self.meta_bytes)
+                xg_span = (xgm, self.meta_bytes, m * k * H * 2)
+                for x in range(e):
+                    dev = a + x
+                    add(f"gu.{s_}.{x}", l, dev, K.KD_OP_GROUPED_GEMM, [xg_span, f"w_gu_e.{l}.{x}", meta_span],
+                        [f"gue.{l}.{s_}.{x}"], K.kd_attr_grouped_gemm(m * k, 2 * F, H, Ex, m, act, x * Ex, E),
+                        2 * m * k * 2 * F * H // e)
+                    add(f"silu.{s_}.{x}", l, dev, K.KD_OP_SILU_MUL, [f"gue.{l}.{s_}.{x}"], [f"ae.{l}.{s_}.{x}"],
+                        K.kd_attr_silu_mul(m * k, F, act, 0))
+                    add(f"down.{s_}.{x}", l, dev, K.KD_OP_GROUPED_GEMM, [f"ae.{l}.{s_}.{x}", f"w_d_e.{l}.{x}", meta_span],
+                        [f"ye.{l}.{s_}.{x}"], K.kd_attr_grouped_gemm(m * k, H, F, Ex, m, act, x * Ex, E),
+                        2 * m * k * H * F // e)
+                add(f"combine.{s_}", l, s_, K.KD_OP_MOE_COMBINE,
+                    [f"ye.{l}.{s_}.{x}" for x in range(e)] + [f"route.{l}.{s_}", meta_span], [f"d.{l}.{s_}"],
+                    K.kd_attr_moe_combine(m, H, E, k, e, 0))
+        for s_ in range(a):
+            add(f"final_add.{s_}", L - 1, s_, K.KD_OP_RESIDUAL_ADD, [f"r.{s_}", f"d.{L-1}.{s_}"], [f"r.{s_}"],
+                K.kd_attr_residual_add(m, H, 1, 0))
+        g.finalize()
+
+    def assign(self) -> List[int]:
+        """Attention/router shards on devices 0..a−1, expert devices a..a+e−1."""
+        return list(self.dev_of)
+
+    def global_rows(self, s: int, i: int) -> np.ndarray:
+        m, a = self.cfg.m, self.a
+        return np.arange((i * a + s) * m, (i * a + s + 1) * m)
+
+    def host_value(self, name, i, inputs):
+        cfg = self.cfg
+        pps = cfg.pages_per_seq
+        parts = name.split(".")
+        base = parts[0]
+        if base in ("r", "bt", "sl"):
+            rr = self.global_rows(int(parts[1]), i)
+            if base == "r":
+                return inputs.x[rr]
+            if base == "sl":
+                return inputs.seq_len[rr]
+            return (np.arange(cfg.m, dtype=np.int32)[:, None] * pps + np.arange(pps, dtype=np.int32)[None, :])
+        l = int(parts[1])
+        lw = inputs.layers[l]
+        if base in ("kc", "vc"):
+            pool = (inputs.k_cache if base == "kc" else inputs.v_cache)[l]
+            return pool[inputs.block_table[self.global_rows(int(parts[2]), i)].reshape(-1)]
+        if base in ("w_gu_e", "w_d_e"):
+            x, Ex = int(parts[2]), cfg.n_experts // self.e
+            return (lw.w_gu_e if base == "w_gu_e" else lw.w_d_e)[x * Ex:(x + 1) * Ex]
+        return {"w_qkv": lw.w_qkv, "w_o": lw.w_o, "w_router": lw.w_router, "g1": lw.gamma1, "g2": lw.gamma2}[base]
+
+    def residual_global(self, rt) -> np.ndarray:
         cfg = self.cfg
         out = np.zeros((self.a * cfg.n_micro * cfg.m, cfg.hidden), np.float32)
         for (name, i, d), t in rt.tensors.items():

@@ -170,7 +170,7 @@ def test_moe_ffn_pipeline_vs_oracle(kd, rows, H, F, E):
     K.check(K.kd_op_grouped_gemm(a2, act.data_ptr(), wd_d.data_ptr(), xgm.data_ptr(), y.data_ptr(),
                                  scr.data_ptr(), s), "down")
     out = torch.empty(rows, H, dtype=torch.bfloat16, device="cuda")
-    K.check(K.kd_op_moe_combine(am, y.data_ptr(), route.data_ptr(), xgm.data_ptr(), out.data_ptr(), s), "combine")
+    K.check(K.kd_op_moe_combine(K.kd_attr_moe_combine(rows, H, E, k, 1, 0), y.data_ptr(), route.data_ptr(), xgm.data_ptr(), out.data_ptr(), s), "combine")
     torch.cuda.synchronize()
     ridx, rw = OL.moe_route(OL.bf16_to_f64(h), wr, k)
     assert np.array_equal(idx, ridx)          # no near-ties with these seeds (checked in the route test)
