@@ -130,6 +130,89 @@ def small_ops(m):
     return out
 
 
+def ssm_ops(rows=64, nh=128, P=64, N=128, G=8, W=4):
+    """Mamba-2 decode kernels at the hybrid config (state fp32
+    [64,128,64,128] = 256 MiB read + write)."""
+    import ctypes as C
+    di = nh * P
+    ch = di + 2 * G * N
+    pin = 2 * di + 2 * G * N + nh
+    a = K.kd_attr_ssm(rows, nh, P, N, G, W, K.KD_BF16, 1e-5)
+    zx = torch.randn(rows, pin, device="cuda").to(torch.bfloat16)
+    cw = (torch.randn(ch, W, device="cuda") * 0.5).to(torch.bfloat16)
+    cb = (torch.randn(ch, device="cuda") * 0.5).to(torch.bfloat16)
+    cst = torch.randn(rows, ch, W - 1, device="cuda").to(torch.bfloat16)
+    xbc = torch.empty(rows, ch, device="cuda", dtype=torch.bfloat16)
+    dtb = torch.full((nh,), -2.0, device="cuda")
+    alog = torch.zeros(nh, device="cuda")
+    Dp = torch.ones(nh, device="cuda")
+    S = torch.randn(rows, nh, P, N, device="cuda") * 0.1
+    y = torch.empty(rows, di, device="cuda", dtype=torch.bfloat16)
+    nw = torch.ones(di, device="cuda").to(torch.bfloat16)
+    yn = torch.empty(rows, di, device="cuda", dtype=torch.bfloat16)
+    st = lambda: torch.cuda.current_stream().cuda_stream
+    out = []
+    out.append(("ssm_conv", timeit(lambda i: K.check(K.kd_op_ssm_conv(a, zx.data_ptr(), cw.data_ptr(), cb.data_ptr(),
+                                                                       cst.data_ptr(), xbc.data_ptr(), st()))),
+                rows * ch * 2 + rows * ch * (W - 1) * 2 * 2 + ch * W * 2 + ch * 2 + rows * ch * 2))
+    out.append(("ssm_update", timeit(lambda i: K.check(K.kd_op_ssm_update(a, xbc.data_ptr(), zx.data_ptr(), dtb.data_ptr(),
+                                                                           alog.data_ptr(), Dp.data_ptr(), S.data_ptr(),
+                                                                           y.data_ptr(), st()))),
+                S.numel() * 4 * 2 + rows * ch * 2 + rows * nh * 2 + rows * di * 2 + nh * 12))
+    out.append(("gated_norm", timeit(lambda i: K.check(K.kd_op_gated_norm(a, y.data_ptr(), zx.data_ptr(), nw.data_ptr(),
+                                                                           yn.data_ptr(), st()))),
+                rows * di * 2 * 3 + di * 2))
+    return out
+
+
+def moe_ops(rows=128, H=4096, F=14336, E=8, k=2):
+    """Mixtral-shaped MoE decode (SURVEY a11, B = 128): router, dispatch, the two
+    grouped expert GEMMs (every expert's weights streamed once: 1.88 + 0.94
+    GB), SiLU·mul on the routed rows, combine."""
+    import ctypes as C
+    h = torch.randn(rows, H, device="cuda").to(torch.bfloat16)
+    wr = torch.randn(E, H, device="cuda") / math.sqrt(H)
+    route = torch.empty(2 * rows * k, dtype=torch.int32, device="cuda")
+    am = K.kd_attr_moe(rows, H, E, k)
+    st = lambda: torch.cuda.current_stream().cuda_stream
+    K.check(K.kd_op_moe_route(am, h.data_ptr(), wr.data_ptr(), route.data_ptr(), st()))
+    mb = C.c_uint64()
+    K.check(K.kd_moe_meta_bytes(rows, E, k, C.byref(mb)))
+    xgm = torch.zeros(mb.value + rows * k * H * 2, dtype=torch.uint8, device="cuda")
+    K.check(K.kd_op_moe_dispatch(am, h.data_ptr(), route.data_ptr(), xgm.data_ptr() + mb.value, xgm.data_ptr(), st()))
+    torch.cuda.synchronize()
+    wgu = torch.randn(E, 2 * F, H, device="cuda").to(torch.bfloat16) * (1 / math.sqrt(H))
+    wd = torch.randn(E, H, F, device="cuda").to(torch.bfloat16) * (1 / math.sqrt(F))
+    a1 = K.kd_attr_grouped_gemm(rows * k, 2 * F, H, E, rows, K.KD_BF16, 0, E)
+    a2 = K.kd_attr_grouped_gemm(rows * k, H, F, E, rows, K.KD_BF16, 0, E)
+    scr = torch.zeros(max(api.op_scratch_bytes(K.KD_OP_GROUPED_GEMM, a1), api.op_scratch_bytes(K.KD_OP_GROUPED_GEMM, a2)),
+                      dtype=torch.uint8, device="cuda")
+    gu = torch.empty(rows * k, 2 * F, dtype=torch.bfloat16, device="cuda")
+    act = torch.empty(rows * k, F, dtype=torch.bfloat16, device="cuda")
+    yg = torch.empty(rows * k, H, dtype=torch.bfloat16, device="cuda")
+    out_t = torch.empty(rows, H, dtype=torch.bfloat16, device="cuda")
+    n = rows * k
+    out = []
+    out.append(("moe_route", timeit(lambda i: K.check(K.kd_op_moe_route(am, h.data_ptr(), wr.data_ptr(), route.data_ptr(),
+                                                                         st()))), rows * H * 2 + E * H * 4 + n * 8))
+    out.append(("moe_dispatch", timeit(lambda i: K.check(K.kd_op_moe_dispatch(am, h.data_ptr(), route.data_ptr(),
+                                                                               xgm.data_ptr() + mb.value, xgm.data_ptr(),
+                                                                               st()))), n * 8 + n * H * 2 * 2 + mb.value))
+    out.append(("grouped_gemm_gate_up", timeit(lambda i: K.check(K.kd_op_grouped_gemm(
+        a1, xgm.data_ptr() + mb.value, wgu.data_ptr(), xgm.data_ptr(), gu.data_ptr(), scr.data_ptr(), st())), iters=5),
+        wgu.numel() * 2 + n * H * 2 + n * 2 * F * 2))
+    sa = K.kd_attr_silu_mul(n, F, K.KD_BF16, 0)
+    out.append(("moe_silu_mul", timeit(lambda i: api.silu_mul(sa, gu, act)), n * F * 2 * 3))
+    out.append(("grouped_gemm_down", timeit(lambda i: K.check(K.kd_op_grouped_gemm(
+        a2, act.data_ptr(), wd.data_ptr(), xgm.data_ptr(), yg.data_ptr(), scr.data_ptr(), st())), iters=5),
+        wd.numel() * 2 + n * F * 2 + n * H * 2))
+    ac = K.kd_attr_moe_combine(rows, H, E, k, 1, 0)
+    out.append(("moe_combine", timeit(lambda i: K.check(K.kd_op_moe_combine(ac, yg.data_ptr(), route.data_ptr(),
+                                                                             xgm.data_ptr(), out_t.data_ptr(), st()))),
+                n * H * 2 + n * 8 + n * 4 + rows * H * 2))
+    return out
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--m", type=int, default=64)
@@ -144,6 +227,13 @@ def main():
              ("gemm_down_norm", lambda: gemm_norm(m, 4096, 14336, 2)),
              ("attention", lambda: attention(m, 32, 8, 128, 4096)),
              ("gemm_overhead_1kb", lambda: gemm(m, 128 * 148, 64, 2))]
+    for grp, fn in (("ssm", ssm_ops), ("moe", moe_ops)):
+        if args.only == grp or args.only == "all2":
+            for name, us, b in fn():
+                print(json.dumps({"kernel": name, "us": round(us, 2), "bytes": b, "GBps": round(b / us / 1e3, 1),
+                                  "frac": round(b / us / 1e3 / pk, 3)}), flush=True)
+    if args.only in ("ssm", "moe", "all2"):
+        return
     if not args.only or args.only == "small":
         for name, us, b in small_ops(m):
             print(json.dumps({"kernel": name, "m": m, "us": round(us, 2), "bytes": b,
