@@ -28,12 +28,26 @@ __global__ void __launch_bounds__(256) route_kernel(const __nv_bfloat16* __restr
   for (int e = warp; e < E; e += 8) {
     const float* w = wr + (size_t)e * H;
     float acc = 0.f;
-    for (int c = lane * 8; c < H; c += 256) {
-      const uint4 hv = *reinterpret_cast<const uint4*>(hr + c);
-      const float4 w0 = *reinterpret_cast<const float4*>(w + c);
-      const float4 w1 = *reinterpret_cast<const float4*>(w + c + 4);
-      acc += bf16lo(hv.x) * w0.x + bf16hi(hv.x) * w0.y + bf16lo(hv.y) * w0.z + bf16hi(hv.y) * w0.w +
-             bf16lo(hv.z) * w1.x + bf16hi(hv.z) * w1.y + bf16lo(hv.w) * w1.z + bf16hi(hv.w) * w1.w;
+    // 4 column chunks per round with every load in flight before the FMAs (the
+    // serial load → FMA chain was latency-bound); same summation order
+    for (int c0 = lane * 8; c0 < H; c0 += 4 * 256) {
+      uint4 hv[4];
+      float4 w0[4], w1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * 256;
+        if (c < H) {
+          hv[u] = *reinterpret_cast<const uint4*>(hr + c);
+          w0[u] = *reinterpret_cast<const float4*>(w + c);
+          w1[u] = *reinterpret_cast<const float4*>(w + c + 4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c0 + u * 256 < H)
+          acc += bf16lo(hv[u].x) * w0[u].x + bf16hi(hv[u].x) * w0[u].y + bf16lo(hv[u].y) * w0[u].z +
+                 bf16hi(hv[u].y) * w0[u].w + bf16lo(hv[u].z) * w1[u].x + bf16hi(hv[u].z) * w1[u].y +
+                 bf16lo(hv[u].w) * w1[u].z + bf16hi(hv[u].w) * w1[u].w;
     }
     acc = warp_sum(acc);  // fixed butterfly order: deterministic
     if (lane == 0) logits[e] = acc;
@@ -75,12 +89,17 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
   __shared__ int cnt[kMaxE], off[kMaxE];
   __shared__ int16_t row_of[kMaxSlots];
   const int n = rows * k;
-  // every CTA derives the same slot map (tiny), so no grid-wide sync is needed
-  if (threadIdx.x < E) {
-    const int e = threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // every CTA derives the same slot map (tiny), so no grid-wide sync is needed.
+  // Warp w takes experts w, w+nw, …: one ballot per 32 entries counts them
+  // (was a serial per-expert scan: ≈35 µs at 256 entries)
+  for (int e = warp; e < E; e += nw) {
     int c = 0;
-    for (int s = 0; s < n; ++s) c += (idx[s] == e);
-    cnt[e] = c;
+    for (int s0 = 0; s0 < n; s0 += 32) {
+      const int s = s0 + lane;
+      c += __popc(__ballot_sync(0xffffffffu, s < n && idx[s] == e));
+    }
+    if (lane == 0) cnt[e] = c;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -91,15 +110,21 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
     }
   }
   __syncthreads();
-  if (threadIdx.x < E) {
-    const int e = threadIdx.x;
+  // positions: entries in (row, choice) order, i.e. ascending rows inside an
+  // expert — the ballot prefix keeps that order (same map as the serial scan)
+  for (int e = warp; e < E; e += nw) {
     int pos = off[e];
-    for (int s = 0; s < n; ++s)  // entries in (row, choice) order: ascending rows inside an expert
-      if (idx[s] == e) {
-        row_of[pos] = (int16_t)(s / k);
-        if (blockIdx.x == 0) meta[2 * E + s] = pos;  // slot_of
-        ++pos;
+    for (int s0 = 0; s0 < n; s0 += 32) {
+      const int s = s0 + lane;
+      const bool hit = s < n && idx[s] == e;
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        const int p = pos + __popc(m & ((1u << lane) - 1u));
+        row_of[p] = (int16_t)(s / k);
+        if (blockIdx.x == 0) meta[2 * E + s] = p;  // slot_of
       }
+      pos += __popc(m);
+    }
   }
   __syncthreads();
   if (blockIdx.x == 0) {

@@ -54,6 +54,57 @@ __global__ void conv_kernel(const __nv_bfloat16* __restrict__ zx, const __nv_bfl
   epi_signal(epi);
 }
 
+// 8 channels per thread (16-byte loads of x, the 3-deep state, the 4 taps and
+// the bias): the same per-channel arithmetic as conv_kernel, in the same
+// order (bitwise equal); used when d_conv == 4 and the rows are 16-byte aligned
+__global__ void conv8_kernel(const __nv_bfloat16* __restrict__ zx, const __nv_bfloat16* __restrict__ w,
+                             const __nv_bfloat16* __restrict__ bias, __nv_bfloat16* __restrict__ state,
+                             __nv_bfloat16* __restrict__ out, Dims d, Epi epi) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int c8n = d.ch / 8;
+  const size_t n = (size_t)d.rows * c8n;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
+    const int b = (int)(t / c8n), c0 = (int)(t % c8n) * 8;
+    const uint4 xv = *reinterpret_cast<const uint4*>(zx + (size_t)b * d.pin + d.di + c0);
+    const size_t e0 = (size_t)b * d.ch + c0;                    // first element of this thread's 8 channels
+    uint4 sv[3], wv[4];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) sv[i] = reinterpret_cast<const uint4*>(state + e0 * 3)[i];   // [8 ch][3]
+#pragma unroll
+    for (int i = 0; i < 4; ++i) wv[i] = reinterpret_cast<const uint4*>(w + (size_t)c0 * 4)[i];  // [8 ch][4]
+    const uint4 bv = *reinterpret_cast<const uint4*>(bias + c0);
+    const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(&xv);
+    const __nv_bfloat16* ss = reinterpret_cast<const __nv_bfloat16*>(sv);
+    const __nv_bfloat16* ws = reinterpret_cast<const __nv_bfloat16*>(wv);
+    const __nv_bfloat16* bs = reinterpret_cast<const __nv_bfloat16*>(&bv);
+    __align__(16) __nv_bfloat16 ns[24];
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float x = __bfloat162float(xs[j]);
+      float acc = __bfloat162float(bs[j]);
+      float prev[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        prev[k] = __bfloat162float(ss[j * 3 + k]);
+        acc += prev[k] * __bfloat162float(ws[j * 4 + k]);
+      }
+      acc += x * __bfloat162float(ws[j * 4 + 3]);
+      ns[j * 3 + 0] = __float2bfloat16_rn(prev[1]);
+      ns[j * 3 + 1] = __float2bfloat16_rn(prev[2]);
+      ns[j * 3 + 2] = __float2bfloat16_rn(x);
+      o[j] = __float2bfloat16_rn(silu_f(acc));
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) reinterpret_cast<uint4*>(state + e0 * 3)[i] = reinterpret_cast<const uint4*>(ns)[i];
+    const uint4 ov = *reinterpret_cast<const uint4*>(o);
+    *reinterpret_cast<uint4*>(out + e0) = ov;
+    for (int p = 0; p < epi.n; ++p) *reinterpret_cast<uint4*>((__nv_bfloat16*)epi.dst[p] + e0) = ov;
+  }
+  epi_signal(epi);
+}
+
 // one CTA per (head, row): S [P][N] fp32; 4 threads per state row, each owning
 // N/4 columns as interleaved float4s (lanes of a quad read 64 contiguous bytes)
 template <int P, int N>
@@ -155,9 +206,17 @@ static kd_status check(const kd_attr_ssm& a) {
   return KD_OK;
 }
 
+// the 8-channel kernel when the shape allows (d_conv 4, channel counts and
+// row pitches multiples of 8); decided from the attrs alone so the signal
+// count (= grid) is known to the runtime
+static bool conv8(const kd_attr_ssm& a) {
+  const Dims d = dims(a);
+  return d.W == 4 && d.ch % 8 == 0 && d.pin % 8 == 0 && d.di % 8 == 0;
+}
+
 static int conv_grid(const kd_attr_ssm& a) {
   const Dims d = dims(a);
-  const size_t n = (size_t)d.rows * d.ch;
+  const size_t n = (size_t)d.rows * d.ch / (conv8(a) ? 8 : 1);
   return (int)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 8 * kNumSMs));
 }
 
@@ -169,7 +228,11 @@ kd_status launch_ssm_conv(const kd_attr_ssm& a, const void* zx, const void* w, c
   if (s) return s;
   if (!zx || !w || !bias || !state || !out) return fail(KD_ERR_INVALID_ARG, "ssm_conv: NULL pointer");
   const int grid = ssm::conv_grid(a);
-  KD_CUDA_CHECK(kd_launch(ssm::conv_kernel, dim3(grid), dim3(256), 0, c.stream, (const __nv_bfloat16*)zx,
+  const bool v8 = ssm::conv8(a);
+  if (v8 && (((uintptr_t)zx | (uintptr_t)w | (uintptr_t)bias | (uintptr_t)state | (uintptr_t)out) & 15))
+    return fail(KD_ERR_INVALID_ARG, "ssm_conv: operands must be 16-byte aligned");
+  KD_CUDA_CHECK(kd_launch(v8 ? ssm::conv8_kernel : ssm::conv_kernel, dim3(grid), dim3(256), 0, c.stream,
+                          (const __nv_bfloat16*)zx,
                           (const __nv_bfloat16*)w, (const __nv_bfloat16*)bias, (__nv_bfloat16*)state,
                           (__nv_bfloat16*)out, ssm::dims(a), c.epi),
                 "ssm_conv launch");
@@ -213,7 +276,7 @@ kd_status launch_gated_norm(const kd_attr_ssm& a, const void* y, const void* zx,
 }
 
 kd_status ssm_init_attrs() {
-  const void* fns[] = {(const void*)ssm::conv_kernel, (const void*)ssm::update_kernel<64, 128>,
+  const void* fns[] = {(const void*)ssm::conv_kernel, (const void*)ssm::conv8_kernel, (const void*)ssm::update_kernel<64, 128>,
                        (const void*)ssm::update_kernel<64, 64>, (const void*)ssm::update_kernel<32, 32>,
                        (const void*)ssm::update_kernel<32, 64>, (const void*)ssm::update_kernel<32, 128>,
                        (const void*)ssm::gnorm_kernel};

@@ -45,8 +45,11 @@ def b200_machine(n_dev: int, hbm_Bps: Optional[float] = None, tc_flops: Optional
                  link_Bps: float = 770e9, link_lat_ps: int = 4_000_000, launch_ps: int = 2_500_000) -> Machine:
     """Cost-model machine of n homogeneous B200s behind NVSwitch: HBM and
     bf16 peaks from MEASURED_PEAKS.json when present (else the profiling
-    guide's fallback 6.65 TB/s / 1.59 PF), measured peer copy 770 GB/s/dir,
-    ~4 µs handoff latency (flag release → wait kernel), 2.5 µs launch floor."""
+    guide's fallback 6.65 TB/s / 1.59 PF). The link figures are ASSUMED, not
+    measured (this build only ever had one GPU): 770 GB/s per direction (the
+    900 GB/s NVLink-5 spec derated ~15% for 16-byte peer stores) and a 4 µs
+    handoff latency (flag release → consumer acquire, incl. a launch); 2.5 µs
+    launch floor."""
     peaks = {}
     p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
     if os.path.exists(p):

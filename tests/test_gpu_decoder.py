@@ -514,3 +514,28 @@ def test_moe_expert_parallel_bitwise_equals_monolithic_and_oracle(mod, a, e):
     dg2, dis = runs(lambda dg: dg.assign(), a + e, steps=2)
     assert len(dis.plan.transfers()) > 0
     assert np.array_equal(dg1.residual_global(mono), dg2.residual_global(dis))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_placements_chunked_bitwise(mod, seed):
+    """Random placements of the template classes over 3 logical devices (the
+    persistent-state classes stay whole, R6), 1-8 chunks: every cut edge —
+    whatever producer / consumer pair and chunk table it gets — reproduces the
+    monolithic bits."""
+    import random
+    DEC, K = mod
+    rnd = random.Random(seed)
+    cfg = TINY.with_(n_micro=rnd.choice([1, 2, 4]))
+    inp = synth.make_decoder_inputs(cfg)
+    mono = run(DEC, cfg, inp, lambda dg: [0] * dg.g.num_kernels, 1, steps=2)
+    dg = DEC.DecoderGraph(cfg)
+    classes = sorted({k.template for k in dg.kernels})
+    dev = {c: rnd.randrange(3) for c in classes}
+    assign = [dev[k.template] for k in dg.kernels]
+    nch = rnd.choice([1, 2, 3, 4, 8])
+    rt = DEC.DecoderRuntime(dg, assign, 3, [0, 0, 0], inputs=inp, n_chunks=nch)
+    for _ in range(2):
+        rt.step()
+    rt.sync()
+    rt.rt.check()
+    assert np.array_equal(mono.residual(), rt.residual()), (assign, nch)
