@@ -70,7 +70,16 @@ enum {
   KD_BUF_OUTPUT = 1u << 2,         /* read by the caller after the step */
   KD_BUF_PERSISTENT = 1u << 3,     /* cross-iteration state (KV cache, SSM state); all
                                       kernels touching it must be co-located (R6) */
-  KD_BUF_PER_MICROBATCH = 1u << 4  /* one instance per micro-batch */
+  KD_BUF_PER_MICROBATCH = 1u << 4, /* one instance per micro-batch */
+  /* with PERSISTENT: cross-iteration state REPLICATED on every device whose
+   * kernels touch it, writes propagated as deltas ("maintains a
+   * replica on each GPU and propagates the delta memory to other replicas").
+   * The caller binds one identically initialised replica per device; a kernel
+   * writing it mirrors exactly the bytes it writes into every peer replica
+   * (fused stores, released with its transfer to that device), so readers on
+   * other devices see them; the cost model charges the delta (e.g. RoPE/append:
+   * the appended K or V slot, rows·Hkv·D·elem), not the declared span. */
+  KD_BUF_REPLICATED = 1u << 5
 };
 
 typedef struct {
@@ -391,6 +400,10 @@ void kd_runtime_destroy(kd_runtime* rt);
 kd_status kd_runtime_bind(kd_runtime* rt, uint32_t buf, uint32_t micro, uint32_t dev, void* dev_ptr);
 kd_status kd_runtime_set_workspace(kd_runtime* rt, uint32_t dev, void* dev_ptr, uint64_t bytes);
 kd_status kd_runtime_set_peer_workspace(kd_runtime* rt, uint32_t dev, void* mapped_ptr);
+/* Multi-process delta replication: the replica of REPLICATED buffer `buf`
+ * (micro-batch instance `micro`) on remote device `dev`, as mapped in this
+ * process (CUDA IPC). In loopback the runtime uses the local bindings. */
+kd_status kd_runtime_set_peer_buffer(kd_runtime* rt, uint32_t buf, uint32_t micro, uint32_t dev, void* mapped_ptr);
 kd_status kd_runtime_set_mode(kd_runtime* rt, uint32_t mode);
 /* 1 = capture each device's step into a CUDA graph on first kd_step and
  * replay it afterwards (default 1). */

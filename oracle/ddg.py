@@ -139,9 +139,18 @@ def brute_force_ddg(kernels) -> List[Edge]:
     return edges
 
 
-def edge_bytes(edges: Sequence[Edge]) -> Dict[Tuple[int, int], int]:
-    """d_ij = Σ record lengths over records (i, j) (Table 2, R3)."""
+def edge_bytes(edges: Sequence[Edge], repl=None) -> Dict[Tuple[int, int], int]:
+    """d_ij = Σ record lengths over records (i, j) (Table 2, R3).
+    repl: {(src, buf): delta bytes} for REPLICATED buffers (P:465-466 delta
+    replication): their records charge the producer's delta once per
+    (src, dst, buf) instead of the span."""
     d: Dict[Tuple[int, int], int] = {}
-    for s, t, _, _, ln in edges:
+    seen = set()
+    for s, t, buf, _, ln in edges:
+        if repl is not None and (s, buf) in repl:
+            add = repl[(s, buf)] if (s, t, buf) not in seen else 0
+            seen.add((s, t, buf))
+            d[(s, t)] = d.get((s, t), 0) + add
+            continue
         d[(s, t)] = d.get((s, t), 0) + ln
     return d

@@ -25,20 +25,47 @@ from .ddg import _union
 from .placement import PS, Machine, ceil_div
 
 
-def transfers_of(edges, assign) -> Dict[Tuple[int, int], int]:
+def transfers_of(edges, assign, repl=None) -> Dict[Tuple[int, int], int]:
     """(producer k, remote device g) -> bytes: union of the edge-record spans
-    from k to kernels placed on g ≠ assign[k] (R3 dedup)."""
+    from k to kernels placed on g ≠ assign[k] (R3 dedup); records on a
+    REPLICATED buffer (repl = {(src, buf): delta bytes}) add the producer's
+    delta once per buffer instead."""
     spans: Dict[Tuple[int, int], list] = {}
+    deltas: Dict[Tuple[int, int], set] = {}
     for s, d, buf, off, ln in edges:
         g = assign[d]
-        if g != assign[s]:
+        if g == assign[s]:
+            continue
+        if repl is not None and (s, buf) in repl:
+            deltas.setdefault((s, g), set()).add(buf)
+            spans.setdefault((s, g), [])
+        else:
             spans.setdefault((s, g), []).append((buf, off, ln))
-    return {key: sum(e - a for ivs in _union(v).values() for a, e in ivs)
+    return {key: sum(e - a for ivs in _union(v).values() for a, e in ivs) +
+            sum(repl[(key[0], b)] for b in deltas.get(key, ()))
             for key, v in spans.items()}
 
 
+def delta_table(kernels, replicated_bufs):
+    """{(kernel, buf): bytes it writes per step into a REPLICATED buffer}: the
+    appended K or V slot for RoPE/append (rows·Hkv·D·elem, capped at the
+    span), else the declared span (R24-R26 reading of P:465-466).
+    kernels[k] = (op_name, attrs_dict, reads, writes)."""
+    out = {}
+    for k, (op, a, _r, writes) in enumerate(kernels):
+        for wi, (buf, _off, ln) in enumerate(writes):
+            if buf not in replicated_bufs:
+                continue
+            d = ln
+            if op in ("ROPE_APPEND", "QKV_ROPE") and wi in (1, 2):
+                esz = 4 if a.get("dtype", 0) == 1 else 2
+                d = min(ln, a["rows"] * a["n_kv_heads"] * a["head_dim"] * esz)
+            out[(k, buf)] = out.get((k, buf), 0) + d
+    return out
+
+
 def list_schedule(K: int, t_dev: Sequence[int], assign: Sequence[int], edges,
-                  m: Machine, n_micro: int):
+                  m: Machine, n_micro: int, repl=None):
     """Simulate one step. t_dev[k] = t_{k,assign[k]} (ps, per micro-batch).
     Returns a list of entries (dev, i, k, start, end) sorted by
     (start, dev, i, k) — a global topological order whose restriction to each
@@ -47,7 +74,7 @@ def list_schedule(K: int, t_dev: Sequence[int], assign: Sequence[int], edges,
     for s, d, *_ in edges:
         if s not in preds[d]:
             preds[d].append(s)
-    xfer = transfers_of(edges, assign)
+    xfer = transfers_of(edges, assign, repl)
     out_x: Dict[int, List[Tuple[int, int]]] = {}
     for (k, g), b in sorted(xfer.items()):
         out_x.setdefault(k, []).append((g, b))

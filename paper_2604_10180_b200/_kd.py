@@ -22,6 +22,7 @@ KD_OK, KD_ERR_INVALID_ARG, KD_ERR_RANGE, KD_ERR_STATE, KD_ERR_PIN_CONFLICT, KD_E
     KD_ERR_UNSUPPORTED, KD_ERR_CUDA, KD_ERR_NCCL, KD_ERR_TIMEOUT, KD_ERR_OOM = range(11)
 # buffer flags
 KD_BUF_WEIGHT, KD_BUF_INPUT, KD_BUF_OUTPUT, KD_BUF_PERSISTENT, KD_BUF_PER_MICROBATCH = 1, 2, 4, 8, 16
+KD_BUF_REPLICATED = 32
 # ops
 KD_OP_NONE, KD_OP_ADD_RMSNORM, KD_OP_GEMM, KD_OP_ROPE_APPEND, KD_OP_ATTENTION, KD_OP_SILU_MUL, \
     KD_OP_RESIDUAL_ADD, KD_OP_MOE_ROUTE, KD_OP_MOE_DISPATCH, KD_OP_GROUPED_GEMM, KD_OP_MOE_COMBINE, \
@@ -212,6 +213,7 @@ _PROTOS = {
     "kd_runtime_bind": (kd_status, [P, u32, u32, u32, P]),
     "kd_runtime_set_workspace": (kd_status, [P, u32, P, u64]),
     "kd_runtime_set_peer_workspace": (kd_status, [P, u32, P]),
+    "kd_runtime_set_peer_buffer": (kd_status, [P, u32, u32, u32, P]),
     "kd_runtime_set_mode": (kd_status, [P, u32]),
     "kd_runtime_set_graph": (kd_status, [P, i32]),
     "kd_runtime_prepare": (kd_status, [P]),

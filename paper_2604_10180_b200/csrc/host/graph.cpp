@@ -124,7 +124,9 @@ kd_status kd_graph_add_buffer(kd_graph* g, uint64_t bytes, uint32_t flags, uint3
   if (!g || !id) return fail(KD_ERR_INVALID_ARG, "kd_graph_add_buffer: NULL argument");
   if (g->finalized) return fail(KD_ERR_STATE, "kd_graph_add_buffer: graph already finalized");
   if (bytes == 0) return fail(KD_ERR_INVALID_ARG, "kd_graph_add_buffer: zero-size buffer");
-  if (flags & ~0x1Fu) return fail(KD_ERR_INVALID_ARG, "kd_graph_add_buffer: unknown flag bits");
+  if (flags & ~0x3Fu) return fail(KD_ERR_INVALID_ARG, "kd_graph_add_buffer: unknown flag bits");
+  if ((flags & KD_BUF_REPLICATED) && !(flags & KD_BUF_PERSISTENT))
+    return fail(KD_ERR_INVALID_ARG, "kd_graph_add_buffer: REPLICATED applies to PERSISTENT buffers");
   g->buffers.push_back({bytes, flags});
   *id = (uint32_t)g->buffers.size() - 1;
   return KD_OK;

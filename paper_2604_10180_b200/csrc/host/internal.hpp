@@ -73,6 +73,15 @@ bool op_count_geometry(const Kernel& k, u64* rows, u64* row_bytes);
 // acquires that input chunk by chunk inside the kernel; 0 = not chunk-aware
 // (the runtime then waits for the whole transfer before launching it)
 u64 op_consumer_unit(const Kernel& k, uint32_t ri, u64 row_bytes);
+// delta replication (KD_BUF_REPLICATED): bytes kernel k actually
+// writes into write span wi of a replicated buffer per step (RoPE/append: the
+// appended K or V slot of every row and kv head), else the span length
+u64 op_delta_bytes(const Kernel& k, uint32_t wi);
+// bytes an edge record charges the cost model and the transfer: the delta for
+// a replicated buffer (once per (src, buf): records after the first cost 0),
+// else the span length
+bool buf_replicated(const kd_graph& g, uint32_t buf);
+u64 delta_of(const kd_graph& g, uint32_t src, uint32_t buf);
 }  // namespace kd
 
 struct kd_plan {

@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <functional>
 #include <limits>
+#include <set>
+#include <tuple>
 
 #include "internal.hpp"
 
@@ -34,10 +36,19 @@ i64 edge_cost(const kd_machine& m, u64 bytes, uint32_t u, uint32_t v) {
   return (i64)(m.link_lat_ps[u * n + v] + ceil_div_u128((u128)bytes * kPs, m.link_Bps[u * n + v]));
 }
 
-// d_ij = Σ record lengths per (src, dst) (Table 2, R3)
+// d_ij = Σ record lengths per (src, dst) (Table 2, R3); records on a
+// REPLICATED buffer charge the producer's delta once per (src, dst, buffer)
 std::vector<std::pair<std::pair<uint32_t, uint32_t>, u64>> edge_pairs(const kd_graph& g) {
   std::map<std::pair<uint32_t, uint32_t>, u64> acc;
-  for (const auto& e : g.edges) acc[{e.src, e.dst}] += e.len;
+  std::set<std::tuple<uint32_t, uint32_t, uint32_t>> seen;
+  for (const auto& e : g.edges) {
+    if (buf_replicated(g, e.buf)) {
+      if (seen.insert({e.src, e.dst, e.buf}).second) acc[{e.src, e.dst}] += delta_of(g, e.src, e.buf);
+      else acc[{e.src, e.dst}] += 0;
+      continue;
+    }
+    acc[{e.src, e.dst}] += e.len;
+  }
   return {acc.begin(), acc.end()};
 }
 

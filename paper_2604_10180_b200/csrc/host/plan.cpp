@@ -122,6 +122,36 @@ u64 op_consumer_unit(const Kernel& k, uint32_t ri, u64 row_bytes) {
   return 0;
 }
 
+u64 op_delta_bytes(const Kernel& k, uint32_t wi) {
+  if (wi >= k.writes.size()) return 0;
+  if ((k.op == KD_OP_ROPE_APPEND || k.op == KD_OP_QKV_ROPE) && (wi == 1 || wi == 2)) {
+    uint32_t rows = 0, hkv = 0, hd = 0, dt = 0;
+    if (k.op == KD_OP_ROPE_APPEND) {
+      kd_attr_rope_append a;
+      if (!attrs_as(k, &a)) return k.writes[wi].len;
+      rows = a.rows, hkv = a.n_kv_heads, hd = a.head_dim, dt = a.dtype;
+    } else {
+      kd_attr_qkv_rope a;
+      if (!attrs_as(k, &a)) return k.writes[wi].len;
+      rows = a.rows, hkv = a.n_kv_heads, hd = a.head_dim, dt = a.dtype;
+    }
+    return std::min<u64>(k.writes[wi].len, (u64)rows * hkv * hd * (dt == KD_F32 ? 4 : 2));
+  }
+  return k.writes[wi].len;
+}
+
+bool buf_replicated(const kd_graph& g, uint32_t buf) {
+  return (g.buffers[buf].flags & (KD_BUF_REPLICATED | KD_BUF_PERSISTENT)) == (KD_BUF_REPLICATED | KD_BUF_PERSISTENT);
+}
+
+u64 delta_of(const kd_graph& g, uint32_t src, uint32_t buf) {
+  const Kernel& K = g.kernels[src];
+  u64 d = 0;
+  for (uint32_t wi = 0; wi < K.writes.size(); ++wi)
+    if (K.writes[wi].buf == buf) d += op_delta_bytes(K, wi);
+  return d;
+}
+
 static u64 gcd_u64(u64 a, u64 b) {
   while (b) {
     u64 t = a % b;
@@ -144,14 +174,15 @@ kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* 
   const uint32_t K = (uint32_t)g->kernels.size(), n = m->n_dev, N = n_micro;
   for (uint32_t k = 0; k < K; ++k)
     if (assign[k] < 0 || (uint32_t)assign[k] >= n) return fail(KD_ERR_INVALID_ARG, "kd_plan_create: bad assign");
-  // R6: every kernel touching a PERSISTENT buffer sits on one device
+  // R6: every kernel touching a PERSISTENT buffer sits on one device, unless
+  // the buffer is REPLICATED (one replica per device, deltas propagated)
   {
     std::map<uint32_t, int32_t> dev_of_buf;
     for (uint32_t k = 0; k < K; ++k) {
       const Kernel& Kk = g->kernels[k];
       for (const auto* v : {&Kk.reads, &Kk.writes})
         for (const auto& s : *v)
-          if (g->buffers[s.buf].flags & KD_BUF_PERSISTENT) {
+          if ((g->buffers[s.buf].flags & KD_BUF_PERSISTENT) && !buf_replicated(*g, s.buf)) {
             auto it = dev_of_buf.find(s.buf);
             if (it == dev_of_buf.end())
               dev_of_buf[s.buf] = assign[k];
@@ -168,17 +199,29 @@ kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* 
   p->n_chunks = n_chunks;
   p->assign.assign(assign, assign + K);
 
-  // predecessors and transfers (producer k, remote device d) = union of spans (R3)
+  // predecessors and transfers (producer k, remote device d) = union of spans
+  // (R3) + the deltas of replicated buffers read there (once per buffer)
   std::vector<std::vector<uint32_t>> preds(K);
   std::map<std::pair<uint32_t, uint32_t>, std::vector<Span>> xspans;
+  std::map<std::pair<uint32_t, uint32_t>, std::set<uint32_t>> xrepl;  // (k, dev) -> replicated bufs
   for (const auto& e : g->edges) {
     auto& pv = preds[e.dst];
     if (std::find(pv.begin(), pv.end(), e.src) == pv.end()) pv.push_back(e.src);
     uint32_t gd = assign[e.dst];
-    if (gd != (uint32_t)assign[e.src]) xspans[{e.src, gd}].push_back({e.buf, e.offset, e.len});
+    if (gd == (uint32_t)assign[e.src]) continue;
+    if (buf_replicated(*g, e.buf)) {
+      xrepl[{e.src, gd}].insert(e.buf);
+      xspans[{e.src, gd}];  // the transfer exists even without a primary-output span
+    } else {
+      xspans[{e.src, gd}].push_back({e.buf, e.offset, e.len});
+    }
   }
   std::vector<std::vector<std::pair<uint32_t, u64>>> out_x(K);  // k -> [(dev, bytes)] ascending dev
-  for (auto& kv : xspans) out_x[kv.first.first].push_back({kv.first.second, union_bytes(kv.second)});
+  for (auto& kv : xspans) {
+    u64 b = union_bytes(kv.second);
+    for (uint32_t rb : xrepl[kv.first]) b += delta_of(*g, kv.first.first, rb);
+    out_x[kv.first.first].push_back({kv.first.second, b});
+  }
 
   std::vector<i64> t(K);
   for (uint32_t k = 0; k < K; ++k) t[k] = kernel_time(*g, *m, k, assign[k]);
@@ -306,7 +349,10 @@ kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* 
       auto& X = p->xchunks[t];
       const u64 len = P.writes.empty() ? 0 : P.writes[0].len;
       u64 rows = 0, rb = 0;
-      if (op_count_geometry(P, &rows, &rb) && rows * rb == len && rb > 0) {
+      bool mirrors = false;  // a producer mirroring replicated-buffer deltas releases per CTA
+      for (const auto& w : P.writes)
+        if (buf_replicated(*g, w.buf)) mirrors = true;
+      if (!mirrors && op_count_geometry(P, &rows, &rb) && rows * rb == len && rb > 0) {
         X.count = true;
         X.rows = rows;
         X.row_bytes = rb;

@@ -46,6 +46,10 @@ struct Epi {
   unsigned long long* flag[kMaxPeers] = {};     // [max(nch,1)] in the peer
   unsigned long long* started[kMaxPeers] = {};  // loopback residency (nullable)
   unsigned long long* logt[kMaxPeers] = {};     // LOG: per-chunk records (nullable)
+  // delta replication (KD_BUF_REPLICATED): the peer's replica base of this
+  // kernel's j-th replicated output; a write at byte offset o of the local
+  // replica is mirrored to mir[p][j] + o (nullable)
+  void* mir[kMaxPeers][2] = {};
 };
 
 // ------------------------------------------------------------------ memory model

@@ -356,6 +356,13 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
     }
     *reinterpret_cast<uint4*>(dst + i0) = lo;
     *reinterpret_cast<uint4*>(dst + half + i0) = hi;
+    if (!is_q)  // delta replication of the K cache: the same slot in every peer replica
+      for (int p = 0; p < epi.n; ++p)
+        if (epi.mir[p][0]) {
+          __nv_bfloat16* pd = (__nv_bfloat16*)epi.mir[p][0] + (dst - kc);
+          *reinterpret_cast<uint4*>(pd + i0) = lo;
+          *reinterpret_cast<uint4*>(pd + half + i0) = hi;
+        }
     if (is_q) {
       for (int p = 0; p < epi.n; ++p) {
         __nv_bfloat16* pd = (__nv_bfloat16*)epi.dst[p] + qoff;
@@ -374,8 +381,12 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
     const int32_t pg = bt[(size_t)b * pps + slot / page];
     const __nv_bfloat16* x = qkv + (size_t)b * (Hq + 2 * Hkv) * D + (size_t)g * (G + 2) * D + (size_t)(G + 1) * D;
     __nv_bfloat16* dst = vc + (((size_t)pg * Hkv + g) * page + slot % page) * D;
-    for (int c8 = t16 * 8; c8 < D; c8 += 128)
-      *reinterpret_cast<uint4*>(dst + c8) = *reinterpret_cast<const uint4*>(x + c8);
+    for (int c8 = t16 * 8; c8 < D; c8 += 128) {
+      const uint4 v = *reinterpret_cast<const uint4*>(x + c8);
+      *reinterpret_cast<uint4*>(dst + c8) = v;
+      for (int p = 0; p < epi.n; ++p)  // delta replication of the V cache
+        if (epi.mir[p][1]) *reinterpret_cast<uint4*>((__nv_bfloat16*)epi.mir[p][1] + (dst - vc) + c8) = v;
+    }
   }
   epi_signal_counts(epi, s_cnt);
 }

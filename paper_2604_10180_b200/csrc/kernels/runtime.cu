@@ -51,6 +51,7 @@ struct kd_runtime {
   std::vector<kd::DevState> devs;              // local devices
   std::vector<uint8_t*> ws_of;                 // workspace base per logical device (local or peer-mapped)
   std::map<std::tuple<uint32_t, uint32_t, uint32_t>, void*> bind;  // (buf, micro, dev)
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, void*> peer_bind;  // replicas of remote devices (IPC-mapped)
   uint32_t mode = KD_MODE_DISAGG;
   bool use_graph = true;
   bool prepared = false;
@@ -334,6 +335,17 @@ kd_status kd_runtime_set_peer_workspace(kd_runtime* rt, uint32_t dev, void* mapp
   return KD_OK;
 }
 
+kd_status kd_runtime_set_peer_buffer(kd_runtime* rt, uint32_t buf, uint32_t micro, uint32_t dev, void* mapped_ptr) {
+  if (!rt || !mapped_ptr || dev >= rt->plan->n_dev || buf >= rt->plan->g->buffers.size())
+    return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_peer_buffer: bad argument");
+  if (!buf_replicated(*rt->plan->g, buf)) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_peer_buffer: not a REPLICATED buffer");
+  for (auto& d : rt->devs)
+    if (d.logical == dev) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_peer_buffer: device is local");
+  rt->peer_bind[{buf, micro, dev}] = mapped_ptr;
+  rt->prepared = false;
+  return KD_OK;
+}
+
 kd_status kd_runtime_set_mode(kd_runtime* rt, uint32_t mode) {
   if (!rt || mode > KD_MODE_LOG) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_mode: bad argument");
   // (LOG = DISAGG plus per-chunk %globaltimer records; its epochs carry releases)
@@ -489,11 +501,12 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
               hit = true;
           if (!hit) continue;
           const Kernel& S = g->kernels[src];
-          for (const auto& e2 : g->edges)
-            if (e2.dst == k && e2.src == src && e2.buf == sp.buf &&
-                (S.writes.empty() || S.writes[0].buf != sp.buf || e2.offset < S.writes[0].off ||
-                 e2.offset + e2.len > S.writes[0].off + S.writes[0].len))
-              return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: a cut edge must read the producer's primary output");
+          if (!buf_replicated(*g, sp.buf))  // (replicated state arrives as the producer's mirrored deltas)
+            for (const auto& e2 : g->edges)
+              if (e2.dst == k && e2.src == src && e2.buf == sp.buf &&
+                  (S.writes.empty() || S.writes[0].buf != sp.buf || e2.offset < S.writes[0].off ||
+                   e2.offset + e2.len > S.writes[0].off + S.writes[0].len))
+                return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: a cut edge must read the producer's primary output");
           srcs_here.push_back(src);
         }
         if (srcs_here.empty()) {
@@ -503,7 +516,11 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
           continue;
         }
         const bool ext = g->buffers[sp.buf].flags & EXT;
-        if (ext) {  // external buffer: one remote producer, its private landing slot
+        if (buf_replicated(*g, sp.buf)) {  // this device's own replica (deltas mirrored into it)
+          void* ptr = local_ptr(sp.buf, i, sp.off);
+          if (!ptr) return fail(KD_ERR_STATE, "kd_runtime_prepare: replica of buffer " + std::to_string(sp.buf) + " not bound on device " + std::to_string(d.logical));
+          l.rd.push_back(ptr);
+        } else if (ext) {  // external buffer: one remote producer, its private landing slot
           if (srcs_here.size() != 1)
             return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: an external buffer read span with several remote producers");
           const Kernel& S = g->kernels[srcs_here[0]];
@@ -599,6 +616,23 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
         ep.flag[ep.n] = (unsigned long long*)(rt->ws_of[v] + land.second);
         ep.started[ep.n] = (X.count && loopback(v)) ? (unsigned long long*)(rt->ws_of[v] + land.second) + nch : nullptr;
         ep.logt[ep.n] = log_on ? (unsigned long long*)(rt->ws_of[v] + Lv.xlog.at(it->second)) : nullptr;
+        // delta replication: the peer's replicas of this kernel's replicated outputs
+        int j = 0;
+        for (const auto& w : K.writes) {
+          if (!buf_replicated(*g, w.buf)) continue;
+          if (K.op != KD_OP_ROPE_APPEND || j >= 2)
+            return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: only RoPE/append mirrors replicated (KV) writes");
+          const uint32_t inst = (g->buffers[w.buf].flags & KD_BUF_PER_MICROBATCH) ? i : 0;
+          void* base = nullptr;
+          auto bi = rt->bind.find({w.buf, inst, v});
+          if (bi != rt->bind.end()) base = bi->second;
+          auto pi = rt->peer_bind.find({w.buf, inst, v});
+          if (pi != rt->peer_bind.end()) base = pi->second;
+          if (P->needs_bind[w.buf][v] && !base)
+            return fail(KD_ERR_STATE, "kd_runtime_prepare: replica of buffer " + std::to_string(w.buf) + " on device " +
+                                          std::to_string(v) + " unknown (kd_runtime_set_peer_buffer)");
+          ep.mir[ep.n][j++] = base ? (uint8_t*)base + w.off : nullptr;
+        }
         ++ep.n;
       }
       l.ctx.scratch = d.ws + L.scratch_off;

@@ -36,8 +36,8 @@ from . import _kd as K
 from .api import Graph, Machine, Plan, Runtime, place
 
 (T_RESID, T_QKV, T_ATTN, T_O, T_GU, T_SILU, T_DOWN, T_ROUTE, T_DISPATCH, T_ESILU, T_COMBINE,
- T_INPROJ, T_SSM, T_OUTPROJ) = range(14)
-MEMORY_ROLE = {T_RESID, T_ATTN, T_SILU, T_ROUTE, T_DISPATCH, T_COMBINE, T_SSM}  # HBM-bound non-GEMM kernels
+ T_INPROJ, T_SSM, T_OUTPROJ, T_ROPE) = range(15)
+MEMORY_ROLE = {T_RESID, T_ATTN, T_SILU, T_ROUTE, T_DISPATCH, T_COMBINE, T_SSM, T_ROPE}  # HBM-bound non-GEMM kernels
 GEMM_ROLE = {T_QKV, T_O, T_GU, T_DOWN, T_ESILU, T_INPROJ, T_OUTPROJ}           # GEMMs (+ the experts' SiLU)
 
 
@@ -79,7 +79,7 @@ class DecoderGraph:
     """Declares the decoder kernel graph for one micro-batch of cfg.m rows."""
 
     def __init__(self, cfg, act: int = K.KD_BF16, fuse_silu: bool = False, fuse_rope: bool = False,
-                 fuse_norm: bool = False):
+                 fuse_norm: bool = False, replicate_kv: bool = False):
         """act: KD_BF16 (throughput path) or KD_F32 (the 1e-5 parity path,
         R13: fp32 weights, activations and KV cache; dense attention layers).
         fuse_silu: declare gate_up and SiLU·mul as ONE kernel (KD_OP_GEMM_SILU,
@@ -93,7 +93,11 @@ class DecoderGraph:
         RMSNorm (norm2), and each dense down GEMM with the next layer's norm1,
         as ONE kernel (KD_OP_GEMM_RMSNORM) — for co-located placements; the o
         and d activations then never exist (except the last layer's d).
-        fuse_norm="o" fuses only O + norm2 (A/B: measured between all and none)."""
+        fuse_norm="o" fuses only O + norm2 (A/B: measured between all and none).
+        replicate_kv: the KV caches are KD_BUF_REPLICATED (P:465-466 delta
+        replication) and RoPE/append gets its own template (T_ROPE), so it can
+        run on another device than attention: the appended slots are mirrored
+        into the attention device's replica."""
         if act not in (K.KD_BF16, K.KD_F32):
             raise ValueError("act must be KD_BF16 or KD_F32")
         if act == K.KD_F32 and (cfg.n_experts or cfg.attn_every):
@@ -180,8 +184,9 @@ class DecoderGraph:
                 buf(f"w_d.{l}", (H, F), adt, W)
             buf(f"g1.{l}", (H,), adt, W)
             buf(f"g2.{l}", (H,), adt, W)
-            buf(f"kc.{l}", (m * pps, Hkv, cfg.page, D), adt, PERS | PM)
-            buf(f"vc.{l}", (m * pps, Hkv, cfg.page, D), adt, PERS | PM)
+            REP = K.KD_BUF_REPLICATED if replicate_kv else 0
+            buf(f"kc.{l}", (m * pps, Hkv, cfg.page, D), adt, PERS | PM | REP)
+            buf(f"vc.{l}", (m * pps, Hkv, cfg.page, D), adt, PERS | PM | REP)
             acts = [("h1", (m, H))] + ([] if fuse_rope else [("qkv", (m, cfg.qkv_dim))]) + [
                 ("q", (m, Hq * D)), ("attn", (m, Hq * D))] + ([] if fuse_norm else [("o", (m, H))]) + [
                 ("h2", (m, H))] + ([] if fused_down(l) else [("d", (m, H))])
@@ -232,7 +237,8 @@ class DecoderGraph:
             else:
                 add("qkv", l, T_QKV, K.KD_OP_GEMM, [f"h1.{l}", f"w_qkv.{l}"], [f"qkv.{l}"],
                     K.kd_attr_gemm(m, cfg.qkv_dim, H, act), 2 * m * cfg.qkv_dim * H)
-                add("rope", l, T_ATTN, K.KD_OP_ROPE_APPEND, [f"qkv.{l}", "bt", "sl"], [f"q.{l}", f"kc.{l}", f"vc.{l}"],
+                add("rope", l, T_ROPE if replicate_kv else T_ATTN, K.KD_OP_ROPE_APPEND, [f"qkv.{l}", "bt", "sl"],
+                    [f"q.{l}", f"kc.{l}", f"vc.{l}"],
                     K.kd_attr_rope_append(m, Hq, Hkv, D, cfg.page, pps, act, 0, float(cfg.rope_theta)))
             add("attn", l, T_ATTN, K.KD_OP_ATTENTION, [f"q.{l}", f"kc.{l}", f"vc.{l}", "bt", "sl"], [f"attn.{l}"],
                 K.kd_attr_attention(m, Hq, Hkv, D, cfg.page, pps, act, 0), 4 * m * Hq * cfg.context * D)

@@ -539,3 +539,34 @@ def test_random_placements_chunked_bitwise(mod, seed):
     rt.sync()
     rt.rt.check()
     assert np.array_equal(mono.residual(), rt.residual()), (assign, nch)
+
+
+# ------------------------------------------------------------------ f2: delta replication
+@pytest.mark.parametrize("n_micro", [1, 2])
+def test_delta_replicated_kv_rope_apart_from_attention(mod, n_micro):
+    """KD_BUF_REPLICATED KV caches: RoPE/append on device 0 writes the new
+    token's K/V slot into its replica and mirrors exactly those bytes into the
+    attention device's replica (fused peer stores, released with its q
+    transfer); attention on device 2 reads its own replica. Bitwise equal to
+    monolithic, and both replicas end identical to the monolithic cache."""
+    DEC, K = mod
+    cfg = TINY.with_(n_micro=n_micro)
+    inp = synth.make_decoder_inputs(cfg)
+    mono = run(DEC, cfg, inp, lambda dg: [0] * dg.g.num_kernels, 1, steps=2)
+    dg = DEC.DecoderGraph(cfg, replicate_kv=True)
+    assign = [{DEC.T_ATTN: 2}.get(k.template, 0 if k.template in DEC.MEMORY_ROLE else 1) for k in dg.kernels]
+    assert len({assign[i] for i, k in enumerate(dg.kernels) if k.name in ("rope", "attn")}) == 2
+    rt = DEC.DecoderRuntime(dg, assign, 3, [0, 0, 0], inputs=inp)
+    for _ in range(2):
+        rt.step()
+    rt.sync()
+    rt.rt.check()
+    assert np.array_equal(mono.residual(), rt.residual())
+    torch = __import__("torch")
+    for l in range(cfg.n_layers):
+        for i in range(n_micro):
+            ref = mono.tensors[(f"kc.{l}", i, 0)].view(torch.int16).cpu().numpy()
+            for d in (0, 2):
+                assert np.array_equal(rt.tensors[(f"kc.{l}", i, d)].view(torch.int16).cpu().numpy(), ref), (l, i, d)
+                assert np.array_equal(rt.tensors[(f"vc.{l}", i, d)].view(torch.int16).cpu().numpy(),
+                                      mono.tensors[(f"vc.{l}", i, 0)].view(torch.int16).cpu().numpy())
