@@ -368,7 +368,9 @@ typedef struct {
   uint32_t chunk;       /* ascending within the transfer */
   uint32_t count_mode;  /* 1: byte-count release per chunk; 0: per-CTA release, one chunk */
   uint32_t pad_;
-  uint64_t rows, row_bytes, unit;
+  uint64_t row0, rows;  /* rows [row0, row0 + rows) of the output travel (a GEMM output scattered
+                           to memory shards carries only the rows that device reads, R24) */
+  uint64_t row_bytes, unit;
   uint64_t begin, end;  /* byte range within every row */
 } kd_chunk;
 kd_status kd_plan_chunks(const kd_plan* p, kd_chunk* out, uint32_t cap, uint32_t* n);

@@ -196,13 +196,15 @@ def consumer_unit(op, a, ri, row_bytes):
     return 0
 
 
-def chunk_table(kernels, edges, assign, transfers, n_chunks):
+def chunk_table(kernels, edges, assign, transfers, n_chunks, replicated=frozenset()):
     """Chunk table of a plan: for every transfer (micro, producer, dst, ...) in
     plan order, (count_mode, rows, row_bytes, unit, [(begin, end), ...]).
     kernels[k] = (op_name, attrs_dict, reads[(buf, off, len)], writes[...]).
     The unit of a producer is the lcm of the units of its remote chunk-aware
-    consumers — reads of exactly its primary output, every byte of which it
-    wrote — capped at the row; chunks follow `chunks` (R10)."""
+    consumers — reads of whole rows of its primary output, every byte of which
+    it wrote — capped at the row; chunks follow `chunks` (R10). A GEMM output
+    scattered to a device carries only the rows read there (R24); producers
+    that mirror replicated buffers release per CTA (R28)."""
     from math import gcd
     srcs: Dict[Tuple[int, int], set] = {}
     for s, d, buf, _off, _ln in edges:
@@ -221,23 +223,37 @@ def chunk_table(kernels, edges, assign, transfers, n_chunks):
             if geo is None or not pw:
                 continue
             rows, rb = geo
-            if (buf, off, ln) != tuple(pw[0]) or rows * rb != pw[0][2]:
+            wb, wo, wl = pw[0]
+            if buf != wb or off < wo or off + ln > wo + wl or rows * rb != wl or (off - wo) % rb or ln % rb:
                 continue
             u = consumer_unit(op, a, ri, rb)
             if u:
                 cur = unit_of.get(src, 0)
                 unit_of[src] = u if cur == 0 else cur // gcd(cur, u) * u
     out = []
-    for (_i, prod, _dst, *_rest) in transfers:
+    for (_i, prod, dst, *_rest) in transfers:
         pop, pa, _pr, pw = kernels[prod]
         ln = pw[0][2] if pw else 0
         geo = count_geometry(pop, pa)
-        if geo is not None and geo[0] * geo[1] == ln and geo[1] > 0:
+        mirrors = any(w[0] in replicated for w in pw)
+        if geo is not None and not mirrors and geo[0] * geo[1] == ln and geo[1] > 0:
             rows, rb = geo
             u = unit_of.get(prod, rb)
             u = rb if u > rb else u
-            out.append((1, rows, rb, u, chunks(rb, u, n_chunks)))
+            row0, nrows = 0, rows
+            if pop in ("GEMM", "GEMM_SILU", "GEMM_RMSNORM"):
+                # scatter: only the rows the destination device reads (one
+                # contiguous range of the read spans, widened to whole rows)
+                w0b, w0o = pw[0][0], pw[0][1]
+                got = _union([(b, o, l) for s_, d_, b, o, l in edges
+                              if s_ == prod and assign[d_] == dst and b == w0b]).get(w0b, [])
+                if got:
+                    lo, hi = got[0][0], got[-1][1]
+                    if sum(e - a for a, e in got) == hi - lo:
+                        row0 = (lo - w0o) // rb
+                        nrows = -(-(hi - w0o) // rb) - row0
+            out.append((1, row0, nrows, rb, u, chunks(rb, u, n_chunks)))
         else:
             L = max(ln, 1)
-            out.append((0, 1, L, L, [(0, L)]))
+            out.append((0, 0, 1, L, L, [(0, L)]))
     return out

@@ -153,8 +153,8 @@ class kd_transfer(C.Structure):
 
 class kd_chunk(C.Structure):
     _fields_ = [("transfer", C.c_uint32), ("chunk", C.c_uint32), ("count_mode", C.c_uint32), ("pad_", C.c_uint32),
-                ("rows", C.c_uint64), ("row_bytes", C.c_uint64), ("unit", C.c_uint64), ("begin", C.c_uint64),
-                ("end", C.c_uint64)]
+                ("row0", C.c_uint64), ("rows", C.c_uint64), ("row_bytes", C.c_uint64), ("unit", C.c_uint64),
+                ("begin", C.c_uint64), ("end", C.c_uint64)]
 
 
 KD_STATS_MAX_DEV = 8

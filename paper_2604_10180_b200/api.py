@@ -189,12 +189,13 @@ class Plan:
         self.n_chunks = n_chunks
 
     def chunks(self):
-        """Chunk table: [(transfer, chunk, count_mode, rows, row_bytes, unit, begin, end)]."""
+        """Chunk table: [(transfer, chunk, count_mode, row0, rows, row_bytes, unit, begin, end)]."""
         n = C.c_uint32()
         K.kd_plan_chunks(self.h, None, 0, C.byref(n))
         arr = (K.kd_chunk * max(1, n.value))()
         check(K.kd_plan_chunks(self.h, arr, n.value, C.byref(n)), "kd_plan_chunks")
-        return [(c.transfer, c.chunk, c.count_mode, c.rows, c.row_bytes, c.unit, c.begin, c.end) for c in arr[:n.value]]
+        return [(c.transfer, c.chunk, c.count_mode, c.row0, c.rows, c.row_bytes, c.unit, c.begin, c.end)
+                for c in arr[:n.value]]
 
     def __del__(self):
         if getattr(self, "h", None):

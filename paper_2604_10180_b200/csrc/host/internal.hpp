@@ -77,6 +77,9 @@ u64 op_consumer_unit(const Kernel& k, uint32_t ri, u64 row_bytes);
 // writes into write span wi of a replicated buffer per step (RoPE/append: the
 // appended K or V slot of every row and kv head), else the span length
 u64 op_delta_bytes(const Kernel& k, uint32_t wi);
+// producers whose peer stores can be filtered to the rows a device reads
+// (the GEMM epilogues): a scatter transfer then carries only those rows
+bool op_row_filter(const Kernel& k);
 // bytes an edge record charges the cost model and the transfer: the delta for
 // a replicated buffer (once per (src, buf): records after the first cost 0),
 // else the span length
@@ -95,6 +98,7 @@ struct kd_plan {
   // chunk-aware consumers' streamable axis (unit = lcm of their units)
   struct XChunks {
     bool count = false;       // COUNT release (bytes per chunk) vs CTA release (1 chunk)
+    kd::u64 row0 = 0;         // first row the transfer carries (row-filtered scatter, R24)
     kd::u64 rows = 1, row_bytes = 0, unit = 0;
     std::vector<std::pair<kd::u64, kd::u64>> ch;
   };

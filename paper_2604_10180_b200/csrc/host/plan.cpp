@@ -140,6 +140,10 @@ u64 op_delta_bytes(const Kernel& k, uint32_t wi) {
   return k.writes[wi].len;
 }
 
+bool op_row_filter(const Kernel& k) {
+  return k.op == KD_OP_GEMM || k.op == KD_OP_GEMM_SILU || k.op == KD_OP_GEMM_RMSNORM;
+}
+
 bool buf_replicated(const kd_graph& g, uint32_t buf) {
   return (g.buffers[buf].flags & (KD_BUF_REPLICATED | KD_BUF_PERSISTENT)) == (KD_BUF_REPLICATED | KD_BUF_PERSISTENT);
 }
@@ -335,7 +339,11 @@ kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* 
         u64 rows = 0, rb = 0;
         if (P.writes.empty() || !op_count_geometry(P, &rows, &rb)) continue;
         const Span& w0 = P.writes[0];
-        if (sp.buf != w0.buf || sp.off != w0.off || sp.len != w0.len || rows * rb != w0.len) continue;
+        // the consumer reads whole rows of the producer's output (all of them,
+        // or its row span of a scattered GEMM output)
+        if (sp.buf != w0.buf || sp.off < w0.off || sp.off + sp.len > w0.off + w0.len || rows * rb != w0.len ||
+            (sp.off - w0.off) % rb || sp.len % rb)
+          continue;
         const u64 u = op_consumer_unit(C, ri, rb);
         if (!u) continue;
         u64& cur = unit_of[src];
@@ -354,8 +362,28 @@ kd_status kd_plan_create(const kd_graph* g, const kd_machine* m, const int32_t* 
         if (buf_replicated(*g, w.buf)) mirrors = true;
       if (!mirrors && op_count_geometry(P, &rows, &rb) && rows * rb == len && rb > 0) {
         X.count = true;
+        X.row0 = 0;
         X.rows = rows;
         X.row_bytes = rb;
+        if (op_row_filter(P)) {  // only the rows the destination's consumers read (one contiguous range)
+          const Span& w0 = P.writes[0];
+          u64 lo = ~0ull, hi = 0, covered = 0;
+          std::vector<Span> sp;
+          for (const auto& e : g->edges)
+            if (e.src == tr.producer && (uint32_t)assign[e.dst] == tr.dst_dev && e.buf == w0.buf)
+              sp.push_back({e.buf, e.offset, e.len});
+          for (const auto& kv : span_union(sp))
+            for (const auto& iv : kv.second) {
+              lo = std::min(lo, iv.s);
+              hi = std::max(hi, iv.e);
+              covered += iv.e - iv.s;
+            }
+          if (hi > lo && covered == hi - lo) {  // contiguous: widen to whole rows
+            const u64 r0 = (lo - w0.off) / rb, r1 = ceil_div(hi - w0.off, rb);
+            X.row0 = r0;
+            X.rows = r1 - r0;
+          }
+        }
         auto it = unit_of.find(tr.producer);
         X.unit = (it == unit_of.end() || it->second > rb) ? rb : it->second;
         const u64 U = ceil_div(rb, X.unit), q = ceil_div(U, n_chunks) * X.unit;
@@ -505,6 +533,7 @@ kd_status kd_plan_chunks(const kd_plan* p, kd_chunk* out, uint32_t cap, uint32_t
       o.chunk = c;
       o.count_mode = X.count ? 1u : 0u;
       o.pad_ = 0;
+      o.row0 = X.row0;
       o.rows = X.rows;
       o.row_bytes = X.row_bytes;
       o.unit = X.unit;

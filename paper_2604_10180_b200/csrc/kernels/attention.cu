@@ -528,7 +528,8 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
         __syncwarp();
         if (lane == 0) {
           if (P.epi.nch)
-            epi_release_range(P.epi, (uint32_t)(g * G * D) * 2u, (uint32_t)((g + 1) * G * D) * 2u, 1u);
+            epi_release_range(P.epi, (uint32_t)(g * G * D) * 2u, (uint32_t)((g + 1) * G * D) * 2u, (uint32_t)b,
+                              (uint32_t)b + 1u);
           else
             epi_release_cta(P.epi);
         }

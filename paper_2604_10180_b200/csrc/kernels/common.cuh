@@ -50,7 +50,19 @@ struct Epi {
   // kernel's j-th replicated output; a write at byte offset o of the local
   // replica is mirrored to mir[p][j] + o (nullable)
   void* mir[kMaxPeers][2] = {};
+  // row filter (scatter of a GEMM output to memory shards, R24): peer p
+  // receives rows [r0, r0 + rn) only; rn == 0: every row
+  uint32_t r0[kMaxPeers] = {}, rn[kMaxPeers] = {};
 };
+__device__ __forceinline__ bool epi_row_in(const Epi& e, int p, uint32_t row) {
+  return e.rn[p] == 0 || row - e.r0[p] < e.rn[p];
+}
+// rows of [row_begin, row_end) that peer p receives
+__device__ __forceinline__ uint32_t epi_rows_for(const Epi& e, int p, uint32_t row_begin, uint32_t row_end) {
+  if (e.rn[p] == 0) return row_end - row_begin;
+  const uint32_t a = max(row_begin, e.r0[p]), b = min(row_end, e.r0[p] + e.rn[p]);
+  return b > a ? b - a : 0u;
+}
 
 // ------------------------------------------------------------------ memory model
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
@@ -91,15 +103,18 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
 constexpr int kLogWords = 4;
 
 // COUNT mode: add rows·|[lo, hi) ∩ chunk c| bytes to every chunk the byte range
-// [lo, hi) of a row touches (a caller that stored those bytes of `rows` rows,
-// after the stores are ordered before this thread: fence / bar.sync)
-__device__ __forceinline__ void epi_release_range(const Epi& e, uint32_t lo, uint32_t hi, uint32_t rows) {
+// [lo, hi) of a row touches (a caller that stored those bytes of rows
+// [row_begin, row_end) — each peer counts the rows it receives — after the
+// stores are ordered before this thread: fence / bar.sync)
+__device__ __forceinline__ void epi_release_range(const Epi& e, uint32_t lo, uint32_t hi, uint32_t row_begin,
+                                                  uint32_t row_end) {
   for (int c = 0; c < e.nch; ++c) {
     const uint32_t a = max(lo, e.cb[c]), b = min(hi, e.cb[c + 1]);
     if (a >= b) continue;
-    const unsigned long long add = (unsigned long long)(b - a) * rows;
     for (int p = 0; p < e.n; ++p) {
-      red_release_sys_add64(e.flag[p] + c, add);
+      const uint32_t rows = epi_rows_for(e, p, row_begin, row_end);
+      if (!rows) continue;
+      red_release_sys_add64(e.flag[p] + c, (unsigned long long)(b - a) * rows);
       if (e.logt[p]) atomicMax(e.logt[p] + c * kLogWords + 3, gtimer_ns());
     }
   }
@@ -123,13 +138,14 @@ __device__ __forceinline__ void epi_started(const Epi& e) {
 // publish this CTA's peer stores: call by ALL threads of the CTA after their
 // stores. CTA mode: one increment; COUNT mode: the CTA declares the byte range
 // [lo, hi) of `rows` rows it wrote (nch == 0 ignores them).
-__device__ __forceinline__ void epi_signal(const Epi& epi, uint32_t lo = 0, uint32_t hi = 0, uint32_t rows = 0) {
+__device__ __forceinline__ void epi_signal(const Epi& epi, uint32_t lo = 0, uint32_t hi = 0, uint32_t row_begin = 0,
+                                           uint32_t row_end = 0) {
   if (epi.n == 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     fence_acq_rel_sys();
     if (epi.nch)
-      epi_release_range(epi, lo, hi, rows);
+      epi_release_range(epi, lo, hi, row_begin, row_end);
     else
       epi_release_cta(epi);
   }
@@ -138,7 +154,8 @@ __device__ __forceinline__ void epi_signal(const Epi& epi, uint32_t lo = 0, uint
 // COUNT-mode release of per-CTA byte tallies (kernels whose stores are not one
 // rectangle per CTA): s_cnt[c] = bytes this CTA stored into chunk c (of every
 // row together). Call by ALL threads after the stores.
-__device__ __forceinline__ void epi_signal_counts(const Epi& epi, const unsigned* s_cnt) {
+// per_peer: s_cnt is [kMaxPeers][kMaxChunks] (row-filtered producers tally per peer)
+__device__ __forceinline__ void epi_signal_counts(const Epi& epi, const unsigned* s_cnt, bool per_peer = false) {
   if (epi.n == 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -148,11 +165,12 @@ __device__ __forceinline__ void epi_signal_counts(const Epi& epi, const unsigned
       return;
     }
     for (int c = 0; c < epi.nch; ++c)
-      if (s_cnt[c])
-        for (int p = 0; p < epi.n; ++p) {
-          red_release_sys_add64(epi.flag[p] + c, (unsigned long long)s_cnt[c]);
-          if (epi.logt[p]) atomicMax(epi.logt[p] + c * kLogWords + 3, gtimer_ns());
-        }
+      for (int p = 0; p < epi.n; ++p) {
+        const unsigned v = s_cnt[(per_peer ? p * kMaxChunks : 0) + c];
+        if (!v) continue;
+        red_release_sys_add64(epi.flag[p] + c, (unsigned long long)v);
+        if (epi.logt[p]) atomicMax(epi.logt[p] + c * kLogWords + 3, gtimer_ns());
+      }
   }
 }
 __device__ __forceinline__ int epi_chunk_of(const Epi& epi, uint32_t byte_in_row) {

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(float* __rest
       for (int p = 0; p < epi.n; ++p) reinterpret_cast<uint4*>(epi.dst[p])[e] = o;
     }
   }
-  epi_signal(epi, 0u, (uint32_t)H * 2u, 1u);  // COUNT: this CTA wrote the whole row
+  epi_signal(epi, 0u, (uint32_t)H * 2u, (uint32_t)row, (uint32_t)row + 1u);  // COUNT: this CTA wrote the whole row
 }
 
 static DeltasF as_f32(const Deltas& d) {

@@ -104,7 +104,7 @@ __device__ __forceinline__ void store_silu4(const Args& A, size_t yo, const floa
   o.x = silu2(g.x, g.y, u.x, u.y);
   o.y = silu2(g.z, g.w, u.z, u.w);
   *reinterpret_cast<uint2*>(A.Y + yo) = o;
-  for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+  for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)(yo / (A.N / 2)))) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
 }
 
 // kX: the round-2 handoff protocol (chunk byte counts, in-kernel acquires,
@@ -132,20 +132,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = (uint32_t*)(fixbar + 1);
   volatile unsigned* s_flag = (volatile unsigned*)(tmem_slot + 1);
   __nv_bfloat16* ystage = (__nv_bfloat16*)(fixbar + 2);  // 2 x [16][128] bf16 epilogue transpose
-  unsigned* s_cnt = (unsigned*)(ystage + 2 * kChunk * kBM);  // COUNT-mode bytes stored per chunk (this CTA)
+  unsigned* s_cnt = (unsigned*)(ystage + 2 * kChunk * kBM);  // COUNT-mode bytes per (peer, chunk) (this CTA)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) KD_TRACE(0);
   pdl_launch_dependents();
   if constexpr (kX) {
     epi_started(A.epi);
-    if (threadIdx.x < kMaxChunks) s_cnt[threadIdx.x] = 0u;  // (ordered by the __syncthreads below)
+    if (threadIdx.x < kMaxPeers * kMaxChunks) s_cnt[threadIdx.x] = 0u;  // (ordered by the __syncthreads below)
   }
   // COUNT mode: tally the bytes this CTA streams into each chunk of the output row
   const int row_elems = A.silu ? A.N / 2 : A.N;
-  auto count = [&](size_t yo, unsigned bytes) {
+  auto count = [&](size_t yo, unsigned bytes) {  // per peer: only the rows it receives
     if constexpr (kX) {
-      if (A.epi.nch) atomicAdd(&s_cnt[epi_chunk_of(A.epi, (uint32_t)(yo % (size_t)row_elems) * 2u)], bytes);
+      if (A.epi.nch) {
+        const int c = epi_chunk_of(A.epi, (uint32_t)(yo % (size_t)row_elems) * 2u);
+        const uint32_t row = (uint32_t)(yo / (size_t)row_elems);
+        for (int p = 0; p < A.epi.n; ++p)
+          if (epi_row_in(A.epi, p, row)) atomicAdd(&s_cnt[p * kMaxChunks + c], bytes);
+      }
     }
   };
   const long long U = A.units, G = gridDim.x, c = blockIdx.x;
@@ -418,13 +423,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const size_t yo = (size_t)(y0 + j) * A.N + nn;
                 if (nn + 4 <= A.N && (A.N & 3) == 0) {
                   *reinterpret_cast<uint2*>(A.Y + yo) = o;
-                  for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+                  for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)(y0 + j))) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
                   count(yo, 8u);
                 } else {
                   const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
                   for (int x = 0; x < 4 && nn + x < A.N; ++x) {
                     A.Y[yo + x] = __float2bfloat16_rn(vv[x]);
-                    for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = __float2bfloat16_rn(vv[x]);
+                    for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)(y0 + j))) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = __float2bfloat16_rn(vv[x]);
                     count(yo + x, 2u);
                   }
                 }
@@ -455,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int qd = 0; qd < 4; ++qd) op[qd] = silu2(bf16lo(gp[qd]), bf16hi(gp[qd]), bf16lo(up[qd]), bf16hi(up[qd]));
               const size_t yo = (size_t)(y0 + j0 + j) * (A.N / 2) + nb0 / 2 + c8;
               *reinterpret_cast<uint4*>(A.Y + yo) = o;
-              for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint4*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+              for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)(y0 + j0 + j))) *reinterpret_cast<uint4*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
               count(yo, 16u);
             }
           }
@@ -469,13 +474,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const size_t yo = (size_t)(y0 + j0 + j) * A.N + nn;
               if (nn + 8 <= A.N && (A.N & 7) == 0) {
                 *reinterpret_cast<uint4*>(A.Y + yo) = val;
-                for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint4*>((__nv_bfloat16*)A.epi.dst[p] + yo) = val;
+                for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)(y0 + j0 + j))) *reinterpret_cast<uint4*>((__nv_bfloat16*)A.epi.dst[p] + yo) = val;
                 count(yo, 16u);
               } else {
                 const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(&val);
                 for (int x = 0; x < 8 && nn + x < A.N; ++x) {
                   A.Y[yo + x] = sv[x];
-                  for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = sv[x];
+                  for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)(y0 + j0 + j))) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = sv[x];
                   count(yo + x, 2u);
                 }
               }
@@ -583,13 +588,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const size_t yo = (size_t)(y0 + j) * A.N + nn;
           if (nn + 4 <= A.N && (A.N & 3) == 0) {
             *reinterpret_cast<uint2*>(A.Y + yo) = o;
-            for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+            for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)(y0 + j))) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
             count(yo, 8u);
           } else {
             const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
             for (int x = 0; x < 4 && nn + x < A.N; ++x) {
               A.Y[yo + x] = __float2bfloat16_rn(vv[x]);
-              for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = __float2bfloat16_rn(vv[x]);
+              for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)(y0 + j))) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = __float2bfloat16_rn(vv[x]);
               count(yo + x, 2u);
             }
           }
@@ -601,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // publish this CTA's stores to the consumer devices: CTA mode one release,
   // COUNT mode the bytes tallied per chunk
   if constexpr (kX) {
-    epi_signal_counts(A.epi, s_cnt);
+    epi_signal_counts(A.epi, s_cnt, true);
   } else if (A.epi.n) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -804,14 +809,14 @@ __device__ __forceinline__ void csk_store4(const Args& A, const RopeSmem& rs, in
     o.x = pack_bf16(v0, v1);
     o.y = pack_bf16(v2, v3);
     *reinterpret_cast<uint2*>(A.Y + yo) = o;
-    for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+    for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)j)) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
   } else {
     const float vv[4] = {v0, v1, v2, v3};
     for (int x = 0; x < 4; ++x)
       if (col + x < A.N) {
         const __nv_bfloat16 h = __float2bfloat16_rn(vv[x]);
         A.Y[yo + x] = h;
-        for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = h;
+        for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)j)) ((__nv_bfloat16*)A.epi.dst[p])[yo + x] = h;
       }
   }
 }
@@ -995,7 +1000,7 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
     const size_t yo = (size_t)j * N + c0 + 4 * l4;
     *reinterpret_cast<float4*>(A.r + yo) = v;
     *reinterpret_cast<uint2*>(Y + yo) = o;
-    for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+    for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)j)) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
   }
   if (threadIdx.x == 0) {
     KD_CTRACE(21);
@@ -1008,7 +1013,7 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
     }
   }
   if (A.epi.n && (split == 1 || my_rows > 0))  // publish: COUNT → h columns [c0, c0 + rows) of all M tokens
-    epi_signal(A.epi, (uint32_t)c0 * 2u, (uint32_t)(c0 + rows) * 2u, (uint32_t)M);
+    epi_signal(A.epi, (uint32_t)c0 * 2u, (uint32_t)(c0 + rows) * 2u, 0u, (uint32_t)M);
 }
 
 template <bool kX>  // as gemm_kernel: the handoff-protocol code only in the kX instance
@@ -1172,7 +1177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto store1 = [&](size_t yo, float v) {
       const __nv_bfloat16 h = __float2bfloat16_rn(v);
       A.Y[yo] = h;
-      for (int p = 0; p < A.epi.n; ++p) ((__nv_bfloat16*)A.epi.dst[p])[yo] = h;
+      for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)(yo / A.N))) ((__nv_bfloat16*)A.epi.dst[p])[yo] = h;
     };
     auto store_y = [&](int j, int col, float v0, float v1, float v2, float v3) {  // 4 consecutive outputs of token j
       if (A.rope) {  // two rotation pairs (col is a multiple of 4)
@@ -1186,7 +1191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         o.x = pack_bf16(v0, v1);
         o.y = pack_bf16(v2, v3);
         *reinterpret_cast<uint2*>(A.Y + yo) = o;
-        for (int p = 0; p < A.epi.n; ++p) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
+        for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)j)) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
       } else {
         if (col < A.N) store1(yo, v0);
         if (col + 1 < A.N) store1(yo + 1, v1);
@@ -1258,7 +1263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ep == 0) {
         fence_acq_rel_sys();
         if (A.epi.nch)
-          epi_release_range(A.epi, (uint32_t)n0 * 2u, (uint32_t)min(n0 + kBM, A.N) * 2u, (uint32_t)M);
+          epi_release_range(A.epi, (uint32_t)n0 * 2u, (uint32_t)min(n0 + kBM, A.N) * 2u, 0u, (uint32_t)M);
         else
           epi_release_cta(A.epi);
       }
@@ -1304,7 +1309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 128) { KD_TRACE(11); KD_CTRACE(25); }
     if (A.epi.n && my_rows > 0) {  // publish: COUNT → this owner's columns of all M tokens
       const int c0 = n0 + rank * rpo;
-      epi_signal(A.epi, (uint32_t)min(c0, A.N) * 2u, (uint32_t)min(c0 + my_rows, A.N) * 2u, (uint32_t)M);
+      epi_signal(A.epi, (uint32_t)min(c0, A.N) * 2u, (uint32_t)min(c0 + my_rows, A.N) * 2u, 0u, (uint32_t)M);
     }
   }
   // No closing cluster barrier: peers only ever WRITE into this CTA's recv
@@ -1412,7 +1417,7 @@ static kd_status geometry(const GemmShape& a, Geometry* g, int sms) {
 
 static size_t smem_bytes(const Geometry& g) {
   return 1024 + (size_t)g.stages * g.kbs * (kStageA + g.mma_n * kBK * 2) + (2 * kMaxStages + 6) * 8 +
-         2 * kChunk * kBM * 2 + 16 + 4 * kMaxChunks;
+         2 * kChunk * kBM * 2 + 16 + 4 * kMaxPeers * kMaxChunks;
 }
 
 // ---------------------------------------------------------------- dense GEMM kernel choice

@@ -556,7 +556,9 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
           }
           // chunk-aware consumer of a COUNT transfer: acquire chunk by chunk
           // inside the kernel (no wait launch); else wait for every chunk first
-          const bool whole = sp.off == S.writes[0].off && sp.len == S.writes[0].len;
+          // whole rows of the producer's output (all, or a scattered GEMM output's row span)
+          const bool whole = X.count && sp.off >= S.writes[0].off && sp.off + sp.len <= S.writes[0].off + S.writes[0].len &&
+                             (sp.off - S.writes[0].off) % X.row_bytes == 0 && sp.len % X.row_bytes == 0;
           const bool in_kernel = srcs_here.size() == 1 && X.count && whole && op_consumer_unit(K, ri, X.row_bytes) > 0 &&
                                  l.ctx.acq.n < kMaxAcqIn && !getenv("KD_NO_INKERNEL_ACQ");
           if (in_kernel) {
@@ -615,6 +617,10 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
         ep.dst[ep.n] = rt->ws_of[v] + land.first;
         ep.flag[ep.n] = (unsigned long long*)(rt->ws_of[v] + land.second);
         ep.started[ep.n] = (X.count && loopback(v)) ? (unsigned long long*)(rt->ws_of[v] + land.second) + nch : nullptr;
+        u64 prows = 0, prb = 0;  // row filter: this peer reads rows [row0, row0 + rows) only
+        const bool filt = X.count && op_count_geometry(K, &prows, &prb) && X.rows < prows;
+        ep.r0[ep.n] = filt ? (uint32_t)X.row0 : 0u;
+        ep.rn[ep.n] = filt ? (uint32_t)X.rows : 0u;
         ep.logt[ep.n] = log_on ? (unsigned long long*)(rt->ws_of[v] + Lv.xlog.at(it->second)) : nullptr;
         // delta replication: the peer's replicas of this kernel's replicated outputs
         int j = 0;

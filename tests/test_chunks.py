@@ -35,8 +35,9 @@ def _check(DEC, K, Plan, dg, assign, n_dev, n_micro, n_chunks):
     plan = Plan(dg.g, DEC.b200_machine(n_dev), assign, n_micro, n_chunks)
     xs = plan.transfers()
     lib = plan.chunks()
-    ref = OS.chunk_table(_oracle_kernels(K, dg.g), dg.g.edges(), assign, xs, n_chunks)
-    flat = [(t, c, cm, rows, rb, u, b, e) for t, (cm, rows, rb, u, chs) in enumerate(ref)
+    repl = {b for b, f in enumerate(dg.g._buf_flags) if f & K.KD_BUF_REPLICATED}
+    ref = OS.chunk_table(_oracle_kernels(K, dg.g), dg.g.edges(), assign, xs, n_chunks, repl)
+    flat = [(t, c, cm, r0, rows, rb, u, b, e) for t, (cm, r0, rows, rb, u, chs) in enumerate(ref)
             for c, (b, e) in enumerate(chs)]
     assert lib == flat
     return xs, ref
@@ -50,6 +51,11 @@ CASES = [
     ("hybrid", lambda DEC: DEC.DecoderGraph(synth.TINY_HYBRID), "role", 2),
     ("tp2", lambda DEC: DEC.TPDecoderGraph(synth.TINY.with_(n_kv_heads=4, n_micro=2), 2), "own", 4),
     ("sharded3", lambda DEC: DEC.ShardedKVDecoderGraph(synth.TINY.with_(n_micro=2), 2), "own", 3),
+    ("role3", lambda DEC: DEC.RoleDecoderGraph(synth.TINY.with_(n_micro=2, batch=4), 3), "own", 4),
+    ("role7_8b", lambda DEC: DEC.RoleDecoderGraph(synth.LLAMA8B.with_(n_layers=1, batch=64, n_micro=2), 7), "own", 8),
+    ("moe_ep", lambda DEC: DEC.MoEEPDecoderGraph(synth.TINY.with_(n_experts=4, top_k=2, n_micro=2, batch=4), 2, 2),
+     "own", 4),
+    ("repl_kv", lambda DEC: DEC.DecoderGraph(synth.TINY.with_(n_micro=2), replicate_kv=True), "repl", 3),
 ]
 
 
@@ -58,8 +64,31 @@ CASES = [
 def test_chunk_table_bit_exact_vs_oracle(mods, name, make, kind, n_dev, n_chunks):
     DEC, K, Plan = mods
     dg = make(DEC)
-    assign = dg.role_assign(0, 1) if kind == "role" else dg.assign()
+    if kind == "role":
+        assign = dg.role_assign(0, 1)
+    elif kind == "repl":  # RoPE/append apart from attention (delta-replicated KV)
+        assign = [{DEC.T_ATTN: 2}.get(k.template, 0 if k.template in DEC.MEMORY_ROLE else 1) for k in dg.kernels]
+    else:
+        assign = dg.assign()
     _check(DEC, K, Plan, dg, assign, n_dev, dg.cfg.n_micro, n_chunks)
+
+
+def test_scatter_rows_hand_values(mods):
+    """3:1 layout (m = 2 rows per shard): the QKV GEMM's output (a·m = 6 rows)
+    travels to shard s as rows [2s, 2s + 2) only; the shards' norm outputs
+    (their own 2 rows) travel whole to the GEMM device."""
+    DEC, K, Plan = mods
+    dg = DEC.RoleDecoderGraph(synth.TINY.with_(n_micro=2, batch=4), 3)
+    xs, ref = _check(DEC, K, Plan, dg, dg.assign(), 4, 2, 4)
+    name = {k.kid: k.name for k in dg.kernels}
+    seen = 0
+    for (i, prod, dst, nbytes, *_), (cm, r0, rows, rb, u, chs) in zip(xs, ref):
+        if name[prod] == "qkv":
+            assert (cm, r0, rows) == (1, 2 * dst, 2) and nbytes == 2 * rb
+            seen += 1
+        if name[prod].startswith("norm1."):
+            assert (r0, rows) == (0, 2)
+    assert seen == 3 * 2 * 2  # 3 shards x 2 micro-batches x 2 layers
 
 
 def test_chunk_table_8b_hand_values(mods):
@@ -83,12 +112,12 @@ def test_chunk_table_8b_hand_values(mods):
     hand = {"norm1": (8192, 256, 2048), "qkv": (12288, 1536, 3072), "attn": (8192, 256, 2048),
             "o": (8192, 16, 2048), "gu": (57344, 256, 14336), "silu": (28672, 256, 7168)}
     seen = set()
-    for (i, prod, dst, *_), (cm, rows, rb, u, chs) in zip(xs, ref):
+    for (i, prod, dst, *_), (cm, r0, rows, rb, u, chs) in zip(xs, ref):
         nm = name[prod]
         if layer[prod] != 1 or nm not in hand:
             continue
         rb_h, u_h, q_h = hand[nm]
-        assert (cm, rows, rb, u) == (1, 32, rb_h, u_h), nm
+        assert (cm, r0, rows, rb, u) == (1, 0, 32, rb_h, u_h), nm
         assert chs == [(c * q_h, (c + 1) * q_h) for c in range(4)], nm
         seen.add(nm)
     assert seen == set(hand)
@@ -117,7 +146,7 @@ def test_cta_mode_for_irregular_producers(mods):
     ops = {k.kid: k.name for k in dg.kernels}
     xs = plan.transfers()
     by_t = {}
-    for t, c, cm, rows, rb, u, b, e in plan.chunks():
+    for t, c, cm, r0, rows, rb, u, b, e in plan.chunks():
         by_t.setdefault(t, []).append((cm, b, e, rb))
     for t, (i, prod, dst, nbytes, *_) in enumerate(xs):
         if ops[prod] in ("dispatch", "gu", "down"):
