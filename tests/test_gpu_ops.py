@@ -87,6 +87,11 @@ GEMM_SHAPES = [
     (32, 4096, 4096),   # 8B O at the disaggregated pair's m=32 (N=2)
     (32, 4096, 14336),  # 8B down at m=32
     (32, 28672, 4096),  # 8B gate_up at m=32
+    (96, 6144, 4096),   # the 3:1 role layout's GEMM rows (3 x 32)
+    (224, 6144, 4096),  # the 7:1 layout (7 x 32): QKV, O, gate_up, down
+    (224, 4096, 4096),
+    (224, 28672, 4096),
+    (224, 4096, 14336),
     (64, 4096, 14336),  # 8B down (stream-K fixup)
     (64, 28672, 4096),  # 8B gate_up
     (128, 1024, 2048),  # m=128
