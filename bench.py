@@ -39,6 +39,8 @@ def parse():
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--kernels", action="store_true", help="also time every op kind (extra passes)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--exec", dest="exec_mode", default="graph", choices=["graph", "mega"],
+                   help="N=1: per-kernel CUDA graph (default) or the f1 megakernel (one launch per step)")
     p.add_argument("--layout", default="search", choices=["search", "pairs"],
                    help="N>1: the role layout kd_place_roles picks (default) or independent 1:1 pairs")
     return p.parse_args()
@@ -215,6 +217,25 @@ def role_layout(cfg, DEC, n_gpus):
     return n_gpus - 1, 2
 
 
+def step_bytes(cfg):
+    """Algorithmic HBM bytes of one monolithic decode step (dense attention
+    layers, N=1): every weight, every KV page, each activation written once
+    and read once, the fp32 residual read and written by each add."""
+    m, H, F, L = cfg.batch, cfg.hidden, cfg.ffn, cfg.n_layers
+    Hq, Hkv, D, pps = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.pages_per_seq
+    qkv = (Hq + 2 * Hkv) * D
+    w = (qkv * H + H * Hq * D + 2 * F * H + H * F + 2 * H) * 2
+    kv = m * pps * Hkv * 16 * D * 2 * 2 + m * pps * 4 + m * 4
+    norm = m * H * (4 + 4 + 2 + 2)                  # r read + write, delta read, h write
+    act = (m * H * 2 + m * qkv * 2 * 2             # QKV: X in, Y out, RoPE reads it
+           + m * Hq * D * 2 * 2 + 2 * m * Hkv * D * 2  # q written + read by attention, K/V slot appends
+           + m * Hq * D * 2 * 2                    # attention out, O reads it
+           + m * H * 2 + m * H * 2                 # O out, gate_up X
+           + m * 2 * F * 2 * 2 + m * F * 2 * 2     # gate_up out + SiLU read, SiLU out + down read
+           + m * H * 2)                            # down out
+    return L * (w + kv + 2 * norm + act) + m * H * (4 + 4 + 2)  # + the final residual add
+
+
 def workload_config(cfg, n_gpus, placement):
     return {"workload": f"{cfg.name} decode B={cfg.batch} C={cfg.context} L={cfg.n_layers}",
             "model_shape": {"hidden": cfg.hidden, "heads": cfg.n_heads, "kv_heads": cfg.n_kv_heads,
@@ -267,13 +288,15 @@ def main():
         # (KD_OP_GEMM_RMSNORM: the per-token Σr² is finished across the grid after an
         # in-kernel barrier; step 8.92 vs 8.95 ms). A/B: KD_BENCH_NO_FUSE (all),
         # KD_BENCH_NO_FUSE_ROPE, KD_BENCH_NO_FUSE_NORM, KD_BENCH_FUSE_NORM=o (O+norm2 only).
-        fuse = not os.environ.get("KD_BENCH_NO_FUSE")
+        mega = args.exec_mode == "mega"
+        fuse = not os.environ.get("KD_BENCH_NO_FUSE") and not mega
         dg = DEC.DecoderGraph(cfg, fuse_silu=fuse, fuse_rope=fuse and not os.environ.get("KD_BENCH_NO_FUSE_ROPE"),
                               fuse_norm=(fuse and not os.environ.get("KD_BENCH_NO_FUSE_NORM")) and
                               (os.environ.get("KD_BENCH_FUSE_NORM") or True))
         assign = [0] * dg.g.num_kernels
-        rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed, use_graph=not args.no_graph)
-        placement = "monolithic (all kernels on one B200)"
+        rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed, use_graph=not args.no_graph, megakernel=mega)
+        placement = "monolithic (all kernels on one B200)" + (
+            ", f1 megakernel: the unfused graph's 9 ops/layer as tasks of ONE persistent launch per step" if mega else "")
     elif cfg.name == "llama3-70b":
         # BASELINE config 3: GEMMs TP-sharded over N/2 GPUs, attention partners on the
         # other N/2 (head-sharded); row-parallel partials streamed to every partner by
@@ -394,21 +417,24 @@ def main():
     # per-kernel CUDA-event timing: a second pass of the same K steps whose
     # graph carries event-record nodes around every attention launch (events
     # split programmatic launch edges, so they are kept out of the headline)
-    rt.rt.profile_op(K.KD_OP_ATTENTION)
-    rt.rt.prepare()
-    for _ in range(2):
-        rt.step()
-    torch.cuda.synchronize()
-    attn_ms_tot, attn_n_tot = 0.0, 0
-    for _ in range(args.steps):
-        rt.step()
+    mega = world == 1 and args.exec_mode == "mega"
+    attn_ms, attn_n = 0.0, 0
+    if not mega:
+        rt.rt.profile_op(K.KD_OP_ATTENTION)
+        rt.rt.prepare()
+        for _ in range(2):
+            rt.step()
         torch.cuda.synchronize()
-        t_ms, t_n = rt.rt.op_time()
-        attn_ms_tot += t_ms
-        attn_n_tot += t_n
-    attn_ms, attn_n = attn_ms_tot / args.steps, attn_n_tot // args.steps
-    rt.rt.profile_op(0)
-    rt.rt.prepare()
+        attn_ms_tot, attn_n_tot = 0.0, 0
+        for _ in range(args.steps):
+            rt.step()
+            torch.cuda.synchronize()
+            t_ms, t_n = rt.rt.op_time()
+            attn_ms_tot += t_ms
+            attn_n_tot += t_n
+        attn_ms, attn_n = attn_ms_tot / args.steps, attn_n_tot // args.steps
+        rt.rt.profile_op(0)
+        rt.rt.prepare()
     if dist is not None:
         t = torch.tensor([ms], device="cpu" if os.environ.get("KD_BENCH_ONE_GPU") else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -434,8 +460,27 @@ def main():
             "peak_source": peak_src,
             "timing": "CUDA events (event-record nodes in the step graph) around every attention launch on its "
                       "stream, averaged over K profiled steps run right after the timed region"}
-    tr_path = os.path.join(ROOT, "profiles", "attention_traffic.json")
-    if os.path.exists(tr_path):
+    if mega:
+        # the megakernel is the step's only kernel: its algorithmic bytes are the
+        # whole step's (KV cache, weights, activations), its
+        # duration the timed step's (CUDA events on its stream)
+        sb = step_bytes(cfg)
+        achieved = sb / (ms_step / 1e3) / 1e9
+        roof = {"kernel": f"mega_kernel<{D}> (f1: the whole step, one launch)", "bound": "hbm",
+                "achieved": round(achieved, 1), "peak": hbm_gbs, "unit": "GB/s", "frac": round(achieved / hbm_gbs, 4),
+                "traffic": None, "bytes_per_launch": sb, "avg_launch_us": round(ms_step * 1e3, 2),
+                "launches_per_step": 1, "share_of_step": 1.0, "peak_source": peak_src,
+                "timing": "CUDA events on the launching stream around the K timed steps (one launch each)"}
+    tr_path = os.path.join(ROOT, "profiles", "mega_traffic.json" if mega else "attention_traffic.json")
+    if mega and os.path.exists(tr_path):
+        try:
+            tr = json.load(open(tr_path))
+            if tr.get("algorithmic_bytes_per_launch") == roof["bytes_per_launch"]:
+                roof["traffic"] = tr.get("bytes_per_launch")
+                roof["traffic_source"] = tr.get("source")
+        except Exception:
+            pass
+    elif os.path.exists(tr_path):
         # ncu dram bytes of the same launch shape (profiles/), ONLY if captured
         # from the kernel sources this build compiled (sha256 stamp), else null
         try:

@@ -412,6 +412,34 @@ kd_status kd_runtime_set_mode(kd_runtime* rt, uint32_t mode);
 kd_status kd_runtime_set_graph(kd_runtime* rt, int32_t enable);
 /* Resolves every pointer, encodes TMA descriptors, enables peer access. */
 kd_status kd_runtime_prepare(kd_runtime* rt);
+/* Execution strategy (launch overhead P:281):
+ *  KD_EXEC_GRAPH (default): one kernel per schedule entry, replayed from a
+ *    per-device CUDA graph with programmatic dependent launch;
+ *  KD_EXEC_MEGAKERNEL: ONE persistent cooperative launch per device per step
+ *    executes the device's whole static schedule (every op a task, in-kernel
+ *    dependency waits on per-task completion counters, weights / KV pages
+ *    streamed across task boundaries). Supported: single-device schedules
+ *    (no cross-device transfers) of bf16 ADD_RMSNORM, GEMM (M <= 128,
+ *    K % 128 == 0, N % 8 == 0), ROPE_APPEND, ATTENTION (head_dim 64/128, no
+ *    LSE flag), SILU_MUL and RESIDUAL_ADD; anything else → KD_ERR_UNSUPPORTED
+ *    at kd_runtime_prepare. Its outputs match the per-kernel path's within
+ *    rounding (add+RMSNorm, RoPE, SiLU and residual add are bitwise identical;
+ *    the GEMM split-K and attention merge orders differ) and are bitwise
+ *    reproducible step to step.
+ * The megakernel needs its own zeroed device workspace per local device:
+ * after kd_runtime_prepare, kd_runtime_exec_workspace_bytes gives the size;
+ * kd_runtime_set_exec_workspace binds it (caller-owned, 256-byte aligned,
+ * zero-initialised; borrowed for the runtime's lifetime). kd_step before that
+ * → KD_ERR_STATE. Device-side watchdogs (a dependency or pipeline wait that
+ * does not complete in ~20 s) record the runtime error word and abort the
+ * launch (kd_runtime_check reports KD_ERR_TIMEOUT). */
+enum { KD_EXEC_GRAPH = 0, KD_EXEC_MEGAKERNEL = 1 };
+kd_status kd_runtime_set_exec(kd_runtime* rt, uint32_t exec);
+kd_status kd_runtime_exec_workspace_bytes(kd_runtime* rt, uint32_t dev, uint64_t* bytes);
+kd_status kd_runtime_set_exec_workspace(kd_runtime* rt, uint32_t dev, void* dev_ptr, uint64_t bytes);
+/* KD_EXEC_MEGAKERNEL: tasks, dynamic shared memory bytes per CTA and grid
+ * (one CTA per SM) of local device j's megakernel (after prepare). */
+kd_status kd_runtime_exec_info(kd_runtime* rt, uint32_t j, uint32_t* n_tasks, uint32_t* smem_bytes, uint32_t* grid);
 /* Per-step statistics (filled by kd_step when `stats` is non-NULL; that call
  * synchronises every local device). Times are ns; index j = local device j.
  *  step_ns[j]: device time of the step on device j (CUDA events on its stream);

@@ -31,6 +31,7 @@ KD_OP_NONE, KD_OP_ADD_RMSNORM, KD_OP_GEMM, KD_OP_ROPE_APPEND, KD_OP_ATTENTION, K
 KD_BF16, KD_F32 = 0, 1
 KD_OBJ_AUTO, KD_OBJ_THROUGHPUT, KD_OBJ_LATENCY = 0, 1, 2
 KD_MODE_DISAGG, KD_MODE_NO_TRANSFER, KD_MODE_LOG = 0, 1, 2
+KD_EXEC_GRAPH, KD_EXEC_MEGAKERNEL = 0, 1
 
 
 class KdError(RuntimeError):
@@ -217,6 +218,10 @@ _PROTOS = {
     "kd_runtime_set_mode": (kd_status, [P, u32]),
     "kd_runtime_set_graph": (kd_status, [P, i32]),
     "kd_runtime_prepare": (kd_status, [P]),
+    "kd_runtime_set_exec": (kd_status, [P, u32]),
+    "kd_runtime_exec_workspace_bytes": (kd_status, [P, u32, PU64]),
+    "kd_runtime_set_exec_workspace": (kd_status, [P, u32, P, u64]),
+    "kd_runtime_exec_info": (kd_status, [P, u32, PU32, PU32, PU32]),
     "kd_step": (kd_status, [P, C.POINTER(P), u64, C.POINTER(kd_step_stats)]),
     "kd_runtime_log": (kd_status, [P, C.POINTER(kd_log_record), u32, PU32]),
     "kd_runtime_check": (kd_status, [P]),

@@ -266,6 +266,24 @@ class Runtime:
     def prepare(self):
         check(K.kd_runtime_prepare(self.h), "kd_runtime_prepare")
 
+    def set_exec(self, exec_mode: int):
+        """KD_EXEC_GRAPH (per-kernel CUDA graph) or KD_EXEC_MEGAKERNEL (f1)."""
+        check(K.kd_runtime_set_exec(self.h, exec_mode), "kd_runtime_set_exec")
+
+    def exec_workspace_bytes(self, dev: int) -> int:
+        n = C.c_uint64()
+        check(K.kd_runtime_exec_workspace_bytes(self.h, dev, C.byref(n)), "kd_runtime_exec_workspace_bytes")
+        return n.value
+
+    def set_exec_workspace(self, dev: int, ptr: int, nbytes: int):
+        check(K.kd_runtime_set_exec_workspace(self.h, dev, C.c_void_p(int(ptr)), int(nbytes)),
+              "kd_runtime_set_exec_workspace")
+
+    def exec_info(self, j: int = 0) -> dict:
+        t, s, g = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        check(K.kd_runtime_exec_info(self.h, j, C.byref(t), C.byref(s), C.byref(g)), "kd_runtime_exec_info")
+        return {"tasks": t.value, "smem_bytes": s.value, "grid": g.value}
+
     def step(self, streams: Sequence[int], step_id: Optional[int] = None, stats: bool = False):
         """One decode step (async). stats=True synchronises and returns
         kd_step_stats as a dict (step_ns / wait_ns / chunk_waits per local

@@ -214,4 +214,24 @@ struct WaitList {
 // base = steps the runtime ran with transfers off (their epochs carry no releases)
 kd_status launch_wait(const WaitList& w, const unsigned* epoch, unsigned base, unsigned* err, cudaStream_t s);
 
+// f1 megakernel (mega.cu): one persistent launch per step executes a device's
+// whole schedule. Each op is described by its attrs and resolved span pointers
+// (the same operands the per-kernel launchers get) plus the span lengths, from
+// which the megakernel derives its in-kernel dependencies.
+struct MegaOpDesc {
+  uint32_t op = 0;
+  std::vector<uint8_t> attrs;
+  std::vector<void*> rd, wr;
+  std::vector<uint64_t> rd_len, wr_len;
+};
+struct MegaPlan;
+kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64_t* ws_bytes);
+// ws: zero-initialised device memory of ws_bytes (256-byte aligned), owned by the caller
+kd_status mega_bind(MegaPlan* p, void* ws, uint64_t bytes, unsigned* err);
+kd_status mega_launch(MegaPlan* p, cudaStream_t s);
+kd_status mega_info(const MegaPlan* p, uint32_t* n_tasks, uint32_t* smem, uint32_t* grid);
+void mega_destroy(MegaPlan* p);
+// the first in-kernel watchdog record of the megakernel (empty if none)
+kd_status mega_diag(const MegaPlan* p, std::string* what);
+
 }  // namespace kd

@@ -1,0 +1,1497 @@
+// mega.cu — f1: a persistent per-device megakernel that executes a device's
+// whole static schedule (the launch-overhead motive is
+// PAPER.md §3.3 P:281 "kernel launch overhead" and P:398 "CUDA Graph ... to
+// reduce launch overheads"). One launch per step replaces the per-kernel CUDA
+// graph: every op of the schedule becomes a task, every task is cut into
+// units, and each CTA (one per SM, co-resident by cooperative launch) walks the
+// task list in schedule order with warp-specialised roles that persist across
+// tasks:
+//  * warp 0, loader: all global→shared traffic through one 8 KB-slot arena —
+//    GEMM stages (weight boxes + activation boxes, TMA) and attention page
+//    slabs (K/V, TMA) — plus the query rows (bulk copy). It runs ahead of the
+//    consumers across task boundaries: a GEMM's weight boxes and an
+//    attention's KV pages do not depend on the previous task, so they are
+//    requested while the previous task's epilogue, fold or norm still runs;
+//    only the activation boxes / query rows / the one page this step appends
+//    to wait for the task's dependencies (in-kernel flag waits, below).
+//  * warp 1, MMA issuer (tcgen05.mma, fp32 accumulators double-buffered in TMEM).
+//  * warp 2, attention merge (per-item warp states, split LSE merge).
+//  * warps 4-11, workers: attention consumers (mma.sync online softmax, one
+//    warp per page slot class), the GEMM epilogue (TMEM → bf16 output or fp32
+//    split partial + fold), and the element-wise tasks (add+RMSNorm, RoPE +
+//    KV append, SiLU·mul, residual add) with the same per-element arithmetic
+//    as the standalone kernels (bitwise identical for those ops).
+// Dependencies: a task waits (ld.acquire.gpu on the producer tasks' completion
+// counters) for exactly the tasks whose declared spans conflict with its own
+// (RAW, WAR, WAW over the plan's buffers — the DAG of P:276 plus the
+// anti-dependences a concurrent executor must also respect), transitively
+// reduced. Counters are monotonic across steps: a task is complete in step e
+// (0-based) at (e + 1) · units, so nothing is ever reset.
+// The schedule is a topological order and every wait points to an earlier
+// task, so with all CTAs resident the kernel cannot deadlock.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "launch.hpp"
+#include "mmasync.cuh"
+#include "tcgen05.cuh"
+
+namespace kd {
+namespace mega {
+
+using gemm::bulk_g2s;
+using gemm::mbar_arrive;
+using gemm::mbar_expect_tx;
+using gemm::mbar_init;
+using gemm::mma_bf16;
+using gemm::mma_commit;
+using gemm::named_bar;
+using gemm::policy_evict_first;
+using gemm::policy_evict_last;
+using gemm::smem_u32;
+using gemm::sw128_desc;
+using gemm::tma_load_2d;
+using gemm::tmem_ld16_nowait;
+using gemm::tmem_ld_wait;
+using mmas::ldsm_x4;
+using mmas::ldsm_x4_t;
+using mmas::mma16816;
+using mmas::movm_t;
+using mmas::tile_off;
+using mmas::tma_3d;
+
+constexpr int kWarps = 12, kThreads = kWarps * 32;
+constexpr int kLoader = 0, kMma = 1, kMerge = 2, kW0 = 4;  // workers: warps 4..11
+constexpr int kWorkers = 8, kWorkerThreads = kWorkers * 32;
+constexpr int kSlot = 8192;   // arena slot: one attention page (K + V slab, D ≤ 128) or 1/SPS GEMM stage
+constexpr int kMaxSlots = 28;
+constexpr int kMaxStages = 8;
+constexpr int kMaxDep = 8;
+constexpr int kMaxG = 8;
+constexpr int kPage = 16;
+constexpr int kAccCols = 128;  // TMEM columns per accumulator (mma_n ≤ 128), two accumulators
+constexpr int kBarW = 1, kBarHalf0 = 2;  // named barriers: all workers; worker halves (2, 3)
+constexpr int kFastSplits = 4, kFastSplitLse = 128;
+
+enum Kind : int { MK_NORM = 1, MK_GEMM = 2, MK_ROPE = 3, MK_ATTN = 4, MK_SILU = 5, MK_RESID = 6 };
+
+struct alignas(64) Task {
+  CUtensorMap tm0;  // GEMM: W [N][K]; ATTN: K cache slabs
+  CUtensorMap tm1;  // GEMM: X [M][K]; ATTN: V cache slabs
+  int kind;
+  unsigned done_units;  // completion increments per step
+  int n_dep;
+  int dep[kMaxDep];
+  unsigned dep_units[kMaxDep];
+  int rot;      // element-wise: unit u runs on CTA (u + rot) % grid
+  int n_units;  // element-wise units; GEMM: tiles·KB k-block units; ATTN: items
+  const void* a0;
+  const void* a1;
+  const void* a2;
+  void* o0;
+  void* o1;
+  void* o2;
+  const void* dl[kMaxDeltas];
+  int n_delta;
+  int M, N, K;                         // GEMM / NORM (M rows, N = hidden) / SILU (N = F) / RESID (K = n8)
+  int KB, tiles, kbs, mma_n, maxc, gg;  // GEMM: k-blocks per tile, tiles, 64-col boxes per stage, MMA N, contributors bound, CTAs
+  unsigned* ctr;                       // GEMM tile arrivals / ATTN unit (split) arrivals
+  unsigned* ticket;                    // ATTN item tickets
+  float* part;                         // GEMM partials [tiles][maxc][M][128] / ATTN part_o
+  float* part_lse;                     // ATTN
+  int Hq, Hkv, D, G, pps, splits, pps_split, page, n_dyn, rows, slot_offset;
+  float scale_log2, eps;
+  const double* freq;                  // ROPE θ^(−2i/D)
+};
+
+struct Geo {
+  int NS, NG, SPS, A;  // arena slots, GEMM stages, slots per stage, attention slots (multiple of 8)
+  int n_tasks;
+  int Gm;              // comb buffers sized for Gm query heads per kv head
+  uint32_t off_q, off_comb, off_ml, off_bar, off_misc;  // dynamic smem offsets
+};
+
+// ------------------------------------------------------------------ waits with watchdogs
+// A broken protocol must not hang the box: every spin is bounded (≈ 4 s of
+// clock). The first thread to time out records where (code, CTA, warp, task,
+// two wait-specific words) in the control block, sets the runtime error word
+// and raises a grid-wide abort flag; every other wait polls the flag and
+// returns, so the launch drains (with garbage) and kd_runtime_check reports it.
+constexpr long long kTimeout = 1ll << 33;
+struct Sm;
+__device__ void report(const Sm& S, unsigned* err, unsigned code, unsigned a, unsigned b);
+__device__ __forceinline__ bool aborted(const Sm& S);
+__device__ __forceinline__ bool mbar_try(uint64_t* b, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mwait(uint64_t* b, unsigned parity, unsigned* err, const Sm& S) {
+  if (mbar_try(b, parity)) return;
+  const long long t0 = clock64();
+  for (unsigned n = 0;; ++n) {
+    if (mbar_try(b, parity)) return;
+    if ((n & 1023u) == 1023u) {
+      if (aborted(S)) return;
+      if (clock64() - t0 > kTimeout) {
+        report(S, err, 5u, smem_u32(b), parity);
+        return;
+      }
+    }
+  }
+}
+__device__ __forceinline__ void mwait_sleep(uint64_t* b, unsigned parity, unsigned* err, const Sm& S) {
+  const long long t0 = clock64();
+  for (unsigned n = 0; !mbar_try(b, parity); ++n) {
+    __nanosleep(128);
+    if ((n & 255u) == 255u) {
+      if (aborted(S)) return;
+      if (clock64() - t0 > kTimeout) {
+        report(S, err, 5u, smem_u32(b), parity);
+        return;
+      }
+    }
+  }
+}
+__device__ __forceinline__ unsigned ld_acq_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_rel_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// publish one completed unit of task t: caller ordered the unit's stores
+// before this thread (bar.sync); the release covers them (cumulativity)
+__device__ __forceinline__ void signal_done(unsigned* done, int t) {
+  fence_acq_rel_gpu();
+  red_rel_gpu(done + t, 1u);
+}
+
+__host__ __device__ __forceinline__ long long ubeg(long long c, long long U, long long G) { return c * U / G; }
+__host__ __device__ __forceinline__ long long uowner(long long u, long long U, long long G) {
+  return ((u + 1) * G + U - 1) / U - 1;
+}
+
+struct Sm {
+  uint8_t* arena;
+  uint64_t *gfull, *gempty, *afull, *aempty, *tfull, *tempty, *qfull, *qempty, *ifull, *iempty, *cfull, *cempty;
+  __nv_bfloat16* qsm;  // [2][Gm·D]
+  float* comb;         // [8][Gm][D]
+  float* comb_ml;      // [8][Gm][2]
+  int* s_item;         // [4]
+  uint8_t* sstate;     // loader: per-slot release state
+  float* red;          // [8] norm partial sums
+  unsigned* bcast;     // [4]
+  float *s_w, *s_M, *s_L, *s_lse;
+  uint32_t* tmem_slot;
+  int* cur;            // [12] task index per warp (diagnostics)
+  unsigned* abortp;    // control block: grid-wide abort flag
+  unsigned* rec;       // control block: first timeout record [8]
+};
+
+__device__ __forceinline__ bool aborted(const Sm& S) { return *(volatile unsigned*)S.abortp != 0u; }
+__device__ void report(const Sm& S, unsigned* err, unsigned code, unsigned a, unsigned b) {
+  if (atomicCAS(S.abortp, 0u, 1u) == 0u) {
+    const int warp = threadIdx.x >> 5;
+    S.rec[0] = code;
+    S.rec[1] = blockIdx.x;
+    S.rec[2] = warp;
+    S.rec[3] = threadIdx.x & 31;
+    S.rec[4] = (unsigned)S.cur[warp];
+    S.rec[5] = a;
+    S.rec[6] = b;
+    S.rec[7] = 1u;
+    __threadfence();
+    if (err) atomicExch(err, code);
+  }
+}
+// the calling thread waits until every dependency of T completed this step
+__device__ void deps_wait(const Task& T, const unsigned* done, unsigned ep, unsigned* err, const Sm& S) {
+  for (int i = 0; i < T.n_dep; ++i) {
+    const unsigned target = (ep + 1u) * T.dep_units[i];
+    const unsigned* p = done + T.dep[i];
+    if (ld_acq_gpu(p) >= target) continue;
+    const long long t0 = clock64();
+    for (unsigned n = 0; ld_acq_gpu(p) < target; ++n) {
+      __nanosleep(64);
+      if ((n & 255u) == 255u) {
+        if (aborted(S)) return;
+        if (clock64() - t0 > kTimeout) {
+          report(S, err, 4u, (unsigned)T.dep[i], ld_acq_gpu(p));
+          return;
+        }
+      }
+    }
+  }
+  fence_acq_rel_gpu();
+}
+
+// loader slot state bits
+constexpr uint8_t SS_PEND = 1, SS_ATTN = 2, SS_RPAR = 4, SS_APAR = 8;
+
+// loader lane 0: make slots [s0, s0 + n) free (their previous use released)
+__device__ __forceinline__ void claim(const Sm& S, const Geo& g, int s0, int n, unsigned* err) {
+  for (int s = s0; s < s0 + n; ++s) {
+    const uint8_t st = S.sstate[s];
+    if (!(st & SS_PEND)) continue;
+    const unsigned par = (st & SS_RPAR) ? 1u : 0u;
+    if (st & SS_ATTN) {
+      mwait(&S.aempty[s], par, err, S);
+      S.sstate[s] = st & ~SS_PEND;
+    } else {
+      const int q = s / g.SPS;
+      mwait(&S.gempty[q], par, err, S);
+      for (int x = q * g.SPS; x < (q + 1) * g.SPS; ++x)
+        if ((S.sstate[x] & (SS_PEND | SS_ATTN)) == SS_PEND) S.sstate[x] &= ~SS_PEND;
+    }
+  }
+}
+
+// ================================================================== loader
+__device__ void load_gemm(const Task& T, const Sm& S, const Geo& g, const unsigned* done, unsigned ep, unsigned* err,
+                          unsigned& gs) {
+  const int lane = threadIdx.x & 31;
+  const long long U = (long long)T.tiles * T.KB;
+  const int c = blockIdx.x;
+  if (c >= T.gg) return;
+  const long long u0 = ubeg(c, U, T.gg), u1 = ubeg(c + 1, U, T.gg);
+  const int n = (int)(u1 - u0);
+  if (lane != 0 || n <= 0) return;
+  const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+  const int kbs = T.kbs, xbox = T.mma_n * 128;
+  const unsigned tx = (unsigned)(kbs * (16384 + xbox));
+  const int npre = min(g.NG, n);
+  const unsigned gs0 = gs;
+  auto stage_base = [&](int q) { return S.arena + (size_t)q * g.SPS * kSlot; };
+  auto load_x = [&](int q, long long u) {
+    const int kb = (int)(u % T.KB);
+    for (int b = 0; b < kbs; ++b)
+      tma_load_2d(stage_base(q) + kbs * 16384 + b * xbox, &T.tm1, (kb * kbs + b) * 64, 0, &S.gfull[q], px);
+  };
+  for (int i = 0; i < n; ++i) {
+    const long long u = u0 + i;
+    const int tile = (int)(u / T.KB), kb = (int)(u % T.KB);
+    const int q = (int)(gs % (unsigned)g.NG);
+    const unsigned use = gs / (unsigned)g.NG;
+    claim(S, g, q * g.SPS, g.SPS, err);
+    mbar_expect_tx(&S.gfull[q], tx);
+    for (int b = 0; b < kbs; ++b)
+      tma_load_2d(stage_base(q) + b * 16384, &T.tm0, (kb * kbs + b) * 64, tile * 128, &S.gfull[q], pw);
+    for (int x = q * g.SPS; x < (q + 1) * g.SPS; ++x)
+      S.sstate[x] = (uint8_t)((S.sstate[x] & SS_APAR) | SS_PEND | ((use & 1u) ? SS_RPAR : 0));
+    ++gs;
+    if (i >= npre) {
+      load_x(q, u);
+    } else if (i == npre - 1) {
+      // weights of the first npre stages are in flight: now wait for the
+      // producers of X, then issue the held-back activation boxes
+      deps_wait(T, done, ep, err, S);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      for (int j = 0; j < npre; ++j) load_x((int)((gs0 + j) % (unsigned)g.NG), u0 + j);
+    }
+  }
+}
+
+__device__ void load_attn(const Task& T, const Sm& S, const Geo& g, const unsigned* done, unsigned ep, unsigned* err,
+                          unsigned& ak, unsigned& ci, int& apos) {
+  const int lane = threadIdx.x & 31;
+  const int G = (int)gridDim.x, c = blockIdx.x;
+  const int D = T.D, Hkv = T.Hkv, Gq = T.G;
+  const unsigned slab = (unsigned)(kPage * D * 2);
+  const unsigned per_step = (unsigned)(T.n_dyn + G);
+  uint64_t pol = policy_evict_first();
+  auto fetch = [&]() -> int {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(T.ticket, 1u) - ep * per_step;
+    t = __shfl_sync(0xffffffffu, t, 0);
+    return t < (unsigned)T.n_dyn ? G + (int)t : -1;
+  };
+  auto publish = [&](int it) {
+    if (lane == 0) {
+      const int is = (int)(ak & 3u);
+      if (ak >= 4) mwait(&S.iempty[is], ((ak >> 2) - 1u) & 1u, err, S);
+      S.s_item[is] = it;
+      mbar_arrive(&S.ifull[is]);
+    }
+    __syncwarp();
+    ++ak;
+  };
+  const int32_t* bt = (const int32_t*)T.a1;
+  const int32_t* sl = (const int32_t*)T.a2;
+  int it = c < T.n_units ? c : fetch();
+  bool first = true;
+  for (;;) {
+    publish(it);
+    if (it < 0) break;
+    const int nxt = fetch();
+    const int split = it % T.splits, unit = it / T.splits;
+    const int gh = unit / T.rows, b = unit % T.rows;
+    const int len = __ldg(sl + b) - T.slot_offset;
+    const int p0 = split * T.pps_split;
+    const int np = max(0, min((len + kPage - 1) / kPage, p0 + T.pps_split) - p0);
+    const int base = (apos + 7) / 8 * 8 % g.A;
+    // pages strictly before the one holding the appended position may be
+    // requested before the dependencies (RoPE/append writes only that page)
+    const int safe = first ? max(0, min(np, (len - 1) / kPage - p0)) : 0;
+    const int npre = min(safe, g.A);
+    auto issue = [&](int t, int pid) {
+      if (lane == 0) {
+        const int s = (base + t) % g.A;
+        claim(S, g, s, 1, err);
+        const uint8_t st = S.sstate[s];
+        const uint8_t ap = st & SS_APAR;
+        S.sstate[s] = (uint8_t)(SS_PEND | SS_ATTN | (ap ? SS_RPAR : 0) | (ap ? 0 : SS_APAR));
+        const int row = (pid * Hkv + gh) * kPage;
+        uint8_t* dst = S.arena + (size_t)s * kSlot;
+        mbar_expect_tx(&S.afull[s], 2u * slab);
+        tma_3d(dst, &T.tm0, 0, 0, row, &S.afull[s], pol);
+        tma_3d(dst + slab, &T.tm1, 0, 0, row, &S.afull[s], pol);
+      }
+    };
+    // the query rows (RoPE output) go out right after the dependency wait —
+    // before any page beyond the ring, whose slot only frees once the
+    // consumers (which need q) release it
+    bool qdone = false;
+    auto load_q = [&]() {
+      if (first) {
+        if (lane == 0) {
+          deps_wait(T, done, ep, err, S);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        first = false;
+      }
+      if (lane == 0) {
+        const int qs = (int)(ci & 1u);
+        if (ci >= 2) mwait(&S.qempty[qs], ((ci >> 1) - 1u) & 1u, err, S);
+        mbar_expect_tx(&S.qfull[qs], (unsigned)(Gq * D * 2));
+        bulk_g2s(S.qsm + (size_t)qs * g.Gm * D, (const __nv_bfloat16*)T.a0 + (size_t)b * T.Hq * D + (size_t)gh * Gq * D,
+                 (unsigned)(Gq * D * 2), &S.qfull[qs]);
+      }
+      __syncwarp();
+      qdone = true;
+    };
+    for (int j0 = 0; j0 < np; j0 += 32) {
+      const int j = j0 + lane;
+      const int mine = j < np ? __ldg(bt + (size_t)b * T.pps + p0 + j) : 0;
+      const int cnt = min(32, np - j0);
+      for (int t = 0; t < cnt; ++t) {
+        const int pid = __shfl_sync(0xffffffffu, mine, t);
+        if (!qdone && (!first || j0 + t == npre)) load_q();
+        issue(j0 + t, pid);
+      }
+    }
+    if (!qdone) load_q();
+    ++ci;
+    apos = (base + np) % g.A;
+    it = nxt;
+  }
+}
+
+// ================================================================== MMA issuer
+__device__ void mma_gemm(const Task& T, const Sm& S, const Geo& g, uint32_t tmem, unsigned* err, unsigned& gs,
+                         unsigned& pc) {
+  const int lane = threadIdx.x & 31;
+  const long long U = (long long)T.tiles * T.KB;
+  const int c = blockIdx.x;
+  if (c >= T.gg) return;
+  const long long u0 = ubeg(c, U, T.gg), u1 = ubeg(c + 1, U, T.gg);
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T.mma_n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const int kbs = T.kbs, xbox = T.mma_n * 128;
+  for (long long u = u0; u < u1;) {
+    const int tile = (int)(u / T.KB);
+    const long long pe = min(u1, (long long)(tile + 1) * T.KB);  // piece [u, pe)
+    const unsigned acc = pc & 1u;
+    if (pc >= 2) mwait(&S.tempty[acc], ((pc >> 1) - 1u) & 1u, err, S);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t td = tmem + acc * kAccCols;
+    for (long long v = u; v < pe; ++v) {
+      const int q = (int)(gs % (unsigned)g.NG);
+      mwait(&S.gfull[q], (gs / (unsigned)g.NG) & 1u, err, S);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (lane == 0) {
+        const uint32_t a = smem_u32(S.arena + (size_t)q * g.SPS * kSlot);
+        const uint32_t bx = a + kbs * 16384;
+        for (int b = 0; b < kbs; ++b)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_bf16(td, sw128_desc(a + b * 16384 + 32 * k), sw128_desc(bx + b * xbox + 32 * k), idesc,
+                     (v > u || b > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&S.gempty[q]);
+      }
+      __syncwarp();
+      ++gs;
+    }
+    if (lane == 0) mma_commit(&S.tfull[acc]);
+    __syncwarp();
+    ++pc;
+    u = pe;
+  }
+}
+
+// ================================================================== workers
+// GEMM epilogue: TMEM → bf16 output (a whole tile) or fp32 partial, and the
+// last contributor of a split tile folds every contributor's partial in
+// contributor order (deterministic) into the bf16 output
+__device__ void epi_gemm(const Task& T, int t, const Sm& S, unsigned* done, unsigned ep, uint32_t tmem, unsigned* err,
+                         unsigned& pc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wt = threadIdx.x - kW0 * 32;
+  const long long U = (long long)T.tiles * T.KB;
+  const int c = blockIdx.x;
+  if (c >= T.gg) return;
+  const long long u0 = ubeg(c, U, T.gg), u1 = ubeg(c + 1, U, T.gg);
+  const int q = warp & 3, h = (warp - kW0) >> 2;
+  const int row = q * 32 + lane;
+  const int M = T.M, N = T.N;
+  __nv_bfloat16* Y = (__nv_bfloat16*)T.o0;
+  for (long long u = u0; u < u1;) {
+    const int tile = (int)(u / T.KB);
+    const long long tb = (long long)tile * T.KB, te = tb + T.KB;
+    const long long pe = min(u1, te);
+    const bool whole = (u == tb && pe == te);
+    const unsigned acc = pc & 1u;
+    mwait_sleep(&S.tfull[acc], (pc >> 1) & 1u, err, S);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t ta = tmem + acc * kAccCols + ((uint32_t)(q * 32) << 16);
+    const int n = tile * 128 + row;
+    const int f = (int)uowner(tb, U, T.gg);
+    const int nc = (int)uowner(te - 1, U, T.gg) - f + 1, cidx = c - f;
+    float* part = T.part + ((size_t)tile * T.maxc + cidx) * (size_t)M * 128;
+    for (int cc = h; cc * 16 < T.mma_n; cc += 2) {
+      uint32_t v[16];
+      tmem_ld16_nowait(ta + cc * 16, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int tok = cc * 16 + j;
+        if (tok < M) {
+          if (whole) {
+            if (n < N) Y[(size_t)tok * N + n] = __float2bfloat16_rn(__uint_as_float(v[j]));
+          } else {
+            part[(size_t)tok * 128 + row] = __uint_as_float(v[j]);
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.tempty[acc]);
+    named_bar(kBarW, kWorkerThreads);
+    if (whole) {
+      if (wt == 0) signal_done(done, t);
+    } else {
+      if (wt == 0) {
+        fence_acq_rel_gpu();
+        const unsigned prev = atom_add_acq_rel_gpu(T.ctr + tile, 1u);
+        S.bcast[0] = (prev + 1u == (ep + 1u) * (unsigned)nc) ? 1u : 0u;
+      }
+      named_bar(kBarW, kWorkerThreads);
+      if (S.bcast[0]) {
+        const float* pt = T.part + (size_t)tile * T.maxc * M * 128;
+        const int n0 = tile * 128;
+        for (int e = wt; e < M * 32; e += kWorkerThreads) {
+          const int tok = e >> 5, r4 = (e & 31) * 4;
+          if (n0 + r4 >= N) continue;
+          float4 a = __ldcg(reinterpret_cast<const float4*>(pt + (size_t)tok * 128 + r4));
+          for (int k = 1; k < nc; ++k) {
+            const float4 b = __ldcg(reinterpret_cast<const float4*>(pt + ((size_t)k * M + tok) * 128 + r4));
+            a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+          }
+          uint2 o;
+          o.x = pack_bf16(a.x, a.y);
+          o.y = pack_bf16(a.z, a.w);
+          *reinterpret_cast<uint2*>(Y + (size_t)tok * N + n0 + r4) = o;
+        }
+        named_bar(kBarW, kWorkerThreads);
+        if (wt == 0) signal_done(done, t);
+      }
+    }
+    ++pc;
+    u = pe;
+  }
+}
+
+// a3 on one row with the worker threads: exactly add_rmsnorm_kernel's
+// element mapping and reduction order (bitwise identical to it)
+constexpr int kNormChunks = 4;
+__device__ void norm_row(const Task& T, const Sm& S, int row) {
+  const int tid = threadIdx.x - kW0 * 32;
+  const int H = T.N, nch = H / 8;
+  float* r = (float*)T.o1;
+  const __nv_bfloat16* gamma = (const __nv_bfloat16*)T.a1;
+  __nv_bfloat16* hout = (__nv_bfloat16*)T.o0;
+  uint4 gm[kNormChunks];
+#pragma unroll
+  for (int c = 0; c < kNormChunks; ++c) {
+    const int ch = tid + c * kWorkerThreads;
+    if (ch < nch) gm[c] = reinterpret_cast<const uint4*>(gamma)[ch];
+  }
+  float v[kNormChunks][8];
+  float ss = 0.f;
+  float* rr = r + (size_t)row * H;
+#pragma unroll
+  for (int c = 0; c < kNormChunks; ++c) {
+    const int ch = tid + c * kWorkerThreads;
+    if (ch < nch) {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(rr) + 2 * ch);
+      const float4 b = __ldcg(reinterpret_cast<const float4*>(rr) + 2 * ch + 1);
+      v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
+      v[c][4] = b.x; v[c][5] = b.y; v[c][6] = b.z; v[c][7] = b.w;
+      if (T.n_delta) {
+        uint4 dv[kMaxDeltas];
+        for (int i = 0; i < T.n_delta; ++i)
+          dv[i] = __ldcg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)T.dl[i] + (size_t)row * H) + ch);
+        for (int i = 0; i < T.n_delta; ++i) {
+          const uint4 d = dv[i];
+          v[c][0] += bf16lo(d.x); v[c][1] += bf16hi(d.x);
+          v[c][2] += bf16lo(d.y); v[c][3] += bf16hi(d.y);
+          v[c][4] += bf16lo(d.z); v[c][5] += bf16hi(d.z);
+          v[c][6] += bf16lo(d.w); v[c][7] += bf16hi(d.w);
+        }
+        reinterpret_cast<float4*>(rr)[2 * ch] = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
+        reinterpret_cast<float4*>(rr)[2 * ch + 1] = make_float4(v[c][4], v[c][5], v[c][6], v[c][7]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss += v[c][j] * v[c][j];
+    }
+  }
+  ss = warp_sum(ss);
+  if ((tid & 31) == 0) S.red[tid >> 5] = ss;
+  named_bar(kBarW, kWorkerThreads);
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < kWorkers; ++w) tot += S.red[w];
+  const float inv = rsqrtf(tot / (float)H + T.eps);
+#pragma unroll
+  for (int c = 0; c < kNormChunks; ++c) {
+    const int ch = tid + c * kWorkerThreads;
+    if (ch < nch) {
+      const uint4 gg = gm[c];
+      uint4 o;
+      o.x = pack_bf16(v[c][0] * inv * bf16lo(gg.x), v[c][1] * inv * bf16hi(gg.x));
+      o.y = pack_bf16(v[c][2] * inv * bf16lo(gg.y), v[c][3] * inv * bf16hi(gg.y));
+      o.z = pack_bf16(v[c][4] * inv * bf16lo(gg.z), v[c][5] * inv * bf16hi(gg.z));
+      o.w = pack_bf16(v[c][6] * inv * bf16lo(gg.w), v[c][7] * inv * bf16hi(gg.w));
+      reinterpret_cast<uint4*>(hout)[(size_t)row * nch + ch] = o;
+    }
+  }
+  named_bar(kBarW, kWorkerThreads);  // S.red reuse + every store before the release
+}
+
+// a5 on one (row, 8-head group) with 128 threads: rope_append_kernel's math
+__device__ void rope_unit(const Task& T, int b, int y, int t128) {
+  const int Hq = T.Hq, Hkv = T.Hkv, D = T.D, page = T.page, half = D / 2, G = Hq / Hkv;
+  const int hh = y * 8 + (t128 >> 4), t16 = t128 & 15;
+  const int n_rot = Hq + Hkv;
+  const __nv_bfloat16* qkv = (const __nv_bfloat16*)T.a0;
+  const int32_t* bt = (const int32_t*)T.a1;
+  const int32_t* sl = (const int32_t*)T.a2;
+  __nv_bfloat16* q_out = (__nv_bfloat16*)T.o0;
+  __nv_bfloat16* kc = (__nv_bfloat16*)T.o1;
+  __nv_bfloat16* vc = (__nv_bfloat16*)T.o2;
+  if (hh < n_rot && t16 * 8 < half) {
+    const int i0 = t16 * 8;
+    const int pos = __ldg(sl + b) - 1;
+    const __nv_bfloat16* src = qkv + (size_t)b * (Hq + 2 * Hkv) * D;
+    const __nv_bfloat16* x;
+    __nv_bfloat16* dst;
+    if (hh < Hq) {
+      const int g = hh / G, j = hh % G;
+      x = src + (size_t)g * (G + 2) * D + (size_t)j * D;
+      dst = q_out + (size_t)b * Hq * D + (size_t)hh * D;
+    } else {
+      const int g = hh - Hq, slot = pos - T.slot_offset;
+      const int32_t pg = __ldg(bt + (size_t)b * T.pps + slot / page);
+      x = src + (size_t)g * (G + 2) * D + (size_t)G * D;
+      dst = kc + (((size_t)pg * Hkv + g) * page + slot % page) * D;
+    }
+    const uint4 xa = __ldcg(reinterpret_cast<const uint4*>(x + i0));
+    const uint4 xb = __ldcg(reinterpret_cast<const uint4*>(x + half + i0));
+    float cs[8], sn[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double ang = (double)pos * T.freq[i0 + k];
+      const double kk = rint(ang * 0.15915494309189535);
+      const double red = fma(-kk, 6.283185307179586, fma(-kk, 2.4492935982947064e-16, ang));
+      sincosf((float)red, &sn[k], &cs[k]);
+    }
+    const uint32_t* pa = &xa.x;
+    const uint32_t* pb = &xb.x;
+    uint4 lo, hi;
+    uint32_t* plo = &lo.x;
+    uint32_t* phi = &hi.x;
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const float x0 = bf16lo(pa[qq]), x1 = bf16hi(pa[qq]), y0 = bf16lo(pb[qq]), y1 = bf16hi(pb[qq]);
+      const float c0 = cs[2 * qq], c1 = cs[2 * qq + 1], s0 = sn[2 * qq], s1 = sn[2 * qq + 1];
+      plo[qq] = pack_bf16(x0 * c0 - y0 * s0, x1 * c1 - y1 * s1);
+      phi[qq] = pack_bf16(y0 * c0 + x0 * s0, y1 * c1 + x1 * s1);
+    }
+    *reinterpret_cast<uint4*>(dst + i0) = lo;
+    *reinterpret_cast<uint4*>(dst + half + i0) = hi;
+  } else if (hh >= n_rot && hh < n_rot + Hkv) {
+    const int g = hh - n_rot;
+    const int slot = __ldg(sl + b) - 1 - T.slot_offset;
+    const int32_t pg = __ldg(bt + (size_t)b * T.pps + slot / page);
+    const __nv_bfloat16* x = qkv + (size_t)b * (Hq + 2 * Hkv) * D + (size_t)g * (G + 2) * D + (size_t)(G + 1) * D;
+    __nv_bfloat16* dst = vc + (((size_t)pg * Hkv + g) * page + slot % page) * D;
+    for (int c8 = t16 * 8; c8 < D; c8 += 128)
+      *reinterpret_cast<uint4*>(dst + c8) = __ldcg(reinterpret_cast<const uint4*>(x + c8));
+  }
+}
+
+// attention consumers (worker w): pages t ≡ w (mod 8) of every item, slot (base + t) mod A
+template <int D>
+__device__ void cons_attn(const Task& T, const Sm& S, const Geo& g, unsigned* err, unsigned& ak, unsigned& ci,
+                          int& apos, uint32_t& apar) {
+  constexpr int KS = D / 16;
+  constexpr int SLAB_B = kPage * D * 2;
+  const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) - kW0;
+  const int gid = lane >> 2, c4 = lane & 3;
+  const int mi = lane >> 3, r8 = lane & 7;
+  const int k_tok = ((mi & 1) << 3) + r8, k_dc = mi >> 1;
+  const int v_tok = ((mi >> 1) << 3) + r8, v_dc = mi & 1;
+  const int Gq = T.G;
+  const int32_t* sl = (const int32_t*)T.a2;
+  for (;;) {
+    const int is = (int)(ak & 3u);
+    mwait_sleep(&S.ifull[is], (ak >> 2) & 1u, err, S);
+    const int it = S.s_item[is];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.iempty[is]);
+    ++ak;
+    if (it < 0) break;
+    const int split = it % T.splits, b = (it / T.splits) % T.rows;
+    const int len = __ldg(sl + b) - T.slot_offset;
+    const int p0 = split * T.pps_split;
+    const int np = max(0, min((len + kPage - 1) / kPage, p0 + T.pps_split) - p0);
+    const int base = (apos + 7) / 8 * 8 % g.A;
+    uint32_t qb[KS][2];
+    {
+      const int qs = (int)(ci & 1u);
+      mwait(&S.qfull[qs], (ci >> 1) & 1u, err, S);
+      const uint32_t* qh = reinterpret_cast<const uint32_t*>(S.qsm + (size_t)qs * g.Gm * D + gid * D);
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+        qb[s][0] = gid < Gq ? qh[8 * s + c4] : 0u;
+        qb[s][1] = gid < Gq ? qh[8 * s + 4 + c4] : 0u;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.qempty[qs]);
+    }
+    float o[KS][4];
+#pragma unroll
+    for (int j = 0; j < KS; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    for (int j = w; j < np; j += kWorkers) {
+      const int st = (base + j) % g.A;
+      const uint32_t bit = 1u << (st >> 3);
+      mwait(&S.afull[st], (apar & bit) ? 1u : 0u, err, S);
+      apar ^= bit;
+      uint8_t* slot = S.arena + (size_t)st * kSlot;
+      const uint32_t kt = smem_u32(slot), vt = kt + SLAB_B;
+      const int tok0 = (p0 + j) * kPage;
+      const int valid = min(kPage, len - tok0);
+      if (valid < kPage) {  // zero the V rows past the end (0·garbage must not be NaN)
+        uint4* vrow = reinterpret_cast<uint4*>(slot + SLAB_B + valid * D * 2);
+        for (int e = lane; e < (kPage - valid) * D / 8; e += 32) vrow[e] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+      }
+      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(kt + tile_off<D>(s >> 2, k_tok, ((s & 3) << 1) + k_dc), a0, a1, a2, a3);
+        if (s & 1)
+          mma16816(sb, a0, a1, a2, a3, qb[s][0], qb[s][1]);
+        else
+          mma16816(sa, a0, a1, a2, a3, qb[s][0], qb[s][1]);
+      }
+      float sv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sv[i] = (sa[i] + sb[i]) * T.scale_log2;
+      if (gid >= valid) sv[0] = sv[1] = -INFINITY;
+      if (gid + 8 >= valid) sv[2] = sv[3] = -INFINITY;
+      float mx0 = fmaxf(sv[0], sv[2]), mx1 = fmaxf(sv[1], sv[3]);
+#pragma unroll
+      for (int x = 4; x < 32; x <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, x));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, x));
+      }
+      const float mn0 = fmaxf(m_run[0], mx0), mn1 = fmaxf(m_run[1], mx1);
+      const float mu0 = (mn0 == -INFINITY) ? 0.f : mn0, mu1 = (mn1 == -INFINITY) ? 0.f : mn1;
+      const float al0 = exp2f(m_run[0] - mu0), al1 = exp2f(m_run[1] - mu1);
+      const float p0v = exp2f(sv[0] - mu0), p1v = exp2f(sv[1] - mu1);
+      const float p2v = exp2f(sv[2] - mu0), p3v = exp2f(sv[3] - mu1);
+      l_run[0] = l_run[0] * al0 + (p0v + p2v);
+      l_run[1] = l_run[1] * al1 + (p1v + p3v);
+      m_run[0] = mn0;
+      m_run[1] = mn1;
+#pragma unroll
+      for (int mb = 0; mb < KS; ++mb) {
+        o[mb][0] *= al0;
+        o[mb][1] *= al1;
+        o[mb][2] *= al0;
+        o[mb][3] *= al1;
+      }
+      const uint32_t pb0 = movm_t(pack_bf16(p0v, p1v));
+      const uint32_t pb1 = movm_t(pack_bf16(p2v, p3v));
+#pragma unroll
+      for (int mb = 0; mb < KS; ++mb) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(vt + tile_off<D>(mb >> 2, v_tok, ((mb & 3) << 1) + v_dc), a0, a1, a2, a3);
+        mma16816(o[mb], a0, a1, a2, a3, pb0, pb1);
+      }
+      // (the zeroing stores above were generic-proxy writes into a slot the
+      // TMA overwrites next: order them before the release)
+      if (valid < kPage) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.aempty[st]);
+    }
+    apos = (base + np) % g.A;
+#pragma unroll
+    for (int x = 4; x < 32; x <<= 1) {
+      l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], x);
+      l_run[1] += __shfl_xor_sync(0xffffffffu, l_run[1], x);
+    }
+    if (ci >= 1) mwait_sleep(S.cempty, (ci - 1u) & 1u, err, S);
+    float* cw = S.comb + (size_t)w * g.Gm * D;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int h = 2 * c4 + hh;
+      if (h < Gq) {
+#pragma unroll
+        for (int mb = 0; mb < KS; ++mb) {
+          cw[h * D + 16 * mb + gid] = o[mb][hh];
+          cw[h * D + 16 * mb + gid + 8] = o[mb][2 + hh];
+        }
+        if (gid == 0) {
+          S.comb_ml[(w * g.Gm + h) * 2 + 0] = m_run[hh];
+          S.comb_ml[(w * g.Gm + h) * 2 + 1] = l_run[hh];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(S.cfull);
+    ++ci;
+  }
+}
+
+// attention merge warp: 8 warp states (fixed order) → output or split partial;
+// the last split of a (sequence, kv head) unit merges the splits (fixed order)
+__device__ void merge_attn(const Task& T, int t, const Sm& S, const Geo& g, unsigned* done, unsigned ep, unsigned* err,
+                           unsigned& ak, unsigned& ci) {
+  const int lane = threadIdx.x & 31;
+  const int Gq = T.G, D = T.D;
+  __nv_bfloat16* out = (__nv_bfloat16*)T.o0;
+  const bool single = T.splits == 1;
+  for (;;) {
+    const int is = (int)(ak & 3u);
+    mwait_sleep(&S.ifull[is], (ak >> 2) & 1u, err, S);
+    const int it = S.s_item[is];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.iempty[is]);
+    ++ak;
+    if (it < 0) break;
+    const int split = it % T.splits, unit = it / T.splits;
+    const int gh = unit / T.rows, b = unit % T.rows;
+    mwait_sleep(S.cfull, ci & 1u, err, S);
+    for (int x = lane; x < kWorkers * Gq; x += 32) {
+      const int w = x / Gq, h = x % Gq;
+      float M = -INFINITY;
+      for (int x = 0; x < kWorkers; ++x) M = fmaxf(M, S.comb_ml[(x * g.Gm + h) * 2]);
+      const float Mu = (M == -INFINITY) ? 0.f : M;
+      float L = 0.f;
+      for (int x = 0; x < kWorkers; ++x) L += exp2f(S.comb_ml[(x * g.Gm + h) * 2] - Mu) * S.comb_ml[(x * g.Gm + h) * 2 + 1];
+      S.s_w[w * kMaxG + h] = exp2f(S.comb_ml[(w * g.Gm + h) * 2] - Mu);
+      if (w == 0) S.s_M[h] = M, S.s_L[h] = L;
+    }
+    __syncwarp();
+    for (int e4 = lane; e4 < Gq * D / 4; e4 += 32) {
+      const int h = (e4 * 4) / D, d0 = (e4 * 4) % D;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < kWorkers; ++w) {
+        const float sc = S.s_w[w * kMaxG + h];
+        const float4 v = *reinterpret_cast<const float4*>(S.comb + ((size_t)w * g.Gm + h) * D + d0);
+        acc.x += sc * v.x, acc.y += sc * v.y, acc.z += sc * v.z, acc.w += sc * v.w;
+      }
+      const float L = S.s_L[h];
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+      acc.x *= inv, acc.y *= inv, acc.z *= inv, acc.w *= inv;
+      if (single) {
+        uint2 pk;
+        pk.x = pack_bf16(acc.x, acc.y);
+        pk.y = pack_bf16(acc.z, acc.w);
+        *reinterpret_cast<uint2*>(out + (size_t)b * T.Hq * D + (size_t)(gh * Gq + h) * D + d0) = pk;
+      } else {
+        const size_t pi = (((size_t)unit * T.splits + split) * Gq + h);
+        *reinterpret_cast<float4*>(T.part + pi * D + d0) = acc;
+        if (d0 == 0) T.part_lse[pi] = L > 0.f ? S.s_M[h] + log2f(L) : -INFINITY;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(S.cempty);
+    ++ci;
+    bool fin = single;
+    if (!single) {
+      fence_acq_rel_gpu();  // every lane: its partial stores before lane 0's release
+      __syncwarp();
+      unsigned prev = 0;
+      if (lane == 0) prev = atom_add_acq_rel_gpu(T.ctr + unit, 1u);
+      fin = __shfl_sync(0xffffffffu, prev, 0) + 1u == (ep + 1u) * (unsigned)T.splits;
+      if (fin) {
+        fence_acq_rel_gpu();
+        const float* lse = T.part_lse + (size_t)unit * T.splits * Gq;
+        const float* po = T.part + (size_t)unit * T.splits * Gq * D;
+        const int nl = T.splits * Gq;
+        if (nl <= kFastSplitLse) {
+          for (int i = lane; i < nl; i += 32) S.s_lse[i] = __ldcg(lse + i);
+          __syncwarp();
+          if (lane < Gq) {
+            float M = -INFINITY;
+            for (int sp = 0; sp < T.splits; ++sp) M = fmaxf(M, S.s_lse[sp * Gq + lane]);
+            const float Mu = (M == -INFINITY) ? 0.f : M;
+            float L = 0.f;
+            for (int sp = 0; sp < T.splits; ++sp) L += exp2f(S.s_lse[sp * Gq + lane] - Mu);
+            S.s_M[lane] = Mu, S.s_L[lane] = L;
+          }
+          __syncwarp();
+          for (int e4 = lane; e4 < Gq * D / 4; e4 += 32) {
+            const int h = (e4 * 4) / D, d0 = (e4 * 4) % D;
+            const float Mu = S.s_M[h];
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            int sp = 0;
+            for (; sp + kFastSplits <= T.splits; sp += kFastSplits) {
+              float4 v[kFastSplits];
+#pragma unroll
+              for (int u = 0; u < kFastSplits; ++u)
+                v[u] = __ldcg(reinterpret_cast<const float4*>(po + ((size_t)(sp + u) * Gq + h) * D + d0));
+#pragma unroll
+              for (int u = 0; u < kFastSplits; ++u) {
+                const float sc = exp2f(S.s_lse[(sp + u) * Gq + h] - Mu);
+                acc.x += sc * v[u].x, acc.y += sc * v[u].y, acc.z += sc * v[u].z, acc.w += sc * v[u].w;
+              }
+            }
+            for (; sp < T.splits; ++sp) {
+              const float sc = exp2f(S.s_lse[sp * Gq + h] - Mu);
+              const float4 v = __ldcg(reinterpret_cast<const float4*>(po + ((size_t)sp * Gq + h) * D + d0));
+              acc.x += sc * v.x, acc.y += sc * v.y, acc.z += sc * v.z, acc.w += sc * v.w;
+            }
+            const float L = S.s_L[h];
+            const float inv = L > 0.f ? 1.f / L : 0.f;
+            acc.x *= inv, acc.y *= inv, acc.z *= inv, acc.w *= inv;
+            uint2 pk;
+            pk.x = pack_bf16(acc.x, acc.y);
+            pk.y = pack_bf16(acc.z, acc.w);
+            *reinterpret_cast<uint2*>(out + (size_t)b * T.Hq * D + (size_t)(gh * Gq + h) * D + d0) = pk;
+          }
+        } else {
+          if (lane == 0) report(S, err, 6u, 0u, 0u);  // host guarantees splits·G ≤ kFastSplitLse
+        }
+      }
+    }
+    if (fin) {
+      fence_acq_rel_gpu();
+      __syncwarp();
+      if (lane == 0) red_rel_gpu(done + t, 1u);
+    }
+  }
+}
+
+// ================================================================== the kernel
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    mega_kernel(const Task* __restrict__ tasks, const __grid_constant__ Geo g, uint8_t* __restrict__ ctrl,
+                unsigned* __restrict__ done, unsigned* __restrict__ err) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  Sm S;
+  S.arena = smem;
+  S.qsm = (__nv_bfloat16*)(smem + g.off_q);
+  S.comb = (float*)(smem + g.off_comb);
+  S.comb_ml = (float*)(smem + g.off_ml);
+  uint64_t* bars = (uint64_t*)(smem + g.off_bar);
+  S.gfull = bars;
+  S.gempty = S.gfull + kMaxStages;
+  S.afull = S.gempty + kMaxStages;
+  S.aempty = S.afull + kMaxSlots;
+  S.tfull = S.aempty + kMaxSlots;
+  S.tempty = S.tfull + 2;
+  S.qfull = S.tempty + 2;
+  S.qempty = S.qfull + 2;
+  S.ifull = S.qempty + 2;
+  S.iempty = S.ifull + 4;
+  S.cfull = S.iempty + 4;
+  S.cempty = S.cfull + 1;
+  uint8_t* misc = smem + g.off_misc;
+  S.s_item = (int*)misc;                      // 16 B
+  S.bcast = (unsigned*)(misc + 16);           // 16 B
+  S.red = (float*)(misc + 32);                // 32 B
+  S.tmem_slot = (uint32_t*)(misc + 64);       // 16 B
+  S.sstate = misc + 80;                       // 32 B
+  S.s_w = (float*)(misc + 112);               // [8][8]
+  S.s_M = S.s_w + kWorkers * kMaxG;           // [8]
+  S.s_L = S.s_M + kMaxG;                      // [8]
+  S.s_lse = S.s_L + kMaxG;                    // [128]
+  __shared__ unsigned s_ep;
+  __shared__ int s_cur[kWarps];
+  S.cur = s_cur;
+  S.abortp = (unsigned*)(ctrl + 8);
+  S.rec = (unsigned*)(ctrl + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kMaxStages; ++i) mbar_init(&S.gfull[i], 1), mbar_init(&S.gempty[i], 1);
+    for (int i = 0; i < kMaxSlots; ++i) mbar_init(&S.afull[i], 1), mbar_init(&S.aempty[i], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S.tfull[i], 1);
+      mbar_init(&S.tempty[i], kWorkers);
+      mbar_init(&S.qfull[i], 1);
+      mbar_init(&S.qempty[i], kWorkers);
+    }
+    for (int i = 0; i < 4; ++i) mbar_init(&S.ifull[i], 1), mbar_init(&S.iempty[i], kWorkers + 1);
+    mbar_init(S.cfull, kWorkers);
+    mbar_init(S.cempty, 1);
+    for (int s = 0; s < kMaxSlots; ++s) S.sstate[s] = 0;
+    for (int w = 0; w < kWarps; ++w) s_cur[w] = -1;
+    s_ep = *(volatile unsigned*)ctrl;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
+                 "r"(2 * kAccCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *S.tmem_slot;
+  const unsigned ep = s_ep;
+  const int Gr = (int)gridDim.x, c = blockIdx.x;
+
+  // role state (each role keeps only its own; all advance identically)
+  unsigned gs = 0, pc = 0, ak = 0, ci = 0;
+  int apos = 0;
+  uint32_t apar = 0;
+  if (warp == kLoader) {
+    for (int t = 0; t < g.n_tasks; ++t) {
+      const Task& T = tasks[t];
+      if (lane == 0) s_cur[warp] = t;
+      if (T.kind == MK_GEMM) load_gemm(T, S, g, done, ep, err, gs);
+      else if (T.kind == MK_ATTN) load_attn(T, S, g, done, ep, err, ak, ci, apos);
+      __syncwarp();
+    }
+  } else if (warp == kMma) {
+    for (int t = 0; t < g.n_tasks; ++t) {
+      const Task& T = tasks[t];
+      if (lane == 0) s_cur[warp] = t;
+      if (T.kind == MK_GEMM) mma_gemm(T, S, g, tmem, err, gs, pc);
+    }
+  } else if (warp == kMerge) {
+    for (int t = 0; t < g.n_tasks; ++t) {
+      const Task& T = tasks[t];
+      if (lane == 0) s_cur[warp] = t;
+      if (T.kind == MK_ATTN) merge_attn(T, t, S, g, done, ep, err, ak, ci);
+    }
+  } else if (warp >= kW0) {
+    const int wt = threadIdx.x - kW0 * 32;
+    for (int t = 0; t < g.n_tasks; ++t) {
+      const Task& T = tasks[t];
+      if (lane == 0) s_cur[warp] = t;
+      switch (T.kind) {
+        case MK_GEMM: epi_gemm(T, t, S, done, ep, tmem, err, pc); break;
+        case MK_ATTN: cons_attn<D>(T, S, g, err, ak, ci, apos, apar); break;
+        case MK_NORM:
+        case MK_SILU:
+        case MK_RESID: {
+          bool waited = false;
+          const int first = ((c - T.rot) % Gr + Gr) % Gr;
+          for (int u = first; u < T.n_units; u += Gr) {
+            if (!waited) {
+              if (wt == 0) deps_wait(T, done, ep, err, S);
+              named_bar(kBarW, kWorkerThreads);
+              waited = true;
+            }
+            if (T.kind == MK_NORM) {
+              norm_row(T, S, u);
+            } else if (T.kind == MK_SILU) {
+              const size_t n = (size_t)T.M * (T.N / 8);
+              const size_t e8 = (size_t)u * kWorkerThreads + wt;
+              if (e8 < n) {
+                const int F = T.N;
+                const size_t row = e8 / (F / 8), i8 = e8 % (F / 8);
+                const int j = (int)(i8 / 8), i = (int)(i8 % 8) * 8;
+                const __nv_bfloat16* gp = (const __nv_bfloat16*)T.a0 + row * 2 * F + 128 * j + i;
+                const uint4 gv = __ldcg(reinterpret_cast<const uint4*>(gp));
+                const uint4 uv = __ldcg(reinterpret_cast<const uint4*>(gp + 64));
+                const uint32_t* gq = &gv.x;
+                const uint32_t* uq = &uv.x;
+                uint4 o;
+                uint32_t* op = &o.x;
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                  const float g0 = bf16lo(gq[qq]), g1 = bf16hi(gq[qq]);
+                  op[qq] = pack_bf16(silu_fast(g0) * bf16lo(uq[qq]), silu_fast(g1) * bf16hi(uq[qq]));
+                }
+                reinterpret_cast<uint4*>(T.o0)[e8] = o;
+              }
+              named_bar(kBarW, kWorkerThreads);
+            } else {  // residual add
+              const size_t i = (size_t)u * kWorkerThreads + wt;
+              if (i < (size_t)T.K) {
+                float* r = (float*)T.o0;
+                float4 a = __ldcg(reinterpret_cast<const float4*>(r) + 2 * i);
+                float4 b = __ldcg(reinterpret_cast<const float4*>(r) + 2 * i + 1);
+                for (int k = 0; k < T.n_delta; ++k) {
+                  const uint4 x = __ldcg(reinterpret_cast<const uint4*>(T.dl[k]) + i);
+                  a.x += bf16lo(x.x); a.y += bf16hi(x.x); a.z += bf16lo(x.y); a.w += bf16hi(x.y);
+                  b.x += bf16lo(x.z); b.y += bf16hi(x.z); b.z += bf16lo(x.w); b.w += bf16hi(x.w);
+                }
+                reinterpret_cast<float4*>(r)[2 * i] = a;
+                reinterpret_cast<float4*>(r)[2 * i + 1] = b;
+              }
+              named_bar(kBarW, kWorkerThreads);
+            }
+            if (wt == 0) signal_done(done, t);
+          }
+          break;
+        }
+        case MK_ROPE: {
+          // two 128-thread halves, units alternate between them
+          const int hf = wt >> 7, t128 = wt & 127;
+          const int ny = (T.Hq + 2 * T.Hkv + 7) / 8;
+          bool waited = false;
+          const int first = ((c - T.rot) % Gr + Gr) % Gr;
+          int k = 0;
+          for (int u = first; u < T.n_units; u += Gr, ++k) {
+            if ((k & 1) != hf) continue;
+            if (!waited) {
+              if (t128 == 0) deps_wait(T, done, ep, err, S);
+              named_bar(kBarHalf0 + hf, 128);
+              waited = true;
+            }
+            rope_unit(T, u / ny, u % ny, t128);
+            named_bar(kBarHalf0 + hf, 128);
+            if (t128 == 0) signal_done(done, t);
+          }
+          break;
+        }
+        default: break;
+      }
+    }
+  }
+  // ---- end of step: every role is done; the last CTA out advances the epoch
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == kMma) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kAccCols));
+  }
+  if (threadIdx.x == 0) {
+    fence_acq_rel_gpu();
+    unsigned* ex = (unsigned*)(ctrl + 4);
+    const unsigned prev = atom_add_acq_rel_gpu(ex, 1u);
+    if (prev + 1u == (ep + 1u) * (unsigned)Gr) {
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"((unsigned*)ctrl), "r"(ep + 1u) : "memory");
+    }
+  }
+}
+
+}  // namespace mega
+
+// ================================================================== host side
+struct MegaPlan {
+  std::vector<mega::Task> tasks;
+  mega::Geo geo{};
+  int D = 0;
+  size_t smem = 0;
+  int grid = 0;
+  // workspace layout (bytes)
+  uint64_t off_ctrl = 0, off_done = 0, off_tick = 0, off_ctr = 0, off_freq = 0, off_tasks = 0, off_gpart = 0,
+           off_apart = 0, total = 0;
+  uint64_t gpart_bytes = 0, apart_bytes = 0;
+  std::vector<uint64_t> ctr_off;  // per task: offset of its counters within the counter region
+  std::vector<int> gpar, apar;    // scratch parity per task (-1 none)
+  std::vector<double> freq;       // concatenated RoPE tables
+  std::vector<int> freq_off;      // per task (doubles)
+  std::vector<MegaOpDesc> ops;
+  uint8_t* ws = nullptr;
+  unsigned* err = nullptr;
+  bool bound = false;
+};
+
+namespace {
+
+struct Range {
+  uintptr_t a, b;
+};
+bool overlap(const std::vector<Range>& x, const std::vector<Range>& y) {
+  for (const auto& p : x)
+    for (const auto& q : y)
+      if (p.a < q.b && q.a < p.b) return true;
+  return false;
+}
+
+template <typename T>
+T get_attr(const MegaOpDesc& o) {
+  T a;
+  std::memcpy(&a, o.attrs.data(), sizeof(T));
+  return a;
+}
+
+}  // namespace
+
+kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64_t* ws_bytes) {
+  using namespace mega;
+  int dev = 0;
+  KD_CUDA_CHECK(cudaGetDevice(&dev), "cudaGetDevice");
+  int sms = 0;
+  KD_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+  auto* P = new MegaPlan();
+  P->ops = ops;
+  P->grid = sms;
+  const int n = (int)ops.size();
+  if (n == 0) {
+    delete P;
+    return fail(KD_ERR_INVALID_ARG, "megakernel: empty schedule");
+  }
+  P->tasks.resize(n);
+  P->ctr_off.assign(n, 0);
+  P->gpar.assign(n, -1);
+  P->apar.assign(n, -1);
+  P->freq_off.assign(n, -1);
+  int D = 0, Gm = 1, maxM = 0;
+  uint64_t ctr_words = 0;
+  int last_g[2] = {-1, -1}, last_a[2] = {-1, -1}, ng = 0, na = 0;
+  std::vector<std::vector<int>> extra(n);  // scratch-reuse guards
+  auto bad = [&](const std::string& m) {
+    delete P;
+    return fail(KD_ERR_UNSUPPORTED, "megakernel: " + m);
+  };
+  int rot = 0;
+  for (int t = 0; t < n; ++t) {
+    const MegaOpDesc& o = ops[t];
+    Task& T = P->tasks[t];
+    std::memset(&T, 0, sizeof(T));
+    T.rot = rot % sms;
+    switch (o.op) {
+      case KD_OP_ADD_RMSNORM: {
+        auto a = get_attr<kd_attr_add_rmsnorm>(o);
+        if (a.dtype != KD_BF16 || a.hidden % 8 || a.hidden > 8 * kWorkerThreads * kNormChunks) return bad("add_rmsnorm shape/dtype");
+        T.kind = MK_NORM;
+        T.M = a.rows, T.N = a.hidden, T.eps = a.eps;
+        T.n_delta = a.n_delta;
+        for (uint32_t i = 0; i < a.n_delta; ++i) T.dl[i] = o.rd[1 + i];
+        T.a1 = o.rd[1 + a.n_delta];
+        T.o0 = o.wr[0];
+        T.o1 = o.wr[1];
+        T.n_units = a.rows;
+        T.done_units = a.rows;
+        break;
+      }
+      case KD_OP_RESIDUAL_ADD: {
+        auto a = get_attr<kd_attr_residual_add>(o);
+        if (a.dtype != KD_BF16 || a.hidden % 8) return bad("residual_add shape/dtype");
+        T.kind = MK_RESID;
+        T.K = (int)((uint64_t)a.rows * a.hidden / 8);
+        T.n_delta = a.n_delta;
+        for (uint32_t i = 0; i < a.n_delta; ++i) T.dl[i] = o.rd[1 + i];
+        T.o0 = o.wr[0];
+        T.n_units = (T.K + kWorkerThreads - 1) / kWorkerThreads;
+        T.done_units = T.n_units;
+        break;
+      }
+      case KD_OP_SILU_MUL: {
+        auto a = get_attr<kd_attr_silu_mul>(o);
+        if (a.dtype != KD_BF16 || a.ffn % 64) return bad("silu_mul shape/dtype");
+        T.kind = MK_SILU;
+        T.M = a.rows, T.N = a.ffn;
+        T.a0 = o.rd[0];
+        T.o0 = o.wr[0];
+        const uint64_t n8 = (uint64_t)a.rows * a.ffn / 8;
+        T.n_units = (int)((n8 + kWorkerThreads - 1) / kWorkerThreads);
+        T.done_units = T.n_units;
+        break;
+      }
+      case KD_OP_ROPE_APPEND: {
+        auto a = get_attr<kd_attr_rope_append>(o);
+        if (a.dtype != KD_BF16 || a.head_dim % 16 || a.head_dim > 256 || a.n_heads % a.n_kv_heads)
+          return bad("rope_append shape/dtype");
+        T.kind = MK_ROPE;
+        T.Hq = a.n_heads, T.Hkv = a.n_kv_heads, T.D = a.head_dim, T.page = a.page, T.pps = a.pages_per_seq;
+        T.slot_offset = a.slot_offset;
+        T.a0 = o.rd[0], T.a1 = o.rd[1], T.a2 = o.rd[2];
+        T.o0 = o.wr[0], T.o1 = o.wr[1], T.o2 = o.wr[2];
+        const int ny = (int)((a.n_heads + 2 * a.n_kv_heads + 7) / 8);
+        T.n_units = a.rows * ny;
+        T.done_units = T.n_units;
+        P->freq_off[t] = (int)P->freq.size();
+        const double l2t = std::log2(a.theta);
+        for (uint32_t i = 0; i < a.head_dim / 2; ++i) P->freq.push_back(std::exp2(-2.0 * (double)i / (double)a.head_dim * l2t));
+        break;
+      }
+      case KD_OP_GEMM: {
+        auto a = get_attr<kd_attr_gemm>(o);
+        if (a.dtype != KD_BF16) return bad("fp32 GEMM");
+        if (a.M == 0 || a.M > 128 || a.K % 128 || a.N % 8) return bad("GEMM shape (M <= 128, K % 128 == 0, N % 8 == 0)");
+        T.kind = MK_GEMM;
+        T.M = a.M, T.N = a.N, T.K = a.K;
+        T.mma_n = (a.M + 15) / 16 * 16;
+        T.kbs = 2;
+        T.KB = a.K / 128;
+        T.tiles = (a.N + 127) / 128;
+        const long long U = (long long)T.tiles * T.KB;
+        T.gg = (int)std::min<long long>(sms, U);
+        int maxc = 0;
+        for (int tl = 0; tl < T.tiles; ++tl)
+          maxc = std::max(maxc, (int)(uowner((long long)(tl + 1) * T.KB - 1, U, T.gg) - uowner((long long)tl * T.KB, U, T.gg) + 1));
+        T.maxc = maxc;
+        T.n_units = (int)U;
+        T.done_units = T.tiles;
+        T.a0 = o.rd[0];  // X
+        T.a1 = o.rd[1];  // W
+        T.o0 = o.wr[0];
+        maxM = std::max(maxM, T.mma_n);
+        P->ctr_off[t] = ctr_words;
+        ctr_words += T.tiles;
+        const int p = ng++ & 1;
+        P->gpar[t] = p;
+        if (last_g[p] >= 0) extra[t].push_back(last_g[p]);
+        last_g[p] = t;
+        P->gpart_bytes = std::max<uint64_t>(P->gpart_bytes, (uint64_t)T.tiles * maxc * a.M * 128 * 4);
+        break;
+      }
+      case KD_OP_ATTENTION: {
+        auto a = get_attr<kd_attr_attention>(o);
+        if (a.dtype != KD_BF16 || (a.head_dim != 64 && a.head_dim != 128) || a.page != kPage || a.flags ||
+            a.n_heads % a.n_kv_heads || a.n_heads / a.n_kv_heads > kMaxG)
+          return bad("attention shape/dtype/flags");
+        if (D && D != (int)a.head_dim) return bad("one head_dim per megakernel");
+        D = a.head_dim;
+        T.kind = MK_ATTN;
+        T.Hq = a.n_heads, T.Hkv = a.n_kv_heads, T.D = a.head_dim, T.G = a.n_heads / a.n_kv_heads, T.pps = a.pages_per_seq;
+        T.rows = a.rows;
+        T.page = kPage;
+        Gm = std::max(Gm, T.G);
+        const long units = (long)a.rows * a.n_kv_heads;
+        int splits = (int)std::max<long>(1, (8L * sms + units - 1) / units);
+        if (const char* e = getenv("KD_MEGA_SPLITS")) splits = std::max(1, atoi(e));
+        splits = std::min(splits, std::max(1, (int)a.pages_per_seq / 16));
+        splits = std::min(splits, kFastSplitLse / T.G);
+        int ppsp = ((int)a.pages_per_seq + splits - 1) / splits;
+        splits = ((int)a.pages_per_seq + ppsp - 1) / ppsp;
+        T.splits = splits;
+        T.pps_split = ppsp;
+        T.n_units = (int)(units * splits);
+        T.n_dyn = std::max(0, T.n_units - sms);
+        T.done_units = (unsigned)units;
+        T.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)a.head_dim));
+        T.a0 = o.rd[0];  // q
+        T.a1 = o.rd[3];  // block table
+        T.a2 = o.rd[4];  // seq_len
+        T.o0 = o.wr[0];
+        P->ctr_off[t] = ctr_words;
+        ctr_words += units + 1;  // unit arrivals + ticket
+        const int p = na++ & 1;
+        P->apar[t] = p;
+        if (last_a[p] >= 0) extra[t].push_back(last_a[p]);
+        last_a[p] = t;
+        if (splits > 1) P->apart_bytes = std::max<uint64_t>(P->apart_bytes, (uint64_t)units * splits * T.G * (a.head_dim + 1) * 4);
+        break;
+      }
+      default:
+        return bad("op " + std::to_string(o.op) + " has no megakernel task (dense decoder ops only)");
+    }
+    rot += (T.kind == MK_GEMM || T.kind == MK_ATTN) ? 0 : T.n_units;
+  }
+  if (!D) D = 128;
+  // ---- dependencies: conflicting declared spans (RAW / WAR / WAW), + scratch guards
+  std::vector<std::vector<Range>> R(n), W(n);
+  for (int t = 0; t < n; ++t) {
+    for (size_t i = 0; i < ops[t].rd.size(); ++i)
+      R[t].push_back({(uintptr_t)ops[t].rd[i], (uintptr_t)ops[t].rd[i] + ops[t].rd_len[i]});
+    for (size_t i = 0; i < ops[t].wr.size(); ++i)
+      W[t].push_back({(uintptr_t)ops[t].wr[i], (uintptr_t)ops[t].wr[i] + ops[t].wr_len[i]});
+  }
+  const int nw = (n + 63) / 64;
+  std::vector<std::vector<uint64_t>> anc(n, std::vector<uint64_t>(nw, 0));
+  for (int t = 0; t < n; ++t) {
+    std::vector<int> cand = extra[t];
+    for (int s = 0; s < t; ++s)
+      if (overlap(W[s], R[t]) || overlap(W[s], W[t]) || overlap(R[s], W[t])) cand.push_back(s);
+    std::sort(cand.begin(), cand.end());
+    cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+    std::vector<int> kept;
+    for (int i = (int)cand.size() - 1; i >= 0; --i) {
+      const int s = cand[i];
+      if (anc[t][s / 64] >> (s % 64) & 1) continue;  // implied by a later kept dependency
+      kept.push_back(s);
+      for (int x = 0; x < nw; ++x) anc[t][x] |= anc[s][x];
+      anc[t][s / 64] |= 1ull << (s % 64);
+    }
+    if ((int)kept.size() > kMaxDep) return bad("a task with more than 8 direct dependencies");
+    Task& T = P->tasks[t];
+    T.n_dep = (int)kept.size();
+    for (int i = 0; i < T.n_dep; ++i) {
+      T.dep[i] = kept[i];
+      T.dep_units[i] = P->tasks[kept[i]].done_units;
+    }
+  }
+  // ---- geometry (shared memory)
+  int SPS = 0;
+  if (maxM) SPS = (2 * 16384 + 2 * maxM * 128 + kSlot - 1) / kSlot;
+  const size_t fixed = (size_t)2 * Gm * D * 2 + (size_t)kWorkers * Gm * D * 4 + (size_t)kWorkers * Gm * 2 * 4 +
+                       (2 * kMaxStages + 2 * kMaxSlots + 24) * 8 + 1024 + 1024;
+  int smem_max = 0;
+  KD_CUDA_CHECK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem opt-in");
+  int NS = std::min<int>(kMaxSlots, (int)(((size_t)smem_max - fixed) / kSlot));
+  Geo& g = P->geo;
+  g.NS = NS;
+  g.SPS = SPS ? SPS : 1;
+  g.NG = SPS ? std::min(kMaxStages, NS / SPS) : 1;
+  g.A = NS / 8 * 8;
+  if ((SPS && g.NG < 2) || g.A < 8) return bad("not enough shared memory for the arena");
+  g.n_tasks = n;
+  g.Gm = Gm;
+  size_t off = (size_t)NS * kSlot;
+  g.off_q = (uint32_t)off;
+  off += (size_t)2 * Gm * D * 2;
+  off = (off + 15) / 16 * 16;
+  g.off_comb = (uint32_t)off;
+  off += (size_t)kWorkers * Gm * D * 4;
+  g.off_ml = (uint32_t)off;
+  off += (size_t)kWorkers * Gm * 2 * 4;
+  off = (off + 7) / 8 * 8;
+  g.off_bar = (uint32_t)off;
+  off += (2 * kMaxStages + 2 * kMaxSlots + 24) * 8;
+  g.off_misc = (uint32_t)off;
+  off += 112 + (kWorkers * kMaxG + 2 * kMaxG + kFastSplitLse) * 4;
+  P->smem = off + 1024;  // + alignment slack
+  if (P->smem > (size_t)smem_max) return bad("shared memory layout exceeds the opt-in limit");
+  P->D = D;
+  // ---- workspace layout
+  uint64_t w = 0;
+  auto take = [&](uint64_t bytes) {
+    const uint64_t o2 = w;
+    w = (w + bytes + 255) / 256 * 256;
+    return o2;
+  };
+  P->off_ctrl = take(256);
+  P->off_done = take((uint64_t)n * 4);
+  P->off_ctr = take(ctr_words * 4 + 4);
+  P->off_freq = take(P->freq.size() * 8 + 8);
+  P->off_tasks = take((uint64_t)n * sizeof(Task));
+  P->off_gpart = take(2 * P->gpart_bytes);
+  P->off_apart = take(2 * P->apart_bytes);
+  P->total = w;
+  auto fn = D == 64 ? mega_kernel<64> : mega_kernel<128>;
+  KD_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem), "mega smem attr");
+  int occ = 0;
+  KD_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, P->smem), "mega occupancy");
+  if (occ < 1) return bad("the megakernel does not fit one SM");
+  *out = P;
+  *ws_bytes = P->total;
+  return KD_OK;
+}
+
+kd_status mega_bind(MegaPlan* P, void* ws, uint64_t bytes, unsigned* err) {
+  using namespace mega;
+  if (!P || !ws) return fail(KD_ERR_INVALID_ARG, "megakernel: NULL workspace");
+  if (bytes < P->total) return fail(KD_ERR_OOM, "megakernel: workspace too small");
+  if ((uintptr_t)ws & 255) return fail(KD_ERR_INVALID_ARG, "megakernel: workspace needs 256-byte alignment");
+  uint8_t* b = (uint8_t*)ws;
+  P->ws = b;
+  P->err = err;
+  const int n = (int)P->tasks.size();
+  for (int t = 0; t < n; ++t) {
+    Task& T = P->tasks[t];
+    const MegaOpDesc& o = P->ops[t];
+    if (T.kind == MK_GEMM) {
+      T.ctr = (unsigned*)(b + P->off_ctr) + P->ctr_off[t];
+      T.part = (float*)(b + P->off_gpart + (uint64_t)P->gpar[t] * P->gpart_bytes);
+      kd_status s = encode_bf16_2d_sw128(&T.tm0, o.rd[1], T.K, T.N, 64, 128);
+      if (s) return s;
+      s = encode_bf16_2d_sw128(&T.tm1, o.rd[0], T.K, T.M, 64, T.mma_n);
+      if (s) return s;
+    } else if (T.kind == MK_ATTN) {
+      T.ctr = (unsigned*)(b + P->off_ctr) + P->ctr_off[t];
+      T.ticket = T.ctr + (uint64_t)T.rows * T.Hkv;
+      T.part = (float*)(b + P->off_apart + (uint64_t)P->apar[t] * P->apart_bytes);
+      T.part_lse = T.part + (uint64_t)T.rows * T.Hkv * T.splits * T.G * T.D;
+      const uint64_t dims[3] = {64, (uint64_t)T.D / 64u, 1ull << 30};
+      const uint64_t strides[2] = {128, (uint64_t)T.D * 2u};
+      const uint32_t box[3] = {64, (uint32_t)T.D / 64u, (uint32_t)kPage};
+      kd_status s = encode_bf16_sw128(&T.tm0, o.rd[1], 3, dims, strides, box);
+      if (s) return s;
+      s = encode_bf16_sw128(&T.tm1, o.rd[2], 3, dims, strides, box);
+      if (s) return s;
+    } else if (T.kind == MK_ROPE) {
+      T.freq = (const double*)(b + P->off_freq) + P->freq_off[t];
+    }
+  }
+  KD_CUDA_CHECK(cudaMemset(b, 0, P->off_tasks), "megakernel: zero counters");
+  if (!P->freq.empty())
+    KD_CUDA_CHECK(cudaMemcpy(b + P->off_freq, P->freq.data(), P->freq.size() * 8, cudaMemcpyHostToDevice), "freq upload");
+  KD_CUDA_CHECK(cudaMemcpy(b + P->off_tasks, P->tasks.data(), (size_t)n * sizeof(Task), cudaMemcpyHostToDevice),
+                "task upload");
+  P->bound = true;
+  return KD_OK;
+}
+
+kd_status mega_launch(MegaPlan* P, cudaStream_t s) {
+  using namespace mega;
+  if (!P || !P->bound) return fail(KD_ERR_STATE, "megakernel: workspace not set");
+  auto fn = P->D == 64 ? mega_kernel<64> : mega_kernel<128>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P->grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = P->smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // every CTA resident (in-kernel waits)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const Task* tasks = (const Task*)(P->ws + P->off_tasks);
+  KD_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tasks, P->geo, P->ws + P->off_ctrl, (unsigned*)(P->ws + P->off_done), P->err),
+                "megakernel launch");
+  return KD_OK;
+}
+
+void mega_destroy(MegaPlan* P) { delete P; }
+
+kd_status mega_diag(const MegaPlan* P, std::string* what) {
+  if (!P || !P->bound) return KD_OK;
+  unsigned rec[8] = {};
+  KD_CUDA_CHECK(cudaMemcpy(rec, P->ws + P->off_ctrl + 16, sizeof rec, cudaMemcpyDeviceToHost), "read megakernel record");
+  if (!rec[7]) return KD_OK;
+  static const char* kinds[] = {"?", "norm", "gemm", "rope", "attention", "silu", "residual"};
+  const int t = (int)rec[4];
+  const char* kind = (t >= 0 && t < (int)P->tasks.size() && P->tasks[t].kind <= 6) ? kinds[P->tasks[t].kind] : "?";
+  char buf[256];
+  snprintf(buf, sizeof buf, "megakernel %s timed out: CTA %u warp %u lane %u, task %d (%s), words %u %u",
+           rec[0] == 4 ? "dependency wait" : rec[0] == 5 ? "pipeline (mbarrier) wait" : "split merge", rec[1], rec[2],
+           rec[3], t, kind, rec[5], rec[6]);
+  *what = buf;
+  return KD_OK;
+}
+
+kd_status mega_info(const MegaPlan* P, uint32_t* n_tasks, uint32_t* smem, uint32_t* grid) {
+  if (!P) return fail(KD_ERR_INVALID_ARG, "megakernel: NULL plan");
+  if (n_tasks) *n_tasks = (uint32_t)P->tasks.size();
+  if (smem) *smem = (uint32_t)P->smem;
+  if (grid) *grid = (uint32_t)P->grid;
+  return KD_OK;
+}
+
+}  // namespace kd

@@ -42,6 +42,10 @@ struct DevState {
   cudaGraphExec_t exec = nullptr;
   bool captured = false;
   cudaEvent_t st0 = nullptr, st1 = nullptr;  // kd_step_stats
+  MegaPlan* mega = nullptr;                  // KD_EXEC_MEGAKERNEL
+  uint64_t mega_bytes = 0;
+  void* mega_ws = nullptr;                   // caller-owned (kd_runtime_set_exec_workspace)
+  uint64_t mega_ws_bytes = 0;
 };
 
 }  // namespace kd
@@ -53,6 +57,7 @@ struct kd_runtime {
   std::map<std::tuple<uint32_t, uint32_t, uint32_t>, void*> bind;  // (buf, micro, dev)
   std::map<std::tuple<uint32_t, uint32_t, uint32_t>, void*> peer_bind;  // replicas of remote devices (IPC-mapped)
   uint32_t mode = KD_MODE_DISAGG;
+  uint32_t exec = KD_EXEC_GRAPH;
   bool use_graph = true;
   bool prepared = false;
   uint32_t profile_op = 0;
@@ -66,6 +71,7 @@ struct kd_runtime {
       if (d.exec) cudaGraphExecDestroy(d.exec);
       if (d.st0) cudaEventDestroy(d.st0);
       if (d.st1) cudaEventDestroy(d.st1);
+      mega_destroy(d.mega);
       for (auto& l : d.launches) {
         delete l.gemm;
         if (l.ev0) cudaEventDestroy(l.ev0);
@@ -676,9 +682,86 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
       }
       d.launches.push_back(std::move(l));
     }
+    mega_destroy(d.mega);
+    d.mega = nullptr;
+    d.mega_bytes = 0;
+    if (rt->exec == KD_EXEC_MEGAKERNEL) {
+      std::vector<MegaOpDesc> ops;
+      for (const auto& l : d.launches) {
+        if (l.kind != Launch::KERNEL || l.ctx.epi.n || l.ctx.acq.n)
+          return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: the megakernel runs single-device schedules only "
+                                          "(device " + std::to_string(d.logical) + " has cross-device transfers)");
+        if (l.op == KD_OP_NONE) continue;
+        const Kernel& K = g->kernels[l.kernel];
+        MegaOpDesc o;
+        o.op = l.op;
+        o.attrs = K.attrs;
+        o.rd = l.rd;
+        o.wr = l.wr;
+        for (const auto& sp : K.reads) o.rd_len.push_back(sp.len);
+        for (const auto& sp : K.writes) o.wr_len.push_back(sp.len);
+        ops.push_back(std::move(o));
+      }
+      kd_status s = mega_create(ops, &d.mega, &d.mega_bytes);
+      if (s) return s;
+      if (d.mega_ws && d.mega_ws_bytes >= d.mega_bytes) {
+        KD_CUDA_CHECK(cudaMemset(d.mega_ws, 0, d.mega_bytes), "zero megakernel workspace");
+        s = mega_bind(d.mega, d.mega_ws, d.mega_ws_bytes, (unsigned*)(d.ws + L.ctrl_off + 4));
+        if (s) return s;
+      }
+    }
   }
   rt->prepared = true;
   return KD_OK;
+}
+
+kd_status kd_runtime_set_exec(kd_runtime* rt, uint32_t exec) {
+  if (!rt || exec > KD_EXEC_MEGAKERNEL) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_exec: bad argument");
+  if (rt->exec != exec) {
+    rt->exec = exec;
+    rt->prepared = false;
+    for (auto& d : rt->devs) d.captured = false;
+  }
+  return KD_OK;
+}
+
+kd_status kd_runtime_exec_workspace_bytes(kd_runtime* rt, uint32_t dev, uint64_t* bytes) {
+  if (!rt || !bytes) return fail(KD_ERR_INVALID_ARG, "kd_runtime_exec_workspace_bytes: NULL argument");
+  if (rt->exec != KD_EXEC_MEGAKERNEL) return fail(KD_ERR_STATE, "kd_runtime_exec_workspace_bytes: not in KD_EXEC_MEGAKERNEL");
+  if (!rt->prepared) {
+    kd_status s = kd_runtime_prepare(rt);
+    if (s) return s;
+  }
+  for (auto& d : rt->devs)
+    if (d.logical == dev) {
+      *bytes = d.mega_bytes;
+      return KD_OK;
+    }
+  return fail(KD_ERR_INVALID_ARG, "kd_runtime_exec_workspace_bytes: device is not local");
+}
+
+kd_status kd_runtime_set_exec_workspace(kd_runtime* rt, uint32_t dev, void* dev_ptr, uint64_t bytes) {
+  if (!rt || !dev_ptr) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_exec_workspace: NULL argument");
+  if ((uintptr_t)dev_ptr & 255) return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_exec_workspace: need 256-byte alignment");
+  for (auto& d : rt->devs)
+    if (d.logical == dev) {
+      d.mega_ws = dev_ptr;
+      d.mega_ws_bytes = bytes;
+      if (rt->prepared && d.mega) {
+        if (bytes < d.mega_bytes) return fail(KD_ERR_OOM, "kd_runtime_set_exec_workspace: workspace too small");
+        KD_CUDA_CHECK(cudaSetDevice(d.cuda), "cudaSetDevice");
+        KD_CUDA_CHECK(cudaMemset(dev_ptr, 0, d.mega_bytes), "zero megakernel workspace");
+        return mega_bind(d.mega, dev_ptr, bytes, (unsigned*)(d.ws + rt->plan->layout[d.logical].ctrl_off + 4));
+      }
+      return KD_OK;
+    }
+  return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_exec_workspace: device is not local");
+}
+
+kd_status kd_runtime_exec_info(kd_runtime* rt, uint32_t j, uint32_t* n_tasks, uint32_t* smem_bytes, uint32_t* grid) {
+  if (!rt || j >= rt->devs.size()) return fail(KD_ERR_INVALID_ARG, "kd_runtime_exec_info: bad argument");
+  if (!rt->prepared || !rt->devs[j].mega) return fail(KD_ERR_STATE, "kd_runtime_exec_info: no prepared megakernel");
+  return mega_info(rt->devs[j].mega, n_tasks, smem_bytes, grid);
 }
 
 kd_status kd_step(kd_runtime* rt, void* const* streams, uint64_t step_id, kd_step_stats* stats) {
@@ -702,7 +785,11 @@ kd_status kd_step(kd_runtime* rt, void* const* streams, uint64_t step_id, kd_ste
       }
       KD_CUDA_CHECK(cudaEventRecord(d.st0, s), "event record");
     }
-    if (!rt->use_graph) {
+    if (rt->exec == KD_EXEC_MEGAKERNEL) {
+      if (!d.mega) return fail(KD_ERR_STATE, "kd_step: megakernel not prepared");
+      kd_status st = mega_launch(d.mega, s);
+      if (st) return st;
+    } else if (!rt->use_graph) {
       for (auto& l : d.launches) {
         kd_status st = enqueue(rt, d, l, s, false);
         if (st) return st;
@@ -816,11 +903,22 @@ kd_status kd_runtime_check(kd_runtime* rt) {
   for (auto& d : rt->devs) {
     KD_CUDA_CHECK(cudaSetDevice(d.cuda), "cudaSetDevice");
     KD_CUDA_CHECK(cudaDeviceSynchronize(), "device synchronize");
+    if (d.mega) {
+      std::string what;
+      kd_status s = mega_diag(d.mega, &what);
+      if (s) return s;
+      if (!what.empty()) return fail(KD_ERR_TIMEOUT, "kd_runtime_check: " + what + " on device " + std::to_string(d.logical));
+    }
     unsigned err = 0;
     KD_CUDA_CHECK(cudaMemcpy(&err, d.ws + rt->plan->layout[d.logical].ctrl_off + 4, 4, cudaMemcpyDeviceToHost),
                   "read error word");
     if (err) {
-      const char* what = err == 2 ? "an in-kernel grid barrier" : err == 3 ? "the step-begin barrier" : "a flag wait";
+      const char* what = err == 2   ? "an in-kernel grid barrier"
+                         : err == 3 ? "the step-begin barrier"
+                         : err == 4 ? "a megakernel dependency wait"
+                         : err == 5 ? "a megakernel pipeline wait"
+                         : err == 6 ? "a megakernel split merge"
+                                    : "a flag wait";
       return fail(KD_ERR_TIMEOUT, std::string("kd_runtime_check: ") + what + " timed out on device " +
                                       std::to_string(d.logical));
     }
@@ -831,7 +929,7 @@ kd_status kd_runtime_check(kd_runtime* rt) {
 kd_status kd_runtime_launch_count(const kd_runtime* rt, uint32_t j, uint32_t* n) {
   if (!rt || !n || j >= rt->devs.size()) return fail(KD_ERR_INVALID_ARG, "kd_runtime_launch_count: bad argument");
   if (!rt->prepared) return fail(KD_ERR_STATE, "kd_runtime_launch_count: runtime not prepared");
-  *n = (uint32_t)rt->devs[j].launches.size();
+  *n = rt->exec == KD_EXEC_MEGAKERNEL ? 1u : (uint32_t)rt->devs[j].launches.size();
   return KD_OK;
 }
 

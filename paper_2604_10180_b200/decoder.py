@@ -877,7 +877,7 @@ class DecoderRuntime:
     def __init__(self, dg: DecoderGraph, assign: Sequence[int], n_dev: int, dev_map: Sequence[int],
                  machine: Optional[Machine] = None, inputs=None, seed: int = 0, use_graph: bool = True,
                  local_devs: Optional[Sequence[int]] = None, dist=None, dist_group=None, n_chunks: int = 4,
-                 mode: Optional[int] = None):
+                 mode: Optional[int] = None, megakernel: bool = False):
         """dev_map[logical] = cuda ordinal for every LOCAL logical device.
         local_devs: logical devices driven by this process (default: all,
         single-process / loopback). With `dist` (torch.distributed, one
@@ -936,6 +936,16 @@ class DecoderRuntime:
         for d in self.local_devs:
             torch.cuda.synchronize(self.dev_map[d])
         self.rt.prepare()
+        if megakernel:  # f1: one persistent launch per device per step (own zeroed workspace)
+            self.rt.set_exec(K.KD_EXEC_MEGAKERNEL)
+            self.mega_ws = {}
+            for d in self.local_devs:
+                nbytes = self.rt.exec_workspace_bytes(d)
+                w = torch.zeros(nbytes + 256, dtype=torch.uint8, device=f"cuda:{self.dev_map[d]}")
+                off = (-w.data_ptr()) % 256
+                self.mega_ws[d] = w
+                torch.cuda.synchronize(self.dev_map[d])
+                self.rt.set_exec_workspace(d, w.data_ptr() + off, nbytes)
         self.streams = [torch.cuda.Stream(device=f"cuda:{self.dev_map[d]}") for d in self.local_devs]
 
     # ------------------------------------------------------------------ inputs
