@@ -232,6 +232,7 @@ _PROTOS = {
     "kd_ipc_open": (kd_status, [P, u64, C.POINTER(P)]),
     "kd_ipc_close": (kd_status, [P]),
     "kd_debug_gemm_trace": (kd_status, [P]),
+    "kd_debug_mega_trace": (kd_status, [P, u32, P]),
     "kd_monitor_create": (kd_status, [u64, u32, u32, u32, C.POINTER(P)]),
     "kd_monitor_destroy": (kd_status, [P]),
     "kd_monitor_record": (kd_status, [P, u64, u64, u64]),

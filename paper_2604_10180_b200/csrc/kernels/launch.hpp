@@ -231,6 +231,8 @@ kd_status mega_bind(MegaPlan* p, void* ws, uint64_t bytes, unsigned* err);
 kd_status mega_launch(MegaPlan* p, cudaStream_t s);
 kd_status mega_info(const MegaPlan* p, uint32_t* n_tasks, uint32_t* smem, uint32_t* grid);
 void mega_destroy(MegaPlan* p);
+// debug: per-(task, CTA, role) %globaltimer stamps into buf (nullable: off)
+void mega_set_trace(MegaPlan* p, void* buf);
 // the first in-kernel watchdog record of the megakernel (empty if none)
 kd_status mega_diag(const MegaPlan* p, std::string* what);
 

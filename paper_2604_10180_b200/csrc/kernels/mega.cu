@@ -64,7 +64,7 @@ using mmas::tile_off;
 using mmas::tma_3d;
 
 constexpr int kWarps = 12, kThreads = kWarps * 32;
-constexpr int kLoader = 0, kMma = 1, kMerge = 2, kW0 = 4;  // workers: warps 4..11
+constexpr int kLoader = 0, kMma = 1, kMerge = 2, kLoader2 = 3, kW0 = 4;  // workers: warps 4..11
 constexpr int kWorkers = 8, kWorkerThreads = kWorkers * 32;
 constexpr int kSlot = 8192;   // arena slot: one attention page (K + V slab, D ≤ 128) or 1/SPS GEMM stage
 constexpr int kMaxSlots = 28;
@@ -112,7 +112,18 @@ struct Geo {
   int n_tasks;
   int Gm;              // comb buffers sized for Gm query heads per kv head
   uint32_t off_q, off_comb, off_ml, off_bar, off_misc;  // dynamic smem offsets
+  unsigned long long* trace;  // debug (nullable): [task][CTA][role 4][start, deps, end] %globaltimer
+  int pf;                     // prefetch each task's tensor maps at its start (A/B knob KD_MEGA_PF)
+  int dbg;                    // experiments (KD_MEGA_DBG): 1 consumers skip the math, 2 + loader skips the TMA
 };
+enum Role : int { R_LOAD = 0, R_MMA = 1, R_MERGE = 2, R_WORK = 3 };
+__device__ __forceinline__ void stamp(const Geo& g, int t, int role, int k) {
+  if (g.trace) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    g.trace[(((size_t)t * gridDim.x + blockIdx.x) * 4 + role) * 3 + k] = v;
+  }
+}
 
 // ------------------------------------------------------------------ waits with watchdogs
 // A broken protocol must not hang the box: every spin is bounded (≈ 4 s of
@@ -189,7 +200,8 @@ struct Sm {
   float* comb;         // [8][Gm][D]
   float* comb_ml;      // [8][Gm][2]
   int* s_item;         // [4]
-  uint8_t* sstate;     // loader: per-slot release state
+  int* s_len;          // [4] item ring: context length of the item
+  uint64_t *xg, *xa;   // arena hand-over between the loaders: GEMM stages drained / odd attention slots drained
   float* red;          // [8] norm partial sums
   unsigned* bcast;     // [4]
   float *s_w, *s_M, *s_L, *s_lse;
@@ -236,205 +248,331 @@ __device__ void deps_wait(const Task& T, const unsigned* done, unsigned ep, unsi
   fence_acq_rel_gpu();
 }
 
-// loader slot state bits
-constexpr uint8_t SS_PEND = 1, SS_ATTN = 2, SS_RPAR = 4, SS_APAR = 8;
-
-// loader lane 0: make slots [s0, s0 + n) free (their previous use released)
-__device__ __forceinline__ void claim(const Sm& S, const Geo& g, int s0, int n, unsigned* err) {
-  for (int s = s0; s < s0 + n; ++s) {
-    const uint8_t st = S.sstate[s];
-    if (!(st & SS_PEND)) continue;
-    const unsigned par = (st & SS_RPAR) ? 1u : 0u;
-    if (st & SS_ATTN) {
-      mwait(&S.aempty[s], par, err, S);
-      S.sstate[s] = st & ~SS_PEND;
-    } else {
-      const int q = s / g.SPS;
-      mwait(&S.gempty[q], par, err, S);
-      for (int x = q * g.SPS; x < (q + 1) * g.SPS; ++x)
-        if ((S.sstate[x] & (SS_PEND | SS_ATTN)) == SS_PEND) S.sstate[x] &= ~SS_PEND;
-    }
+// Loader state, all in registers (lane 0 of the loader warp). The arena's
+// slots are used either as GEMM stages (stage q = slots [q·SPS, (q+1)·SPS),
+// round robin) or as attention page slots (round robin, items start on a
+// multiple of 8). Before a slot is refilled, the release of its previous use
+// must have been waited for: masks of the uses whose release is still owed,
+// and the mbarrier parity of that release.
+struct Ld {
+  unsigned gs = 0;         // GEMM stage fills so far (the MMA warp counts the same)
+  int gq = 0;              // next stage
+  unsigned gph = 0;        // use parity of the next fill of stage gq (= (gs / NG) & 1)
+  uint32_t gpend = 0;      // stages whose release is owed
+  uint32_t gpar = 0;       // their release parity
+  uint32_t gslots = 0;     // slots covered by owed stages
+  uint32_t apend = 0;      // attention slots whose release is owed
+  uint32_t apar = 0;       // their release parity
+  uint32_t afill = 0;      // per slot: use parity of its next attention fill
+  int apos = 0;            // next attention slot
+};
+__device__ __forceinline__ uint32_t stage_mask(int q, int SPS) { return ((1u << SPS) - 1u) << (q * SPS); }
+// wait for the owed release of GEMM stage q (if any)
+__device__ __forceinline__ void free_stage(Ld& L, const Sm& S, int q, int SPS, unsigned* err) {
+  if ((L.gpend >> q) & 1u) {
+    mwait(&S.gempty[q], (L.gpar >> q) & 1u, err, S);
+    L.gpend &= ~(1u << q);
+    L.gslots &= ~stage_mask(q, SPS);
+  }
+}
+// wait for every owed attention release among the slots of mask m
+__device__ __forceinline__ void free_attn(Ld& L, const Sm& S, uint32_t m, unsigned* err) {
+  m &= L.apend;
+  L.apend &= ~m;
+  while (m) {
+    const int s = __ffs(m) - 1;
+    mwait(&S.aempty[s], (L.apar >> s) & 1u, err, S);
+    m &= m - 1u;
   }
 }
 
 // ================================================================== loader
-__device__ void load_gemm(const Task& T, const Sm& S, const Geo& g, const unsigned* done, unsigned ep, unsigned* err,
-                          unsigned& gs) {
+__device__ void load_gemm(const Task& T, int t, const Sm& S, const Geo& g, const unsigned* done, unsigned ep, unsigned* err,
+                          Ld& L, unsigned nattn, unsigned& xa_seen) {
   const int lane = threadIdx.x & 31;
-  const long long U = (long long)T.tiles * T.KB;
+  // the secondary loader's odd attention slots are all released (every xa
+  // phase is consumed in order, before the primary re-arms xg: no aliasing)
+  if (lane == 0)
+    for (; xa_seen != nattn; ++xa_seen) mwait(S.xa, xa_seen & 1u, err, S);
+  const int KB = T.KB, gg = T.gg, NG = g.NG, SPS = g.SPS;
+  const long long U = (long long)T.tiles * KB;
   const int c = blockIdx.x;
-  if (c >= T.gg) return;
-  const long long u0 = ubeg(c, U, T.gg), u1 = ubeg(c + 1, U, T.gg);
+  if (c >= gg) return;
+  const long long u0 = ubeg(c, U, gg), u1 = ubeg(c + 1, U, gg);
   const int n = (int)(u1 - u0);
   if (lane != 0 || n <= 0) return;
   const uint64_t pw = policy_evict_first(), px = policy_evict_last();
   const int kbs = T.kbs, xbox = T.mma_n * 128;
   const unsigned tx = (unsigned)(kbs * (16384 + xbox));
-  const int npre = min(g.NG, n);
-  const unsigned gs0 = gs;
-  auto stage_base = [&](int q) { return S.arena + (size_t)q * g.SPS * kSlot; };
-  auto load_x = [&](int q, long long u) {
-    const int kb = (int)(u % T.KB);
-    for (int b = 0; b < kbs; ++b)
-      tma_load_2d(stage_base(q) + kbs * 16384 + b * xbox, &T.tm1, (kb * kbs + b) * 64, 0, &S.gfull[q], px);
+  const int npre = min(NG, n);
+  const CUtensorMap* mw = &T.tm0;
+  const CUtensorMap* mx = &T.tm1;
+  uint8_t* const arena = S.arena;
+  // (tile, k-block) and the ring position advance incrementally: a 64-bit
+  // division is a ~300-cycle subroutine, per stage
+  int tile = (int)(u0 / KB), kb = (int)(u0 % KB);
+  const int kb0 = kb, q0 = L.gq;
+  auto load_x = [&](int qq, int kk) {
+    uint8_t* base = arena + (size_t)qq * SPS * kSlot + kbs * 16384;
+    for (int b = 0; b < kbs; ++b) tma_load_2d(base + b * xbox, mx, (kk * kbs + b) * 64, 0, &S.gfull[qq], px);
   };
   for (int i = 0; i < n; ++i) {
-    const long long u = u0 + i;
-    const int tile = (int)(u / T.KB), kb = (int)(u % T.KB);
-    const int q = (int)(gs % (unsigned)g.NG);
-    const unsigned use = gs / (unsigned)g.NG;
-    claim(S, g, q * g.SPS, g.SPS, err);
+    const int q = L.gq;
+    free_attn(L, S, stage_mask(q, SPS), err);  // (slots last used by attention pages)
+    free_stage(L, S, q, SPS, err);
     mbar_expect_tx(&S.gfull[q], tx);
-    for (int b = 0; b < kbs; ++b)
-      tma_load_2d(stage_base(q) + b * 16384, &T.tm0, (kb * kbs + b) * 64, tile * 128, &S.gfull[q], pw);
-    for (int x = q * g.SPS; x < (q + 1) * g.SPS; ++x)
-      S.sstate[x] = (uint8_t)((S.sstate[x] & SS_APAR) | SS_PEND | ((use & 1u) ? SS_RPAR : 0));
-    ++gs;
+    uint8_t* base = arena + (size_t)q * SPS * kSlot;
+    for (int b = 0; b < kbs; ++b) tma_load_2d(base + b * 16384, mw, (kb * kbs + b) * 64, tile * 128, &S.gfull[q], pw);
+    L.gpend |= 1u << q;
+    L.gpar = (L.gpar & ~(1u << q)) | (L.gph << q);
+    L.gslots |= stage_mask(q, SPS);
     if (i >= npre) {
-      load_x(q, u);
+      load_x(q, kb);
     } else if (i == npre - 1) {
       // weights of the first npre stages are in flight: now wait for the
       // producers of X, then issue the held-back activation boxes
       deps_wait(T, done, ep, err, S);
+      stamp(g, t, R_LOAD, 1);
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      for (int j = 0; j < npre; ++j) load_x((int)((gs0 + j) % (unsigned)g.NG), u0 + j);
+      int qq = q0, kk = kb0;
+      for (int j = 0; j < npre; ++j) {
+        load_x(qq, kk);
+        if (++qq == NG) qq = 0;
+        if (++kk == KB) kk = 0;
+      }
     }
+    ++L.gs;
+    if (++L.gq == NG) L.gq = 0, L.gph ^= 1u;
+    if (++kb == KB) kb = 0, ++tile;
   }
 }
 
-__device__ void load_attn(const Task& T, const Sm& S, const Geo& g, const unsigned* done, unsigned ep, unsigned* err,
-                          unsigned& ak, unsigned& ci, int& apos) {
+// Attention pages are requested by TWO loader warps (a single warp's
+// ~300-cycle dependent issue path per page cannot keep up with HBM): page t
+// of an item goes to slot (base + t) mod A, base and A even, so loader warp 0
+// (the primary: tickets, item ring, query rows, GEMM stages) fills the even
+// slots and warp 3 (the secondary, attention only) the odd ones. The arena
+// changes hands at task-kind boundaries: before an attention task the primary
+// waits for every owed GEMM-stage release and arrives on xg (the secondary
+// waits xg before its first page); after one the secondary waits for every
+// owed odd-slot release and arrives on xa (the primary waits xa before its
+// next GEMM stage).
+template <bool kPrimary>
+__device__ void load_attn(const Task& T, int t, const Sm& S, const Geo& g, const unsigned* done, unsigned ep, unsigned* err,
+                          unsigned& ak, unsigned& ci, Ld& L, unsigned& nattn, unsigned* xa_seen) {
   const int lane = threadIdx.x & 31;
   const int G = (int)gridDim.x, c = blockIdx.x;
-  const int D = T.D, Hkv = T.Hkv, Gq = T.G;
+  const int D = T.D, Hkv = T.Hkv, Gq = T.G, A = g.A, splits = T.splits, rows = T.rows, ppsp = T.pps_split;
+  const int pps = T.pps, Hq = T.Hq, n_dyn = T.n_dyn, n_items = T.n_units, Gm = g.Gm, NG = g.NG;
+  const int soff = T.slot_offset;
   const unsigned slab = (unsigned)(kPage * D * 2);
-  const unsigned per_step = (unsigned)(T.n_dyn + G);
-  uint64_t pol = policy_evict_first();
-  auto fetch = [&]() -> int {
-    unsigned t = 0;
-    if (lane == 0) t = atomicAdd(T.ticket, 1u) - ep * per_step;
-    t = __shfl_sync(0xffffffffu, t, 0);
-    return t < (unsigned)T.n_dyn ? G + (int)t : -1;
-  };
-  auto publish = [&](int it) {
+  const unsigned per_step = (unsigned)(n_dyn + G);
+  unsigned* const ticket = T.ticket;
+  const CUtensorMap* mk = &T.tm0;
+  const CUtensorMap* mv = &T.tm1;
+  const __nv_bfloat16* qg = (const __nv_bfloat16*)T.a0;
+  uint8_t* const arena = S.arena;
+  const uint64_t pol = policy_evict_first();
+  const int32_t* bt = (const int32_t*)T.a1;
+  const int32_t* sl = (const int32_t*)T.a2;
+  const int par = kPrimary ? 0 : 1;
+  // ---- arena hand-over (GEMM stages → attention slots)
+  if (kPrimary) {
+    if (lane == 0) {
+      for (; *xa_seen != nattn; ++*xa_seen) mwait(S.xa, *xa_seen & 1u, err, S);
+      for (int q = 0; q < NG; ++q) free_stage(L, S, q, g.SPS, err);
+      mbar_arrive(S.xg);
+    }
+  } else {
+    if (lane == 0) mwait(S.xg, nattn & 1u, err, S);
+  }
+  __syncwarp();
+  auto publish = [&](int it, int len) {
     if (lane == 0) {
       const int is = (int)(ak & 3u);
       if (ak >= 4) mwait(&S.iempty[is], ((ak >> 2) - 1u) & 1u, err, S);
       S.s_item[is] = it;
+      S.s_len[is] = len;
       mbar_arrive(&S.ifull[is]);
     }
     __syncwarp();
     ++ak;
   };
-  const int32_t* bt = (const int32_t*)T.a1;
-  const int32_t* sl = (const int32_t*)T.a2;
-  int it = c < T.n_units ? c : fetch();
+  auto take = [&](int& len) -> int {  // the secondary reads the item ring
+    const int is = (int)(ak & 3u);
+    mwait(&S.ifull[is], (ak >> 2) & 1u, err, S);
+    const int it = S.s_item[is];
+    len = S.s_len[is];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.iempty[is]);
+    ++ak;
+    return it;
+  };
+  // ticket of the next item: the atomic is issued early and resolved later
+  // (its ~1 µs round trip overlaps the current item's page requests)
+  auto draw = [&]() -> unsigned { return lane == 0 ? atomicAdd(ticket, 1u) : 0u; };
+  auto resolve = [&](unsigned raw) -> int {
+    const unsigned tk = __shfl_sync(0xffffffffu, raw, 0) - ep * per_step;
+    return tk < (unsigned)n_dyn ? G + (int)tk : -1;
+  };
+  int it = -1, len = 0;
+  if (kPrimary) {
+    it = c < n_items ? c : resolve(draw());
+    len = it >= 0 ? __ldg(sl + (it / splits) % rows) - soff : 0;
+  }
   bool first = true;
   for (;;) {
-    publish(it);
-    if (it < 0) break;
-    const int nxt = fetch();
-    const int split = it % T.splits, unit = it / T.splits;
-    const int gh = unit / T.rows, b = unit % T.rows;
-    const int len = __ldg(sl + b) - T.slot_offset;
-    const int p0 = split * T.pps_split;
-    const int np = max(0, min((len + kPage - 1) / kPage, p0 + T.pps_split) - p0);
-    const int base = (apos + 7) / 8 * 8 % g.A;
+    unsigned raw_next = 0;
+    if (kPrimary) {
+      publish(it, len);
+      if (it < 0) break;
+      raw_next = draw();
+    } else {
+      it = take(len);
+      if (it < 0) break;
+    }
+    const int split = it % splits, unit = it / splits;
+    const int gh = unit / rows, b = unit % rows;
+    const int p0 = split * ppsp;
+    const int np = max(0, min((len + kPage - 1) / kPage, p0 + ppsp) - p0);
+    int base = (L.apos + 7) / 8 * 8;
+    if (base >= A) base -= A;
     // pages strictly before the one holding the appended position may be
     // requested before the dependencies (RoPE/append writes only that page)
     const int safe = first ? max(0, min(np, (len - 1) / kPage - p0)) : 0;
-    const int npre = min(safe, g.A);
-    auto issue = [&](int t, int pid) {
-      if (lane == 0) {
-        const int s = (base + t) % g.A;
-        claim(S, g, s, 1, err);
-        const uint8_t st = S.sstate[s];
-        const uint8_t ap = st & SS_APAR;
-        S.sstate[s] = (uint8_t)(SS_PEND | SS_ATTN | (ap ? SS_RPAR : 0) | (ap ? 0 : SS_APAR));
-        const int row = (pid * Hkv + gh) * kPage;
-        uint8_t* dst = S.arena + (size_t)s * kSlot;
-        mbar_expect_tx(&S.afull[s], 2u * slab);
-        tma_3d(dst, &T.tm0, 0, 0, row, &S.afull[s], pol);
-        tma_3d(dst + slab, &T.tm1, 0, 0, row, &S.afull[s], pol);
-      }
-    };
-    // the query rows (RoPE output) go out right after the dependency wait —
-    // before any page beyond the ring, whose slot only frees once the
-    // consumers (which need q) release it
-    bool qdone = false;
-    auto load_q = [&]() {
+    const int npre = min(safe, A);
+    // the primary sends the query rows (RoPE output) right after its
+    // dependency wait — before any page beyond the ring, whose slot only
+    // frees once the consumers (which need q) release it
+    bool qdone = !kPrimary;
+    auto gate = [&]() {
       if (first) {
         if (lane == 0) {
           deps_wait(T, done, ep, err, S);
+          if (kPrimary) stamp(g, t, R_LOAD, 1);
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         first = false;
       }
-      if (lane == 0) {
-        const int qs = (int)(ci & 1u);
-        if (ci >= 2) mwait(&S.qempty[qs], ((ci >> 1) - 1u) & 1u, err, S);
-        mbar_expect_tx(&S.qfull[qs], (unsigned)(Gq * D * 2));
-        bulk_g2s(S.qsm + (size_t)qs * g.Gm * D, (const __nv_bfloat16*)T.a0 + (size_t)b * T.Hq * D + (size_t)gh * Gq * D,
-                 (unsigned)(Gq * D * 2), &S.qfull[qs]);
+      if (kPrimary && !qdone) {
+        if (lane == 0) {
+          const int qs = (int)(ci & 1u);
+          if (ci >= 2) mwait(&S.qempty[qs], ((ci >> 1) - 1u) & 1u, err, S);
+          mbar_expect_tx(&S.qfull[qs], (unsigned)(Gq * D * 2));
+          bulk_g2s(S.qsm + (size_t)qs * Gm * D, qg + (size_t)b * Hq * D + (size_t)gh * Gq * D, (unsigned)(Gq * D * 2),
+                   &S.qfull[qs]);
+        }
+        qdone = true;
       }
       __syncwarp();
-      qdone = true;
     };
+    const int32_t* btr = bt + (size_t)b * pps + p0;
+    int ids = lane < np ? __ldg(btr + lane) : 0;  // this lane's page id, 32-page chunks, one chunk ahead
+    int it_next = -2, len_next = 0;
+    int s = base + par;
     for (int j0 = 0; j0 < np; j0 += 32) {
-      const int j = j0 + lane;
-      const int mine = j < np ? __ldg(bt + (size_t)b * T.pps + p0 + j) : 0;
+      const int cur = ids;
+      if (j0 + 32 < np) ids = j0 + 32 + lane < np ? __ldg(btr + j0 + 32 + lane) : 0;
       const int cnt = min(32, np - j0);
-      for (int t = 0; t < cnt; ++t) {
-        const int pid = __shfl_sync(0xffffffffu, mine, t);
-        if (!qdone && (!first || j0 + t == npre)) load_q();
-        issue(j0 + t, pid);
+      for (int x = par; x < cnt; x += 2) {
+        if (first ? (j0 + x >= npre) : !qdone) gate();
+        const int pid = __shfl_sync(0xffffffffu, cur, x);
+        if (lane == 0) {
+          const uint32_t bit = 1u << s;
+          if (L.apend & bit) mwait(&S.aempty[s], (L.apar >> s) & 1u, err, S);
+          const uint32_t p = (L.afill >> s) & 1u;
+          L.apend |= bit;
+          L.apar = (L.apar & ~bit) | (p << s);
+          L.afill ^= bit;
+          const int row = (pid * Hkv + gh) * kPage;
+          uint8_t* dst = arena + (size_t)s * kSlot;
+          if (g.dbg >= 2) {
+            mbar_arrive(&S.afull[s]);
+          } else {
+            mbar_expect_tx(&S.afull[s], 2u * slab);
+            tma_3d(dst, mk, 0, 0, row, &S.afull[s], pol);
+            tma_3d(dst + slab, mv, 0, 0, row, &S.afull[s], pol);
+          }
+        }
+        s += 2;
+        if (s >= A) s -= A;
+      }
+      if (kPrimary && j0 == 0) {  // next item's ticket and length, well before they are needed
+        it_next = resolve(raw_next);
+        len_next = it_next >= 0 ? __ldg(sl + (it_next / splits) % rows) - soff : 0;
       }
     }
-    if (!qdone) load_q();
-    ++ci;
-    apos = (base + np) % g.A;
-    it = nxt;
+    if (first || !qdone) gate();
+    if (kPrimary) {
+      if (it_next == -2) {
+        it_next = resolve(raw_next);
+        len_next = it_next >= 0 ? __ldg(sl + (it_next / splits) % rows) - soff : 0;
+      }
+      ++ci;
+      it = it_next;
+      len = len_next;
+    }
+    L.apos = base + np;
+    while (L.apos >= A) L.apos -= A;
   }
+  // ---- arena hand-over (odd attention slots → the primary's next GEMM stages)
+  if (!kPrimary && lane == 0) {
+    const uint32_t m = L.apend;
+    L.apend = 0;
+    for (uint32_t x = m; x; x &= x - 1u) {
+      const int s2 = __ffs(x) - 1;
+      mwait(&S.aempty[s2], (L.apar >> s2) & 1u, err, S);
+    }
+    mbar_arrive(S.xa);
+  }
+  __syncwarp();
+  ++nattn;
 }
 
 // ================================================================== MMA issuer
 __device__ void mma_gemm(const Task& T, const Sm& S, const Geo& g, uint32_t tmem, unsigned* err, unsigned& gs,
                          unsigned& pc) {
   const int lane = threadIdx.x & 31;
-  const long long U = (long long)T.tiles * T.KB;
+  const int KB = T.KB, gg = T.gg, NG = g.NG, SPS = g.SPS;
+  const long long U = (long long)T.tiles * KB;
   const int c = blockIdx.x;
-  if (c >= T.gg) return;
-  const long long u0 = ubeg(c, U, T.gg), u1 = ubeg(c + 1, U, T.gg);
+  if (c >= gg) return;
+  const long long u0 = ubeg(c, U, gg), u1 = ubeg(c + 1, U, gg);
   const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T.mma_n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   const int kbs = T.kbs, xbox = T.mma_n * 128;
-  for (long long u = u0; u < u1;) {
-    const int tile = (int)(u / T.KB);
-    const long long pe = min(u1, (long long)(tile + 1) * T.KB);  // piece [u, pe)
+  const uint32_t arena = smem_u32(S.arena);
+  int q = (int)(gs % (unsigned)NG);
+  unsigned ph = (gs / (unsigned)NG) & 1u;
+  int kb = (int)(u0 % KB);
+  const int n = (int)(u1 - u0);
+  for (int i = 0; i < n;) {
+    const int len = min(n - i, KB - kb);  // piece: the rest of this tile within my range
     const unsigned acc = pc & 1u;
     if (pc >= 2) mwait(&S.tempty[acc], ((pc >> 1) - 1u) & 1u, err, S);
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t td = tmem + acc * kAccCols;
-    for (long long v = u; v < pe; ++v) {
-      const int q = (int)(gs % (unsigned)g.NG);
-      mwait(&S.gfull[q], (gs / (unsigned)g.NG) & 1u, err, S);
+    for (int v = 0; v < len; ++v) {
+      mwait(&S.gfull[q], ph, err, S);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (lane == 0) {
-        const uint32_t a = smem_u32(S.arena + (size_t)q * g.SPS * kSlot);
+        const uint32_t a = arena + (uint32_t)(q * SPS * kSlot);
         const uint32_t bx = a + kbs * 16384;
         for (int b = 0; b < kbs; ++b)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             mma_bf16(td, sw128_desc(a + b * 16384 + 32 * k), sw128_desc(bx + b * xbox + 32 * k), idesc,
-                     (v > u || b > 0 || k > 0) ? 1u : 0u);
+                     (v > 0 || b > 0 || k > 0) ? 1u : 0u);
         mma_commit(&S.gempty[q]);
       }
       __syncwarp();
       ++gs;
+      if (++q == NG) q = 0, ph ^= 1u;
     }
     if (lane == 0) mma_commit(&S.tfull[acc]);
     __syncwarp();
     ++pc;
-    u = pe;
+    i += len;
+    kb = 0;
   }
 }
 
@@ -498,18 +636,36 @@ __device__ void epi_gemm(const Task& T, int t, const Sm& S, unsigned* done, unsi
       if (S.bcast[0]) {
         const float* pt = T.part + (size_t)tile * T.maxc * M * 128;
         const int n0 = tile * 128;
-        for (int e = wt; e < M * 32; e += kWorkerThreads) {
-          const int tok = e >> 5, r4 = (e & 31) * 4;
-          if (n0 + r4 >= N) continue;
-          float4 a = __ldcg(reinterpret_cast<const float4*>(pt + (size_t)tok * 128 + r4));
-          for (int k = 1; k < nc; ++k) {
-            const float4 b = __ldcg(reinterpret_cast<const float4*>(pt + ((size_t)k * M + tok) * 128 + r4));
-            a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+        // every partial this thread sums is requested before the first add
+        // (a dependent L2 round trip is ~1 µs here; the fold is the tail of
+        // the GEMM): 2 float4 positions × up to 4 contributors in flight
+        for (int e0 = wt; e0 < M * 32; e0 += 2 * kWorkerThreads) {
+          float4 v[2][4];
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            const int e = e0 + x * kWorkerThreads, tok = e >> 5, r4 = (e & 31) * 4;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (e < M * 32 && k < nc && n0 + r4 < N)
+                v[x][k] = __ldcg(reinterpret_cast<const float4*>(pt + ((size_t)k * M + tok) * 128 + r4));
           }
-          uint2 o;
-          o.x = pack_bf16(a.x, a.y);
-          o.y = pack_bf16(a.z, a.w);
-          *reinterpret_cast<uint2*>(Y + (size_t)tok * N + n0 + r4) = o;
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            const int e = e0 + x * kWorkerThreads, tok = e >> 5, r4 = (e & 31) * 4;
+            if (e >= M * 32 || n0 + r4 >= N) continue;
+            float4 a = v[x][0];
+#pragma unroll
+            for (int k = 1; k < 4; ++k)
+              if (k < nc) a.x += v[x][k].x, a.y += v[x][k].y, a.z += v[x][k].z, a.w += v[x][k].w;
+            for (int k = 4; k < nc; ++k) {  // (more than 4 contributors: rare, sequential)
+              const float4 b2 = __ldcg(reinterpret_cast<const float4*>(pt + ((size_t)k * M + tok) * 128 + r4));
+              a.x += b2.x, a.y += b2.y, a.z += b2.z, a.w += b2.w;
+            }
+            uint2 o;
+            o.x = pack_bf16(a.x, a.y);
+            o.y = pack_bf16(a.z, a.w);
+            *reinterpret_cast<uint2*>(Y + (size_t)tok * N + n0 + r4) = o;
+          }
         }
         named_bar(kBarW, kWorkerThreads);
         if (wt == 0) signal_done(done, t);
@@ -660,7 +816,8 @@ __device__ void cons_attn(const Task& T, const Sm& S, const Geo& g, unsigned* er
   const int mi = lane >> 3, r8 = lane & 7;
   const int k_tok = ((mi & 1) << 3) + r8, k_dc = mi >> 1;
   const int v_tok = ((mi >> 1) << 3) + r8, v_dc = mi & 1;
-  const int Gq = T.G;
+  const int Gq = T.G, A = g.A;
+  const float scale = T.scale_log2;
   const int32_t* sl = (const int32_t*)T.a2;
   for (;;) {
     const int is = (int)(ak & 3u);
@@ -674,7 +831,8 @@ __device__ void cons_attn(const Task& T, const Sm& S, const Geo& g, unsigned* er
     const int len = __ldg(sl + b) - T.slot_offset;
     const int p0 = split * T.pps_split;
     const int np = max(0, min((len + kPage - 1) / kPage, p0 + T.pps_split) - p0);
-    const int base = (apos + 7) / 8 * 8 % g.A;
+    int base = (apos + 7) / 8 * 8;
+    if (base >= A) base -= A;
     uint32_t qb[KS][2];
     {
       const int qs = (int)(ci & 1u);
@@ -692,11 +850,17 @@ __device__ void cons_attn(const Task& T, const Sm& S, const Geo& g, unsigned* er
 #pragma unroll
     for (int j = 0; j < KS; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
     float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
-    for (int j = w; j < np; j += kWorkers) {
-      const int st = (base + j) % g.A;
+    int st = base + w;
+    if (st >= A) st -= A;
+    for (int j = w; j < np; j += kWorkers, st = st + kWorkers >= A ? st + kWorkers - A : st + kWorkers) {
       const uint32_t bit = 1u << (st >> 3);
       mwait(&S.afull[st], (apar & bit) ? 1u : 0u, err, S);
       apar ^= bit;
+      if (g.dbg) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.aempty[st]);
+        continue;
+      }
       uint8_t* slot = S.arena + (size_t)st * kSlot;
       const uint32_t kt = smem_u32(slot), vt = kt + SLAB_B;
       const int tok0 = (p0 + j) * kPage;
@@ -718,7 +882,7 @@ __device__ void cons_attn(const Task& T, const Sm& S, const Geo& g, unsigned* er
       }
       float sv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) sv[i] = (sa[i] + sb[i]) * T.scale_log2;
+      for (int i = 0; i < 4; ++i) sv[i] = (sa[i] + sb[i]) * scale;
       if (gid >= valid) sv[0] = sv[1] = -INFINITY;
       if (gid + 8 >= valid) sv[2] = sv[3] = -INFINITY;
       float mx0 = fmaxf(sv[0], sv[2]), mx1 = fmaxf(sv[1], sv[3]);
@@ -757,7 +921,7 @@ __device__ void cons_attn(const Task& T, const Sm& S, const Geo& g, unsigned* er
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.aempty[st]);
     }
-    apos = (base + np) % g.A;
+    apos = (base + np) % A;  // (once per item)
 #pragma unroll
     for (int x = 4; x < 32; x <<= 1) {
       l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], x);
@@ -933,12 +1097,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   S.iempty = S.ifull + 4;
   S.cfull = S.iempty + 4;
   S.cempty = S.cfull + 1;
+  S.xg = S.cempty + 1;
+  S.xa = S.xg + 1;
   uint8_t* misc = smem + g.off_misc;
   S.s_item = (int*)misc;                      // 16 B
   S.bcast = (unsigned*)(misc + 16);           // 16 B
   S.red = (float*)(misc + 32);                // 32 B
   S.tmem_slot = (uint32_t*)(misc + 64);       // 16 B
-  S.sstate = misc + 80;                       // 32 B
+  S.s_len = (int*)(misc + 80);                // 16 B (+16 spare)
   S.s_w = (float*)(misc + 112);               // [8][8]
   S.s_M = S.s_w + kWorkers * kMaxG;           // [8]
   S.s_L = S.s_M + kMaxG;                      // [8]
@@ -959,10 +1125,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&S.qfull[i], 1);
       mbar_init(&S.qempty[i], kWorkers);
     }
-    for (int i = 0; i < 4; ++i) mbar_init(&S.ifull[i], 1), mbar_init(&S.iempty[i], kWorkers + 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&S.ifull[i], 1), mbar_init(&S.iempty[i], kWorkers + 2);
+    mbar_init(S.xg, 1);
+    mbar_init(S.xa, 1);
     mbar_init(S.cfull, kWorkers);
     mbar_init(S.cempty, 1);
-    for (int s = 0; s < kMaxSlots; ++s) S.sstate[s] = 0;
     for (int w = 0; w < kWarps; ++w) s_cur[w] = -1;
     s_ep = *(volatile unsigned*)ctrl;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -983,31 +1150,47 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned gs = 0, pc = 0, ak = 0, ci = 0;
   int apos = 0;
   uint32_t apar = 0;
+  Ld ld;
+  unsigned nattn = 0, xa_seen = 0;
   if (warp == kLoader) {
     for (int t = 0; t < g.n_tasks; ++t) {
       const Task& T = tasks[t];
-      if (lane == 0) s_cur[warp] = t;
-      if (T.kind == MK_GEMM) load_gemm(T, S, g, done, ep, err, gs);
-      else if (T.kind == MK_ATTN) load_attn(T, S, g, done, ep, err, ak, ci, apos);
+      if (lane == 0) s_cur[warp] = t, stamp(g, t, R_LOAD, 0);
+      if (lane == 0 && g.pf && (T.kind == MK_GEMM || T.kind == MK_ATTN)) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&T.tm0) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&T.tm1) : "memory");
+      }
+      if (T.kind == MK_GEMM) load_gemm(T, t, S, g, done, ep, err, ld, nattn, xa_seen);
+      else if (T.kind == MK_ATTN) load_attn<true>(T, t, S, g, done, ep, err, ak, ci, ld, nattn, &xa_seen);
       __syncwarp();
+      if (lane == 0) stamp(g, t, R_LOAD, 2);
     }
   } else if (warp == kMma) {
     for (int t = 0; t < g.n_tasks; ++t) {
       const Task& T = tasks[t];
-      if (lane == 0) s_cur[warp] = t;
+      if (lane == 0) s_cur[warp] = t, stamp(g, t, R_MMA, 0);
       if (T.kind == MK_GEMM) mma_gemm(T, S, g, tmem, err, gs, pc);
+      if (lane == 0) stamp(g, t, R_MMA, 2);
+    }
+  } else if (warp == kLoader2) {
+    for (int t = 0; t < g.n_tasks; ++t) {
+      const Task& T = tasks[t];
+      if (lane == 0) s_cur[warp] = t;
+      if (T.kind == MK_ATTN) load_attn<false>(T, t, S, g, done, ep, err, ak, ci, ld, nattn, nullptr);
     }
   } else if (warp == kMerge) {
     for (int t = 0; t < g.n_tasks; ++t) {
       const Task& T = tasks[t];
-      if (lane == 0) s_cur[warp] = t;
+      if (lane == 0) s_cur[warp] = t, stamp(g, t, R_MERGE, 0);
       if (T.kind == MK_ATTN) merge_attn(T, t, S, g, done, ep, err, ak, ci);
+      if (lane == 0) stamp(g, t, R_MERGE, 2);
     }
   } else if (warp >= kW0) {
     const int wt = threadIdx.x - kW0 * 32;
     for (int t = 0; t < g.n_tasks; ++t) {
       const Task& T = tasks[t];
       if (lane == 0) s_cur[warp] = t;
+      if (wt == 0) stamp(g, t, R_WORK, 0);
       switch (T.kind) {
         case MK_GEMM: epi_gemm(T, t, S, done, ep, tmem, err, pc); break;
         case MK_ATTN: cons_attn<D>(T, S, g, err, ak, ci, apos, apar); break;
@@ -1018,7 +1201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int first = ((c - T.rot) % Gr + Gr) % Gr;
           for (int u = first; u < T.n_units; u += Gr) {
             if (!waited) {
-              if (wt == 0) deps_wait(T, done, ep, err, S);
+              if (wt == 0) deps_wait(T, done, ep, err, S), stamp(g, t, R_WORK, 1);
               named_bar(kBarW, kWorkerThreads);
               waited = true;
             }
@@ -1076,7 +1259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int u = first; u < T.n_units; u += Gr, ++k) {
             if ((k & 1) != hf) continue;
             if (!waited) {
-              if (t128 == 0) deps_wait(T, done, ep, err, S);
+              if (t128 == 0) deps_wait(T, done, ep, err, S), stamp(g, t, R_WORK, 1);
               named_bar(kBarHalf0 + hf, 128);
               waited = true;
             }
@@ -1088,6 +1271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         default: break;
       }
+      if (wt == 0) stamp(g, t, R_WORK, 2);
     }
   }
   // ---- end of step: every role is done; the last CTA out advances the epoch
@@ -1128,6 +1312,7 @@ struct MegaPlan {
   uint8_t* ws = nullptr;
   unsigned* err = nullptr;
   bool bound = false;
+  unsigned long long* trace = nullptr;
 };
 
 namespace {
@@ -1360,9 +1545,12 @@ kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64
   g.SPS = SPS ? SPS : 1;
   g.NG = SPS ? std::min(kMaxStages, NS / SPS) : 1;
   g.A = NS / 8 * 8;
+  if (const char* e = getenv("KD_MEGA_A")) g.A = std::max(8, std::min(g.A, atoi(e) / 8 * 8));  // A/B knob
   if ((SPS && g.NG < 2) || g.A < 8) return bad("not enough shared memory for the arena");
   g.n_tasks = n;
   g.Gm = Gm;
+  g.pf = getenv("KD_MEGA_PF") ? atoi(getenv("KD_MEGA_PF")) : 1;
+  g.dbg = getenv("KD_MEGA_DBG") ? atoi(getenv("KD_MEGA_DBG")) : 0;
   size_t off = (size_t)NS * kSlot;
   g.off_q = (uint32_t)off;
   off += (size_t)2 * Gm * D * 2;
@@ -1463,12 +1651,17 @@ kd_status mega_launch(MegaPlan* P, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const Task* tasks = (const Task*)(P->ws + P->off_tasks);
+  P->geo.trace = P->trace;
   KD_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, tasks, P->geo, P->ws + P->off_ctrl, (unsigned*)(P->ws + P->off_done), P->err),
                 "megakernel launch");
   return KD_OK;
 }
 
 void mega_destroy(MegaPlan* P) { delete P; }
+
+void mega_set_trace(MegaPlan* P, void* buf) {
+  if (P) P->trace = (unsigned long long*)buf;
+}
 
 kd_status mega_diag(const MegaPlan* P, std::string* what) {
   if (!P || !P->bound) return KD_OK;

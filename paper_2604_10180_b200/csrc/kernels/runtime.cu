@@ -758,6 +758,13 @@ kd_status kd_runtime_set_exec_workspace(kd_runtime* rt, uint32_t dev, void* dev_
   return fail(KD_ERR_INVALID_ARG, "kd_runtime_set_exec_workspace: device is not local");
 }
 
+kd_status kd_debug_mega_trace(kd_runtime* rt, uint32_t j, void* dev_buf) {
+  if (!rt || j >= rt->devs.size()) return fail(KD_ERR_INVALID_ARG, "kd_debug_mega_trace: bad argument");
+  if (!rt->devs[j].mega) return fail(KD_ERR_STATE, "kd_debug_mega_trace: no prepared megakernel");
+  mega_set_trace(rt->devs[j].mega, dev_buf);
+  return KD_OK;
+}
+
 kd_status kd_runtime_exec_info(kd_runtime* rt, uint32_t j, uint32_t* n_tasks, uint32_t* smem_bytes, uint32_t* grid) {
   if (!rt || j >= rt->devs.size()) return fail(KD_ERR_INVALID_ARG, "kd_runtime_exec_info: bad argument");
   if (!rt->prepared || !rt->devs[j].mega) return fail(KD_ERR_STATE, "kd_runtime_exec_info: no prepared megakernel");
