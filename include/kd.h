@@ -507,10 +507,12 @@ kd_status kd_set_pdl(int32_t enable);
  * last commit, per-segment epilogue start/end, fixup start/end, exit) to
  * dev_buf[cta*32 + slot] (u64, >= 148*32 entries). NULL disables (default). */
 kd_status kd_debug_gemm_trace(void* dev_buf);
-/* Debug: KD_EXEC_MEGAKERNEL timeline. dev_buf (device, >= n_tasks·grid·4·3
+/* Debug: KD_EXEC_MEGAKERNEL timeline. dev_buf (device, >= n_tasks·grid·5·4
  * u64, see kd_runtime_exec_info; NULL = off) receives, for every (task, CTA,
  * role ∈ {loader, MMA, merge, workers}), the %globaltimer ns at the role's task
- * start, after its dependency wait (0 if it waited none) and at its end. */
+ * start, after its dependency wait (0 if it waited none) and at its end; role 4
+ * = the GEMM epilogue of the CTA's last piece (TMEM ready, partial published,
+ * all partials present, fold done). */
 kd_status kd_debug_mega_trace(kd_runtime* rt, uint32_t j, void* dev_buf);
 
 /* Tiling the library picks for a plain decode GEMM Y[M,N] = X[M,K]·W[N,K]ᵀ on

@@ -82,6 +82,7 @@ struct alignas(64) Task {
   CUtensorMap tm0;  // GEMM: W [N][K]; ATTN: K cache slabs
   CUtensorMap tm1;  // GEMM: X [M][K]; ATTN: V cache slabs
   int kind;
+  int epi;              // GEMM epilogue: 0 plain bf16 Y, 1 RoPE + KV append (KD_OP_QKV_ROPE), 2 SiLU·mul (KD_OP_GEMM_SILU)
   unsigned done_units;  // completion increments per step
   int n_dep;
   int dep[kMaxDep];
@@ -100,11 +101,13 @@ struct alignas(64) Task {
   int KB, tiles, kbs, mma_n, maxc, gg;  // GEMM: k-blocks per tile, tiles, 64-col boxes per stage, MMA N, contributors bound, CTAs
   unsigned* ctr;                       // GEMM tile arrivals / ATTN unit (split) arrivals
   unsigned* ticket;                    // ATTN item tickets
+  const void* ctr2;                    // GEMM RoPE epilogue: block table
   float* part;                         // GEMM partials [tiles][maxc][M][128] / ATTN part_o
   float* part_lse;                     // ATTN
   int Hq, Hkv, D, G, pps, splits, pps_split, page, n_dyn, rows, slot_offset;
   float scale_log2, eps;
   const double* freq;                  // ROPE θ^(−2i/D)
+  const float2* rtab;                  // GEMM RoPE epilogue: (cos, sin)[row][D/2] of this step
 };
 
 struct Geo {
@@ -115,13 +118,28 @@ struct Geo {
   unsigned long long* trace;  // debug (nullable): [task][CTA][role 4][start, deps, end] %globaltimer
   int pf;                     // prefetch each task's tensor maps at its start (A/B knob KD_MEGA_PF)
   int dbg;                    // experiments (KD_MEGA_DBG): 1 consumers skip the math, 2 + loader skips the TMA
+  int l2pf;                   // GEMM weight stages prefetched into L2 during the dependency wait (KD_MEGA_L2PF)
+  // RoPE (cos, sin) tables, one per distinct (seq_len buffer, rows, D/2, θ):
+  // every CTA computes a slice at kernel start (the step's positions are
+  // fixed for the whole step), tab_ready counts the CTAs that finished
+  int n_tab;
+  const int32_t* tab_sl[4];
+  const double* tab_freq[4];
+  float2* tab[4];
+  int tab_rows[4], tab_half[4];
+  unsigned* tab_ready;
 };
 enum Role : int { R_LOAD = 0, R_MMA = 1, R_MERGE = 2, R_WORK = 3 };
+// trace layout: [task][CTA][role 5][4 stamps]; role R_EPI = the GEMM epilogue
+// of the CTA's last piece: tfull seen, partial stored + arrived, all partials
+// present, fold done
+constexpr int kRoles = 5, kStamps = 4;
+enum { R_EPI = 4 };
 __device__ __forceinline__ void stamp(const Geo& g, int t, int role, int k) {
   if (g.trace) {
     unsigned long long v;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
-    g.trace[(((size_t)t * gridDim.x + blockIdx.x) * 4 + role) * 3 + k] = v;
+    g.trace[(((size_t)t * gridDim.x + blockIdx.x) * kRoles + role) * kStamps + k] = v;
   }
 }
 
@@ -183,9 +201,9 @@ __device__ __forceinline__ void red_rel_gpu(unsigned* p, unsigned v) {
 }
 // publish one completed unit of task t: caller ordered the unit's stores
 // before this thread (bar.sync); the release covers them (cumulativity)
-__device__ __forceinline__ void signal_done(unsigned* done, int t) {
+__device__ __forceinline__ void signal_done(unsigned* done, int t, unsigned units = 1u) {
   fence_acq_rel_gpu();
-  red_rel_gpu(done + t, 1u);
+  red_rel_gpu(done + t, units);
 }
 
 __host__ __device__ __forceinline__ long long ubeg(long long c, long long U, long long G) { return c * U / G; }
@@ -201,6 +219,7 @@ struct Sm {
   float* comb_ml;      // [8][Gm][2]
   int* s_item;         // [4]
   int* s_len;          // [4] item ring: context length of the item
+  int *rpos, *rpg;     // [128] fused-RoPE fold staging
   uint64_t *xg, *xa;   // arena hand-over between the loaders: GEMM stages drained / odd attention slots drained
   float* red;          // [8] norm partial sums
   unsigned* bcast;     // [4]
@@ -329,8 +348,18 @@ __device__ void load_gemm(const Task& T, int t, const Sm& S, const Geo& g, const
     if (i >= npre) {
       load_x(q, kb);
     } else if (i == npre - 1) {
-      // weights of the first npre stages are in flight: now wait for the
-      // producers of X, then issue the held-back activation boxes
+      // weights of the first npre stages are in flight; the HBM would idle
+      // while X's producers finish (their fold / norm chain outlasts the
+      // ring), so the next l2pf stages' weights go to L2 (bulk prefetch),
+      // then wait for the producers of X and issue the held-back X boxes
+      {
+        int tt = tile, kk = kb;
+        const int pf = min(n - npre, g.l2pf);
+        for (int j = 0; j < pf; ++j) {
+          if (++kk == KB) kk = 0, ++tt;
+          for (int b = 0; b < kbs; ++b) gemm::tma_prefetch_2d(mw, (kk * kbs + b) * 64, tt * 128);
+        }
+      }
       deps_wait(T, done, ep, err, S);
       stamp(g, t, R_LOAD, 1);
       asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -530,7 +559,7 @@ __device__ void load_attn(const Task& T, int t, const Sm& S, const Geo& g, const
 }
 
 // ================================================================== MMA issuer
-__device__ void mma_gemm(const Task& T, const Sm& S, const Geo& g, uint32_t tmem, unsigned* err, unsigned& gs,
+__device__ void mma_gemm(const Task& T, int tmark, const Sm& S, const Geo& g, uint32_t tmem, unsigned* err, unsigned& gs,
                          unsigned& pc) {
   const int lane = threadIdx.x & 31;
   const int KB = T.KB, gg = T.gg, NG = g.NG, SPS = g.SPS;
@@ -553,6 +582,7 @@ __device__ void mma_gemm(const Task& T, const Sm& S, const Geo& g, uint32_t tmem
     const uint32_t td = tmem + acc * kAccCols;
     for (int v = 0; v < len; ++v) {
       mwait(&S.gfull[q], ph, err, S);
+      if (g.trace && lane == 0 && i + v == n - 1) stamp(g, tmark, R_MMA, 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (lane == 0) {
         const uint32_t a = arena + (uint32_t)(q * SPS * kSlot);
@@ -576,12 +606,47 @@ __device__ void mma_gemm(const Task& T, const Sm& S, const Geo& g, uint32_t tmem
   }
 }
 
+// fused a5 on the folded QKV tile (KD_OP_QKV_ROPE, weight rows pair-interleaved
+// inside each head: rows n..n+3 = dims p, p + D/2, p + 1, p + 1 + D/2): the
+// per-element arithmetic of rope_append_kernel on the bf16-rounded GEMM output
+__device__ __forceinline__ float rbf(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ void rope_quad_m(const Task& T, const Sm& S, int j, int n, float4 a) {
+  const int D = T.D, half = D / 2, G = T.Hq / T.Hkv;
+  const int hall = n / D, rr = n - hall * D, p = rr >> 1;
+  const int grp = hall / (G + 2), slot = hall - grp * (G + 2);
+  const float xs[2] = {rbf(a.x), rbf(a.z)};
+  const float ys[2] = {rbf(a.y), rbf(a.w)};
+  const int pos = S.rpos[j];
+  __nv_bfloat16 lo[2], hi[2];
+  const float4 csn = __ldcg(reinterpret_cast<const float4*>(T.rtab + (size_t)j * half + p));  // pairs p, p + 1
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (slot <= G) {
+      const float cs = u ? csn.z : csn.x, sn = u ? csn.w : csn.y;
+      lo[u] = __float2bfloat16_rn(xs[u] * cs - ys[u] * sn);
+      hi[u] = __float2bfloat16_rn(ys[u] * cs + xs[u] * sn);
+    } else {
+      lo[u] = __float2bfloat16_rn(xs[u]);
+      hi[u] = __float2bfloat16_rn(ys[u]);
+    }
+  }
+  const __nv_bfloat162 l2 = __halves2bfloat162(lo[0], lo[1]), h2 = __halves2bfloat162(hi[0], hi[1]);
+  __nv_bfloat16* dst;
+  if (slot < G) {
+    dst = (__nv_bfloat16*)T.o0 + ((size_t)j * T.Hq + (size_t)grp * G + slot) * D;
+  } else {
+    dst = (__nv_bfloat16*)(slot == G ? T.o1 : T.o2) + (((size_t)S.rpg[j] * T.Hkv + grp) * T.page + pos % T.page) * D;
+  }
+  *reinterpret_cast<__nv_bfloat162*>(dst + p) = l2;
+  *reinterpret_cast<__nv_bfloat162*>(dst + p + half) = h2;
+}
+
 // ================================================================== workers
 // GEMM epilogue: TMEM → bf16 output (a whole tile) or fp32 partial, and the
 // last contributor of a split tile folds every contributor's partial in
 // contributor order (deterministic) into the bf16 output
-__device__ void epi_gemm(const Task& T, int t, const Sm& S, unsigned* done, unsigned ep, uint32_t tmem, unsigned* err,
-                         unsigned& pc) {
+__device__ void epi_gemm(const Task& T, int t, const Sm& S, const Geo& g, unsigned* done, unsigned ep, uint32_t tmem,
+                         unsigned* err, unsigned& pc, const unsigned* g_tab_ready) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wt = threadIdx.x - kW0 * 32;
   const long long U = (long long)T.tiles * T.KB;
   const int c = blockIdx.x;
@@ -591,84 +656,203 @@ __device__ void epi_gemm(const Task& T, int t, const Sm& S, unsigned* done, unsi
   const int row = q * 32 + lane;
   const int M = T.M, N = T.N;
   __nv_bfloat16* Y = (__nv_bfloat16*)T.o0;
+  if (T.epi == 1) {
+    // fused RoPE: each token's position and page of the appended slot, and the
+    // step's (cos, sin) tables (every CTA computed a slice at kernel start) —
+    // staged while the first piece still streams, off the fold's tail
+    const int32_t* sl = (const int32_t*)T.a2;
+    const int32_t* btp = (const int32_t*)T.ctr2;
+    for (int j = wt; j < M; j += kWorkerThreads) {
+      const int pos = __ldg(sl + j) - 1;
+      S.rpos[j] = pos;
+      S.rpg[j] = __ldg(btp + (size_t)j * T.pps + pos / T.page);
+    }
+    if (wt == 0) {
+      const unsigned target = (ep + 1u) * gridDim.x;
+      for (long long n2 = 0; ld_acq_gpu(g_tab_ready) < target; ++n2) {
+        __nanosleep(32);
+        if (n2 > (1ll << 26)) { report(S, err, 4u, 0xFFFFu, 0u); break; }
+      }
+      fence_acq_rel_gpu();
+    }
+    named_bar(kBarW, kWorkerThreads);
+  }
   for (long long u = u0; u < u1;) {
     const int tile = (int)(u / T.KB);
     const long long tb = (long long)tile * T.KB, te = tb + T.KB;
     const long long pe = min(u1, te);
-    const bool whole = (u == tb && pe == te);
+    const bool whole = (u == tb && pe == te) && T.epi == 0;  // (fused epilogues always go through the fold)
     const unsigned acc = pc & 1u;
     mwait_sleep(&S.tfull[acc], (pc >> 1) & 1u, err, S);
     asm volatile("tcgen05.fence::after_thread_sync;");
+    const bool lastp = pe == u1;
+    if (lastp && wt == 0) stamp(g, t, R_EPI, 0);
     const uint32_t ta = tmem + acc * kAccCols + ((uint32_t)(q * 32) << 16);
     const int n = tile * 128 + row;
     const int f = (int)uowner(tb, U, T.gg);
     const int nc = (int)uowner(te - 1, U, T.gg) - f + 1, cidx = c - f;
-    float* part = T.part + ((size_t)tile * T.maxc + cidx) * (size_t)M * 128;
-    for (int cc = h; cc * 16 < T.mma_n; cc += 2) {
-      uint32_t v[16];
-      tmem_ld16_nowait(ta + cc * 16, v);
+    // partial layout [tile][contributor][weight row][Mp] (Mp = mma_n): a thread
+    // owns one weight row, so its 16-token chunk goes out as 4 × 16-byte stores
+    const int Mp = T.mma_n;
+    float* part = T.part + ((size_t)tile * T.maxc + cidx) * (size_t)Mp * 128 + (size_t)row * Mp;
+    for (int cc0 = h; cc0 * 16 < Mp; cc0 += 2) {
+      uint32_t v[1][16];
+#pragma unroll
+      for (int b = 0; b < 1; ++b)
+        if ((cc0 + 2 * b) * 16 < Mp) tmem_ld16_nowait(ta + (cc0 + 2 * b) * 16, v[b]);
       tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int tok = cc * 16 + j;
-        if (tok < M) {
-          if (whole) {
-            if (n < N) Y[(size_t)tok * N + n] = __float2bfloat16_rn(__uint_as_float(v[j]));
-          } else {
-            part[(size_t)tok * 128 + row] = __uint_as_float(v[j]);
+      for (int b = 0; b < 1; ++b) {
+        const int cc = cc0 + 2 * b;
+        if (cc * 16 >= Mp) continue;
+        if (whole) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int tok = cc * 16 + j;
+            if (tok < M && n < N) Y[(size_t)tok * N + n] = __float2bfloat16_rn(__uint_as_float(v[b][j]));
           }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<uint4*>(part + cc * 16 + j) = make_uint4(v[b][j], v[b][j + 1], v[b][j + 2], v[b][j + 3]);
         }
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.tempty[acc]);
+    if (lastp && wt == 0) stamp(g, t, R_WORK, 1);
     named_bar(kBarW, kWorkerThreads);
     if (whole) {
       if (wt == 0) signal_done(done, t);
+      if (lastp && wt == 0) stamp(g, t, R_EPI, 3);
     } else {
+      // Split tile: every contributor publishes its partial (arrival count).
+      // The contributors whose LAST piece of this task is this tile (all but
+      // possibly the one whose range continues past the tile) then fold one
+      // row slice each, in parallel, once every partial has landed.
+      const int l = f + nc - 1;
+      const bool l_folds = ubeg(l + 1, U, T.gg) == te;
+      const int nf = nc == 1 ? 1 : (l - f) + (l_folds ? 1 : 0);
+      const bool folder = nc == 1 || c < l || l_folds;
       if (wt == 0) {
-        fence_acq_rel_gpu();
-        const unsigned prev = atom_add_acq_rel_gpu(T.ctr + tile, 1u);
-        S.bcast[0] = (prev + 1u == (ep + 1u) * (unsigned)nc) ? 1u : 0u;
-      }
-      named_bar(kBarW, kWorkerThreads);
-      if (S.bcast[0]) {
-        const float* pt = T.part + (size_t)tile * T.maxc * M * 128;
-        const int n0 = tile * 128;
-        // every partial this thread sums is requested before the first add
-        // (a dependent L2 round trip is ~1 µs here; the fold is the tail of
-        // the GEMM): 2 float4 positions × up to 4 contributors in flight
-        for (int e0 = wt; e0 < M * 32; e0 += 2 * kWorkerThreads) {
-          float4 v[2][4];
-#pragma unroll
-          for (int x = 0; x < 2; ++x) {
-            const int e = e0 + x * kWorkerThreads, tok = e >> 5, r4 = (e & 31) * 4;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if (e < M * 32 && k < nc && n0 + r4 < N)
-                v[x][k] = __ldcg(reinterpret_cast<const float4*>(pt + ((size_t)k * M + tok) * 128 + r4));
-          }
-#pragma unroll
-          for (int x = 0; x < 2; ++x) {
-            const int e = e0 + x * kWorkerThreads, tok = e >> 5, r4 = (e & 31) * 4;
-            if (e >= M * 32 || n0 + r4 >= N) continue;
-            float4 a = v[x][0];
-#pragma unroll
-            for (int k = 1; k < 4; ++k)
-              if (k < nc) a.x += v[x][k].x, a.y += v[x][k].y, a.z += v[x][k].z, a.w += v[x][k].w;
-            for (int k = 4; k < nc; ++k) {  // (more than 4 contributors: rare, sequential)
-              const float4 b2 = __ldcg(reinterpret_cast<const float4*>(pt + ((size_t)k * M + tok) * 128 + r4));
-              a.x += b2.x, a.y += b2.y, a.z += b2.z, a.w += b2.w;
+        // (the acq_rel add releases every worker's partial stores: they are
+        // ordered before it by the bar.sync above — cumulativity)
+        atom_add_acq_rel_gpu(T.ctr + tile, 1u);
+        if (lastp) stamp(g, t, R_EPI, 1);
+        if (folder && nc > 1) {  // wait for the other contributors' partials
+          const unsigned target = (ep + 1u) * (unsigned)nc;
+          const long long t0 = clock64();
+          for (unsigned it2 = 0; ld_acq_gpu(T.ctr + tile) < target; ++it2) {
+            __nanosleep(32);
+            if ((it2 & 255u) == 255u && (aborted(S) || clock64() - t0 > kTimeout)) {
+              if (!aborted(S)) report(S, err, 4u, 0x10000u + (unsigned)tile, 0u);
+              break;
             }
-            uint2 o;
-            o.x = pack_bf16(a.x, a.y);
-            o.y = pack_bf16(a.z, a.w);
-            *reinterpret_cast<uint2*>(Y + (size_t)tok * N + n0 + r4) = o;
+          }
+          fence_acq_rel_gpu();
+        }
+      }
+      if (lastp && wt == 0) stamp(g, t, R_EPI, 2);
+      named_bar(kBarW, kWorkerThreads);
+      if (folder) {
+        const float* pt = T.part + (size_t)tile * T.maxc * Mp * 128;
+        const int n0 = tile * 128;
+        const int fi = nc == 1 ? 0 : c - f;
+        if (T.epi == 2) {
+          // SiLU·mul: tile = gate block (rows 0-63) + up block (rows 64-127);
+          // a[tok][64·tile + i] = silu(bf16 g)·bf16 u — silu_mul_kernel's math.
+          // This folder's 4-column groups: [g0, g1) of 16
+          const int F = N / 2;
+          const int g0 = fi * 16 / nf, ng = (fi + 1) * 16 / nf - g0;
+          const int nt4 = (M + 3) / 4;
+          for (int e = wt; e < ng * nt4; e += kWorkerThreads) {
+            const int gi = e / nt4, t4 = (e - gi * nt4) * 4, i4 = (g0 + gi) * 4;
+            float4 ga[4], ua[4];
+            for (int k = 0; k < nc; ++k) {
+              float4 gv[4], uv[4];
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                gv[r] = __ldcg(reinterpret_cast<const float4*>(pt + ((size_t)k * 128 + i4 + r) * Mp + t4));
+                uv[r] = __ldcg(reinterpret_cast<const float4*>(pt + ((size_t)k * 128 + 64 + i4 + r) * Mp + t4));
+              }
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                if (k == 0) {
+                  ga[r] = gv[r], ua[r] = uv[r];
+                } else {
+                  ga[r].x += gv[r].x, ga[r].y += gv[r].y, ga[r].z += gv[r].z, ga[r].w += gv[r].w;
+                  ua[r].x += uv[r].x, ua[r].y += uv[r].y, ua[r].z += uv[r].z, ua[r].w += uv[r].w;
+                }
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int tok = t4 + j;
+              if (tok >= M) break;
+              float gq[4], uq[4];
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                gq[r] = rbf(j == 0 ? ga[r].x : j == 1 ? ga[r].y : j == 2 ? ga[r].z : ga[r].w);
+                uq[r] = rbf(j == 0 ? ua[r].x : j == 1 ? ua[r].y : j == 2 ? ua[r].z : ua[r].w);
+              }
+              uint2 o;
+              o.x = pack_bf16(silu_fast(gq[0]) * uq[0], silu_fast(gq[1]) * uq[1]);
+              o.y = pack_bf16(silu_fast(gq[2]) * uq[2], silu_fast(gq[3]) * uq[3]);
+              *reinterpret_cast<uint2*>(Y + (size_t)tok * F + 64 * tile + i4) = o;
+            }
+          }
+        } else {
+          // this folder's 4-row groups [g0, g1) of 32; a thread folds a 4-row ×
+          // 4-token block (4 float4 per contributor, rows are contiguous in
+          // tokens), contributors in order (deterministic), then emits 4 tokens
+          // × 4 consecutive outputs
+          const int g0 = fi * 32 / nf, ng = (fi + 1) * 32 / nf - g0;
+          const int nt4 = (M + 3) / 4;
+          for (int e = wt; e < ng * nt4; e += kWorkerThreads) {
+            const int gi = e / nt4, t4 = (e - gi * nt4) * 4, r4 = (g0 + gi) * 4;
+            if (n0 + r4 >= N) continue;
+            float4 acc[4];
+            for (int k0 = 0; k0 < nc; k0 += 1) {
+              float4 v[1][4];
+#pragma unroll
+              for (int k = 0; k < 1; ++k)
+                if (k0 + k < nc)
+#pragma unroll
+                  for (int r = 0; r < 4; ++r)
+                    v[k][r] = __ldcg(reinterpret_cast<const float4*>(pt + ((size_t)(k0 + k) * 128 + r4 + r) * Mp + t4));
+#pragma unroll
+              for (int k = 0; k < 1; ++k)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                  if (k0 + k >= nc) continue;
+                  if (k0 + k == 0) acc[r] = v[k][r];
+                  else acc[r].x += v[k][r].x, acc[r].y += v[k][r].y, acc[r].z += v[k][r].z, acc[r].w += v[k][r].w;
+                }
+            }
+            // acc[r] = rows r4 + r at tokens t4..t4+3 → per token the 4 rows
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int tok = t4 + j;
+              if (tok >= M) break;
+              const float4 o4 = j == 0 ? make_float4(acc[0].x, acc[1].x, acc[2].x, acc[3].x)
+                              : j == 1 ? make_float4(acc[0].y, acc[1].y, acc[2].y, acc[3].y)
+                              : j == 2 ? make_float4(acc[0].z, acc[1].z, acc[2].z, acc[3].z)
+                                       : make_float4(acc[0].w, acc[1].w, acc[2].w, acc[3].w);
+              if (T.epi == 1) {
+                rope_quad_m(T, S, tok, n0 + r4, o4);
+              } else {
+                uint2 o;
+                o.x = pack_bf16(o4.x, o4.y);
+                o.y = pack_bf16(o4.z, o4.w);
+                *reinterpret_cast<uint2*>(Y + (size_t)tok * N + n0 + r4) = o;
+              }
+            }
           }
         }
         named_bar(kBarW, kWorkerThreads);
         if (wt == 0) signal_done(done, t);
+        if (lastp && wt == 0) stamp(g, t, R_EPI, 3);
       }
     }
     ++pc;
@@ -703,11 +887,10 @@ __device__ void norm_row(const Task& T, const Sm& S, int row) {
       v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
       v[c][4] = b.x; v[c][5] = b.y; v[c][6] = b.z; v[c][7] = b.w;
       if (T.n_delta) {
-        uint4 dv[kMaxDeltas];
-        for (int i = 0; i < T.n_delta; ++i)
-          dv[i] = __ldcg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)T.dl[i] + (size_t)row * H) + ch);
+        // (one delta — every decoder norm — stays in registers; more in index order)
+        const uint4 d0 = __ldcg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)T.dl[0] + (size_t)row * H) + ch);
         for (int i = 0; i < T.n_delta; ++i) {
-          const uint4 d = dv[i];
+          const uint4 d = i == 0 ? d0 : __ldcg(reinterpret_cast<const uint4*>((const __nv_bfloat16*)T.dl[i] + (size_t)row * H) + ch);
           v[c][0] += bf16lo(d.x); v[c][1] += bf16hi(d.x);
           v[c][2] += bf16lo(d.y); v[c][3] += bf16hi(d.y);
           v[c][4] += bf16lo(d.z); v[c][5] += bf16hi(d.z);
@@ -927,7 +1110,7 @@ __device__ void cons_attn(const Task& T, const Sm& S, const Geo& g, unsigned* er
       l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], x);
       l_run[1] += __shfl_xor_sync(0xffffffffu, l_run[1], x);
     }
-    if (ci >= 1) mwait_sleep(S.cempty, (ci - 1u) & 1u, err, S);
+    if (ci >= 1) mwait_sleep(&S.cempty[(ci - 1u) & 1u], ((ci - 1u) >> 1) & 1u, err, S);
     float* cw = S.comb + (size_t)w * g.Gm * D;
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
@@ -945,15 +1128,23 @@ __device__ void cons_attn(const Task& T, const Sm& S, const Geo& g, unsigned* er
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(S.cfull);
+    if (lane == 0) mbar_arrive(&S.cfull[ci & 1u]);
     ++ci;
   }
 }
 
 // attention merge warp: 8 warp states (fixed order) → output or split partial;
 // the last split of a (sequence, kv head) unit merges the splits (fixed order)
-__device__ void merge_attn(const Task& T, int t, const Sm& S, const Geo& g, unsigned* done, unsigned ep, unsigned* err,
-                           unsigned& ak, unsigned& ci) {
+// two merge warps (the MMA warp is idle during attention): item ci is merged
+// by warp ci mod 2, so one item's split handling (stores, fences, the arrival
+// atomic, the last split's merge) overlaps the next item's merge
+__device__ void merge_attn(const Task& T, int t, const Sm& S0, const Geo& g, unsigned* done, unsigned ep, unsigned* err,
+                           unsigned& ak, unsigned& ci, int sub) {
+  Sm S = S0;  // this merge warp's own scratch
+  S.s_w += sub * (kWorkers * kMaxG + 2 * kMaxG + kFastSplitLse);
+  S.s_M += sub * (kWorkers * kMaxG + 2 * kMaxG + kFastSplitLse);
+  S.s_L += sub * (kWorkers * kMaxG + 2 * kMaxG + kFastSplitLse);
+  S.s_lse += sub * (kWorkers * kMaxG + 2 * kMaxG + kFastSplitLse);
   const int lane = threadIdx.x & 31;
   const int Gq = T.G, D = T.D;
   __nv_bfloat16* out = (__nv_bfloat16*)T.o0;
@@ -966,9 +1157,13 @@ __device__ void merge_attn(const Task& T, int t, const Sm& S, const Geo& g, unsi
     if (lane == 0) mbar_arrive(&S.iempty[is]);
     ++ak;
     if (it < 0) break;
+    if ((int)(ci & 1u) != sub) {  // the other merge warp's item
+      ++ci;
+      continue;
+    }
     const int split = it % T.splits, unit = it / T.splits;
     const int gh = unit / T.rows, b = unit % T.rows;
-    mwait_sleep(S.cfull, ci & 1u, err, S);
+    mwait_sleep(&S.cfull[ci & 1u], (ci >> 1) & 1u, err, S);
     for (int x = lane; x < kWorkers * Gq; x += 32) {
       const int w = x / Gq, h = x % Gq;
       float M = -INFINITY;
@@ -1004,7 +1199,7 @@ __device__ void merge_attn(const Task& T, int t, const Sm& S, const Geo& g, unsi
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(S.cempty);
+    if (lane == 0) mbar_arrive(&S.cempty[ci & 1u]);
     ++ci;
     bool fin = single;
     if (!single) {
@@ -1096,8 +1291,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   S.ifull = S.qempty + 2;
   S.iempty = S.ifull + 4;
   S.cfull = S.iempty + 4;
-  S.cempty = S.cfull + 1;
-  S.xg = S.cempty + 1;
+  S.cempty = S.cfull + 2;
+  S.xg = S.cempty + 2;
   S.xa = S.xg + 1;
   uint8_t* misc = smem + g.off_misc;
   S.s_item = (int*)misc;                      // 16 B
@@ -1105,6 +1300,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   S.red = (float*)(misc + 32);                // 32 B
   S.tmem_slot = (uint32_t*)(misc + 64);       // 16 B
   S.s_len = (int*)(misc + 80);                // 16 B (+16 spare)
+  __shared__ int s_rpos[128], s_rpg[128];     // fused RoPE fold: per-token position and page
+  S.rpos = s_rpos;
+  S.rpg = s_rpg;
   S.s_w = (float*)(misc + 112);               // [8][8]
   S.s_M = S.s_w + kWorkers * kMaxG;           // [8]
   S.s_L = S.s_M + kMaxG;                      // [8]
@@ -1125,11 +1323,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&S.qfull[i], 1);
       mbar_init(&S.qempty[i], kWorkers);
     }
-    for (int i = 0; i < 4; ++i) mbar_init(&S.ifull[i], 1), mbar_init(&S.iempty[i], kWorkers + 2);
+    for (int i = 0; i < 4; ++i) mbar_init(&S.ifull[i], 1), mbar_init(&S.iempty[i], kWorkers + 3);
     mbar_init(S.xg, 1);
     mbar_init(S.xa, 1);
-    mbar_init(S.cfull, kWorkers);
-    mbar_init(S.cempty, 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&S.cfull[i], kWorkers), mbar_init(&S.cempty[i], 1);
     for (int w = 0; w < kWarps; ++w) s_cur[w] = -1;
     s_ep = *(volatile unsigned*)ctrl;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1145,6 +1342,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *S.tmem_slot;
   const unsigned ep = s_ep;
   const int Gr = (int)gridDim.x, c = blockIdx.x;
+  if (g.n_tab) {
+    // this step's RoPE (cos, sin) tables: entry e of the concatenated tables is
+    // computed by CTA e mod grid — rope_append_kernel's arithmetic (fp64 angle,
+    // reduced to [−π, π], fp32 sincos of the reduced angle)
+    int base = 0;
+    for (int i = 0; i < g.n_tab; ++i) {
+      const int n = g.tab_rows[i] * g.tab_half[i];
+      for (int e = base + c + Gr * (int)threadIdx.x; e < base + n; e += Gr * kThreads) {
+        const int le = e - base, row = le / g.tab_half[i], p = le - row * g.tab_half[i];
+        const int pos = __ldg(g.tab_sl[i] + row) - 1;
+        const double ang = (double)pos * g.tab_freq[i][p];
+        const double k = rint(ang * 0.15915494309189535);
+        const double red = fma(-k, 6.283185307179586, fma(-k, 2.4492935982947064e-16, ang));
+        float sn, cs;
+        sincosf((float)red, &sn, &cs);
+        g.tab[i][le] = make_float2(cs, sn);
+      }
+      base += n;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) signal_done(g.tab_ready, 0);
+  }
 
   // role state (each role keeps only its own; all advance identically)
   unsigned gs = 0, pc = 0, ak = 0, ci = 0;
@@ -1169,7 +1388,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0; t < g.n_tasks; ++t) {
       const Task& T = tasks[t];
       if (lane == 0) s_cur[warp] = t, stamp(g, t, R_MMA, 0);
-      if (T.kind == MK_GEMM) mma_gemm(T, S, g, tmem, err, gs, pc);
+      if (T.kind == MK_GEMM) mma_gemm(T, t, S, g, tmem, err, gs, pc);
+      else if (T.kind == MK_ATTN) merge_attn(T, t, S, g, done, ep, err, ak, ci, 1);
       if (lane == 0) stamp(g, t, R_MMA, 2);
     }
   } else if (warp == kLoader2) {
@@ -1182,7 +1402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0; t < g.n_tasks; ++t) {
       const Task& T = tasks[t];
       if (lane == 0) s_cur[warp] = t, stamp(g, t, R_MERGE, 0);
-      if (T.kind == MK_ATTN) merge_attn(T, t, S, g, done, ep, err, ak, ci);
+      if (T.kind == MK_ATTN) merge_attn(T, t, S, g, done, ep, err, ak, ci, 0);
       if (lane == 0) stamp(g, t, R_MERGE, 2);
     }
   } else if (warp >= kW0) {
@@ -1192,14 +1412,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) s_cur[warp] = t;
       if (wt == 0) stamp(g, t, R_WORK, 0);
       switch (T.kind) {
-        case MK_GEMM: epi_gemm(T, t, S, done, ep, tmem, err, pc); break;
+        case MK_GEMM: epi_gemm(T, t, S, g, done, ep, tmem, err, pc, g.tab_ready); break;
         case MK_ATTN: cons_attn<D>(T, S, g, err, ak, ci, apos, apar); break;
         case MK_NORM:
         case MK_SILU:
         case MK_RESID: {
           bool waited = false;
+          unsigned nu = 0;
           const int first = ((c - T.rot) % Gr + Gr) % Gr;
-          for (int u = first; u < T.n_units; u += Gr) {
+          for (int u = first; u < T.n_units; u += Gr, ++nu) {
             if (!waited) {
               if (wt == 0) deps_wait(T, done, ep, err, S), stamp(g, t, R_WORK, 1);
               named_bar(kBarW, kWorkerThreads);
@@ -1245,8 +1466,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               named_bar(kBarW, kWorkerThreads);
             }
-            if (wt == 0) signal_done(done, t);
           }
+          // one release for all of this CTA's units (every unit ended in a worker barrier)
+          if (nu && wt == 0) signal_done(done, t, nu);
           break;
         }
         case MK_ROPE: {
@@ -1254,10 +1476,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int hf = wt >> 7, t128 = wt & 127;
           const int ny = (T.Hq + 2 * T.Hkv + 7) / 8;
           bool waited = false;
+          unsigned nu = 0;
           const int first = ((c - T.rot) % Gr + Gr) % Gr;
           int k = 0;
           for (int u = first; u < T.n_units; u += Gr, ++k) {
             if ((k & 1) != hf) continue;
+            ++nu;
             if (!waited) {
               if (t128 == 0) deps_wait(T, done, ep, err, S), stamp(g, t, R_WORK, 1);
               named_bar(kBarHalf0 + hf, 128);
@@ -1265,8 +1489,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             rope_unit(T, u / ny, u % ny, t128);
             named_bar(kBarHalf0 + hf, 128);
-            if (t128 == 0) signal_done(done, t);
           }
+          if (nu && t128 == 0) signal_done(done, t, nu);
           break;
         }
         default: break;
@@ -1308,6 +1532,16 @@ struct MegaPlan {
   std::vector<int> gpar, apar;    // scratch parity per task (-1 none)
   std::vector<double> freq;       // concatenated RoPE tables
   std::vector<int> freq_off;      // per task (doubles)
+  struct Tab {
+    const void* sl;
+    int rows, half;
+    double theta;
+    int freq_off;      // its θ^(−2i/D) in freq
+    uint64_t off;      // byte offset of its (cos, sin) table in the workspace
+  };
+  std::vector<Tab> tabs;
+  std::vector<int> tab_of;        // per task (-1 none)
+  uint64_t off_tab = 0;
   std::vector<MegaOpDesc> ops;
   uint8_t* ws = nullptr;
   unsigned* err = nullptr;
@@ -1355,6 +1589,7 @@ kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64
   P->gpar.assign(n, -1);
   P->apar.assign(n, -1);
   P->freq_off.assign(n, -1);
+  P->tab_of.assign(n, -1);
   int D = 0, Gm = 1, maxM = 0;
   uint64_t ctr_words = 0;
   int last_g[2] = {-1, -1}, last_a[2] = {-1, -1}, ng = 0, na = 0;
@@ -1425,8 +1660,37 @@ kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64
         for (uint32_t i = 0; i < a.head_dim / 2; ++i) P->freq.push_back(std::exp2(-2.0 * (double)i / (double)a.head_dim * l2t));
         break;
       }
-      case KD_OP_GEMM: {
-        auto a = get_attr<kd_attr_gemm>(o);
+      case KD_OP_GEMM:
+      case KD_OP_GEMM_SILU:
+      case KD_OP_QKV_ROPE: {
+        kd_attr_gemm a{};
+        if (o.op == KD_OP_QKV_ROPE) {
+          auto r = get_attr<kd_attr_qkv_rope>(o);
+          if (r.head_dim % 4 || 128 % r.head_dim || r.n_heads % r.n_kv_heads) return bad("QKV+RoPE head shape");
+          a.M = r.rows, a.N = (r.n_heads + 2 * r.n_kv_heads) * r.head_dim, a.K = r.hidden, a.dtype = r.dtype;
+          T.epi = 1;
+          T.Hq = r.n_heads, T.Hkv = r.n_kv_heads, T.D = r.head_dim, T.page = r.page, T.pps = r.pages_per_seq;
+          {  // one (cos, sin) table per distinct (seq_len buffer, rows, D/2, θ)
+            int ti = -1;
+            for (int i = 0; i < (int)P->tabs.size(); ++i)
+              if (P->tabs[i].sl == o.rd[3] && P->tabs[i].rows == (int)r.rows && P->tabs[i].half == (int)r.head_dim / 2 &&
+                  P->tabs[i].theta == r.theta)
+                ti = i;
+            if (ti < 0) {
+              if (P->tabs.size() == 4) return bad("more than 4 distinct RoPE position sets");
+              P->tabs.push_back({o.rd[3], (int)r.rows, (int)r.head_dim / 2, r.theta, (int)P->freq.size(), 0});
+              ti = (int)P->tabs.size() - 1;
+            }
+            P->tab_of[t] = ti;
+          }
+          P->freq_off[t] = (int)P->freq.size();
+          const double l2t = std::log2(r.theta);
+          for (uint32_t i = 0; i < r.head_dim / 2; ++i)
+            P->freq.push_back(std::exp2(-2.0 * (double)i / (double)r.head_dim * l2t));
+        } else {
+          a = get_attr<kd_attr_gemm>(o);
+          T.epi = o.op == KD_OP_GEMM_SILU ? 2 : 0;
+        }
         if (a.dtype != KD_BF16) return bad("fp32 GEMM");
         if (a.M == 0 || a.M > 128 || a.K % 128 || a.N % 8) return bad("GEMM shape (M <= 128, K % 128 == 0, N % 8 == 0)");
         T.kind = MK_GEMM;
@@ -1442,10 +1706,25 @@ kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64
           maxc = std::max(maxc, (int)(uowner((long long)(tl + 1) * T.KB - 1, U, T.gg) - uowner((long long)tl * T.KB, U, T.gg) + 1));
         T.maxc = maxc;
         T.n_units = (int)U;
-        T.done_units = T.tiles;
+        {  // completion units: one per tile slice (a whole tile or a folder's share of a split tile)
+          unsigned units = 0;
+          for (int tl = 0; tl < T.tiles; ++tl) {
+            const long long tb = (long long)tl * T.KB, te = tb + T.KB;
+            const int f = (int)uowner(tb, U, T.gg), l = (int)uowner(te - 1, U, T.gg);
+            const int nc = l - f + 1;
+            units += nc == 1 ? 1u : (unsigned)((l - f) + (ubeg(l + 1, U, T.gg) == te ? 1 : 0));
+          }
+          T.done_units = units;
+        }
         T.a0 = o.rd[0];  // X
         T.a1 = o.rd[1];  // W
         T.o0 = o.wr[0];
+        if (T.epi == 1) {
+          T.ctr2 = o.rd[2];  // block table
+          T.a2 = o.rd[3];    // seq_len
+          T.o1 = o.wr[1];
+          T.o2 = o.wr[2];
+        }
         maxM = std::max(maxM, T.mma_n);
         P->ctr_off[t] = ctr_words;
         ctr_words += T.tiles;
@@ -1453,7 +1732,7 @@ kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64
         P->gpar[t] = p;
         if (last_g[p] >= 0) extra[t].push_back(last_g[p]);
         last_g[p] = t;
-        P->gpart_bytes = std::max<uint64_t>(P->gpart_bytes, (uint64_t)T.tiles * maxc * a.M * 128 * 4);
+        P->gpart_bytes = std::max<uint64_t>(P->gpart_bytes, (uint64_t)T.tiles * maxc * T.mma_n * 128 * 4);
         break;
       }
       case KD_OP_ATTENTION: {
@@ -1536,7 +1815,8 @@ kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64
   int SPS = 0;
   if (maxM) SPS = (2 * 16384 + 2 * maxM * 128 + kSlot - 1) / kSlot;
   const size_t fixed = (size_t)2 * Gm * D * 2 + (size_t)kWorkers * Gm * D * 4 + (size_t)kWorkers * Gm * 2 * 4 +
-                       (2 * kMaxStages + 2 * kMaxSlots + 24) * 8 + 1024 + 1024;
+                       (2 * kMaxStages + 2 * kMaxSlots + 24) * 8 + 112 + 2 * (kWorkers * kMaxG + 2 * kMaxG + kFastSplitLse) * 4 +
+                       2048 /* static */ + 1024 /* alignment */;
   int smem_max = 0;
   KD_CUDA_CHECK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem opt-in");
   int NS = std::min<int>(kMaxSlots, (int)(((size_t)smem_max - fixed) / kSlot));
@@ -1551,6 +1831,7 @@ kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64
   g.Gm = Gm;
   g.pf = getenv("KD_MEGA_PF") ? atoi(getenv("KD_MEGA_PF")) : 1;
   g.dbg = getenv("KD_MEGA_DBG") ? atoi(getenv("KD_MEGA_DBG")) : 0;
+  g.l2pf = getenv("KD_MEGA_L2PF") ? atoi(getenv("KD_MEGA_L2PF")) : 0;  // (8/16: no gain, measured)
   size_t off = (size_t)NS * kSlot;
   g.off_q = (uint32_t)off;
   off += (size_t)2 * Gm * D * 2;
@@ -1563,7 +1844,7 @@ kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64
   g.off_bar = (uint32_t)off;
   off += (2 * kMaxStages + 2 * kMaxSlots + 24) * 8;
   g.off_misc = (uint32_t)off;
-  off += 112 + (kWorkers * kMaxG + 2 * kMaxG + kFastSplitLse) * 4;
+  off += 112 + 2 * (kWorkers * kMaxG + 2 * kMaxG + kFastSplitLse) * 4;
   P->smem = off + 1024;  // + alignment slack
   if (P->smem > (size_t)smem_max) return bad("shared memory layout exceeds the opt-in limit");
   P->D = D;
@@ -1579,6 +1860,11 @@ kd_status mega_create(const std::vector<MegaOpDesc>& ops, MegaPlan** out, uint64
   P->off_ctr = take(ctr_words * 4 + 4);
   P->off_freq = take(P->freq.size() * 8 + 8);
   P->off_tasks = take((uint64_t)n * sizeof(Task));
+  {
+    uint64_t tb = 0;
+    for (auto& tbl : P->tabs) tbl.off = tb, tb += (uint64_t)tbl.rows * tbl.half * 8;
+    P->off_tab = take(tb + 8);
+  }
   P->off_gpart = take(2 * P->gpart_bytes);
   P->off_apart = take(2 * P->apart_bytes);
   P->total = w;
@@ -1626,7 +1912,21 @@ kd_status mega_bind(MegaPlan* P, void* ws, uint64_t bytes, unsigned* err) {
     } else if (T.kind == MK_ROPE) {
       T.freq = (const double*)(b + P->off_freq) + P->freq_off[t];
     }
+    if (T.kind == MK_GEMM && T.epi == 1) {
+      T.freq = (const double*)(b + P->off_freq) + P->freq_off[t];
+      T.rtab = (const float2*)(b + P->off_tab + P->tabs[P->tab_of[t]].off);
+    }
   }
+  Geo& g = P->geo;
+  g.n_tab = (int)P->tabs.size();
+  for (int i = 0; i < g.n_tab; ++i) {
+    g.tab_sl[i] = (const int32_t*)P->tabs[i].sl;
+    g.tab_freq[i] = (const double*)(b + P->off_freq) + P->tabs[i].freq_off;
+    g.tab[i] = (float2*)(b + P->off_tab + P->tabs[i].off);
+    g.tab_rows[i] = P->tabs[i].rows;
+    g.tab_half[i] = P->tabs[i].half;
+  }
+  g.tab_ready = (unsigned*)(b + P->off_ctrl + 64);
   KD_CUDA_CHECK(cudaMemset(b, 0, P->off_tasks), "megakernel: zero counters");
   if (!P->freq.empty())
     KD_CUDA_CHECK(cudaMemcpy(b + P->off_freq, P->freq.data(), P->freq.size() * 8, cudaMemcpyHostToDevice), "freq upload");

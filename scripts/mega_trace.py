@@ -29,13 +29,14 @@ def main():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--config", default="llama3-8b")
     ap.add_argument("--out", default="")
+    ap.add_argument("--unfused", action="store_true")
     a = ap.parse_args()
     cfg = synth.CONFIGS[a.config].with_(n_layers=a.layers, batch=a.batch, n_micro=1)
-    dg = DEC.DecoderGraph(cfg)
+    dg = DEC.DecoderGraph(cfg, fuse_silu=not a.unfused, fuse_rope=not a.unfused)
     rt = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], seed=cfg.seed, megakernel=True)
     info = rt.rt.exec_info(0)
     nt, grid = info["tasks"], info["grid"]
-    buf = torch.zeros(nt * grid * 4 * 3, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(nt * grid * 5 * 4, dtype=torch.int64, device="cuda")
     for _ in range(3):
         rt.step()
     torch.cuda.synchronize()
@@ -51,7 +52,7 @@ def main():
     e1.record(rt.streams[0])
     torch.cuda.synchronize()
     step_ms = e0.elapsed_time(e1) / 5
-    tr = buf.cpu().numpy().astype(np.int64).reshape(nt, grid, 4, 3)
+    tr = buf.cpu().numpy().astype(np.int64).reshape(nt, grid, 5, 4)
     t0 = tr[tr > 0].min()
     names = [k.name for k in dg.kernels]
     rows = []
@@ -71,7 +72,36 @@ def main():
             cols.append(f"{beg:9.1f} {dep:9.1f} {end:9.1f}")
         rows.append(row)
         print(f"{t:4d} {row['name']:<10} " + " ".join(cols))
+    print("GEMM epilogue (last piece), max over CTAs, relative to that task's MMA end (us):")
+    for t in range(nt):
+        ep_ = tr[t, :, 4, :]
+        if not (ep_[:, 0] > 0).any():
+            continue
+        mma_end = tr[t, :, 1, 2].max()
+        def mx(k):
+            v = ep_[:, k]
+            return (v[v > 0].max() - mma_end) / 1e3 if (v > 0).any() else float("nan")
+        def md(k, k0):
+            v = ep_[:, k] - ep_[:, k0]
+            ok = (ep_[:, k] > 0) & (ep_[:, k0] > 0)
+            return float(np.median(v[ok])) / 1e3 if ok.any() else float("nan")
+        lastdata = tr[t, :, 1, 1]
+        mma_last = tr[t, :, 1, 2]
+        okm = (lastdata > 0) & (mma_last > 0)
+        stores = tr[t, :, 3, 1]
+        oks = (stores > 0) & (ep_[:, 0] > 0)
+        print(f"      median per CTA: last data -> mma commit {np.median((mma_last - lastdata)[okm]) / 1e3:5.2f}  "
+              f"mma commit -> tmem seen {np.median((ep_[:, 0] - mma_last)[okm & (ep_[:, 0] > 0)]) / 1e3:5.2f}  "
+              f"tmem -> own stores done {np.median((stores - ep_[:, 0])[oks]) / 1e3:5.2f}  "
+              f"own stores -> published {np.median((ep_[:, 1] - stores)[oks & (ep_[:, 1] > 0)]) / 1e3:5.2f}")
+        print(f"  {t:3d} {names[t] if t < len(names) else '?':<9} tmem {mx(0):6.1f} published {mx(1):6.1f} "
+              f"all-present {mx(2):6.1f} folded {mx(3):6.1f} | median per CTA: store+arrive {md(1,0):5.1f} "
+              f"wait {md(2,1):5.1f} fold {md(3,2):5.1f}")
     attn = [r for r in rows if r["name"] == "attn"]
+    lay = [r for r in rows if r["name"] == "norm1"]
+    if len(lay) >= 3:
+        print(f"SUMMARY per-layer span (norm1 start to next norm1 start) us: "
+              f"{(lay[2]['work'][0] - lay[1]['work'][0]):.1f}")
     if attn:
         import statistics
         spans = [r["load"][2] - r["load"][1] for r in attn[1:]] or [attn[0]["load"][2] - attn[0]["load"][1]]

@@ -29,8 +29,8 @@ def relerr(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
 
 
-def run(DEC, cfg, inp, steps=1, mega=True):
-    dg = DEC.DecoderGraph(cfg)
+def run(DEC, cfg, inp, steps=1, mega=True, fused=False):
+    dg = DEC.DecoderGraph(cfg, fuse_silu=fused, fuse_rope=fused)
     rt = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp, megakernel=mega)
     for _ in range(steps):
         rt.step()
@@ -122,6 +122,27 @@ def test_megakernel_8b_layers_vs_graph_path_and_oracle(mod):
     assert_elementwise(m.residual(), g.residual(), 4, 2e-2, "residual (B=64) vs graph path")
     for l in range(cfg.n_layers):
         assert_elementwise(OL.bf16_to_f64(m.cache("kc", l)), OL.bf16_to_f64(g.cache("kc", l)), 2, 2e-2, f"k cache {l}")
+
+
+@pytest.mark.parametrize("name", ["tiny_m4", "tiny_gqa_ragged"])
+def test_megakernel_fused_graph_vs_oracle_and_graph_path(mod, name):
+    """The graph with QKV+RoPE/append and gate_up+SiLU declared as single
+    kernels (KD_OP_QKV_ROPE, KD_OP_GEMM_SILU): the megakernel applies RoPE and
+    SiLU·mul in the GEMM fold (rope_append / silu_mul per-element arithmetic on
+    the bf16-rounded sums). vs the oracle, and vs the per-kernel fused path."""
+    DEC, K, api = mod
+    cfg = CFGS[name]
+    inp = synth.make_decoder_inputs(cfg)
+    rt = run(DEC, cfg, inp, fused=True)
+    assert rt.rt.exec_info(0)["tasks"] == rt.dg.g.num_kernels * cfg.n_micro
+    r_ref, kcs, vcs = OL.decoder_step(inp, act="bf16")
+    assert relerr(rt.residual(), r_ref) < 5e-3
+    assert_elementwise(rt.residual(), r_ref, 2, 1e-2, "residual")
+    for l in range(cfg.n_layers):
+        assert_elementwise(OL.bf16_to_f64(rt.cache("kc", l)), kcs[l], 2, 2e-2, f"k cache {l}")
+        assert_elementwise(OL.bf16_to_f64(rt.cache("vc", l)), vcs[l], 2, 1e-2, f"v cache {l}")
+    g = run(DEC, cfg, inp, steps=1, mega=False, fused=True)
+    assert_elementwise(rt.residual(), g.residual(), 2, 1e-2, "residual vs per-kernel fused path")
 
 
 def test_megakernel_rejects_unsupported_schedules(mod):
