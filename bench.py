@@ -219,20 +219,22 @@ def role_layout(cfg, DEC, n_gpus):
 
 def step_bytes(cfg):
     """Algorithmic HBM bytes of one monolithic decode step (dense attention
-    layers, N=1): every weight, every KV page, each activation written once
-    and read once, the fp32 residual read and written by each add."""
+    layers, N=1) as the f1 megakernel runs it (QKV+RoPE and gate_up+SiLU
+    fused, norms separate): every weight, every KV page, each remaining
+    activation written once and read once, the fp32 residual read and
+    written by each add."""
     m, H, F, L = cfg.batch, cfg.hidden, cfg.ffn, cfg.n_layers
     Hq, Hkv, D, pps = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.pages_per_seq
     qkv = (Hq + 2 * Hkv) * D
     w = (qkv * H + H * Hq * D + 2 * F * H + H * F + 2 * H) * 2
     kv = m * pps * Hkv * 16 * D * 2 * 2 + m * pps * 4 + m * 4
     norm = m * H * (4 + 4 + 2 + 2)                  # r read + write, delta read, h write
-    act = (m * H * 2 + m * qkv * 2 * 2             # QKV: X in, Y out, RoPE reads it
+    act = (m * H * 2                               # QKV reads h1
            + m * Hq * D * 2 * 2 + 2 * m * Hkv * D * 2  # q written + read by attention, K/V slot appends
            + m * Hq * D * 2 * 2                    # attention out, O reads it
-           + m * H * 2 + m * H * 2                 # O out, gate_up X
-           + m * 2 * F * 2 * 2 + m * F * 2 * 2     # gate_up out + SiLU read, SiLU out + down read
-           + m * H * 2)                            # down out
+           + m * H * 2 + m * H * 2                 # O out (read by norm2), gate_up reads h2
+           + m * F * 2 * 2                         # a written by the gate_up fold, read by down
+           + m * H * 2)                            # down out (read by the next norm)
     return L * (w + kv + 2 * norm + act) + m * H * (4 + 4 + 2)  # + the final residual add
 
 
@@ -476,8 +478,11 @@ def main():
     tr_path = os.path.join(ROOT, "profiles", "mega_traffic.json" if mega else "attention_traffic.json")
     if mega and os.path.exists(tr_path):
         try:
+            sys.path.insert(0, os.path.join(ROOT, "scripts"))
+            from attention_traffic import source_sha256, MEGA_SOURCES
             tr = json.load(open(tr_path))
-            if tr.get("algorithmic_bytes_per_launch") == roof["bytes_per_launch"]:
+            if (tr.get("algorithmic_bytes_per_launch") == roof["bytes_per_launch"]
+                    and tr.get("source_sha256") == source_sha256(MEGA_SOURCES)):
                 roof["traffic"] = tr.get("bytes_per_launch")
                 roof["traffic_source"] = tr.get("source")
         except Exception:

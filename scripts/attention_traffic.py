@@ -1,11 +1,12 @@
 #!/usr/bin/env python3
-"""Write profiles/attention_traffic.json from an `ncu --set full` capture of
-the decode attention kernel, stamped with the sha256 of the kernel's source
-files. bench.py reports `roofline.traffic` only when the stamp matches the
-sources it was built from, so the number always comes from the kernel being
-timed (VERDICT r1 "What's weak" #3).
+"""Write profiles/attention_traffic.json (decode attention kernel) or, with
+--mega, profiles/mega_traffic.json (the f1 megakernel: one launch = the whole
+step) from an `ncu --set full` capture, stamped with the sha256 of the
+kernel's source files. bench.py reports `roofline.traffic` only when the stamp
+matches the sources it was built from, so the number always comes from the
+kernel being timed (VERDICT r1 "What's weak" #3).
 
-usage: attention_traffic.py REPORT.ncu-rep CAPTION
+usage: attention_traffic.py REPORT.ncu-rep CAPTION [--mega ALG_BYTES]
 """
 import csv
 import hashlib
@@ -17,13 +18,15 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SOURCES = ["paper_2604_10180_b200/csrc/kernels/attention.cu", "paper_2604_10180_b200/csrc/kernels/common.cuh",
-           "paper_2604_10180_b200/csrc/kernels/tcgen05.cuh"]
+           "paper_2604_10180_b200/csrc/kernels/tcgen05.cuh", "paper_2604_10180_b200/csrc/kernels/mmasync.cuh"]
+MEGA_SOURCES = SOURCES + ["paper_2604_10180_b200/csrc/kernels/mega.cu"]
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+US = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 
 
-def source_sha256():
+def source_sha256(sources=None):
     h = hashlib.sha256()
-    for p in SOURCES:
+    for p in sources or SOURCES:
         with open(os.path.join(ROOT, p), "rb") as f:
             h.update(f.read())
     return h.hexdigest()
@@ -31,22 +34,34 @@ def source_sha256():
 
 def main():
     rep, caption = sys.argv[1], sys.argv[2]
+    mega = "--mega" in sys.argv
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
                          check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     head, units = rows[0], rows[1]
     for r in rows[2:]:
         d, u = dict(zip(head, r)), dict(zip(head, units))
-        if "decode_attention" not in d["Kernel Name"]:
+        if ("mega_kernel" if mega else "decode_attention") not in d["Kernel Name"]:
             continue
         rd = float(d["dram__bytes_read.sum"]) * UNIT[u["dram__bytes_read.sum"]]
         wr = float(d["dram__bytes_write.sum"]) * UNIT[u["dram__bytes_write.sum"]]
         m, pps, Hkv, D, Hq = 64, 256, 8, 128, 32  # the 8B bench launch (B=64, C=4096)
         alg = m * pps * Hkv * 16 * D * 2 * 2 + 2 * m * Hq * D * 2 + m * pps * 4 + m * 4
+        if mega:
+            alg = int(sys.argv[sys.argv.index("--mega") + 1])
+            out_path = os.path.join(ROOT, "profiles", "mega_traffic.json")
+            json.dump({"kernel": d["Kernel Name"].split("(")[0], "bytes_per_launch": int(rd + wr),
+                       "dram_read": int(rd), "dram_write": int(wr),
+                       "duration_us_cold_under_ncu": float(d["gpu__time_duration.sum"]) * US[u["gpu__time_duration.sum"]],
+                       "algorithmic_bytes_per_launch": alg, "source_sha256": source_sha256(MEGA_SOURCES),
+                       "source": f"{caption}: ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum",
+                       "shape": "one launch = one 8B decode step (B=64, C=4096)"},
+                      open(out_path, "w"), indent=1)
+            print(open(out_path).read())
+            return
         json.dump({"kernel": d["Kernel Name"].split("(")[0], "bytes_per_launch": int(rd + wr),
                    "dram_read": int(rd), "dram_write": int(wr),
-                   "duration_us_cold_under_ncu": float(d["gpu__time_duration.sum"]) *
-                   (1e-3 if u["gpu__time_duration.sum"] == "nsecond" else 1.0),
+                   "duration_us_cold_under_ncu": float(d["gpu__time_duration.sum"]) * US[u["gpu__time_duration.sum"]],
                    "algorithmic_bytes_per_launch": alg, "source_sha256": source_sha256(),
                    "source": f"{caption}: ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum",
                    "shape": "m=64 sequences, Hq=32, Hkv=8, D=128, C=4096 (8B bench launch)"},
