@@ -10,6 +10,8 @@ here; if the CUDA extension is missing the product fails loudly.
 Modules (each function cites the passage it follows; P:n = PAPER.md line n,
 S:n = SPEC.md line n, R# = the readings listed in SURVEY.md §8(c) and DESIGN.md):
   layer     — decoder-layer math in fp64 (C1; R12 storage rounding)
+  prefill   — the prefill phase of the same layer: RoPE at every prompt
+              position + paged-cache fill, causal attention (f4)
   ddg       — RAW data-dependency graph by last-writer registry + per-byte
               brute force (C2)
   placement — cost model, objective E1–E7 in integer picoseconds, plain
@@ -22,4 +24,4 @@ S:n = SPEC.md line n, R# = the readings listed in SURVEY.md §8(c) and DESIGN.md
 Parity pins live in tests/test_oracle_*.py. Functions without an independent
 pin say "parity unpinned" in their docstring (none at present).
 """
-from . import layer, ddg, placement, schedule, monitor  # noqa: F401
+from . import layer, prefill, ddg, placement, schedule, monitor  # noqa: F401
