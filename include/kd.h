@@ -113,6 +113,11 @@ enum {
                             * kv-group-interleaved QKV weight with rows pair-interleaved inside every head
                             * (row 2p ← dim p, row 2p+1 ← dim p + D/2); bits identical to a4 then a5 */
   KD_OP_ATTN_MERGE = 16,   /* f2 reads [part_0 .. part_{n-1}] ([out|lse] of KD_ATTN_LSE attentions) writes [out] */
+  KD_OP_ROPE_PREFILL = 18,  /* f4 reads [qkv, block_table] writes [q, Kc, Vc]: RoPE at every prompt position
+                            * (token row r = b·S + t rotated by t·θ^(−2i/D)) and the paged-cache fill of slots
+                            * 0..S−1 (oracle/prefill.py rope_prefill) */
+  KD_OP_PREFILL_ATTENTION = 19,  /* f4 reads [q, Kc, Vc, block_table] writes [out]: causal GQA self-attention
+                            * over each sequence's S prompt tokens (row r = b·S + t attends keys 0..t) */
   KD_OP_GEMM_RMSNORM = 17  /* a7+a3 / a10+a3 fused (co-located O or down GEMM and the next residual add +
                             * RMSNorm): reads [X, W, r, gamma] writes [h, r] with kd_attr_gemm_rmsnorm:
                             * r' = r + bf16(X·Wᵀ) (bits identical to a GEMM then a3's add), h =
@@ -158,6 +163,18 @@ typedef struct {
   double theta;   /* RoPE base (R12) */
 } kd_attr_qkv_rope;  /* X [rows, hidden]; q [rows, n_heads·D]; caches as for rope_append */
 typedef struct { uint32_t rows, ffn, dtype, pad_; } kd_attr_silu_mul;  /* gu [rows, 2F] 64-col gate/up blocks */
+/* f4 prefill: `seqs` sequences of `seq_len` prompt tokens each;
+ * activations have seqs·seq_len rows (row b·seq_len + t). Caches as for
+ * rope_append (HND pages of `page` tokens, block_table [seqs, pages_per_seq],
+ * pages_per_seq·page ≥ seq_len). The prefill GEMMs are KD_OP_GEMM with
+ * M = seqs·seq_len > 256 rows (the tensor-bound tcgen05 kernel). */
+typedef struct {
+  uint32_t seqs, seq_len, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype;
+  double theta;
+} kd_attr_rope_prefill;
+typedef struct {
+  uint32_t seqs, seq_len, n_heads, n_kv_heads, head_dim, page, pages_per_seq, dtype;
+} kd_attr_prefill_attention;  /* seq_len % 16 == 0, head_dim 64 or 128, page 16 */
 typedef struct { uint32_t rows, hidden, n_delta, dtype; } kd_attr_residual_add; /* r fp32 [rows,H] += Σ deltas (dtype: bf16 or fp32) */
 /* MoE. route buffer: int32 idx[rows][top_k] then fp32
  * w[rows][top_k]; meta buffer: int32 count[E], offset[E], slot_of[rows][top_k]
@@ -572,6 +589,11 @@ kd_status kd_op_attention(const kd_attr_attention* a, const void* q, const void*
 kd_status kd_op_attn_merge(const kd_attr_attn_merge* a, const void* const* parts, void* out, void* stream);
 /* a8: a[:, 64j+i] = silu(gu[:, 128j+i]) · gu[:, 128j+64+i] */
 kd_status kd_op_silu_mul(const kd_attr_silu_mul* a, const void* gu, void* out, void* stream);
+/* f4: KD_OP_ROPE_PREFILL and KD_OP_PREFILL_ATTENTION as single launches (bf16). */
+kd_status kd_op_rope_prefill(const kd_attr_rope_prefill* a, const void* qkv, const int32_t* block_table, void* q_out,
+                             void* k_cache, void* v_cache, void* stream);
+kd_status kd_op_prefill_attention(const kd_attr_prefill_attention* a, const void* q, const void* k_cache,
+                                  const void* v_cache, const int32_t* block_table, void* out, void* stream);
 /* C1.11: r += Σ_i deltas[i] (index order) */
 kd_status kd_op_residual_add(const kd_attr_residual_add* a, float* r, const void* const* deltas, void* stream);
 /* a12: conv step: window = [state, x]; xbc = silu(window·w + b); state ← window[1:] (in place) */

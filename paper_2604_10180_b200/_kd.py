@@ -28,6 +28,7 @@ KD_OP_NONE, KD_OP_ADD_RMSNORM, KD_OP_GEMM, KD_OP_ROPE_APPEND, KD_OP_ATTENTION, K
     KD_OP_RESIDUAL_ADD, KD_OP_MOE_ROUTE, KD_OP_MOE_DISPATCH, KD_OP_GROUPED_GEMM, KD_OP_MOE_COMBINE, \
     KD_OP_SSM_CONV, KD_OP_SSM_UPDATE, KD_OP_GATED_NORM, KD_OP_GEMM_SILU, KD_OP_QKV_ROPE, KD_OP_ATTN_MERGE, \
     KD_OP_GEMM_RMSNORM = range(18)
+KD_OP_ROPE_PREFILL, KD_OP_PREFILL_ATTENTION = 18, 19
 KD_BF16, KD_F32 = 0, 1
 KD_OBJ_AUTO, KD_OBJ_THROUGHPUT, KD_OBJ_LATENCY = 0, 1, 2
 KD_MODE_DISAGG, KD_MODE_NO_TRANSFER, KD_MODE_LOG = 0, 1, 2
@@ -64,6 +65,17 @@ class kd_attr_rope_append(C.Structure):
     _fields_ = [("rows", C.c_uint32), ("n_heads", C.c_uint32), ("n_kv_heads", C.c_uint32), ("head_dim", C.c_uint32),
                 ("page", C.c_uint32), ("pages_per_seq", C.c_uint32), ("dtype", C.c_uint32), ("slot_offset", C.c_uint32),
                 ("theta", C.c_double)]
+
+
+class kd_attr_rope_prefill(C.Structure):
+    _fields_ = [("seqs", C.c_uint32), ("seq_len", C.c_uint32), ("n_heads", C.c_uint32), ("n_kv_heads", C.c_uint32),
+                ("head_dim", C.c_uint32), ("page", C.c_uint32), ("pages_per_seq", C.c_uint32), ("dtype", C.c_uint32),
+                ("theta", C.c_double)]
+
+
+class kd_attr_prefill_attention(C.Structure):
+    _fields_ = [("seqs", C.c_uint32), ("seq_len", C.c_uint32), ("n_heads", C.c_uint32), ("n_kv_heads", C.c_uint32),
+                ("head_dim", C.c_uint32), ("page", C.c_uint32), ("pages_per_seq", C.c_uint32), ("dtype", C.c_uint32)]
 
 
 class kd_attr_attention(C.Structure):
@@ -257,6 +269,8 @@ _PROTOS = {
     "kd_op_rope_append": (kd_status, [C.POINTER(kd_attr_rope_append), P, P, P, P, P, P, P]),
     "kd_op_attention": (kd_status, [C.POINTER(kd_attr_attention), P, P, P, P, P, P, P, P]),
     "kd_op_silu_mul": (kd_status, [C.POINTER(kd_attr_silu_mul), P, P, P]),
+    "kd_op_rope_prefill": (kd_status, [C.POINTER(kd_attr_rope_prefill), P, P, P, P, P, P]),
+    "kd_op_prefill_attention": (kd_status, [C.POINTER(kd_attr_prefill_attention), P, P, P, P, P, P]),
     "kd_op_residual_add": (kd_status, [C.POINTER(kd_attr_residual_add), P, P, P]),
 }
 

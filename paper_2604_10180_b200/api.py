@@ -393,3 +393,15 @@ def silu_mul(attrs, gu, out, stream=None):
 def residual_add(attrs, r, deltas, stream=None):
     arr, _ = _ptr_array(deltas)
     check(K.kd_op_residual_add(C.byref(attrs), _p(r), arr, _stream(stream)), "kd_op_residual_add")
+
+
+def rope_prefill(attrs, qkv, block_table, q_out, k_cache, v_cache, stream=None):
+    """f4: RoPE at every prompt position + paged-cache fill (KD_OP_ROPE_PREFILL)."""
+    check(K.kd_op_rope_prefill(C.byref(attrs), _p(qkv), _p(block_table), _p(q_out), _p(k_cache), _p(v_cache),
+                               _stream(stream)), "kd_op_rope_prefill")
+
+
+def prefill_attention(attrs, q, k_cache, v_cache, block_table, out, stream=None):
+    """f4: causal GQA attention over the prompt (KD_OP_PREFILL_ATTENTION)."""
+    check(K.kd_op_prefill_attention(C.byref(attrs), _p(q), _p(k_cache), _p(v_cache), _p(block_table), _p(out),
+                                    _stream(stream)), "kd_op_prefill_attention")

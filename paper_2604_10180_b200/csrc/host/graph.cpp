@@ -150,7 +150,7 @@ static kd_status copy_spans(const kd_graph* g, const kd_span* in, uint32_t n, st
 kd_status kd_graph_add_kernel(kd_graph* g, const kd_kernel_desc* d, uint32_t* id) {
   if (!g || !d || !id) return fail(KD_ERR_INVALID_ARG, "kd_graph_add_kernel: NULL argument");
   if (g->finalized) return fail(KD_ERR_STATE, "kd_graph_add_kernel: graph already finalized");
-  if (d->op > KD_OP_GEMM_RMSNORM) return fail(KD_ERR_INVALID_ARG, "kd_graph_add_kernel: unknown op");
+  if (d->op > KD_OP_PREFILL_ATTENTION) return fail(KD_ERR_INVALID_ARG, "kd_graph_add_kernel: unknown op");
   Kernel k;
   k.op = d->op;
   k.pin = d->pin_device;

@@ -36,7 +36,8 @@ bool op_count_geometry(const Kernel& k, u64* rows, u64* row_bytes) {
     case KD_OP_GEMM:
     case KD_OP_GEMM_SILU: {
       kd_attr_gemm a;
-      if (!attrs_as(k, &a) || a.dtype != KD_BF16) return false;
+      // (M > 256: the f4 prefill kernel releases once per CTA — CTA mode)
+      if (!attrs_as(k, &a) || a.dtype != KD_BF16 || a.M > 256) return false;
       *rows = a.M, *row_bytes = 2ull * (k.op == KD_OP_GEMM_SILU ? a.N / 2 : a.N);
       return true;
     }
@@ -84,7 +85,7 @@ u64 op_consumer_unit(const Kernel& k, uint32_t ri, u64 row_bytes) {
     case KD_OP_GEMM:
     case KD_OP_GEMM_SILU: {
       kd_attr_gemm a;
-      if (ri != 0 || !attrs_as(k, &a) || a.dtype != KD_BF16 || 2ull * a.K != row_bytes) return 0;
+      if (ri != 0 || !attrs_as(k, &a) || a.dtype != KD_BF16 || 2ull * a.K != row_bytes || a.M > 256) return 0;
       return ((a.M + 15) / 16 * 16 <= 128 ? 2ull : 1ull) * 64 * 2;
     }
     case KD_OP_GEMM_RMSNORM: {

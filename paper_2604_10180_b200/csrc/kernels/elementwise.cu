@@ -632,6 +632,18 @@ kd_status op_signals(uint32_t op, const std::vector<uint8_t>& attrs, uint32_t* s
     case KD_OP_SSM_CONV:
     case KD_OP_SSM_UPDATE:
     case KD_OP_GATED_NORM: return ssm_signals(op, attrs, signals);
+    case KD_OP_ROPE_PREFILL: {
+      kd_attr_rope_prefill a;
+      if ((st = attrs_of(attrs, &a)) || (st = rope_prefill_validate(a))) return st;
+      *signals = rope_prefill_signals(a);
+      return KD_OK;
+    }
+    case KD_OP_PREFILL_ATTENTION: {
+      kd_attr_prefill_attention a;
+      if ((st = attrs_of(attrs, &a)) || (st = prefill_attention_validate(a))) return st;
+      *signals = prefill_attention_signals(a);
+      return KD_OK;
+    }
   }
   *signals = 0;
   return KD_OK;

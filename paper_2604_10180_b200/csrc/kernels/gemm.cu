@@ -1642,6 +1642,10 @@ kd_status gemm_scratch_bytes(const GemmShape& a, uint64_t* bytes) {
     *bytes = 256;
     return KD_OK;
   }
+  if (gemm_is_prefill(a)) {  // f4 large-M kernel: no split-K, no scratch
+    *bytes = 256;
+    return KD_OK;
+  }
   gemm::Geometry g;
   kd_status s = gemm::geometry(a, &g, gemm::device_sms());
   if (s) return s;
@@ -1662,6 +1666,7 @@ kd_status gemm_prepare(const GemmShape& a, const void* X, const void* W, const v
     gp->dense = false;
     return KD_OK;
   }
+  if (gemm_is_prefill(a)) return gemm_prefill_prepare(a, X, W, gp);  // f4: M > 256 rows, tensor-bound
   gemm::Geometry g;
   kd_status s = gemm::geometry(a, &g, gemm::device_sms());
   if (s) return s;
@@ -1747,6 +1752,7 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
     if (!st && signals) *signals = gemm_f32_signals(gp.sh.N);
     return st;
   }
+  if (gp.prefill) return launch_gemm_prefill(gp, Y, c, signals);
   if (gp.dense) return launch_gemm_dense(gp, Y, c, signals);
   gemm::Geometry g;
   kd_status s = gemm::geometry(gp.sh, &g, gemm::device_sms());
@@ -1839,6 +1845,10 @@ kd_status gemm_signals(const GemmShape& a, uint32_t* s) {
     *s = gemm_f32_signals(a.N);
     return KD_OK;
   }
+  if (gemm_is_prefill(a)) {
+    *s = gemm_prefill_signals(a);
+    return KD_OK;
+  }
   if (gemm::use_dense(a)) {
     // one release per storing CTA: every tile once (split 1), else every
     // cluster rank that owns weight rows
@@ -1860,6 +1870,10 @@ kd_status gemm_signals(const GemmShape& a, uint32_t* s) {
 
 kd_status gemm_grid(const GemmShape& a, uint32_t* grid) {
   if (a.dtype == KD_F32) return fail(KD_ERR_UNSUPPORTED, "gemm_grid: bf16 only");
+  if (gemm_is_prefill(a)) {
+    *grid = gemm_prefill_signals(a);
+    return KD_OK;
+  }
   if (gemm::use_dense(a)) {
     GemmTile t;
     double ns = 0;

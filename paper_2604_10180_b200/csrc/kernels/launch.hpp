@@ -161,6 +161,7 @@ struct GemmPlan {
   const int* meta = nullptr;  // grouped: int32 counts (+expert0); offsets at meta + moff
   int moff = 0;               // grouped: meta_experts (offsets follow the counts of every expert)
   bool dense = false;         // cluster split-K kernel (else stream-K)
+  bool prefill = false;       // f4 large-M (M > 256) tensor-bound kernel (prefill.cu)
   const void* X = nullptr;    // fp32 path: plain operand pointers (SIMT kernel)
   const void* W = nullptr;
   RopeEpi rp;                 // KD_OP_QKV_ROPE
@@ -170,6 +171,19 @@ struct GemmPlan {
   GemmTile tile;
 };
 kd_status gemm_scratch_bytes(const GemmShape& sh, uint64_t* bytes);
+// f4 prefill kernels (prefill.cu)
+bool gemm_is_prefill(const GemmShape& a);
+kd_status gemm_prefill_prepare(const GemmShape& a, const void* X, const void* W, GemmPlan* gp);
+kd_status launch_gemm_prefill(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t* signals);
+uint32_t gemm_prefill_signals(const GemmShape& a);
+kd_status rope_prefill_validate(const kd_attr_rope_prefill& a);
+kd_status launch_rope_prefill(const kd_attr_rope_prefill& a, const void* qkv, const int32_t* bt, void* q_out, void* kc,
+                              void* vc, const LaunchCtx& c, uint32_t* signals);
+uint32_t rope_prefill_signals(const kd_attr_rope_prefill& a);
+kd_status prefill_attention_validate(const kd_attr_prefill_attention& a);
+kd_status launch_prefill_attention(const kd_attr_prefill_attention& a, const void* q, const void* kc, const void* vc,
+                                   const int32_t* bt, void* out, const LaunchCtx& c, uint32_t* signals);
+uint32_t prefill_attention_signals(const kd_attr_prefill_attention& a);
 kd_status gemm_prepare(const GemmShape& sh, const void* X, const void* W, const void* meta, GemmPlan* gp);
 kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t* signals);
 

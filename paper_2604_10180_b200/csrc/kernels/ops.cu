@@ -75,7 +75,9 @@ kd_status kd_op_scratch_bytes(uint32_t op, const void* attrs, uint64_t* bytes) {
     case KD_OP_ADD_RMSNORM:
     case KD_OP_ROPE_APPEND:
     case KD_OP_SILU_MUL:
-    case KD_OP_RESIDUAL_ADD: *bytes = 0; return KD_OK;
+    case KD_OP_RESIDUAL_ADD:
+    case KD_OP_ROPE_PREFILL:
+    case KD_OP_PREFILL_ATTENTION: *bytes = 0; return KD_OK;
   }
   return fail(KD_ERR_INVALID_ARG, "kd_op_scratch_bytes: unknown op");
 }
@@ -176,6 +178,22 @@ kd_status kd_op_attention(const kd_attr_attention* a, const void* q, const void*
   c.stream = (cudaStream_t)stream;
   c.scratch = scratch;
   return launch_attention(*a, q, k_cache, v_cache, block_table, seq_len, out, c, nullptr);
+}
+
+kd_status kd_op_rope_prefill(const kd_attr_rope_prefill* a, const void* qkv, const int32_t* block_table, void* q_out,
+                             void* k_cache, void* v_cache, void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_rope_prefill: NULL attrs");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  return launch_rope_prefill(*a, qkv, block_table, q_out, k_cache, v_cache, c, nullptr);
+}
+
+kd_status kd_op_prefill_attention(const kd_attr_prefill_attention* a, const void* q, const void* k_cache,
+                                  const void* v_cache, const int32_t* block_table, void* out, void* stream) {
+  if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_prefill_attention: NULL attrs");
+  LaunchCtx c;
+  c.stream = (cudaStream_t)stream;
+  return launch_prefill_attention(*a, q, k_cache, v_cache, block_table, out, c, nullptr);
 }
 
 kd_status kd_op_silu_mul(const kd_attr_silu_mul* a, const void* gu, void* out, void* stream) {

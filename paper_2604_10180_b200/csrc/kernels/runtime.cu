@@ -113,6 +113,8 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_SSM_CONV:
     case KD_OP_SSM_UPDATE:
     case KD_OP_GATED_NORM: need = sizeof(kd_attr_ssm); break;
+    case KD_OP_ROPE_PREFILL: need = sizeof(kd_attr_rope_prefill); break;
+    case KD_OP_PREFILL_ATTENTION: need = sizeof(kd_attr_prefill_attention); break;
     default: return fail(KD_ERR_UNSUPPORTED, "runtime: unknown op");
   }
   if (k.attrs.size() != need) return fail(KD_ERR_INVALID_ARG, "runtime: op attrs have the wrong size");
@@ -157,6 +159,8 @@ kd_status check_attrs(const Kernel& k) {
     case KD_OP_SSM_CONV: ok = nr == 4 && nw == 2; break;      // reads [zx, w, b, state] writes [xbc, state]
     case KD_OP_SSM_UPDATE: ok = nr == 6 && nw == 2; break;    // reads [xbc, zx, dt_b, A_log, D, S] writes [y, S]
     case KD_OP_GATED_NORM: ok = nr == 3 && nw == 1; break;    // reads [y, zx, w]
+    case KD_OP_ROPE_PREFILL: ok = nr == 2 && nw == 3; break;  // reads [qkv, bt] writes [q, Kc, Vc]
+    case KD_OP_PREFILL_ATTENTION: ok = nr == 4 && nw == 1; break;  // reads [q, Kc, Vc, bt]
   }
   if (!ok) return fail(KD_ERR_INVALID_ARG, "runtime: wrong number of read/write spans for the op");
   return KD_OK;
@@ -262,6 +266,16 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
       auto a = attrs_get<kd_attr_moe_combine>(K);
       const uint32_t np = std::max(1u, a.n_parts);
       st = launch_moe_combine(a, (const void* const*)l.rd.data(), l.rd[np], l.rd[np + 1], l.wr[0], c, &sig);
+      break;
+    }
+    case KD_OP_ROPE_PREFILL: {
+      auto a = attrs_get<kd_attr_rope_prefill>(K);
+      st = launch_rope_prefill(a, l.rd[0], (const int32_t*)l.rd[1], l.wr[0], l.wr[1], l.wr[2], c, &sig);
+      break;
+    }
+    case KD_OP_PREFILL_ATTENTION: {
+      auto a = attrs_get<kd_attr_prefill_attention>(K);
+      st = launch_prefill_attention(a, l.rd[0], l.rd[1], l.rd[2], (const int32_t*)l.rd[3], l.wr[0], c, &sig);
       break;
     }
   }

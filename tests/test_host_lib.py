@@ -68,7 +68,7 @@ def test_fused_norm_op_host_checks(kd):
                                                        (16, K.KD_BUF_WEIGHT), (32, 0)))
     g.add_kernel(K.KD_OP_GEMM_RMSNORM, [(X, 0, 64), (W, 0, 64), (r, 0, 64), (gam, 0, 16)], [(h, 0, 32), (r, 0, 64)], a)
     with pytest.raises(K.KdError):
-        g.add_kernel(K.KD_OP_GEMM_RMSNORM + 1, [], [(h, 0, 8)])
+        g.add_kernel(K.KD_OP_PREFILL_ATTENTION + 1, [], [(h, 0, 8)])  # (the highest op id + 1)
     g.finalize()
 
 
