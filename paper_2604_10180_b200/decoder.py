@@ -289,6 +289,119 @@ class DecoderGraph:
         return [mem_dev if k.template in MEMORY_ROLE else gemm_dev for k in self.kernels]
 
 
+class PrefillGraph:
+    """f4: the PREFILL kernel graph of the same dense
+    Llama-style layer, declared on the same DAG / placement / runtime
+    machinery. S prompt tokens of each of the B sequences are processed at
+    once: every activation has B·S rows (row b·S + t), the GEMMs are
+    KD_OP_GEMM with M = B·S (the tensor-bound kernel for M > 256), RoPE runs
+    at every prompt position and fills cache slots 0..S−1
+    (KD_OP_ROPE_PREFILL), attention is causal over the prompt
+    (KD_OP_PREFILL_ATTENTION). One micro-batch (the prompt batch).
+
+      per layer l:  norm1 → qkv → rope_prefill (writes q, K_l, V_l) →
+                    prefill_attn → o → norm2 → gu → silu → down
+      after layer L−1: final residual add
+
+    Templates as DecoderGraph (rope and attention share T_ATTN: the cache
+    writers and readers stay co-located, R6). Math: oracle/prefill.py."""
+
+    def __init__(self, cfg, seq_len: int):
+        assert cfg.n_micro == 1 and not cfg.n_experts and not cfg.attn_every, "dense single-micro-batch prefill"
+        S = int(seq_len)
+        assert S % 16 == 0 and S <= cfg.pages_per_seq * cfg.page, "prompt length: multiple of 16 within the cache"
+        self.cfg, self.S = cfg, S
+        B, H, L = cfg.batch, cfg.hidden, cfg.n_layers
+        Hq, Hkv, D, F = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn
+        rows = B * S
+        self.rows = rows
+        pps = cfg.pages_per_seq
+        g = Graph()
+        self.g = g
+        self.buf: Dict[str, int] = {}
+        self.shape: Dict[str, tuple] = {}
+        self.dtype: Dict[str, str] = {}
+        W, PM = K.KD_BUF_WEIGHT, K.KD_BUF_PER_MICROBATCH
+        PERS, INP, OUT = K.KD_BUF_PERSISTENT, K.KD_BUF_INPUT, K.KD_BUF_OUTPUT
+
+        def buf(name, shape, dt, flags):
+            nbytes = int(np.prod(shape)) * {"bf16": 2, "f32": 4, "i32": 4}[dt]
+            self.buf[name] = g.add_buffer(nbytes, flags)
+            self.shape[name] = tuple(shape)
+            self.dtype[name] = dt
+            return self.buf[name]
+
+        def whole(name):
+            b = self.buf[name]
+            n = int(np.prod(self.shape[name])) * {"bf16": 2, "f32": 4, "i32": 4}[self.dtype[name]]
+            return (b, 0, n)
+
+        buf("r", (rows, H), "f32", PERS | INP | OUT | PM)
+        buf("bt", (B, pps), "i32", INP | PM)
+        for l in range(L):
+            buf(f"w_qkv.{l}", (cfg.qkv_dim, H), "bf16", W)
+            buf(f"w_o.{l}", (H, Hq * D), "bf16", W)
+            buf(f"w_gu.{l}", (2 * F, H), "bf16", W)
+            buf(f"w_d.{l}", (H, F), "bf16", W)
+            buf(f"g1.{l}", (H,), "bf16", W)
+            buf(f"g2.{l}", (H,), "bf16", W)
+            buf(f"kc.{l}", (B * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+            buf(f"vc.{l}", (B * pps, Hkv, cfg.page, D), "bf16", PERS | PM)
+            for nm, shp in (("h1", (rows, H)), ("qkv", (rows, cfg.qkv_dim)), ("q", (rows, Hq * D)),
+                            ("attn", (rows, Hq * D)), ("o", (rows, H)), ("h2", (rows, H)), ("gu", (rows, 2 * F)),
+                            ("a", (rows, F)), ("d", (rows, H))):
+                buf(f"{nm}.{l}", shp, "bf16", PM)
+        self.kernels: List[KernelInfo] = []
+
+        def add(name, layer, tmpl, op, reads, writes, attrs, flops=0):
+            span = lambda x: x if isinstance(x, tuple) else whole(x)
+            kid = g.add_kernel(op, [span(x) for x in reads], [span(x) for x in writes], attrs, flops, -1, tmpl)
+            self.kernels.append(KernelInfo(name, layer, tmpl, kid))
+            return kid
+
+        eps, bf = float(cfg.eps), K.KD_BF16
+        attn_flops = 2 * B * Hq * D * S * (S + 64)  # causal QKᵀ + PV over the computed (diagonal-padded) blocks
+        for l in range(L):
+            has_d = 1 if l > 0 else 0
+            add("norm1", l, T_RESID, K.KD_OP_ADD_RMSNORM, ["r"] + ([f"d.{l-1}"] if has_d else []) + [f"g1.{l}"],
+                [f"h1.{l}", "r"], K.kd_attr_add_rmsnorm(rows, H, has_d, bf, eps, 0))
+            add("qkv", l, T_QKV, K.KD_OP_GEMM, [f"h1.{l}", f"w_qkv.{l}"], [f"qkv.{l}"],
+                K.kd_attr_gemm(rows, cfg.qkv_dim, H, bf), 2 * rows * cfg.qkv_dim * H)
+            add("rope", l, T_ATTN, K.KD_OP_ROPE_PREFILL, [f"qkv.{l}", "bt"], [f"q.{l}", f"kc.{l}", f"vc.{l}"],
+                K.kd_attr_rope_prefill(B, S, Hq, Hkv, D, cfg.page, pps, bf, float(cfg.rope_theta)))
+            add("attn", l, T_ATTN, K.KD_OP_PREFILL_ATTENTION, [f"q.{l}", f"kc.{l}", f"vc.{l}", "bt"], [f"attn.{l}"],
+                K.kd_attr_prefill_attention(B, S, Hq, Hkv, D, cfg.page, pps, bf), attn_flops)
+            add("o", l, T_O, K.KD_OP_GEMM, [f"attn.{l}", f"w_o.{l}"], [f"o.{l}"],
+                K.kd_attr_gemm(rows, H, Hq * D, bf), 2 * rows * H * Hq * D)
+            add("norm2", l, T_RESID, K.KD_OP_ADD_RMSNORM, ["r", f"o.{l}", f"g2.{l}"], [f"h2.{l}", "r"],
+                K.kd_attr_add_rmsnorm(rows, H, 1, bf, eps, 0))
+            add("gu", l, T_GU, K.KD_OP_GEMM, [f"h2.{l}", f"w_gu.{l}"], [f"gu.{l}"],
+                K.kd_attr_gemm(rows, 2 * F, H, bf), 2 * rows * 2 * F * H)
+            add("silu", l, T_SILU, K.KD_OP_SILU_MUL, [f"gu.{l}"], [f"a.{l}"], K.kd_attr_silu_mul(rows, F, bf, 0))
+            add("down", l, T_DOWN, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
+                K.kd_attr_gemm(rows, H, F, bf), 2 * rows * H * F)
+        add("final_add", L - 1, T_RESID, K.KD_OP_RESIDUAL_ADD, ["r", f"d.{L-1}"], ["r"],
+            K.kd_attr_residual_add(rows, H, 1, bf))
+        g.finalize()
+
+    def role_assign(self, mem_dev: int = 0, gemm_dev: int = 1) -> List[int]:
+        """Norms, RoPE + cache fill, attention and SiLU on one device, GEMMs on another."""
+        return [mem_dev if k.template in MEMORY_ROLE else gemm_dev for k in self.kernels]
+
+    def host_value(self, name, i, inputs):
+        """Exact host values from synth.DecoderInputs whose x has B·S rows."""
+        base, _, lay = name.partition(".")
+        if name == "r":
+            return np.asarray(inputs.x, np.float32)
+        if name == "bt":
+            return np.asarray(inputs.block_table, np.int32)
+        if base in ("kc", "vc"):
+            return (inputs.k_cache if base == "kc" else inputs.v_cache)[int(lay)]
+        lw = inputs.layers[int(lay)]
+        return {"w_qkv": lw.w_qkv, "w_o": lw.w_o, "w_gu": lw.w_gu, "w_d": lw.w_d, "g1": lw.gamma1,
+                "g2": lw.gamma2}[base]
+
+
 class TPDecoderGraph:
     """Tensor-parallel disaggregated decoder graph (BJ config 3):
     T GEMM ranks (logical devices T..2T−1) each paired with a memory-role
