@@ -10,7 +10,8 @@
 //    256-column TMEM accumulators, so the 4 epilogue warps (tcgen05.ld →
 //    bf16 → global) drain tile i while tile i+1 accumulates.
 //  * RoPE at every prompt position + paged KV fill (KD_OP_ROPE_PREFILL):
-//    rope_append_kernel's per-element arithmetic with position t = r mod S.
+//    rope_append_kernel's per-element arithmetic with position t = r mod S,
+//    the row's (cos, sin) pairs formed once per token in shared memory.
 //  * causal GQA attention (KD_OP_PREFILL_ATTENTION): FlashAttention-2 style —
 //    a CTA owns 64 query tokens of one head, 4 consumer warps × 16 tokens;
 //    a producer warp streams 64-key blocks of the paged K/V cache (one TMA per
@@ -210,26 +211,40 @@ static int device_sms() {
 }
 
 // ======================================================================= RoPE + KV fill
-constexpr int kRopeHeadsPerCta = 8;
+constexpr int kRopeThreads = 256;
 struct RopeFreq {
   double f[128];
 };
 
-__global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
+// one CTA per token row: the row's D/2 (cos, sin) pairs are computed once
+// (rope_append_kernel's arithmetic: fp64 angle reduced to [−π, π], fp32
+// sincos of the reduced angle) into shared memory, then every (head, 8-dim
+// group) of the row is rotated / copied with 16-byte loads and stores
+__global__ void __launch_bounds__(kRopeThreads)
     rope_prefill_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ bt,
                         __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kc,
                         __nv_bfloat16* __restrict__ vc, int S, int Hq, int Hkv, int D, int page, int pps,
                         const __grid_constant__ RopeFreq fr, Epi epi) {
+  __shared__ float s_c[128], s_s[128];
   pdl_launch_dependents();
-  pdl_wait();
   const int r = blockIdx.x, half = D / 2, G = Hq / Hkv;
   const int b = r / S, pos = r - b * S;
-  const int hh = blockIdx.y * kRopeHeadsPerCta + (int)(threadIdx.x >> 4), t16 = threadIdx.x & 15;
-  const int n_rot = Hq + Hkv;
+  for (int i = threadIdx.x; i < half; i += kRopeThreads) {
+    const double ang = (double)pos * fr.f[i];
+    const double kk = rint(ang * 0.15915494309189535);
+    const double red = fma(-kk, 6.283185307179586, fma(-kk, 2.4492935982947064e-16, ang));
+    sincosf((float)red, &s_s[i], &s_c[i]);
+  }
+  __syncthreads();
+  pdl_wait();
   const __nv_bfloat16* src = qkv + (size_t)r * (Hq + 2 * Hkv) * D;
   const int32_t pg = __ldg(bt + (size_t)b * pps + pos / page);
-  if (hh < n_rot) {
-    for (int i0 = t16 * 8; i0 < half; i0 += 128) {
+  const int gpr = half / 8;                      // 8-dim groups per rotated half-head
+  const int n_rot = (Hq + Hkv) * gpr;            // rotation work items: q heads, then k heads
+  const int n_v = Hkv * (D / 8);                 // v copy items
+  for (int w = threadIdx.x; w < n_rot + n_v; w += kRopeThreads) {
+    if (w < n_rot) {
+      const int hh = w / gpr, i0 = (w - hh * gpr) * 8;
       const __nv_bfloat16* x;
       __nv_bfloat16* dst;
       size_t qoff = 0;
@@ -246,14 +261,6 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
       }
       const uint4 xa = *reinterpret_cast<const uint4*>(x + i0);
       const uint4 xb = *reinterpret_cast<const uint4*>(x + half + i0);
-      float c[8], sn[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {  // rope_append_kernel's angle: fp64, reduced to [−π, π], fp32 sincos
-        const double ang = (double)pos * fr.f[i0 + k];
-        const double kk = rint(ang * 0.15915494309189535);
-        const double red = fma(-kk, 6.283185307179586, fma(-kk, 2.4492935982947064e-16, ang));
-        sincosf((float)red, &sn[k], &c[k]);
-      }
       const uint32_t* pa = &xa.x;
       const uint32_t* pb = &xb.x;
       uint4 lo, hi;
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) {
         const float x0 = bf16lo(pa[qq]), x1 = bf16hi(pa[qq]), y0 = bf16lo(pb[qq]), y1 = bf16hi(pb[qq]);
-        const float c0 = c[2 * qq], c1 = c[2 * qq + 1], s0 = sn[2 * qq], s1 = sn[2 * qq + 1];
+        const float c0 = s_c[i0 + 2 * qq], c1 = s_c[i0 + 2 * qq + 1], s0 = s_s[i0 + 2 * qq], s1 = s_s[i0 + 2 * qq + 1];
         plo[qq] = pack_bf16(x0 * c0 - y0 * s0, x1 * c1 - y1 * s1);
         phi[qq] = pack_bf16(y0 * c0 + x0 * s0, y1 * c1 + x1 * s1);
       }
@@ -274,12 +281,12 @@ __global__ void __launch_bounds__(kRopeHeadsPerCta * 16)
           *reinterpret_cast<uint4*>(pd + i0) = lo;
           *reinterpret_cast<uint4*>(pd + half + i0) = hi;
         }
+    } else {
+      const int v = w - n_rot, g = v / (D / 8), c8 = (v - g * (D / 8)) * 8;
+      const __nv_bfloat16* x = src + (size_t)g * (G + 2) * D + (size_t)(G + 1) * D;
+      __nv_bfloat16* dst = vc + (((size_t)pg * Hkv + g) * page + pos % page) * D;
+      *reinterpret_cast<uint4*>(dst + c8) = *reinterpret_cast<const uint4*>(x + c8);
     }
-  } else if (hh < n_rot + Hkv) {
-    const int g = hh - n_rot;
-    const __nv_bfloat16* x = src + (size_t)g * (G + 2) * D + (size_t)(G + 1) * D;
-    __nv_bfloat16* dst = vc + (((size_t)pg * Hkv + g) * page + pos % page) * D;
-    for (int c8 = t16 * 8; c8 < D; c8 += 128) *reinterpret_cast<uint4*>(dst + c8) = *reinterpret_cast<const uint4*>(x + c8);
   }
   epi_signal(epi);
 }
@@ -552,15 +559,12 @@ kd_status launch_gemm_prefill(const GemmPlan& gp, void* Y, const LaunchCtx& c, u
   return KD_OK;
 }
 
-static dim3 rope_prefill_grid(const kd_attr_rope_prefill& a) {
-  const int heads = (int)(a.n_heads + 2 * a.n_kv_heads);
-  return dim3(a.seqs * a.seq_len, (heads + pre::kRopeHeadsPerCta - 1) / pre::kRopeHeadsPerCta);
-}
+static dim3 rope_prefill_grid(const kd_attr_rope_prefill& a) { return dim3(a.seqs * a.seq_len); }
 
 kd_status rope_prefill_validate(const kd_attr_rope_prefill& a) {
   if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "rope_prefill: bf16 only");
   if (a.seqs == 0 || a.seq_len == 0 || a.n_kv_heads == 0 || a.n_heads % a.n_kv_heads || a.head_dim % 16 ||
-      a.head_dim > 256 || a.page == 0 || (uint64_t)a.pages_per_seq * a.page < a.seq_len)
+      a.head_dim > 256 || a.page == 0 || (uint64_t)a.pages_per_seq * a.page < a.seq_len)  // (D/2 ≤ 128 table)
     return fail(KD_ERR_UNSUPPORTED, "rope_prefill: unsupported shape (head_dim % 16, pages cover the prompt)");
   return KD_OK;
 }
@@ -574,7 +578,7 @@ kd_status launch_rope_prefill(const kd_attr_rope_prefill& a, const void* qkv, co
   const double l2t = std::log2(a.theta);
   for (uint32_t i = 0; i < a.head_dim / 2; ++i) fr.f[i] = std::exp2(-2.0 * (double)i / (double)a.head_dim * l2t);
   const dim3 grid = rope_prefill_grid(a);
-  KD_CUDA_CHECK(kd_launch(pre::rope_prefill_kernel, grid, dim3(pre::kRopeHeadsPerCta * 16), 0, c.stream,
+  KD_CUDA_CHECK(kd_launch(pre::rope_prefill_kernel, grid, dim3(pre::kRopeThreads), 0, c.stream,
                           (const __nv_bfloat16*)qkv, bt, (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc,
                           (int)a.seq_len, (int)a.n_heads, (int)a.n_kv_heads, (int)a.head_dim, (int)a.page,
                           (int)a.pages_per_seq, fr, c.epi),
