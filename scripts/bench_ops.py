@@ -57,6 +57,16 @@ def gemm(M, N, Kd, copies):
     return us, b
 
 
+def gemm_cublas(M, N, Kd, copies):
+    """The same decode GEMM through torch.matmul (cuBLAS / cuBLASLt), same
+    rotating weight copies: the library baseline beside our kernels."""
+    X = torch.randn(M, Kd, device="cuda").to(torch.bfloat16)
+    Ws = [torch.randn(N, Kd, device="cuda").to(torch.bfloat16) * (1 / math.sqrt(Kd)) for _ in range(copies)]
+    Y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    us = timeit(lambda i: torch.matmul(X, Ws[i % copies].t(), out=Y))
+    return us, N * Kd * 2 + M * Kd * 2 + M * N * 2
+
+
 def gemm_norm(M, N, Kd, copies):
     """O/down GEMM with the fused residual add + RMSNorm epilogue (KD_OP_GEMM_RMSNORM)."""
     a = K.kd_attr_gemm_rmsnorm(M, N, Kd, K.KD_BF16, 1e-5, 0)
@@ -226,7 +236,9 @@ def main():
              ("gemm_qkv_rope", lambda: qkv_rope(m, 4096, 32, 8, 128, 4096, 4)),
              ("gemm_down_norm", lambda: gemm_norm(m, 4096, 14336, 2)),
              ("attention", lambda: attention(m, 32, 8, 128, 4096)),
-             ("gemm_overhead_1kb", lambda: gemm(m, 128 * 148, 64, 2))]
+             ("gemm_overhead_1kb", lambda: gemm(m, 128 * 148, 64, 2)),
+             ("cublas_qkv", lambda: gemm_cublas(m, 6144, 4096, 4)), ("cublas_o", lambda: gemm_cublas(m, 4096, 4096, 5)),
+             ("cublas_gu", lambda: gemm_cublas(m, 28672, 4096, 2)), ("cublas_down", lambda: gemm_cublas(m, 4096, 14336, 2))]
     for grp, fn in (("ssm", ssm_ops), ("moe", moe_ops)):
         if args.only == grp or args.only == "all2":
             for name, us, b in fn():
