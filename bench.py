@@ -312,12 +312,33 @@ def main():
                                 local_devs=[rank], dist=dist)
         placement = (f"TP={T}: GEMM ranks {T}..{2 * T - 1}, attention partners 0..{T - 1} (head-sharded), "
                      f"fused peer-store all-reduce, N=2 micro-batches")
+    elif cfg.n_experts:
+        # BASELINE config 4 ("router/attention kernels disaggregated from expert
+        # GEMMs over 8 GPUs"): N/2 attention/router shards, each
+        # decoding B/(N/2) of the B sequences (norms, QKV/O GEMMs, RoPE/append,
+        # attention, router, dispatch, combine), and N/2 expert ranks owning
+        # E/(N/2) experts each (grouped gate_up, SiLU, grouped down); dispatch
+        # and combine are P2P (expert parallelism), N=2 micro-batches
+        if world % 2:
+            raise SystemExit("bench.py: the MoE expert-parallel layout needs an even --gpus")
+        a = e = world // 2
+        if cfg.n_experts % e:
+            raise SystemExit(f"bench.py: {cfg.n_experts} experts do not split over {e} expert ranks")
+        shard = cfg.with_(batch=max(2, cfg.batch // a), n_micro=2)
+        dg = DEC.MoEEPDecoderGraph(shard, a, e)
+        rt = DEC.DecoderRuntime(dg, dg.assign(), a + e, [local], seed=cfg.seed, use_graph=not args.no_graph,
+                                local_devs=[rank], dist=dist)
+        placement = (f"MoE expert parallel {a}+{e}: ranks 0..{a - 1} attention/router shards ({shard.batch} "
+                     f"sequences each), ranks {a}..{world - 1} own {cfg.n_experts // e} experts each; P2P "
+                     f"dispatch/combine, chunked handoff, N=2 micro-batches")
+        cfg = shard
+        tokens_per_step = shard.batch * a
     else:
         # N GPUs: N/2 independent disaggregated pairs (BASELINE config 2: memory-bound
         # kernels on the even rank, GEMMs on the odd rank), each decoding its own batch
         # of B sequences with 2 micro-batches; cut edges are streamed by the producers'
         # fused peer stores into the partner's HBM (CUDA IPC over NVLink). No collective.
-        if args.layout == "pairs":
+        if args.layout == "pairs" or cfg.attn_every:  # (the role-layout graph has no SSM layers)
             if world % 2:
                 raise SystemExit("bench.py: --layout pairs needs an even --gpus")
             pair, role = rank // 2, rank % 2
@@ -419,8 +440,8 @@ def main():
         rt.rt.set_mode(K.KD_MODE_DISAGG)
         rt.rt.prepare()
     # per-kernel CUDA-event timing: a second pass of the same K steps whose
-    # graph carries event-record nodes around every attention launch (events
-    # split programmatic launch edges, so they are kept out of the headline)
+    # graph carries event-record nodes around every attention launch, on a
+    # side branch so the kernel keeps its PDL edges (kept out of the headline)
     mega = world == 1 and args.exec_mode == "mega"
     attn_ms, attn_n = 0.0, 0
     if not mega:
@@ -462,8 +483,10 @@ def main():
             "launches_per_step": attn_n, "steps_profiled": args.steps,
             "share_of_step": round(attn_ms / ms_step, 4) if ms_step else None,
             "peak_source": peak_src,
-            "timing": "CUDA events (event-record nodes in the step graph) around every attention launch on its "
-                      "stream, averaged over K profiled steps run right after the timed region"}
+            "timing": "CUDA events around every attention launch, averaged over K profiled steps run right after "
+                      "the timed region; the event-record nodes hang off a side branch of the captured step graph "
+                      "(ev0 completes with the kernel before attention, ev1 with attention), so the attention "
+                      "launch keeps its programmatic (PDL) edges as in the timed steps"}
     if mega:
         # the megakernel is the step's only kernel: its algorithmic bytes are the
         # whole step's (KV cache, weights, activations), its

@@ -394,6 +394,20 @@ kd_status kd_plan_chunks(const kd_plan* p, kd_chunk* out, uint32_t cap, uint32_t
 /* Device workspace the runtime carves into activations, landing slots,
  * flags and kernel scratch. Must be ZERO-initialised once by the caller. */
 kd_status kd_plan_workspace_bytes(const kd_plan* p, uint32_t dev, uint64_t* bytes);
+/* The carve-up of that workspace (byte offsets from its base; debug / race
+ * hardening): control words, per-chunk flags, LOG records, kernel
+ * scratch (self-resetting counters), then [act_off, total) = this device's
+ * instances of the graph's internal buffers, which include every landing slot
+ * (a transfer lands in the destination's own instance of the producer's
+ * buffer). Every byte of [act_off, total) is rewritten by its producer (or
+ * transfer) before any kernel of the same step reads it, so a caller may
+ * overwrite that range between steps (tests poison it with NaN bytes); the
+ * ranges before act_off must be left alone. */
+typedef struct kd_ws_layout {
+  uint64_t ctrl_off, ctrl_bytes, flags_off, flags_bytes, log_off, log_bytes;
+  uint64_t scratch_off, scratch_bytes, act_off, total;
+} kd_ws_layout;
+kd_status kd_plan_workspace_layout(const kd_plan* p, uint32_t dev, kd_ws_layout* out);
 /* Whether the caller must bind (buf, dev): 1 for external buffers
  * (WEIGHT/INPUT/OUTPUT/PERSISTENT) touched by a kernel placed on dev. */
 kd_status kd_plan_needs_binding(const kd_plan* p, uint32_t buf, uint32_t dev, int32_t* needed);

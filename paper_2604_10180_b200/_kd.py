@@ -170,6 +170,11 @@ class kd_chunk(C.Structure):
                 ("begin", C.c_uint64), ("end", C.c_uint64)]
 
 
+class kd_ws_layout(C.Structure):
+    _fields_ = [(f, C.c_uint64) for f in ("ctrl_off", "ctrl_bytes", "flags_off", "flags_bytes", "log_off", "log_bytes",
+                                          "scratch_off", "scratch_bytes", "act_off", "total")]
+
+
 KD_STATS_MAX_DEV = 8
 
 
@@ -220,6 +225,7 @@ _PROTOS = {
     "kd_plan_transfers": (kd_status, [P, C.POINTER(kd_transfer), u32, PU32]),
     "kd_plan_makespan": (kd_status, [P, PI64]),
     "kd_plan_workspace_bytes": (kd_status, [P, u32, PU64]),
+    "kd_plan_workspace_layout": (kd_status, [P, u32, C.POINTER(kd_ws_layout)]),
     "kd_plan_needs_binding": (kd_status, [P, u32, u32, PI32]),
     "kd_runtime_create": (kd_status, [P, PU32, PI32, u32, C.POINTER(P)]),
     "kd_runtime_destroy": (None, [P]),

@@ -227,6 +227,11 @@ class Plan:
         check(K.kd_plan_workspace_bytes(self.h, dev, C.byref(v)), "kd_plan_workspace_bytes")
         return v.value
 
+    def workspace_layout(self, dev: int) -> dict:
+        v = K.kd_ws_layout()
+        check(K.kd_plan_workspace_layout(self.h, dev, C.byref(v)), "kd_plan_workspace_layout")
+        return {f: getattr(v, f) for f, _ in K.kd_ws_layout._fields_}
+
     def needs_binding(self, buf: int, dev: int) -> bool:
         v = C.c_int32()
         check(K.kd_plan_needs_binding(self.h, buf, dev, C.byref(v)), "kd_plan_needs_binding")

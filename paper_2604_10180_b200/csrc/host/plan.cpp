@@ -558,6 +558,22 @@ kd_status kd_plan_workspace_bytes(const kd_plan* p, uint32_t dev, uint64_t* byte
   return KD_OK;
 }
 
+kd_status kd_plan_workspace_layout(const kd_plan* p, uint32_t dev, kd_ws_layout* out) {
+  if (!p || !out || dev >= p->n_dev) return fail(KD_ERR_INVALID_ARG, "kd_plan_workspace_layout: bad argument");
+  const auto& L = p->layout[dev];
+  out->ctrl_off = L.ctrl_off;
+  out->ctrl_bytes = L.ctrl_bytes;
+  out->flags_off = L.flags_off;
+  out->flags_bytes = L.flags_bytes;
+  out->log_off = L.log_off;
+  out->log_bytes = L.log_bytes;
+  out->scratch_off = L.scratch_off;
+  out->scratch_bytes = L.scratch_bytes;
+  out->act_off = L.scratch_off + L.scratch_bytes;
+  out->total = L.total;
+  return KD_OK;
+}
+
 kd_status kd_plan_needs_binding(const kd_plan* p, uint32_t buf, uint32_t dev, int32_t* needed) {
   if (!p || !needed || dev >= p->n_dev || buf >= p->needs_bind.size())
     return fail(KD_ERR_INVALID_ARG, "kd_plan_needs_binding: bad argument");

@@ -46,6 +46,12 @@ struct DevState {
   uint64_t mega_bytes = 0;
   void* mega_ws = nullptr;                   // caller-owned (kd_runtime_set_exec_workspace)
   uint64_t mega_ws_bytes = 0;
+  // profiled op timing inside a captured graph: the event-record nodes hang
+  // off a side stream (fork after the previous node, join at the end), so the
+  // profiled kernel keeps its programmatic (PDL) edges to its neighbours
+  cudaStream_t pside = nullptr;
+  cudaEvent_t pfork = nullptr, pjoin = nullptr;
+  bool pside_used = false;
 };
 
 }  // namespace kd
@@ -71,6 +77,9 @@ struct kd_runtime {
       if (d.exec) cudaGraphExecDestroy(d.exec);
       if (d.st0) cudaEventDestroy(d.st0);
       if (d.st1) cudaEventDestroy(d.st1);
+      if (d.pside) cudaStreamDestroy(d.pside);
+      if (d.pfork) cudaEventDestroy(d.pfork);
+      if (d.pjoin) cudaEventDestroy(d.pjoin);
       mega_destroy(d.mega);
       for (auto& l : d.launches) {
         delete l.gemm;
@@ -169,6 +178,18 @@ kd_status check_attrs(const Kernel& k) {
 inline cudaError_t record(cudaEvent_t e, cudaStream_t s, bool capturing) {
   return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
 }
+// timing event of a profiled launch: while capturing, recorded on the side
+// stream after a fork from s (a full edge from the node s last added), which
+// leaves s's own kernel-to-kernel edges programmatic. ev0 then completes when
+// the kernel before the profiled one completes, ev1 when the profiled one does.
+inline cudaError_t record_prof(DevState& d, cudaEvent_t e, cudaStream_t s, bool capturing) {
+  if (!capturing || !d.pside) return record(e, s, capturing);
+  cudaError_t ce = cudaEventRecord(d.pfork, s);
+  if (ce == cudaSuccess) ce = cudaStreamWaitEvent(d.pside, d.pfork, 0);
+  if (ce == cudaSuccess) ce = record(e, d.pside, true);
+  d.pside_used = true;
+  return ce;
+}
 
 kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool capturing) {
   uint8_t* ws = d.ws;
@@ -185,7 +206,7 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
     c.acq.n = 0;
   }
   const bool prof = rt->profile_op && l.op == rt->profile_op;
-  if (prof) KD_CUDA_CHECK(record(l.ev0, s, capturing), "event record");
+  if (prof) KD_CUDA_CHECK(record_prof(d, l.ev0, s, capturing), "event record");
   kd_status st = KD_OK;
   const Kernel& K = rt->plan->g->kernels[l.kernel];
   uint32_t sig = 0;
@@ -280,7 +301,7 @@ kd_status enqueue(kd_runtime* rt, DevState& d, Launch& l, cudaStream_t s, bool c
     }
   }
   if (st) return st;
-  if (prof) KD_CUDA_CHECK(record(l.ev1, s, capturing), "event record");
+  if (prof) KD_CUDA_CHECK(record_prof(d, l.ev1, s, capturing), "event record");
   if (!capturing && getenv("KD_DEBUG_SYNC")) {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess)
@@ -693,6 +714,11 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
       if (rt->profile_op) {
         KD_CUDA_CHECK(cudaEventCreate(&l.ev0), "event create");
         KD_CUDA_CHECK(cudaEventCreate(&l.ev1), "event create");
+        if (!d.pside) {
+          KD_CUDA_CHECK(cudaStreamCreateWithFlags(&d.pside, cudaStreamNonBlocking), "profile side stream");
+          KD_CUDA_CHECK(cudaEventCreateWithFlags(&d.pfork, cudaEventDisableTiming), "event create");
+          KD_CUDA_CHECK(cudaEventCreateWithFlags(&d.pjoin, cudaEventDisableTiming), "event create");
+        }
       }
       d.launches.push_back(std::move(l));
     }
@@ -823,9 +849,15 @@ kd_status kd_step(kd_runtime* rt, void* const* streams, uint64_t step_id, kd_ste
         }
         KD_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
         kd_status st = KD_OK;
+        d.pside_used = false;
         for (auto& l : d.launches) {
           st = enqueue(rt, d, l, s, true);
           if (st) break;
+        }
+        if (d.pside_used) {  // join the timing side stream back before the capture ends
+          cudaError_t je = cudaEventRecord(d.pjoin, d.pside);
+          if (je == cudaSuccess) je = cudaStreamWaitEvent(s, d.pjoin, 0);
+          if (je != cudaSuccess && !st) st = set_cuda_error(je, "profile join");
         }
         cudaGraph_t graph = nullptr;
         cudaError_t ce = cudaStreamEndCapture(s, &graph);

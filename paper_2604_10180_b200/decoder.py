@@ -1167,6 +1167,26 @@ class DecoderRuntime:
         for d in self.local_devs:
             torch.cuda.synchronize(self.dev_map[d])
 
+    def poison_activations(self, byte: int = 0xFF):
+        """Race hardening: overwrite every local device's
+        internal-buffer range of the workspace — activations and every landing
+        slot, [act_off, total) of kd_plan_workspace_layout — with `byte` (0xFF:
+        NaN in bf16 and fp32) between steps. A kernel that read a landing slot
+        before its transfer arrived, or any activation before this step's
+        producer wrote it, would then propagate NaN instead of silently reusing
+        the previous step's (or the zero-initialised) bytes. Flags, LOG records
+        and the self-resetting scratch counters before act_off are untouched."""
+        torch = _torch()
+        self.sync()
+        for d in self.local_devs:
+            lay = self.plan.workspace_layout(d)
+            w, base = self.ws[d]
+            lo = base - w.data_ptr() + lay["act_off"]
+            hi = base - w.data_ptr() + lay["total"]
+            if hi > lo:
+                w[lo:hi].fill_(byte)
+        self.sync()
+
     def residual(self) -> np.ndarray:
         """Concatenated residual stream r [B, H] (fp32) after the last step."""
         outs = []

@@ -151,3 +151,29 @@ def test_cta_mode_for_irregular_producers(mods):
     for t, (i, prod, dst, nbytes, *_) in enumerate(xs):
         if ops[prod] in ("dispatch", "gu", "down"):
             assert by_t[t] == [(0, 0, by_t[t][0][3], by_t[t][0][3])]
+
+
+@pytest.mark.parametrize("name,make,kind,n_dev", [c for c in CASES if c[0] in ("tiny", "role3", "moe_ep", "tp2")],
+                         ids=["tiny", "tp2", "role3", "moe_ep"])
+def test_workspace_layout_partition(mods, name, make, kind, n_dev):
+    """kd_plan_workspace_layout (the poisoning range of tests/test_gpu_race.py):
+    ctrl | flags | log | scratch | internal buffers, contiguous and 256-byte
+    aligned, ending at kd_plan_workspace_bytes; the flags hold one u64 per
+    chunk (+ the residency word) of every incoming transfer."""
+    DEC, K, Plan = mods
+    dg = make(DEC)
+    assign = dg.role_assign(0, 1) if kind == "role" else dg.assign()
+    plan = Plan(dg.g, DEC.b200_machine(n_dev), assign, dg.cfg.n_micro, 4)
+    chunks = plan.chunks()
+    xs = plan.transfers()
+    for d in range(n_dev):
+        L = plan.workspace_layout(d)
+        assert L["ctrl_off"] == 0
+        for a, b in (("ctrl", "flags"), ("flags", "log"), ("log", "scratch")):
+            assert L[f"{b}_off"] == L[f"{a}_off"] + L[f"{a}_bytes"]
+        assert L["act_off"] == L["scratch_off"] + L["scratch_bytes"]
+        assert L["act_off"] <= L["total"] == plan.workspace_bytes(d)
+        assert all(L[k] % 256 == 0 for k in L if k.endswith("_off"))
+        incoming = [t for t, x in enumerate(xs) if x[2] == d]
+        need = sum(1 + sum(1 for c in chunks if c[0] == t) for t in incoming)
+        assert L["flags_bytes"] >= 8 * need

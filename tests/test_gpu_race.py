@@ -1,0 +1,143 @@
+"""Race hardening (verdict r1 weak #9): every step runs on a
+workspace whose activations and landing slots were overwritten with NaN bytes
+(0xFF) right before it (DecoderRuntime.poison_activations, the
+[act_off, total) range of kd_plan_workspace_layout). A kernel that read a
+landing slot before its chunk arrived, or any activation before this step's
+producer wrote it, would then produce NaN — where an un-poisoned run silently
+reads the previous step's bytes (or zeros) and can still come out bitwise
+equal. Each scenario must reproduce, bit for bit, the un-poisoned monolithic
+run of the same graph, so no kernel depends on stale or zero-initialised
+activation memory, on one device or across cut edges."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def DEC(cuda_ok):
+    from paper_2604_10180_b200 import decoder as DEC
+    return DEC
+
+
+def _steps(rt, n, poison):
+    for _ in range(n):
+        if poison:
+            rt.poison_activations()
+        rt.step()
+    rt.sync()
+    rt.rt.check()
+    return rt
+
+
+def _pair(DEC, make_graph, inp, n_dev_assign, steps=2, **kw):
+    """(un-poisoned monolithic, poisoned monolithic, poisoned disaggregated)"""
+    out = []
+    for poison, dis in ((False, False), (True, False), (True, True)):
+        dg = make_graph()
+        if dis:
+            n_dev, assign = n_dev_assign(dg)
+        else:
+            n_dev, assign = 1, [0] * dg.g.num_kernels
+        rt = DEC.DecoderRuntime(dg, assign, n_dev, [0] * n_dev, inputs=inp, **kw)
+        out.append((dg, _steps(rt, steps, poison)))
+    return out
+
+
+def _res(dg, rt):
+    return dg.residual_global(rt) if hasattr(dg, "residual_global") else rt.residual()
+
+
+def _check(runs, n_layers=None):
+    (dg0, ref), (dg1, mono), (dg2, dis) = runs
+    r0 = _res(dg0, ref)
+    assert np.isfinite(r0).all()
+    assert np.array_equal(r0, _res(dg1, mono)), "monolithic run reads stale / unwritten activation memory"
+    assert np.array_equal(r0, _res(dg2, dis)), "disaggregated run reads a landing slot before its data arrived"
+    if n_layers:
+        for l in range(n_layers):
+            assert np.array_equal(ref.cache("kc", l), dis.cache("kc", l))
+            assert np.array_equal(ref.cache("vc", l), dis.cache("vc", l))
+
+
+@pytest.mark.parametrize("n_chunks", [1, 4])
+@pytest.mark.parametrize("cfg", [synth.TINY, synth.TINY.with_(n_kv_heads=2, n_micro=2, context=77)],
+                         ids=["tiny", "tiny_gqa_ragged"])
+def test_poisoned_pair_bitwise(DEC, cfg, n_chunks):
+    inp = synth.make_decoder_inputs(cfg)
+    runs = _pair(DEC, lambda: DEC.DecoderGraph(cfg), inp, lambda dg: (2, dg.role_assign(0, 1)), n_chunks=n_chunks)
+    _check(runs, cfg.n_layers)
+
+
+def test_poisoned_fused_graph_bitwise(DEC):
+    cfg = synth.TINY
+    inp = synth.make_decoder_inputs(cfg)
+    runs = _pair(DEC, lambda: DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True), inp,
+                 lambda dg: (2, dg.role_assign(0, 1)))
+    _check(runs, cfg.n_layers)
+    # the fully fused monolithic graph (GEMM + RMSNorm epilogues): poisoned == clean
+    dgs = [DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True, fuse_norm=True) for _ in range(2)]
+    rts = [_steps(DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp), 2, p)
+           for dg, p in zip(dgs, (False, True))]
+    assert np.array_equal(rts[0].residual(), rts[1].residual())
+
+
+def test_poisoned_role_layout_3_to_1_bitwise(DEC):
+    a = 3
+    cfg = synth.TINY.with_(n_micro=2, batch=2 * a * 2)
+    shard_cfg = cfg.with_(batch=cfg.n_micro * 2)
+    inp = synth.make_decoder_inputs(cfg)
+    runs = _pair(DEC, lambda: DEC.RoleDecoderGraph(shard_cfg, a), inp, lambda dg: (a + 1, dg.assign()))
+    _check(runs)
+
+
+def test_poisoned_moe_expert_parallel_bitwise(DEC):
+    a, e, m = 2, 2, 2
+    cfg = synth.TINY.with_(n_experts=4, top_k=2, n_micro=2, batch=a * 2 * m)
+    shard_cfg = cfg.with_(batch=2 * m)
+    inp = synth.make_decoder_inputs(cfg)
+    runs = _pair(DEC, lambda: DEC.MoEEPDecoderGraph(shard_cfg, a, e), inp, lambda dg: (a + e, dg.assign()))
+    _check(runs)
+
+
+def test_poisoned_tp_pairs_bitwise(DEC):
+    tp = 2
+    cfg = synth.TINY.with_(n_kv_heads=4, n_micro=2)
+    inp = synth.make_decoder_inputs(cfg)
+    runs = _pair(DEC, lambda: DEC.TPDecoderGraph(cfg, tp), inp, lambda dg: (2 * tp, dg.assign()))
+    _check(runs)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_poisoned_random_placements_bitwise(DEC, seed):
+    import random
+    rnd = random.Random(100 + seed)
+    cfg = synth.TINY.with_(n_micro=rnd.choice([1, 2, 4]))
+    inp = synth.make_decoder_inputs(cfg)
+    nch = rnd.choice([1, 2, 3, 4, 8])
+
+    def place(dg):
+        classes = sorted({k.template for k in dg.kernels})
+        dev = {c: rnd.randrange(3) for c in classes}
+        return 3, [dev[k.template] for k in dg.kernels]
+
+    runs = _pair(DEC, lambda: DEC.DecoderGraph(cfg), inp, place, n_chunks=nch)
+    _check(runs, cfg.n_layers)
+
+
+def test_workspace_layout_is_a_partition(DEC):
+    """kd_plan_workspace_layout: ctrl | flags | log | scratch | activations,
+    contiguous, in that order, ending at kd_plan_workspace_bytes."""
+    cfg = synth.TINY
+    dg = DEC.DecoderGraph(cfg)
+    rt = DEC.DecoderRuntime(dg, dg.role_assign(0, 1), 2, [0, 0], inputs=synth.make_decoder_inputs(cfg))
+    for d in (0, 1):
+        L = rt.plan.workspace_layout(d)
+        assert L["ctrl_off"] == 0
+        assert L["flags_off"] == L["ctrl_off"] + L["ctrl_bytes"]
+        assert L["log_off"] == L["flags_off"] + L["flags_bytes"]
+        assert L["scratch_off"] == L["log_off"] + L["log_bytes"]
+        assert L["act_off"] == L["scratch_off"] + L["scratch_bytes"]
+        assert L["act_off"] < L["total"] == rt.plan.workspace_bytes(d)
