@@ -265,7 +265,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full[s], (unsigned)(ph & 1));
         if (++st == S) st = 0, ++ph;
         asm volatile("tcgen05.fence::after_thread_sync;");
-        if (lane == 0) {
+        if (KD_MMA_WS) {  // every lane, elect.sync issues (uniform operands)
+          if (lane == 0 && i == 0) KD_TRACE(4);
+          const uint32_t a_addr = smem_u32(sa + (size_t)s * wst);
+          const uint32_t b_addr = smem_u32(sb + (size_t)s * xst);
+          for (int b = 0; b < kbs; ++b)
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              mma_bf16_ws(tmem_d, sw128_desc(a_addr + b * kStageA + 32 * k), sw128_desc(b_addr + b * xbox + 32 * k),
+                          idesc, (first && b == 0 && k == 0) ? 0u : 1u);
+          mma_commit_ws(&empty[s]);
+        } else if (lane == 0) {
           if (i == 0) KD_TRACE(4);
           const uint32_t a_addr = smem_u32(sa + (size_t)s * wst);
           const uint32_t b_addr = smem_u32(sb + (size_t)s * xst);
@@ -1139,7 +1149,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full[s], (unsigned)(ph & 1));
       if (++st == S) st = 0, ++ph;
       asm volatile("tcgen05.fence::after_thread_sync;");
-      if (lane == 0) {
+      if (KD_MMA_WS) {  // every lane, elect.sync issues (uniform operands)
+        if (lane == 0 && i == 0) KD_TRACE(4);
+        const uint32_t a_addr = smem_u32(sa + (size_t)s * wst);
+        const uint32_t b_addr = smem_u32(sb + (size_t)s * xst);
+        for (int b = 0; b < kbs; ++b)
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            mma_bf16_ws(tmem_base, sw128_desc(a_addr + b * kStageA + 32 * k), sw128_desc(b_addr + b * xbox + 32 * k),
+                        idesc, (i > 0 || b > 0 || k > 0) ? 1u : 0u);
+        mma_commit_ws(&empty[s]);
+      } else if (lane == 0) {
         if (i == 0) KD_TRACE(4);
         const uint32_t a_addr = smem_u32(sa + (size_t)s * wst);
         const uint32_t b_addr = smem_u32(sb + (size_t)s * xst);
