@@ -47,6 +47,8 @@ using gemm::mbar_arrive;
 using gemm::mbar_expect_tx;
 using gemm::mbar_init;
 using gemm::mma_bf16;
+using gemm::mma_bf16_ws;
+using gemm::mma_commit_ws;
 using gemm::mma_commit;
 using gemm::named_bar;
 using gemm::policy_evict_first;
@@ -584,15 +586,16 @@ __device__ void mma_gemm(const Task& T, int tmark, const Sm& S, const Geo& g, ui
       mwait(&S.gfull[q], ph, err, S);
       if (g.trace && lane == 0 && i + v == n - 1) stamp(g, tmark, R_MMA, 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      if (lane == 0) {
+      {  // warp-uniform issue (elect.sync inside the asm: uniform descriptors, no waterfall)
         const uint32_t a = arena + (uint32_t)(q * SPS * kSlot);
         const uint32_t bx = a + kbs * 16384;
+        const uint64_t ad0 = sw128_desc(a), bd0 = sw128_desc(bx);
         for (int b = 0; b < kbs; ++b)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_bf16(td, sw128_desc(a + b * 16384 + 32 * k), sw128_desc(bx + b * xbox + 32 * k), idesc,
-                     (v > 0 || b > 0 || k > 0) ? 1u : 0u);
-        mma_commit(&S.gempty[q]);
+            mma_bf16_ws(td, ad0 + (uint64_t)(b * 1024 + 2 * k), bd0 + (uint64_t)(b * (xbox >> 4) + 2 * k), idesc,
+                        (v > 0 || b > 0 || k > 0) ? 1u : 0u);
+        mma_commit_ws(&S.gempty[q]);
       }
       __syncwarp();
       ++gs;

@@ -38,6 +38,8 @@ using gemm::mbar_init;
 using gemm::mbar_wait;
 using gemm::mbar_wait_sleep;
 using gemm::mma_bf16;
+using gemm::mma_bf16_ws;
+using gemm::mma_commit_ws;
 using gemm::mma_commit;
 using gemm::policy_evict_first;
 using gemm::policy_evict_last;
@@ -127,12 +129,12 @@ __global__ void __launch_bounds__(kGThreads, 1)
       for (int kb = 0; kb < KB; ++kb) {
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        if (lane == 0) {
-          const uint32_t a = smem_u32(sx + (size_t)s * kXBytes), b = smem_u32(sw + (size_t)s * kWBytes);
+        {  // warp-uniform issue (elect.sync inside the asm: uniform descriptors, no waterfall)
+          const uint64_t ad = sw128_desc(smem_u32(sx + (size_t)s * kXBytes));
+          const uint64_t bd = sw128_desc(smem_u32(sw + (size_t)s * kWBytes));
 #pragma unroll
-          for (int k = 0; k < kTK / 16; ++k)
-            mma_bf16(td, sw128_desc(a + 32 * k), sw128_desc(b + 32 * k), idesc, (kb > 0 || k > 0) ? 1u : 0u);
-          mma_commit(&empty[s]);
+          for (int k = 0; k < kTK / 16; ++k) mma_bf16_ws(td, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          mma_commit_ws(&empty[s]);
         }
         __syncwarp();
         if (++s == kStages) s = 0, ph ^= 1u;
