@@ -538,6 +538,17 @@ kd_status kd_set_pdl(int32_t enable);
  * last commit, per-segment epilogue start/end, fixup start/end, exit) to
  * dev_buf[cta*32 + slot] (u64, >= 148*32 entries). NULL disables (default). */
 kd_status kd_debug_gemm_trace(void* dev_buf);
+/* Debug: step timeline. When dev_buf is non-NULL (device, zeroed, `bytes`
+ * long), launch i made after this call (e.g. the launches captured into a
+ * step graph) writes %globaltimer stamps per CTA to dev_buf[i*16384 + cta*32 +
+ * slot] (u64): GEMMs the kd_debug_gemm_trace slots, attention [0] entry, [1]
+ * producer past its dependency wait, [2] producer done, [3] epilogue done, [4]
+ * consumers done (max over CTAs' warps). Launches beyond bytes/131072 are not
+ * traced. kd_debug_timeline_kinds returns each traced launch's kind: 100 +
+ * rope + 2·norm (cluster split-K GEMM), 200 + silu (stream-K GEMM), 300
+ * (decode attention). Off by default; NULL turns it off and clears the list. */
+kd_status kd_debug_timeline(void* dev_buf, uint64_t bytes);
+kd_status kd_debug_timeline_kinds(int32_t* out, uint32_t cap, uint32_t* n);
 /* Debug: KD_EXEC_MEGAKERNEL timeline. dev_buf (device, >= n_tasks·grid·5·4
  * u64, see kd_runtime_exec_info; NULL = off) receives, for every (task, CTA,
  * role ∈ {loader, MMA, merge, workers}), the %globaltimer ns at the role's task

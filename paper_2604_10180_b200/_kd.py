@@ -250,6 +250,8 @@ _PROTOS = {
     "kd_ipc_open": (kd_status, [P, u64, C.POINTER(P)]),
     "kd_ipc_close": (kd_status, [P]),
     "kd_debug_gemm_trace": (kd_status, [P]),
+    "kd_debug_timeline": (kd_status, [P, u64]),
+    "kd_debug_timeline_kinds": (kd_status, [PI32, u32, PU32]),
     "kd_debug_mega_trace": (kd_status, [P, u32, P]),
     "kd_monitor_create": (kd_status, [u64, u32, u32, u32, C.POINTER(P)]),
     "kd_monitor_destroy": (kd_status, [P]),

@@ -62,6 +62,8 @@ struct Params {
   float* part_lse;    // [rows][Hkv][splits][G]
   unsigned* counter;  // [rows][Hkv]
   unsigned* work;     // item ticket counter (last word of the counter region)
+  unsigned long long* tl;    // kd_debug_timeline region (nullable): per CTA [0] entry, [1] producer past
+                             // its dependency wait, [2] producer done, [3] epilogue done, [4] consumers done
   unsigned long long* prof;  // KD_ATTN_PROF experiments: [0] producer empty-wait cycles, [1] consumer full-wait, [2] consumer busy, [3] pages
   int Hq, Hkv, G, pps, splits, pages_per_split;
   int rows;           // sequences; items are kv-head-major: it = (g·rows + b)·splits + split
@@ -170,6 +172,12 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
   pdl_launch_dependents();
   epi_started(P.epi);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto tl_stamp = [&](int slot) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+    atomicMax(&P.tl[blockIdx.x * 32 + slot], gt);
+  };
+  if (P.tl && threadIdx.x == 0) tl_stamp(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -259,6 +267,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
       gj = (uint32_t)n_pre;
     }
     pdl_wait();
+    if (P.tl && lane == 0) tl_stamp(1);
     int it = it0 == -2 ? fetch() : it0;
     if (it0 == -2) mine = ids_of(it, 0);
     for (int k = 0;; ++k) {
@@ -309,6 +318,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
       }
       it = it_next;
     }
+    if (P.tl && lane == 0) tl_stamp(2);
     if (P.prof && lane == 0) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
@@ -501,6 +511,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
         }
       }
     }
+    if (P.tl && lane == 0) tl_stamp(3);
     if (P.prof && lane == 0) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
@@ -643,6 +654,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
     __syncwarp();
     if (lane == 0) mbar_arrive(&cfull[cs]);
   }
+  if (P.tl && lane == 0) tl_stamp(4);
   if (P.prof && lane == 0) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
@@ -814,6 +826,7 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
   const bool do_prof = getenv("KD_ATTN_PROF") && cap == cudaStreamCaptureStatusNone;
   if (do_prof && !prof) cudaMalloc(&prof, 64 + 8 * 5 * 4096);
   P.prof = do_prof ? prof : nullptr;
+  P.tl = tl_next(300);
   static cudaEvent_t pe0 = nullptr, pe1 = nullptr;
   if (do_prof) {
     cudaMemsetAsync(prof, 0, 64 + 8 * 5 * 4096, c.stream);

@@ -1514,7 +1514,7 @@ static kd_status choose(const GemmShape& a, GemmTile* t, double* best_ns) {
   double best = -1;
   for (int s = 1; s <= 8; ++s) {
     if (force_s && s != force_s) continue;
-    const int maxc = max_clusters(s);
+    const int maxc = getenv("KD_GEMM_ANY_CLUSTERS") ? 1 << 20 : max_clusters(s);  // A/B: allow a second wave
     if (tiles > maxc) continue;
     if (a.norm && tiles * s > kNormMaxGrid) continue;  // per-CTA partial sums in scratch
     const int kbs = mma_n <= 128 ? 2 : 1;
@@ -1715,6 +1715,17 @@ kd_status gemm_prepare(const GemmShape& a, const void* X, const void* W, const v
 
 static unsigned long long* g_gemm_trace = nullptr;
 
+// step timeline (kd_debug_timeline): launch i of the captured step writes its
+// per-CTA stamps to region i (kTlRegion u64); the launch kinds are kept here
+static unsigned long long* g_tl = nullptr;
+static uint64_t g_tl_cap = 0;
+static std::vector<int32_t> g_tl_kinds;
+unsigned long long* tl_next(int32_t kind) {
+  if (!g_tl || g_tl_kinds.size() >= g_tl_cap) return nullptr;
+  g_tl_kinds.push_back(kind);
+  return g_tl + (g_tl_kinds.size() - 1) * kTlRegion;
+}
+
 // the kX kernel instance is needed when the launch streams chunked (COUNT)
 // output, acquires remote inputs in-kernel, or records residency / log words
 static bool kx_needed(const LaunchCtx& c) {
@@ -1752,7 +1763,7 @@ static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx&
   A.epi = c.epi;
   A.err = c.err;
   A.acq = c.acq;
-  A.trace = g_gemm_trace;
+  A.trace = g_gemm_trace ? g_gemm_trace : tl_next(100 + (int)gp.sh.rope + 2 * (int)gp.sh.norm);
   kd_status ks = kernels_init();
   if (ks) return ks;
   const bool x = kx_needed(c);
@@ -1806,7 +1817,7 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   A.epi = c.epi;
   A.err = c.err;
   A.acq = c.acq;
-  A.trace = g_gemm_trace;
+  A.trace = g_gemm_trace ? g_gemm_trace : tl_next(200 + (int)gp.sh.silu);
   {
     static int dbg = -1;
     if (dbg < 0) dbg = getenv("KD_GEMM_DBG") ? atoi(getenv("KD_GEMM_DBG")) : 0;
@@ -1855,6 +1866,21 @@ extern "C" kd_status kd_gemm_tiling(uint32_t M, uint32_t N, uint32_t K, int32_t*
 
 extern "C" kd_status kd_debug_gemm_trace(void* dev_buf) {  // 32 u64 stamps per CTA
   kd::g_gemm_trace = (unsigned long long*)dev_buf;
+  return KD_OK;
+}
+
+extern "C" kd_status kd_debug_timeline(void* dev_buf, uint64_t bytes) {
+  kd::g_tl = (unsigned long long*)dev_buf;
+  kd::g_tl_cap = dev_buf ? bytes / (kd::kTlRegion * 8) : 0;
+  kd::g_tl_kinds.clear();
+  return KD_OK;
+}
+
+extern "C" kd_status kd_debug_timeline_kinds(int32_t* out, uint32_t cap, uint32_t* n) {
+  if (!n) return kd::fail(KD_ERR_INVALID_ARG, "kd_debug_timeline_kinds: NULL n");
+  *n = (uint32_t)kd::g_tl_kinds.size();
+  if (out)
+    for (uint32_t i = 0; i < *n && i < cap; ++i) out[i] = kd::g_tl_kinds[i];
   return KD_OK;
 }
 

@@ -22,6 +22,11 @@ struct LaunchCtx {
 
 kd_status set_cuda_error(cudaError_t e, const char* where);
 
+// kd_debug_timeline: per-launch stamp region (512 CTAs x 32 u64) of the next
+// launch, tagged with its kind; nullptr when the timeline is off
+constexpr uint64_t kTlRegion = 512 * 32;
+unsigned long long* tl_next(int32_t kind);
+
 // PDL switch (kd_set_pdl); read at launch time
 extern bool g_pdl;
 
@@ -149,6 +154,7 @@ kd_status gemm_rmsnorm_bind(const kd_attr_gemm_rmsnorm& a, float* r, const void*
 kd_status qkv_rope_bind(const kd_attr_qkv_rope& a, const int32_t* bt, const int32_t* sl, void* q, void* kc, void* vc,
                         GemmPlan* gp);
 GemmShape gemm_shape(const kd_attr_grouped_gemm& a);
+
 // dense (non-grouped) GEMM tiling, chosen per shape and device (gemm.cu)
 struct GemmTile {
   int split = 0, kbs = 0, kblocks = 0, mt = 0 /* MMA N (tokens rounded to 16) */, stages = 0, rpo = 0, tiles = 0;

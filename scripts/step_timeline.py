@@ -1,0 +1,113 @@
+#!/usr/bin/env python3
+"""In-step timeline of the 8B decode step (kd_debug_timeline).
+
+Runs the bench's 1-GPU monolithic step (fused graph, CUDA graph + PDL) with
+every GEMM / attention launch writing per-CTA %globaltimer stamps, then prints,
+per launch kind averaged over the layers, when the launch's CTAs start, pass
+their dependency wait, finish streaming (last MMA / producer done) and exit,
+relative to the previous launch's last CTA exit — i.e. where each kernel
+boundary spends its time with HBM idle.
+
+usage: step_timeline.py [--layers L] [--steps K] [--json out.json]"""
+import argparse, ctypes as C, json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--layers", type=int, default=32)
+ap.add_argument("--steps", type=int, default=6)
+ap.add_argument("--json", default="")
+args = ap.parse_args()
+
+import synth
+from paper_2604_10180_b200 import decoder as DEC, _kd as K
+
+cfg = synth.CONFIGS["llama3-8b"].with_(n_micro=1, n_layers=args.layers)
+dg = DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True, fuse_norm=True)
+rt = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], seed=cfg.seed, use_graph=True)
+REG = 512 * 32
+n_max = 8 * args.layers + 16
+buf = torch.zeros(n_max * REG, dtype=torch.int64, device="cuda")
+K.kd_debug_timeline(C.c_void_p(buf.data_ptr()), C.c_uint64(buf.numel() * 8))
+for _ in range(args.steps):
+    rt.step()
+torch.cuda.synchronize()
+n = C.c_uint32()
+K.kd_debug_timeline_kinds(None, 0, C.byref(n))
+kinds = (C.c_int32 * n.value)()
+K.kd_debug_timeline_kinds(kinds, n.value, C.byref(n))
+K.kd_debug_timeline(None, 0)
+kinds = list(kinds)
+T = buf.view(n_max, 512, 32)[: len(kinds)].cpu().numpy().astype(np.float64)
+name = {100: "qkv/o csk", 101: "qkv+rope", 102: "gemm+norm(csk)", 200: "gemm(sk)", 201: "gate_up+silu",
+        202: "gemm+norm(sk)", 300: "attention"}
+
+recs = []
+slots = {}  # launch label -> list over layers of per-slot (median, max) over CTAs, µs after the previous end
+prev_end = None
+prev_kind = None
+t0 = None
+for i, k in enumerate(kinds):
+    R = T[i]
+    live = R[:, 0] > 0
+    if not live.any():
+        continue
+    R = R[live]
+    if t0 is None:
+        t0 = R[:, 0].min()
+    rel = lambda v: float(v - (prev_end if prev_end is not None else t0)) / 1e3  # µs after previous launch's end
+    if k == 300:
+        end = R[:, [3, 4]].max()
+        rec = dict(kind=name[k], first_entry=rel(R[:, 0].min()), last_entry=rel(R[:, 0].max()),
+                   wait_done=rel(R[:, 1][R[:, 1] > 0].min()), stream_done_first=rel(R[:, 2].min()),
+                   stream_done_last=rel(R[:, 2].max()), end=rel(end))
+    else:
+        end = R[:, 15].max()
+        lastmma = R[:, 5][R[:, 5] > 0]
+        ep = R[:, 6][R[:, 6] > 0]
+        rec = dict(kind=name.get(k, str(k)), first_entry=rel(R[:, 0].min()), last_entry=rel(R[:, 0].max()),
+                   first_mma=rel(R[:, 4][R[:, 4] > 0].min()), first_mma_last=rel(R[:, 4][R[:, 4] > 0].max()),
+                   last_mma_first=rel(lastmma.min()) if lastmma.size else None,
+                   last_mma_last=rel(lastmma.max()) if lastmma.size else None,
+                   epi_start_med=rel(np.median(ep)) if ep.size else None, exit_first=rel(R[:, 15][R[:, 15] > 0].min()),
+                   end=rel(end))
+    rec["span"] = rec["end"] - 0.0
+    recs.append(rec)
+    if prev_end is not None:
+        label = rec["kind"] + ("" if k not in (102,) else (" [O+norm2]" if prev_kind == 300 else " [down+norm1]"))
+        row = []
+        for sl in range(16):
+            v = R[:, sl][R[:, sl] > 0]
+            row.append((rel(np.median(v)), rel(v.max())) if v.size else (None, None))
+        slots.setdefault(label, []).append(row)
+    prev_end = end
+    prev_kind = k
+
+# group by position in the layer pattern (kind sequence repeats per layer)
+by = {}
+for r in recs[1:]:  # drop the first launch (no previous end in this step)
+    by.setdefault(r["kind"], []).append(r)
+out = {}
+print(f"{len(recs)} traced launches; µs relative to the previous launch's last CTA exit (mean over layers)")
+for k, rs in by.items():
+    keys = [x for x in rs[0] if x != "kind" and rs[0][x] is not None]
+    avg = {x: float(np.mean([r[x] for r in rs if r.get(x) is not None])) for x in keys}
+    out[k] = dict(n=len(rs), **{x: round(v, 2) for x, v in avg.items()})
+    print(f"{k:16s} n={len(rs):3d} " + " ".join(f"{x}={v:7.2f}" for x, v in avg.items()))
+print("per-slot stamps (median / max over CTAs, mean over layers; µs after the previous launch's end):")
+slot_out = {}
+for label, rows in slots.items():
+    parts = []
+    slot_out[label] = {}
+    for sl in range(16):
+        med = [r[sl][0] for r in rows if r[sl][0] is not None]
+        mx = [r[sl][1] for r in rows if r[sl][1] is not None]
+        if med:
+            slot_out[label][sl] = (round(float(np.mean(med)), 2), round(float(np.mean(mx)), 2))
+            parts.append(f"{sl}:{np.mean(med):.1f}/{np.mean(mx):.1f}")
+    print(f"  {label:28s} " + " ".join(parts))
+total = sum(r["span"] for r in recs[1:])
+print(f"sum of spans {total / 1e3:.3f} ms over {len(recs) - 1} launches")
+if args.json:
+    json.dump(dict(per_kind=out, slots=slot_out, launches=recs), open(args.json, "w"), indent=1)
