@@ -107,6 +107,23 @@ for label, rows in slots.items():
             slot_out[label][sl] = (round(float(np.mean(med)), 2), round(float(np.mean(mx)), 2))
             parts.append(f"{sl}:{np.mean(med):.1f}/{np.mean(mx):.1f}")
     print(f"  {label:28s} " + " ".join(parts))
+# fused-norm epilogue sub-phases (clock64 stamps, slots 16-24; cycles, median over CTAs, mean over launches)
+chain = [(22, "waits"), (16, "sum+add"), (17, "sync"), (18, "ssq"), (24, "sync"), (23, "barrier"), (19, "x-CTA sums"),
+         (20, "sync"), (21, "norm+stores")]
+ph = {}
+for i, k in enumerate(kinds):
+    if k != 102:
+        continue
+    R = T[i]
+    R = R[R[:, 0] > 0]
+    for (a, _), (b, nm) in zip(chain, chain[1:]):
+        d = R[:, b] - R[:, a]
+        d = d[(R[:, a] > 0) & (R[:, b] > 0)]
+        if d.size:
+            ph.setdefault(nm, []).append(float(np.median(d)))
+if ph:
+    print("fused-norm epilogue phases (cycles, median over CTAs): " +
+          " ".join(f"{nm}={np.mean(v):.0f}" for nm, v in ph.items()))
 total = sum(r["span"] for r in recs[1:])
 print(f"sum of spans {total / 1e3:.3f} ms over {len(recs) - 1} launches")
 if args.json:
