@@ -543,7 +543,9 @@ kd_status kd_debug_gemm_trace(void* dev_buf);
  * step graph) writes %globaltimer stamps per CTA to dev_buf[i*16384 + cta*32 +
  * slot] (u64): GEMMs the kd_debug_gemm_trace slots, attention [0] entry, [1]
  * producer past its dependency wait, [2] producer done, [3] epilogue done, [4]
- * consumers done (max over CTAs' warps). Launches beyond bytes/131072 are not
+ * consumers done (max over CTAs' warps), [5]/[6] and [7]/[8] the epilogue
+ * warp's combine-slot acquire / done of its last two items, [9] its last split
+ * counter atomic. Launches beyond bytes/131072 are not
  * traced. kd_debug_timeline_kinds returns each traced launch's kind: 100 +
  * rope + 2·norm (cluster split-K GEMM), 200 + silu (stream-K GEMM), 300
  * (decode attention). Off by default; NULL turns it off and clears the list. */

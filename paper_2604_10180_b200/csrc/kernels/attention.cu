@@ -63,7 +63,8 @@ struct Params {
   unsigned* counter;  // [rows][Hkv]
   unsigned* work;     // item ticket counter (last word of the counter region)
   unsigned long long* tl;    // kd_debug_timeline region (nullable): per CTA [0] entry, [1] producer past
-                             // its dependency wait, [2] producer done, [3] epilogue done, [4] consumers done
+                             // its dependency wait, [2] producer done, [3] epilogue done, [4] consumers done,
+                             // [5..8] epilogue slot acquired / done of its last two items, [9] last split atomic
   unsigned long long* prof;  // KD_ATTN_PROF experiments: [0] producer empty-wait cycles, [1] consumer full-wait, [2] consumer busy, [3] pages
   int Hq, Hkv, G, pps, splits, pages_per_split;
   int rows;           // sequences; items are kv-head-major: it = (g·rows + b)·splits + split
@@ -73,6 +74,26 @@ struct Params {
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void st_f4_keep(float* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_f1_keep(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+// L2 load issued at this point of the program (asm volatile: the compiler
+// cannot sink it to the first use, so a batch of them is in flight together)
+__device__ __forceinline__ float4 ldcg_f4_now(const float* p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -338,13 +359,24 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
 
   if (warp == kWarps + 1) {
     // ================= epilogue: merge warps (fixed order), then splits (fixed order)
+    // timeline (P.tl): combine slot acquired / item done of the last two items, last split atomic
+    unsigned long long e_c[2] = {0, 0}, e_d[2] = {0, 0}, e_a = 0;
+    uint64_t pkeep = 0;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pkeep));
+    auto gnow = [] {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      return t;
+    };
     for (int k = 0;; ++k) {
+      if (P.tl && k > 0) e_d[1] = gnow();
       const int it = next_item(k);
       if (it < 0) break;
       const int split = it % P.splits, unit = it / P.splits;
       const int g = unit / P.rows, b = unit % P.rows;
       const int cs = k & 1;
       mbar_wait(&cfull[cs], (k >> 1) & 1);
+      if (P.tl) e_c[0] = e_c[1], e_d[0] = e_d[1], e_c[1] = gnow();
       const float* cb = comb + (size_t)cs * kWarps * G * D;
       const float* cml = comb_ml + cs * kWarps * G * 2;
       // per-head warp weights: lane (w, h) → s_w[w][h] = 2^(m_w − M_h); s_M, s_L
@@ -378,8 +410,10 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
           if (P.lse && d0 == 0) store_lse(P, (size_t)b * P.Hq + g * G + h, L > 0.f ? s_M[h] + log2f(L) : -INFINITY);
         } else {
           const size_t pi = (((size_t)unit * P.splits + split) * G + h);
-          *reinterpret_cast<float4*>(P.part_o + pi * D + d0) = acc;
-          if (d0 == 0) P.part_lse[pi] = L > 0.f ? s_M[h] + log2f(L) : -INFINITY;
+          // evict_last: the unit's last split merges these up to a whole
+          // launch later, after ~1 GB of KV pages streamed through L2
+          st_f4_keep(P.part_o + pi * D + d0, acc, pkeep);
+          if (d0 == 0) st_f1_keep(P.part_lse + pi, L > 0.f ? s_M[h] + log2f(L) : -INFINITY, pkeep);
         }
       }
       // every lane fences its own partial stores at gpu scope before lane 0's
@@ -396,9 +430,15 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
         // the other splits' partials for the last arriver
         if (lane == 0) prev = atom_add_acq_rel_gpu(&P.counter[unit], 1u);
         done = __shfl_sync(0xffffffffu, prev, 0) == (unsigned)P.splits - 1;
+        if (P.tl) e_a = gnow();
         if (done) {
           __syncwarp();
-          fence_acq_rel_gpu();  // each lane: its partial loads below are ordered after lane 0's acquire
+          // each lane acquires the counter itself until it reads every split's
+          // arrival (lane 0's add above made it P.splits), so its partial loads
+          // below are ordered after all splits' releases (one L2 round trip;
+          // was a fence.acq_rel.gpu after the warp sync, ≈1.7 µs at the tail)
+          while (ld_acquire_gpu_u32(&P.counter[unit]) < (unsigned)P.splits) {
+          }
           const float* lse = P.part_lse + (size_t)unit * P.splits * G;  // [split][G]
           const float* po = P.part_o + (size_t)unit * P.splits * G * D;  // [split][G][D]
           const int nl = P.splits * G, n_e4 = G * D / 4;
@@ -414,7 +454,7 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
 #pragma unroll
               for (int sp = 0; sp < kFastSplits; ++sp)
                 if (e4 < n_e4 && sp < P.splits)
-                  v[k][sp] = __ldcg(reinterpret_cast<const float4*>(po + ((size_t)sp * G + h) * D + d0));
+                  v[k][sp] = ldcg_f4_now(po + ((size_t)sp * G + h) * D + d0);
             }
             for (int i = lane; i < nl; i += 32) s_lse[i] = __ldcg(lse + i);  // (both batches in flight)
             __syncwarp();
@@ -511,7 +551,14 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
         }
       }
     }
-    if (P.tl && lane == 0) tl_stamp(3);
+    if (P.tl && lane == 0) {
+      tl_stamp(3);
+      P.tl[blockIdx.x * 32 + 5] = e_c[0];
+      P.tl[blockIdx.x * 32 + 6] = e_d[0];
+      P.tl[blockIdx.x * 32 + 7] = e_c[1];
+      P.tl[blockIdx.x * 32 + 8] = e_d[1];
+      P.tl[blockIdx.x * 32 + 9] = e_a;
+    }
     if (P.prof && lane == 0) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));

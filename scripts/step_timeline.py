@@ -107,6 +107,23 @@ for label, rows in slots.items():
             slot_out[label][sl] = (round(float(np.mean(med)), 2), round(float(np.mean(mx)), 2))
             parts.append(f"{sl}:{np.mean(med):.1f}/{np.mean(mx):.1f}")
     print(f"  {label:28s} " + " ".join(parts))
+# attention tail: per CTA, epilogue lag behind its consumers and the last two items' epilogue spans
+lag, last_items, worst = [], [], []
+for i, k in enumerate(kinds):
+    if k != 300 or i == 0:
+        continue
+    R = T[i]
+    R = R[R[:, 0] > 0]
+    lag.append(float(np.median(R[:, 3] - R[:, 4])) / 1e3)
+    v = (R[:, 8] > 0) & (R[:, 7] > 0)
+    last_items.append((float(np.median(R[v, 8] - R[v, 7])) / 1e3, float(np.median(R[v, 7] - R[v, 6])) / 1e3))
+    w = int(np.argmax(R[:, 3]))
+    worst.append([(R[w, sl] - R[w, 4]) / 1e3 for sl in (5, 6, 7, 8, 9, 3)])
+if lag:
+    print(f"attention epilogue lag behind consumers (median over CTAs) {np.mean(lag):.2f} us; last item epilogue "
+          f"{np.mean([a for a, _ in last_items]):.2f} us, gap before it {np.mean([b for _, b in last_items]):.2f} us")
+    print("  last CTA out, relative to its consumers' end (us): prev item acquired/done, last acquired/done, "
+          "split atomic, exit: " + " ".join(f"{x:.2f}" for x in np.mean(np.array(worst), axis=0)))
 # fused-norm epilogue sub-phases (clock64 stamps, slots 16-24; cycles, median over CTAs, mean over launches)
 chain = [(22, "waits"), (16, "sum+add"), (17, "sync"), (18, "ssq"), (24, "sync"), (23, "barrier"), (19, "x-CTA sums"),
          (20, "sync"), (21, "norm+stores")]
