@@ -124,6 +124,20 @@ if lag:
           f"{np.mean([a for a, _ in last_items]):.2f} us, gap before it {np.mean([b for _, b in last_items]):.2f} us")
     print("  last CTA out, relative to its consumers' end (us): prev item acquired/done, last acquired/done, "
           "split atomic, exit: " + " ".join(f"{x:.2f}" for x in np.mean(np.array(worst), axis=0)))
+# cluster split-K epilogue (non-norm: QKV+RoPE, plain): TMEM → DSMEM push (clock64 slots 21 → 22),
+# owner sum + stores (24 → 25), in cycles
+for kk, nm in ((101, "qkv+rope"), (100, "plain csk")):
+    push, own = [], []
+    for i, k in enumerate(kinds):
+        if k != kk:
+            continue
+        R = T[i]
+        R = R[(R[:, 0] > 0) & (R[:, 21] > 0) & (R[:, 25] > 0)]
+        if len(R):
+            push.append(float(np.median(R[:, 22] - R[:, 21])))
+            own.append(float(np.median(R[:, 25] - R[:, 24])))
+    if push:
+        print(f"{nm} epilogue (cycles, median over CTAs): push={np.mean(push):.0f} owner-sum+stores={np.mean(own):.0f}")
 # fused-norm epilogue sub-phases (clock64 stamps, slots 16-24; cycles, median over CTAs, mean over launches)
 chain = [(22, "waits"), (16, "sum+add"), (17, "sync"), (18, "ssq"), (24, "sync"), (23, "barrier"), (19, "x-CTA sums"),
          (20, "sync"), (21, "norm+stores")]
