@@ -294,10 +294,18 @@ __global__ void __launch_bounds__(kRopeThreads)
 }
 
 // ======================================================================= causal attention
-constexpr int kAQ = 64;          // query tokens per CTA
-constexpr int kAK = 64;          // keys per block (4 pages of 16)
+#ifndef KD_PA_WARPS
+#define KD_PA_WARPS 11
+#endif
+// Registers are allocated to a CTA in groups of 4 warps: the 1 producer + 4
+// consumer warps of a 64-query CTA (174 registers/thread) paid for 8 warps, so
+// only one such CTA fit per SM (ncu: 7 % achieved occupancy). 7 consumer warps
+// + the producer use those same registers: 112 queries per CTA, 1.75× the
+// consumer warps per SM.
+constexpr int kAWarps = KD_PA_WARPS;  // consumers (16 query rows each); + 1 producer warp
+constexpr int kAQ = 16 * kAWarps;     // query tokens per CTA
+constexpr int kAK = 64;               // keys per block (4 pages of 16)
 constexpr int kAStages = 3;
-constexpr int kAWarps = 4;       // consumers; + 1 producer warp
 constexpr int kAThreads = (kAWarps + 1) * 32;
 
 struct AArgs {
@@ -621,6 +629,15 @@ kd_status launch_prefill_attention(const kd_attr_prefill_attention& a, const voi
     KD_CUDA_CHECK(cudaFuncSetAttribute(pre::prefill_attention_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)pre::attn_smem<64>()),
                   "prefill attention smem attr");
+    // the whole shared-memory carveout: left to the driver, the 99 KB CTA got a
+    // 102 KB configuration, i.e. one CTA (5 warps) per SM (ncu: 7 % achieved
+    // occupancy, 5.3 cycles between issues); two fit in the full 228 KB
+    KD_CUDA_CHECK(cudaFuncSetAttribute(pre::prefill_attention_kernel<128>,
+                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                  "prefill attention carveout");
+    KD_CUDA_CHECK(cudaFuncSetAttribute(pre::prefill_attention_kernel<64>,
+                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                  "prefill attention carveout");
     init = true;
   }
   CUtensorMap tk, tv;
@@ -643,6 +660,18 @@ kd_status launch_prefill_attention(const kd_attr_prefill_attention& a, const voi
   A.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)a.head_dim));
   A.epi = c.epi;
   const dim3 grid(A.n_qt, a.n_heads, a.seqs);
+  if (getenv("KD_ATTN_DEBUG")) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pre::prefill_attention_kernel<128>, pre::kAThreads,
+                                                  pre::attn_smem<128>());
+    int occ0 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, pre::prefill_attention_kernel<128>, pre::kAThreads, 0);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, pre::prefill_attention_kernel<128>);
+    fprintf(stderr, "prefill attention: %d CTAs/SM (smem %zu B, %d threads); %d without smem; regs %d, static smem %zu, max dyn %d, carveout %d\n",
+            occ, pre::attn_smem<128>(), pre::kAThreads, occ0, fa.numRegs, fa.sharedSizeBytes,
+            fa.maxDynamicSharedSizeBytes, fa.preferredShmemCarveout);
+  }
   if (a.head_dim == 128)
     KD_CUDA_CHECK(kd_launch(pre::prefill_attention_kernel<128>, grid, dim3(pre::kAThreads), pre::attn_smem<128>(),
                             c.stream, tk, tv, A),
