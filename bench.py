@@ -287,15 +287,18 @@ def main():
         # (KD_OP_GEMM_SILU, bit-identical to the pair); so are QKV + RoPE/append
         # (KD_OP_QKV_ROPE, bit-identical to the pair: 17.0 vs 15.0 + 3.7 µs, step 9.04 vs
         # 9.13 ms) and the O GEMM with norm2 / the down GEMM with the next layer's norm1
-        # (KD_OP_GEMM_RMSNORM: the per-token Σr² is finished across the grid after an
-        # in-kernel barrier; step 8.92 vs 8.95 ms). A/B: KD_BENCH_NO_FUSE (all),
-        # KD_BENCH_NO_FUSE_ROPE, KD_BENCH_NO_FUSE_NORM, KD_BENCH_FUSE_NORM=o (O+norm2 only).
+        # (KD_OP_GEMM_RMSNORM), with the RMSNorm's per-token 1/rms deferred to the
+        # consumers (KD_NORM_DEFER: gate_up+SiLU and QKV+RoPE scale their fp32 sums; no
+        # grid barrier in the O / down epilogues: 8.73 vs 8.84 ms same box). A/B:
+        # KD_BENCH_NO_FUSE (all), KD_BENCH_NO_FUSE_ROPE, KD_BENCH_NO_FUSE_NORM,
+        # KD_BENCH_FUSE_NORM=o (O+norm2 only), KD_BENCH_FUSE_NORM=1 (norm in the GEMM epilogue
+        # after an in-kernel grid barrier).
         mega = args.exec_mode == "mega"
         fuse = not os.environ.get("KD_BENCH_NO_FUSE")
         # (the megakernel has no GEMM + RMSNorm task: the norms stay separate tasks)
         dg = DEC.DecoderGraph(cfg, fuse_silu=fuse, fuse_rope=fuse and not os.environ.get("KD_BENCH_NO_FUSE_ROPE"),
                               fuse_norm=(fuse and not mega and not os.environ.get("KD_BENCH_NO_FUSE_NORM")) and
-                              (os.environ.get("KD_BENCH_FUSE_NORM") or True))
+                              (os.environ.get("KD_BENCH_FUSE_NORM") or "defer"))
         assign = [0] * dg.g.num_kernels
         rt = DEC.DecoderRuntime(dg, assign, 1, [local], seed=cfg.seed, use_graph=not args.no_graph, megakernel=mega)
         placement = "monolithic (all kernels on one B200)" + (

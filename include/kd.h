@@ -121,7 +121,13 @@ enum {
   KD_OP_GEMM_RMSNORM = 17  /* a7+a3 / a10+a3 fused (co-located O or down GEMM and the next residual add +
                             * RMSNorm): reads [X, W, r, gamma] writes [h, r] with kd_attr_gemm_rmsnorm:
                             * r' = r + bf16(X·Wᵀ) (bits identical to a GEMM then a3's add), h =
-                            * r'/sqrt(mean r'² + eps)·gamma (Σr'² in another order than a3: not bitwise) */
+                            * r'/sqrt(mean r'² + eps)·gamma (Σr'² in another order than a3: not bitwise).
+                            * flags KD_NORM_DEFER: writes [xs, r, ssq] instead — xs = bf16(r'·gamma) and the
+                            * per-token partial sums of r'² (layout KD_DNORM_*, one per CTA), no grid-wide
+                            * wait; the 1/rms factor is applied by the co-located consumer GEMM
+                            * (KD_OP_GEMM_SILU / KD_OP_QKV_ROPE with ssq as an extra last read), which
+                            * scales its fp32 sums row by row: (xs·Wᵀ)·rsqrt(Σ ssq / N + eps) — RMSNorm's
+                            * per-token factor moved past the linear map (same math, other rounding point) */
 };
 
 /* element types of activations / KV */
@@ -137,7 +143,14 @@ enum { KD_BF16 = 0, KD_F32 = 1 };
 typedef struct { uint32_t rows, hidden, n_delta, dtype; float eps; uint32_t pad_; } kd_attr_add_rmsnorm;
 typedef struct { uint32_t M, N, K, dtype; } kd_attr_gemm;            /* X [M,K], W [N,K] row-major, Y [M,N] */
 /* X [M,K], W [N,K] (N = hidden), r fp32 [M,N], gamma [N], h [M,N]; bf16 only */
-typedef struct { uint32_t M, N, K, dtype; float eps; uint32_t pad_; } kd_attr_gemm_rmsnorm;
+typedef struct { uint32_t M, N, K, dtype; float eps; uint32_t flags; } kd_attr_gemm_rmsnorm;
+/* KD_OP_GEMM_RMSNORM flags; deferred-norm partial sums (fp32 buffer of
+ * KD_DNORM_BYTES(M) bytes): [0] eps, [1] N (as float), then from float
+ * KD_DNORM_HDR on, row j (token) holds KD_DNORM_PARTS partials (unused ones
+ * zero) summed in index order by the consumer */
+enum { KD_NORM_DEFER = 1 };
+enum { KD_DNORM_HDR = 16, KD_DNORM_PARTS = 160 };
+#define KD_DNORM_BYTES(M) (4ull * (KD_DNORM_HDR + (uint64_t)(M) * KD_DNORM_PARTS))
 /* slot_offset: tokens of each sequence held by earlier KV shards (f2, long
  * context split over devices): the rotation angle uses the absolute position
  * seq_len − 1, the appended slot is (seq_len − 1 − slot_offset) in this

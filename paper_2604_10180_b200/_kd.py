@@ -95,7 +95,15 @@ class kd_attr_qkv_rope(C.Structure):
 
 class kd_attr_gemm_rmsnorm(C.Structure):
     _fields_ = [("M", C.c_uint32), ("N", C.c_uint32), ("K", C.c_uint32), ("dtype", C.c_uint32),
-                ("eps", C.c_float), ("pad_", C.c_uint32)]
+                ("eps", C.c_float), ("flags", C.c_uint32)]
+
+
+KD_NORM_DEFER = 1
+KD_DNORM_HDR, KD_DNORM_PARTS = 16, 160
+
+
+def KD_DNORM_BYTES(M):
+    return 4 * (KD_DNORM_HDR + M * KD_DNORM_PARTS)
 
 
 class kd_attr_attn_merge(C.Structure):

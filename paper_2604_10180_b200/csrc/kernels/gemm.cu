@@ -60,6 +60,7 @@ struct Args {
   int dbg;                    // debug A/B knob (KD_GEMM_DBG): 1 skip owner Y stores, 2 skip owner fold
   unsigned* err;              // runtime error word (nullable): set to 2 when the fold barrier times out
   Acq acq;                    // chunk-aware consumer: X (slot 0) acquired per k-block by the TMA warp
+  const float* dssq;          // deferred RMSNorm of X (nullable, silu only): gate/up sums × 1/rms(token)
 };
 
 #define KD_TRACE(slot) \
@@ -107,6 +108,25 @@ __device__ __forceinline__ void store_silu4(const Args& A, size_t yo, const floa
   for (int p = 0; p < A.epi.n; ++p) if (epi_row_in(A.epi, p, (uint32_t)(yo / (A.N / 2)))) *reinterpret_cast<uint2*>((__nv_bfloat16*)A.epi.dst[p] + yo) = o;
 }
 
+// deferred RMSNorm (KD_NORM_DEFER): 1/rms of token j from the producer's
+// per-CTA partial sums of r'² (layout KD_DNORM_*: eps, N, then KD_DNORM_PARTS
+// partials per token, unused ones zero), summed in index order
+__device__ __forceinline__ float dnorm_inv(const float* d, int j) {
+  const float4* p = reinterpret_cast<const float4*>(d + KD_DNORM_HDR + (size_t)j * KD_DNORM_PARTS);
+  float4 v[KD_DNORM_PARTS / 4];
+#pragma unroll
+  for (int c = 0; c < KD_DNORM_PARTS / 4; ++c) v[c] = __ldcg(p + c);  // all in flight
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < KD_DNORM_PARTS / 4; ++c) {
+    s += v[c].x;
+    s += v[c].y;
+    s += v[c].z;
+    s += v[c].w;
+  }
+  return rsqrtf(s / __ldcg(d + 1) + __ldcg(d));
+}
+
 // kX: the round-2 handoff protocol (chunk byte counts, in-kernel acquires,
 // residency / log words) is compiled in; launches without chunked transfers
 // use the kX = false instance, whose code is the plain GEMM + CTA-mode peer
@@ -133,6 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   volatile unsigned* s_flag = (volatile unsigned*)(tmem_slot + 1);
   __nv_bfloat16* ystage = (__nv_bfloat16*)(fixbar + 2);  // 2 x [16][128] bf16 epilogue transpose
   unsigned* s_cnt = (unsigned*)(ystage + 2 * kChunk * kBM);  // COUNT-mode bytes per (peer, chunk) (this CTA)
+  float* s_inv = (float*)(s_cnt + kMaxPeers * kMaxChunks);    // [M] deferred-norm 1/rms per token (dssq)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) KD_TRACE(0);
@@ -310,6 +331,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ep_tid = threadIdx.x - 128;
     const size_t part_elems = (size_t)A.M * kBM;
     pdl_wait();  // scratch and Y may still be in use by the previous kernel
+    if (A.dssq) {  // deferred RMSNorm of X: per-token 1/rms while the first tile still streams
+      for (int j = ep_tid; j < A.M; j += 128) s_inv[j] = dnorm_inv(A.dssq, j);
+      named_bar(1, 128);
+    }
     int seg = 0;
     long long u = u0;
     auto out_coords = [&](int t, int* nb0, int* y0, int* mv) {
@@ -397,6 +422,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                   if (w < A.M * 16 && j < mv)
                   {
                     const size_t yo = (size_t)(y0 + j) * (A.N / 2) + (nb0 / 2) + (w & 15) * 4;
+                    if (A.dssq) {  // deferred RMSNorm of X: the folded sums × 1/rms(token)
+                      const float sc = s_inv[j];
+                      g[i].x *= sc, g[i].y *= sc, g[i].z *= sc, g[i].w *= sc;
+                      uu[i].x *= sc, uu[i].y *= sc, uu[i].z *= sc, uu[i].w *= sc;
+                    }
                     store_silu4(A, yo, g[i], uu[i]);
                     count(yo, 8u);
                   }
@@ -453,6 +483,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           float v[kChunk];
           tmem_ld16(tbase + j0, v);
           __nv_bfloat16* st = ystage + (size_t)((j0 / kChunk) & 1) * kChunk * kBM;
+#pragma unroll
+          if (A.dssq)
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) v[j] *= j0 + j < A.M ? s_inv[j0 + j] : 0.f;
 #pragma unroll
           for (int j = 0; j < kChunk; ++j) st[j * kBM + row_in_tile] = __float2bfloat16_rn(v[j]);
           named_bar(2, 128);
@@ -693,6 +727,10 @@ struct Args {
   float* ssq;                   // [M][gridDim.x] per-CTA partial Σr² (scratch)
   unsigned* err;                // runtime error word (nullable): set to 2 when the grid barrier times out
   Acq acq;                      // chunk-aware consumer: X (slot 0) acquired per k-block by the TMA warp
+  // norm == 2 (KD_NORM_DEFER): no grid barrier — Y = bf16(r'·gamma), per-CTA Σr'² to ssq (the declared
+  // partial-sum buffer past its header), 1/rms left to the consumer
+  float* dssq_out;              // norm == 2: the partial-sum buffer (header written by CTA 0)
+  const float* dssq;            // rope: deferred RMSNorm of X (nullable): the QKV sums × 1/rms(token)
 };
 
 // a5 fused into the QKV GEMM epilogue. W rows are pair-interleaved within each
@@ -708,6 +746,7 @@ struct RopeSmem {
   int* pos;      // [M] seq_len − 1
   int* pg;       // [M] page holding pos (block_table entry)
   double* f;     // [D/2]
+  float* inv;    // [M] deferred-norm 1/rms per token (A.dssq)
 };
 
 __device__ __forceinline__ void rope_stage(const Args& A, const RopeSmem& rs) {
@@ -719,6 +758,7 @@ __device__ __forceinline__ void rope_stage(const Args& A, const RopeSmem& rs) {
     const int pos = R.sl[j] - 1;
     rs.pos[j] = pos;
     rs.pg[j] = R.bt[(size_t)j * R.pps + pos / R.page];
+    if (A.dssq) rs.inv[j] = dnorm_inv(A.dssq, j);
   }
 }
 
@@ -727,6 +767,7 @@ __device__ __forceinline__ void rope_pair(const Args& A, const RopeSmem& rs, int
   const int D = R.D, half = D / 2, G = R.Hq / R.Hkv;
   const int hall = n / D, rr = n - hall * D, p = rr >> 1;
   const int grp = hall / (G + 2), slot = hall - grp * (G + 2);
+  if (A.dssq) xs *= rs.inv[j], ys *= rs.inv[j];  // deferred RMSNorm of X: the fp32 sums × 1/rms
   const float x = __bfloat162float(__float2bfloat16_rn(xs)), y = __bfloat162float(__float2bfloat16_rn(ys));
   const int pos = rs.pos[j];
   __nv_bfloat16 lo, hi;
@@ -768,6 +809,10 @@ __device__ __forceinline__ void rope_quad(const Args& A, const RopeSmem& rs, int
   const int D = R.D, half = D / 2, G = R.Hq / R.Hkv;
   const int hall = n / D, rr = n - hall * D, p = rr >> 1;
   const int grp = hall / (G + 2), slot = hall - grp * (G + 2);
+  if (A.dssq) {  // deferred RMSNorm of X: the fp32 sums × 1/rms
+    const float sc = rs.inv[j];
+    a.x *= sc, a.y *= sc, a.z *= sc, a.w *= sc;
+  }
   const float xs[2] = {__bfloat162float(__float2bfloat16_rn(a.x)), __bfloat162float(__float2bfloat16_rn(a.z))};
   const float ys[2] = {__bfloat162float(__float2bfloat16_rn(a.y)), __bfloat162float(__float2bfloat16_rn(a.w))};
   const int pos = rs.pos[j];
@@ -885,7 +930,9 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
   float* const ssq = A.ssq;
   float* const rs = ns.rs;
   const int Tp = ns.Tp;
-  const int G = gridDim.x, Gp = (G + 15) / 16 * 16;  // ssq row pitch
+  const int G = gridDim.x;
+  const bool defer = A.norm == 2;                   // KD_NORM_DEFER: partial sums to the declared buffer
+  const int Gp = defer ? KD_DNORM_PARTS : (G + 15) / 16 * 16;  // ssq row pitch
   __syncthreads();  // staging (split 1) and the r/gamma slices are complete; my own rows are in recv[rank]
   if (split > 1) mbar_wait(rbar, 0);
   pdl_wait();
@@ -931,10 +978,19 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
       ss += v.w * v.w;
     }
     ssq[(size_t)j * Gp + blockIdx.x] = ss;
+    // deferred: the consumer sums all KD_DNORM_PARTS entries; CTA c also zeroes entry G + c
+    if (defer && G + (int)blockIdx.x < KD_DNORM_PARTS) ssq[(size_t)j * Gp + G + blockIdx.x] = 0.f;
+  }
+  if (defer) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      A.dssq_out[0] = A.eps;
+      A.dssq_out[1] = (float)N;
+    }
+    for (int j = threadIdx.x; j < M; j += kThreads) ns.invs[j] = 1.f;  // h = bf16(r'·1·γ): the 1/rms is deferred
   }
   if (threadIdx.x == 0) KD_CTRACE(18);
   __syncthreads();
-  if (threadIdx.x == 0) {  // grid barrier (self-resetting: see the departure at the end)
+  if (!defer && threadIdx.x == 0) {  // grid barrier (self-resetting: see the departure at the end)
     KD_TRACE(13);
     KD_CTRACE(24);
     // the acq_rel add releases this CTA's partial sums (ordered before it by
@@ -953,12 +1009,12 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
     KD_CTRACE(23);
   }
   __syncthreads();
-  // per token Σ over CTAs: a warp takes kTpw tokens; each lane loads 16-byte
+  // per token Σ over CTAs (not when deferred): a warp takes kTpw tokens; each lane loads 16-byte
   // chunks lane and lane + 32 of every row (coalesced, all loads in flight),
   // sums its components in c order, then the tokens' shuffle trees run
   // interleaved. Fixed order: deterministic. Entries ≥ G are masked (the pad
   // of a row is not ours: the scratch is shared with other kernels).
-  {
+  if (!defer) {
     constexpr int kTpw = 6, kCh = (kNormMaxGrid + 127) / 128;  // ≤ 2 float4 per lane per row (G ≤ 160)
     for (int j0 = warp * kTpw; j0 < M; j0 += kTpw * (kThreads / 32)) {
       float4 v[kTpw][kCh];
@@ -1017,7 +1073,7 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
     KD_TRACE(15);
     // departure, off the critical path: the last CTA to leave (every CTA has
     // passed the arrival spin by then) zeroes both words for the next launch
-    if (atom_add_acq_rel_gpu(A.bar + 1, 1u) == (unsigned)G - 1) {
+    if (!defer && atom_add_acq_rel_gpu(A.bar + 1, 1u) == (unsigned)G - 1) {
       A.bar[0] = 0u;
       A.bar[1] = 0u;
     }
@@ -1057,6 +1113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   ropes.pos = (int*)(ns.invs + 256);                  // [256]
   ropes.pg = ropes.pos + 256;                         // [256]
   ropes.f = (double*)(ropes.pg + 256);                // [128]
+  ropes.inv = (float*)(ropes.f + 128);                // [256]
   float* send = (float*)smem;  // split == 1: [M][128] fp32 staging, reuses the idle ring after the last MMA
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1437,7 +1494,7 @@ static kd_status geometry(const GemmShape& a, Geometry* g, int sms) {
 
 static size_t smem_bytes(const Geometry& g) {
   return 1024 + (size_t)g.stages * g.kbs * (kStageA + g.mma_n * kBK * 2) + (2 * kMaxStages + 6) * 8 +
-         2 * kChunk * kBM * 2 + 16 + 4 * kMaxPeers * kMaxChunks;
+         2 * kChunk * kBM * 2 + 16 + 4 * kMaxPeers * kMaxChunks + 256 * 4;
 }
 
 // ---------------------------------------------------------------- dense GEMM kernel choice
@@ -1449,7 +1506,7 @@ static size_t smem_for(int mma_n, int kbs, int stages, int split, int rpo, int M
     const size_t tp = (split > 1 ? rpo : kBM) + 4;
     return smem_for(mma_n, kbs, stages, split, rpo, M, false, false) + (size_t)M * tp * 4 + 256;
   }
-  if (rope) return smem_for(mma_n, kbs, stages, split, rpo, M, false, false) + 256 * 4 * 2 + 128 * 8;
+  if (rope) return smem_for(mma_n, kbs, stages, split, rpo, M, false, false) + 256 * 4 * 3 + 128 * 8;
   return 1024 + (size_t)stages * kbs * (kStageA + (size_t)mma_n * kBK * 2) + recv + (2 * kMaxStages + 4) * 8 + 16 +
          256 * 4;  // + the norm epilogue's per-token 1/rms
 }
@@ -1606,7 +1663,13 @@ GemmShape gemm_shape(const kd_attr_gemm_rmsnorm& a) {
   return s;
 }
 
-kd_status gemm_rmsnorm_bind(const kd_attr_gemm_rmsnorm& a, float* r, const void* gamma, GemmPlan* gp) {
+kd_status gemm_rmsnorm_bind(const kd_attr_gemm_rmsnorm& a, float* r, const void* gamma, GemmPlan* gp, float* ssq_out) {
+  if (a.flags & ~(uint32_t)KD_NORM_DEFER) return fail(KD_ERR_INVALID_ARG, "gemm_rmsnorm: unknown flags");
+  gp->defer = (a.flags & KD_NORM_DEFER) != 0;
+  if (gp->defer && (!ssq_out || ((uintptr_t)ssq_out & 15)))
+    return fail(KD_ERR_INVALID_ARG, "gemm_rmsnorm (deferred): a 16-byte aligned partial-sum buffer is required");
+  if (gp->defer && a.M > 256) return fail(KD_ERR_UNSUPPORTED, "gemm_rmsnorm (deferred): at most 256 rows");
+  gp->dssq_out = ssq_out;
   if (a.dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "gemm_rmsnorm: bf16 only");
   if (a.N % 8) return fail(KD_ERR_UNSUPPORTED, "gemm_rmsnorm: hidden must be a multiple of 8");
   if (!r || !gamma) return fail(KD_ERR_INVALID_ARG, "gemm_rmsnorm: NULL r or gamma");
@@ -1751,15 +1814,20 @@ static kd_status launch_gemm_dense(const GemmPlan& gp, void* Y, const LaunchCtx&
   A.dbg = getenv("KD_GEMM_DBG") ? atoi(getenv("KD_GEMM_DBG")) : 0;
   A.rope = (int)gp.sh.rope;
   A.rp = gp.rp;
-  A.norm = (int)gp.sh.norm;
+  A.norm = gp.defer ? 2 : (int)gp.sh.norm;
+  A.dssq_out = gp.dssq_out;
+  A.dssq = gp.dssq;
+  if (A.dssq && !A.rope) return fail(KD_ERR_UNSUPPORTED, "gemm: a deferred-norm input needs the QKV+RoPE epilogue here");
   A.r = gp.r;
   A.gamma = (const __nv_bfloat16*)gp.gamma;
   A.eps = gp.eps;
   A.bar = (unsigned*)c.scratch;
-  A.ssq = c.scratch ? (float*)((uint8_t*)c.scratch + kScratchCounterBytes) : nullptr;
+  A.ssq = gp.defer ? gp.dssq_out + KD_DNORM_HDR
+                   : (c.scratch ? (float*)((uint8_t*)c.scratch + kScratchCounterBytes) : nullptr);
   if (A.norm && (!c.scratch || !A.r || !A.gamma))
     return fail(KD_ERR_INVALID_ARG, "gemm_rmsnorm: scratch, r and gamma are required");
   if (A.norm && t.tiles * t.split > kNormMaxGrid) return fail(KD_ERR_UNSUPPORTED, "gemm_rmsnorm: grid too large");
+  static_assert(kNormMaxGrid <= KD_DNORM_PARTS, "deferred-norm partials: one per CTA");
   A.epi = c.epi;
   A.err = c.err;
   A.acq = c.acq;
@@ -1818,6 +1886,9 @@ kd_status launch_gemm(const GemmPlan& gp, void* Y, const LaunchCtx& c, uint32_t*
   A.err = c.err;
   A.acq = c.acq;
   A.trace = g_gemm_trace ? g_gemm_trace : tl_next(200 + (int)gp.sh.silu);
+  A.dssq = gp.dssq;
+  if (A.dssq && (!A.silu || A.M > 256))
+    return fail(KD_ERR_UNSUPPORTED, "gemm: a deferred-norm input needs the fused SiLU epilogue here (M <= 256)");
   {
     static int dbg = -1;
     if (dbg < 0) dbg = getenv("KD_GEMM_DBG") ? atoi(getenv("KD_GEMM_DBG")) : 0;

@@ -149,7 +149,9 @@ GemmShape gemm_shape(const kd_attr_qkv_rope& a);
 GemmShape gemm_shape(const kd_attr_gemm_rmsnorm& a);
 struct GemmPlan;
 // fill the a3 operands of a KD_OP_GEMM_RMSNORM plan (after gemm_prepare)
-kd_status gemm_rmsnorm_bind(const kd_attr_gemm_rmsnorm& a, float* r, const void* gamma, GemmPlan* gp);
+// (a.flags & KD_NORM_DEFER: ssq_out = the deferred-norm partial-sum buffer, KD_DNORM_BYTES(M))
+kd_status gemm_rmsnorm_bind(const kd_attr_gemm_rmsnorm& a, float* r, const void* gamma, GemmPlan* gp,
+                            float* ssq_out = nullptr);
 // fill gp->rp for a KD_OP_QKV_ROPE plan (after gemm_prepare)
 kd_status qkv_rope_bind(const kd_attr_qkv_rope& a, const int32_t* bt, const int32_t* sl, void* q, void* kc, void* vc,
                         GemmPlan* gp);
@@ -174,6 +176,9 @@ struct GemmPlan {
   float* r = nullptr;         // KD_OP_GEMM_RMSNORM: residual, gamma, eps
   const void* gamma = nullptr;
   float eps = 0.f;
+  bool defer = false;           // KD_NORM_DEFER producer: partial sums to dssq_out, 1/rms left to the consumer
+  float* dssq_out = nullptr;
+  const float* dssq = nullptr;  // deferred-norm consumer (GEMM_SILU / QKV_ROPE with the partial sums as last read)
   GemmTile tile;
 };
 kd_status gemm_scratch_bytes(const GemmShape& sh, uint64_t* bytes);

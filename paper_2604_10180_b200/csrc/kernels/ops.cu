@@ -138,6 +138,7 @@ kd_status kd_op_gemm_rmsnorm(const kd_attr_gemm_rmsnorm* a, const void* X, const
                              const void* gamma, void* h, void* scratch, void* stream) {
   if (!a) return fail(KD_ERR_INVALID_ARG, "kd_op_gemm_rmsnorm: NULL attrs");
   if (a->dtype != KD_BF16) return fail(KD_ERR_UNSUPPORTED, "kd_op_gemm_rmsnorm: bf16 only");
+  if (a->flags) return fail(KD_ERR_UNSUPPORTED, "kd_op_gemm_rmsnorm: KD_NORM_DEFER is a graph-level fusion (its consumer scales)");
   GemmPlan gp;
   kd_status s = gemm_prepare(gemm_shape(*a), X, W, nullptr, &gp);
   if (s) return s;

@@ -137,10 +137,15 @@ kd_status check_attrs(const Kernel& k) {
       ok = a.n_delta <= (uint32_t)kMaxDeltas && nr == 2 + a.n_delta && nw == 2;
       break;
     }
-    case KD_OP_GEMM:
-    case KD_OP_GEMM_SILU: ok = nr == 2 && nw == 1; break;
-    case KD_OP_QKV_ROPE: ok = nr == 4 && nw == 3; break;  // reads [X, W', bt, sl] writes [q, Kc, Vc]
-    case KD_OP_GEMM_RMSNORM: ok = nr == 4 && nw == 2; break;  // reads [X, W, r, gamma] writes [h, r]
+    case KD_OP_GEMM: ok = nr == 2 && nw == 1; break;
+    case KD_OP_GEMM_SILU: ok = (nr == 2 || nr == 3) && nw == 1; break;  // (+ deferred-norm partial sums)
+    case KD_OP_QKV_ROPE: ok = (nr == 4 || nr == 5) && nw == 3; break;  // reads [X, W', bt, sl (, ssq)] writes [q, Kc, Vc]
+    case KD_OP_GEMM_RMSNORM: {  // reads [X, W, r, gamma] writes [h, r] (deferred: [xs, r, ssq])
+      kd_attr_gemm_rmsnorm a;
+      std::memcpy(&a, k.attrs.data(), sizeof a);
+      ok = nr == 4 && nw == ((a.flags & KD_NORM_DEFER) ? 3u : 2u);
+      break;
+    }
     case KD_OP_ATTN_MERGE: {
       kd_attr_attn_merge a;
       std::memcpy(&a, k.attrs.data(), sizeof a);
@@ -696,13 +701,14 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
         if (s3) return s3;
         s3 = qkv_rope_bind(a, (const int32_t*)l.rd[2], (const int32_t*)l.rd[3], l.wr[0], l.wr[1], l.wr[2], l.gemm);
         if (s3) return s3;
+        if (l.rd.size() == 5) l.gemm->dssq = (const float*)l.rd[4];
       }
       if (K.op == KD_OP_GEMM_RMSNORM) {
         const auto a = attrs_get<kd_attr_gemm_rmsnorm>(K);
         l.gemm = new GemmPlan();
         kd_status s3 = gemm_prepare(gemm_shape(a), l.rd[0], l.rd[1], nullptr, l.gemm);
         if (s3) return s3;
-        s3 = gemm_rmsnorm_bind(a, (float*)l.wr[1], l.rd[3], l.gemm);
+        s3 = gemm_rmsnorm_bind(a, (float*)l.wr[1], l.rd[3], l.gemm, l.wr.size() == 3 ? (float*)l.wr[2] : nullptr);
         if (s3) return s3;
       }
       if (K.op == KD_OP_GEMM || K.op == KD_OP_GEMM_SILU) {
@@ -710,6 +716,7 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
         kd_status s3 = gemm_prepare(gemm_shape(attrs_get<kd_attr_gemm>(K), K.op == KD_OP_GEMM_SILU), l.rd[0], l.rd[1],
                                     nullptr, l.gemm);
         if (s3) return s3;
+        if (K.op == KD_OP_GEMM_SILU && l.rd.size() == 3) l.gemm->dssq = (const float*)l.rd[2];
       }
       if (rt->profile_op) {
         KD_CUDA_CHECK(cudaEventCreate(&l.ev0), "event create");
@@ -728,6 +735,8 @@ kd_status kd_runtime_prepare(kd_runtime* rt) {
     if (rt->exec == KD_EXEC_MEGAKERNEL) {
       std::vector<MegaOpDesc> ops;
       for (const auto& l : d.launches) {
+        if (l.kind == Launch::KERNEL && l.gemm && (l.gemm->defer || l.gemm->dssq))
+          return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: the megakernel has no deferred-norm GEMM tasks");
         if (l.kind != Launch::KERNEL || l.ctx.epi.n || l.ctx.acq.n)
           return fail(KD_ERR_UNSUPPORTED, "kd_runtime_prepare: the megakernel runs single-device schedules only "
                                           "(device " + std::to_string(d.logical) + " has cross-device transfers)");

@@ -94,6 +94,10 @@ class DecoderGraph:
         as ONE kernel (KD_OP_GEMM_RMSNORM) — for co-located placements; the o
         and d activations then never exist (except the last layer's d).
         fuse_norm="o" fuses only O + norm2 (A/B: measured between all and none).
+        fuse_norm="defer" (with fuse_silu and fuse_rope): the fused O / down GEMMs
+        write bf16(r'·gamma) and per-CTA partial sums of r'² (KD_NORM_DEFER) and
+        their co-located consumers (gate_up+SiLU, QKV+RoPE) scale their fp32
+        sums by the token's 1/rms — no grid-wide wait in the producers.
         replicate_kv: the KV caches are KD_BUF_REPLICATED (P:465-466 delta
         replication) and RoPE/append gets its own template (T_ROPE), so it can
         run on another device than attention: the appended slots are mirrored
@@ -108,6 +112,11 @@ class DecoderGraph:
         fuse_rope = bool(fuse_rope) and act == K.KD_BF16
         self.fuse_rope = fuse_rope
         norm_o_only = fuse_norm == "o"  # fuse only O + norm2 (keep down → norm1 apart)
+        # "defer": the fused O / down GEMMs leave RMSNorm's per-token 1/rms to their
+        # co-located consumers (KD_NORM_DEFER: gate_up+SiLU and QKV+RoPE scale their
+        # fp32 sums), so they need no grid-wide wait; requires the SiLU / RoPE fusions
+        defer = fuse_norm == "defer" and bool(fuse_silu) and bool(fuse_rope)
+        self.defer_norm = defer and act == K.KD_BF16
         fuse_norm = bool(fuse_norm) and act == K.KD_BF16
         self.fuse_norm = fuse_norm
         adt = "bf16" if act == K.KD_BF16 else "f32"  # storage of weights, activations and KV cache
@@ -194,6 +203,10 @@ class DecoderGraph:
                 acts += ([] if fuse_silu else [("gu", (m, 2 * F))]) + [("a", (m, F))]
             for nm, shp in acts:
                 buf(f"{nm}.{l}", shp, adt, PM)
+            if self.defer_norm and not E:  # deferred-norm partial sums (KD_DNORM layout, fp32)
+                buf(f"ssq2.{l}", (K.KD_DNORM_HDR + m * K.KD_DNORM_PARTS,), "f32", PM)
+                if fused_down(l):
+                    buf(f"ssq1.{l+1}", (K.KD_DNORM_HDR + m * K.KD_DNORM_PARTS,), "f32", PM)
 
         self.kernels: List[KernelInfo] = []
 
@@ -230,7 +243,8 @@ class DecoderGraph:
                     ["r"] + ([f"d.{l-1}"] if has_d else []) + [f"g1.{l}"], [f"h1.{l}", "r"],
                     K.kd_attr_add_rmsnorm(m, H, has_d, act, eps, 0))
             if fuse_rope:
-                add("qkv_rope", l, T_ATTN, K.KD_OP_QKV_ROPE, [f"h1.{l}", f"w_qkv.{l}", "bt", "sl"],
+                dq = [f"ssq1.{l}"] if f"ssq1.{l}" in self.buf else []  # h1 from a deferred down+norm1
+                add("qkv_rope", l, T_ATTN, K.KD_OP_QKV_ROPE, [f"h1.{l}", f"w_qkv.{l}", "bt", "sl"] + dq,
                     [f"q.{l}", f"kc.{l}", f"vc.{l}"],
                     K.kd_attr_qkv_rope(m, H, Hq, Hkv, D, cfg.page, pps, act, float(cfg.rope_theta)),
                     2 * m * cfg.qkv_dim * H)
@@ -243,8 +257,10 @@ class DecoderGraph:
             add("attn", l, T_ATTN, K.KD_OP_ATTENTION, [f"q.{l}", f"kc.{l}", f"vc.{l}", "bt", "sl"], [f"attn.{l}"],
                 K.kd_attr_attention(m, Hq, Hkv, D, cfg.page, pps, act, 0), 4 * m * Hq * cfg.context * D)
             if fuse_norm:
-                add("o_norm", l, T_O, K.KD_OP_GEMM_RMSNORM, [f"attn.{l}", f"w_o.{l}", "r", f"g2.{l}"], [f"h2.{l}", "r"],
-                    K.kd_attr_gemm_rmsnorm(m, H, Hq * D, act, eps, 0), 2 * m * H * Hq * D)
+                d2 = f"ssq2.{l}" in self.buf
+                add("o_norm", l, T_O, K.KD_OP_GEMM_RMSNORM, [f"attn.{l}", f"w_o.{l}", "r", f"g2.{l}"],
+                    [f"h2.{l}", "r"] + ([f"ssq2.{l}"] if d2 else []),
+                    K.kd_attr_gemm_rmsnorm(m, H, Hq * D, act, eps, K.KD_NORM_DEFER if d2 else 0), 2 * m * H * Hq * D)
             else:
                 add("o", l, T_O, K.KD_OP_GEMM, [f"attn.{l}", f"w_o.{l}"], [f"o.{l}"],
                     K.kd_attr_gemm(m, H, Hq * D, act), 2 * m * H * Hq * D)
@@ -268,15 +284,18 @@ class DecoderGraph:
                     K.kd_attr_moe_combine(m, H, E, k, 1, 0))
             else:
                 if fuse_silu:
-                    add("gu_silu", l, T_GU, K.KD_OP_GEMM_SILU, [f"h2.{l}", f"w_gu.{l}"], [f"a.{l}"],
+                    dq = [f"ssq2.{l}"] if (fuse_norm and f"ssq2.{l}" in self.buf) else []
+                    add("gu_silu", l, T_GU, K.KD_OP_GEMM_SILU, [f"h2.{l}", f"w_gu.{l}"] + dq, [f"a.{l}"],
                         K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
                 else:
                     add("gu", l, T_GU, K.KD_OP_GEMM, [f"h2.{l}", f"w_gu.{l}"], [f"gu.{l}"],
                         K.kd_attr_gemm(m, 2 * F, H, act), 2 * m * 2 * F * H)
                     add("silu", l, T_SILU, K.KD_OP_SILU_MUL, [f"gu.{l}"], [f"a.{l}"], K.kd_attr_silu_mul(m, F, act, 0))
                 if fused_down(l):
+                    d1 = f"ssq1.{l+1}" in self.buf
                     add("down_norm", l, T_DOWN, K.KD_OP_GEMM_RMSNORM, [f"a.{l}", f"w_d.{l}", "r", f"g1.{l+1}"],
-                        [f"h1.{l+1}", "r"], K.kd_attr_gemm_rmsnorm(m, H, F, act, eps, 0), 2 * m * H * F)
+                        [f"h1.{l+1}", "r"] + ([f"ssq1.{l+1}"] if d1 else []),
+                        K.kd_attr_gemm_rmsnorm(m, H, F, act, eps, K.KD_NORM_DEFER if d1 else 0), 2 * m * H * F)
                 else:
                     add("down", l, T_DOWN, K.KD_OP_GEMM, [f"a.{l}", f"w_d.{l}"], [f"d.{l}"],
                         K.kd_attr_gemm(m, H, F, act), 2 * m * H * F)

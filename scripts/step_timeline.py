@@ -24,7 +24,7 @@ import synth
 from paper_2604_10180_b200 import decoder as DEC, _kd as K
 
 cfg = synth.CONFIGS["llama3-8b"].with_(n_micro=1, n_layers=args.layers)
-dg = DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True, fuse_norm=True)
+dg = DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True, fuse_norm=os.environ.get("KD_TL_FUSE_NORM", "defer"))
 rt = DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], seed=cfg.seed, use_graph=True)
 REG = 512 * 32
 n_max = 8 * args.layers + 16

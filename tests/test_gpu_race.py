@@ -78,10 +78,12 @@ def test_poisoned_fused_graph_bitwise(DEC):
                  lambda dg: (2, dg.role_assign(0, 1)))
     _check(runs, cfg.n_layers)
     # the fully fused monolithic graph (GEMM + RMSNorm epilogues): poisoned == clean
-    dgs = [DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True, fuse_norm=True) for _ in range(2)]
-    rts = [_steps(DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp), 2, p)
-           for dg, p in zip(dgs, (False, True))]
-    assert np.array_equal(rts[0].residual(), rts[1].residual())
+    # (and with the deferred RMSNorm: xs and the partial sums are poisoned too)
+    for mode in (True, "defer"):
+        dgs = [DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True, fuse_norm=mode) for _ in range(2)]
+        rts = [_steps(DEC.DecoderRuntime(dg, [0] * dg.g.num_kernels, 1, [0], inputs=inp), 2, p)
+               for dg, p in zip(dgs, (False, True))]
+        assert np.array_equal(rts[0].residual(), rts[1].residual())
 
 
 def test_poisoned_role_layout_3_to_1_bitwise(DEC):
