@@ -978,8 +978,9 @@ __device__ __forceinline__ void norm_epilogue(const Args& A, const NormSmem& ns,
       ss += v.w * v.w;
     }
     ssq[(size_t)j * Gp + blockIdx.x] = ss;
-    // deferred: the consumer sums all KD_DNORM_PARTS entries; CTA c also zeroes entry G + c
-    if (defer && G + (int)blockIdx.x < KD_DNORM_PARTS) ssq[(size_t)j * Gp + G + blockIdx.x] = 0.f;
+    // deferred: the consumer sums all KD_DNORM_PARTS entries; CTA c also zeroes entries G + c + k·G
+    if (defer)
+      for (int e = G + (int)blockIdx.x; e < KD_DNORM_PARTS; e += G) ssq[(size_t)j * Gp + e] = 0.f;
   }
   if (defer) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
