@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """One small decode configuration per kernel family, eager launches (no CUDA
 graph), for compute-sanitizer (memcheck / racecheck / synccheck):
-  python scripts/sanitize_step.py [dense|fused|moe|ssm|all]
+  python scripts/sanitize_step.py [dense|fused|defer|moe|ssm|all]
 dense: TINY 2-device loopback pair with 4-chunk handoff; fused: the 1-GPU
 fused graph (QKV+RoPE, gate_up+SiLU, GEMM+RMSNorm); moe: Mixtral-shaped tiny
 EP 1+2; ssm: the hybrid tiny graph. Exits non-zero on a runtime error."""
@@ -39,6 +39,12 @@ def main(which):
         dg = DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True, fuse_norm=True)
         run(dg, [0] * dg.g.num_kernels, 1, inp)
         print("fused ok", flush=True)
+    if which in ("defer", "all"):  # the bench's 1-GPU graph: RMSNorm's 1/rms deferred to the consumers (R31)
+        cfg = synth.TINY
+        inp = synth.make_decoder_inputs(cfg)
+        dg = DEC.DecoderGraph(cfg, fuse_silu=True, fuse_rope=True, fuse_norm="defer")
+        run(dg, [0] * dg.g.num_kernels, 1, inp)
+        print("deferred-norm fused ok", flush=True)
     if which in ("moe", "all"):
         a, e, m = 1, 2, 2
         cfg = synth.TINY.with_(n_experts=4, top_k=2, n_micro=2, batch=a * 2 * m)
