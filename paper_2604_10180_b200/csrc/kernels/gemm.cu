@@ -1374,7 +1374,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // second pass: lanes walk a token's rows, so the output (and peer) stores
     // coalesce; walking tokens, as the sum must, scatters every warp store
     // over 32 rows of Y (measured: the RoPE epilogue's 2-byte stores cost ≈4 µs)
+    if (threadIdx.x == 128) KD_CTRACE(27);
     __syncthreads();
+    if (threadIdx.x == 128) KD_CTRACE(28);
     for (int e = threadIdx.x; e < M * r4n; e += kThreads) {
       const int j = e / r4n, l4 = e - j * r4n, n = n0 + rank * rpo + 4 * l4;
       const float4 v = *reinterpret_cast<const float4*>(T + (size_t)j * Tp + 4 * l4);

@@ -132,12 +132,15 @@ for kk, nm in ((101, "qkv+rope"), (100, "plain csk")):
         if k != kk:
             continue
         R = T[i]
-        R = R[(R[:, 0] > 0) & (R[:, 21] > 0) & (R[:, 25] > 0)]
+        R = R[(R[:, 0] > 0) & (R[:, 24] > 0) & (R[:, 25] > 0)]
         if len(R):
             push.append(float(np.median(R[:, 22] - R[:, 21])))
-            own.append(float(np.median(R[:, 25] - R[:, 24])))
+            own.append((float(np.median(R[:, 27] - R[:, 24])), float(np.median(R[:, 28] - R[:, 27])),
+                        float(np.median(R[:, 25] - R[:, 28]))))
     if push:
-        print(f"{nm} epilogue (cycles, median over CTAs): push={np.mean(push):.0f} owner-sum+stores={np.mean(own):.0f}")
+        o = np.mean(np.array(own), axis=0)
+        print(f"{nm} epilogue (cycles, median over CTAs): push={np.mean(push):.0f} owner sum={o[0]:.0f} "
+              f"sync={o[1]:.0f} stores (RoPE)={o[2]:.0f}")
 # fused-norm epilogue sub-phases (clock64 stamps, slots 16-24; cycles, median over CTAs, mean over launches)
 chain = [(22, "waits"), (16, "sum+add"), (17, "sync"), (18, "ssq"), (24, "sync"), (23, "barrier"), (19, "x-CTA sums"),
          (20, "sync"), (21, "norm+stores")]
