@@ -483,7 +483,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           float v[kChunk];
           tmem_ld16(tbase + j0, v);
           __nv_bfloat16* st = ystage + (size_t)((j0 / kChunk) & 1) * kChunk * kBM;
-#pragma unroll
           if (A.dssq)
 #pragma unroll
             for (int j = 0; j < kChunk; ++j) v[j] *= j0 + j < A.M ? s_inv[j0 + j] : 0.f;
