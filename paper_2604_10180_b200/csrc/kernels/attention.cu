@@ -437,7 +437,9 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
           // arrival (lane 0's add above made it P.splits), so its partial loads
           // below are ordered after all splits' releases (one L2 round trip;
           // was a fence.acq_rel.gpu after the warp sync, ≈1.7 µs at the tail)
-          while (ld_acquire_gpu_u32(&P.counter[unit]) < (unsigned)P.splits) {
+          // (lane 0's add already made the count P.splits: the first read
+          // normally succeeds; the bound only guards against a broken invariant)
+          for (int spins = 0; ld_acquire_gpu_u32(&P.counter[unit]) < (unsigned)P.splits && spins < (1 << 20); ++spins) {
           }
           const float* lse = P.part_lse + (size_t)unit * P.splits * G;  // [split][G]
           const float* po = P.part_o + (size_t)unit * P.splits * G * D;  // [split][G][D]
