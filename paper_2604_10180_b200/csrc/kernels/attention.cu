@@ -69,6 +69,7 @@ struct Params {
   int Hq, Hkv, G, pps, splits, pages_per_split;
   int rows;           // sequences; items are kv-head-major: it = (g·rows + b)·splits + split
   int prefetch;       // stream the first item's safe pages before griddepcontrol.wait (KD_ATTN_PREFETCH=0 disables)
+  int l2pf;           // pages of the first item past the smem ring the idle epilogue warp warms L2 with (KD_ATTN_L2PF)
   float scale_log2;   // log2(e)/sqrt(D)
   Epi epi;
 };
@@ -88,6 +89,12 @@ __device__ __forceinline__ float4 ldcg_f4_now(const float* p) {
   float4 v;
   asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
   return v;
+}
+// L2 prefetch of one 3-D K/V slab box (no shared memory, no completion)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"((uint64_t)map), "r"(c0), "r"(c1),
+               "r"(c2)
+               : "memory");
 }
 __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
   unsigned v;
@@ -359,6 +366,26 @@ __global__ void __launch_bounds__(kThreads) decode_attention_kernel(const __grid
 
   if (warp == kWarps + 1) {
     // ================= epilogue: merge warps (fixed order), then splits (fixed order)
+    // Idle until the first item's pages are consumed: warm L2 with that
+    // item's pages past the producer's smem prefill (step inputs and earlier
+    // steps' cache only — the appended page is excluded), so a CTA resident
+    // before its dependency resolves (on SMs the previous kernel leaves free)
+    // turns its wait into HBM traffic the first item then finds in L2
+    if (P.l2pf > 0 && (int)blockIdx.x < n_items) {
+      const int it0 = (int)blockIdx.x, split = it0 % P.splits, unit = it0 / P.splits;
+      const int g = unit / P.rows, b = unit % P.rows;
+      const int len = __ldg(P.sl + b);
+      const int p0 = split * P.pages_per_split;
+      const int np = max(0, min((len + kPage - 1) / kPage, p0 + P.pages_per_split) - p0);
+      const int safe = max(0, min(np, (len - 1) / kPage - p0));
+      const int t0 = P.prefetch ? min(min(S, 32), safe) : 0, t1 = min(safe, t0 + P.l2pf);
+      for (int t = t0 + lane; t < t1; t += 32) {
+        const int pid = __ldg(P.bt + (size_t)b * P.pps + p0 + t);
+        const int row = (pid * Hkv + g) * kPage;
+        tma_prefetch_3d(&tk, 0, 0, row);
+        tma_prefetch_3d(&tv, 0, 0, row);
+      }
+    }
     // timeline (P.tl): combine slot acquired / item done of the last two items, last split atomic
     unsigned long long e_c[2] = {0, 0}, e_d[2] = {0, 0}, e_a = 0;
     uint64_t pkeep = 0;
@@ -843,6 +870,8 @@ kd_status launch_attention(const kd_attr_attention& a, const void* q, const void
   {
     const char* e = getenv("KD_ATTN_PREFETCH");
     P.prefetch = e ? atoi(e) : 1;
+    const char* e2 = getenv("KD_ATTN_L2PF");
+    P.l2pf = e2 ? atoi(e2) : 8;  // (same box, 3 rounds: 0 / 8 / 16 / 24 pages → 8.75 / 8.71 / 8.71 / 8.74 ms per step)
   }
   P.lse = (a.flags & KD_ATTN_LSE) ? (float*)((uint8_t*)out + P.lse_off) : nullptr;
   const uint64_t units = (uint64_t)a.rows * a.n_kv_heads;
